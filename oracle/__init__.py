@@ -1,0 +1,332 @@
+"""CPU fp64 oracle for the Krylov projected-reachability hot path of arXiv 1804.01583.
+
+TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package. The product path (paper_1804_01583_b200/) never
+imports it, and the two share no code: the numerics live in oracle/krylov_oracle.c (plain C, fp64,
+single thread, -ffp-contract=off) and in the plain numpy orchestration below.
+
+What it computes (PAPER.md, "P:<line>"):
+  * directions v_d: generator columns of E (§3.2), plus the fixed-term direction
+    v_f = [c; 1] when there is a center c or an affine term b (lifting P:157-165, superposition of
+    fixed terms P:1197-1225);
+  * per direction, k steps of Arnoldi (Alg. 1) or Lanczos (Alg. 3/4) with the
+    projection P = C V (Alg. 4);
+  * per time point t_j = j*step, x_{d,j} = e^{H t_j} e_1 (Eq. 2) by Pade scaling and
+    squaring and the basis-matrix entries c[j][r][d] = ||v_d|| (P_d x_{d,j})_r
+    (= C e^{A t_j} E in the Krylov approximation, §3);
+  * the per-step safety check specialised to a box initial set and one output half-space, i.e. the
+    exact LP value max/min over the box (Fig. 2(c)), first violating step
+    and witness;
+  * the Lemma 1 a posteriori bound as a diagnostic.
+Readings of ambiguous passages are SURVEY.md §8(c) A1-A20 and are listed in DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "krylov_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+GE, LE, EQ = 0, 1, 2
+
+
+def build(force=False):
+    """Compile the C oracle with gcc (plain -O2, no FMA contraction, no vectorised reassociation)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99",
+                               "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class _Op(C.Structure):
+    _fields_ = [("op", C.c_int32), ("mx", C.c_int64), ("my", C.c_int64), ("mz", C.c_int64),
+                ("alpha", C.c_double), ("n", C.c_int64), ("row_ptr", C.c_void_p),
+                ("col_idx", C.c_void_p), ("val", C.c_void_p), ("b", C.c_void_p)]
+
+
+class _Row(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("nnz", C.c_int64), ("idx", C.c_void_p), ("val", C.c_void_p),
+                ("lo", C.c_int64 * 3), ("hi", C.c_int64 * 3), ("value", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        dp = C.POINTER(C.c_double)
+        _lib.oracle_sum.restype = C.c_double
+        _lib.oracle_sum.argtypes = [C.c_void_p, C.c_int64]
+        _lib.oracle_dot.restype = C.c_double
+        _lib.oracle_dot.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        _lib.oracle_op_dim.restype = C.c_int64
+        _lib.oracle_op_dim.argtypes = [C.POINTER(_Op)]
+        _lib.oracle_op_apply.argtypes = [C.POINTER(_Op), C.c_void_p, C.c_void_p]
+        _lib.oracle_row_dot.restype = C.c_double
+        _lib.oracle_row_dot.argtypes = [C.POINTER(_Op), C.POINTER(_Row), C.c_void_p]
+        _lib.oracle_lanczos.argtypes = [C.POINTER(_Op), C.c_void_p, C.c_int32, C.c_int32, C.POINTER(_Row),
+                                        C.c_void_p, C.c_void_p, C.c_void_p, dp, C.POINTER(C.c_int32)]
+        _lib.oracle_arnoldi.argtypes = [C.POINTER(_Op), C.c_void_p, C.c_int32, C.c_int32, C.POINTER(_Row),
+                                        C.c_void_p, C.c_void_p, dp, C.POINTER(C.c_int32)]
+        _lib.oracle_expm.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
+        _lib.oracle_expm_e1_times.argtypes = [C.c_int32, C.c_void_p, C.c_double, C.c_int64, C.c_void_p]
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class Operator:
+    """Keeps the numpy arrays alive next to the ctypes struct."""
+
+    def __init__(self, p):
+        self.p = p
+        self.keep = []
+        if p["op"] == "stencil":
+            self.s = _Op(0, p["mx"], p["my"], p["mz"], p["alpha"], 0, None, None, None, None)
+        else:
+            rp = np.ascontiguousarray(p["row_ptr"], dtype=np.int64)
+            ci = np.ascontiguousarray(p["col_idx"], dtype=np.int32)
+            va = np.ascontiguousarray(p["val"], dtype=np.float64)
+            b = None if p.get("b") is None else np.ascontiguousarray(p["b"], dtype=np.float64)
+            self.keep += [rp, ci, va, b]
+            self.s = _Op(1, 0, 0, 0, 0.0, p["n"], _ptr(rp), _ptr(ci), _ptr(va), _ptr(b))
+        self.dim = int(lib().oracle_op_dim(C.byref(self.s)))
+
+    def apply(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.dim)
+        lib().oracle_op_apply(C.byref(self.s), _ptr(x), _ptr(y))
+        return y
+
+
+def _rows(p):
+    rows = (_Row * max(1, len(p["outs"])))()
+    keep = []
+    for r, v in enumerate(p["outs"]):
+        if v["kind"] == "sparse":
+            idx = np.ascontiguousarray(v["idx"], dtype=np.int64)
+            val = np.ascontiguousarray(v["val"], dtype=np.float64)
+            keep += [idx, val]
+            rows[r] = _Row(0, idx.size, _ptr(idx), _ptr(val), (C.c_int64 * 3)(0, 0, 0),
+                           (C.c_int64 * 3)(0, 0, 0), 0.0)
+        elif v["kind"] == "all":
+            rows[r] = _Row(2, 0, None, None, (C.c_int64 * 3)(0, 0, 0), (C.c_int64 * 3)(0, 0, 0), v["value"])
+        else:
+            rows[r] = _Row(1, 0, None, None, (C.c_int64 * 3)(*v["lo"]), (C.c_int64 * 3)(*v["hi"]), v["value"])
+    return rows, keep
+
+
+def _dense(v, p, n):
+    """Dense materialisation of a compact vector (box / all / sparse entries) of length n."""
+    out = np.zeros(n)
+    if v["kind"] == "all":
+        out[:] = v["value"]
+    elif v["kind"] == "sparse":
+        for i, x in zip(v["idx"], v["val"]):
+            out[int(i)] += x
+    elif p["op"] == "stencil":
+        g = out.reshape(p["mz"], p["my"], p["mx"])
+        (x0, y0, z0), (x1, y1, z1) = v["lo"], v["hi"]
+        g[z0:z1, y0:y1, x0:x1] = v["value"]
+    else:
+        out[v["lo"][0]:v["hi"][0]] = v["value"]
+    return out
+
+
+def directions(p):
+    """Simulation directions: generator columns of E, plus the fixed-term direction
+    v_f = [c; 1] (lifted) or v_f = c (no affine term) — superposition."""
+    op = Operator(p)
+    n = op.dim
+    nb = n - 1 if (p["op"] == "csr" and p.get("b") is not None) else n
+    dirs = []
+    for g in p["gens"]:
+        v = np.zeros(n)
+        v[:nb] = _dense(g, p, nb)
+        dirs.append(v)
+    if p.get("b") is not None or p.get("center") is not None:
+        v = np.zeros(n)
+        if p.get("center") is not None:
+            v[:nb] = _dense(p["center"], p, nb)
+        if n != nb:
+            v[nb] = 1.0
+        dirs.append(v)
+    return dirs
+
+
+def lanczos(p, v, k):
+    """Alg. 3 + projection of Alg. 4 (see krylov_oracle.c). Returns dict(alpha, beta, P, beta0, k_eff)."""
+    op = Operator(p)
+    rows, keep = _rows(p)
+    o = len(p["outs"])
+    alpha = np.zeros(k)
+    beta = np.zeros(k)
+    P = np.zeros((max(o, 1), k))
+    b0 = C.c_double()
+    ke = C.c_int32()
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    st = lib().oracle_lanczos(C.byref(op.s), _ptr(v), k, o, rows, _ptr(alpha), _ptr(beta), _ptr(P),
+                              C.byref(b0), C.byref(ke))
+    if st != 0:
+        raise ValueError("zero start vector")
+    kk = ke.value
+    H = np.diag(alpha[:kk]) + np.diag(beta[:kk - 1], 1) + np.diag(beta[:kk - 1], -1)
+    return {"alpha": alpha[:kk], "beta": beta[:kk], "H": H, "P": P[:o, :kk], "beta0": b0.value,
+            "k_eff": kk, "h_next": beta[kk - 1]}
+
+
+def arnoldi(p, v, k):
+    """Alg. 1 with MGS (see krylov_oracle.c). Returns dict(H (k_eff x k_eff), P, beta0, k_eff, h_next)."""
+    op = Operator(p)
+    rows, keep = _rows(p)
+    o = len(p["outs"])
+    H = np.zeros((k + 1, k))
+    P = np.zeros((max(o, 1), k))
+    b0 = C.c_double()
+    ke = C.c_int32()
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    st = lib().oracle_arnoldi(C.byref(op.s), _ptr(v), k, o, rows, _ptr(H), _ptr(P), C.byref(b0), C.byref(ke))
+    if st != 0:
+        raise ValueError("zero start vector")
+    kk = ke.value
+    return {"H": H[:kk, :kk].copy(), "Hfull": H, "P": P[:o, :kk], "beta0": b0.value, "k_eff": kk,
+            "h_next": H[kk, kk - 1]}
+
+
+def expm(M):
+    """Moler-Van Loan / Golub-Van Loan diagonal Pade (q=8) with scaling and squaring."""
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    F = np.zeros_like(M)
+    lib().oracle_expm(M.shape[0], _ptr(M), _ptr(F))
+    return F
+
+
+def expm_e1_times(H, step, n_steps):
+    """x_j = e^{H t_j} e_1, t_j = (double)j*step, j = 0..n_steps (Eq. 2)."""
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    k = H.shape[0]
+    X = np.zeros((n_steps + 1, k))
+    lib().oracle_expm_e1_times(k, _ptr(H), step, n_steps, _ptr(X))
+    return X
+
+
+def gershgorin_mu(p):
+    """Upper bound on mu(A) = lambda_max((A+A^T)/2) by Gershgorin discs (reading for Lemma 1's
+    nu(B) = -mu(A) with B = -A). Lifted matrix when b is present."""
+    if p["op"] == "stencil":
+        best = -math.inf
+        ih = [float(p[a] + 1) ** 2 for a in ("mx", "my", "mz")]
+        nb = [min(2, p[a] - 1) for a in ("mx", "my", "mz")]
+        # the most interior cell maximises diag + sum |offdiag| (all off-diagonals are positive)
+        best = p["alpha"] * sum((nb[a] - 2) * ih[a] for a in range(3))
+        return best
+    n = p["n"]
+    rp, ci, va = p["row_ptr"], p["col_idx"], p["val"]
+    N = n + (1 if p.get("b") is not None else 0)
+    diag = np.zeros(N)
+    off = {}
+    for r in range(n):
+        for e in range(rp[r], rp[r + 1]):
+            c = int(ci[e])
+            if c == r:
+                diag[r] += va[e]
+            else:
+                off[(r, c)] = off.get((r, c), 0.0) + 0.5 * va[e]
+                off[(c, r)] = off.get((c, r), 0.0) + 0.5 * va[e]
+        if p.get("b") is not None and p["b"][r] != 0.0:
+            off[(r, n)] = off.get((r, n), 0.0) + 0.5 * p["b"][r]
+            off[(n, r)] = off.get((n, r), 0.0) + 0.5 * p["b"][r]
+    rad = np.zeros(N)
+    for (r, c), s in off.items():
+        rad[r] += abs(s)
+    return float(np.max(diag + rad))
+
+
+def krylov_project(p, method=None):
+    """The whole basis-matrix sequence: coeff[j][r][d] ~= C_r e^{A t_j} v_d for j = 0..N.
+    Returns dict(coeff, per_dir=[...], lemma1[d], times)."""
+    method = method or p["method"]
+    dirs = directions(p)
+    o = len(p["outs"])
+    N = p["n_steps"]
+    nd = len(dirs)
+    coeff = np.zeros((N + 1, o, nd))
+    per_dir = []
+    T = N * p["step"]
+    mu = gershgorin_mu(p)
+    lemma = np.zeros(nd)
+    for d, v in enumerate(dirs):
+        r = lanczos(p, v, p["k"]) if method == "lanczos" else arnoldi(p, v, p["k"])
+        X = expm_e1_times(r["H"], p["step"], N)  # (N+1) x k_eff
+        coeff[:, :, d] = r["beta0"] * (X @ r["P"].T)  # c[j][r] = ||v|| (P x_j)_r
+        r["X"] = X
+        # Lemma 1: ||v|| h_{k+1,k} e^{max(mu,0) T} int_0^T |e_k^T e^{Ht} e_1| dt, trapezoid
+        h = np.abs(X[:, -1])
+        integral = float(np.sum(0.5 * p["step"] * (h[1:] + h[:-1]))) if N > 0 else 0.0
+        lemma[d] = r["beta0"] * r["h_next"] * math.exp(max(mu, 0.0) * T) * integral
+        per_dir.append(r)
+    return {"coeff": coeff, "per_dir": per_dir, "lemma1": lemma, "mu": mu,
+            "times": np.arange(N + 1) * p["step"]}
+
+
+def z_bounds(p):
+    """Box bounds per direction; the fixed-term direction has z_f = 1."""
+    lo = list(np.asarray(p["z_lo"], dtype=np.float64))
+    hi = list(np.asarray(p["z_hi"], dtype=np.float64))
+    if p.get("b") is not None or p.get("center") is not None:
+        lo.append(1.0)
+        hi.append(1.0)
+    return np.array(lo), np.array(hi)
+
+
+def check_box(p, coeff, thresholds=None):
+    """Per-step interval bounds of each output over the box initial set, the exact LP optimum for a
+    box (Fig. 2(c)), the first violating step and a witness.
+    thresholds: list of (row, sense, theta). Returns dict(lo, hi, found, step, row, y, z)."""
+    thresholds = p["thresholds"] if thresholds is None else thresholds
+    zlo, zhi = z_bounds(p)
+    Np1, o, nd = coeff.shape
+    lo = np.zeros((Np1, o))
+    hi = np.zeros((Np1, o))
+    for j in range(Np1):
+        for r in range(o):
+            a = 0.0
+            b = 0.0
+            for d in range(nd):
+                c = coeff[j, r, d]
+                a += min(c * zlo[d], c * zhi[d])
+                b += max(c * zlo[d], c * zhi[d])
+            lo[j, r] = a
+            hi[j, r] = b
+    res = {"lo": lo, "hi": hi, "found": False, "step": -1, "row": -1, "y": 0.0, "z": None}
+    sense_of = {r: (s, th) for (r, s, th) in thresholds}
+    for j in range(Np1):
+        for r in range(o):
+            if r not in sense_of:
+                continue
+            s, th = sense_of[r]
+            bad = (hi[j, r] >= th) if s == GE else (lo[j, r] <= th) if s == LE else (lo[j, r] <= th <= hi[j, r])
+            if not bad:
+                continue
+            c = coeff[j, r]
+            if s == GE:
+                z = np.where(c >= 0, zhi, zlo)
+            elif s == LE:
+                z = np.where(c >= 0, zlo, zhi)
+            else:
+                lam = 0.0 if hi[j, r] == lo[j, r] else (th - lo[j, r]) / (hi[j, r] - lo[j, r])
+                z = np.where(c >= 0, zlo + lam * (zhi - zlo), zhi - lam * (zhi - zlo))
+            y = float(np.sum(c * z))
+            res.update(found=True, step=j, row=r, y=y, z=z, time=j * p["step"])
+            return res
+    return res

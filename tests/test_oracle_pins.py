@@ -1,0 +1,418 @@
+"""Pins for the CPU oracle (oracle/) against things other than itself: the paper's printed worked
+example, closed forms, library routines (scipy) on special cases, invariants and brute force.
+Each test names what it pins and where the expected value comes from. CPU only (-m "not gpu")."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sp
+from scipy.optimize import linprog
+
+import oracle
+import workloads as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def kron_laplacian(mx, my, mz, alpha):
+    """Independent construction of A = alpha * L_h (Dirichlet, h_a = 1/(m_a+1)) as a Kronecker sum
+    of 1-D second-difference matrices (textbook), x fastest."""
+    def t1(m):
+        return sp.diags([np.ones(m - 1), -2 * np.ones(m), np.ones(m - 1)], [-1, 0, 1]) * float(m + 1) ** 2
+    Ix, Iy, Iz = sp.identity(mx), sp.identity(my), sp.identity(mz)
+    L = sp.kron(Iz, sp.kron(Iy, t1(mx))) + sp.kron(Iz, sp.kron(t1(my), Ix)) + sp.kron(t1(mz), sp.kron(Iy, Ix))
+    return (alpha * L).tocsr()
+
+
+def sine_mode(m, p):
+    x = np.arange(m)
+    return np.sin((x + 1) * p * np.pi / (m + 1))
+
+
+def lam1(m, p, alpha):
+    """1-D Dirichlet eigenvalue of alpha*T_h: -4 alpha (m+1)^2 sin^2(p pi / (2(m+1)))."""
+    return -4.0 * alpha * (m + 1) ** 2 * math.sin(p * math.pi / (2 * (m + 1))) ** 2
+
+
+# ---------------------------------------------------------------------------------------------
+# Operators
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("mx,my,mz", [(5, 5, 5), (6, 4, 7), (1, 3, 2), (12, 12, 12)])
+def test_stencil_sine_modes_closed_form(mx, my, mz):
+    """Sine modes are exact eigenvectors of the Dirichlet 7-point Laplacian (closed form)."""
+    alpha = 0.01
+    p = W.heat(mx, 1, 1, my=my, mz=mz, extras=False)
+    op = oracle.Operator(p)
+    rng = np.random.default_rng(0)
+    for _ in range(4):
+        px, py, pz = rng.integers(1, mx + 1), rng.integers(1, my + 1), rng.integers(1, mz + 1)
+        phi = np.einsum("k,j,i->kji", sine_mode(mz, pz), sine_mode(my, py), sine_mode(mx, px)).ravel()
+        lam = lam1(mx, px, alpha) + lam1(my, py, alpha) + lam1(mz, pz, alpha)
+        y = op.apply(phi)
+        assert np.max(np.abs(y - lam * phi)) <= 1e-13 * abs(lam) * np.max(np.abs(phi)) + 1e-300
+
+
+def test_stencil_matches_kronecker_sum():
+    p = W.heat(7, 2, 1, my=5, mz=6, extras=False)
+    A = kron_laplacian(7, 5, 6, 0.01)
+    u = np.random.default_rng(1).standard_normal(7 * 5 * 6)
+    y = oracle.Operator(p).apply(u)
+    assert np.allclose(y, A @ u, rtol=1e-14, atol=1e-14 * np.abs(A @ u).max())
+
+
+def test_csr_apply_examples_and_scipy():
+    # SPEC example: [[0,1],[-1,0]] (3,4) = (4,-3)
+    p = {"op": "csr", "n": 2, "row_ptr": np.array([0, 1, 2]), "col_idx": np.array([1, 0], dtype=np.int32),
+         "val": np.array([1.0, -1.0]), "b": None}
+    assert np.array_equal(oracle.Operator(p).apply(np.array([3.0, 4.0])), np.array([4.0, -3.0]))
+    rp, ci, va, dense = W.random_csr(40, 6, seed=3)
+    p = {"op": "csr", "n": 40, "row_ptr": rp, "col_idx": ci, "val": va, "b": None}
+    x = np.random.default_rng(2).standard_normal(40)
+    assert np.allclose(oracle.Operator(p).apply(x), dense @ x, rtol=1e-14, atol=1e-13)
+
+
+def test_lifting_is_augmented_matrix():
+    """A' = [[A, b], [0, 0]]; the extra coordinate stays 1."""
+    rp, ci, va, dense = W.random_csr(10, 4, seed=5)
+    b = np.random.default_rng(6).uniform(-1, 1, 10)
+    p = {"op": "csr", "n": 10, "row_ptr": rp, "col_idx": ci, "val": va, "b": b}
+    Ap = np.zeros((11, 11))
+    Ap[:10, :10] = dense
+    Ap[:10, 10] = b
+    x = np.random.default_rng(7).standard_normal(11)
+    y = oracle.Operator(p).apply(x)
+    assert y[10] == 0.0
+    assert np.allclose(y, Ap @ x, rtol=1e-14, atol=1e-13)
+
+
+# ---------------------------------------------------------------------------------------------
+# Small expm
+# ---------------------------------------------------------------------------------------------
+def test_expm_identities_and_scipy():
+    k = 9
+    assert np.array_equal(oracle.expm(np.zeros((k, k))), np.eye(k))  # e^0 = I exactly
+    d = np.array([-3.0, -0.5, 0.0, 1.0, 2.5])
+    assert np.allclose(oracle.expm(np.diag(d)), np.diag(np.exp(d)), rtol=1e-14, atol=0)
+    rng = np.random.default_rng(0)
+    for scale in (0.1, 3.0, 50.0):
+        M = rng.standard_normal((k, k)) * scale / k
+        F = oracle.expm(M)
+        S = sla.expm(M)
+        assert np.max(np.abs(F - S)) <= 1e-12 * np.max(np.abs(S))
+        assert np.allclose(oracle.expm(M.T), F.T, rtol=1e-12, atol=1e-12 * np.abs(F).max())
+        if scale <= 3.0:
+            assert np.allclose(F @ oracle.expm(-M), np.eye(k), atol=1e-12)
+
+
+def test_expm_large_norm_symmetric_mpmath():
+    """Symmetric negative definite H with eigenvalues over 7 decades, ||H t|| up to 2e6 (C5 scale):
+    against a 40-digit mpmath expm. Scaling and squaring with ||.|| <= 1/2 needs up to 23 squarings
+    here; the rounding error grows ~2^s eps, measured 1.2e-10 at t=20 (scipy's Pade-13, 3 fewer
+    squarings: 1.0e-11), so the pin is 2e-10 of max(1, |ref|)."""
+    import mpmath as mp
+    rng = np.random.default_rng(1)
+    Q, _ = np.linalg.qr(rng.standard_normal((30, 30)))
+    lam = -np.logspace(-2, 5, 30)
+    H = (Q * lam) @ Q.T
+    H = 0.5 * (H + H.T)
+    mp.mp.dps = 40
+    for t, tol in ((0.02, 2e-12), (1.0, 5e-11), (20.0, 2e-10)):
+        E = mp.expm(mp.matrix(H * t))
+        ref = np.array([float(E[i, 0]) for i in range(30)])
+        x = oracle.expm(H * t)[:, 0]
+        assert np.max(np.abs(x - ref)) <= tol * max(1.0, np.abs(ref).max())
+
+
+def test_expm_semigroup():
+    """e^{H(t+s)} = e^{Hs} e^{Ht}."""
+    rng = np.random.default_rng(4)
+    H = rng.standard_normal((12, 12))
+    X = oracle.expm_e1_times(H, 0.05, 40)
+    E = oracle.expm(H * 0.05)
+    for j in range(40):
+        assert np.allclose(E @ X[j], X[j + 1], rtol=1e-12, atol=1e-12 * np.abs(X[j + 1]).max())
+
+
+# ---------------------------------------------------------------------------------------------
+# Lanczos / Arnoldi
+# ---------------------------------------------------------------------------------------------
+def identity_rows(n):
+    return [W.sparse([i], [1.0]) for i in range(n)]
+
+
+def test_arnoldi_krylov_relation_and_orthonormality():
+    rp, ci, va, dense = W.random_csr(60, 8, seed=11)
+    p = {"op": "csr", "n": 60, "row_ptr": rp, "col_idx": ci, "val": va, "b": None, "outs": identity_rows(60)}
+    v = np.random.default_rng(12).standard_normal(60)
+    k = 20
+    r = oracle.arnoldi(p, v, k)
+    V = r["P"]  # C = I so P = V_k
+    Hf = r["Hfull"]
+    # single-pass MGS loses orthogonality ~ eps * cond(Krylov basis) (measured 1.4e-8 here)
+    assert np.allclose(V.T @ V, np.eye(k), atol=1e-7)
+    R = dense @ V - V @ Hf[:k, :k]
+    # the residual lives only in the last column with norm h_{k+1,k}
+    assert np.max(np.abs(R[:, :-1])) <= 1e-12 * (1 + np.abs(dense).sum(axis=0).max())
+    assert abs(np.linalg.norm(R[:, -1]) - Hf[k, k - 1]) <= 1e-12 * (1 + Hf[k, k - 1])
+    assert np.allclose(V[:, 0], v / np.linalg.norm(v), atol=1e-15)
+    assert np.allclose(np.triu(Hf[:k, :k].T, 2), 0.0)  # Hessenberg
+
+
+def test_lanczos_equals_arnoldi_on_symmetric_input():
+    p = W.heat(6, 2, 10, extras=False)
+    p["outs"] = identity_rows(216)
+    v = np.random.default_rng(5).standard_normal(216)
+    la = oracle.lanczos(p, v, 10)
+    ar = oracle.arnoldi(p, v, 10)
+    assert np.allclose(la["H"], ar["H"], rtol=1e-9, atol=1e-9 * np.abs(ar["H"]).max())
+    assert np.allclose(la["P"], ar["P"], atol=1e-9)
+    assert np.allclose(la["H"], la["H"].T)
+
+
+def test_lanczos_eigenvector_start_breaks_down():
+    """Start = sine mode -> breakdown after one step with H = [lambda]."""
+    m = 8
+    p = W.heat(m, 1, 10, extras=False)
+    p["outs"] = [W.allv()]
+    phi = np.einsum("k,j,i->kji", sine_mode(m, 2), sine_mode(m, 1), sine_mode(m, 3)).ravel()
+    lam = lam1(m, 3, 0.01) + lam1(m, 1, 0.01) + lam1(m, 2, 0.01)
+    for fn in (oracle.lanczos, oracle.arnoldi):
+        r = fn(p, phi, 10)
+        assert r["k_eff"] == 1
+        assert abs(r["H"][0, 0] - lam) <= 1e-13 * abs(lam)
+
+
+def test_lanczos_diag_exact_at_full_dimension():
+    """diag(1,2,3), v=(1,1,1)/sqrt(3), k=3: exact vs diagonal expm."""
+    p = {"op": "csr", "n": 3, "row_ptr": np.array([0, 1, 2, 3]), "col_idx": np.array([0, 1, 2], dtype=np.int32),
+         "val": np.array([1.0, 2.0, 3.0]), "b": None, "outs": identity_rows(3),
+         "gens": [W.sparse([0, 1, 2], [1 / math.sqrt(3)] * 3)], "z_lo": [0.0], "z_hi": [1.0],
+         "center": None, "step": 0.1, "n_steps": 10, "k": 3, "method": "lanczos", "thresholds": []}
+    res = oracle.krylov_project(p)
+    for j, t in enumerate(res["times"]):
+        exact = np.exp(np.array([1.0, 2.0, 3.0]) * t) / math.sqrt(3)
+        assert np.allclose(res["coeff"][j, :, 0], exact, rtol=1e-12)
+
+
+def test_scale_invariance():
+    p = W.heat(5, 2, 8, extras=True)
+    v = W.dense_vec(p["gens"][0], p)
+    a = oracle.lanczos(p, v, 8)
+    b = oracle.lanczos(p, 4.0 * v, 8)  # power-of-two scale: bitwise identical basis
+    assert np.array_equal(a["H"], b["H"]) and np.array_equal(a["P"], b["P"])
+    assert b["beta0"] == 4.0 * a["beta0"]
+
+
+def test_first_lanczos_step_closed_form():
+    """Corner block b^3, Dirichlet stencil, c = alpha (m+1)^2: alpha_1 = -6c/b and
+    beta_1^2 = c^2 [sum_{s=0..3} C(3,s) 2^s (b-2)^{3-s} (6/b - s)^2 + 3 b^2] / b^3 (cell counting,
+    SURVEY A.16); first projections: total heat b^1.5, corner b^-1.5, cell (b,b,b) 0."""
+    for m, b in [(20, 4), (40, 4), (100, 10), (12, 3)]:
+        p = W.heat(m, b, 2)
+        v = W.dense_vec(p["gens"][0], p)
+        r = oracle.lanczos(p, v, 2)
+        c = 0.01 * (m + 1) ** 2
+        a1 = -6 * c / b
+        s = sum(math.comb(3, q) * 2 ** q * (b - 2) ** (3 - q) * (6 / b - q) ** 2 for q in range(4))
+        b1 = math.sqrt(c * c * (s + 3 * b * b) / b ** 3)
+        assert abs(r["alpha"][0] - a1) <= 1e-13 * abs(a1)
+        assert abs(r["beta"][0] - b1) <= 1e-13 * b1
+        P1 = r["P"][:, 0]
+        assert P1[0] == 0.0  # center cell far from the block
+        assert abs(P1[1] - b ** 1.5) <= 1e-13 * b ** 1.5
+        assert P1[2] == 0.0
+        assert abs(P1[3] - b ** -1.5) <= 1e-15
+
+
+# ---------------------------------------------------------------------------------------------
+# Krylov approximant against the plain definition where they coincide
+# ---------------------------------------------------------------------------------------------
+def test_config1_matches_dense_expm():
+    """C1 (n=125, only 25 distinct eigenvalues): k=30 >= Krylov dimension, so the Arnoldi result
+    equals O e^{At} v_d; dense expm by scipy (library routine) on the Kronecker-sum matrix."""
+    p = W.config1()
+    res = oracle.krylov_project(p)
+    A = kron_laplacian(5, 5, 5, 0.01).toarray()
+    O = np.array([W.dense_vec(o, p) for o in p["outs"]])
+    E = np.array([W.dense_vec(g, p) for g in p["gens"]]).T
+    scale = np.abs(res["coeff"]).max()
+    for j in range(0, p["n_steps"] + 1, 7):
+        ref = O @ sla.expm(A * (j * p["step"])) @ E
+        assert np.max(np.abs(res["coeff"][j] - ref)) <= 1e-12 * scale
+
+
+def test_config1_verdicts():
+    """C1: exact hi peak 0.0298306499842393895 at step 145 (mpmath); theta=0.05 SAFE;
+    theta=0.02 UNSAFE first at step 74. Cross-checked here against scipy dense expm."""
+    p = W.config1()
+    res = oracle.krylov_project(p)
+    cb = oracle.check_box(p, res["coeff"])
+    assert not cb["found"]
+    assert int(np.argmax(cb["hi"][:, 0])) == 145
+    assert abs(cb["hi"][:, 0].max() - 0.0298306499842393895) <= 1e-14
+    cb2 = oracle.check_box(p, res["coeff"], [(0, W.GE, 0.02)])
+    assert cb2["found"] and cb2["step"] == 74
+    A = kron_laplacian(5, 5, 5, 0.01).toarray()
+    O = np.array([W.dense_vec(o, p) for o in p["outs"]])
+    E = np.array([W.dense_vec(g, p) for g in p["gens"]]).T
+    hi = lambda j: np.sum(np.maximum(0.9 * (O @ sla.expm(A * j * 0.02) @ E), 1.1 * (O @ sla.expm(A * j * 0.02) @ E)))
+    assert hi(73) < 0.02 <= hi(74)
+    assert abs(hi(145) - 0.0298306499842393895) <= 1e-14
+
+
+def dst_heat_projection(m, b, t, alpha=0.01):
+    """Closed form for a tensor-product start on the Dirichlet stencil: e^{At}(1_b x 1_b x 1_b) is
+    the tensor product of 1-D solutions u(t) = S diag(e^{lam t}) S^T 1_b, S = orthonormal DST-I
+    basis (separable eigendecomposition)."""
+    x = np.arange(m)
+    S = np.sqrt(2.0 / (m + 1)) * np.sin(np.outer(x + 1, np.arange(1, m + 1)) * np.pi / (m + 1))
+    lam = np.array([lam1(m, q, alpha) for q in range(1, m + 1)])
+    v = np.zeros(m)
+    v[:b] = 1.0
+    return S @ (np.exp(lam * t) * (S.T @ v))
+
+
+def test_lanczos_converges_to_dst_closed_form():
+    """Lanczos reaches the separable closed form at 1e-12 with k=60 (m=10)."""
+    m, b = 10, 3
+    p = W.heat(m, b, 60, n_steps=50, step=0.2)
+    res = oracle.krylov_project(p)
+    c = W.center_index(m)
+    for j in range(0, 51, 5):
+        u = dst_heat_projection(m, b, j * 0.2)
+        exact = [u[c] ** 3, u.sum() ** 3, u[b] ** 3, u[0] ** 3]
+        got = res["coeff"][j, :, 0]
+        assert np.max(np.abs(got - np.array(exact))) <= 1e-11 * max(1.0, abs(exact[1]))
+
+
+def test_t0_identity():
+    """c[0][r][d] = C_r v_d: e^0 = I exactly."""
+    p = W.config3(n_steps=3)
+    p = dict(p, mx=30, my=30, mz=30, gens=[W.box((0, 0, 0), (5, 5, 5))], k=12,
+             outs=[W.point(14, 14, 14), W.allv(), W.point(5, 5, 5), W.point(0, 0, 0), W.box((2, 2, 2), (9, 9, 9), 0.5)])
+    res = oracle.krylov_project(p)
+    assert res["coeff"][0, 0, 0] == 0.0 and res["coeff"][0, 2, 0] == 0.0
+    assert abs(res["coeff"][0, 1, 0] - 125.0) <= 1e-12 * 125
+    assert abs(res["coeff"][0, 3, 0] - 1.0) <= 1e-14
+    assert abs(res["coeff"][0, 4, 0] - 0.5 * 27) <= 1e-13 * 13.5
+
+
+def test_heat_invariants_dense():
+    """Physics of P:973 on the converged path: 0 <= e^{At}v <= max v and total heat decreasing."""
+    m, b = 8, 2
+    p = W.heat(m, b, 100, n_steps=40, step=0.5)
+    p["outs"] = [W.allv()] + [W.point(x, y, z) for (x, y, z) in [(0, 0, 0), (3, 3, 3), (7, 7, 7)]]
+    res = oracle.krylov_project(p)
+    tot = res["coeff"][:, 0, 0]
+    assert np.all(np.diff(tot) <= 1e-12 * tot[0])
+    pts = res["coeff"][:, 1:, 0]
+    assert np.all(pts >= -1e-13) and np.all(pts <= 1 + 1e-13)
+
+
+# ---------------------------------------------------------------------------------------------
+# The paper's worked example (Fig. 2, §2.2, §3, §4.1)
+# ---------------------------------------------------------------------------------------------
+def test_oscillator_paper_example():
+    g = json.load(open(os.path.join(GOLD, "oscillator.json")))
+    p = W.oscillator()
+    res = oracle.krylov_project(p)
+    # basis row at 3pi/4 (Fig. 2c): columns (i_y, i_f)
+    row = res["coeff"][3, 0, :]
+    assert np.allclose(row, g["basis_row_3pi4"]["value"], atol=g["basis_row_3pi4"]["printed_digits_tol"])
+    cb = oracle.check_box(p, res["coeff"])
+    assert cb["found"] and cb["step"] == g["first_unsafe_step"]["value"]
+    for j in g["infeasible_steps"]["value"]:
+        assert not (cb["lo"][j, 0] <= 4.0 <= cb["hi"][j, 0])
+    # x0 = (-5, y0, 0, 1): y0 = z_y
+    assert abs(cb["z"][0] - g["x0"]["value"][1]) <= g["x0"]["printed_digits_tol"]
+    assert abs(cb["z"][0] - (4 * math.sqrt(2) - 5)) <= 1e-12  # exact: y0 = 4 sqrt2 - 5
+    # unsafe state (4, 3.07, 2.36, 1): simulate from x0 with full-state outputs
+    q = dict(p, outs=[W.sparse([i], [1.0]) for i in range(4)])
+    full = oracle.krylov_project(q)["coeff"][3]  # 4 x 2
+    state = full @ cb["z"]
+    assert np.allclose(state, g["unsafe_state"]["value"], atol=g["unsafe_state"]["printed_digits_tol"])
+    # expm block of Fig. 2a: e^{A 3pi/4} columns from unit directions (full state, 4 simulations)
+    Ap = np.array([[0, 1, 0, 0], [-1, 0, 0, 0], [0, 0, 0, 1], [0, 0, 0, 0]], dtype=float)
+    F = oracle.expm(Ap * 3 * math.pi / 4)
+    assert np.allclose(F[:2, :2], g["expAt_3pi4_block"]["value"], atol=g["expAt_3pi4_block"]["printed_digits_tol"])
+    assert abs(F[2, 3] - g["expAt_3pi4_t_row_a_entry"]["value"]) <= g["expAt_3pi4_t_row_a_entry"]["printed_digits_tol"]
+    # transpose simulation: simulate A^T from C^T = e_1
+    assert np.allclose(F.T[:, 0], g["transpose_state_3pi4"]["value"], atol=g["transpose_state_3pi4"]["printed_digits_tol"])
+    # Arnoldi from the y0 generator breaks down exactly (h_32 = 0, k_eff = 2)
+    assert res["per_dir"][0]["k_eff"] == 2 and res["per_dir"][0]["h_next"] == 0.0
+
+
+# ---------------------------------------------------------------------------------------------
+# Box check = the LP of Fig. 2(c) for a box initial set and one output half-space
+# ---------------------------------------------------------------------------------------------
+def test_box_check_equals_lp():
+    rng = np.random.default_rng(9)
+    for trial in range(20):
+        nd = int(rng.integers(1, 6))
+        c = rng.standard_normal((1, 1, nd))
+        zlo = rng.uniform(-2, 0, nd)
+        zhi = zlo + rng.uniform(0, 2, nd)
+        p = {"z_lo": zlo, "z_hi": zhi, "b": None, "center": None, "step": 1.0}
+        cb = oracle.check_box(p, c, [])
+        for sgn, key in ((1, "lo"), (-1, "hi")):
+            r = linprog(sgn * c[0, 0], bounds=list(zip(zlo, zhi)), method="highs")
+            assert abs(sgn * r.fun - cb[key][0, 0]) <= 1e-9 * (1 + np.abs(c).sum())
+        # verdict + witness feasibility for each sense
+        th = float(rng.uniform(cb["lo"][0, 0] - 1, cb["hi"][0, 0] + 1))
+        for s in (W.GE, W.LE, W.EQ):
+            cbs = oracle.check_box(p, c, [(0, s, th)])
+            A_eq = c[0]
+            if s == W.EQ:
+                r = linprog(np.zeros(nd), A_eq=A_eq, b_eq=[th], bounds=list(zip(zlo, zhi)), method="highs")
+            else:
+                sign = -1.0 if s == W.GE else 1.0  # GE: -c z <= -th ; LE: c z <= th
+                r = linprog(np.zeros(nd), A_ub=sign * A_eq, b_ub=[sign * th], bounds=list(zip(zlo, zhi)), method="highs")
+            feasible = r.status == 0
+            assert cbs["found"] == feasible
+            if feasible:
+                z = cbs["z"]
+                assert np.all(z >= zlo - 1e-12) and np.all(z <= zhi + 1e-12)
+                y = float(c[0, 0] @ z)
+                assert abs(y - cbs["y"]) <= 1e-12 * (1 + abs(y))
+                if s == W.GE:
+                    assert y >= th - 1e-12
+                elif s == W.LE:
+                    assert y <= th + 1e-12
+                else:
+                    assert abs(y - th) <= 1e-9 * (1 + abs(th))
+
+
+# ---------------------------------------------------------------------------------------------
+# Lemma 1 diagnostic
+# ---------------------------------------------------------------------------------------------
+def test_lemma1_sound_on_heat():
+    """bound >= actual full-state error (+ a rounding floor: the lemma is exact arithmetic)."""
+    m, b = 12, 3
+    for k in (10, 20, 40):
+        p = W.heat(m, b, k, n_steps=100, step=0.05)
+        n = m ** 3
+        p["outs"] = identity_rows(n)
+        res = oracle.krylov_project(p)
+        A = kron_laplacian(m, m, m, 0.01).toarray()
+        v = W.dense_vec(p["gens"][0], p)
+        T = 100 * 0.05
+        err = np.linalg.norm(sla.expm(A * T) @ v - res["coeff"][-1, :, 0])
+        assert res["mu"] <= 0.0
+        assert err <= res["lemma1"][0] + 1e-13 * np.linalg.norm(v)
+
+
+def test_gershgorin_mu_upper_bounds_symmetric_part():
+    rp, ci, va, dense = W.random_csr(30, 5, seed=21)
+    b = np.random.default_rng(3).uniform(-0.1, 0.1, 30)
+    p = {"op": "csr", "n": 30, "row_ptr": rp, "col_idx": ci, "val": va, "b": b}
+    Ap = np.zeros((31, 31))
+    Ap[:30, :30] = dense
+    Ap[:30, 30] = b
+    lam = np.linalg.eigvalsh(0.5 * (Ap + Ap.T)).max()
+    assert oracle.gershgorin_mu(p) >= lam - 1e-12
+    ph = W.heat(6, 2, 3)
+    lamh = np.linalg.eigvalsh(kron_laplacian(6, 6, 6, 0.01).toarray()).max()
+    assert oracle.gershgorin_mu(ph) >= lamh
