@@ -1,0 +1,189 @@
+/*
+ * krylov_reach.h — C ABI of the B200-native Krylov projected-reachability hot path
+ * (arXiv 1804.01583; PAPER.md cited as P:<line>; SURVEY.md §8(b) is the design note).
+ *
+ * What the library computes. For the affine system x' = Ax + b, an initial set
+ * x0 = c + sum_d z_d g_d with a box z_lo <= z <= z_hi (initial space E, §3.2), output rows
+ * C (o x n, §3.1), a step delta and N steps (t_j = j*delta, j = 0..N), it returns the
+ * basis-matrix sequence C e^{A t_j} E by Krylov simulation of one direction per column of E
+ * (§4.1; Eq. 2) — Arnoldi (Alg. 1) or Lanczos with projection
+ * (Alg. 3/4) — and, per step, the interval bounds of every output over the box together
+ * with the first violating step and a witness (Fig. 2(c)).
+ *
+ * Conventions (all functions):
+ *  - Every pointer argument of kr_problem is HOST memory, borrowed for the duration of
+ *    krylov_reach_create only: the library deep-copies what it needs to the device.
+ *  - Output arrays are caller-allocated HOST buffers whose sizes follow from the problem:
+ *    n_dir = n_gen + has_fixed, has_fixed = (center != NULL || b != NULL).
+ *  - Errors: every call returns a kr_status; krylov_last_error() returns a thread-local message for
+ *    the last non-OK status. After KR_ECUDA or KR_ENCCL the handle is unusable (destroy it).
+ *  - No C++ types, exceptions or torch types cross this ABI.
+ *  - Numerics: fp64 throughout. Results are bit-reproducible for identical inputs
+ *    and identical partitioning (fixed-order reductions, no floating-point atomics).
+ */
+#ifndef KRYLOV_REACH_H
+#define KRYLOV_REACH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KR_OK = 0,
+    KR_EINVAL = 1,      /* invalid argument: k < 1, step <= 0, n_steps < 0, z_lo > z_hi, bad enum, NULL */
+    KR_EDIM = 2,        /* dimension mismatch / index out of range                          */
+    KR_ENOMEM = 3,      /* device allocation failed or caller workspace too small                      */
+    KR_ECUDA = 4,       /* CUDA runtime / driver failure                                               */
+    KR_ENCCL = 5,       /* NCCL failure                                                                */
+    KR_ENOTSYM = 6,     /* Lanczos requested on a non-symmetric operator (Alg. 3 needs A = A^T, §4.3)  */
+    KR_EZERO = 7,       /* a direction vector is zero: ||v|| = 0 cannot be normalised (Alg. 1 line 1)  */
+    KR_ENONFINITE = 8,  /* non-finite input value                                                      */
+    KR_ESTATE = 9       /* call out of order (check_box before project)                               */
+} kr_status;
+
+typedef enum { KR_OP_STENCIL7 = 0, KR_OP_CSR = 1 } kr_op;
+typedef enum { KR_AUTO = 0, KR_ARNOLDI = 1, KR_LANCZOS = 2 } kr_method;
+typedef enum { KR_PART_NONE = 0, KR_PART_ZSLAB = 1, KR_PART_DIRS = 2 } kr_partition;
+typedef enum { KR_GE = 0, KR_LE = 1, KR_EQ = 2, KR_NONE = 3 } kr_sense;
+typedef enum { KR_VEC_SPARSE = 0, KR_VEC_BOX = 1, KR_VEC_ALL = 2 } kr_vec_kind;
+
+/* An n-vector given compactly: a generator column of E, the center c, or an output row of C
+ * (P:447). Linear index of stencil cell (x,y,z) is x + mx*(y + my*z) (x fastest).
+ *  KR_VEC_SPARSE: entries val[e] at idx[e] (e < nnz; duplicates add).
+ *  KR_VEC_BOX:    value on the index box [lo, hi) (stencil: 3D; CSR: axis 0 only, lo[1..2]/hi[1..2] ignored).
+ *  KR_VEC_ALL:    value everywhere (e.g. total heat). Never includes the lifted coordinate. */
+typedef struct {
+    int32_t kind;
+    int64_t nnz;
+    const int64_t* idx;
+    const double* val;
+    int64_t lo[3], hi[3];
+    double value;
+} kr_vec;
+
+/* Opaque multi-GPU communicator (one process per GPU; NCCL over NVLink/NVSwitch). */
+typedef struct kr_comm kr_comm;
+
+typedef struct {
+    /* Operator A. */
+    int32_t op;                 /* kr_op */
+    int64_t mx, my, mz;         /* STENCIL7: grid; A = alpha * L_h, Dirichlet, h_a = 1/(m_a+1) */
+    double alpha;
+    int64_t n, nnz;             /* CSR: n x n, row_ptr[n+1] (int64), col_idx[nnz] (int32), val[nnz]   */
+    const int64_t* row_ptr;
+    const int32_t* col_idx;
+    const double* val;
+    const double* b;            /* CSR only: affine term (length n) or NULL. Lifted into A' = [[A,b],[0,0]]
+                                   with the extra coordinate fixed at 1. Must be NULL for STENCIL7. */
+    /* Initial set. */
+    int32_t n_gen;              /* generator directions g_d, d < n_gen                                  */
+    const kr_vec* gen;
+    const double* z_lo;         /* box on z, length n_gen                                               */
+    const double* z_hi;
+    const kr_vec* center;       /* c, or NULL for 0. With b != NULL or center != NULL one fixed direction
+                                   v_f = [c; 1] (or c) with z_f = 1 is appended             */
+    /* Output space. */
+    int32_t n_out;
+    const kr_vec* out;          /* rows of C; entries at the lifted coordinate are 0                   */
+    /* Time grid: t_j = (double)j * step, j = 0..n_steps. */
+    double step;
+    int64_t n_steps;
+    /* Krylov iteration. */
+    int32_t k;                  /* Krylov dimension (max; k_eff < k on breakdown), 1..64     */
+    int32_t method;             /* kr_method. AUTO: Lanczos for STENCIL7 or exactly symmetric CSR (b=NULL) */
+    /* Partitioning. */
+    int32_t part;               /* kr_partition. ZSLAB: STENCIL7 + LANCZOS only; DIRS: any             */
+    int32_t virtual_slabs;      /* ZSLAB without a comm: emulate P = virtual_slabs slabs in this process
+                                   on one device (halo copies instead of NCCL); 0/1 = off                */
+    kr_comm* comm;              /* NULL = single process; otherwise create/project/check are collective */
+    int32_t device;             /* CUDA device ordinal                                                  */
+    void* stream;               /* cudaStream_t to run on, or NULL for a library-owned stream           */
+    void* workspace;            /* optional caller-owned device buffer for the state vectors (e.g. a torch
+                                   uint8 tensor) of at least krylov_workspace_bytes; NULL = library
+                                   allocates. Must outlive the handle. Small descriptors and results are
+                                   always library-allocated.                                             */
+    size_t workspace_bytes;
+} kr_problem;
+
+typedef struct kr_handle kr_handle;
+
+/* Per-direction diagnostics (Lemma 1). */
+typedef struct {
+    int32_t k_eff;              /* Krylov dimension actually used                                       */
+    double beta0;               /* ||v_d||                                                              */
+    double h_next;              /* h_{k_eff+1,k_eff} (0 on exact breakdown)                             */
+    double lemma1_bound;        /* beta0 * h_next * e^{max(mu,0) T} * int_0^T |e_k^T e^{Ht} e_1| dt, with
+                                   mu a Gershgorin upper bound of lambda_max((A+A^T)/2) and the integral
+                                   by the trapezoid rule on the t_j grid                                 */
+} kr_dir_stats;
+
+/* Counter-example. */
+typedef struct {
+    int32_t found;              /* 1 = UNSAFE (some row violates at some step), 0 = SAFE               */
+    int64_t step;               /* first violating j (first-hit semantics)                 */
+    double time;                /* (double)step * delta                                                */
+    int32_t row;                /* lowest violating output row at that step                            */
+    double y;                   /* output value at the witness: sum_d c[j][row][d] z*_d                 */
+} kr_cex;
+
+/* Device bytes this rank needs for p (3 slab vectors + halos + scratch for the Lanczos stencil path;
+ * (k+1) vectors per direction for Arnoldi). Host-only, no GPU work. */
+kr_status krylov_workspace_bytes(const kr_problem* p, size_t* bytes);
+
+/* Validate p, select the device, allocate (or bind the caller workspace), upload the operator and
+ * descriptors, and prepare the per-step launch graph. Collective when p->comm != NULL. */
+kr_status krylov_reach_create(const kr_problem* p, kr_handle** out);
+
+/* Run the hot path: start vectors, k Krylov steps per direction (fused stencil Lanczos in one HBM pass
+ * per step, or batched SpMM + Gram-Schmidt Arnoldi), batched k x k Pade exponentials for every t_j
+ * (Eq. 2) and the projection through P = C V_k (Alg. 4).
+ * coeff: HOST [(n_steps+1)][n_out][n_dir] basis-matrix entries c[j][r][d] ~= C_r e^{A t_j} v_d.
+ * stats: HOST [n_dir] or NULL. Either output may be NULL to leave the results on the device only
+ * (then krylov_check_box still works). Synchronises the stream before returning. */
+kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats);
+
+/* Per-step safety check over the box initial set (the exact LP optimum of Fig. 2(c) for a box and one
+ * output half-space per row): lo/hi[j][r] = c_f + sum_d min/max(c z_lo_d, c z_hi_d); row r is unsafe at
+ * step j if (GE) hi >= thr, (LE) lo <= thr, (EQ) lo <= thr <= hi; KR_NONE rows are never unsafe.
+ * sense, thr: HOST [n_out]. lo, hi: HOST [(n_steps+1)][n_out] or NULL. cex: HOST, required.
+ * z_witness: HOST [n_dir] or NULL: GE -> z_hi where c >= 0 else z_lo; LE mirrored; EQ interpolates
+ * lambda = (thr-lo)/(hi-lo) along that vertex path. Requires a prior krylov_project. */
+kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr, double* lo, double* hi,
+                           kr_cex* cex, double* z_witness);
+
+void krylov_reach_destroy(kr_handle* h);
+
+const char* krylov_last_error(void);
+
+/* Number of this library's kernel launches issued so far on h (graph nodes counted per replay). */
+int64_t krylov_launch_count(const kr_handle* h);
+
+/* Device-side duration in ms of the last krylov_project's Krylov iteration phase and of its dominant
+ * kernel (mean per launch), measured with CUDA events on the library stream. */
+kr_status krylov_last_timing(const kr_handle* h, double* iter_ms, double* step_kernel_ms_mean,
+                             int64_t* step_kernel_launches, double* step_kernel_bytes);
+
+/* Copy direction `dir`'s Krylov data to the host: H [(k+1)][k] row-major (the (k+1) x k Hessenberg
+ * of Alg. 1 / tridiagonal of Alg. 3, entries beyond k_eff are 0) and P = C V [n_out][k] (Alg. 4).
+ * Either pointer may be NULL. KR_EDIM if `dir` is not handled by this rank. Requires krylov_project. */
+kr_status krylov_krylov_data(const kr_handle* h, int32_t dir, double* H, double* P);
+
+/* ---- multi-GPU plumbing (one process per GPU) -------------------------------------------------- */
+/* Rank 0 calls krylov_comm_unique_id (128 bytes out), the caller broadcasts it (torch.distributed),
+ * then every rank calls krylov_comm_create. Collective. */
+kr_status krylov_comm_unique_id(void* id128);
+kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int32_t device, kr_comm** out);
+void krylov_comm_destroy(kr_comm* c);
+
+/* z-slab partition of the stencil grid (host logic, no GPU): rank r of world owns global planes
+ * [z0, z1). Balanced: the first mz % world ranks own one extra plane. KR_EINVAL if a rank would own
+ * fewer than 2 planes (the depth-2 halo comes from one neighbour). */
+kr_status krylov_zslab_range(int64_t mz, int32_t world, int32_t rank, int64_t* z0, int64_t* z1);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRYLOV_REACH_H */

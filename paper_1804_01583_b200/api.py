@@ -1,0 +1,235 @@
+"""Thin Python binding over the C ABI (include/krylov_reach.h). Same names as the ABI; argument
+marshalling only. Problems are the dicts of workloads/ (see its docstring)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi as A
+
+_METHOD = {"auto": A.KR_AUTO, "arnoldi": A.KR_ARNOLDI, "lanczos": A.KR_LANCZOS}
+_PART = {None: A.KR_PART_NONE, "none": A.KR_PART_NONE, "zslab": A.KR_PART_ZSLAB, "dirs": A.KR_PART_DIRS}
+_KIND = {"sparse": A.KR_VEC_SPARSE, "box": A.KR_VEC_BOX, "all": A.KR_VEC_ALL}
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+class _Marshal:
+    """Builds a kr_problem and keeps every numpy buffer alive while the C call borrows it."""
+
+    def __init__(self, prob, device=0, stream=None, workspace=None, workspace_bytes=0, comm=None, part=None,
+                 virtual_slabs=0, method=None):
+        self.keep = []
+        p = A.kr_problem()
+        if prob["op"] == "stencil":
+            p.op = A.KR_OP_STENCIL7
+            p.mx, p.my, p.mz = int(prob["mx"]), int(prob["my"]), int(prob["mz"])
+            p.alpha = float(prob["alpha"])
+        else:
+            p.op = A.KR_OP_CSR
+            rp = self._arr(prob["row_ptr"], np.int64)
+            ci = self._arr(prob["col_idx"], np.int32)
+            va = self._arr(prob["val"], np.float64)
+            p.n, p.nnz = int(prob["n"]), int(ci.size)
+            p.row_ptr, p.col_idx, p.val = _p(rp), _p(ci), _p(va)
+            if prob.get("b") is not None:
+                p.b = _p(self._arr(prob["b"], np.float64))
+        gens = prob["gens"]
+        p.n_gen = len(gens)
+        if gens:
+            gv = (A.kr_vec * len(gens))(*[self._vec(g) for g in gens])
+            self.keep.append(gv)
+            p.gen = gv
+            p.z_lo = _p(self._arr(prob["z_lo"], np.float64))
+            p.z_hi = _p(self._arr(prob["z_hi"], np.float64))
+        if prob.get("center") is not None:
+            cv = self._vec(prob["center"])
+            self.keep.append(cv)
+            p.center = C.pointer(cv)
+        outs = prob["outs"]
+        ov = (A.kr_vec * len(outs))(*[self._vec(o) for o in outs])
+        self.keep.append(ov)
+        p.n_out, p.out = len(outs), ov
+        p.step, p.n_steps = float(prob["step"]), int(prob["n_steps"])
+        p.k = int(prob["k"])
+        p.method = _METHOD[method or prob.get("method", "auto")]
+        p.part = _PART[part]
+        p.virtual_slabs = int(virtual_slabs)
+        p.comm = comm.ptr if comm is not None else None
+        p.device = int(device)
+        p.stream = stream
+        p.workspace = workspace
+        p.workspace_bytes = int(workspace_bytes)
+        self.p = p
+
+    def _arr(self, a, dt):
+        a = np.ascontiguousarray(a, dtype=dt)
+        self.keep.append(a)
+        return a
+
+    def _vec(self, v):
+        kv = A.kr_vec()
+        kv.kind = _KIND[v["kind"]]
+        if v["kind"] == "sparse":
+            idx = self._arr(v["idx"], np.int64)
+            val = self._arr(v["val"], np.float64)
+            kv.nnz, kv.idx, kv.val = idx.size, _p(idx), _p(val)
+        else:
+            kv.value = float(v["value"])
+            if v["kind"] == "box":
+                lo, hi = list(v["lo"]) + [0] * (3 - len(v["lo"])), list(v["hi"]) + [0] * (3 - len(v["hi"]))
+                kv.lo = (C.c_int64 * 3)(*lo)
+                kv.hi = (C.c_int64 * 3)(*hi)
+        return kv
+
+
+def n_dirs(prob):
+    return len(prob["gens"]) + (1 if (prob.get("center") is not None or prob.get("b") is not None) else 0)
+
+
+def krylov_workspace_bytes(prob, **kw):
+    m = _Marshal(prob, **kw)
+    out = C.c_size_t()
+    A.check(A.lib().krylov_workspace_bytes(C.byref(m.p), C.byref(out)))
+    return out.value
+
+
+class KrylovReach:
+    """One handle = one problem on one device (krylov_reach_create). project() runs the hot path,
+    check_box() the per-step safety check."""
+
+    def __init__(self, prob, device=0, stream=None, workspace=None, workspace_bytes=0, comm=None, part=None,
+                 virtual_slabs=0, method=None):
+        self.prob = prob
+        m = _Marshal(prob, device, stream, workspace, workspace_bytes, comm, part, virtual_slabs, method)
+        h = C.c_void_p()
+        A.check(A.lib().krylov_reach_create(C.byref(m.p), C.byref(h)))
+        self.h = h
+        self.n_out = len(prob["outs"])
+        self.n_dir = n_dirs(prob)
+        self.n_steps = int(prob["n_steps"])
+
+    def project(self, want=True):
+        if not want:
+            A.check(A.lib().krylov_project(self.h, None, None))
+            return None, None
+        coeff = np.empty((self.n_steps + 1, self.n_out, self.n_dir))
+        st = (A.kr_dir_stats * self.n_dir)()
+        A.check(A.lib().krylov_project(self.h, _p(coeff), st))
+        stats = [{"k_eff": s.k_eff, "beta0": s.beta0, "h_next": s.h_next, "lemma1": s.lemma1_bound} for s in st]
+        return coeff, stats
+
+    def check_box(self, thresholds=None, want_bounds=True):
+        """thresholds: list of (row, sense, theta) with sense 0=GE, 1=LE, 2=EQ (rows not listed: none)."""
+        thresholds = self.prob.get("thresholds", []) if thresholds is None else thresholds
+        sense = np.full(self.n_out, A.KR_NONE, dtype=np.int32)
+        thr = np.zeros(self.n_out)
+        for r, s, t in thresholds:
+            sense[r] = s
+            thr[r] = t
+        lo = hi = None
+        if want_bounds:
+            lo = np.empty((self.n_steps + 1, self.n_out))
+            hi = np.empty((self.n_steps + 1, self.n_out))
+        cex = A.kr_cex()
+        z = np.empty(self.n_dir)
+        A.check(A.lib().krylov_check_box(self.h, _p(sense), _p(thr), _p(lo), _p(hi), C.byref(cex), _p(z)))
+        return {"lo": lo, "hi": hi, "found": bool(cex.found), "step": int(cex.step), "time": cex.time,
+                "row": int(cex.row), "y": cex.y, "z": z if cex.found else None}
+
+    def krylov_data(self, d=0):
+        """(H [(k+1) x k], P [n_out x k]) of direction d (Hessenberg / tridiagonal and P = C V)."""
+        k = int(self.prob["k"])
+        H = np.zeros((k + 1, k))
+        P = np.zeros((self.n_out, k))
+        A.check(A.lib().krylov_krylov_data(self.h, int(d), _p(H), _p(P)))
+        return H, P
+
+    def launch_count(self):
+        return int(A.lib().krylov_launch_count(self.h))
+
+    def last_timing(self):
+        it, st, bytes_ = C.c_double(), C.c_double(), C.c_double()
+        n = C.c_int64()
+        A.check(A.lib().krylov_last_timing(self.h, C.byref(it), C.byref(st), C.byref(n), C.byref(bytes_)))
+        return {"iter_ms": it.value, "step_ms_mean": st.value, "step_launches": n.value, "step_bytes": bytes_.value}
+
+    def close(self):
+        if getattr(self, "h", None):
+            A.lib().krylov_reach_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+# ABI-named functional wrappers
+def krylov_reach_create(prob, **kw):
+    return KrylovReach(prob, **kw)
+
+
+def krylov_project(handle):
+    return handle.project()
+
+
+def krylov_check_box(handle, thresholds=None):
+    return handle.check_box(thresholds)
+
+
+def krylov_reach_destroy(handle):
+    handle.close()
+
+
+def krylov_zslab_range(mz, world, rank):
+    z0, z1 = C.c_int64(), C.c_int64()
+    A.check(A.lib().krylov_zslab_range(int(mz), int(world), int(rank), C.byref(z0), C.byref(z1)))
+    return z0.value, z1.value
+
+
+class KrComm:
+    """NCCL communicator for one process per GPU. The 128-byte ncclUniqueId is produced by rank 0
+    (krylov_comm_unique_id) and broadcast with torch.distributed (any backend)."""
+
+    def __init__(self, rank, world, device, broadcast):
+        """broadcast(bytes_or_None) -> bytes: rank 0 passes the id, every rank gets it back."""
+        idbuf = (C.c_ubyte * 128)()
+        if rank == 0:
+            A.check(A.lib().krylov_comm_unique_id(idbuf))
+            data = bytes(idbuf)
+        else:
+            data = None
+        data = broadcast(data)
+        idbuf = (C.c_ubyte * 128).from_buffer_copy(data)
+        ptr = C.c_void_p()
+        A.check(A.lib().krylov_comm_create(idbuf, int(rank), int(world), int(device), C.byref(ptr)))
+        self.ptr = ptr
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.ptr:
+            A.lib().krylov_comm_destroy(self.ptr)
+            self.ptr = None
+
+
+def torch_broadcast_id(data):
+    """Broadcast the 128-byte NCCL id from rank 0 over the default torch.distributed group."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if data is not None:
+        t.copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
+    dist.broadcast(t, src=0)
+    return bytes(t.cpu().numpy().tobytes())

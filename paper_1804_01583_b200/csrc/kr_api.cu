@@ -1,0 +1,802 @@
+// kr_api.cu — the C ABI of include/krylov_reach.h: validation, device memory, descriptor upload,
+// CUDA-graph capture of the hot path, results download. See the header for the contract.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <utility>
+
+#include "kr_internal.h"
+
+static thread_local std::string g_err;
+void kr_set_error(const std::string& m) { g_err = m; }
+
+kr_status kr_comm_unique_id_impl(void* id128);
+kr_comm* kr_comm_create_impl(const void* id128, int32_t rank, int32_t world, int32_t device);
+void kr_comm_destroy_impl(kr_comm* c);
+size_t kr_box_cex_bytes();
+int kr_lz_occupancy(int TX, int TY);
+void kr_lz_prepare(kr_handle* h);
+void kr_expm_prepare(kr_handle* h);
+void kr_ge_prepare();
+
+namespace {
+
+bool finite(double v) { return std::isfinite(v); }
+
+int64_t n_state(const kr_problem* p) { return p->op == KR_OP_STENCIL7 ? p->mx * p->my * p->mz : p->n; }
+
+void validate_vec(const kr_problem* p, const kr_vec& v, const char* what) {
+    const int64_t n = n_state(p);
+    if (v.kind == KR_VEC_SPARSE) {
+        if (v.nnz < 0 || (v.nnz > 0 && (!v.idx || !v.val))) KR_THROW(KR_EINVAL, std::string(what) + ": bad sparse vector");
+        for (int64_t e = 0; e < v.nnz; ++e) {
+            if (v.idx[e] < 0 || v.idx[e] >= n) KR_THROW(KR_EDIM, std::string(what) + ": index out of range");
+            if (!finite(v.val[e])) KR_THROW(KR_ENONFINITE, std::string(what) + ": non-finite value");
+        }
+    } else if (v.kind == KR_VEC_BOX || v.kind == KR_VEC_ALL) {
+        if (!finite(v.value)) KR_THROW(KR_ENONFINITE, std::string(what) + ": non-finite value");
+        if (v.kind == KR_VEC_BOX) {
+            const int axes = p->op == KR_OP_STENCIL7 ? 3 : 1;
+            const int64_t ext[3] = {p->op == KR_OP_STENCIL7 ? p->mx : p->n, p->my, p->mz};
+            for (int a = 0; a < axes; ++a)
+                if (v.lo[a] < 0 || v.hi[a] > ext[a] || v.lo[a] > v.hi[a])
+                    KR_THROW(KR_EDIM, std::string(what) + ": box out of range");
+        }
+    } else {
+        KR_THROW(KR_EINVAL, std::string(what) + ": bad vector kind");
+    }
+}
+
+bool vec_is_zero(const kr_problem* p, const kr_vec& v) {
+    if (v.kind == KR_VEC_SPARSE) {
+        for (int64_t e = 0; e < v.nnz; ++e)
+            if (v.val[e] != 0.0) return false;
+        return true;
+    }
+    if (v.value == 0.0) return true;
+    if (v.kind == KR_VEC_ALL) return n_state(p) == 0;
+    const int axes = p->op == KR_OP_STENCIL7 ? 3 : 1;
+    for (int a = 0; a < axes; ++a)
+        if (v.hi[a] <= v.lo[a]) return true;
+    return false;
+}
+
+bool csr_exactly_symmetric(const kr_problem* p) {
+    std::map<std::pair<int64_t, int64_t>, double> m;
+    for (int64_t r = 0; r < p->n; ++r)
+        for (int64_t e = p->row_ptr[r]; e < p->row_ptr[r + 1]; ++e) m[{r, p->col_idx[e]}] += p->val[e];
+    for (auto& kv : m) {
+        auto it = m.find({kv.first.second, kv.first.first});
+        const double o = it == m.end() ? 0.0 : it->second;
+        if (o != kv.second) return false;
+    }
+    return true;
+}
+
+// Gershgorin upper bound of lambda_max((A+A^T)/2) (Lemma 1's nu(B) = -mu(A), B = -A).
+double gershgorin_mu(const kr_problem* p) {
+    if (p->op == KR_OP_STENCIL7) {
+        const int64_t m[3] = {p->mx, p->my, p->mz};
+        double s = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            const double ih = (double)(m[a] + 1) * (double)(m[a] + 1);
+            s += (double)(std::min<int64_t>(2, m[a] - 1) - 2) * ih;
+        }
+        return p->alpha * s;
+    }
+    const int64_t n = p->n, N = n + (p->b ? 1 : 0);
+    std::vector<double> diag(N, 0.0), rad(N, 0.0);
+    std::vector<std::pair<std::pair<int64_t, int64_t>, double>> off;
+    off.reserve((size_t)p->nnz * 2 + (p->b ? 2 * n : 0));
+    for (int64_t r = 0; r < n; ++r) {
+        for (int64_t e = p->row_ptr[r]; e < p->row_ptr[r + 1]; ++e) {
+            const int64_t c = p->col_idx[e];
+            if (c == r)
+                diag[r] += p->val[e];
+            else {
+                off.push_back({{r, c}, 0.5 * p->val[e]});
+                off.push_back({{c, r}, 0.5 * p->val[e]});
+            }
+        }
+        if (p->b && p->b[r] != 0.0) {
+            off.push_back({{r, n}, 0.5 * p->b[r]});
+            off.push_back({{n, r}, 0.5 * p->b[r]});
+        }
+    }
+    std::sort(off.begin(), off.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (size_t i = 0; i < off.size();) {
+        size_t j = i;
+        double s = 0.0;
+        while (j < off.size() && off[j].first == off[i].first) s += off[j++].second;
+        rad[off[i].first.first] += std::fabs(s);
+        i = j;
+    }
+    double mu = -INFINITY;
+    for (int64_t r = 0; r < N; ++r) mu = std::max(mu, diag[r] + rad[r]);
+    return mu;
+}
+
+void* dalloc(kr_handle* h, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) KR_THROW(KR_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    h->extra_allocs.push_back(p);
+    return p;
+}
+
+void* carve(kr_handle* h, size_t bytes) {
+    const size_t off = (h->ws_used + 255) & ~size_t(255);
+    if (off + bytes > h->ws_bytes) KR_THROW(KR_ENOMEM, "workspace too small");
+    h->ws_used = off + bytes;
+    return h->ws + off;
+}
+
+template <class T>
+T* upload(kr_handle* h, const T* src, size_t count) {
+    T* d = reinterpret_cast<T*>(dalloc(h, count * sizeof(T)));
+    if (count) KR_CUDA(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+}
+
+// Sort + merge duplicate sparse entries on the host, upload; box/all copied as is.
+DVec make_dvec(kr_handle* h, const kr_vec& v) {
+    DVec d{};
+    d.kind = v.kind;
+    d.value = v.value;
+    for (int a = 0; a < 3; ++a) {
+        d.lo[a] = v.lo[a];
+        d.hi[a] = v.hi[a];
+    }
+    if (v.kind == KR_VEC_SPARSE) {
+        std::vector<std::pair<int64_t, double>> e((size_t)v.nnz);
+        for (int64_t i = 0; i < v.nnz; ++i) e[i] = {v.idx[i], v.val[i]};
+        std::stable_sort(e.begin(), e.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        std::vector<int64_t> idx;
+        std::vector<double> val;
+        for (size_t i = 0; i < e.size();) {
+            size_t j = i;
+            double s = 0.0;
+            while (j < e.size() && e[j].first == e[i].first) s += e[j++].second;
+            idx.push_back(e[i].first);
+            val.push_back(s);
+            i = j;
+        }
+        d.nnz = (int64_t)idx.size();
+        d.idx = upload(h, idx.data(), idx.size());
+        d.val = upload(h, val.data(), val.size());
+    }
+    return d;
+}
+
+struct Sizes {
+    int path, method;
+    int64_t N;
+    int ndl;
+    size_t state_bytes;
+};
+
+int resolve_method(const kr_problem* p) {
+    if (p->method == KR_ARNOLDI || p->method == KR_LANCZOS) return p->method;
+    if (p->op == KR_OP_STENCIL7) return KR_LANCZOS;
+    if (!p->b && csr_exactly_symmetric(p)) return KR_LANCZOS;
+    return KR_ARNOLDI;
+}
+
+int local_dirs(const kr_problem* p, int n_dir, int rank, int world) {
+    if (p->part != KR_PART_DIRS || world <= 1) return n_dir;
+    int c = 0;
+    for (int d = rank; d < n_dir; d += world) ++c;
+    return c;
+}
+
+void validate(const kr_problem* p) {
+    if (!p) KR_THROW(KR_EINVAL, "NULL problem");
+    if (p->op != KR_OP_STENCIL7 && p->op != KR_OP_CSR) KR_THROW(KR_EINVAL, "bad op");
+    if (p->op == KR_OP_STENCIL7) {
+        if (p->mx < 1 || p->my < 1 || p->mz < 1) KR_THROW(KR_EDIM, "stencil grid must be >= 1 per axis");
+        if (p->mx > (1 << 30) || p->my > (1 << 30) || p->mz > (1 << 30)) KR_THROW(KR_EDIM, "grid too large");
+        if (!finite(p->alpha)) KR_THROW(KR_ENONFINITE, "alpha");
+        if (p->b) KR_THROW(KR_EINVAL, "affine term b is supported for CSR only (lift explicitly)");
+    } else {
+        if (p->n < 1 || !p->row_ptr || (p->nnz > 0 && (!p->col_idx || !p->val))) KR_THROW(KR_EINVAL, "bad CSR");
+        if (p->row_ptr[0] != 0 || p->row_ptr[p->n] != p->nnz) KR_THROW(KR_EDIM, "row_ptr inconsistent with nnz");
+        for (int64_t r = 0; r < p->n; ++r)
+            if (p->row_ptr[r + 1] < p->row_ptr[r]) KR_THROW(KR_EDIM, "row_ptr not monotone");
+        for (int64_t e = 0; e < p->nnz; ++e) {
+            if (p->col_idx[e] < 0 || p->col_idx[e] >= p->n) KR_THROW(KR_EDIM, "col_idx out of range");
+            if (!finite(p->val[e])) KR_THROW(KR_ENONFINITE, "non-finite matrix value");
+        }
+        if (p->b)
+            for (int64_t r = 0; r < p->n; ++r)
+                if (!finite(p->b[r])) KR_THROW(KR_ENONFINITE, "non-finite b");
+    }
+    if (p->n_gen < 0 || (p->n_gen > 0 && (!p->gen || !p->z_lo || !p->z_hi))) KR_THROW(KR_EINVAL, "bad generators");
+    if (p->n_out < 1 || p->n_out > KR_MAX_OUT || !p->out) KR_THROW(KR_EINVAL, "n_out must be 1..64");
+    if (!(p->step > 0.0) || !finite(p->step)) KR_THROW(KR_EINVAL, "step must be > 0");
+    if (p->n_steps < 0) KR_THROW(KR_EINVAL, "n_steps must be >= 0");
+    if (p->k < 1 || p->k > 64) KR_THROW(KR_EINVAL, "k must be 1..64");
+    if (p->method < 0 || p->method > 2) KR_THROW(KR_EINVAL, "bad method");
+    if (p->part < 0 || p->part > 2) KR_THROW(KR_EINVAL, "bad partition");
+    for (int d = 0; d < p->n_gen; ++d) {
+        validate_vec(p, p->gen[d], "generator");
+        if (!finite(p->z_lo[d]) || !finite(p->z_hi[d])) KR_THROW(KR_ENONFINITE, "z bounds");
+        if (p->z_lo[d] > p->z_hi[d]) KR_THROW(KR_EINVAL, "z_lo > z_hi");
+        if (vec_is_zero(p, p->gen[d])) KR_THROW(KR_EZERO, "generator " + std::to_string(d) + " is zero");
+    }
+    if (p->center) validate_vec(p, *p->center, "center");
+    if (p->center && !p->b && vec_is_zero(p, *p->center)) KR_THROW(KR_EZERO, "center is zero (pass NULL)");
+    for (int r = 0; r < p->n_out; ++r) validate_vec(p, p->out[r], "output row");
+    const int n_dir = p->n_gen + ((p->center || p->b) ? 1 : 0);
+    if (n_dir < 1) KR_THROW(KR_EINVAL, "no directions");
+}
+
+Sizes plan(const kr_problem* p, int rank, int world) {
+    Sizes s{};
+    s.method = resolve_method(p);
+    if (s.method == KR_LANCZOS) {
+        if (p->b) KR_THROW(KR_ENOTSYM, "lifted affine system is not symmetric; use Arnoldi");
+        if (p->op == KR_OP_CSR && !csr_exactly_symmetric(p)) KR_THROW(KR_ENOTSYM, "CSR matrix is not symmetric");
+    }
+    s.N = p->op == KR_OP_STENCIL7 ? p->mx * p->my * p->mz : p->n + (p->b ? 1 : 0);
+    const int n_dir = p->n_gen + ((p->center || p->b) ? 1 : 0);
+    s.ndl = local_dirs(p, n_dir, rank, world);
+    s.path = (p->op == KR_OP_STENCIL7 && s.method == KR_LANCZOS) ? PATH_FUSED_LANCZOS : PATH_GENERIC;
+    if (s.path == PATH_GENERIC && (p->part == KR_PART_ZSLAB || p->virtual_slabs > 1))
+        KR_THROW(KR_EINVAL, "z-slab partition needs the stencil Lanczos path");
+    if (s.path == PATH_FUSED_LANCZOS) {
+        const int64_t pitch = (p->mx + 1) & ~int64_t(1);
+        int nsl = 1, W = 1, R = 0;
+        if (p->part == KR_PART_ZSLAB && world > 1) {
+            W = world;
+            R = rank;
+        } else if (p->virtual_slabs > 1) {
+            nsl = p->virtual_slabs;
+        }
+        size_t b = 0;
+        for (int s2 = 0; s2 < nsl; ++s2) {
+            int64_t z0, z1;
+            if (krylov_zslab_range(p->mz, nsl > 1 ? nsl : W, nsl > 1 ? s2 : R, &z0, &z1) != KR_OK)
+                KR_THROW(KR_EINVAL, "each slab needs >= 2 planes");
+            b += (size_t)3 * (size_t)(z1 - z0 + 3) * (size_t)p->my * (size_t)pitch * sizeof(double);
+        }
+        s.state_bytes = b;
+    } else {
+        if (s.N > 27648) KR_THROW(KR_EDIM, "the stored-basis (Arnoldi) path supports operator dimension <= 27648");
+        s.state_bytes = (size_t)s.ndl * (size_t)(p->k + 2) * (size_t)s.N * sizeof(double);
+    }
+    return s;
+}
+
+__global__ void reorder_dirs_kernel(const double* g, double* coeff, int64_t np1, int n_out, int n_dir, int world,
+                                    int ndl_max) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= np1 * n_out * n_dir) return;
+    const int d = (int)(e % n_dir);
+    const int64_t jr = e / n_dir;
+    const int w = d % world, dl = d / world;
+    coeff[e] = g[((int64_t)w * np1 * n_out + jr) * ndl_max + dl];
+}
+
+__global__ void pack_stats_kernel(const double* beta0, const double* hnext, const double* lemma, const int32_t* keff,
+                                  int ndl, double* out) {
+    const int d = threadIdx.x;
+    if (d < ndl) {
+        out[d * 4 + 0] = beta0[d];
+        out[d * 4 + 1] = hnext[d];
+        out[d * 4 + 2] = lemma[d];
+        out[d * 4 + 3] = (double)keff[d];
+    }
+}
+
+template <class F>
+kr_status guarded(F&& f) {
+    try {
+        f();
+        return KR_OK;
+    } catch (const KrError& e) {
+        kr_set_error(e.msg);
+        return e.st;
+    } catch (const std::exception& e) {
+        kr_set_error(e.what());
+        return KR_EINVAL;
+    }
+}
+
+void free_handle(kr_handle* h) {
+    if (!h) return;
+    if (h->graph_ready) cudaGraphExecDestroy(h->gexec);
+    for (auto e : h->ev) cudaEventDestroy(e);
+    if (h->ev_it0) cudaEventDestroy(h->ev_it0);
+    if (h->ev_it1) cudaEventDestroy(h->ev_it1);
+    for (void* p : h->extra_allocs) cudaFree(p);
+    if (h->own_ws && h->ws) cudaFree(h->ws);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* krylov_last_error(void) { return g_err.c_str(); }
+
+kr_status krylov_zslab_range(int64_t mz, int32_t world, int32_t rank, int64_t* z0, int64_t* z1) {
+    if (world < 1 || rank < 0 || rank >= world || mz < 1 || !z0 || !z1) {
+        kr_set_error("krylov_zslab_range: bad arguments");
+        return KR_EINVAL;
+    }
+    const int64_t base = mz / world, rem = mz % world;
+    const int64_t nz = base + (rank < rem ? 1 : 0);
+    *z0 = rank * base + std::min<int64_t>(rank, rem);
+    *z1 = *z0 + nz;
+    if (world > 1 && nz < 2) {
+        kr_set_error("krylov_zslab_range: each rank needs >= 2 planes");
+        return KR_EINVAL;
+    }
+    return KR_OK;
+}
+
+kr_status krylov_workspace_bytes(const kr_problem* p, size_t* bytes) {
+    return guarded([&] {
+        validate(p);
+        if (!bytes) KR_THROW(KR_EINVAL, "NULL bytes");
+        const int rank = p->comm ? p->comm->rank : 0, world = p->comm ? p->comm->world : 1;
+        *bytes = plan(p, rank, world).state_bytes;
+    });
+}
+
+kr_status krylov_comm_unique_id(void* id128) {
+    if (!id128) return KR_EINVAL;
+    return kr_comm_unique_id_impl(id128);
+}
+
+kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int32_t device, kr_comm** out) {
+    return guarded([&] {
+        if (!id128 || !out || world < 1 || rank < 0 || rank >= world) KR_THROW(KR_EINVAL, "bad comm arguments");
+        *out = kr_comm_create_impl(id128, rank, world, device);
+    });
+}
+
+void krylov_comm_destroy(kr_comm* c) { kr_comm_destroy_impl(c); }
+
+kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
+    kr_handle* h = nullptr;
+    kr_status st = guarded([&] {
+        if (!out) KR_THROW(KR_EINVAL, "NULL out");
+        *out = nullptr;
+        validate(p);
+        h = new kr_handle();
+        h->comm = p->comm;
+        h->rank = p->comm ? p->comm->rank : 0;
+        h->world = p->comm ? p->comm->world : 1;
+        if (p->comm && p->comm->device != p->device) KR_THROW(KR_EINVAL, "comm device != problem device");
+        if (p->virtual_slabs > 1 && h->world > 1) KR_THROW(KR_EINVAL, "virtual slabs need world == 1");
+        const Sizes sz = plan(p, h->rank, h->world);
+        h->op = p->op;
+        h->method = sz.method;
+        h->path = sz.path;
+        h->part = p->part;
+        h->mx = p->op == KR_OP_STENCIL7 ? p->mx : p->n;
+        h->my = p->op == KR_OP_STENCIL7 ? p->my : 1;
+        h->mz = p->op == KR_OP_STENCIL7 ? p->mz : 1;
+        h->pitch = (h->mx + 1) & ~int64_t(1);
+        h->alpha = p->alpha;
+        if (p->op == KR_OP_STENCIL7) {
+            h->cx = p->alpha * (double)(p->mx + 1) * (double)(p->mx + 1);
+            h->cy = p->alpha * (double)(p->my + 1) * (double)(p->my + 1);
+            h->cz = p->alpha * (double)(p->mz + 1) * (double)(p->mz + 1);
+        }
+        h->n = n_state(p);
+        h->N = sz.N;
+        h->lifted = p->b != nullptr;
+        h->n_gen = p->n_gen;
+        h->n_dir = p->n_gen + ((p->center || p->b) ? 1 : 0);
+        h->n_out = p->n_out;
+        h->k = p->k;
+        h->n_steps = p->n_steps;
+        h->step = p->step;
+        h->mu = gershgorin_mu(p);
+        h->device = p->device;
+        KR_CUDA(cudaSetDevice(p->device));
+        if (p->stream) {
+            h->stream = reinterpret_cast<cudaStream_t>(p->stream);
+        } else {
+            KR_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            h->own_stream = true;
+        }
+        for (int d = 0; d < h->n_dir; ++d)
+            if (p->part != KR_PART_DIRS || h->world <= 1 || d % h->world == h->rank) h->my_dirs.push_back(d);
+        const int ndl = (int)h->my_dirs.size();
+        // directions and box bounds
+        for (int d = 0; d < p->n_gen; ++d) {
+            h->dirs_h.push_back(make_dvec(h, p->gen[d]));
+            h->dir_lift1.push_back(0);
+            h->zlo.push_back(p->z_lo[d]);
+            h->zhi.push_back(p->z_hi[d]);
+        }
+        if (h->n_dir > p->n_gen) {
+            if (p->center) {
+                h->dirs_h.push_back(make_dvec(h, *p->center));
+            } else {
+                DVec z{};
+                z.kind = KR_VEC_ALL;
+                z.value = 0.0;
+                h->dirs_h.push_back(z);
+            }
+            h->dir_lift1.push_back(p->b ? 1 : 0);
+            h->zlo.push_back(1.0);
+            h->zhi.push_back(1.0);
+        }
+        for (int r = 0; r < p->n_out; ++r) h->outs_h.push_back(make_dvec(h, p->out[r]));
+        h->d_outs = upload(h, h->outs_h.data(), h->outs_h.size());
+        h->d_zlo = upload(h, h->zlo.data(), h->zlo.size());
+        h->d_zhi = upload(h, h->zhi.data(), h->zhi.size());
+        // workspace (state vectors)
+        if (p->workspace) {
+            if (p->workspace_bytes < sz.state_bytes) KR_THROW(KR_ENOMEM, "caller workspace too small");
+            h->ws = reinterpret_cast<char*>(p->workspace);
+            h->ws_bytes = p->workspace_bytes;
+        } else {
+            h->ws_bytes = sz.state_bytes + 256 * 8;
+            cudaError_t e = cudaMalloc(&h->ws, h->ws_bytes);
+            if (e != cudaSuccess) KR_THROW(KR_ENOMEM, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
+            h->own_ws = true;
+        }
+        const int k = h->k;
+        const int64_t np1 = h->n_steps + 1;
+        h->d_H = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * (k + 1) * k * 8));
+        h->d_P = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * h->n_out * k * 8));
+        h->d_beta0 = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 8));
+        h->d_hnext = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 8));
+        h->d_hmax = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 8));
+        h->d_lemma = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 8));
+        h->d_keff = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4));
+        h->d_done = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4));
+        h->d_status = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4 + 64));
+        KR_CUDA(cudaMemset(h->d_H, 0, (size_t)ndl * (k + 1) * k * 8));
+        KR_CUDA(cudaMemset(h->d_P, 0, (size_t)ndl * h->n_out * k * 8));
+        KR_CUDA(cudaMemset(h->d_hnext, 0, (size_t)ndl * 8));
+        KR_CUDA(cudaMemset(h->d_status, 0, (size_t)ndl * 4 + 64));
+        h->d_coeff = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * h->n_dir * 8));
+        if (p->part == KR_PART_DIRS && h->world > 1) {
+            const int ndl_max = (h->n_dir + h->world - 1) / h->world;
+            h->d_coeff_loc = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * ndl_max * 8 * h->world));
+            h->d_gather = reinterpret_cast<double*>(dalloc(h, (size_t)ndl_max * 4 * 8 * h->world));
+        } else {
+            h->d_coeff_loc = h->d_coeff;
+        }
+        h->d_hlast = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * np1 * 8));
+        h->d_box = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * (8 + 8 + 4) + 16));
+        h->d_cex = dalloc(h, 64 + (size_t)h->n_dir * 8);
+        if (h->path == PATH_FUSED_LANCZOS) {
+            // box-kind output rows are reduced inside the fused kernel, sparse rows gathered after it
+            std::vector<int32_t> slots;
+            for (int r = 0; r < h->n_out; ++r) {
+                const kr_vec& o = p->out[r];
+                if (o.kind == KR_VEC_SPARSE) continue;
+                BoxRow b{};
+                if (o.kind == KR_VEC_ALL) {
+                    b.lo[0] = b.lo[1] = b.lo[2] = 0;
+                    b.hi[0] = (int32_t)h->mx;
+                    b.hi[1] = (int32_t)h->my;
+                    b.hi[2] = (int32_t)h->mz;
+                } else {
+                    for (int a = 0; a < 3; ++a) {
+                        b.lo[a] = (int32_t)o.lo[a];
+                        b.hi[a] = (int32_t)o.hi[a];
+                    }
+                }
+                b.slot = r;
+                if (h->boxes.size() >= KR_MAX_BOX) KR_THROW(KR_EINVAL, "at most 8 box/all output rows on the stencil path");
+                h->boxes.push_back(b);
+                slots.push_back(r);
+            }
+            // the fused kernel accumulates sum(w) over the box; the row value multiplies in finalize:
+            // fold the value into the slot table by scaling in the reduce (value kept in outs_h)
+            h->d_box_slot = upload(h, slots.data(), slots.size());
+            std::vector<double> bvals;
+            for (int32_t r : slots) bvals.push_back(p->out[r].kind == KR_VEC_ALL || p->out[r].kind == KR_VEC_BOX ? p->out[r].value : 1.0);
+            h->d_box_val = upload(h, bvals.data(), bvals.size());
+            h->nq = 2 + h->n_out;
+            h->nqp = 2 + (int)h->boxes.size();
+            // tile choice: TX in {64, 32} by ragged waste, TY = 8
+            auto waste = [&](int64_t t) { return (double)(((h->mx + t - 1) / t) * t - h->mx) / (double)h->mx; };
+            h->TX = (waste(64) <= waste(32) + 0.02) ? 64 : 32;
+            h->TY = 8;
+            int nsl = 1, W = h->world, R = h->rank;
+            if (p->virtual_slabs > 1) {
+                nsl = p->virtual_slabs;
+                W = nsl;
+            }
+            if (p->part != KR_PART_ZSLAB && nsl == 1) {
+                W = 1;
+                R = 0;
+            }
+            const int occ = std::max(1, kr_lz_occupancy(h->TX, h->TY));
+            int dev_sms = 148;
+            KR_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
+            const char* env_zc = getenv("KR_ZCHUNK");
+            for (int s = 0; s < nsl; ++s) {
+                Slab sl{};
+                if (krylov_zslab_range(h->mz, W, nsl > 1 ? s : R, &sl.z0, &sl.z1) != KR_OK)
+                    KR_THROW(KR_EINVAL, "each slab needs >= 2 planes");
+                sl.nz = sl.z1 - sl.z0;
+                const size_t vb = (size_t)(sl.nz + 3) * h->my * h->pitch * sizeof(double);
+                for (int b = 0; b < 3; ++b) {
+                    sl.u[b] = reinterpret_cast<double*>(carve(h, vb));
+                    KR_CUDA(cudaMemset(sl.u[b], 0, vb));
+                }
+                const int64_t gx = (h->mx + h->TX - 1) / h->TX, gy = (h->my + h->TY - 1) / h->TY;
+                const int64_t slots_total = (int64_t)dev_sms * occ;
+                // z-chunking: enough CTAs for ~full waves; each chunk re-reads 3 halo planes
+                int best_zc = (int)sl.nz;
+                double best_cost = 1e300;
+                for (int nzc = 1; nzc <= 256 && nzc <= sl.nz; ++nzc) {
+                    const int64_t zc = (sl.nz + nzc - 1) / nzc;
+                    const int64_t nch = (sl.nz + zc - 1) / zc;
+                    const int64_t nb = gx * gy * nch;
+                    const double waves = (double)nb / (double)slots_total;
+                    const double eff = waves / std::ceil(waves);
+                    const double cost = (1.0 + 1.5 / (double)zc) / eff;
+                    if (cost < best_cost - 1e-9) {
+                        best_cost = cost;
+                        best_zc = (int)zc;
+                    }
+                }
+                if (env_zc) best_zc = std::max(1, atoi(env_zc));
+                sl.zchunk = best_zc;
+                const int64_t nch = (sl.nz + sl.zchunk - 1) / sl.zchunk;
+                sl.grid = dim3((unsigned)gx, (unsigned)gy, (unsigned)nch);
+                sl.nblk = gx * gy * nch;
+                sl.partials = reinterpret_cast<double*>(dalloc(h, (size_t)sl.nblk * h->nqp * 8));
+                h->slabs.push_back(sl);
+            }
+            kr_lz_encode_maps(h);
+            kr_lz_prepare(h);
+            const int R_total = (int)h->slabs.size() * h->world;
+            h->d_rankvec = reinterpret_cast<double*>(dalloc(h, (size_t)R_total * h->nq * 8));
+            h->d_sc = reinterpret_cast<LzScalars*>(dalloc(h, (size_t)ndl * sizeof(LzScalars)));
+            KR_CUDA(cudaMemset(h->d_sc, 0, (size_t)ndl * sizeof(LzScalars)));
+            int64_t nloc = 0;
+            for (auto& sl : h->slabs) nloc += sl.nz * h->mx * h->my;
+            h->step_bytes = 24.0 * (double)nloc;
+        } else {
+            if (p->op == KR_OP_CSR) {
+                h->d_rp = upload(h, p->row_ptr, (size_t)p->n + 1);
+                h->d_ci = upload(h, p->col_idx, (size_t)p->nnz);
+                h->d_val = upload(h, p->val, (size_t)p->nnz);
+                h->d_b = p->b ? upload(h, p->b, (size_t)p->n) : nullptr;
+            }
+            kr_ge_prepare();
+            h->d_V = reinterpret_cast<double*>(carve(h, (size_t)ndl * (k + 1) * h->N * 8));
+            h->d_W = reinterpret_cast<double*>(carve(h, (size_t)ndl * h->N * 8));
+            h->d_O = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * h->N * 8));
+            int64_t dummy = 0;
+            for (int r = 0; r < h->n_out; ++r)
+                kr_fill_dense(h->stream, h->d_O + (int64_t)r * h->N, h->N, h->n, h->mx, h->my,
+                              h->op == KR_OP_STENCIL7, h->outs_h[r], 0, 1.0, 0, &dummy);
+            KR_CUDA(cudaStreamSynchronize(h->stream));
+            // bytes per batched operator launch: A once + X and Y per direction (context only)
+            h->step_bytes = (h->op == KR_OP_CSR ? (double)p->nnz * 12.0 + (double)(p->n + 1) * 8.0 : 0.0) +
+                            16.0 * (double)h->N * ndl;
+        }
+        kr_expm_prepare(h);
+        h->d_sense = reinterpret_cast<int32_t*>(dalloc(h, (size_t)h->n_out * 4));
+        h->d_thr = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * 8));
+        h->timing = true;
+        h->ev.resize((size_t)2 * k);
+        for (auto& e : h->ev) KR_CUDA(cudaEventCreate(&e));
+        KR_CUDA(cudaEventCreate(&h->ev_it0));
+        KR_CUDA(cudaEventCreate(&h->ev_it1));
+        *out = h;
+    });
+    if (st != KR_OK) free_handle(h);
+    return st;
+}
+
+kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
+    return guarded([&] {
+        if (!h) KR_THROW(KR_EINVAL, "NULL handle");
+        KR_CUDA(cudaSetDevice(h->device));
+        const int ndl = (int)h->my_dirs.size();
+        const bool dirs_gather = h->part == KR_PART_DIRS && h->world > 1;
+        const int ndl_max = dirs_gather ? (h->n_dir + h->world - 1) / h->world : ndl;
+        const int64_t np1 = h->n_steps + 1;
+        auto enqueue = [&](bool ev) {
+            KR_CUDA(cudaEventRecord(h->ev_it0, h->stream));
+            if (h->path == PATH_FUSED_LANCZOS) {
+                for (int dl = 0; dl < ndl; ++dl) kr_lz_enqueue_direction(h, dl, ev);
+            } else {
+                kr_ge_enqueue_direction_set(h);
+            }
+            KR_CUDA(cudaEventRecord(h->ev_it1, h->stream));
+            kr_expm_enqueue(h);
+            if (dirs_gather) {
+                double* loc = h->d_coeff_loc + (size_t)h->rank * np1 * h->n_out * ndl_max;
+                // expm wrote rank-local slots at the start of d_coeff_loc; move into the rank's block
+                if (h->rank != 0)
+                    KR_CUDA(cudaMemcpyAsync(loc, h->d_coeff_loc, (size_t)np1 * h->n_out * ndl_max * 8,
+                                            cudaMemcpyDeviceToDevice, h->stream));
+                kr_nccl_allgather(h->comm, loc, h->d_coeff_loc, (size_t)np1 * h->n_out * ndl_max, h->stream);
+                const int64_t tot = np1 * h->n_out * h->n_dir;
+                reorder_dirs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(
+                    h->d_coeff_loc, h->d_coeff, np1, h->n_out, h->n_dir, h->world, ndl_max);
+                KR_CUDA(cudaGetLastError());
+                h->launches++;
+                pack_stats_kernel<<<1, 256, 0, h->stream>>>(h->d_beta0, h->d_hnext, h->d_lemma, h->d_keff, ndl,
+                                                             h->d_gather + (size_t)h->rank * ndl_max * 4);
+                KR_CUDA(cudaGetLastError());
+                h->launches++;
+                kr_nccl_allgather(h->comm, h->d_gather + (size_t)h->rank * ndl_max * 4, h->d_gather,
+                                  (size_t)ndl_max * 4, h->stream);
+            }
+        };
+        const bool use_graph = getenv("KR_NO_GRAPH") == nullptr;
+        if (use_graph && !h->graph_ready) {
+            const int64_t before = h->launches;
+            cudaGraph_t g;
+            KR_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue(h->timing);
+            } catch (...) {
+                cudaStreamEndCapture(h->stream, &g);
+                throw;
+            }
+            KR_CUDA(cudaStreamEndCapture(h->stream, &g));
+            KR_CUDA(cudaGraphInstantiate(&h->gexec, g, 0));
+            KR_CUDA(cudaGraphDestroy(g));
+            h->graph_launches = h->launches - before;
+            h->launches = before;
+            h->graph_ready = true;
+        }
+        if (use_graph) {
+            KR_CUDA(cudaGraphLaunch(h->gexec, h->stream));
+            h->launches += h->graph_launches;
+        } else {
+            enqueue(h->timing);
+        }
+        KR_CUDA(cudaStreamSynchronize(h->stream));
+        // device-side status (zero direction / non-finite)
+        int32_t worst = 0;
+        if (h->path == PATH_FUSED_LANCZOS) {
+            std::vector<LzScalars> sc(ndl);
+            KR_CUDA(cudaMemcpy(sc.data(), h->d_sc, ndl * sizeof(LzScalars), cudaMemcpyDeviceToHost));
+            for (auto& s : sc)
+                if (s.status) worst = s.status;
+        } else {
+            std::vector<int32_t> stv(ndl);
+            KR_CUDA(cudaMemcpy(stv.data(), h->d_status, ndl * 4, cudaMemcpyDeviceToHost));
+            for (auto s : stv)
+                if (s) worst = s;
+        }
+        if (worst) KR_THROW((kr_status)worst, worst == KR_EZERO ? "zero direction vector" : "non-finite value in iteration");
+        if (h->timing) {
+            float ms = 0.f;
+            KR_CUDA(cudaEventElapsedTime(&ms, h->ev_it0, h->ev_it1));
+            h->last_iter_ms = ms;
+            double tot = 0.0;
+            int64_t cnt = 0;
+            int keff0 = h->k;
+            if (ndl > 0) KR_CUDA(cudaMemcpy(&keff0, h->d_keff, 4, cudaMemcpyDeviceToHost));
+            for (int i = 0; i < h->k; ++i) {
+                float t = 0.f;
+                KR_CUDA(cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]));
+                if (i < std::max(1, keff0)) {
+                    tot += t;
+                    cnt++;
+                }
+            }
+            h->last_step_ms_mean = cnt ? tot / cnt : 0.0;
+            h->last_step_launches = cnt * (h->path == PATH_FUSED_LANCZOS ? (int64_t)h->slabs.size() : 1);
+        }
+        if (coeff)
+            KR_CUDA(cudaMemcpy(coeff, h->d_coeff, (size_t)np1 * h->n_out * h->n_dir * 8, cudaMemcpyDeviceToHost));
+        if (stats) {
+            if (dirs_gather) {
+                std::vector<double> g((size_t)ndl_max * 4 * h->world);
+                KR_CUDA(cudaMemcpy(g.data(), h->d_gather, g.size() * 8, cudaMemcpyDeviceToHost));
+                for (int d = 0; d < h->n_dir; ++d) {
+                    const int w = d % h->world, dl = d / h->world;
+                    const double* s = &g[((size_t)w * ndl_max + dl) * 4];
+                    stats[d].beta0 = s[0];
+                    stats[d].h_next = s[1];
+                    stats[d].lemma1_bound = s[2];
+                    stats[d].k_eff = (int32_t)s[3];
+                }
+            } else {
+                std::vector<double> b0(ndl), hn(ndl), lm(ndl);
+                std::vector<int32_t> ke(ndl);
+                KR_CUDA(cudaMemcpy(b0.data(), h->d_beta0, ndl * 8, cudaMemcpyDeviceToHost));
+                KR_CUDA(cudaMemcpy(hn.data(), h->d_hnext, ndl * 8, cudaMemcpyDeviceToHost));
+                KR_CUDA(cudaMemcpy(lm.data(), h->d_lemma, ndl * 8, cudaMemcpyDeviceToHost));
+                KR_CUDA(cudaMemcpy(ke.data(), h->d_keff, ndl * 4, cudaMemcpyDeviceToHost));
+                for (int dl = 0; dl < ndl; ++dl) {
+                    const int d = h->my_dirs[dl];
+                    stats[d].beta0 = b0[dl];
+                    stats[d].h_next = hn[dl];
+                    stats[d].lemma1_bound = lm[dl];
+                    stats[d].k_eff = ke[dl];
+                }
+            }
+        }
+        h->projected = true;
+    });
+}
+
+kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr, double* lo, double* hi,
+                           kr_cex* cex, double* z_witness) {
+    return guarded([&] {
+        if (!h || !sense || !thr || !cex) KR_THROW(KR_EINVAL, "NULL argument");
+        if (!h->projected) KR_THROW(KR_ESTATE, "krylov_check_box before krylov_project");
+        for (int r = 0; r < h->n_out; ++r) {
+            if (sense[r] < 0 || sense[r] > KR_NONE) KR_THROW(KR_EINVAL, "bad sense");
+            if (sense[r] != KR_NONE && !std::isfinite(thr[r])) KR_THROW(KR_ENONFINITE, "non-finite threshold");
+        }
+        KR_CUDA(cudaSetDevice(h->device));
+        const int64_t np1 = h->n_steps + 1;
+        const int64_t total = np1 * h->n_out;
+        int32_t* ds = h->d_sense;
+        double* dt = h->d_thr;
+        KR_CUDA(cudaMemcpyAsync(ds, sense, (size_t)h->n_out * 4, cudaMemcpyHostToDevice, h->stream));
+        KR_CUDA(cudaMemcpyAsync(dt, thr, (size_t)h->n_out * 8, cudaMemcpyHostToDevice, h->stream));
+        kr_box_enqueue(h, ds, dt);
+        if (lo) KR_CUDA(cudaMemcpyAsync(lo, h->d_box, total * 8, cudaMemcpyDeviceToHost, h->stream));
+        if (hi) KR_CUDA(cudaMemcpyAsync(hi, h->d_box + total, total * 8, cudaMemcpyDeviceToHost, h->stream));
+        struct {
+            int32_t found;
+            int64_t step;
+            int32_t row;
+            double y;
+        } dc;
+        static_assert(sizeof(dc) <= 64, "cex");
+        KR_CUDA(cudaMemcpyAsync(&dc, h->d_cex, sizeof(dc), cudaMemcpyDeviceToHost, h->stream));
+        std::vector<double> zw(h->n_dir);
+        KR_CUDA(cudaMemcpyAsync(zw.data(), reinterpret_cast<char*>(h->d_cex) + 64, (size_t)h->n_dir * 8,
+                                cudaMemcpyDeviceToHost, h->stream));
+        KR_CUDA(cudaStreamSynchronize(h->stream));
+        cex->found = dc.found;
+        cex->step = dc.step;
+        cex->row = dc.row;
+        cex->y = dc.y;
+        cex->time = dc.found ? (double)dc.step * h->step : 0.0;
+        if (z_witness)
+            for (int d = 0; d < h->n_dir; ++d) z_witness[d] = zw[d];
+    });
+}
+
+void krylov_reach_destroy(kr_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    free_handle(h);
+}
+
+kr_status krylov_krylov_data(const kr_handle* h, int32_t dir, double* H, double* P) {
+    return guarded([&] {
+        if (!h) KR_THROW(KR_EINVAL, "NULL handle");
+        if (!h->projected) KR_THROW(KR_ESTATE, "krylov_krylov_data before krylov_project");
+        int dl = -1;
+        for (size_t i = 0; i < h->my_dirs.size(); ++i)
+            if (h->my_dirs[i] == dir) dl = (int)i;
+        if (dl < 0) KR_THROW(KR_EDIM, "direction not handled by this rank");
+        const int k = h->k;
+        if (H) KR_CUDA(cudaMemcpy(H, h->d_H + (size_t)dl * (k + 1) * k, (size_t)(k + 1) * k * 8, cudaMemcpyDeviceToHost));
+        if (P) KR_CUDA(cudaMemcpy(P, h->d_P + (size_t)dl * h->n_out * k, (size_t)h->n_out * k * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int64_t krylov_launch_count(const kr_handle* h) { return h ? h->launches : 0; }
+
+kr_status krylov_last_timing(const kr_handle* h, double* iter_ms, double* step_kernel_ms_mean,
+                             int64_t* step_kernel_launches, double* step_kernel_bytes) {
+    if (!h) return KR_EINVAL;
+    if (iter_ms) *iter_ms = h->last_iter_ms;
+    if (step_kernel_ms_mean) *step_kernel_ms_mean = h->last_step_ms_mean;
+    if (step_kernel_launches) *step_kernel_launches = h->last_step_launches;
+    if (step_kernel_bytes) *step_kernel_bytes = h->step_bytes;
+    return KR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,286 @@
+// kr_expm.cu — batched small-matrix exponentials and the basis-matrix projection (Eq. 2,
+// PAPER.md:651-655; projected form of Alg. 4):
+//     x_{d,j} = e^{H_d t_j} e_1,   c[j][r][d] = ||v_d|| * sum_l P_d[r][l] x_{d,j}[l],   t_j = j*step.
+// One CTA per (time step j, direction d): scaling and squaring with the degree-13 diagonal Pade
+// approximant (Higham 2005 coefficients, theta_13 = 5.3719; the paper defers to "squaring and scaling
+// and Pade"), matrices held in shared memory (k <= 64), 16x16 threads with 4x4
+// register micro-tiles per matmul, LU with partial pivoting for the Pade solve. j = 0 is exactly e_1
+// (e^0 = I). Also records h(t_j) = e_k^T e^{H t_j} e_1 for the Lemma 1 diagnostic
+// and integrates it (trapezoid on the t_j grid).
+#include <math.h>
+
+#include "kr_internal.h"
+
+namespace {
+
+constexpr int ET = 256;
+
+// C = A * B (n x n, leading dimension ld); caller synchronises before and after.
+__device__ __forceinline__ void mm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                                   int n, int ld) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int l = 0; l < n; ++l) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int i = ty + 16 * a;
+            av[a] = i < n ? A[i * ld + l] : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = tx + 16 * b;
+            bv[b] = j < n ? B[l * ld + j] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int i = ty + 16 * a, j = tx + 16 * b;
+            if (i < n && j < n) C[i * ld + j] = acc[a][b];
+        }
+}
+
+struct ExpmArgs {
+    const double* H;     // [ndl][k+1][k]
+    const double* P;     // [ndl][n_out][k]
+    const double* beta0; // [ndl]
+    const int32_t* keff; // [ndl]
+    int k, n_out, ndl_stride;
+    int64_t n_steps;
+    double step;
+    double* coeff;       // [(n_steps+1)][n_out][ndl_stride]
+    double* hlast;       // [ndl][n_steps+1]
+};
+
+__global__ void __launch_bounds__(ET) expm_project_kernel(ExpmArgs a) {
+    const int64_t j = blockIdx.x;
+    const int d = blockIdx.y;
+    const int n = a.keff[d];
+    const int k = a.k;
+    extern __shared__ double sm[];
+    __shared__ double xs[64];
+    __shared__ double fac[64];
+    __shared__ int piv_s;
+    __shared__ int sq_s;
+    if (n <= 0) {
+        for (int r = threadIdx.x; r < a.n_out; r += ET) a.coeff[(j * a.n_out + r) * a.ndl_stride + d] = 0.0;
+        return;
+    }
+    const int ld = n + 1;
+    const int msz = n * ld;
+    double* B0 = sm;
+    double* B1 = B0 + msz;
+    double* B2 = B1 + msz;
+    double* B3 = B2 + msz;
+    double* B4 = B3 + msz;
+    double* B5 = B4 + msz;
+    if (j == 0) {
+        for (int i = threadIdx.x; i < n; i += ET) xs[i] = i == 0 ? 1.0 : 0.0;  // e^{H 0} e_1 = e_1 exactly
+    } else {
+        const double t = (double)j * a.step;
+        const double* Hd = a.H + (int64_t)d * (k + 1) * k;
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int r = e / n, c = e - r * n;
+            B0[r * ld + c] = Hd[r * k + c] * t;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // 1-norm (max column sum) -> number of squarings
+            double cmax = 0.0;
+            for (int c = threadIdx.x; c < n; c += 32) {
+                double s = 0.0;
+                for (int r = 0; r < n; ++r) s += fabs(B0[r * ld + c]);
+                cmax = fmax(cmax, s);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cmax = fmax(cmax, __shfl_down_sync(0xffffffffu, cmax, o));
+            if (threadIdx.x == 0) {
+                const double theta13 = 5.371920351148152;
+                int s = 0;
+                if (cmax > theta13) s = (int)ceil(log2(cmax / theta13));
+                while (ldexp(cmax, -s) > theta13) ++s;
+                sq_s = s < 0 ? 0 : s;
+            }
+        }
+        __syncthreads();
+        const int s = sq_s;
+        if (s > 0)
+            for (int e = threadIdx.x; e < n * n; e += ET) {
+                const int r = e / n, c = e - r * n;
+                B0[r * ld + c] = ldexp(B0[r * ld + c], -s);
+            }
+        __syncthreads();
+        const double b0 = 64764752532480000.0, b1 = 32382376266240000.0, b2 = 7771770303897600.0,
+                     b3 = 1187353796428800.0, b4 = 129060195264000.0, b5 = 10559470521600.0, b6 = 670442572800.0,
+                     b7 = 33522128640.0, b8 = 1323241920.0, b9 = 40840800.0, b10 = 960960.0, b11 = 16380.0,
+                     b12 = 182.0, b13 = 1.0;
+        mm(B0, B0, B1, n, ld);  // A2
+        __syncthreads();
+        mm(B1, B1, B2, n, ld);  // A4
+        __syncthreads();
+        mm(B2, B1, B3, n, ld);  // A6
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int o = (e / n) * ld + e % n;
+            B4[o] = b13 * B3[o] + b11 * B2[o] + b9 * B1[o];
+        }
+        __syncthreads();
+        mm(B3, B4, B5, n, ld);  // A6 (b13 A6 + b11 A4 + b9 A2)
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int r = e / n, c = e - r * n, o = r * ld + c;
+            B5[o] = B5[o] + b7 * B3[o] + b5 * B2[o] + b3 * B1[o] + (r == c ? b1 : 0.0);
+        }
+        __syncthreads();
+        mm(B0, B5, B4, n, ld);  // U = A * (...)
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int o = (e / n) * ld + e % n;
+            B5[o] = b12 * B3[o] + b10 * B2[o] + b8 * B1[o];
+        }
+        __syncthreads();
+        mm(B3, B5, B0, n, ld);  // A6 (b12 A6 + b10 A4 + b8 A2)  (A no longer needed)
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int r = e / n, c = e - r * n, o = r * ld + c;
+            const double V = B0[o] + b6 * B3[o] + b4 * B2[o] + b2 * B1[o] + (r == c ? b0 : 0.0);
+            const double U = B4[o];
+            B1[o] = V + U;  // P
+            B2[o] = V - U;  // Q
+        }
+        __syncthreads();
+        // solve Q F = P: LU with partial pivoting (lowest index wins ties), F overwrites P
+        double* Q = B2;
+        double* F = B1;
+        for (int c = 0; c < n; ++c) {
+            if (threadIdx.x < 32) {
+                double best = -1.0;
+                int bi = c;
+                for (int i = c + threadIdx.x; i < n; i += 32) {
+                    const double v = fabs(Q[i * ld + c]);
+                    if (v > best) {
+                        best = v;
+                        bi = i;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ob = __shfl_down_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                    if (ob > best || (ob == best && oi < bi)) {
+                        best = ob;
+                        bi = oi;
+                    }
+                }
+                if (threadIdx.x == 0) piv_s = bi;
+            }
+            __syncthreads();
+            const int p = piv_s;
+            if (p != c)
+                for (int col = threadIdx.x; col < n; col += ET) {
+                    double t0 = Q[c * ld + col];
+                    Q[c * ld + col] = Q[p * ld + col];
+                    Q[p * ld + col] = t0;
+                    t0 = F[c * ld + col];
+                    F[c * ld + col] = F[p * ld + col];
+                    F[p * ld + col] = t0;
+                }
+            __syncthreads();
+            for (int i = c + 1 + threadIdx.x; i < n; i += ET) fac[i] = Q[i * ld + c] / Q[c * ld + c];
+            __syncthreads();
+            const int rows = n - c - 1;
+            for (int e = threadIdx.x; e < rows * n; e += ET) {
+                const int i = c + 1 + e / n, col = e % n;
+                const double f = fac[i];
+                F[i * ld + col] -= f * F[c * ld + col];
+                if (col > c) Q[i * ld + col] -= f * Q[c * ld + col];
+            }
+            __syncthreads();
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            for (int col = threadIdx.x; col < n; col += ET) {
+                double t0 = F[i * ld + col];
+                for (int l = i + 1; l < n; ++l) t0 -= Q[i * ld + l] * F[l * ld + col];
+                F[i * ld + col] = t0 / Q[i * ld + i];
+            }
+            __syncthreads();
+        }
+        // square s times
+        double* X = F;
+        double* Y = B3;
+        for (int r = 0; r < s; ++r) {
+            mm(X, X, Y, n, ld);
+            __syncthreads();
+            double* t0 = X;
+            X = Y;
+            Y = t0;
+        }
+        for (int i = threadIdx.x; i < n; i += ET) xs[i] = X[i * ld + 0];
+    }
+    __syncthreads();
+    const double* Pd = a.P + (int64_t)d * a.n_out * k;
+    const double bz = a.beta0[d];
+    for (int r = threadIdx.x; r < a.n_out; r += ET) {
+        double s = 0.0;
+        for (int l = 0; l < n; ++l) s = fma(Pd[(int64_t)r * k + l], xs[l], s);
+        a.coeff[(j * a.n_out + r) * a.ndl_stride + d] = bz * s;
+    }
+    if (threadIdx.x == 0) a.hlast[(int64_t)d * (a.n_steps + 1) + j] = xs[n - 1];
+}
+
+__global__ void lemma_kernel(const double* hlast, const double* beta0, const double* hnext, const int32_t* keff,
+                             int64_t n_steps, double step, double mu, int ndl, double* lemma) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= ndl) return;
+    if (keff[d] <= 0) {
+        lemma[d] = 0.0;
+        return;
+    }
+    const double* h = hlast + (int64_t)d * (n_steps + 1);
+    double integral = 0.0;
+    for (int64_t j = 0; j < n_steps; ++j) integral += 0.5 * step * (fabs(h[j]) + fabs(h[j + 1]));
+    const double T = (double)n_steps * step;
+    lemma[d] = beta0[d] * hnext[d] * exp(fmax(mu, 0.0) * T) * integral;
+}
+
+}  // namespace
+
+void kr_expm_prepare(kr_handle* h) {
+    const size_t smem = (size_t)6 * h->k * (h->k + 1) * sizeof(double);
+    KR_CUDA(cudaFuncSetAttribute(expm_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+void kr_expm_enqueue(kr_handle* h) {
+    const int ndl = (int)h->my_dirs.size();
+    if (ndl == 0) return;
+    const int k = h->k;
+    const size_t smem = (size_t)6 * k * (k + 1) * sizeof(double);
+    ExpmArgs a;
+    a.H = h->d_H;
+    a.P = h->d_P;
+    a.beta0 = h->d_beta0;
+    a.keff = h->d_keff;
+    a.k = k;
+    a.n_out = h->n_out;
+    a.ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
+    a.n_steps = h->n_steps;
+    a.step = h->step;
+    a.coeff = h->d_coeff_loc;
+    a.hlast = h->d_hlast;
+    expm_project_kernel<<<dim3((unsigned)(h->n_steps + 1), ndl), ET, smem, h->stream>>>(a);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    lemma_kernel<<<(ndl + 63) / 64, 64, 0, h->stream>>>(h->d_hlast, h->d_beta0, h->d_hnext, h->d_keff, h->n_steps,
+                                                        h->step, h->mu, ndl, h->d_lemma);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+}

@@ -1,0 +1,390 @@
+// kr_generic.cu — direction-batched Krylov iteration with a stored basis V (Arnoldi, Alg. 1,
+// PAPER.md:617-635; or Lanczos, Alg. 3) for the CSR operator (optionally lifted,
+// PAPER.md:157-165) and for small stencil problems; plus the vector fill kernels.
+//
+// Per Krylov step j, two launches for ALL directions of this rank:
+//  1. the operator: W[d] = A V[d][j-1] — one CSR SpMM that streams A once for every direction
+//     (thread per (row, direction)), or the matrix-free stencil;
+//  2. orthogonalisation, one CTA (1024 threads) per direction: the new vector is held in registers
+//     (EPT elements per thread), each previous basis vector is read ONCE per MGS iteration (dot, fixed
+//     order block reduction, axpy from the same registers), then ||w||, breakdown, V[d][j] = w/||w||
+//     and P[d][:, j] = C V[d][j] (Alg. 4's projection).
+#include <float.h>
+
+#include "kr_internal.h"
+
+// ------------------------------------------------------------------------------------------------
+// fills
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ double box_value(const DVec& v, int64_t x, int64_t y, int64_t z) {
+    if (v.kind == KR_VEC_ALL) return v.value;
+    if (v.kind == KR_VEC_BOX)
+        return (x >= v.lo[0] && x < v.hi[0] && y >= v.lo[1] && y < v.hi[1] && z >= v.lo[2] && z < v.hi[2]) ? v.value
+                                                                                                           : 0.0;
+    return 0.0;
+}
+
+__global__ void fill_grid_kernel(double* dst, int64_t mx, int64_t my, int64_t pitch, int64_t nplanes, int64_t zbase,
+                                 int64_t mz, DVec v) {
+    const int64_t total = nplanes * my * pitch;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / (my * pitch), rem = e - b * my * pitch;
+        const int64_t y = rem / pitch, x = rem - y * pitch;
+        const int64_t gz = zbase + b;
+        double val = 0.0;
+        if (x < mx && gz >= 0 && gz < mz) val = box_value(v, x, y, gz);
+        dst[e] = val;
+    }
+}
+
+__global__ void scatter_grid_kernel(double* dst, int64_t mx, int64_t my, int64_t pitch, int64_t nplanes, int64_t zbase,
+                                    DVec v) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < v.nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t idx = v.idx[e];
+        const int64_t z = idx / (mx * my), rem = idx - z * mx * my;
+        const int64_t y = rem / mx, x = rem - y * mx;
+        const int64_t b = z - zbase;
+        if (b >= 0 && b < nplanes) dst[(b * my + y) * pitch + x] = v.val[e];  // host merged duplicates
+    }
+}
+
+void kr_fill_grid(cudaStream_t s, double* dst, int64_t mx, int64_t my, int64_t pitch, int64_t nplanes, int64_t zbase,
+                  int64_t mz, const DVec& v, int64_t* launches) {
+    const int64_t total = nplanes * my * pitch;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    fill_grid_kernel<<<blocks, 256, 0, s>>>(dst, mx, my, pitch, nplanes, zbase, mz, v);
+    KR_CUDA(cudaGetLastError());
+    (*launches)++;
+    if (v.kind == KR_VEC_SPARSE && v.nnz > 0) {
+        int b2 = (int)std::min<int64_t>((v.nnz + 255) / 256, 148 * 8);
+        scatter_grid_kernel<<<b2, 256, 0, s>>>(dst, mx, my, pitch, nplanes, zbase, v);
+        KR_CUDA(cudaGetLastError());
+        (*launches)++;
+    }
+}
+
+__global__ void fill_dense_kernel(double* dst, int64_t N, int64_t n, int64_t mx, int64_t my, int stencil, DVec v,
+                                  int lift1) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N; c += (int64_t)gridDim.x * blockDim.x) {
+        double val = 0.0;
+        if (c < n) {
+            if (stencil) {
+                const int64_t z = c / (mx * my), rem = c - z * mx * my;
+                const int64_t y = rem / mx, x = rem - y * mx;
+                val = box_value(v, x, y, z);
+            } else {
+                if (v.kind == KR_VEC_ALL) val = v.value;
+                if (v.kind == KR_VEC_BOX) val = (c >= v.lo[0] && c < v.hi[0]) ? v.value : 0.0;
+            }
+        } else {
+            val = lift1 ? 1.0 : 0.0;
+        }
+        dst[c] = val;
+    }
+}
+
+__global__ void scatter_dense_kernel(double* dst, DVec v) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < v.nnz; e += (int64_t)gridDim.x * blockDim.x)
+        dst[v.idx[e]] = v.val[e];
+}
+
+void kr_fill_dense(cudaStream_t s, double* dst, int64_t N, int64_t n, int64_t mx, int64_t my, bool stencil,
+                   const DVec& v, int lift1, double, int, int64_t* launches) {
+    int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 16);
+    fill_dense_kernel<<<blocks, 256, 0, s>>>(dst, N, n, mx, my, stencil ? 1 : 0, v, lift1);
+    KR_CUDA(cudaGetLastError());
+    (*launches)++;
+    if (v.kind == KR_VEC_SPARSE && v.nnz > 0) {
+        int b2 = (int)std::min<int64_t>((v.nnz + 255) / 256, 148 * 8);
+        scatter_dense_kernel<<<b2, 256, 0, s>>>(dst, v);
+        KR_CUDA(cudaGetLastError());
+        (*launches)++;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// operators, batched over directions: Y[d] = A X[d]  (X, Y with a per-direction stride)
+// ------------------------------------------------------------------------------------------------
+__global__ void spmm_csr_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const double* __restrict__ val, const double* __restrict__ b, int64_t n, int64_t N,
+                                const double* __restrict__ X, int64_t xstride, double* __restrict__ Y,
+                                int64_t ystride, int ndl, const int32_t* __restrict__ done) {
+    const int d = blockIdx.y;
+    if (done[d]) return;
+    const double* x = X + (int64_t)d * xstride;
+    double* y = Y + (int64_t)d * ystride;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        if (r < n) {
+            const int64_t e1 = rp[r + 1];
+            for (int64_t e = rp[r]; e < e1; ++e) s = fma(val[e], __ldg(&x[ci[e]]), s);
+            if (b) s = fma(b[r], x[n], s);
+        }
+        y[r] = s;
+    }
+}
+
+__global__ void stencil_apply_kernel(int64_t mx, int64_t my, int64_t mz, double cx, double cy, double cz,
+                                     const double* __restrict__ X, int64_t xstride, double* __restrict__ Y,
+                                     int64_t ystride, const int32_t* __restrict__ done) {
+    const int d = blockIdx.y;
+    if (done[d]) return;
+    const double* u = X + (int64_t)d * xstride;
+    double* y = Y + (int64_t)d * ystride;
+    const int64_t n = mx * my * mz;
+    const double diag = 2.0 * (cx + cy + cz);
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = c / (mx * my), rem = c - z * mx * my;
+        const int64_t yy = rem / mx, x = rem - yy * mx;
+        const double sx = (x > 0 ? u[c - 1] : 0.0) + (x < mx - 1 ? u[c + 1] : 0.0);
+        const double sy = (yy > 0 ? u[c - mx] : 0.0) + (yy < my - 1 ? u[c + mx] : 0.0);
+        const double sz = (z > 0 ? u[c - mx * my] : 0.0) + (z < mz - 1 ? u[c + mx * my] : 0.0);
+        y[c] = cx * sx + cy * sy + cz * sz - diag * u[c];
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// orthogonalisation (one CTA of 1024 threads per direction)
+// ------------------------------------------------------------------------------------------------
+constexpr int OT = 1024;
+
+__device__ __forceinline__ double block_sum_1024(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        v = red[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) red[32] = v;
+    }
+    __syncthreads();
+    const double r = red[32];
+    __syncthreads();
+    return r;
+}
+
+struct OrthoArgs {
+    double* V;        // [ndl][k+1][N]
+    const double* W;  // [ndl][N]  (A v_{j-1}); for j == 0 unused
+    int64_t N;
+    int k, j;         // producing basis vector index j (0 = init: normalise the start vector)
+    int lanczos;
+    double* H;        // [ndl][k+1][k]
+    double* P;        // [ndl][n_out][k]
+    const double* O;  // [n_out][N]
+    int n_out;
+    double* beta0;
+    double* hnext;
+    double* hmax;
+    int32_t* keff;
+    int32_t* done;
+    int32_t* status;
+};
+
+// SW: keep w in shared memory (large N; registers would spill at 1024 threads x 64 registers).
+template <int EPT, bool SW>
+__global__ void __launch_bounds__(OT) ortho_kernel(OrthoArgs a) {
+    const int d = blockIdx.x;
+    if (a.done[d]) return;
+    __shared__ double red[33];
+    extern __shared__ double wsm[];
+    const int64_t N = a.N;
+    const int k = a.k, j = a.j;
+    double* V = a.V + (int64_t)d * (k + 1) * N;
+    double* H = a.H + (int64_t)d * (k + 1) * k;
+    double wr[SW ? 1 : EPT];
+#define WV(e) (SW ? wsm[threadIdx.x + (e) * OT] : wr[SW ? 0 : (e)])
+    const double* src = (j == 0) ? V : a.W + (int64_t)d * N;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        const int64_t c = threadIdx.x + (int64_t)e * OT;
+        WV(e) = c < N ? src[c] : 0.0;
+    }
+    double hm = (j == 0) ? 0.0 : a.hmax[d];
+    if (j > 0) {
+        int l0 = 0;
+        if (a.lanczos) {
+            // Alg. 3: w -= H_{j-1,j} V_{j-2} with H_{j-1,j} = H_{j,j-1} (known), then one dot for alpha
+            if (j >= 2) {
+                const double bprev = H[(int64_t)(j - 1) * k + (j - 2)];
+                const double* Vl = V + (int64_t)(j - 2) * N;
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) {
+                    const int64_t c = threadIdx.x + (int64_t)e * OT;
+                    if (c < N) WV(e) = WV(e) - bprev * Vl[c];
+                }
+                if (threadIdx.x == 0) H[(int64_t)(j - 2) * k + (j - 1)] = bprev;
+            }
+            l0 = j - 1;
+        }
+        for (int l = l0; l <= j - 1; ++l) {  // MGS, the printed inner loop read as 1..i-1
+            const double* Vl = V + (int64_t)l * N;
+            double vl[EPT];
+            double s = 0.0;
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {
+                const int64_t c = threadIdx.x + (int64_t)e * OT;
+                vl[e] = c < N ? Vl[c] : 0.0;
+                s = fma(vl[e], WV(e), s);
+            }
+            const double h = block_sum_1024(s, red);
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) WV(e) = WV(e) - h * vl[e];
+            if (threadIdx.x == 0) H[(int64_t)l * k + (j - 1)] = h;
+            hm = fmax(hm, fabs(h));
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) s = fma(WV(e), WV(e), s);
+    const double nb = sqrt(block_sum_1024(s, red));
+    if (j == 0) {
+        if (threadIdx.x == 0) {
+            a.beta0[d] = nb;
+            a.keff[d] = 1;
+            a.hmax[d] = 0.0;
+            if (!(nb > 0.0) || !isfinite(nb)) {
+                a.done[d] = 1;
+                a.keff[d] = 0;
+                a.status[d] = nb == 0.0 ? KR_EZERO : KR_ENONFINITE;
+            }
+        }
+        if (!(nb > 0.0) || !isfinite(nb)) return;
+    } else {
+        if (threadIdx.x == 0) H[(int64_t)j * k + (j - 1)] = nb;
+        if (!isfinite(nb)) {
+            if (threadIdx.x == 0) {
+                a.done[d] = 1;
+                a.status[d] = KR_ENONFINITE;
+            }
+            return;
+        }
+        if (nb == 0.0 || nb <= 16.0 * DBL_EPSILON * hm || j == k) {  // breakdown or extra column
+            if (threadIdx.x == 0) {
+                a.done[d] = 1;
+                a.keff[d] = j;
+                a.hnext[d] = nb;
+            }
+            return;
+        }
+        hm = fmax(hm, nb);
+        if (threadIdx.x == 0) {
+            a.hmax[d] = hm;
+            a.keff[d] = j + 1;
+        }
+    }
+    double* Vj = V + (int64_t)j * N;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        const int64_t c = threadIdx.x + (int64_t)e * OT;
+        WV(e) = WV(e) / nb;
+        if (c < N) Vj[c] = WV(e);
+    }
+    // P_{., j} = C V_{*, j}
+    for (int r = 0; r < a.n_out; ++r) {
+        const double* Or = a.O + (int64_t)r * N;
+        double t = 0.0;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int64_t c = threadIdx.x + (int64_t)e * OT;
+            if (c < N) t = fma(Or[c], WV(e), t);
+        }
+        const double pr = block_sum_1024(t, red);
+        if (threadIdx.x == 0) a.P[((int64_t)d * a.n_out + r) * k + j] = pr;
+    }
+#undef WV
+}
+
+static void launch_ortho(kr_handle* h, int j, int ndl) {
+    OrthoArgs a;
+    a.V = h->d_V;
+    a.W = h->d_W;
+    a.N = h->N;
+    a.k = h->k;
+    a.j = j;
+    a.lanczos = h->method == KR_LANCZOS ? 1 : 0;
+    a.H = h->d_H;
+    a.P = h->d_P;
+    a.O = h->d_O;
+    a.n_out = h->n_out;
+    a.beta0 = h->d_beta0;
+    a.hnext = h->d_hnext;
+    a.hmax = h->d_hmax;
+    a.keff = h->d_keff;
+    a.done = h->d_done;
+    a.status = h->d_status;
+    const int64_t ept = (h->N + OT - 1) / OT;
+    const size_t sm = (size_t)ept * OT * sizeof(double);
+    if (ept <= 1)
+        ortho_kernel<1, false><<<ndl, OT, 0, h->stream>>>(a);
+    else if (ept <= 2)
+        ortho_kernel<2, false><<<ndl, OT, 0, h->stream>>>(a);
+    else if (ept <= 4)
+        ortho_kernel<4, false><<<ndl, OT, 0, h->stream>>>(a);
+    else if (ept <= 8)
+        ortho_kernel<8, false><<<ndl, OT, 0, h->stream>>>(a);
+    else if (ept <= 12)
+        ortho_kernel<12, true><<<ndl, OT, 12 * OT * 8, h->stream>>>(a);
+    else if (ept <= 16)
+        ortho_kernel<16, true><<<ndl, OT, 16 * OT * 8, h->stream>>>(a);
+    else if (ept <= 20)
+        ortho_kernel<20, true><<<ndl, OT, 20 * OT * 8, h->stream>>>(a);
+    else if (ept <= 24)
+        ortho_kernel<24, true><<<ndl, OT, 24 * OT * 8, h->stream>>>(a);
+    else if (ept <= 27)
+        ortho_kernel<27, true><<<ndl, OT, 27 * OT * 8, h->stream>>>(a);
+    else
+        KR_THROW(KR_EDIM, "stored-basis Krylov path supports operator dimension <= 27648");
+    (void)sm;
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+}
+
+__global__ void ge_reset(int32_t* done, int32_t* status, int ndl) {
+    for (int d = threadIdx.x; d < ndl; d += blockDim.x) {
+        done[d] = 0;
+        status[d] = 0;
+    }
+}
+
+void kr_ge_prepare() {
+    KR_CUDA(cudaFuncSetAttribute(ortho_kernel<12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * OT * 8));
+    KR_CUDA(cudaFuncSetAttribute(ortho_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * OT * 8));
+    KR_CUDA(cudaFuncSetAttribute(ortho_kernel<20, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 20 * OT * 8));
+    KR_CUDA(cudaFuncSetAttribute(ortho_kernel<24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * OT * 8));
+    KR_CUDA(cudaFuncSetAttribute(ortho_kernel<27, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 27 * OT * 8));
+}
+
+void kr_ge_enqueue_direction_set(kr_handle* h) {
+    const int ndl = (int)h->my_dirs.size();
+    const int64_t N = h->N;
+    const int k = h->k;
+    ge_reset<<<1, 256, 0, h->stream>>>(h->d_done, h->d_status, ndl);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    for (int dl = 0; dl < ndl; ++dl) {
+        const int d = h->my_dirs[dl];
+        kr_fill_dense(h->stream, h->d_V + (int64_t)dl * (k + 1) * N, N, h->n, h->mx, h->my, h->op == KR_OP_STENCIL7,
+                      h->dirs_h[d], h->dir_lift1[d], 1.0, 0, &h->launches);
+    }
+    launch_ortho(h, 0, ndl);
+    const int64_t vstride = (int64_t)(k + 1) * N;
+    const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
+    for (int j = 1; j <= k; ++j) {
+        const double* X = h->d_V + (int64_t)(j - 1) * N;
+        if (h->timing) KR_CUDA(cudaEventRecord(h->ev[2 * (j - 1)], h->stream));
+        if (h->op == KR_OP_CSR)
+            spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X,
+                                                                  vstride, h->d_W, N, ndl, h->d_done);
+        else
+            stencil_apply_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->mx, h->my, h->mz, h->cx, h->cy, h->cz, X,
+                                                                       vstride, h->d_W, N, h->d_done);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        if (h->timing) KR_CUDA(cudaEventRecord(h->ev[2 * (j - 1) + 1], h->stream));
+        launch_ortho(h, j, ndl);
+    }
+}

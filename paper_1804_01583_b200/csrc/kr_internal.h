@@ -1,0 +1,211 @@
+// kr_internal.h — internal types shared by the CUDA translation units of libkrylov_reach.so.
+// Not part of the ABI (include/krylov_reach.h is). sm_100a only.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/krylov_reach.h"
+
+#define KR_KMAX 256        // max Krylov dimension (expm smem sized per launch from k_eff)
+#define KR_MAX_BOX 8       // box-kind output rows handled inside the fused stencil kernel
+#define KR_MAX_OUT 64      // output rows
+
+// ------------------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------------------
+void kr_set_error(const std::string& msg);
+struct KrError {
+    kr_status st;
+    std::string msg;
+};
+#define KR_THROW(st, msg) throw KrError{(st), (msg)}
+#define KR_CUDA(call)                                                                                   \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            KR_THROW(KR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + ":" + \
+                                   std::to_string(__LINE__));                                          \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------------
+// device-side descriptors
+// ------------------------------------------------------------------------------------------------
+// A compact vector on the device (kr_vec with device idx/val; sparse entries sorted and merged on host)
+struct DVec {
+    int32_t kind;
+    int64_t nnz;
+    const int64_t* idx;
+    const double* val;
+    int64_t lo[3], hi[3];
+    double value;
+};
+
+struct BoxRow {  // a KR_VEC_BOX / KR_VEC_ALL output row as seen by the fused kernel (global coords)
+    int32_t lo[3], hi[3];
+    int32_t slot;  // output row index r
+};
+
+// Per-direction Lanczos scalars of the fused path (device memory, written by lz_finalize).
+// Index convention (1-based as in Alg. 3): alpha[i] = H_{i,i}, beta[i] = H_{i+1,i}, s[i] = 1/||u_i||.
+struct LzScalars {
+    double alpha[KR_KMAX + 2];
+    double beta[KR_KMAX + 2];
+    double s[KR_KMAX + 2];
+    double hmax;
+    double beta0;
+    double h_next;
+    int32_t done;
+    int32_t k_eff;
+    int32_t status;  // KR_OK or KR_EZERO / KR_ENONFINITE detected on device
+    int32_t pad;
+};
+
+// One z-slab of the fused Lanczos path. Vector buffers hold (nz + 3) planes of my x pitch doubles:
+// buffer plane 0 = global plane z0-1 (ghost / halo), planes 1..nz = owned z0..z1-1, planes nz+1, nz+2 =
+// halo z1, z1+1 (zero ghosts where outside the global grid).
+struct Slab {
+    int64_t z0, z1, nz;
+    double* u[3];
+    CUtensorMap tmC[3];  // "center" role box (TX+4, TY+3, 1)
+    CUtensorMap tmP[3];  // "previous" role box (TX+2, TY+1, 1)
+    double* partials;    // [nblk][nqp]
+    int64_t nblk;
+    dim3 grid;
+    int zchunk;
+};
+
+struct SlabInfo {  // device-visible copy for the local-reduce sparse gather
+    int64_t z0, z1, nz;
+    const double* u[3];
+};
+
+// ------------------------------------------------------------------------------------------------
+// handle
+// ------------------------------------------------------------------------------------------------
+enum { PATH_FUSED_LANCZOS = 0, PATH_GENERIC = 1 };
+
+struct kr_comm {
+    void* nccl;  // ncclComm_t
+    int32_t rank, world, device;
+};
+
+struct kr_handle {
+    // problem (host copies of scalars)
+    int32_t op, method, path, part;
+    int64_t mx, my, mz, pitch;
+    double alpha, cx, cy, cz;
+    int64_t n;  // unlifted state count
+    int64_t N;  // operator dimension (n or n+1)
+    bool lifted;
+    int32_t n_gen, n_dir, n_out, k;
+    int64_t n_steps;
+    double step;
+    double mu;  // Gershgorin upper bound of lambda_max(sym A)
+    int32_t device;
+    cudaStream_t stream;
+    bool own_stream;
+    kr_comm* comm;
+    int32_t rank, world;
+    std::vector<int32_t> my_dirs;  // global direction indices handled by this rank
+    std::vector<double> zlo, zhi;  // per global direction (fixed direction: 1,1)
+
+    // device memory
+    char* ws;
+    size_t ws_bytes, ws_used;
+    bool own_ws;
+    std::vector<void*> extra_allocs;
+
+    // descriptors
+    std::vector<DVec> dirs_h;          // per global direction: up to 2 pieces (gen/center + lifted one)
+    std::vector<int32_t> dir_lift1;    // per global direction: 1 if the lifted coordinate is 1
+    DVec* d_outs;                      // [n_out]
+    std::vector<DVec> outs_h;
+    double* d_O;                       // generic path: dense [n_out][N]
+    // CSR
+    int64_t* d_rp;
+    int32_t* d_ci;
+    double* d_val;
+    double* d_b;
+
+    // results [local dirs]
+    double* d_H;      // [ndl][k+1][k]
+    double* d_P;      // [ndl][n_out][k]
+    double* d_beta0;  // [ndl]
+    double* d_hnext;  // [ndl]
+    int32_t* d_keff;  // [ndl]
+    int32_t* d_done;  // [ndl]
+    double* d_hmax;   // [ndl]
+    double* d_coeff;  // [(n_steps+1)][n_out][n_dir]  (full, after gather)
+    double* d_coeff_loc;  // [(n_steps+1)][n_out][ndl]
+    double* d_hlast;  // [ndl][n_steps+1]
+    double* d_lemma;  // [ndl]
+    double* d_zlo;    // [n_dir]
+    double* d_zhi;
+    double* d_box;    // box-check outputs: lo, hi [(N+1)][n_out]
+    void* d_cex;      // device cex + witness
+    double* d_gather; // dirs partition gather scratch
+    int32_t* d_status;
+    int32_t* d_box_slot;  // [n_box] output row of each fused box row
+    double* d_box_val;    // [n_box] value of each fused box row
+    int32_t* d_sense;     // [n_out] check_box scratch
+    double* d_thr;        // [n_out]
+
+    // fused path
+    std::vector<Slab> slabs;
+    SlabInfo* d_slabinfo;
+    LzScalars* d_sc;       // [ndl]
+    double* d_rankvec;     // [world*nslabs][nq]
+    int32_t nq, nqp;       // 2 + n_out ; 2 + n_box
+    std::vector<BoxRow> boxes;
+    int32_t TX, TY;
+
+    // generic path
+    double* d_V;  // [ndl][k+1][N]
+    double* d_W;  // [ndl][N]
+
+    // graph
+    cudaGraphExec_t gexec;
+    bool graph_ready;
+    int64_t graph_launches;  // kernel nodes in the Krylov graph
+    int64_t launches;
+    bool projected;
+
+    // timing
+    bool timing;
+    std::vector<cudaEvent_t> ev;  // pairs around each step kernel
+    cudaEvent_t ev_it0, ev_it1;
+    double last_iter_ms, last_step_ms_mean;
+    int64_t last_step_launches;
+    double step_bytes;  // algorithmic bytes per fused step launch (24 n_local)
+};
+
+// ------------------------------------------------------------------------------------------------
+// launchers (implemented in the .cu files)
+// ------------------------------------------------------------------------------------------------
+// fill: dst[(plane b, y, x)] for b in [0, nplanes) representing global plane zbase + b, pitch doubles per row
+void kr_fill_grid(cudaStream_t s, double* dst, int64_t mx, int64_t my, int64_t pitch, int64_t nplanes,
+                  int64_t zbase, int64_t mz, const DVec& v, int64_t* launches);
+void kr_fill_dense(cudaStream_t s, double* dst, int64_t N, int64_t n, int64_t mx, int64_t my, bool stencil,
+                   const DVec& v, int lift1, double scale, int accumulate, int64_t* launches);
+
+// fused Lanczos
+void kr_lz_encode_maps(kr_handle* h);
+void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events);
+size_t kr_lz_step_smem(int TX, int TY);
+
+// generic
+void kr_ge_enqueue_direction_set(kr_handle* h);
+
+// expm + projection + lemma
+void kr_expm_enqueue(kr_handle* h);
+// box
+void kr_box_enqueue(kr_handle* h, const int32_t* d_sense, const double* d_thr);
+
+// nccl
+void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s);
+void kr_nccl_halo(kr_comm* c, kr_handle* h, int buf, cudaStream_t s);
