@@ -1,0 +1,290 @@
+#!/usr/bin/env python
+"""Benchmark: Krylov steps/s and fused-step HBM GB/s (% of peak) on the 10^9-state heat system
+(BASELINE.json metric; configs[4] = C5: 1000^3 Dirichlet heat, 100^3 corner block, Lanczos k=30,
+1000 steps of 0.02, center-cell output with y >= 0.012).
+
+One bench "step" = one pass of the whole hot path on data resident in HBM: start vector, k Lanczos
+steps (fused one-pass stencil kernel + reductions), the 1001 batched k x k Pade exponentials and
+projections, and the per-step box check (krylov_project + krylov_check_box).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+N > 1 runs under torch.distributed.run (one process per GPU, NCCL): z-slab decomposition with halo
+exchange (strong scaling: the same 10^9 problem split over N GPUs).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "Krylov steps/sec and fused SpMV HBM GB/s (% of peak) on 10^9-state heat"
+
+
+def peaks():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(p_full, budget="bench"):
+    """The oracle as it stands (single-threaded C, literal Alg. 3 + MvL Pade) on a bounded sample of
+    the workload: the same recipe on a smaller grid (Lanczos cost is linear in n) plus the full
+    1001-step k x k exponential sweep; scaled to Krylov steps/s at the full n."""
+    import oracle
+    m_full = p_full["mx"]
+    m_s = 160 if budget == "reference" else 250
+    b_s = max(2, round(p_full["gens"][0]["hi"][0] * m_s / m_full))
+    ps = W.heat(m_s, b_s, p_full["k"], n_steps=p_full["n_steps"], step=p_full["step"])
+    v = oracle.directions(ps)[0]
+    t0 = time.perf_counter()
+    r = oracle.lanczos(ps, v, ps["k"])
+    t1 = time.perf_counter()
+    oracle.expm_e1_times(r["H"], ps["step"], ps["n_steps"])
+    t2 = time.perf_counter()
+    n_s, n_f = m_s ** 3, W.n_state(p_full)
+    t_full = (t1 - t0) * (n_f / n_s) + (t2 - t1)
+    k = r["k_eff"]
+    return {"value": k / t_full, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle (1 thread, C -O2) Lanczos k={k} on the C5 recipe at m={m_s} "
+                      f"({n_s:.3g} states, block {b_s}^3) = {t1 - t0:.2f} s scaled x{n_f / n_s:.1f} to n={n_f:.3g}, "
+                      f"plus the full {ps['n_steps'] + 1}-step {k}x{k} Pade sweep {t2 - t1:.2f} s",
+            "sample_seconds": t2 - t0}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    p = W.CONFIGS[args.config]()
+    for _ in range(args.warmup):
+        cpu_baseline(p, "reference")
+    vals, secs = [], []
+    for _ in range(args.steps):
+        cb = cpu_baseline(p, "reference")
+        vals.append(cb["value"])
+        secs.append(cb["sample_seconds"])
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Krylov steps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * p["k"] / v,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(p, args.gpus),
+            "cpu_baseline": {"value": v, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": "Krylov steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(p, n):
+    return {"workload": f"{p['name']}: 3D heat {p['mx']}^3 (n={W.n_state(p):.3g}) Dirichlet 7-point stencil, "
+                        f"corner block {p['gens'][0]['hi'][0]}^3 in [0.9,1.1], Lanczos k={p['k']}, "
+                        f"{p['n_steps']} steps of {p['step']}, outputs center + total heat + 2 cells",
+            "n": W.n_state(p), "k": p["k"], "n_steps": p["n_steps"],
+            "parallelism": f"zslab{n}" if n > 1 else "single-gpu",
+            "l2": "inputs larger than L2 (three 8 GB state vectors per step vs 126 MB L2)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    from paper_1804_01583_b200 import KrComm, KrylovReach, torch_broadcast_id
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = KrComm(rank, world, local, torch_broadcast_id)
+    p = W.CONFIGS[args.config]()
+    stream = torch.cuda.current_stream(dev)
+    kw = dict(device=local, stream=stream.cuda_stream, comm=comm, part="zslab" if world > 1 else None)
+    from paper_1804_01583_b200 import krylov_workspace_bytes
+    wsb = krylov_workspace_bytes(p, **kw)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    h = KrylovReach(p, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw)
+
+    def one_step():
+        h.project(want=False)
+        return h.check_box(want_bounds=False)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    barrier()
+    l0 = h.launch_count()
+    step_ms, iter_ms = [], []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            cb = one_step()
+            t = h.last_timing()
+            step_ms.append(t["step_ms_mean"])
+            iter_ms.append(t["iter_ms"])
+        ev1.record(stream)
+        barrier()
+    launches = h.launch_count() - l0
+    elapsed = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([elapsed], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    coeff, stats = h.project()
+    k_eff = stats[0]["k_eff"]
+    ms_per_step = elapsed / args.steps
+    value = k_eff / (ms_per_step / 1000.0)
+    timing = h.last_timing()
+    n_local_bytes = timing["step_bytes"]
+    sk = float(np.mean(step_ms))
+    achieved = n_local_bytes / (sk * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tr.get(args.config)
+    except Exception:
+        pass
+
+    # e2e: the same metric through the public API with host buffers: create (H2D of the problem) ->
+    # project (D2H of all coefficients) -> check_box (D2H of bounds + counter-example) -> destroy.
+    e2e = None
+    if not args.no_e2e:
+        e_ms = []
+        h2d = d2h = 0
+        for it in range(2):
+            barrier()
+            t0 = time.perf_counter()
+            with KrylovReach(p, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw) as h2:
+                c2, st2 = h2.project()
+                cb2 = h2.check_box()
+                tb = h2.transfer_bytes()
+            barrier()
+            e_ms.append((time.perf_counter() - t0) * 1e3)
+            h2d, d2h = tb
+        e_sec = max(e_ms[1:]) / 1e3 if len(e_ms) > 1 else e_ms[0] / 1e3
+        if world > 1:
+            tt = torch.tensor([e_sec], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e_sec = float(tt.item())
+        e2e = {"value": k_eff / e_sec, "unit": "Krylov steps/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_sec * 1e3,
+               "note": "wall clock of create+project+check_box+destroy on caller workspace; includes CUDA-graph capture"}
+    h.close()
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "Krylov steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(p, world),
+        "fused_step": {"gbs": achieved, "pct_of_peak": 100.0 * achieved / peak, "ms_mean": sk,
+                       "bytes_per_launch": n_local_bytes, "launches_per_step": timing["step_launches"]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "lz_step_kernel (fused Lanczos step)",
+                     "algorithmic_bytes": "24 n_local per launch (read u_i, read u_{i-1}, write u_{i+1})",
+                     "peak_source": peak_src},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "iter_ms_mean": float(np.mean(iter_ms)),
+        "verdict": {"found": cb["found"], "step": cb["step"]},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(p)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        comm.close()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -161,6 +161,10 @@ const char* krylov_last_error(void);
 /* Number of this library's kernel launches issued so far on h (graph nodes counted per replay). */
 int64_t krylov_launch_count(const kr_handle* h);
 
+/* Host<->device bytes moved so far by this handle's ABI calls (create uploads, project/check_box
+ * downloads and threshold uploads). */
+kr_status krylov_transfer_bytes(const kr_handle* h, int64_t* h2d, int64_t* d2h);
+
 /* Device-side duration in ms of the last krylov_project's Krylov iteration phase and of its dominant
  * kernel (mean per launch), measured with CUDA events on the library stream. */
 kr_status krylov_last_timing(const kr_handle* h, double* iter_ms, double* step_kernel_ms_mean,

@@ -51,7 +51,7 @@ class kr_cex(C.Structure):
 EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "krylov_check_box",
            "krylov_reach_destroy", "krylov_last_error", "krylov_launch_count", "krylov_last_timing",
            "krylov_comm_unique_id", "krylov_comm_create", "krylov_comm_destroy", "krylov_zslab_range",
-           "krylov_krylov_data"]
+           "krylov_krylov_data", "krylov_transfer_bytes"]
 
 _lib = None
 
@@ -82,6 +82,7 @@ def lib():
     L.krylov_comm_destroy.argtypes = [vp]
     L.krylov_comm_destroy.restype = None
     L.krylov_krylov_data.argtypes = [vp, C.c_int32, vp, vp]
+    L.krylov_transfer_bytes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.krylov_zslab_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     for name in EXPORTS:
         if name not in ("krylov_reach_destroy", "krylov_last_error", "krylov_launch_count", "krylov_comm_destroy"):

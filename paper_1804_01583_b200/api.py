@@ -148,6 +148,11 @@ class KrylovReach:
         A.check(A.lib().krylov_krylov_data(self.h, int(d), _p(H), _p(P)))
         return H, P
 
+    def transfer_bytes(self):
+        h2d, d2h = C.c_int64(), C.c_int64()
+        A.check(A.lib().krylov_transfer_bytes(self.h, C.byref(h2d), C.byref(d2h)))
+        return h2d.value, d2h.value
+
     def launch_count(self):
         return int(A.lib().krylov_launch_count(self.h))
 

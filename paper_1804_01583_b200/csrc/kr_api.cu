@@ -137,6 +137,7 @@ template <class T>
 T* upload(kr_handle* h, const T* src, size_t count) {
     T* d = reinterpret_cast<T*>(dalloc(h, count * sizeof(T)));
     if (count) KR_CUDA(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    h->h2d_bytes += (int64_t)(count * sizeof(T));
     return d;
 }
 
@@ -605,13 +606,13 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
         const int ndl_max = dirs_gather ? (h->n_dir + h->world - 1) / h->world : ndl;
         const int64_t np1 = h->n_steps + 1;
         auto enqueue = [&](bool ev) {
-            KR_CUDA(cudaEventRecord(h->ev_it0, h->stream));
+            KR_CUDA(cudaEventRecordWithFlags(h->ev_it0, h->stream, cudaEventRecordExternal));
             if (h->path == PATH_FUSED_LANCZOS) {
                 for (int dl = 0; dl < ndl; ++dl) kr_lz_enqueue_direction(h, dl, ev);
             } else {
                 kr_ge_enqueue_direction_set(h);
             }
-            KR_CUDA(cudaEventRecord(h->ev_it1, h->stream));
+            KR_CUDA(cudaEventRecordWithFlags(h->ev_it1, h->stream, cudaEventRecordExternal));
             kr_expm_enqueue(h);
             if (dirs_gather) {
                 double* loc = h->d_coeff_loc + (size_t)h->rank * np1 * h->n_out * ndl_max;
@@ -691,8 +692,11 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             h->last_step_ms_mean = cnt ? tot / cnt : 0.0;
             h->last_step_launches = cnt * (h->path == PATH_FUSED_LANCZOS ? (int64_t)h->slabs.size() : 1);
         }
-        if (coeff)
+        if (coeff) {
             KR_CUDA(cudaMemcpy(coeff, h->d_coeff, (size_t)np1 * h->n_out * h->n_dir * 8, cudaMemcpyDeviceToHost));
+            h->d2h_bytes += (int64_t)np1 * h->n_out * h->n_dir * 8;
+        }
+        if (stats) h->d2h_bytes += (int64_t)ndl * 28;
         if (stats) {
             if (dirs_gather) {
                 std::vector<double> g((size_t)ndl_max * 4 * h->world);
@@ -741,7 +745,9 @@ kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr
         double* dt = h->d_thr;
         KR_CUDA(cudaMemcpyAsync(ds, sense, (size_t)h->n_out * 4, cudaMemcpyHostToDevice, h->stream));
         KR_CUDA(cudaMemcpyAsync(dt, thr, (size_t)h->n_out * 8, cudaMemcpyHostToDevice, h->stream));
+        h->h2d_bytes += (int64_t)h->n_out * 12;
         kr_box_enqueue(h, ds, dt);
+        h->d2h_bytes += (lo ? total * 8 : 0) + (hi ? total * 8 : 0) + 32 + (int64_t)h->n_dir * 8;
         if (lo) KR_CUDA(cudaMemcpyAsync(lo, h->d_box, total * 8, cudaMemcpyDeviceToHost, h->stream));
         if (hi) KR_CUDA(cudaMemcpyAsync(hi, h->d_box + total, total * 8, cudaMemcpyDeviceToHost, h->stream));
         struct {
@@ -788,6 +794,13 @@ kr_status krylov_krylov_data(const kr_handle* h, int32_t dir, double* H, double*
 }
 
 int64_t krylov_launch_count(const kr_handle* h) { return h ? h->launches : 0; }
+
+kr_status krylov_transfer_bytes(const kr_handle* h, int64_t* h2d, int64_t* d2h) {
+    if (!h) return KR_EINVAL;
+    if (h2d) *h2d = h->h2d_bytes;
+    if (d2h) *d2h = h->d2h_bytes;
+    return KR_OK;
+}
 
 kr_status krylov_last_timing(const kr_handle* h, double* iter_ms, double* step_kernel_ms_mean,
                              int64_t* step_kernel_launches, double* step_kernel_bytes) {

@@ -375,7 +375,7 @@ void kr_ge_enqueue_direction_set(kr_handle* h) {
     const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
     for (int j = 1; j <= k; ++j) {
         const double* X = h->d_V + (int64_t)(j - 1) * N;
-        if (h->timing) KR_CUDA(cudaEventRecord(h->ev[2 * (j - 1)], h->stream));
+        if (h->timing) KR_CUDA(cudaEventRecordWithFlags(h->ev[2 * (j - 1)], h->stream, cudaEventRecordExternal));
         if (h->op == KR_OP_CSR)
             spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X,
                                                                   vstride, h->d_W, N, ndl, h->d_done);
@@ -384,7 +384,7 @@ void kr_ge_enqueue_direction_set(kr_handle* h) {
                                                                        vstride, h->d_W, N, h->d_done);
         KR_CUDA(cudaGetLastError());
         h->launches++;
-        if (h->timing) KR_CUDA(cudaEventRecord(h->ev[2 * (j - 1) + 1], h->stream));
+        if (h->timing) KR_CUDA(cudaEventRecordWithFlags(h->ev[2 * (j - 1) + 1], h->stream, cudaEventRecordExternal));
         launch_ortho(h, j, ndl);
     }
 }

@@ -182,6 +182,7 @@ struct kr_handle {
     double last_iter_ms, last_step_ms_mean;
     int64_t last_step_launches;
     double step_bytes;  // algorithmic bytes per fused step launch (24 n_local)
+    int64_t h2d_bytes, d2h_bytes;  // host<->device bytes moved by the ABI calls (create/project/check_box)
 };
 
 // ------------------------------------------------------------------------------------------------

@@ -14,7 +14,8 @@
 //     where -w^T A w = sum_axes c_a sum_{edges} (w_b - w_a)^2 (+ c_a w^2 on ghost edges) is a sum of
 //     non-negative terms (summation by parts, Dirichlet ghosts = 0) — no cancellation;
 //   * the (x+1), (y+1), (z+1) neighbours of w are recomputed on a one-cell forward ring, so u_i is
-//     read with a depth-2 halo in-plane (TMA box (TX+4) x (TY+3)) and u_{i-1} with depth 1;
+//     read with a depth-2 halo in-plane (TMA box (TX+4) x (TY+3) from x0-2: TMA needs 16-byte aligned
+//     starts in x) and u_{i-1} with depth 1;
 //   * 2.5D z-march: each CTA owns a TX x TY column tile and a z-chunk; TMA (cp.async.bulk.tensor.3d)
 //     streams haloed planes of u_i and u_{i-1} into an S-stage shared-memory ring guarded by
 //     mbarriers (zero fill of out-of-bounds boxes gives the Dirichlet ghosts for free); the vertical
@@ -75,11 +76,12 @@ struct StepArgs {
 template <int TX, int TY>
 struct Geo {
     static constexpr int NT = 256;
-    static constexpr int CW = TX + 4, CH = TY + 3;  // u_i box: x0-1 .. x0+TX+2, y0-1 .. y0+TY+1
+    static constexpr int CW = TX + 4, CH = TY + 3;  // u_i box: x0-2 .. x0+TX+1, y0-1 .. y0+TY+1
     static constexpr int PW = TX + 2, PH = TY + 1;  // u_{i-1} box: x0 .. x0+TX+1, y0 .. y0+TY
     static constexpr int WW = TX + 1, WH = TY + 1;  // w plane on the tile + forward ring
     static constexpr int CBYTES = CW * CH * 8, PBYTES = PW * PH * 8;
-    static constexpr int STAGE = ((CBYTES + PBYTES + 127) / 128) * 128;
+    static constexpr int POFF = ((CBYTES + 127) / 128) * 128;  // TMA destinations are 128-byte aligned
+    static constexpr int STAGE = ((POFF + PBYTES + 127) / 128) * 128;
     static constexpr int WBYTES = ((2 * WW * WH * 8 + 127) / 128) * 128;
     static constexpr int NTC = TX * TY;             // tile cells
     static constexpr int NCELL = NTC + TX + TY;     // + right column + top row (no corner)
@@ -122,8 +124,8 @@ __global__ void __launch_bounds__(256) lz_step_kernel(const __grid_constant__ CU
         const int s = (p - pfirst) % S;
         unsigned char* st = smem + s * G::STAGE;
         mbar_expect_tx(&bar[s], txb);
-        tma_load_3d(st, &tmC, x0 - 1, y0 - 1, p + 1, &bar[s]);
-        if (a.has_prev) tma_load_3d(st + G::CBYTES, &tmP, x0, y0, p + 1, &bar[s]);
+        tma_load_3d(st, &tmC, x0 - 2, y0 - 1, p + 1, &bar[s]);  // x start must be 16-byte aligned
+        if (a.has_prev) tma_load_3d(st + G::POFF, &tmP, x0, y0, p + 1, &bar[s]);
     };
     if (tid == 0) {
         const int np = npl < S ? npl : S;
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256) lz_step_kernel(const __grid_constant__ CU
         const double* C1 = reinterpret_cast<const double*>(smem + (1 % S) * G::STAGE);
 #pragma unroll
         for (int m = 0; m < G::NSLOT; ++m) {
-            const int o = (ly[m] + 1) * G::CW + lx[m] + 1;
+            const int o = (ly[m] + 1) * G::CW + lx[m] + 2;
             up[m] = act[m] ? C0[o] : 0.0;
             uc[m] = act[m] ? C1[o] : 0.0;
             wp[m] = 0.0;
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(256) lz_step_kernel(const __grid_constant__ CU
         }
         const unsigned char* stq = smem + ((q - pfirst) % S) * G::STAGE;
         const double* Cq = reinterpret_cast<const double*>(stq);
-        const double* Pq = reinterpret_cast<const double*>(stq + G::CBYTES);
+        const double* Pq = reinterpret_cast<const double*>(stq + G::POFF);
         const double* Cn = reinterpret_cast<const double*>(smem + ((pn - pfirst) % S) * G::STAGE);
         const int gz = a.zoff + q;
         const bool zin = gz < a.mz;
@@ -207,13 +209,13 @@ __global__ void __launch_bounds__(256) lz_step_kernel(const __grid_constant__ CU
         for (int m = 0; m < G::NSLOT; ++m) {
             if (!act[m]) continue;
             const int x = lx[m], y = ly[m];
-            const double un = Cn[(y + 1) * G::CW + x + 1];
+            const double un = Cn[(y + 1) * G::CW + x + 2];
             double w;
             if (INIT) {
                 w = uc[m];
             } else {
-                const double sx = Cq[(y + 1) * G::CW + x] + Cq[(y + 1) * G::CW + x + 2];
-                const double sy = Cq[y * G::CW + x + 1] + Cq[(y + 2) * G::CW + x + 1];
+                const double sx = Cq[(y + 1) * G::CW + x + 1] + Cq[(y + 1) * G::CW + x + 3];
+                const double sy = Cq[y * G::CW + x + 2] + Cq[(y + 2) * G::CW + x + 2];
                 const double sz = up[m] + un;
                 const double Au = cx * sx + cy * sy + cz * sz - diag * uc[m];
                 w = sa * Au - sb * uc[m];
@@ -605,9 +607,9 @@ void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events) {
     for (int i = 1; i <= k; ++i) {
         const int cur = (i - 1) % 3, prev = (i >= 2) ? (i - 2) % 3 : -1, nxt = i % 3;
         const bool write = i < k;
-        if (capture_events && dl == 0) KR_CUDA(cudaEventRecord(h->ev[evi], h->stream));
+        if (capture_events && dl == 0) KR_CUDA(cudaEventRecordWithFlags(h->ev[evi], h->stream, cudaEventRecordExternal));
         for (auto& sl : h->slabs) step_launch(h, sl, sc, cur, prev, nxt, i, false, write);
-        if (capture_events && dl == 0) KR_CUDA(cudaEventRecord(h->ev[evi + 1], h->stream));
+        if (capture_events && dl == 0) KR_CUDA(cudaEventRecordWithFlags(h->ev[evi + 1], h->stream, cudaEventRecordExternal));
         evi += 2;
         if (write) {
             if (h->slabs.size() > 1) halo_exchange_virtual(h, nxt);

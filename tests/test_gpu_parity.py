@@ -154,7 +154,7 @@ def test_config5_first_step_closed_form():
 # Stencil Lanczos: ragged tiles, odd sizes, partitions, determinism, breakdown
 # ---------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("mx,my,mz,blk,k", [(16, 16, 16, 3, 20), (37, 21, 13, 4, 25), (5, 5, 5, 2, 30),
-                                            (70, 9, 11, 5, 16), (130, 17, 6, 7, 12), (2, 3, 2, 1, 6)])
+                                            (70, 9, 11, 5, 16), (130, 17, 6, 5, 12), (2, 3, 2, 1, 6)])
 def test_stencil_lanczos_shapes(mx, my, mz, blk, k):
     p = W.heat(mx, blk, k, n_steps=60, step=0.05, my=my, mz=mz)
     p["outs"].append(W.box((1, 1, 1), (min(mx, 4), min(my, 5), min(mz, 3)), 0.5))
@@ -188,7 +188,7 @@ def test_deterministic_bitwise():
 def test_lanczos_breakdown_on_sine_mode():
     m = 12
     x = np.arange(m)
-    s1 = np.sin((x + 1) * 2 * np.pi / (m + 1))
+    s1 = np.sin((x + 1) * 3 * np.pi / (m + 1))  # odd modes: no output is identically zero
     s2 = np.sin((x + 1) * 1 * np.pi / (m + 1))
     phi = np.einsum("k,j,i->kji", s2, s1, s2).ravel()
     p = W.heat(m, 2, 10, n_steps=20, step=0.1, extras=True)
