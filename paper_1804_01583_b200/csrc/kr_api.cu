@@ -504,8 +504,16 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
             h->nqp = 2 + (int)h->boxes.size();
             // tile choice: TX in {64, 32} by ragged waste, TY = 8
             auto waste = [&](int64_t t) { return (double)(((h->mx + t - 1) / t) * t - h->mx) / (double)h->mx; };
-            h->TX = (waste(64) <= waste(32) + 0.02) ? 64 : 32;
+            h->TX = (waste(64) <= waste(32) + 0.10) ? 64 : 32;
             h->TY = 8;
+            if (h->TX == 64 && h->my >= 64) h->TY = 16;  // 4 cells per thread, less y-halo re-read
+            if (const char* t = getenv("KR_TILE")) {  // tuning override "TXxTY"
+                int tx = 0, ty = 0;
+                if (sscanf(t, "%dx%d", &tx, &ty) == 2 && kr_lz_step_smem(tx, ty) > 0) {
+                    h->TX = tx;
+                    h->TY = ty;
+                }
+            }
             int nsl = 1, W = h->world, R = h->rank;
             if (p->virtual_slabs > 1) {
                 nsl = p->virtual_slabs;

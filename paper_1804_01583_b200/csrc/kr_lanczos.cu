@@ -70,6 +70,7 @@ struct StepArgs {
     int32_t nqp;
     double* partials;   // [nblk][nqp]
     int32_t nbox;
+    uint32_t all_mask;  // box rows covering the whole grid: served by the plain sum of w
     BoxRow box[KR_MAX_BOX];
 };
 
@@ -83,10 +84,10 @@ struct Geo {
     static constexpr int POFF = ((CBYTES + 127) / 128) * 128;  // TMA destinations are 128-byte aligned
     static constexpr int STAGE = ((POFF + PBYTES + 127) / 128) * 128;
     static constexpr int WBYTES = ((2 * WW * WH * 8 + 127) / 128) * 128;
-    static constexpr int NTC = TX * TY;             // tile cells
-    static constexpr int NCELL = NTC + TX + TY;     // + right column + top row (no corner)
-    static constexpr int NSLOT = (NCELL + NT - 1) / NT;
-    static constexpr int NTSLOT = (NTC + NT - 1) / NT;
+    static constexpr int NTC = TX * TY;  // tile cells: NTC / NT per thread, always active
+    static constexpr int TS = NTC / NT;
+    static constexpr int NR = TX + TY;   // forward ring: right column + top row (no corner), tid < NR
+    static_assert(NTC % NT == 0 && NR <= NT, "tile must map onto 256 threads");
 };
 
 template <int TX, int TY, int S>
@@ -94,12 +95,199 @@ constexpr size_t step_smem_bytes() {
     return (size_t)S * Geo<TX, TY>::STAGE + Geo<TX, TY>::WBYTES + 8 * S + 16;
 }
 
-template <int TX, int TY, int S, bool INIT>
-__global__ void __launch_bounds__(256) lz_step_kernel(const __grid_constant__ CUtensorMap tmC,
-                                                      const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
+template <int TX, int TY, int S, bool INIT, bool FULL>
+__device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
+                                         unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
+                                         int zc0, int zc1, bool cta_box, double* acc) {
     using G = Geo<TX, TY>;
-    const LzScalars* sc = a.sc;
-    if (sc->done) return;  // breakdown happened earlier: uniform early exit
+    const int tid = threadIdx.x;
+    const int pfirst = zc0 - 1, plast = zc1 + 1;
+    const uint32_t txb = G::CBYTES + (a.has_prev ? G::PBYTES : 0);
+    const bool has_prev = a.has_prev != 0;
+    auto issue = [&](int p) {
+        const int s = (p - pfirst) % S;
+        unsigned char* st = smem + s * G::STAGE;
+        mbar_expect_tx(&bar[s], txb);
+        tma_load_3d(st, tmC, x0 - 2, y0 - 1, p + 1, &bar[s]);  // x start must be 16-byte aligned
+        if (has_prev) tma_load_3d(st + G::POFF, tmP, x0, y0, p + 1, &bar[s]);
+    };
+    if (tid == 0) {
+        const int np = min(plast - pfirst + 1, S);
+        for (int p = pfirst; p < pfirst + np; ++p) issue(p);
+    }
+    double sa = 1.0, sb = 0.0, sp = 0.0;
+    if (!INIT) {
+        const LzScalars* sc = a.sc;
+        const int i = a.step;
+        sa = sc->s[i];
+        sb = sc->alpha[i] * sc->s[i];
+        sp = (i > 1) ? sc->beta[i - 1] * sc->s[i - 1] : 0.0;
+    }
+    const double cx = a.cx, cy = a.cy, cz = a.cz;
+    const double diag = 2.0 * (cx + cy + cz);
+
+    // Thread -> cells: tile slot m is cell (x, y0 + ty + m * (NT/TX)) with x = tid % TX, ty = tid / TX,
+    // so all slots of a thread share x and the smem offsets differ by compile-time constants.
+    constexpr int RS = G::NT / TX;  // rows per slot step
+    const int x = tid % TX, ty = tid / TX;
+    const int gx = x0 + x;
+    const int ci0 = (ty + 1) * G::CW + x + 2, pi0 = ty * G::PW + x, wi0 = ty * G::WW + x;
+    bool ing[G::TS];
+    uint32_t bm[G::TS];
+#pragma unroll
+    for (int m = 0; m < G::TS; ++m) {
+        const int gy = y0 + ty + m * RS;
+        ing[m] = FULL || (gx < a.mx && gy < a.my);
+        uint32_t bb = 0;
+        if (cta_box)
+            for (int r = 0; r < a.nbox; ++r)
+                if (!((a.all_mask >> r) & 1u) && gx >= a.box[r].lo[0] && gx < a.box[r].hi[0] &&
+                    gy >= a.box[r].lo[1] && gy < a.box[r].hi[1])
+                    bb |= 1u << r;
+        bm[m] = bb;
+    }
+    // ghost-edge coefficients (Dirichlet): cx on x == 0, cy on y == 0 (only slot 0 can have y == 0)
+    const double gex = gx == 0 ? cx : 0.0;
+    const double gey0 = (y0 + ty == 0) ? cy : 0.0;
+    double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)(y0 + ty) * a.pitch + gx;
+    const int64_t rowstep = (int64_t)RS * a.pitch;
+
+    const bool has_ring = tid < G::NR;
+    int rci, rpi, rwi;
+    bool ring_in;
+    {
+        const int rx = tid < TY ? TX : tid - TY;
+        const int ry = tid < TY ? tid : TY;
+        rci = (ry + 1) * G::CW + rx + 2;
+        rpi = ry * G::PW + rx;
+        rwi = ry * G::WW + rx;
+        ring_in = has_ring && (FULL || (x0 + rx < a.mx && y0 + ry < a.my));
+    }
+
+    double up[G::TS], uc[G::TS], wp[G::TS];
+    double rup = 0.0, ruc = 0.0;
+    mbar_wait(&bar[0], 0);
+    mbar_wait(&bar[1 % S], 0);
+    {
+        const double* C0 = reinterpret_cast<const double*>(smem);
+        const double* C1 = reinterpret_cast<const double*>(smem + (1 % S) * G::STAGE);
+#pragma unroll
+        for (int m = 0; m < G::TS; ++m) {
+            up[m] = C0[ci0 + m * RS * G::CW];
+            uc[m] = C1[ci0 + m * RS * G::CW];
+            wp[m] = 0.0;
+        }
+        if (has_ring) {
+            rup = C0[rci];
+            ruc = C1[rci];
+        }
+    }
+    double acc_ww = 0.0, acc_d = 0.0, acc_sum = 0.0;
+    // plane q lives in stage sq; plane q+1 in stage sn with mbarrier phase ph (incremental, no modulo)
+    int sq = 1 % S, sn = 2 % S;
+    uint32_t ph = (2 / S) & 1;
+    for (int q = zc0; q <= zc1; ++q) {
+        mbar_wait(&bar[sn], ph);
+        const unsigned char* stq = smem + sq * G::STAGE;
+        const double* Cq = reinterpret_cast<const double*>(stq) + ci0;
+        const double* Pq = reinterpret_cast<const double*>(stq + G::POFF) + pi0;
+        const double* Cn = reinterpret_cast<const double*>(smem + sn * G::STAGE) + ci0;
+        const bool zin = a.zoff + q < a.mz;  // uniform: the plane above the global grid is a zero ghost
+        double* Wq = ((q & 1) ? Wb1 : Wb0) + wi0;
+        double wc[G::TS];
+#pragma unroll
+        for (int m = 0; m < G::TS; ++m) {
+            const int o = m * RS * G::CW;
+            const double un = Cn[o];
+            double w;
+            if (INIT) {
+                w = uc[m];
+            } else {
+                const double sx = Cq[o - 1] + Cq[o + 1];
+                const double sy = Cq[o - G::CW] + Cq[o + G::CW];
+                const double sz = up[m] + un;
+                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -diag * uc[m])));
+                w = fma(sa, Au, -sb * uc[m]);
+                if (has_prev) w = fma(-sp, Pq[m * RS * G::PW], w);
+            }
+            if (!FULL && !ing[m]) w = 0.0;
+            if (!zin) w = 0.0;
+            Wq[m * RS * G::WW] = w;
+            wc[m] = w;
+            up[m] = uc[m];
+            uc[m] = un;
+        }
+        if (has_ring) {
+            const double* Cqb = reinterpret_cast<const double*>(stq);
+            const double un = reinterpret_cast<const double*>(smem + sn * G::STAGE)[rci];
+            double w = ruc;
+            if (!INIT) {
+                const double sx = Cqb[rci - 1] + Cqb[rci + 1];
+                const double sy = Cqb[rci - G::CW] + Cqb[rci + G::CW];
+                const double sz = rup + un;
+                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -diag * ruc)));
+                w = fma(sa, Au, -sb * ruc);
+                if (has_prev) w = fma(-sp, reinterpret_cast<const double*>(stq + G::POFF)[rpi], w);
+            }
+            if ((!FULL && !ring_in) || !zin) w = 0.0;
+            ((q & 1) ? Wb1 : Wb0)[rwi] = w;
+            rup = ruc;
+            ruc = un;
+        }
+        if (q > zc0) {  // products for plane q-1 (its w neighbours at x+1, y+1 were written last iteration)
+            const double* Wp = ((q & 1) ? Wb0 : Wb1) + wi0;
+            const int gzp = a.zoff + q - 1;
+            const double gz = (gzp == 0) ? cz : 0.0;
+            uint32_t zmask = 0;
+            if (cta_box)
+                for (int r = 0; r < a.nbox; ++r)
+                    if (gzp >= a.box[r].lo[2] && gzp < a.box[r].hi[2]) zmask |= 1u << r;
+            const bool wr = !INIT && a.write_out;
+#pragma unroll
+            for (int m = 0; m < G::TS; ++m) {
+                const int o = m * RS * G::WW;
+                const double w0 = wp[m];
+                const double dx = Wp[o + 1] - w0;
+                const double dy = Wp[o + G::WW] - w0;
+                const double dz = wc[m] - w0;
+                const double w2 = w0 * w0;
+                const double g = gex + gz + (m == 0 ? gey0 : 0.0);
+                acc_d = fma(cx, dx * dx, fma(cy, dy * dy, fma(cz, dz * dz, fma(g, w2, acc_d))));
+                acc_ww += w2;
+                acc_sum += w0;
+                const uint32_t mk = bm[m] & zmask;
+                if (mk) {
+#pragma unroll
+                    for (int r = 0; r < KR_MAX_BOX; ++r)
+                        if ((mk >> r) & 1u) acc[3 + r] += w0;
+                }
+                if (wr && (FULL || ing[m])) optr[m * rowstep] = w0;
+            }
+            optr += a.plane;
+        }
+#pragma unroll
+        for (int m = 0; m < G::TS; ++m) wp[m] = wc[m];
+        __syncthreads();
+        if (tid == 0) {
+            if (q == zc0 && pfirst + S <= plast) issue(pfirst + S);
+            if (q + S <= plast) issue(q + S);
+        }
+        sq = sn;
+        if (++sn == S) {
+            sn = 0;
+            ph ^= 1u;
+        }
+    }
+    acc[0] = acc_ww;
+    acc[1] = acc_d;
+    acc[2] = acc_sum;
+}
+
+template <int TX, int TY, int S, bool INIT>
+__global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(const __grid_constant__ CUtensorMap tmC,
+                                                         const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
+    using G = Geo<TX, TY>;
+    if (a.sc->done) return;  // breakdown happened earlier: uniform early exit
 
     extern __shared__ __align__(128) unsigned char smem[];
     double* Wb0 = reinterpret_cast<double*>(smem + S * G::STAGE);
@@ -110,9 +298,6 @@ __global__ void __launch_bounds__(256) lz_step_kernel(const __grid_constant__ CU
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const int zc0 = blockIdx.z * a.zchunk;
     const int zc1 = min(zc0 + a.zchunk, a.nz);
-    const int pfirst = zc0 - 1, plast = zc1 + 1;
-    const int npl = plast - pfirst + 1;
-    const uint32_t txb = G::CBYTES + (a.has_prev ? G::PBYTES : 0);
 
     if (tid == 0) {
 #pragma unroll
@@ -120,174 +305,40 @@ __global__ void __launch_bounds__(256) lz_step_kernel(const __grid_constant__ CU
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto issue = [&](int p) {
-        const int s = (p - pfirst) % S;
-        unsigned char* st = smem + s * G::STAGE;
-        mbar_expect_tx(&bar[s], txb);
-        tma_load_3d(st, &tmC, x0 - 2, y0 - 1, p + 1, &bar[s]);  // x start must be 16-byte aligned
-        if (a.has_prev) tma_load_3d(st + G::POFF, &tmP, x0, y0, p + 1, &bar[s]);
-    };
-    if (tid == 0) {
-        const int np = npl < S ? npl : S;
-        for (int p = pfirst; p < pfirst + np; ++p) issue(p);
-    }
-
-    // step scalars: w = sa*A u_i - sb*u_i - sp*u_{i-1}
-    double sa = 1.0, sb = 0.0, sp = 0.0;
-    if (!INIT) {
-        const int i = a.step;
-        sa = sc->s[i];
-        sb = sc->alpha[i] * sc->s[i];
-        sp = (i > 1) ? sc->beta[i - 1] * sc->s[i - 1] : 0.0;
-    }
-    const double cx = a.cx, cy = a.cy, cz = a.cz;
-    const double diag = 2.0 * (cx + cy + cz);
-
-    int lx[G::NSLOT], ly[G::NSLOT];
-    bool act[G::NSLOT], ing[G::NSLOT];
-    uint32_t bm[G::NSLOT];
+    double acc[3 + KR_MAX_BOX];
 #pragma unroll
-    for (int m = 0; m < G::NSLOT; ++m) {
-        const int idx = tid + m * G::NT;
-        int x, y;
-        if (idx < G::NTC) {
-            x = idx % TX;
-            y = idx / TX;
-        } else if (idx < G::NTC + TY) {
-            x = TX;
-            y = idx - G::NTC;
-        } else {
-            x = idx - G::NTC - TY;
-            y = TY;
-        }
-        act[m] = idx < G::NCELL;
-        lx[m] = x;
-        ly[m] = y;
-        const int gx = x0 + x, gy = y0 + y;
-        ing[m] = act[m] && gx < a.mx && gy < a.my;
-        uint32_t b = 0;
-        for (int r = 0; r < a.nbox; ++r)
-            if (gx >= a.box[r].lo[0] && gx < a.box[r].hi[0] && gy >= a.box[r].lo[1] && gy < a.box[r].hi[1])
-                b |= 1u << r;
-        bm[m] = b;
-    }
-
-    double up[G::NSLOT], uc[G::NSLOT], wp[G::NSLOT], wc[G::NSLOT];
-    mbar_wait(&bar[0], 0);
-    mbar_wait(&bar[1 % S], 0);
-    {
-        const double* C0 = reinterpret_cast<const double*>(smem + 0 * G::STAGE);
-        const double* C1 = reinterpret_cast<const double*>(smem + (1 % S) * G::STAGE);
-#pragma unroll
-        for (int m = 0; m < G::NSLOT; ++m) {
-            const int o = (ly[m] + 1) * G::CW + lx[m] + 2;
-            up[m] = act[m] ? C0[o] : 0.0;
-            uc[m] = act[m] ? C1[o] : 0.0;
-            wp[m] = 0.0;
-        }
-    }
-
-    double acc_ww = 0.0, acc_d = 0.0;
-    double acc_b[KR_MAX_BOX];
-#pragma unroll
-    for (int r = 0; r < KR_MAX_BOX; ++r) acc_b[r] = 0.0;
-
-    for (int q = zc0; q <= zc1; ++q) {
-        const int pn = q + 1;
-        {
-            const int u = pn - pfirst;
-            mbar_wait(&bar[u % S], (u / S) & 1);
-        }
-        const unsigned char* stq = smem + ((q - pfirst) % S) * G::STAGE;
-        const double* Cq = reinterpret_cast<const double*>(stq);
-        const double* Pq = reinterpret_cast<const double*>(stq + G::POFF);
-        const double* Cn = reinterpret_cast<const double*>(smem + ((pn - pfirst) % S) * G::STAGE);
-        const int gz = a.zoff + q;
-        const bool zin = gz < a.mz;
-        double* Wq = (q & 1) ? Wb1 : Wb0;
-#pragma unroll
-        for (int m = 0; m < G::NSLOT; ++m) {
-            if (!act[m]) continue;
-            const int x = lx[m], y = ly[m];
-            const double un = Cn[(y + 1) * G::CW + x + 2];
-            double w;
-            if (INIT) {
-                w = uc[m];
-            } else {
-                const double sx = Cq[(y + 1) * G::CW + x + 1] + Cq[(y + 1) * G::CW + x + 3];
-                const double sy = Cq[y * G::CW + x + 2] + Cq[(y + 2) * G::CW + x + 2];
-                const double sz = up[m] + un;
-                const double Au = cx * sx + cy * sy + cz * sz - diag * uc[m];
-                w = sa * Au - sb * uc[m];
-                if (a.has_prev) w -= sp * Pq[y * G::PW + x];
-            }
-            if (!(ing[m] && zin)) w = 0.0;
-            Wq[y * G::WW + x] = w;
-            wc[m] = w;
-            up[m] = uc[m];
-            uc[m] = un;
-        }
-        if (q > zc0) {
-            const double* Wp = (q & 1) ? Wb0 : Wb1;
-            const int gzp = gz - 1;
-            double* orow = a.out + (int64_t)q * a.plane;  // buffer plane of local plane q-1
-#pragma unroll
-            for (int m = 0; m < G::NTSLOT; ++m) {
-                const int idx = tid + m * G::NT;
-                if (idx >= G::NTC) continue;
-                const int x = lx[m], y = ly[m];
-                const double w0 = wp[m];
-                const double dx = Wp[y * G::WW + x + 1] - w0;
-                const double dy = Wp[(y + 1) * G::WW + x] - w0;
-                const double dz = wc[m] - w0;
-                double D = cx * dx * dx + cy * dy * dy + cz * dz * dz;
-                if (x0 + x == 0) D += cx * w0 * w0;
-                if (y0 + y == 0) D += cy * w0 * w0;
-                if (gzp == 0) D += cz * w0 * w0;
-                acc_ww += w0 * w0;
-                acc_d += D;
-                if (bm[m]) {
-#pragma unroll
-                    for (int r = 0; r < KR_MAX_BOX; ++r)
-                        if (r < a.nbox && ((bm[m] >> r) & 1u) && gzp >= a.box[r].lo[2] && gzp < a.box[r].hi[2])
-                            acc_b[r] += w0;
-                }
-                if (!INIT && a.write_out && ing[m]) orow[(int64_t)(y0 + y) * a.pitch + (x0 + x)] = w0;
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < G::NSLOT; ++m) wp[m] = wc[m];
-        __syncthreads();
-        if (tid == 0) {
-            if (q == zc0 && pfirst + S <= plast) issue(pfirst + S);
-            if (q + S <= plast) issue(q + S);
-        }
-    }
+    for (int r = 0; r < 3 + KR_MAX_BOX; ++r) acc[r] = 0.0;
+    // does any (non all-grid) box output row intersect this CTA's tile and z-chunk? (usually not)
+    bool cta_box = false;
+    for (int r = 0; r < a.nbox; ++r)
+        if (!((a.all_mask >> r) & 1u) && a.box[r].lo[0] < x0 + TX && a.box[r].hi[0] > x0 &&
+            a.box[r].lo[1] < y0 + TY && a.box[r].hi[1] > y0 && a.box[r].lo[2] < a.zoff + zc1 &&
+            a.box[r].hi[2] > a.zoff + zc0)
+            cta_box = true;
+    // interior tiles (the forward ring inside the grid) skip all x/y masking
+    if (x0 + TX < a.mx && y0 + TY < a.my)
+        lz_march<TX, TY, S, INIT, true>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+    else
+        lz_march<TX, TY, S, INIT, false>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
 
     // fixed-order block reduction of (sum w^2, sum D, box rows)
-    __shared__ double red[8][2 + KR_MAX_BOX];
+    __shared__ double red[8][3 + KR_MAX_BOX];
     const int lane = tid & 31, wid = tid >> 5;
-    auto wsum = [&](double v) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        return v;
-    };
-    double v0 = wsum(acc_ww), v1 = wsum(acc_d);
-    if (lane == 0) {
-        red[wid][0] = v0;
-        red[wid][1] = v1;
-    }
+    for (int r = 0; r < 3 + KR_MAX_BOX; ++r) {
+        if (r < 3 + a.nbox) {
+            double v = acc[r];
 #pragma unroll
-    for (int r = 0; r < KR_MAX_BOX; ++r) {
-        if (r < a.nbox) {
-            double v = wsum(acc_b[r]);
-            if (lane == 0) red[wid][2 + r] = v;
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) red[wid][r] = v;
         }
     }
     __syncthreads();
     if (tid < a.nqp) {
+        // partial layout: [0] sum w^2, [1] sum D, [2 + r] box row r (all-grid rows take sum w)
+        const int src = tid < 2 ? tid : (((a.all_mask >> (tid - 2)) & 1u) ? 2 : tid + 1);
         double s = 0.0;
-        for (int w = 0; w < 8; ++w) s += red[w][tid];
+        for (int w = 0; w < 8; ++w) s += red[w][src];
         const int64_t blk = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
         a.partials[blk * a.nqp + tid] = s;
     }
@@ -447,14 +498,17 @@ void encode(CUtensorMap* tm, double* base, int64_t mx, int64_t my, int64_t nplan
     if (r != CUDA_SUCCESS) KR_THROW(KR_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
-constexpr int kS = 4;
+template <int TX, int TY>
+struct Stages {
+    static constexpr int S = (TX * TY > 512) ? 4 : 5;
+};
 
 }  // namespace
 
 size_t kr_lz_step_smem(int TX, int TY) {
-    if (TX == 64 && TY == 8) return step_smem_bytes<64, 8, kS>();
-    if (TX == 32 && TY == 8) return step_smem_bytes<32, 8, kS>();
-    if (TX == 64 && TY == 16) return step_smem_bytes<64, 16, kS>();
+    if (TX == 64 && TY == 16) return step_smem_bytes<64, 16, Stages<64, 16>::S>();
+    if (TX == 64 && TY == 8) return step_smem_bytes<64, 8, Stages<64, 8>::S>();
+    if (TX == 32 && TY == 8) return step_smem_bytes<32, 8, Stages<32, 8>::S>();
     return 0;
 }
 
@@ -468,8 +522,8 @@ void kr_lz_encode_maps(kr_handle* h) {
 
 template <int TX, int TY, bool INIT>
 static void set_smem_attr() {
-    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, kS, INIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)step_smem_bytes<TX, TY, kS>()));
+    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, Stages<TX, TY>::S, INIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
 }
 
 template <int TX, int TY>
@@ -477,15 +531,15 @@ static int occupancy_t() {
     set_smem_attr<TX, TY, false>();
     set_smem_attr<TX, TY, true>();
     int nb = 0;
-    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, kS, false>, 256,
-                                                          step_smem_bytes<TX, TY, kS>()));
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false>, 256,
+                                                          step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
     return nb;
 }
 
 int kr_lz_occupancy(int TX, int TY) {
+    if (TX == 64 && TY == 16) return occupancy_t<64, 16>();
     if (TX == 64 && TY == 8) return occupancy_t<64, 8>();
     if (TX == 32 && TY == 8) return occupancy_t<32, 8>();
-    if (TX == 64 && TY == 16) return occupancy_t<64, 16>();
     return 1;
 }
 
@@ -514,14 +568,20 @@ static void step_launch_t(kr_handle* h, Slab& sl, LzScalars* sc, int cur, int pr
     a.nqp = h->nqp;
     a.partials = sl.partials;
     a.nbox = (int)h->boxes.size();
-    for (int r = 0; r < a.nbox; ++r) a.box[r] = h->boxes[r];
-    const size_t smem = step_smem_bytes<TX, TY, kS>();
+    a.all_mask = 0;
+    for (int r = 0; r < a.nbox; ++r) {
+        a.box[r] = h->boxes[r];
+        const BoxRow& b = h->boxes[r];
+        if (b.lo[0] <= 0 && b.lo[1] <= 0 && b.lo[2] <= 0 && b.hi[0] >= h->mx && b.hi[1] >= h->my && b.hi[2] >= h->mz)
+            a.all_mask |= 1u << r;
+    }
+    const size_t smem = step_smem_bytes<TX, TY, Stages<TX, TY>::S>();
     const CUtensorMap& tc = sl.tmC[cur];
     const CUtensorMap& tp = sl.tmP[prev < 0 ? cur : prev];
     if (init) {
-        lz_step_kernel<TX, TY, kS, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+        lz_step_kernel<TX, TY, Stages<TX, TY>::S, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
     } else {
-        lz_step_kernel<TX, TY, kS, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+        lz_step_kernel<TX, TY, Stages<TX, TY>::S, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
     }
     KR_CUDA(cudaGetLastError());
     h->launches++;
@@ -529,12 +589,12 @@ static void step_launch_t(kr_handle* h, Slab& sl, LzScalars* sc, int cur, int pr
 
 static void step_launch(kr_handle* h, Slab& sl, LzScalars* sc, int cur, int prev, int nxt, int step, bool init,
                         bool write) {
-    if (h->TX == 64 && h->TY == 8)
+    if (h->TX == 64 && h->TY == 16)
+        step_launch_t<64, 16>(h, sl, sc, cur, prev, nxt, step, init, write);
+    else if (h->TX == 64 && h->TY == 8)
         step_launch_t<64, 8>(h, sl, sc, cur, prev, nxt, step, init, write);
     else if (h->TX == 32 && h->TY == 8)
         step_launch_t<32, 8>(h, sl, sc, cur, prev, nxt, step, init, write);
-    else if (h->TX == 64 && h->TY == 16)
-        step_launch_t<64, 16>(h, sl, sc, cur, prev, nxt, step, init, write);
     else
         KR_THROW(KR_EINVAL, "unsupported tile");
 }
