@@ -456,10 +456,10 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         h->d_keff = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4));
         h->d_done = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4));
         h->d_status = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4 + 64));
-        KR_CUDA(cudaMemset(h->d_H, 0, (size_t)ndl * (k + 1) * k * 8));
-        KR_CUDA(cudaMemset(h->d_P, 0, (size_t)ndl * h->n_out * k * 8));
-        KR_CUDA(cudaMemset(h->d_hnext, 0, (size_t)ndl * 8));
-        KR_CUDA(cudaMemset(h->d_status, 0, (size_t)ndl * 4 + 64));
+        KR_CUDA(cudaMemsetAsync(h->d_H, 0, (size_t)ndl * (k + 1) * k * 8, h->stream));
+        KR_CUDA(cudaMemsetAsync(h->d_P, 0, (size_t)ndl * h->n_out * k * 8, h->stream));
+        KR_CUDA(cudaMemsetAsync(h->d_hnext, 0, (size_t)ndl * 8, h->stream));
+        KR_CUDA(cudaMemsetAsync(h->d_status, 0, (size_t)ndl * 4 + 64, h->stream));
         h->d_coeff = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * h->n_dir * 8));
         if (p->part == KR_PART_DIRS && h->world > 1) {
             const int ndl_max = (h->n_dir + h->world - 1) / h->world;
@@ -535,7 +535,7 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
                 const size_t vb = (size_t)(sl.nz + 3) * h->my * h->pitch * sizeof(double);
                 for (int b = 0; b < 3; ++b) {
                     sl.u[b] = reinterpret_cast<double*>(carve(h, vb));
-                    KR_CUDA(cudaMemset(sl.u[b], 0, vb));
+                    KR_CUDA(cudaMemsetAsync(sl.u[b], 0, vb, h->stream));
                 }
                 const int64_t gx = (h->mx + h->TX - 1) / h->TX, gy = (h->my + h->TY - 1) / h->TY;
                 const int64_t slots_total = (int64_t)dev_sms * occ;
@@ -557,9 +557,16 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
                 if (env_zc) best_zc = std::max(1, atoi(env_zc));
                 sl.zchunk = best_zc;
                 const int64_t nch = (sl.nz + sl.zchunk - 1) / sl.zchunk;
-                sl.grid = dim3((unsigned)gx, (unsigned)gy, (unsigned)nch);
-                sl.nblk = gx * gy * nch;
-                sl.partials = reinterpret_cast<double*>(dalloc(h, (size_t)sl.nblk * h->nqp * 8));
+                sl.gx = (int32_t)gx;
+                sl.gy = (int32_t)gy;
+                sl.nitems = gx * gy * nch;
+                sl.nblk = sl.nitems;  // one work item per CTA: the block scheduler keeps neighbours co-resident
+                if (const char* e = getenv("KR_PERSIST")) sl.nblk = std::min<int64_t>(sl.nitems, std::max(1, atoi(e)));
+                sl.grid = dim3((unsigned)sl.nblk, 1, 1);
+                const int64_t ngrp = (sl.nblk + 63) / 64;
+                sl.partials = reinterpret_cast<double*>(dalloc(h, (size_t)(sl.nblk + ngrp) * h->nqp * 8));
+                sl.counter = reinterpret_cast<int32_t*>(dalloc(h, (size_t)(1 + ngrp) * 4));
+                KR_CUDA(cudaMemsetAsync(sl.counter, 0, (size_t)(1 + ngrp) * 4, h->stream));
                 h->slabs.push_back(sl);
             }
             kr_lz_encode_maps(h);
@@ -567,7 +574,7 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
             const int R_total = (int)h->slabs.size() * h->world;
             h->d_rankvec = reinterpret_cast<double*>(dalloc(h, (size_t)R_total * h->nq * 8));
             h->d_sc = reinterpret_cast<LzScalars*>(dalloc(h, (size_t)ndl * sizeof(LzScalars)));
-            KR_CUDA(cudaMemset(h->d_sc, 0, (size_t)ndl * sizeof(LzScalars)));
+            KR_CUDA(cudaMemsetAsync(h->d_sc, 0, (size_t)ndl * sizeof(LzScalars), h->stream));
             int64_t nloc = 0;
             for (auto& sl : h->slabs) nloc += sl.nz * h->mx * h->my;
             h->step_bytes = 24.0 * (double)nloc;
@@ -599,6 +606,9 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         for (auto& e : h->ev) KR_CUDA(cudaEventCreate(&e));
         KR_CUDA(cudaEventCreate(&h->ev_it0));
         KR_CUDA(cudaEventCreate(&h->ev_it1));
+        // all set-up work (zeroing of the state buffers, descriptors) ran on h->stream, which does not
+        // synchronise with the legacy default stream: finish it before the handle is used
+        KR_CUDA(cudaStreamSynchronize(h->stream));
         *out = h;
     });
     if (st != KR_OK) free_handle(h);

@@ -74,7 +74,10 @@ struct Slab {
     CUtensorMap tmC[3];  // "center" role box (TX+4, TY+3, 1)
     CUtensorMap tmP[3];  // "previous" role box (TX+2, TY+1, 1)
     double* partials;    // [nblk][nqp]
-    int64_t nblk;
+    int32_t* counter;    // last-CTA arrival counter of the fused reduction
+    int64_t nblk;        // persistent CTAs (= number of partial-sum slots)
+    int32_t gx, gy;      // tiles per x / y
+    int64_t nitems;      // work items = gx * gy * z-chunks
     dim3 grid;
     int zchunk;
 };

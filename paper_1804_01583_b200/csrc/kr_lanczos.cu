@@ -62,6 +62,7 @@ struct StepArgs {
     double* out;  // buffer receiving u_{i+1} (buffer plane 0 = ghost below the slab)
     int64_t pitch, plane;
     int32_t mx, my, mz, nz, zoff, zchunk;
+    int32_t gx, gy, nitems;  // persistent work items: gx * gy tiles x ceil(nz / zchunk) chunks
     double cx, cy, cz;  // alpha / h_a^2
     const LzScalars* sc;
     int32_t step;       // i (1-based); 0 = init pass
@@ -72,7 +73,26 @@ struct StepArgs {
     int32_t nbox;
     uint32_t all_mask;  // box rows covering the whole grid: served by the plain sum of w
     BoxRow box[KR_MAX_BOX];
+    // epilogue: the last CTA to finish reduces all partials in a fixed order (no float atomics)
+    int32_t* counter;        // per-slab arrival counter (reset to 0 by the last CTA)
+    double* rankvec;         // this slab's reduced vector [2 + n_out]
+    const int32_t* box_slot; // output row of each box row
+    const double* box_val;   // value of each box row
+    const DVec* outs;        // sparse output rows are gathered from `gather_u`
+    const double* gather_u;  // buffer holding the new vector (u_{i+1}, or u_1 for the init pass), or NULL
+    int32_t n_out;
+    int32_t fin;             // 1: this slab is the only contributor -> also do the scalar update
+    int32_t k;
+    double* H;
+    double* P;
+    double* beta0_out;
+    double* hnext_out;
+    int32_t* keff_out;
+    LzScalars* scw;          // writable scalars (same as sc)
+    DVec gen;                // init pass with an analytic generator (box / all): fill u_1 in the same pass
 };
+
+__device__ void lz_epilogue(const StepArgs& a, const double* acc, double* red, int64_t plane_elems);
 
 template <int TX, int TY>
 struct Geo {
@@ -102,14 +122,14 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
     using G = Geo<TX, TY>;
     const int tid = threadIdx.x;
     const int pfirst = zc0 - 1, plast = zc1 + 1;
-    const uint32_t txb = G::CBYTES + (a.has_prev ? G::PBYTES : 0);
     const bool has_prev = a.has_prev != 0;
     auto issue = [&](int p) {
         const int s = (p - pfirst) % S;
         unsigned char* st = smem + s * G::STAGE;
-        mbar_expect_tx(&bar[s], txb);
+        const bool lp = has_prev && p > pfirst && p < plast;  // u_{i-1} is needed on planes zc0..zc1 only
+        mbar_expect_tx(&bar[s], G::CBYTES + (lp ? G::PBYTES : 0));
         tma_load_3d(st, tmC, x0 - 2, y0 - 1, p + 1, &bar[s]);  // x start must be 16-byte aligned
-        if (has_prev) tma_load_3d(st + G::POFF, tmP, x0, y0, p + 1, &bar[s]);
+        if (lp) tma_load_3d(st + G::POFF, tmP, x0, y0, p + 1, &bar[s]);
     };
     if (tid == 0) {
         const int np = min(plast - pfirst + 1, S);
@@ -278,9 +298,9 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
             ph ^= 1u;
         }
     }
-    acc[0] = acc_ww;
-    acc[1] = acc_d;
-    acc[2] = acc_sum;
+    acc[0] += acc_ww;
+    acc[1] += acc_d;
+    acc[2] += acc_sum;
 }
 
 template <int TX, int TY, int S, bool INIT>
@@ -295,117 +315,50 @@ __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(c
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * G::STAGE + G::WBYTES);
 
     const int tid = threadIdx.x;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int zc0 = blockIdx.z * a.zchunk;
-    const int zc1 = min(zc0 + a.zchunk, a.nz);
-
-    if (tid == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
     double acc[3 + KR_MAX_BOX];
 #pragma unroll
     for (int r = 0; r < 3 + KR_MAX_BOX; ++r) acc[r] = 0.0;
-    // does any (non all-grid) box output row intersect this CTA's tile and z-chunk? (usually not)
-    bool cta_box = false;
-    for (int r = 0; r < a.nbox; ++r)
-        if (!((a.all_mask >> r) & 1u) && a.box[r].lo[0] < x0 + TX && a.box[r].hi[0] > x0 &&
-            a.box[r].lo[1] < y0 + TY && a.box[r].hi[1] > y0 && a.box[r].lo[2] < a.zoff + zc1 &&
-            a.box[r].hi[2] > a.zoff + zc0)
-            cta_box = true;
-    // interior tiles (the forward ring inside the grid) skip all x/y masking
-    if (x0 + TX < a.mx && y0 + TY < a.my)
-        lz_march<TX, TY, S, INIT, true>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
-    else
-        lz_march<TX, TY, S, INIT, false>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
-
-    // fixed-order block reduction of (sum w^2, sum D, box rows)
-    __shared__ double red[8][3 + KR_MAX_BOX];
-    const int lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-    for (int r = 0; r < 3 + KR_MAX_BOX; ++r) {
-        if (r < 3 + a.nbox) {
-            double v = acc[r];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-            if (lane == 0) red[wid][r] = v;
-        }
-    }
-    __syncthreads();
-    if (tid < a.nqp) {
-        // partial layout: [0] sum w^2, [1] sum D, [2 + r] box row r (all-grid rows take sum w)
-        const int src = tid < 2 ? tid : (((a.all_mask >> (tid - 2)) & 1u) ? 2 : tid + 1);
-        double s = 0.0;
-        for (int w = 0; w < 8; ++w) s += red[w][src];
-        const int64_t blk = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
-        a.partials[blk * a.nqp + tid] = s;
-    }
-}
-
-// Local reduction of the per-CTA partials of one slab, plus sparse output rows gathered from the
-// freshly written vector. rankvec[0] = sum w^2, [1] = sum D, [2+r] = C_r w.
-__global__ void __launch_bounds__(256) lz_local_reduce(const double* partials, int64_t nblk, int nqp,
-                                                       const int32_t* box_slot, const double* box_val, int nbox,
-                                                       int n_out,
-                                                       const DVec* outs, SlabInfo si, int buf, int gather,
-                                                       int64_t mx, int64_t my, int64_t pitch,
-                                                       const LzScalars* sc, double* rankvec) {
-    if (sc->done) return;
-    __shared__ double red[256];
-    __shared__ double res[2 + KR_MAX_OUT];
-    const int tid = threadIdx.x;
-    for (int r = tid; r < 2 + n_out; r += 256) res[r] = 0.0;
-    __syncthreads();
-    auto block_sum = [&](double v) -> double {
-        red[tid] = v;
-        __syncthreads();
-        for (int o = 128; o > 0; o >>= 1) {
-            if (tid < o) red[tid] += red[tid + o];
-            __syncthreads();
-        }
-        double r = red[0];
-        __syncthreads();
-        return r;
-    };
-    for (int qi = 0; qi < nqp; ++qi) {
-        double v = 0.0;
-        for (int64_t b = tid; b < nblk; b += 256) v += partials[b * nqp + qi];
-        double s = block_sum(v);
+    // Persistent CTAs: work items (x-tile, y-tile, z-chunk) are dealt round-robin (fixed assignment,
+    // deterministic); consecutive items run concurrently, so neighbouring tiles share halo planes in L2.
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+        const int xt = item % a.gx, yt = (item / a.gx) % a.gy, zt = item / (a.gx * a.gy);
+        const int x0 = xt * TX, y0 = yt * TY;
+        const int zc0 = zt * a.zchunk;
+        const int zc1 = min(zc0 + a.zchunk, a.nz);
         if (tid == 0) {
-            if (qi < 2)
-                res[qi] = s;
-            else
-                res[2 + box_slot[qi - 2]] = s * box_val[qi - 2];
+#pragma unroll
+            for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        // does any (non all-grid) box output row intersect this tile and z-chunk? (usually not)
+        bool cta_box = false;
+        for (int r = 0; r < a.nbox; ++r)
+            if (!((a.all_mask >> r) & 1u) && a.box[r].lo[0] < x0 + TX && a.box[r].hi[0] > x0 &&
+                a.box[r].lo[1] < y0 + TY && a.box[r].hi[1] > y0 && a.box[r].lo[2] < a.zoff + zc1 &&
+                a.box[r].hi[2] > a.zoff + zc0)
+                cta_box = true;
+        // interior tiles (the forward ring inside the grid) skip all x/y masking
+        if (x0 + TX < a.mx && y0 + TY < a.my)
+            lz_march<TX, TY, S, INIT, true>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+        else
+            lz_march<TX, TY, S, INIT, false>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+        __syncthreads();  // every issued plane was consumed: the barriers can be recycled for the next item
+        if (tid == 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar[s])) : "memory");
         }
     }
-    if (gather) {
-        const double* u = si.u[buf];
-        const int64_t plane = my * pitch;
-        for (int r = 0; r < n_out; ++r) {
-            const DVec o = outs[r];
-            if (o.kind != KR_VEC_SPARSE) continue;
-            double v = 0.0;
-            for (int64_t e = tid; e < o.nnz; e += 256) {
-                const int64_t idx = o.idx[e];
-                const int64_t z = idx / (mx * my), rem = idx - z * mx * my;
-                const int64_t y = rem / mx, x = rem - y * mx;
-                if (z >= si.z0 && z < si.z1) v += o.val[e] * u[(z - si.z0 + 1) * plane + y * pitch + x];
-            }
-            double s = block_sum(v);
-            if (tid == 0) res[2 + r] = s;
-        }
-    }
-    __syncthreads();
-    for (int r = tid; r < 2 + n_out; r += 256) rankvec[r] = res[r];
+
+    __syncthreads();  // stage buffers are free: reuse them as reduction scratch
+    lz_epilogue(a, acc, reinterpret_cast<double*>(smem), a.plane);
 }
 
 // Scalar update after the (global) reduction: fixed-order sum over the R rank/slab vectors, then
 // beta_i, alpha_{i+1}, s_{i+1}, H and P entries, breakdown test.
-__global__ void lz_finalize(const double* rankvec, int R, int nq, int n_out, int step, int k, LzScalars* sc,
-                            double* H, double* P, double* beta0_out, double* hnext_out, int32_t* keff_out) {
-    if (threadIdx.x != 0 || sc->done) return;
+__device__ void lz_finalize_dev(const double* rankvec, int R, int nq, int n_out, int step, int k, LzScalars* sc,
+                                double* H, double* P, double* beta0_out, double* hnext_out, int32_t* keff_out) {
     double S[2 + KR_MAX_OUT];
     for (int q = 0; q < nq; ++q) S[q] = 0.0;
     for (int r = 0; r < R; ++r)
@@ -458,6 +411,199 @@ __global__ void lz_finalize(const double* rankvec, int R, int nq, int n_out, int
     sc->hmax = fmax(sc->hmax, fmax(b, fabs(an)));
     sc->k_eff = i + 1;
     *keff_out = i + 1;
+}
+
+__global__ void lz_finalize(const double* rankvec, int R, int nq, int n_out, int step, int k, LzScalars* sc,
+                            double* H, double* P, double* beta0_out, double* hnext_out, int32_t* keff_out) {
+    if (threadIdx.x != 0 || sc->done) return;
+    lz_finalize_dev(rankvec, R, nq, n_out, step, k, sc, H, P, beta0_out, hnext_out, keff_out);
+}
+
+// Per-CTA partial sums, quantity-major [nqp][nblk]: [0] sum w^2, [1] sum D, [2 + r] box row r (all-grid
+// rows take sum w). No fence or atomic: the CTA exits immediately; lz_reduce_kernel (next launch)
+// reduces them in a fixed order.
+__device__ void lz_epilogue(const StepArgs& a, const double* acc, double* red, int64_t plane_elems) {
+    (void)red;
+    (void)plane_elems;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __shared__ double wred[8][3 + KR_MAX_BOX];
+#pragma unroll
+    for (int r = 0; r < 3 + KR_MAX_BOX; ++r) {
+        if (r < 3 + a.nbox) {
+            double v = acc[r];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) wred[wid][r] = v;
+        }
+    }
+    __syncthreads();
+    if (tid < a.nqp) {
+        const int src = tid < 2 ? tid : (((a.all_mask >> (tid - 2)) & 1u) ? 2 : tid + 1);
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += wred[w][src];
+        const int64_t nblk = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+        const int64_t blk = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
+        a.partials[(int64_t)tid * nblk + blk] = s;
+    }
+}
+
+// One CTA: fixed-order reduction of a slab's partials (per-thread strided sums with nqp independent
+// loads in flight, warp trees, warps in order), sparse output rows gathered from the new vector, the
+// slab's vector [2 + n_out] written to rankvec, and — for a single slab on a single rank — the scalar
+// update. Same result for every run (no atomics).
+constexpr int RT = 512;
+__global__ void __launch_bounds__(RT) lz_reduce_kernel(const StepArgs a, int64_t nblk) {
+    if (a.sc->done) return;
+    __shared__ double red[KR_MAX_BOX + 2][RT / 32];
+    __shared__ double res[2 + KR_MAX_OUT];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nqp = a.nqp;
+    double v[2 + KR_MAX_BOX];
+#pragma unroll
+    for (int q = 0; q < 2 + KR_MAX_BOX; ++q) v[q] = 0.0;
+    for (int64_t b = tid; b < nblk; b += RT) {
+#pragma unroll
+        for (int q = 0; q < 2 + KR_MAX_BOX; ++q)
+            if (q < nqp) v[q] += a.partials[(int64_t)q * nblk + b];
+    }
+#pragma unroll
+    for (int q = 0; q < 2 + KR_MAX_BOX; ++q) {
+        if (q < nqp) {
+            double t = v[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+            if (lane == 0) red[q][wid] = t;
+        }
+    }
+    for (int r = tid; r < 2 + a.n_out; r += RT) res[r] = 0.0;
+    __syncthreads();
+    if (tid < nqp) {
+        double s = 0.0;
+        for (int w = 0; w < RT / 32; ++w) s += red[tid][w];
+        if (tid < 2)
+            res[tid] = s;
+        else
+            res[2 + a.box_slot[tid - 2]] = s * a.box_val[tid - 2];
+    }
+    __syncthreads();
+    if (a.gather_u) {  // sparse output rows from the freshly written vector (owned planes)
+        __shared__ double gred[RT / 32];
+        const int64_t mxy = (int64_t)a.mx * a.my;
+        for (int r = 0; r < a.n_out; ++r) {
+            const DVec o = a.outs[r];
+            if (o.kind != KR_VEC_SPARSE) continue;
+            double t = 0.0;
+            for (int64_t e = tid; e < o.nnz; e += RT) {
+                const int64_t idx = o.idx[e];
+                const int64_t z = idx / mxy, rem = idx - z * mxy;
+                const int64_t y = rem / a.mx, x = rem - y * a.mx;
+                const int64_t zl = z - a.zoff;
+                if (zl >= 0 && zl < a.nz) t += o.val[e] * a.gather_u[(zl + 1) * a.plane + y * a.pitch + x];
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
+            if (lane == 0) gred[wid] = t;
+            __syncthreads();
+            if (tid == 0) {
+                double s2 = 0.0;
+                for (int w = 0; w < RT / 32; ++w) s2 += gred[w];
+                res[2 + r] = s2;
+            }
+            __syncthreads();
+        }
+    }
+    for (int r = tid; r < 2 + a.n_out; r += RT) a.rankvec[r] = res[r];
+    __syncthreads();
+    if (tid == 0 && a.fin)
+        lz_finalize_dev(res, 1, 2 + a.n_out, a.n_out, a.step, a.k, a.scw, a.H, a.P, a.beta0_out, a.hnext_out,
+                        a.keff_out);
+}
+
+// Init pass for an analytic generator (KR_VEC_BOX / KR_VEC_ALL): writes u_1 = v over the slab buffer
+// (owned planes, plus the ghost/halo planes from the global description) and, in the same pass,
+// accumulates ||v||^2, -v^T A v (edge form) and the box-row projections C v (Alg. 4 lines 1-2,
+// P:782-783). One 8n-byte write instead of a fill (8n write) followed by a read pass (8n).
+// v = value * [x in X][y in Y][z in Z] with X, Y, Z the box ranges clipped to the grid (ALL = whole grid),
+// so membership is precomputed per axis.
+template <int TX, int TY>
+__global__ void __launch_bounds__(256) lz_fillinit_kernel(const StepArgs a) {
+    using G = Geo<TX, TY>;
+    if (a.sc->done) return;
+    double* red_s = nullptr;  // the epilogue needs no scratch
+    constexpr int RS = G::NT / TX;
+    const int tid = threadIdx.x;
+    const double cx = a.cx, cy = a.cy, cz = a.cz;
+    const DVec g = a.gen;
+    const bool all = g.kind == KR_VEC_ALL;
+    auto clip = [](int64_t v, int64_t lo, int64_t hi) { return (int)(v < lo ? lo : (v > hi ? hi : v)); };
+    const int lx = all ? 0 : clip(g.lo[0], 0, a.mx), hx = all ? a.mx : clip(g.hi[0], 0, a.mx);
+    const int ly = all ? 0 : clip(g.lo[1], 0, a.my), hy = all ? a.my : clip(g.hi[1], 0, a.my);
+    const int lz = all ? 0 : clip(g.lo[2], 0, a.mz), hz = all ? a.mz : clip(g.hi[2], 0, a.mz);
+    const double val = g.value;
+    double acc[3 + KR_MAX_BOX];
+#pragma unroll
+    for (int r = 0; r < 3 + KR_MAX_BOX; ++r) acc[r] = 0.0;
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+        const int xt = item % a.gx, yt = (item / a.gx) % a.gy, zt = item / (a.gx * a.gy);
+        const int x0 = xt * TX, y0 = yt * TY;
+        const int zc0 = zt * a.zchunk;
+        const int zc1 = min(zc0 + a.zchunk, a.nz);
+        const int x = tid % TX, ty = tid / TX, gx = x0 + x;
+        const bool fx0 = gx >= lx && gx < hx, fx1 = gx + 1 >= lx && gx + 1 < hx;
+        const double gex = gx == 0 ? cx : 0.0;
+        bool fy0[G::TS], fy1[G::TS], okc[G::TS];
+        uint32_t bm[G::TS];
+#pragma unroll
+        for (int m = 0; m < G::TS; ++m) {
+            const int gy = y0 + ty + m * RS;
+            fy0[m] = gy >= ly && gy < hy;
+            fy1[m] = gy + 1 >= ly && gy + 1 < hy;
+            okc[m] = gx < a.mx && gy < a.my;
+            uint32_t bb = 0;
+            for (int r = 0; r < a.nbox; ++r)
+                if (!((a.all_mask >> r) & 1u) && gx >= a.box[r].lo[0] && gx < a.box[r].hi[0] &&
+                    gy >= a.box[r].lo[1] && gy < a.box[r].hi[1])
+                    bb |= 1u << r;
+            bm[m] = bb;
+        }
+        double* optr = a.out + (int64_t)(y0 + ty) * a.pitch + gx;
+        const int64_t rowstep = (int64_t)RS * a.pitch;
+        const int qa = (zt == 0) ? -1 : zc0;
+        const int qb = (zc1 == a.nz) ? a.nz + 2 : zc1;  // exclusive
+        for (int q = qa; q < qb; ++q) {
+            const int gz = a.zoff + q;
+            const bool own = q >= zc0 && q < zc1;
+            const bool fz0 = gz >= lz && gz < hz, fz1 = gz + 1 >= lz && gz + 1 < hz;
+            const double gez = gex + (gz == 0 ? cz : 0.0);
+            uint32_t zmask = 0;
+            if (own)
+                for (int r = 0; r < a.nbox; ++r)
+                    if (!((a.all_mask >> r) & 1u) && gz >= a.box[r].lo[2] && gz < a.box[r].hi[2]) zmask |= 1u << r;
+            double* orow = optr + (int64_t)(q + 1) * a.plane;
+#pragma unroll
+            for (int m = 0; m < G::TS; ++m) {
+                if (!okc[m]) continue;
+                const double v = (fx0 && fy0[m] && fz0) ? val : 0.0;
+                orow[m * rowstep] = v;
+                if (!own) continue;
+                const double dx = ((fx1 && fy0[m] && fz0) ? val : 0.0) - v;
+                const double dy = ((fx0 && fy1[m] && fz0) ? val : 0.0) - v;
+                const double dz = ((fx0 && fy0[m] && fz1) ? val : 0.0) - v;
+                const double ge = gez + ((y0 + ty + m * RS) == 0 ? cy : 0.0);
+                const double v2 = v * v;
+                acc[0] += v2;
+                acc[1] = fma(cx, dx * dx, fma(cy, dy * dy, fma(cz, dz * dz, fma(ge, v2, acc[1]))));
+                acc[2] += v;
+                const uint32_t mk = bm[m] & zmask;
+                if (mk) {
+#pragma unroll
+                    for (int r = 0; r < KR_MAX_BOX; ++r)
+                        if ((mk >> r) & 1u) acc[3 + r] += v;
+                }
+            }
+        }
+    }
+    lz_epilogue(a, acc, red_s, a.plane);
 }
 
 __global__ void lz_reset(LzScalars* sc) {
@@ -545,10 +691,10 @@ int kr_lz_occupancy(int TX, int TY) {
 
 void kr_lz_prepare(kr_handle* h) { (void)kr_lz_occupancy(h->TX, h->TY); }
 
-template <int TX, int TY>
-static void step_launch_t(kr_handle* h, Slab& sl, LzScalars* sc, int cur, int prev, int nxt, int step, bool init,
-                          bool write) {
+static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf) {
     StepArgs a{};
+    LzScalars* sc = h->d_sc + dl;
+    const int k = h->k;
     a.out = sl.u[nxt];
     a.pitch = h->pitch;
     a.plane = h->pitch * h->my;
@@ -558,10 +704,14 @@ static void step_launch_t(kr_handle* h, Slab& sl, LzScalars* sc, int cur, int pr
     a.nz = (int)sl.nz;
     a.zoff = (int)sl.z0;
     a.zchunk = sl.zchunk;
+    a.gx = sl.gx;
+    a.gy = sl.gy;
+    a.nitems = (int)sl.nitems;
     a.cx = h->cx;
     a.cy = h->cy;
     a.cz = h->cz;
     a.sc = sc;
+    a.scw = sc;
     a.step = step;
     a.has_prev = (!init && step > 1) ? 1 : 0;
     a.write_out = write ? 1 : 0;
@@ -575,26 +725,64 @@ static void step_launch_t(kr_handle* h, Slab& sl, LzScalars* sc, int cur, int pr
         if (b.lo[0] <= 0 && b.lo[1] <= 0 && b.lo[2] <= 0 && b.hi[0] >= h->mx && b.hi[1] >= h->my && b.hi[2] >= h->mz)
             a.all_mask |= 1u << r;
     }
+    a.counter = sl.counter;
+    const int S = (int)h->slabs.size();
+    const int sidx = (int)(&sl - &h->slabs[0]);
+    a.rankvec = h->d_rankvec + ((size_t)h->rank * S + sidx) * h->nq;
+    a.box_slot = h->d_box_slot;
+    a.box_val = h->d_box_val;
+    a.outs = h->d_outs;
+    bool has_sparse = false;
+    for (const DVec& o : h->outs_h) has_sparse |= o.kind == KR_VEC_SPARSE;
+    a.gather_u = (gather_buf >= 0 && has_sparse) ? sl.u[gather_buf] : nullptr;
+    a.n_out = h->n_out;
+    a.fin = (S == 1 && h->world == 1) ? 1 : 0;
+    a.k = k;
+    a.H = h->d_H + (size_t)dl * (k + 1) * k;
+    a.P = h->d_P + (size_t)dl * h->n_out * k;
+    a.beta0_out = h->d_beta0 + dl;
+    a.hnext_out = h->d_hnext + dl;
+    a.keff_out = h->d_keff + dl;
+    return a;
+}
+
+template <int TX, int TY>
+static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int nxt, int step, bool init,
+                          bool write, bool fillinit) {
     const size_t smem = step_smem_bytes<TX, TY, Stages<TX, TY>::S>();
-    const CUtensorMap& tc = sl.tmC[cur];
-    const CUtensorMap& tp = sl.tmP[prev < 0 ? cur : prev];
-    if (init) {
-        lz_step_kernel<TX, TY, Stages<TX, TY>::S, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+    if (fillinit) {
+        StepArgs a = make_args(h, sl, dl, cur, 0, true, false, cur);
+        a.gen = h->dirs_h[h->my_dirs[dl]];
+        lz_fillinit_kernel<TX, TY><<<sl.grid, 256, 0, h->stream>>>(a);
     } else {
-        lz_step_kernel<TX, TY, Stages<TX, TY>::S, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+        StepArgs a = make_args(h, sl, dl, nxt, step, init, write, init ? cur : (write ? nxt : -1));
+        const CUtensorMap& tc = sl.tmC[cur];
+        const CUtensorMap& tp = sl.tmP[prev < 0 ? cur : prev];
+        if (init)
+            lz_step_kernel<TX, TY, Stages<TX, TY>::S, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+        else
+            lz_step_kernel<TX, TY, Stages<TX, TY>::S, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
     }
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }
 
-static void step_launch(kr_handle* h, Slab& sl, LzScalars* sc, int cur, int prev, int nxt, int step, bool init,
-                        bool write) {
+// The slab reduction (+ scalar update when fin) after a step / init launch on slab sl.
+static void reduce_launch(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf) {
+    StepArgs a = make_args(h, sl, dl, nxt, step, init, write, gather_buf);
+    lz_reduce_kernel<<<1, RT, 0, h->stream>>>(a, sl.nblk);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+}
+
+static void step_launch(kr_handle* h, Slab& sl, int dl, int cur, int prev, int nxt, int step, bool init, bool write,
+                        bool fillinit = false) {
     if (h->TX == 64 && h->TY == 16)
-        step_launch_t<64, 16>(h, sl, sc, cur, prev, nxt, step, init, write);
+        step_launch_t<64, 16>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
     else if (h->TX == 64 && h->TY == 8)
-        step_launch_t<64, 8>(h, sl, sc, cur, prev, nxt, step, init, write);
+        step_launch_t<64, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
     else if (h->TX == 32 && h->TY == 8)
-        step_launch_t<32, 8>(h, sl, sc, cur, prev, nxt, step, init, write);
+        step_launch_t<32, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
     else
         KR_THROW(KR_EINVAL, "unsupported tile");
 }
@@ -617,27 +805,14 @@ static void halo_exchange_virtual(kr_handle* h, int buf) {
     }
 }
 
-// Reduction + scalar update for one step (all slabs of this process, then across ranks).
-static void reduce_and_finalize(kr_handle* h, int dl, int buf, int step, bool gather) {
+// After the per-slab step kernels (whose last CTA wrote each slab's reduced vector): combine slabs /
+// ranks and update the scalars — unless a single slab on a single rank already did it in-kernel.
+static void combine_and_finalize(kr_handle* h, int dl, int step) {
     const int S = (int)h->slabs.size();
-    int32_t* box_slot = h->d_box_slot;
+    if (S == 1 && h->world == 1) return;
     LzScalars* sc = h->d_sc + dl;
     const int R = S * h->world;
     double* rv_local = h->d_rankvec + (size_t)h->rank * S * h->nq;
-    for (int s = 0; s < S; ++s) {
-        Slab& sl = h->slabs[s];
-        SlabInfo si;
-        si.z0 = sl.z0;
-        si.z1 = sl.z1;
-        si.nz = sl.nz;
-        for (int b = 0; b < 3; ++b) si.u[b] = sl.u[b];
-        lz_local_reduce<<<1, 256, 0, h->stream>>>(sl.partials, sl.nblk, h->nqp, box_slot, h->d_box_val,
-                                                  (int)h->boxes.size(),
-                                                  h->n_out, h->d_outs, si, buf, gather ? 1 : 0, h->mx, h->my,
-                                                  h->pitch, sc, rv_local + (size_t)s * h->nq);
-        KR_CUDA(cudaGetLastError());
-        h->launches++;
-    }
     if (h->world > 1) kr_nccl_allgather(h->comm, rv_local, h->d_rankvec, (size_t)S * h->nq, h->stream);
     const int k = h->k;
     lz_finalize<<<1, 32, 0, h->stream>>>(h->d_rankvec, R, h->nq, h->n_out, step, k, sc,
@@ -654,27 +829,34 @@ void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events) {
     lz_reset<<<1, 32, 0, h->stream>>>(sc);
     KR_CUDA(cudaGetLastError());
     h->launches++;
-    // u_1 = v_d, materialised on every slab including halo planes (analytic: no exchange needed)
-    for (auto& sl : h->slabs) {
-        kr_fill_grid(h->stream, sl.u[0], h->mx, h->my, h->pitch, sl.nz + 3, sl.z0 - 1, h->mz, h->dirs_h[d],
-                     &h->launches);
+    // u_1 = v_d on every slab including halo planes (analytic: no exchange needed); init pass: beta0,
+    // alpha_1, P_{.,1}. Box/all generators: one fused fill+init pass; sparse: fill then the init pass.
+    const DVec& g = h->dirs_h[d];
+    if (g.kind == KR_VEC_BOX || g.kind == KR_VEC_ALL) {
+        for (auto& sl : h->slabs) step_launch(h, sl, dl, 0, -1, 0, 0, true, false, true);
+    } else {
+        for (auto& sl : h->slabs)
+            kr_fill_grid(h->stream, sl.u[0], h->mx, h->my, h->pitch, sl.nz + 3, sl.z0 - 1, h->mz, g, &h->launches);
+        for (auto& sl : h->slabs) step_launch(h, sl, dl, 0, -1, 0, 0, true, false);
     }
-    // init pass: beta0, alpha_1, P_{.,1}
-    for (auto& sl : h->slabs) step_launch(h, sl, sc, 0, -1, 0, 0, true, false);
-    reduce_and_finalize(h, dl, 0, 0, true);
+    for (auto& sl : h->slabs) reduce_launch(h, sl, dl, 0, 0, true, false, 0);
+    combine_and_finalize(h, dl, 0);
     const int k = h->k;
     int evi = 0;
     for (int i = 1; i <= k; ++i) {
         const int cur = (i - 1) % 3, prev = (i >= 2) ? (i - 2) % 3 : -1, nxt = i % 3;
         const bool write = i < k;
-        if (capture_events && dl == 0) KR_CUDA(cudaEventRecordWithFlags(h->ev[evi], h->stream, cudaEventRecordExternal));
-        for (auto& sl : h->slabs) step_launch(h, sl, sc, cur, prev, nxt, i, false, write);
-        if (capture_events && dl == 0) KR_CUDA(cudaEventRecordWithFlags(h->ev[evi + 1], h->stream, cudaEventRecordExternal));
+        if (capture_events && dl == 0)
+            KR_CUDA(cudaEventRecordWithFlags(h->ev[evi], h->stream, cudaEventRecordExternal));
+        for (auto& sl : h->slabs) step_launch(h, sl, dl, cur, prev, nxt, i, false, write);
+        if (capture_events && dl == 0)
+            KR_CUDA(cudaEventRecordWithFlags(h->ev[evi + 1], h->stream, cudaEventRecordExternal));
         evi += 2;
+        for (auto& sl : h->slabs) reduce_launch(h, sl, dl, nxt, i, false, write, write ? nxt : -1);
         if (write) {
             if (h->slabs.size() > 1) halo_exchange_virtual(h, nxt);
             if (h->world > 1) kr_nccl_halo(h->comm, h, nxt, h->stream);
         }
-        reduce_and_finalize(h, dl, nxt, i, write);
+        combine_and_finalize(h, dl, i);
     }
 }
