@@ -187,6 +187,21 @@ void krylov_comm_destroy(kr_comm* c);
  * fewer than 2 planes (the depth-2 halo comes from one neighbour). */
 kr_status krylov_zslab_range(int64_t mz, int32_t world, int32_t rank, int64_t* z0, int64_t* z1);
 
+/* One halo transfer of the z-slab decomposition (host logic, no GPU). Buffer planes of a rank holding
+ * nz owned planes: 0 = halo below (global z0-1), 1..nz = owned, nz+1 and nz+2 = halo above (z1, z1+1).
+ * The fused step needs u_i at depth 2 above and depth 1 below, u_{i-1} at depth 1 above. */
+typedef struct {
+    int32_t is_send;   /* 1 = send my planes [plane, plane+nplanes) to peer; 0 = receive into them */
+    int32_t peer;      /* neighbouring rank                                                          */
+    int64_t plane;     /* first buffer plane (of this rank's buffer)                                  */
+    int64_t nplanes;   /* 2 towards the lower neighbour, 1 towards the upper neighbour                */
+} kr_halo_op;
+
+/* The exchange schedule of rank `rank` after each Krylov step, in issue order (sends and receives
+ * paired as one NCCL group): to rank-1 send planes [1,3) and receive into plane 0; to rank+1 send plane
+ * nz and receive into [nz+1, nz+3). ops must hold 4 entries; *n_ops receives the count. */
+kr_status krylov_zslab_halo_plan(int64_t mz, int32_t world, int32_t rank, kr_halo_op* ops, int32_t* n_ops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,10 @@ class kr_dir_stats(C.Structure):
     _fields_ = [("k_eff", C.c_int32), ("beta0", C.c_double), ("h_next", C.c_double), ("lemma1_bound", C.c_double)]
 
 
+class kr_halo_op(C.Structure):
+    _fields_ = [("is_send", C.c_int32), ("peer", C.c_int32), ("plane", C.c_int64), ("nplanes", C.c_int64)]
+
+
 class kr_cex(C.Structure):
     _fields_ = [("found", C.c_int32), ("step", C.c_int64), ("time", C.c_double), ("row", C.c_int32),
                 ("y", C.c_double)]
@@ -51,7 +55,7 @@ class kr_cex(C.Structure):
 EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "krylov_check_box",
            "krylov_reach_destroy", "krylov_last_error", "krylov_launch_count", "krylov_last_timing",
            "krylov_comm_unique_id", "krylov_comm_create", "krylov_comm_destroy", "krylov_zslab_range",
-           "krylov_krylov_data", "krylov_transfer_bytes"]
+           "krylov_krylov_data", "krylov_transfer_bytes", "krylov_zslab_halo_plan"]
 
 _lib = None
 
@@ -82,6 +86,8 @@ def lib():
     L.krylov_comm_destroy.argtypes = [vp]
     L.krylov_comm_destroy.restype = None
     L.krylov_krylov_data.argtypes = [vp, C.c_int32, vp, vp]
+    L.krylov_zslab_halo_plan.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(kr_halo_op),
+                                         C.POINTER(C.c_int32)]
     L.krylov_transfer_bytes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.krylov_zslab_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     for name in EXPORTS:

@@ -203,6 +203,14 @@ def krylov_zslab_range(mz, world, rank):
     return z0.value, z1.value
 
 
+def krylov_zslab_halo_plan(mz, world, rank):
+    """Halo schedule of a z-slab rank: list of (is_send, peer, first_buffer_plane, nplanes)."""
+    ops = (A.kr_halo_op * 4)()
+    n = C.c_int32()
+    A.check(A.lib().krylov_zslab_halo_plan(int(mz), int(world), int(rank), ops, C.byref(n)))
+    return [(bool(o.is_send), int(o.peer), int(o.plane), int(o.nplanes)) for o in ops[:n.value]]
+
+
 class KrComm:
     """NCCL communicator for one process per GPU. The 128-byte ncclUniqueId is produced by rank 0
     (krylov_comm_unique_id) and broadcast with torch.distributed (any backend)."""

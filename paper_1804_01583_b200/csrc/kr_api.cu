@@ -339,6 +339,28 @@ kr_status krylov_zslab_range(int64_t mz, int32_t world, int32_t rank, int64_t* z
     return KR_OK;
 }
 
+kr_status krylov_zslab_halo_plan(int64_t mz, int32_t world, int32_t rank, kr_halo_op* ops, int32_t* n_ops) {
+    if (!ops || !n_ops) {
+        kr_set_error("krylov_zslab_halo_plan: NULL output");
+        return KR_EINVAL;
+    }
+    int64_t z0, z1;
+    const kr_status st = krylov_zslab_range(mz, world, rank, &z0, &z1);
+    if (st != KR_OK) return st;
+    const int64_t nz = z1 - z0;
+    int n = 0;
+    if (rank > 0) {  // lower neighbour: it needs my first two planes (its depth-2 upper halo)
+        ops[n++] = kr_halo_op{1, rank - 1, 1, 2};
+        ops[n++] = kr_halo_op{0, rank - 1, 0, 1};
+    }
+    if (rank + 1 < world) {  // upper neighbour: it needs my last plane (its depth-1 lower halo)
+        ops[n++] = kr_halo_op{1, rank + 1, nz, 1};
+        ops[n++] = kr_halo_op{0, rank + 1, nz + 1, 2};
+    }
+    *n_ops = n;
+    return KR_OK;
+}
+
 kr_status krylov_workspace_bytes(const kr_problem* p, size_t* bytes) {
     return guarded([&] {
         validate(p);

@@ -53,15 +53,16 @@ void kr_nccl_halo(kr_comm* c, kr_handle* h, int buf, cudaStream_t s) {
     ncclComm_t comm = reinterpret_cast<ncclComm_t>(c->nccl);
     Slab& sl = h->slabs[0];
     const size_t plane = (size_t)h->pitch * h->my;
-    const int r = c->rank, W = c->world;
+    kr_halo_op ops[4];
+    int32_t n = 0;
+    if (krylov_zslab_halo_plan(h->mz, c->world, c->rank, ops, &n) != KR_OK) KR_THROW(KR_EINVAL, "halo plan");
     KR_NCCL(ncclGroupStart());
-    if (r > 0) {
-        KR_NCCL(ncclSend(sl.u[buf] + 1 * plane, 2 * plane, ncclDouble, r - 1, comm, s));
-        KR_NCCL(ncclRecv(sl.u[buf], plane, ncclDouble, r - 1, comm, s));
-    }
-    if (r + 1 < W) {
-        KR_NCCL(ncclSend(sl.u[buf] + sl.nz * plane, plane, ncclDouble, r + 1, comm, s));
-        KR_NCCL(ncclRecv(sl.u[buf] + (sl.nz + 1) * plane, 2 * plane, ncclDouble, r + 1, comm, s));
+    for (int i = 0; i < n; ++i) {
+        double* p = sl.u[buf] + ops[i].plane * plane;
+        if (ops[i].is_send)
+            KR_NCCL(ncclSend(p, ops[i].nplanes * plane, ncclDouble, ops[i].peer, comm, s));
+        else
+            KR_NCCL(ncclRecv(p, ops[i].nplanes * plane, ncclDouble, ops[i].peer, comm, s));
     }
     KR_NCCL(ncclGroupEnd());
 }

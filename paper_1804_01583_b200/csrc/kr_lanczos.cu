@@ -788,19 +788,27 @@ static void step_launch(kr_handle* h, Slab& sl, int dl, int cur, int prev, int n
 }
 
 static void halo_exchange_virtual(kr_handle* h, int buf) {
-    const size_t pb = (size_t)h->pitch * h->my * sizeof(double);
+    // the same schedule as the NCCL transport (krylov_zslab_halo_plan), executed as device copies: each
+    // receive of slab s is served by the matching send of its peer
+    const size_t plane = (size_t)h->pitch * h->my;
     const int S = (int)h->slabs.size();
     for (int s = 0; s < S; ++s) {
-        Slab& me = h->slabs[s];
-        if (s > 0) {  // my first two owned planes -> lower neighbour's upper halo
-            Slab& lo = h->slabs[s - 1];
-            KR_CUDA(cudaMemcpyAsync(lo.u[buf] + (lo.nz + 1) * h->pitch * h->my, me.u[buf] + 1 * h->pitch * h->my,
-                                    2 * pb, cudaMemcpyDeviceToDevice, h->stream));
-        }
-        if (s + 1 < S) {  // my last owned plane -> upper neighbour's lower halo
-            Slab& hi = h->slabs[s + 1];
-            KR_CUDA(cudaMemcpyAsync(hi.u[buf], me.u[buf] + me.nz * h->pitch * h->my, pb, cudaMemcpyDeviceToDevice,
-                                    h->stream));
+        kr_halo_op ops[4];
+        int32_t n = 0;
+        if (krylov_zslab_halo_plan(h->mz, S, s, ops, &n) != KR_OK) KR_THROW(KR_EINVAL, "halo plan");
+        for (int i = 0; i < n; ++i) {
+            if (ops[i].is_send) continue;
+            const Slab& peer = h->slabs[ops[i].peer];
+            kr_halo_op pops[4];
+            int32_t pn = 0;
+            krylov_zslab_halo_plan(h->mz, S, ops[i].peer, pops, &pn);
+            for (int j = 0; j < pn; ++j)
+                if (pops[j].is_send && pops[j].peer == s) {
+                    if (pops[j].nplanes != ops[i].nplanes) KR_THROW(KR_EINVAL, "halo plan mismatch");
+                    KR_CUDA(cudaMemcpyAsync(h->slabs[s].u[buf] + ops[i].plane * plane, peer.u[buf] + pops[j].plane * plane,
+                                            ops[i].nplanes * plane * sizeof(double), cudaMemcpyDeviceToDevice,
+                                            h->stream));
+                }
         }
     }
 }
