@@ -262,10 +262,10 @@ Sizes plan(const kr_problem* p, int rank, int world) {
                 KR_THROW(KR_EINVAL, "each slab needs >= 2 planes");
             b += (size_t)3 * (size_t)(z1 - z0 + 3) * (size_t)p->my * (size_t)pitch * sizeof(double);
         }
-        s.state_bytes = b;
+        s.state_bytes = b + (size_t)3 * 256 * (size_t)nsl;  // + 256-byte alignment of each carved buffer
     } else {
         if (s.N > 27648) KR_THROW(KR_EDIM, "the stored-basis (Arnoldi) path supports operator dimension <= 27648");
-        s.state_bytes = (size_t)s.ndl * (size_t)(p->k + 2) * (size_t)s.N * sizeof(double);
+        s.state_bytes = (size_t)s.ndl * (size_t)(p->k + 2) * (size_t)s.N * sizeof(double) + 2 * 256;
     }
     return s;
 }

@@ -65,11 +65,11 @@ def test_workspace_bytes_host_only():
     p = W.config5()
     b = krylov_workspace_bytes(p)
     pitch = 1000
-    assert b == 3 * (1000 + 3) * 1000 * pitch * 8  # 3 vectors + ghost planes (Eq. 6's 3n)
+    assert b == 3 * (1000 + 3) * 1000 * pitch * 8 + 3 * 256  # 3 vectors + ghost planes (Eq. 6's 3n) + alignment
     p4 = W.heat(401, 40, 40)
-    assert krylov_workspace_bytes(p4) == 3 * (401 + 3) * 401 * 402 * 8  # pitch padded to even
+    assert krylov_workspace_bytes(p4) == 3 * (401 + 3) * 401 * 402 * 8 + 3 * 256  # pitch padded to even
     q = W.config2()
-    assert krylov_workspace_bytes(q) == 21 * 42 * 20001 * 8  # Arnoldi stores k+1 vectors (+W) per direction
+    assert krylov_workspace_bytes(q) == 21 * 42 * 20001 * 8 + 512  # Arnoldi stores k+1 vectors (+W) per direction
 
 
 @pytest.mark.parametrize("mutate,code", [
