@@ -58,6 +58,12 @@ typedef struct {
     const int32_t* col_idx;
     const double* val;
     const double* b; /* NULL = no affine term */
+    /* stencil boundary per face (x-, x+, y-, y+, z-, z+): 0 Dirichlet (zero ghost, BASELINE configs),
+       1 insulated (the missing neighbour is dropped), 2 insulated + exchange: diagonal -= gamma[f]
+       (units of A). The paper's heat benchmark (SURVEY A1/A2 reconstruction): all faces
+       insulated except x = 1 with exchange 0.5, A = 0.01 (L - (0.5/h) e_{x=m-1}). */
+    int32_t bc[6];
+    double gamma[6];
 } oracle_op;
 
 int64_t oracle_op_dim(const oracle_op* A) {
@@ -87,6 +93,39 @@ void oracle_stencil_apply(int64_t mx, int64_t my, int64_t mz, double alpha, cons
             }
 }
 
+/* General boundaries: (Au)_c = alpha sum_axes sum_{s=+-} t_s / h_a^2 - sum_{faces f at c} gamma_f u_c with
+ * t_s = u_{c+s} - u_c if the neighbour exists, -u_c on a Dirichlet face, 0 on an insulated face. */
+void oracle_stencil_apply_bc(int64_t mx, int64_t my, int64_t mz, double alpha, const int32_t* bc, const double* gamma,
+                             const double* u, double* y) {
+    const int64_t m[3] = {mx, my, mz};
+    const int64_t st[3] = {1, mx, mx * my};
+    double ih2[3];
+    for (int a = 0; a < 3; ++a) ih2[a] = (double)(m[a] + 1) * (double)(m[a] + 1);
+    for (int64_t z = 0; z < mz; ++z)
+        for (int64_t yy = 0; yy < my; ++yy)
+            for (int64_t x = 0; x < mx; ++x) {
+                const int64_t c = x + mx * (yy + my * z);
+                const int64_t pos[3] = {x, yy, z};
+                const double uc = u[c];
+                double acc = 0.0, diag = 0.0;
+                for (int a = 0; a < 3; ++a) {
+                    double t = 0.0;
+                    for (int sgn = 0; sgn < 2; ++sgn) {
+                        const int face = 2 * a + sgn;
+                        const int has = sgn == 0 ? pos[a] > 0 : pos[a] < m[a] - 1;
+                        if (has)
+                            t += u[c + (sgn == 0 ? -st[a] : st[a])] - uc;
+                        else if (bc[face] == 0)
+                            t += -uc;
+                        else if (bc[face] == 2)
+                            diag += gamma[face];
+                    }
+                    acc += t * ih2[a];
+                }
+                y[c] = alpha * acc - diag * uc;
+            }
+}
+
 void oracle_csr_apply(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
                       const double* b, const double* x, double* y) {
     for (int64_t r = 0; r < n; ++r) {
@@ -99,8 +138,12 @@ void oracle_csr_apply(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
 }
 
 void oracle_op_apply(const oracle_op* A, const double* x, double* y) {
-    if (A->op == 0)
+    int dirichlet = 1;
+    for (int f = 0; f < 6; ++f) dirichlet &= A->bc[f] == 0;
+    if (A->op == 0 && dirichlet)
         oracle_stencil_apply(A->mx, A->my, A->mz, A->alpha, x, y);
+    else if (A->op == 0)
+        oracle_stencil_apply_bc(A->mx, A->my, A->mz, A->alpha, A->bc, A->gamma, x, y);
     else
         oracle_csr_apply(A->n, A->row_ptr, A->col_idx, A->val, A->b, x, y);
 }

@@ -197,7 +197,38 @@ def random_csr(n, nnz_per_row, seed, symmetric=False, scale=1.0):
     return row_ptr, np.concatenate(cols_l).astype(np.int32), np.concatenate(vals_l), dense
 
 
-CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5}
+BC_DIRICHLET, BC_NEUMANN, BC_ROBIN = 0, 1, 2
+
+
+def heat_paper(m, eps=1e-6, k_max=8000, n_steps=1000, step=0.02):
+    """The paper's own 3D heat benchmark (§5.3): unit cube, all faces
+    insulated except x = 1, which exchanges heat with constant 0.5; heated region
+    x in [0,0.4], y in [0,0.2], z in [0,0.1] at [0.9,1.1], rest 0; u_t = alpha^2 Lap u with
+    'alpha = 0.01' (P:972-973). Reading (SURVEY A1/A2, DESIGN R18): grid points x_i = (i+1) h, h = 1/(m+1);
+    insulated faces drop the missing neighbour; the x = 1 face adds -0.5/h to the diagonal; the whole
+    operator is scaled by 0.01 (this reproduces ||A 50|| = 32771611 of P:674 to 3e-8). Heated cells:
+    (i+1) h <= bound. Output: center point. T = 20, delta = 0.02. Adaptive k with
+    Lemma 1 to eps = 1e-6."""
+    h = 1.0 / (m + 1)
+    n_x = int(math.floor(0.4 * (m + 1) + 1e-9))
+    n_y = int(math.floor(0.2 * (m + 1) + 1e-9))
+    n_z = int(math.floor(0.1 * (m + 1) + 1e-9))
+    c = center_index(m)
+    gamma = 0.01 * 0.5 / h
+    return {
+        "name": f"heat_paper{m}", "op": "stencil", "mx": m, "my": m, "mz": m, "alpha": 0.01,
+        "bc": [BC_NEUMANN, BC_ROBIN, BC_NEUMANN, BC_NEUMANN, BC_NEUMANN, BC_NEUMANN],
+        "gamma": [0.0, gamma, 0.0, 0.0, 0.0, 0.0],
+        "gens": [box((0, 0, 0), (n_x, n_y, n_z), 1.0)],
+        "z_lo": np.array([0.9]), "z_hi": np.array([1.1]),
+        "center": None, "b": None, "outs": [point(c, c, c), allv(1.0)],
+        "step": float(step), "n_steps": int(n_steps), "k": int(k_max), "method": "lanczos",
+        "eps": float(eps), "k_max": int(k_max), "thresholds": [],
+    }
+
+
+CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5,
+           "P100": lambda: heat_paper(100), "P1000": lambda: heat_paper(1000)}
 
 
 def n_state(p):
