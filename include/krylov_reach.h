@@ -49,6 +49,15 @@ typedef enum { KR_AUTO = 0, KR_ARNOLDI = 1, KR_LANCZOS = 2 } kr_method;
 typedef enum { KR_PART_NONE = 0, KR_PART_ZSLAB = 1, KR_PART_DIRS = 2 } kr_partition;
 typedef enum { KR_GE = 0, KR_LE = 1, KR_EQ = 2, KR_NONE = 3 } kr_sense;
 typedef enum { KR_VEC_SPARSE = 0, KR_VEC_BOX = 1, KR_VEC_ALL = 2 } kr_vec_kind;
+/* Stencil boundary condition of one grid face (the paper's heat model, §5.3: all faces insulated
+ * except x = 1, which exchanges heat with constant 0.5; SURVEY A1/A2 reconstruction, DESIGN R18):
+ *  KR_BC_DIRICHLET: zero ghost value beyond the face (BASELINE configs; A = alpha L_h).
+ *  KR_BC_INSULATED: the missing neighbour is dropped (zero flux): a face cell's diagonal is -(#neighbours) c_a.
+ *  KR_BC_ROBIN:     insulated plus exchange with a zero ambient: the face cell's diagonal also gets -gamma
+ *                   (gamma in units of A, e.g. 0.01 * 0.5 / h for the paper's x = 1 face).             */
+typedef enum { KR_BC_DIRICHLET = 0, KR_BC_INSULATED = 1, KR_BC_ROBIN = 2 } kr_bc;
+#define KR_K_MAX_FIXED_PADE 64   /* fixed k up to this uses per-step Pade-13 exponentials            */
+#define KR_K_MAX 16384           /* Lanczos (stencil) Krylov dimension cap; Arnoldi stays <= 64     */
 
 /* An n-vector given compactly: a generator column of E, the center c, or an output row of C
  * (P:447). Linear index of stencil cell (x,y,z) is x + mx*(y + my*z) (x fastest).
@@ -92,8 +101,21 @@ typedef struct {
     double step;
     int64_t n_steps;
     /* Krylov iteration. */
-    int32_t k;                  /* Krylov dimension (max; k_eff < k on breakdown), 1..64     */
+    int32_t k;                  /* Krylov dimension (max; k_eff < k on breakdown). Arnoldi and
+                                   CSR: 1..64. Stencil Lanczos: 1..KR_K_MAX (k > 64 or eps > 0 use the
+                                   large-k exponential route, see krylov_project)                         */
     int32_t method;             /* kr_method. AUTO: Lanczos for STENCIL7 or exactly symmetric CSR (b=NULL) */
+    /* Adaptive Krylov dimension, Alg. 2/4: eps > 0 runs the stencil Lanczos with
+       error control — the Lemma 1 bound (unit start vector, tau = T, trapezoid on the t_j grid)
+       is evaluated at the checkpoints k = 4, ceil(1.1 k), ... (fp64) and the first checkpoint
+       whose bound is < eps is accepted; `k` is then the maximum (k_max). An exact breakdown before k_max
+       is accepted with bound 0. If no checkpoint up to k_max meets eps, the k_max result is returned and
+       kr_dir_stats.lemma1_bound reports its (too large) bound. eps = 0: fixed k. Stencil Lanczos only.  */
+    double eps;
+    /* Stencil boundary conditions per face, order x-, x+, y-, y+, z-, z+ (kr_bc; all zero = Dirichlet,
+       the BASELINE configs) and the Robin exchange coefficients (used where bc = KR_BC_ROBIN, >= 0).   */
+    int32_t bc[6];
+    double gamma[6];
     /* Partitioning. */
     int32_t part;               /* kr_partition. ZSLAB: STENCIL7 + LANCZOS only; DIRS: any             */
     int32_t virtual_slabs;      /* ZSLAB without a comm: emulate P = virtual_slabs slabs in this process
@@ -170,10 +192,26 @@ kr_status krylov_transfer_bytes(const kr_handle* h, int64_t* h2d, int64_t* d2h);
 kr_status krylov_last_timing(const kr_handle* h, double* iter_ms, double* step_kernel_ms_mean,
                              int64_t* step_kernel_launches, double* step_kernel_bytes);
 
+/* Device time in ms spent by the last krylov_project in the large-k exponential route (all checkpoint
+ * evaluations: e^{H delta} by scaling and squaring, the time march, projection and Lemma 1 bound;
+ * CUDA events on the library stream) and the number of evaluations. 0 / 0 on the small-k route.    */
+kr_status krylov_last_timing_large(const kr_handle* h, double* expm_ms, int32_t* n_evals);
+
 /* Copy direction `dir`'s Krylov data to the host: H [(k+1)][k] row-major (the (k+1) x k Hessenberg
  * of Alg. 1 / tridiagonal of Alg. 3, entries beyond k_eff are 0) and P = C V [n_out][k] (Alg. 4).
  * Either pointer may be NULL. KR_EDIM if `dir` is not handled by this rank. Requires krylov_project. */
 kr_status krylov_krylov_data(const kr_handle* h, int32_t dir, double* H, double* P);
+
+/* Lanczos tridiagonal of direction `dir` (Alg. 3/4 keep H as 3 arrays, Eq. 6): alpha[i] =
+ * H_{i+1,i+1}, beta[i] = H_{i+2,i+1} for i < k_eff (beta[k_eff-1] = h_{k_eff+1,k_eff}). HOST buffers of
+ * `cap` doubles, either may be NULL; *k_eff receives k_eff. Stencil Lanczos path only (else KR_EINVAL). */
+kr_status krylov_tridiag(const kr_handle* h, int32_t dir, double* alpha, double* beta, int32_t cap, int32_t* k_eff);
+
+/* Adaptive error control trace of direction `dir` (eps > 0): the checkpoints evaluated, in order, with
+ * the Lemma 1 bound of each (unit start vector). HOST buffers of `cap` entries; *n receives
+ * the number of checkpoints evaluated (the last one evaluated is the accepted one unless breakdown).   */
+kr_status krylov_adaptive_checks(const kr_handle* h, int32_t dir, int32_t* ks, double* bounds, int32_t cap,
+                                 int32_t* n);
 
 /* ---- multi-GPU plumbing (one process per GPU) -------------------------------------------------- */
 /* Rank 0 calls krylov_comm_unique_id (128 bytes out), the caller broadcasts it (torch.distributed),

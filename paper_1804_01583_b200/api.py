@@ -28,6 +28,10 @@ class _Marshal:
             p.op = A.KR_OP_STENCIL7
             p.mx, p.my, p.mz = int(prob["mx"]), int(prob["my"]), int(prob["mz"])
             p.alpha = float(prob["alpha"])
+            bc = prob.get("bc") or [A.KR_BC_DIRICHLET] * 6
+            gm = prob.get("gamma") or [0.0] * 6
+            p.bc = (C.c_int32 * 6)(*[int(b) for b in bc])
+            p.gamma = (C.c_double * 6)(*[float(g) for g in gm])
         else:
             p.op = A.KR_OP_CSR
             rp = self._arr(prob["row_ptr"], np.int64)
@@ -55,6 +59,7 @@ class _Marshal:
         p.n_out, p.out = len(outs), ov
         p.step, p.n_steps = float(prob["step"]), int(prob["n_steps"])
         p.k = int(prob["k"])
+        p.eps = float(prob.get("eps", 0.0) or 0.0)
         p.method = _METHOD[method or prob.get("method", "auto")]
         p.part = _PART[part]
         p.virtual_slabs = int(virtual_slabs)
@@ -148,6 +153,23 @@ class KrylovReach:
         A.check(A.lib().krylov_krylov_data(self.h, int(d), _p(H), _p(P)))
         return H, P
 
+    def tridiag(self, d=0):
+        """(alpha [k_eff], beta [k_eff]) of the Lanczos tridiagonal of direction d (stencil Lanczos path)."""
+        k = int(self.prob["k"])
+        al, be = np.zeros(k), np.zeros(k)
+        ke = C.c_int32()
+        A.check(A.lib().krylov_tridiag(self.h, int(d), _p(al), _p(be), k, C.byref(ke)))
+        return al[:ke.value].copy(), be[:ke.value].copy()
+
+    def adaptive_checks(self, d=0):
+        """[(k, unit-vector Lemma 1 bound)] at the Alg. 4 checkpoints evaluated for direction d."""
+        cap = 512
+        ks = np.zeros(cap, dtype=np.int32)
+        bs = np.zeros(cap)
+        n = C.c_int32()
+        A.check(A.lib().krylov_adaptive_checks(self.h, int(d), _p(ks), _p(bs), cap, C.byref(n)))
+        return [(int(ks[i]), float(bs[i])) for i in range(min(n.value, cap))]
+
     def transfer_bytes(self):
         h2d, d2h = C.c_int64(), C.c_int64()
         A.check(A.lib().krylov_transfer_bytes(self.h, C.byref(h2d), C.byref(d2h)))
@@ -160,7 +182,10 @@ class KrylovReach:
         it, st, bytes_ = C.c_double(), C.c_double(), C.c_double()
         n = C.c_int64()
         A.check(A.lib().krylov_last_timing(self.h, C.byref(it), C.byref(st), C.byref(n), C.byref(bytes_)))
-        return {"iter_ms": it.value, "step_ms_mean": st.value, "step_launches": n.value, "step_bytes": bytes_.value}
+        lg, ne = C.c_double(), C.c_int32()
+        A.check(A.lib().krylov_last_timing_large(self.h, C.byref(lg), C.byref(ne)))
+        return {"iter_ms": it.value, "step_ms_mean": st.value, "step_launches": n.value, "step_bytes": bytes_.value,
+                "large_ms": lg.value, "large_evals": ne.value}
 
     def close(self):
         if getattr(self, "h", None):

@@ -11,6 +11,14 @@
 static thread_local std::string g_err;
 void kr_set_error(const std::string& m) { g_err = m; }
 
+cudaError_t kr_event_record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t r = cudaStreamIsCapturing(s, &cs);
+    if (r != cudaSuccess) return r;
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, s);
+}
+
 kr_status kr_comm_unique_id_impl(void* id128);
 kr_comm* kr_comm_create_impl(const void* id128, int32_t rank, int32_t world, int32_t device);
 void kr_comm_destroy_impl(kr_comm* c);
@@ -217,8 +225,22 @@ void validate(const kr_problem* p) {
     if (p->n_out < 1 || p->n_out > KR_MAX_OUT || !p->out) KR_THROW(KR_EINVAL, "n_out must be 1..64");
     if (!(p->step > 0.0) || !finite(p->step)) KR_THROW(KR_EINVAL, "step must be > 0");
     if (p->n_steps < 0) KR_THROW(KR_EINVAL, "n_steps must be >= 0");
-    if (p->k < 1 || p->k > 64) KR_THROW(KR_EINVAL, "k must be 1..64");
     if (p->method < 0 || p->method > 2) KR_THROW(KR_EINVAL, "bad method");
+    {
+        const bool stencil_lz = p->op == KR_OP_STENCIL7 && p->method != KR_ARNOLDI;
+        const int kmax = stencil_lz ? KR_K_MAX : KR_K_MAX_FIXED_PADE;
+        if (p->k < 1 || p->k > kmax)
+            KR_THROW(KR_EINVAL, "k must be 1.." + std::to_string(kmax) + (stencil_lz ? "" : " (Arnoldi / CSR)"));
+        if (!(p->eps >= 0.0) || !finite(p->eps)) KR_THROW(KR_EINVAL, "eps must be >= 0");
+        if (p->eps > 0.0 && !stencil_lz) KR_THROW(KR_EINVAL, "adaptive k (eps > 0) needs the stencil Lanczos path");
+        for (int f = 0; f < 6; ++f) {
+            if (p->bc[f] < KR_BC_DIRICHLET || p->bc[f] > KR_BC_ROBIN) KR_THROW(KR_EINVAL, "bad boundary condition");
+            if (p->bc[f] != KR_BC_DIRICHLET && p->op != KR_OP_STENCIL7)
+                KR_THROW(KR_EINVAL, "boundary conditions apply to the stencil operator only");
+            if (p->bc[f] == KR_BC_ROBIN && (!finite(p->gamma[f]) || p->gamma[f] < 0.0))
+                KR_THROW(KR_EINVAL, "Robin gamma must be finite and >= 0");
+        }
+    }
     if (p->part < 0 || p->part > 2) KR_THROW(KR_EINVAL, "bad partition");
     for (int d = 0; d < p->n_gen; ++d) {
         validate_vec(p, p->gen[d], "generator");
@@ -311,6 +333,8 @@ void free_handle(kr_handle* h) {
     for (auto e : h->ev) cudaEventDestroy(e);
     if (h->ev_it0) cudaEventDestroy(h->ev_it0);
     if (h->ev_it1) cudaEventDestroy(h->ev_it1);
+    if (h->ev_lg0) cudaEventDestroy(h->ev_lg0);
+    if (h->ev_lg1) cudaEventDestroy(h->ev_lg1);
     for (void* p : h->extra_allocs) cudaFree(p);
     if (h->own_ws && h->ws) cudaFree(h->ws);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -406,6 +430,13 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         h->mz = p->op == KR_OP_STENCIL7 ? p->mz : 1;
         h->pitch = (h->mx + 1) & ~int64_t(1);
         h->alpha = p->alpha;
+        h->gen_bc = false;
+        for (int f = 0; f < 6; ++f) {
+            h->bc[f] = p->op == KR_OP_STENCIL7 ? p->bc[f] : KR_BC_DIRICHLET;
+            h->gamma[f] = h->bc[f] == KR_BC_ROBIN ? p->gamma[f] : 0.0;
+            h->gen_bc |= h->bc[f] != KR_BC_DIRICHLET;
+        }
+        h->eps = p->eps;
         if (p->op == KR_OP_STENCIL7) {
             h->cx = p->alpha * (double)(p->mx + 1) * (double)(p->mx + 1);
             h->cy = p->alpha * (double)(p->my + 1) * (double)(p->my + 1);
@@ -469,7 +500,13 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         }
         const int k = h->k;
         const int64_t np1 = h->n_steps + 1;
-        h->d_H = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * (k + 1) * k * 8));
+        h->large_route = h->path == PATH_FUSED_LANCZOS && (h->eps > 0.0 || k > KR_K_MAX_FIXED_PADE);
+        h->checks.assign(ndl, {});
+        h->d_scratch = reinterpret_cast<double*>(dalloc(h, 64));
+        if (!h->large_route) {
+            h->d_H = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * (k + 1) * k * 8));
+            KR_CUDA(cudaMemsetAsync(h->d_H, 0, (size_t)ndl * (k + 1) * k * 8, h->stream));
+        }
         h->d_P = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * h->n_out * k * 8));
         h->d_beta0 = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 8));
         h->d_hnext = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 8));
@@ -478,7 +515,6 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         h->d_keff = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4));
         h->d_done = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4));
         h->d_status = reinterpret_cast<int32_t*>(dalloc(h, (size_t)ndl * 4 + 64));
-        KR_CUDA(cudaMemsetAsync(h->d_H, 0, (size_t)ndl * (k + 1) * k * 8, h->stream));
         KR_CUDA(cudaMemsetAsync(h->d_P, 0, (size_t)ndl * h->n_out * k * 8, h->stream));
         KR_CUDA(cudaMemsetAsync(h->d_hnext, 0, (size_t)ndl * 8, h->stream));
         KR_CUDA(cudaMemsetAsync(h->d_status, 0, (size_t)ndl * 4 + 64, h->stream));
@@ -596,7 +632,21 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
             const int R_total = (int)h->slabs.size() * h->world;
             h->d_rankvec = reinterpret_cast<double*>(dalloc(h, (size_t)R_total * h->nq * 8));
             h->d_sc = reinterpret_cast<LzScalars*>(dalloc(h, (size_t)ndl * sizeof(LzScalars)));
-            KR_CUDA(cudaMemsetAsync(h->d_sc, 0, (size_t)ndl * sizeof(LzScalars), h->stream));
+            h->d_lzarr = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 3 * (k + 2) * 8));
+            KR_CUDA(cudaMemsetAsync(h->d_lzarr, 0, (size_t)ndl * 3 * (k + 2) * 8, h->stream));
+            {
+                std::vector<LzScalars> scs(ndl);
+                for (int dl = 0; dl < ndl; ++dl) {
+                    std::memset(&scs[dl], 0, sizeof(LzScalars));
+                    double* base = h->d_lzarr + (size_t)dl * 3 * (k + 2);
+                    scs[dl].alpha = base;
+                    scs[dl].beta = base + (k + 2);
+                    scs[dl].s = base + 2 * (k + 2);
+                }
+                KR_CUDA(cudaMemcpyAsync(h->d_sc, scs.data(), (size_t)ndl * sizeof(LzScalars), cudaMemcpyHostToDevice,
+                                        h->stream));
+                KR_CUDA(cudaStreamSynchronize(h->stream));
+            }
             int64_t nloc = 0;
             for (auto& sl : h->slabs) nloc += sl.nz * h->mx * h->my;
             h->step_bytes = 24.0 * (double)nloc;
@@ -620,11 +670,11 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
             h->step_bytes = (h->op == KR_OP_CSR ? (double)p->nnz * 12.0 + (double)(p->n + 1) * 8.0 : 0.0) +
                             16.0 * (double)h->N * ndl;
         }
-        kr_expm_prepare(h);
+        if (!h->large_route) kr_expm_prepare(h);
         h->d_sense = reinterpret_cast<int32_t*>(dalloc(h, (size_t)h->n_out * 4));
         h->d_thr = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * 8));
         h->timing = true;
-        h->ev.resize((size_t)2 * k);
+        h->ev.resize((size_t)2 * std::min(k, 256));
         for (auto& e : h->ev) KR_CUDA(cudaEventCreate(&e));
         KR_CUDA(cudaEventCreate(&h->ev_it0));
         KR_CUDA(cudaEventCreate(&h->ev_it1));
@@ -645,15 +695,7 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
         const bool dirs_gather = h->part == KR_PART_DIRS && h->world > 1;
         const int ndl_max = dirs_gather ? (h->n_dir + h->world - 1) / h->world : ndl;
         const int64_t np1 = h->n_steps + 1;
-        auto enqueue = [&](bool ev) {
-            KR_CUDA(cudaEventRecordWithFlags(h->ev_it0, h->stream, cudaEventRecordExternal));
-            if (h->path == PATH_FUSED_LANCZOS) {
-                for (int dl = 0; dl < ndl; ++dl) kr_lz_enqueue_direction(h, dl, ev);
-            } else {
-                kr_ge_enqueue_direction_set(h);
-            }
-            KR_CUDA(cudaEventRecordWithFlags(h->ev_it1, h->stream, cudaEventRecordExternal));
-            kr_expm_enqueue(h);
+        auto post = [&]() {
             if (dirs_gather) {
                 double* loc = h->d_coeff_loc + (size_t)h->rank * np1 * h->n_out * ndl_max;
                 // expm wrote rank-local slots at the start of d_coeff_loc; move into the rank's block
@@ -674,8 +716,76 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                                   (size_t)ndl_max * 4, h->stream);
             }
         };
-        const bool use_graph = getenv("KR_NO_GRAPH") == nullptr;
-        if (use_graph && !h->graph_ready) {
+        auto enqueue = [&](bool ev) {
+            KR_CUDA(kr_event_record(h->ev_it0, h->stream));
+            if (h->path == PATH_FUSED_LANCZOS) {
+                for (int dl = 0; dl < ndl; ++dl) kr_lz_enqueue_direction(h, dl, ev);
+            } else {
+                kr_ge_enqueue_direction_set(h);
+            }
+            KR_CUDA(kr_event_record(h->ev_it1, h->stream));
+            kr_expm_enqueue(h);
+            post();
+        };
+        // Large-k route (eps > 0: Alg. 4 with Lemma 1 checkpoints; or fixed k > 64): host-driven, since the
+        // number of Krylov steps depends on the bounds. Each checkpoint synchronises once (a few per run).
+        auto run_large = [&]() {
+            auto read_sc = [&](int dl) {
+                LzScalars sc;
+                KR_CUDA(cudaMemcpyAsync(&sc, h->d_sc + dl, sizeof(LzScalars), cudaMemcpyDeviceToHost, h->stream));
+                KR_CUDA(cudaStreamSynchronize(h->stream));
+                return sc;
+            };
+            h->large_ms = 0.0;
+            h->large_evals = 0;
+            KR_CUDA(cudaEventRecord(h->ev_it0, h->stream));
+            for (int dl = 0; dl < ndl; ++dl) {
+                h->checks[dl].clear();
+                kr_lz_enqueue_init(h, dl);
+                int i = 0, accepted = -1;
+                bool failed = false;
+                if (h->eps > 0.0) {
+                    // checkpoints k = 4, ceil(1.1 k), ... in fp64 (Alg. 2 lines 11-16)
+                    for (int kc = 4; kc <= h->k; kc = (int)std::ceil(1.1 * (double)kc)) {
+                        while (i < kc) kr_lz_enqueue_step(h, dl, ++i, h->timing);
+                        const LzScalars sc = read_sc(dl);
+                        if (sc.status) {
+                            failed = true;
+                            break;
+                        }
+                        if (dl == 0) h->steps_run0 = std::min(i, std::max(1, sc.k_eff));
+                        if (sc.done && sc.k_eff < h->k) {  // exact breakdown: the approximation is exact
+                            kr_large_eval(h, dl, std::max(1, sc.k_eff), true, true);
+                            accepted = sc.k_eff;
+                            break;
+                        }
+                        const double b = kr_large_eval(h, dl, kc, true, false);
+                        h->checks[dl].push_back({kc, b});
+                        if (b < h->eps) {
+                            accepted = kc;
+                            break;
+                        }
+                    }
+                }
+                if (accepted < 0 && !failed) {  // fixed k, or k_max reached without meeting eps
+                    while (i < h->k) kr_lz_enqueue_step(h, dl, ++i, h->timing);
+                    if (dl == 0) h->steps_run0 = i;
+                    const LzScalars sc = read_sc(dl);
+                    if (!sc.status) {
+                        const int ke = std::max(1, sc.k_eff);
+                        const bool brk = h->eps > 0.0 && sc.done && sc.k_eff < h->k;
+                        const double b = kr_large_eval(h, dl, ke, true, brk);
+                        if (h->eps > 0.0 && !brk) h->checks[dl].push_back({ke, b});
+                    }
+                }
+            }
+            KR_CUDA(cudaEventRecord(h->ev_it1, h->stream));
+            post();
+        };
+        const bool use_graph = getenv("KR_NO_GRAPH") == nullptr && !h->large_route;
+        if (h->large_route) {
+            run_large();
+        } else if (use_graph && !h->graph_ready) {
             const int64_t before = h->launches;
             cudaGraph_t g;
             KR_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -692,7 +802,8 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             h->launches = before;
             h->graph_ready = true;
         }
-        if (use_graph) {
+        if (h->large_route) {
+        } else if (use_graph) {
             KR_CUDA(cudaGraphLaunch(h->gexec, h->stream));
             h->launches += h->graph_launches;
         } else {
@@ -721,16 +832,18 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             int64_t cnt = 0;
             int keff0 = h->k;
             if (ndl > 0) KR_CUDA(cudaMemcpy(&keff0, h->d_keff, 4, cudaMemcpyDeviceToHost));
-            for (int i = 0; i < h->k; ++i) {
+            if (h->large_route) keff0 = h->steps_run0;  // Lanczos steps enqueued for direction 0
+            const int nev = (int)(h->ev.size() / 2);
+            const int nrec = std::min(std::min(h->k, nev), std::max(1, keff0));  // pairs recorded this run
+            for (int i = 0; i < nrec; ++i) {
                 float t = 0.f;
                 KR_CUDA(cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]));
-                if (i < std::max(1, keff0)) {
-                    tot += t;
-                    cnt++;
-                }
+                tot += t;
+                cnt++;
             }
             h->last_step_ms_mean = cnt ? tot / cnt : 0.0;
-            h->last_step_launches = cnt * (h->path == PATH_FUSED_LANCZOS ? (int64_t)h->slabs.size() : 1);
+            h->last_step_launches = (h->large_route ? (int64_t)keff0 : cnt) *
+                                    (h->path == PATH_FUSED_LANCZOS ? (int64_t)h->slabs.size() : 1);
         }
         if (coeff) {
             KR_CUDA(cudaMemcpy(coeff, h->d_coeff, (size_t)np1 * h->n_out * h->n_dir * 8, cudaMemcpyDeviceToHost));
@@ -828,9 +941,70 @@ kr_status krylov_krylov_data(const kr_handle* h, int32_t dir, double* H, double*
             if (h->my_dirs[i] == dir) dl = (int)i;
         if (dl < 0) KR_THROW(KR_EDIM, "direction not handled by this rank");
         const int k = h->k;
-        if (H) KR_CUDA(cudaMemcpy(H, h->d_H + (size_t)dl * (k + 1) * k, (size_t)(k + 1) * k * 8, cudaMemcpyDeviceToHost));
+        if (H && h->d_H) {
+            KR_CUDA(cudaMemcpy(H, h->d_H + (size_t)dl * (k + 1) * k, (size_t)(k + 1) * k * 8, cudaMemcpyDeviceToHost));
+        } else if (H) {  // large-k route keeps H tridiagonal (Eq. 6): expand alpha / beta
+            LzScalars sc;
+            KR_CUDA(cudaMemcpy(&sc, h->d_sc + dl, sizeof(LzScalars), cudaMemcpyDeviceToHost));
+            int ke = 0;
+            KR_CUDA(cudaMemcpy(&ke, h->d_keff + dl, 4, cudaMemcpyDeviceToHost));
+            std::vector<double> al(k + 2), be(k + 2);
+            KR_CUDA(cudaMemcpy(al.data(), sc.alpha, (size_t)(k + 2) * 8, cudaMemcpyDeviceToHost));
+            KR_CUDA(cudaMemcpy(be.data(), sc.beta, (size_t)(k + 2) * 8, cudaMemcpyDeviceToHost));
+            std::memset(H, 0, (size_t)(k + 1) * k * 8);
+            for (int i = 0; i < ke; ++i) {
+                H[(size_t)i * k + i] = al[i + 1];
+                H[(size_t)(i + 1) * k + i] = be[i + 1];
+                if (i + 1 < ke) H[(size_t)i * k + i + 1] = be[i + 1];
+            }
+        }
         if (P) KR_CUDA(cudaMemcpy(P, h->d_P + (size_t)dl * h->n_out * k, (size_t)h->n_out * k * 8, cudaMemcpyDeviceToHost));
     });
+}
+
+kr_status krylov_tridiag(const kr_handle* h, int32_t dir, double* alpha, double* beta, int32_t cap, int32_t* k_eff) {
+    return guarded([&] {
+        if (!h || !k_eff || cap < 0) KR_THROW(KR_EINVAL, "bad arguments");
+        if (h->path != PATH_FUSED_LANCZOS) KR_THROW(KR_EINVAL, "krylov_tridiag: stencil Lanczos path only");
+        if (!h->projected) KR_THROW(KR_ESTATE, "krylov_tridiag before krylov_project");
+        int dl = -1;
+        for (size_t i = 0; i < h->my_dirs.size(); ++i)
+            if (h->my_dirs[i] == dir) dl = (int)i;
+        if (dl < 0) KR_THROW(KR_EDIM, "direction not handled by this rank");
+        int ke = 0;
+        KR_CUDA(cudaMemcpy(&ke, h->d_keff + dl, 4, cudaMemcpyDeviceToHost));
+        *k_eff = ke;
+        LzScalars sc;
+        KR_CUDA(cudaMemcpy(&sc, h->d_sc + dl, sizeof(LzScalars), cudaMemcpyDeviceToHost));
+        const int n = std::min(ke, cap);
+        if (alpha && n > 0) KR_CUDA(cudaMemcpy(alpha, sc.alpha + 1, (size_t)n * 8, cudaMemcpyDeviceToHost));
+        if (beta && n > 0) KR_CUDA(cudaMemcpy(beta, sc.beta + 1, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+kr_status krylov_adaptive_checks(const kr_handle* h, int32_t dir, int32_t* ks, double* bounds, int32_t cap,
+                                 int32_t* n) {
+    return guarded([&] {
+        if (!h || !n || cap < 0) KR_THROW(KR_EINVAL, "bad arguments");
+        if (!h->projected) KR_THROW(KR_ESTATE, "krylov_adaptive_checks before krylov_project");
+        int dl = -1;
+        for (size_t i = 0; i < h->my_dirs.size(); ++i)
+            if (h->my_dirs[i] == dir) dl = (int)i;
+        if (dl < 0) KR_THROW(KR_EDIM, "direction not handled by this rank");
+        const auto& c = h->checks[dl];
+        *n = (int32_t)c.size();
+        for (int i = 0; i < (int)c.size() && i < cap; ++i) {
+            if (ks) ks[i] = c[i].first;
+            if (bounds) bounds[i] = c[i].second;
+        }
+    });
+}
+
+kr_status krylov_last_timing_large(const kr_handle* h, double* expm_ms, int32_t* n_evals) {
+    if (!h) return KR_EINVAL;
+    if (expm_ms) *expm_ms = h->large_ms;
+    if (n_evals) *n_evals = h->large_evals;
+    return KR_OK;
 }
 
 int64_t krylov_launch_count(const kr_handle* h) { return h ? h->launches : 0; }

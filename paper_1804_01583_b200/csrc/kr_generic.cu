@@ -124,9 +124,13 @@ __global__ void spmm_csr_kernel(const int64_t* __restrict__ rp, const int32_t* _
     }
 }
 
+struct FaceCor {  // per-face diagonal correction of face cells relative to Dirichlet (x-, x+, y-, y+, z-, z+)
+    double e[6];
+};
+
 __global__ void stencil_apply_kernel(int64_t mx, int64_t my, int64_t mz, double cx, double cy, double cz,
                                      const double* __restrict__ X, int64_t xstride, double* __restrict__ Y,
-                                     int64_t ystride, const int32_t* __restrict__ done) {
+                                     int64_t ystride, const int32_t* __restrict__ done, FaceCor fc) {
     const int d = blockIdx.y;
     if (done[d]) return;
     const double* u = X + (int64_t)d * xstride;
@@ -139,7 +143,10 @@ __global__ void stencil_apply_kernel(int64_t mx, int64_t my, int64_t mz, double 
         const double sx = (x > 0 ? u[c - 1] : 0.0) + (x < mx - 1 ? u[c + 1] : 0.0);
         const double sy = (yy > 0 ? u[c - mx] : 0.0) + (yy < my - 1 ? u[c + mx] : 0.0);
         const double sz = (z > 0 ? u[c - mx * my] : 0.0) + (z < mz - 1 ? u[c + mx * my] : 0.0);
-        y[c] = cx * sx + cy * sy + cz * sz - diag * u[c];
+        const double dg = diag - (x == 0 ? fc.e[0] : 0.0) - (x == mx - 1 ? fc.e[1] : 0.0) -
+                          (yy == 0 ? fc.e[2] : 0.0) - (yy == my - 1 ? fc.e[3] : 0.0) -
+                          (z == 0 ? fc.e[4] : 0.0) - (z == mz - 1 ? fc.e[5] : 0.0);
+        y[c] = cx * sx + cy * sy + cz * sz - dg * u[c];
     }
 }
 
@@ -373,18 +380,25 @@ void kr_ge_enqueue_direction_set(kr_handle* h) {
     launch_ortho(h, 0, ndl);
     const int64_t vstride = (int64_t)(k + 1) * N;
     const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
+    FaceCor fc{};
+    {
+        const double c[3] = {h->cx, h->cy, h->cz};
+        for (int f = 0; f < 6; ++f)
+            fc.e[f] = (h->bc[f] != KR_BC_DIRICHLET ? c[f / 2] : 0.0) - (h->bc[f] == KR_BC_ROBIN ? h->gamma[f] : 0.0);
+    }
     for (int j = 1; j <= k; ++j) {
         const double* X = h->d_V + (int64_t)(j - 1) * N;
-        if (h->timing) KR_CUDA(cudaEventRecordWithFlags(h->ev[2 * (j - 1)], h->stream, cudaEventRecordExternal));
+        const bool evj = h->timing && (size_t)(2 * j) <= h->ev.size();
+        if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1)], h->stream));
         if (h->op == KR_OP_CSR)
             spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X,
                                                                   vstride, h->d_W, N, ndl, h->d_done);
         else
             stencil_apply_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->mx, h->my, h->mz, h->cx, h->cy, h->cz, X,
-                                                                       vstride, h->d_W, N, h->d_done);
+                                                                       vstride, h->d_W, N, h->d_done, fc);
         KR_CUDA(cudaGetLastError());
         h->launches++;
-        if (h->timing) KR_CUDA(cudaEventRecordWithFlags(h->ev[2 * (j - 1) + 1], h->stream, cudaEventRecordExternal));
+        if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1) + 1], h->stream));
         launch_ortho(h, j, ndl);
     }
 }

@@ -11,7 +11,7 @@
 
 #include "../../include/krylov_reach.h"
 
-#define KR_KMAX 256        // max Krylov dimension (expm smem sized per launch from k_eff)
+#define KR_KMAX KR_K_MAX   // max Krylov dimension (stencil Lanczos; Arnoldi <= KR_K_MAX_FIXED_PADE)
 #define KR_MAX_BOX 8       // box-kind output rows handled inside the fused stencil kernel
 #define KR_MAX_OUT 64      // output rows
 
@@ -19,6 +19,8 @@
 // error plumbing
 // ------------------------------------------------------------------------------------------------
 void kr_set_error(const std::string& msg);
+// record an event on s: an external event node inside stream capture, a plain record otherwise
+cudaError_t kr_event_record(cudaEvent_t e, cudaStream_t s);
 struct KrError {
     kr_status st;
     std::string msg;
@@ -52,10 +54,11 @@ struct BoxRow {  // a KR_VEC_BOX / KR_VEC_ALL output row as seen by the fused ke
 
 // Per-direction Lanczos scalars of the fused path (device memory, written by lz_finalize).
 // Index convention (1-based as in Alg. 3): alpha[i] = H_{i,i}, beta[i] = H_{i+1,i}, s[i] = 1/||u_i||.
+// The three arrays (k + 2 entries each) are the 3k of Eq. 6: H is kept tridiagonal.
 struct LzScalars {
-    double alpha[KR_KMAX + 2];
-    double beta[KR_KMAX + 2];
-    double s[KR_KMAX + 2];
+    double* alpha;
+    double* beta;
+    double* s;
     double hmax;
     double beta0;
     double h_next;
@@ -102,6 +105,10 @@ struct kr_handle {
     int32_t op, method, path, part;
     int64_t mx, my, mz, pitch;
     double alpha, cx, cy, cz;
+    int32_t bc[6];      // stencil face boundary conditions (kr_bc), x-, x+, y-, y+, z-, z+
+    double gamma[6];    // Robin coefficients (units of A)
+    bool gen_bc;        // any non-Dirichlet face
+    double eps;         // adaptive error target (0 = fixed k)
     int64_t n;  // unlifted state count
     int64_t N;  // operator dimension (n or n+1)
     bool lifted;
@@ -167,6 +174,19 @@ struct kr_handle {
     std::vector<BoxRow> boxes;
     int32_t TX, TY;
 
+    double* d_lzarr;       // [ndl][3][k+2] alpha / beta / s arrays of d_sc
+    int steps_run0 = 0;
+    double large_ms = 0.0;  // device time of the large-k route (exponentials + bounds) in the last project
+    int32_t large_evals = 0;
+    cudaEvent_t ev_lg0 = nullptr, ev_lg1 = nullptr;    // Lanczos steps run for local direction 0 by the last large-route project
+    bool large_route;      // exponentials through the large-k route (kr_large.cu) instead of per-step Pade
+    // large-k route scratch (allocated at the first project that needs it, for kcap = k)
+    double* d_big;         // 6 x kcap^2 doubles: X, X^2, X^3, X^4, Y, Y'
+    double* d_traj;        // [(n_steps+1)][kcap] x_j = e^{H t_j} e_1
+    double* d_lbound;      // [ndl] unit-vector Lemma 1 bound of the accepted k
+    double* d_scratch;     // small device scratch (norms, bound)
+    std::vector<std::vector<std::pair<int32_t, double>>> checks;  // per local direction: (k, bound)
+
     // generic path
     double* d_V;  // [ndl][k+1][N]
     double* d_W;  // [ndl][N]
@@ -207,6 +227,14 @@ void kr_ge_enqueue_direction_set(kr_handle* h);
 
 // expm + projection + lemma
 void kr_expm_enqueue(kr_handle* h);
+// large-k route (kr_large.cu): x_j = e^{H t_j} e_1 for the tridiagonal of local direction dl at dimension
+// kc, the coefficients c[j][.][d] of direction dl and the unit-vector Lemma 1 bound (returned; 0 with
+// zero_bound, an exact breakdown); fin also writes the direction's stats. Synchronises the stream.
+double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound);
+void kr_large_alloc(kr_handle* h);
+// fused Lanczos building blocks for the adaptive (host-driven) loop
+void kr_lz_enqueue_init(kr_handle* h, int dl);
+void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events);
 // box
 void kr_box_enqueue(kr_handle* h, const int32_t* d_sense, const double* d_thr);
 

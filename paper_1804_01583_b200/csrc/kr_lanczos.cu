@@ -64,6 +64,10 @@ struct StepArgs {
     int32_t mx, my, mz, nz, zoff, zchunk;
     int32_t gx, gy, nitems;  // persistent work items: gx * gy tiles x ceil(nz / zchunk) chunks
     double cx, cy, cz;  // alpha / h_a^2
+    // per-face boundary terms (x-, x+, y-, y+, z-, z+; kr_bc): ecor = diagonal correction of face cells
+    // relative to the Dirichlet stencil ((bc != DIRICHLET) c_a - (bc == ROBIN) gamma); gq = coefficient of
+    // w_c^2 in -w^T A w for a face cell (DIRICHLET c_a, INSULATED 0, ROBIN gamma). Dirichlet: ecor = 0, gq = c.
+    double ecor[6], gq[6];
     const LzScalars* sc;
     int32_t step;       // i (1-based); 0 = init pass
     int32_t has_prev;
@@ -115,7 +119,7 @@ constexpr size_t step_smem_bytes() {
     return (size_t)S * Geo<TX, TY>::STAGE + Geo<TX, TY>::WBYTES + 8 * S + 16;
 }
 
-template <int TX, int TY, int S, bool INIT, bool FULL>
+template <int TX, int TY, int S, bool INIT, bool FULL, bool BC>
 __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
                                          unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
                                          int zc0, int zc1, bool cta_box, double* acc) {
@@ -166,15 +170,19 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                     bb |= 1u << r;
         bm[m] = bb;
     }
-    // ghost-edge coefficients (Dirichlet): cx on x == 0, cy on y == 0 (only slot 0 can have y == 0)
-    const double gex = gx == 0 ? cx : 0.0;
-    const double gey0 = (y0 + ty == 0) ? cy : 0.0;
+    // ghost-edge coefficients of the low faces (Dirichlet: c_a): x == 0, y == 0 (only slot 0 can have y == 0)
+    const double gex = gx == 0 ? (BC ? a.gq[0] : cx) : 0.0;
+    const double gey0 = (y0 + ty == 0) ? (BC ? a.gq[2] : cy) : 0.0;
+    // general boundaries: diagonal corrections of face cells and the high-face edge coefficients
+    const double ex = BC ? ((gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0)) : 0.0;
+    const double kx = (BC && gx == a.mx - 1) ? a.gq[1] : cx;
     double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)(y0 + ty) * a.pitch + gx;
     const int64_t rowstep = (int64_t)RS * a.pitch;
 
     const bool has_ring = tid < G::NR;
     int rci, rpi, rwi;
     bool ring_in;
+    double rexy = 0.0;  // ring cell's x/y diagonal correction (general boundaries)
     {
         const int rx = tid < TY ? TX : tid - TY;
         const int ry = tid < TY ? tid : TY;
@@ -182,6 +190,11 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         rpi = ry * G::PW + rx;
         rwi = ry * G::WW + rx;
         ring_in = has_ring && (FULL || (x0 + rx < a.mx && y0 + ry < a.my));
+        if (BC) {
+            const int rgx = x0 + rx, rgy = y0 + ry;
+            rexy = (rgx == 0 ? a.ecor[0] : 0.0) + (rgx == a.mx - 1 ? a.ecor[1] : 0.0) +
+                   (rgy == 0 ? a.ecor[2] : 0.0) + (rgy == a.my - 1 ? a.ecor[3] : 0.0);
+        }
     }
 
     double up[G::TS], uc[G::TS], wp[G::TS];
@@ -215,6 +228,10 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         const bool zin = a.zoff + q < a.mz;  // uniform: the plane above the global grid is a zero ghost
         double* Wq = ((q & 1) ? Wb1 : Wb0) + wi0;
         double wc[G::TS];
+        // general boundaries: diagonal of this plane's cells relative to the Dirichlet stencil
+        const double dgz = BC ? diag - ex - ((a.zoff + q == 0) ? a.ecor[4] : 0.0) -
+                                    ((a.zoff + q == a.mz - 1) ? a.ecor[5] : 0.0)
+                              : diag;
 #pragma unroll
         for (int m = 0; m < G::TS; ++m) {
             const int o = m * RS * G::CW;
@@ -226,7 +243,12 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 const double sx = Cq[o - 1] + Cq[o + 1];
                 const double sy = Cq[o - G::CW] + Cq[o + G::CW];
                 const double sz = up[m] + un;
-                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -diag * uc[m])));
+                double dg = dgz;
+                if (BC) {
+                    const int gy = y0 + ty + m * RS;
+                    dg -= (gy == 0 ? a.ecor[2] : 0.0) + (gy == a.my - 1 ? a.ecor[3] : 0.0);
+                }
+                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -dg * uc[m])));
                 w = fma(sa, Au, -sb * uc[m]);
                 if (has_prev) w = fma(-sp, Pq[m * RS * G::PW], w);
             }
@@ -245,7 +267,8 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 const double sx = Cqb[rci - 1] + Cqb[rci + 1];
                 const double sy = Cqb[rci - G::CW] + Cqb[rci + G::CW];
                 const double sz = rup + un;
-                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -diag * ruc)));
+                const double rdg = BC ? dgz + ex - rexy : diag;  // dgz holds this thread's ex: swap in the ring's
+                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -rdg * ruc)));
                 w = fma(sa, Au, -sb * ruc);
                 if (has_prev) w = fma(-sp, reinterpret_cast<const double*>(stq + G::POFF)[rpi], w);
             }
@@ -257,7 +280,8 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         if (q > zc0) {  // products for plane q-1 (its w neighbours at x+1, y+1 were written last iteration)
             const double* Wp = ((q & 1) ? Wb0 : Wb1) + wi0;
             const int gzp = a.zoff + q - 1;
-            const double gz = (gzp == 0) ? cz : 0.0;
+            const double gz = (gzp == 0) ? (BC ? a.gq[4] : cz) : 0.0;
+            const double kz = (BC && gzp == a.mz - 1) ? a.gq[5] : cz;
             uint32_t zmask = 0;
             if (cta_box)
                 for (int r = 0; r < a.nbox; ++r)
@@ -272,7 +296,8 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 const double dz = wc[m] - w0;
                 const double w2 = w0 * w0;
                 const double g = gex + gz + (m == 0 ? gey0 : 0.0);
-                acc_d = fma(cx, dx * dx, fma(cy, dy * dy, fma(cz, dz * dz, fma(g, w2, acc_d))));
+                const double ky = (BC && y0 + ty + m * RS == a.my - 1) ? a.gq[3] : cy;
+                acc_d = fma(kx, dx * dx, fma(ky, dy * dy, fma(kz, dz * dz, fma(g, w2, acc_d))));
                 acc_ww += w2;
                 acc_sum += w0;
                 const uint32_t mk = bm[m] & zmask;
@@ -303,7 +328,7 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
     acc[2] += acc_sum;
 }
 
-template <int TX, int TY, int S, bool INIT>
+template <int TX, int TY, int S, bool INIT, bool BC>
 __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(const __grid_constant__ CUtensorMap tmC,
                                                          const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
     using G = Geo<TX, TY>;
@@ -340,9 +365,9 @@ __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(c
                 cta_box = true;
         // interior tiles (the forward ring inside the grid) skip all x/y masking
         if (x0 + TX < a.mx && y0 + TY < a.my)
-            lz_march<TX, TY, S, INIT, true>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+            lz_march<TX, TY, S, INIT, true, BC>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
         else
-            lz_march<TX, TY, S, INIT, false>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+            lz_march<TX, TY, S, INIT, false, BC>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
         __syncthreads();  // every issued plane was consumed: the barriers can be recycled for the next item
         if (tid == 0) {
 #pragma unroll
@@ -379,7 +404,7 @@ __device__ void lz_finalize_dev(const double* rankvec, int R, int nq, int n_out,
         const double a1 = -SD / Sww;
         sc->alpha[1] = a1;
         sc->hmax = fabs(a1);
-        H[0] = a1;
+        if (H) H[0] = a1;
         for (int r = 0; r < n_out; ++r) P[(int64_t)r * k + 0] = sc->s[1] * S[2 + r];
         sc->k_eff = 1;
         *keff_out = 1;
@@ -393,7 +418,7 @@ __device__ void lz_finalize_dev(const double* rankvec, int R, int nq, int n_out,
         return;
     }
     sc->beta[i] = b;
-    H[(int64_t)i * k + (i - 1)] = b;  // h_{i+1,i}: row i of the (k+1) x k Hessenberg
+    if (H) H[(int64_t)i * k + (i - 1)] = b;  // h_{i+1,i}: row i of the (k+1) x k Hessenberg (dense only for small k)
     if (b == 0.0 || b <= 16.0 * DBL_EPSILON * sc->hmax || i == k) {
         sc->done = 1;
         sc->k_eff = i;
@@ -402,11 +427,11 @@ __device__ void lz_finalize_dev(const double* rankvec, int R, int nq, int n_out,
         *hnext_out = b;
         return;
     }
-    H[(int64_t)(i - 1) * k + i] = b;
+    if (H) H[(int64_t)(i - 1) * k + i] = b;
     sc->s[i + 1] = 1.0 / b;
     const double an = -SD / Sww;
     sc->alpha[i + 1] = an;
-    H[(int64_t)i * k + i] = an;
+    if (H) H[(int64_t)i * k + i] = an;
     for (int r = 0; r < n_out; ++r) P[(int64_t)r * k + i] = sc->s[i + 1] * S[2 + r];
     sc->hmax = fmax(sc->hmax, fmax(b, fabs(an)));
     sc->k_eff = i + 1;
@@ -550,7 +575,10 @@ __global__ void __launch_bounds__(256) lz_fillinit_kernel(const StepArgs a) {
         const int zc1 = min(zc0 + a.zchunk, a.nz);
         const int x = tid % TX, ty = tid / TX, gx = x0 + x;
         const bool fx0 = gx >= lx && gx < hx, fx1 = gx + 1 >= lx && gx + 1 < hx;
-        const double gex = gx == 0 ? cx : 0.0;
+        // face terms of -v^T A v (gq = c_a on Dirichlet faces, 0 insulated, gamma Robin): low faces as ghost
+        // terms, high faces replace the edge coefficient (the value beyond the grid is 0)
+        const double gex = gx == 0 ? a.gq[0] : 0.0;
+        const double kx = gx == a.mx - 1 ? a.gq[1] : cx;
         bool fy0[G::TS], fy1[G::TS], okc[G::TS];
         uint32_t bm[G::TS];
 #pragma unroll
@@ -574,7 +602,8 @@ __global__ void __launch_bounds__(256) lz_fillinit_kernel(const StepArgs a) {
             const int gz = a.zoff + q;
             const bool own = q >= zc0 && q < zc1;
             const bool fz0 = gz >= lz && gz < hz, fz1 = gz + 1 >= lz && gz + 1 < hz;
-            const double gez = gex + (gz == 0 ? cz : 0.0);
+            const double gez = gex + (gz == 0 ? a.gq[4] : 0.0);
+            const double kz = gz == a.mz - 1 ? a.gq[5] : cz;
             uint32_t zmask = 0;
             if (own)
                 for (int r = 0; r < a.nbox; ++r)
@@ -589,10 +618,12 @@ __global__ void __launch_bounds__(256) lz_fillinit_kernel(const StepArgs a) {
                 const double dx = ((fx1 && fy0[m] && fz0) ? val : 0.0) - v;
                 const double dy = ((fx0 && fy1[m] && fz0) ? val : 0.0) - v;
                 const double dz = ((fx0 && fy0[m] && fz1) ? val : 0.0) - v;
-                const double ge = gez + ((y0 + ty + m * RS) == 0 ? cy : 0.0);
+                const int gy = y0 + ty + m * RS;
+                const double ge = gez + (gy == 0 ? a.gq[2] : 0.0);
+                const double ky = gy == a.my - 1 ? a.gq[3] : cy;
                 const double v2 = v * v;
                 acc[0] += v2;
-                acc[1] = fma(cx, dx * dx, fma(cy, dy * dy, fma(cz, dz * dz, fma(ge, v2, acc[1]))));
+                acc[1] = fma(kx, dx * dx, fma(ky, dy * dy, fma(kz, dz * dz, fma(ge, v2, acc[1]))));
                 acc[2] += v;
                 const uint32_t mk = bm[m] & zmask;
                 if (mk) {
@@ -666,20 +697,25 @@ void kr_lz_encode_maps(kr_handle* h) {
         }
 }
 
-template <int TX, int TY, bool INIT>
+template <int TX, int TY, bool INIT, bool BC>
 static void set_smem_attr() {
-    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, Stages<TX, TY>::S, INIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, Stages<TX, TY>::S, INIT, BC>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
 }
 
 template <int TX, int TY>
 static int occupancy_t() {
-    set_smem_attr<TX, TY, false>();
-    set_smem_attr<TX, TY, true>();
-    int nb = 0;
-    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false>, 256,
-                                                          step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
-    return nb;
+    set_smem_attr<TX, TY, false, false>();
+    set_smem_attr<TX, TY, true, false>();
+    set_smem_attr<TX, TY, false, true>();
+    set_smem_attr<TX, TY, true, true>();
+    int nb = 0, nb2 = 0;
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, false>,
+                                                          256, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, true>,
+                                                          256, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
+    return nb < nb2 ? nb : nb2;
 }
 
 int kr_lz_occupancy(int TX, int TY) {
@@ -710,6 +746,15 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     a.cx = h->cx;
     a.cy = h->cy;
     a.cz = h->cz;
+    {
+        const double c[3] = {h->cx, h->cy, h->cz};
+        for (int f = 0; f < 6; ++f) {
+            const double ca = c[f / 2];
+            const int bc = h->bc[f];
+            a.ecor[f] = (bc != KR_BC_DIRICHLET ? ca : 0.0) - (bc == KR_BC_ROBIN ? h->gamma[f] : 0.0);
+            a.gq[f] = bc == KR_BC_DIRICHLET ? ca : (bc == KR_BC_ROBIN ? h->gamma[f] : 0.0);
+        }
+    }
     a.sc = sc;
     a.scw = sc;
     a.step = step;
@@ -738,7 +783,7 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     a.n_out = h->n_out;
     a.fin = (S == 1 && h->world == 1) ? 1 : 0;
     a.k = k;
-    a.H = h->d_H + (size_t)dl * (k + 1) * k;
+    a.H = h->d_H ? h->d_H + (size_t)dl * (k + 1) * k : nullptr;
     a.P = h->d_P + (size_t)dl * h->n_out * k;
     a.beta0_out = h->d_beta0 + dl;
     a.hnext_out = h->d_hnext + dl;
@@ -758,10 +803,18 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
         StepArgs a = make_args(h, sl, dl, nxt, step, init, write, init ? cur : (write ? nxt : -1));
         const CUtensorMap& tc = sl.tmC[cur];
         const CUtensorMap& tp = sl.tmP[prev < 0 ? cur : prev];
-        if (init)
-            lz_step_kernel<TX, TY, Stages<TX, TY>::S, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
-        else
-            lz_step_kernel<TX, TY, Stages<TX, TY>::S, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+        constexpr int S = Stages<TX, TY>::S;
+        if (h->gen_bc) {
+            if (init)
+                lz_step_kernel<TX, TY, S, true, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+            else
+                lz_step_kernel<TX, TY, S, false, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+        } else {
+            if (init)
+                lz_step_kernel<TX, TY, S, true, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+            else
+                lz_step_kernel<TX, TY, S, false, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+        }
     }
     KR_CUDA(cudaGetLastError());
     h->launches++;
@@ -824,14 +877,15 @@ static void combine_and_finalize(kr_handle* h, int dl, int step) {
     if (h->world > 1) kr_nccl_allgather(h->comm, rv_local, h->d_rankvec, (size_t)S * h->nq, h->stream);
     const int k = h->k;
     lz_finalize<<<1, 32, 0, h->stream>>>(h->d_rankvec, R, h->nq, h->n_out, step, k, sc,
-                                         h->d_H + (size_t)dl * (k + 1) * k, h->d_P + (size_t)dl * h->n_out * k,
+                                         h->d_H ? h->d_H + (size_t)dl * (k + 1) * k : nullptr,
+                                         h->d_P + (size_t)dl * h->n_out * k,
                                          h->d_beta0 + dl, h->d_hnext + dl, h->d_keff + dl);
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }
 
-// Enqueue the complete Lanczos run for local direction dl on h->stream (capturable).
-void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events) {
+// Start of a Lanczos run for local direction dl on h->stream (capturable): reset, u_1, init pass.
+void kr_lz_enqueue_init(kr_handle* h, int dl) {
     const int d = h->my_dirs[dl];
     LzScalars* sc = h->d_sc + dl;
     lz_reset<<<1, 32, 0, h->stream>>>(sc);
@@ -849,22 +903,28 @@ void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events) {
     }
     for (auto& sl : h->slabs) reduce_launch(h, sl, dl, 0, 0, true, false, 0);
     combine_and_finalize(h, dl, 0);
+}
+
+// Lanczos step i (1-based: computes beta_i, alpha_{i+1}, u_{i+1}) for local direction dl. Steps whose
+// direction already stopped (breakdown / k reached) exit at once on the device flag.
+void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events) {
     const int k = h->k;
-    int evi = 0;
-    for (int i = 1; i <= k; ++i) {
-        const int cur = (i - 1) % 3, prev = (i >= 2) ? (i - 2) % 3 : -1, nxt = i % 3;
-        const bool write = i < k;
-        if (capture_events && dl == 0)
-            KR_CUDA(cudaEventRecordWithFlags(h->ev[evi], h->stream, cudaEventRecordExternal));
-        for (auto& sl : h->slabs) step_launch(h, sl, dl, cur, prev, nxt, i, false, write);
-        if (capture_events && dl == 0)
-            KR_CUDA(cudaEventRecordWithFlags(h->ev[evi + 1], h->stream, cudaEventRecordExternal));
-        evi += 2;
-        for (auto& sl : h->slabs) reduce_launch(h, sl, dl, nxt, i, false, write, write ? nxt : -1);
-        if (write) {
-            if (h->slabs.size() > 1) halo_exchange_virtual(h, nxt);
-            if (h->world > 1) kr_nccl_halo(h->comm, h, nxt, h->stream);
-        }
-        combine_and_finalize(h, dl, i);
+    const int cur = (i - 1) % 3, prev = (i >= 2) ? (i - 2) % 3 : -1, nxt = i % 3;
+    const bool write = i < k;
+    const bool ev = capture_events && dl == 0 && (size_t)(2 * i) <= h->ev.size();
+    if (ev) KR_CUDA(kr_event_record(h->ev[2 * i - 2], h->stream));
+    for (auto& sl : h->slabs) step_launch(h, sl, dl, cur, prev, nxt, i, false, write);
+    if (ev) KR_CUDA(kr_event_record(h->ev[2 * i - 1], h->stream));
+    for (auto& sl : h->slabs) reduce_launch(h, sl, dl, nxt, i, false, write, write ? nxt : -1);
+    if (write) {
+        if (h->slabs.size() > 1) halo_exchange_virtual(h, nxt);
+        if (h->world > 1) kr_nccl_halo(h->comm, h, nxt, h->stream);
     }
+    combine_and_finalize(h, dl, i);
+}
+
+// Enqueue the complete fixed-k Lanczos run for local direction dl on h->stream (capturable).
+void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events) {
+    kr_lz_enqueue_init(h, dl);
+    for (int i = 1; i <= h->k; ++i) kr_lz_enqueue_step(h, dl, i, capture_events);
 }

@@ -1,0 +1,345 @@
+// kr_large.cu — the large-k exponential route of the stencil Lanczos path (adaptive k, Alg. 2/4,
+// PAPER.md:690-700 / 777-809; the paper's heat benchmark needs k = 544 at 10^6 states and k = 5932 at
+// 10^9).
+//
+// For the tridiagonal H_kc = tridiag(beta; alpha; beta) of one Krylov run, kc up to KR_K_MAX, it computes
+//     x_j = e^{H_kc t_j} e_1,  t_j = j * delta, j = 0..N            (Eq. 2)
+// then the Lemma 1 bound (unit start vector, tau = T, trapezoid on the t_j grid) and the
+// basis-matrix coefficients c[j][r] = ||v|| (P x_j)_r (Alg. 4's projected form).
+//
+// Per-step Pade (the k <= 64 route in kr_expm.cu) costs O(kc^3) per time step; here the time grid is
+// uniform, so x_{j+1} = E x_j with E = e^{H delta} computed ONCE per checkpoint:
+//   * scaling and squaring ("squaring and scaling"): X = H delta / 2^s with ||X||_1 <= 1, then
+//     E = T_18(X)^(2^s) where T_18 is the degree-18 Taylor polynomial (truncation < 1/19! ~ 8e-18 for
+//     ||X|| <= 1; Horner, no linear solve). H is tridiagonal, so T_18(X) is banded (bandwidth 18) and the
+//     first squarings stay banded: the fp64 GEMM below skips the structural zeros tile by tile (exact —
+//     products of banded matrices are exactly zero outside the band) and only the last few squarings
+//     are dense kc x kc products;
+//   * the time march x_{j+1} = E x_j (N sequential matrix-vector products) runs in ONE cooperative
+//     kernel: warp per row, fixed-order warp reductions, a grid barrier per time step;
+//   * t = 0 is e_1 exactly.
+// The GEMM is plain fp64 (DFMA; B200 runs fp64 at the same rate on its CUDA cores as on the fp64 MMA
+// path, and this step is a few percent of the adaptive run).
+#include <cooperative_groups.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "kr_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int GT = 64;   // output tile (GT x GT) per CTA
+constexpr int GK = 16;   // k-depth per smem stage
+constexpr int GTH = 256; // threads: 16 x 16, 4 x 4 micro-tile each
+constexpr int SP = GT + 4;  // smem row stride (doubles) of the k-major tiles
+
+int kpad(int kc) { return ((kc + GT - 1) / GT) * GT; }
+
+// C = scale * (A B) + diag * I (diagonal added for rows < kc only), all kp x kp row-major, with A of
+// bandwidth ba and B of bandwidth bb (>= kp - 1 means dense): tiles outside the band of C are written
+// as zeros, and the k-loop of each tile is clipped to the band.
+__global__ void __launch_bounds__(GTH) gemm_band_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                        double* __restrict__ C, int kp, int kc, int ba, int bb,
+                                                        double scale, double diag) {
+    __shared__ double As[2][GK][SP];  // As[k][m] (k-major: conflict-free broadcast reads)
+    __shared__ double Bs[2][GK][SP];  // Bs[k][n]
+    const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long long bc = (long long)ba + bb;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    const bool outside = ((long long)j0 - (i0 + GT - 1) > bc) || ((long long)i0 - (j0 + GT - 1) > bc);
+    if (!outside) {
+        long long lo = max((long long)i0 - ba, (long long)j0 - bb);
+        long long hi = min((long long)i0 + GT - 1 + ba, (long long)j0 + GT - 1 + bb) + 1;
+        lo = max(lo, 0LL);
+        hi = min(hi, (long long)kp);
+        const int l0 = (int)(lo / GK) * GK;
+        const int l1 = (int)((hi + GK - 1) / GK) * GK;
+        const int nkt = (l1 - l0) / GK;
+        // global -> register staging: A tile rows i0..i0+63, cols l..l+15 (4 per thread); B rows l..l+15,
+        // cols j0..j0+63 (4 per thread)
+        const int ar = tid >> 4, ac = tid & 15;  // A: row ar + 16q, col ac
+        const int br = tid >> 6, bcn = tid & 63; // B: row br + 4q, col bcn
+        double ra[4], rb[4];
+        auto gload = [&](int l) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ra[q] = A[(size_t)(i0 + ar + 16 * q) * kp + l + ac];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rb[q] = B[(size_t)(l + br + 4 * q) * kp + j0 + bcn];
+        };
+        auto sstore = [&](int buf) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) As[buf][ac][ar + 16 * q] = ra[q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Bs[buf][br + 4 * q][bcn] = rb[q];
+        };
+        if (nkt > 0) {
+            gload(l0);
+            sstore(0);
+            __syncthreads();
+            for (int t = 0; t < nkt; ++t) {
+                const int buf = t & 1;
+                if (t + 1 < nkt) gload(l0 + (t + 1) * GK);
+#pragma unroll
+                for (int kk = 0; kk < GK; ++kk) {
+                    double av[4], bv[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) av[a] = As[buf][kk][ty + 16 * a];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) bv[b] = Bs[buf][kk][tx + 16 * b];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+                }
+                if (t + 1 < nkt) sstore(buf ^ 1);
+                __syncthreads();
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+            double v = scale * acc[a][b];
+            if (i == j && i < kc) v += diag;
+            C[(size_t)i * kp + j] = v;
+        }
+}
+
+// ||H delta||_1 (max column sum of the symmetric tridiagonal; 1-based alpha[1..kc], beta[1..kc-1]).
+__global__ void large_norm_kernel(const LzScalars* sc, int kc, double delta, double* out) {
+    __shared__ double red[256];
+    double m = 0.0;
+    for (int i = 1 + threadIdx.x; i <= kc; i += blockDim.x) {
+        const double c = fabs(sc->alpha[i]) + (i > 1 ? fabs(sc->beta[i - 1]) : 0.0) + (i < kc ? fabs(sc->beta[i]) : 0.0);
+        m = fmax(m, c);
+    }
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = red[0] * delta;
+}
+
+// X = H delta / 2^s (dense kp x kp, zero outside the tridiagonal band and in the padding);
+// Y = I + X / 18 (the innermost Horner factor of T_18).
+__global__ void large_build_kernel(const LzScalars* sc, int kc, int kp, double f, double* X, double* Y) {
+    const int64_t n = (int64_t)kp * kp;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / kp), j = (int)(e - (int64_t)i * kp);
+        double x = 0.0;
+        if (i < kc && j < kc) {
+            if (i == j)
+                x = sc->alpha[i + 1] * f;
+            else if (j == i + 1)
+                x = sc->beta[i + 1] * f;
+            else if (i == j + 1)
+                x = sc->beta[j + 1] * f;
+        }
+        X[e] = x;
+        Y[e] = x * (1.0 / 18.0) + ((i == j && i < kc) ? 1.0 : 0.0);
+    }
+}
+
+// x_0 = e_1; x_{j+1} = E x_j (E banded with bandwidth bw), one warp per row, grid barrier per step.
+__global__ void __launch_bounds__(256) large_chain_kernel(const double* __restrict__ E, int kp, int kc, int bw,
+                                                          double* traj, int64_t n_steps) {
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < kc; e += (int64_t)gridDim.x * blockDim.x)
+        traj[e] = e == 0 ? 1.0 : 0.0;  // e^{H 0} e_1 = e_1 exactly
+    grid.sync();
+    for (int64_t j = 0; j < n_steps; ++j) {
+        const double* x = traj + j * kp;
+        double* y = traj + (j + 1) * kp;
+        for (int64_t r = gw; r < kc; r += nw) {
+            const int l0 = (int)max((long long)r - bw, 0LL), l1 = (int)min((long long)r + bw + 1, (long long)kc);
+            const double* Er = E + r * kp;
+            double s = 0.0;
+            for (int l = l0 + lane; l < l1; l += 32) s = fma(Er[l], __ldcg(&x[l]), s);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            if (lane == 0) y[r] = s;
+        }
+        grid.sync();
+    }
+}
+
+// c[j][r][d] = beta0 * sum_l P[r][l] x_j[l]  and  h_j = x_j[kc-1]  (one CTA per time step j)
+__global__ void large_project_kernel(const double* traj, int kp, int kc, const double* P, int kstride, int n_out,
+                                     const double* beta0, double* coeff, int ndl_stride, int dl, double* hlast,
+                                     int64_t n_steps) {
+    const int64_t j = blockIdx.x;
+    const double* x = traj + j * kp;
+    __shared__ double red[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double b0 = *beta0;
+    for (int r = 0; r < n_out; ++r) {
+        const double* Pr = P + (int64_t)r * kstride;
+        double s = 0.0;
+        for (int l = threadIdx.x; l < kc; l += blockDim.x) s = fma(Pr[l], x[l], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (lane == 0) red[wid] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            coeff[(j * n_out + r) * ndl_stride + dl] = b0 * t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) hlast[j] = x[kc - 1];
+}
+
+// Lemma 1 for the unit start vector: h_{kc+1,kc} e^{max(mu,0) T} int_0^T |h(t)| dt, trapezoid on
+// the t_j grid, fixed-order reduction. out[0] = bound; with fin != 0 also the direction's stats.
+__global__ void large_bound_kernel(const double* hlast, int64_t n_steps, double step, double mu, const LzScalars* sc,
+                                   int kc, int zero_bound, double* out, int fin, const double* beta0, double* lemma,
+                                   double* hnext, int32_t* keff) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n_steps; j += blockDim.x) s += 0.5 * step * (fabs(hlast[j]) + fabs(hlast[j + 1]));
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double hn = zero_bound ? 0.0 : sc->beta[kc];
+        const double T = (double)n_steps * step;
+        const double b = zero_bound ? 0.0 : hn * exp(fmax(mu, 0.0) * T) * red[0];
+        out[0] = b;
+        if (fin) {
+            *lemma = *beta0 * b;
+            *hnext = hn;
+            *keff = kc;
+        }
+    }
+}
+
+}  // namespace
+
+void kr_large_alloc(kr_handle* h) {
+    if (h->d_big) return;
+    const int kp = kpad(h->k);
+    const size_t mat = (size_t)kp * kp;
+    KR_CUDA(cudaMalloc(&h->d_big, 3 * mat * sizeof(double)));
+    h->extra_allocs.push_back(h->d_big);
+    KR_CUDA(cudaMalloc(&h->d_traj, (size_t)(h->n_steps + 1) * kp * sizeof(double)));
+    h->extra_allocs.push_back(h->d_traj);
+}
+
+// Evaluate the large-k route for local direction dl at dimension kc (the leading kc x kc block of the
+// Lanczos tridiagonal, whose entries are final once step kc ran). Synchronises the stream. Returns the
+// unit-vector Lemma 1 bound. fin: also write stats (k_eff = kc, h_next, beta0 * bound) — the
+// coefficients of direction dl are always written (the last evaluation is the accepted one).
+// zero_bound: exact breakdown at kc (the approximation is exact): bound 0.
+double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
+    kr_large_alloc(h);
+    if (!h->ev_lg0) {
+        KR_CUDA(cudaEventCreate(&h->ev_lg0));
+        KR_CUDA(cudaEventCreate(&h->ev_lg1));
+    }
+    KR_CUDA(cudaEventRecord(h->ev_lg0, h->stream));
+    const int kp = kpad(kc);
+    const size_t mat = (size_t)kp * kp;
+    double* X = h->d_big;
+    double* Y0 = X + mat;
+    double* Y1 = Y0 + mat;
+    LzScalars* sc = h->d_sc + dl;
+    cudaStream_t st = h->stream;
+    // scaling: ||H delta||_1 -> s with ||H delta||_1 / 2^s <= 1
+    large_norm_kernel<<<1, 256, 0, st>>>(sc, kc, h->step, h->d_scratch);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    double nrm = 0.0;
+    KR_CUDA(cudaMemcpyAsync(&nrm, h->d_scratch, 8, cudaMemcpyDeviceToHost, st));
+    KR_CUDA(cudaStreamSynchronize(st));
+    if (!std::isfinite(nrm)) KR_THROW(KR_ENONFINITE, "non-finite Lanczos tridiagonal");
+    int s = 0;
+    while (std::ldexp(nrm, -s) > 1.0) ++s;
+    const double f = std::ldexp(h->step, -s);
+    const int bmax = kp - 1;
+    {
+        const int64_t n = (int64_t)mat;
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+        large_build_kernel<<<blocks, 256, 0, st>>>(sc, kc, kp, f, X, Y0);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+    }
+    // Horner: Y = I + X Y / q, q = 17..1  ->  Y = T_18(X); bandwidth of Y grows by one per product
+    const dim3 grid(kp / GT, kp / GT);
+    int bwY = 1;
+    double* Y = Y0;
+    double* Z = Y1;
+    for (int q = 17; q >= 1; --q) {
+        gemm_band_kernel<<<grid, GTH, 0, st>>>(X, Y, Z, kp, kc, 1, std::min(bwY, bmax), 1.0 / q, 1.0);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        bwY = std::min(bwY + 1, bmax);
+        std::swap(Y, Z);
+    }
+    // squaring: E = Y^(2^s)
+    for (int r = 0; r < s; ++r) {
+        gemm_band_kernel<<<grid, GTH, 0, st>>>(Y, Y, Z, kp, kc, bwY, bwY, 1.0, 0.0);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        bwY = std::min(2 * bwY, bmax);
+        std::swap(Y, Z);
+    }
+    // time march (cooperative: every CTA co-resident for the per-step grid barrier)
+    {
+        int dev = 0, sms = 148, per_sm = 0;
+        KR_CUDA(cudaGetDevice(&dev));
+        KR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, large_chain_kernel, 256, 0));
+        const int want = (kc + 7) / 8;  // 8 warps per CTA, >= 1 row per warp
+        int nb = std::max(1, std::min(want, sms * std::max(1, std::min(per_sm, 2))));
+        const double* Ec = Y;
+        int bw = std::min(bwY, kc);
+        int kpa = kp, kca = kc;
+        int64_t ns = h->n_steps;
+        double* tr = h->d_traj;
+        void* args[] = {(void*)&Ec, (void*)&kpa, (void*)&kca, (void*)&bw, (void*)&tr, (void*)&ns};
+        KR_CUDA(cudaLaunchCooperativeKernel((const void*)large_chain_kernel, dim3(nb), dim3(256), args, 0, st));
+        h->launches++;
+    }
+    const int ndl = (int)h->my_dirs.size();
+    const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
+    double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
+    large_project_kernel<<<(unsigned)(h->n_steps + 1), 256, 0, st>>>(
+        h->d_traj, kp, kc, h->d_P + (size_t)dl * h->n_out * h->k, h->k, h->n_out, h->d_beta0 + dl, h->d_coeff_loc,
+        ndl_stride, dl, hl, h->n_steps);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    large_bound_kernel<<<1, 256, 0, st>>>(hl, h->n_steps, h->step, h->mu, sc, kc, zero_bound ? 1 : 0, h->d_scratch + 1,
+                                          fin ? 1 : 0, h->d_beta0 + dl, h->d_lemma + dl, h->d_hnext + dl,
+                                          h->d_keff + dl);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    KR_CUDA(cudaEventRecord(h->ev_lg1, st));
+    double b = 0.0;
+    KR_CUDA(cudaMemcpyAsync(&b, h->d_scratch + 1, 8, cudaMemcpyDeviceToHost, st));
+    KR_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    KR_CUDA(cudaEventElapsedTime(&ms, h->ev_lg0, h->ev_lg1));
+    h->large_ms += ms;
+    h->large_evals++;
+    return b;
+}

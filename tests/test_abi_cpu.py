@@ -74,7 +74,12 @@ def test_workspace_bytes_host_only():
 
 @pytest.mark.parametrize("mutate,code", [
     (lambda p: p.update(k=0), "KR_EINVAL"),
-    (lambda p: p.update(k=65), "KR_EINVAL"),
+    (lambda p: p.update(k=16385), "KR_EINVAL"),
+    (lambda p: p.update(k=65, method="arnoldi"), "KR_EINVAL"),
+    (lambda p: p.update(eps=-1e-6), "KR_EINVAL"),
+    (lambda p: p.update(eps=1e-6, method="arnoldi"), "KR_EINVAL"),
+    (lambda p: p.update(bc=[3, 0, 0, 0, 0, 0]), "KR_EINVAL"),
+    (lambda p: p.update(bc=[2, 0, 0, 0, 0, 0], gamma=[-1.0, 0, 0, 0, 0, 0]), "KR_EINVAL"),
     (lambda p: p.update(step=0.0), "KR_EINVAL"),
     (lambda p: p.update(n_steps=-1), "KR_EINVAL"),
     (lambda p: p.update(z_lo=np.array([2.0])), "KR_EINVAL"),
@@ -91,6 +96,16 @@ def test_validation_errors(mutate, code):
     with pytest.raises(KrylovError) as e:
         krylov_workspace_bytes(p)
     assert code in str(e.value)
+
+
+def test_large_k_and_boundaries_accepted_host_side():
+    """NEXT-1: stencil Lanczos takes k up to KR_K_MAX, adaptive eps and per-face boundaries (host-only sizing)."""
+    from paper_1804_01583_b200 import krylov_workspace_bytes
+    p = W.heat_paper(20, eps=1e-6, k_max=16384)
+    assert krylov_workspace_bytes(p) == 3 * (20 + 3) * 20 * 20 * 8 + 3 * 256
+    p = W.heat(10, 2, 5)
+    p.update(k=500, bc=[1, 2, 1, 1, 0, 1], gamma=[0, 0.3, 0, 0, 0, 0])
+    assert krylov_workspace_bytes(p) > 0
 
 
 def test_lanczos_on_nonsymmetric_rejected():
