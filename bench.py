@@ -87,12 +87,34 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(p_full, budget="bench"):
+def cpu_baseline(p_full, budget="bench", k_full=None):
     """The oracle as it stands (single-threaded C, literal Alg. 3 + MvL Pade) on a bounded sample of
     the workload: the same recipe on a smaller grid (Lanczos cost is linear in n) plus the full
     1001-step k x k exponential sweep; scaled to Krylov steps/s at the full n."""
     import oracle
     m_full = p_full["mx"]
+    if p_full.get("eps", 0.0) > 0.0:  # the paper's heat model (adaptive): literal Alg. 3 steps + one eig checkpoint
+        m_s = 120 if budget == "reference" else 200
+        ps = W.heat_paper(m_s, n_steps=p_full["n_steps"], step=p_full["step"])
+        v = oracle.directions(ps)[0]
+        ks = 60
+        t0 = time.perf_counter()
+        r = oracle.lanczos(ps, v, ks)
+        t1 = time.perf_counter()
+        kc = int(k_full or 544)
+        rng = np.random.default_rng(0)
+        al = -np.abs(rng.standard_normal(kc)) * 1e3
+        be = np.abs(rng.standard_normal(kc)) * 1e2
+        oracle.eig_e1_times(al, be, ps["step"], ps["n_steps"])
+        t2 = time.perf_counter()
+        n_s, n_f = m_s ** 3, W.n_state(p_full)
+        per_step = (t1 - t0) / ks * (n_f / n_s)
+        return {"value": 1.0 / per_step, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle",
+                "sample": f"oracle (1 thread, C -O2) literal Alg. 3 on the paper heat operator at m={m_s} "
+                          f"({n_s:.3g} states), {ks} steps = {t1 - t0:.2f} s scaled x{n_f / n_s:.1f} to n={n_f:.3g}; "
+                          f"the Lemma 1 checkpoints (numpy eigh route; one at k={kc} took {t2 - t1:.2f} s) "
+                          f"are not included",
+                "sample_seconds": t2 - t0}
     m_s = 160 if budget == "reference" else 250
     b_s = max(2, round(p_full["gens"][0]["hi"][0] * m_s / m_full))
     ps = W.heat(m_s, b_s, p_full["k"], n_steps=p_full["n_steps"], step=p_full["step"])
@@ -144,15 +166,23 @@ def run_reference(args):
 
 
 def config_dict(p, n):
-    if p["op"] == "stencil":
+    if p["op"] == "stencil" and p.get("eps", 0.0) > 0.0:
+        g = p["gens"][0]
+        wl = (f"{p['name']}: the paper's 3D heat model {p['mx']}^3 (n={W.n_state(p):.3g}), insulated faces + Robin "
+              f"0.5 at x=1, heated region {g['hi'][0]}x{g['hi'][1]}x{g['hi'][2]} cells in [0.9,1.1], adaptive Lanczos "
+              f"(Alg. 4, Lemma 1 eps={p['eps']}, k_max={p['k']}), {p['n_steps']} steps of {p['step']}, "
+              f"{len(p['outs'])} output rows")
+    elif p["op"] == "stencil":
         wl = (f"{p['name']}: 3D heat {p['mx']}^3 (n={W.n_state(p):.3g}) Dirichlet 7-point stencil, "
               f"corner block {p['gens'][0]['hi'][0]}^3 in [0.9,1.1], {p['method'].capitalize()} k={p['k']}, "
               f"{p['n_steps']} steps of {p['step']}, {len(p['outs'])} output rows")
-        l2 = ("inputs larger than L2 (three 8 GB state vectors per step vs 126 MB L2)" if W.n_state(p) * 24 > 126e6
-              else "small problem: L2-resident, not flushed (latency-bound context case)")
     else:
         wl = (f"{p['name']}: CSR n={p['n']} ({len(p['col_idx'])} nnz){' lifted affine' if p.get('b') is not None else ''}, "
               f"{W.n_dirs(p)} directions, {p['method'].capitalize()} k={p['k']}, {p['n_steps']} steps of {p['step']}")
+    if p["op"] == "stencil":
+        l2 = (f"inputs larger than L2 (three {8 * W.n_state(p) / 1e9:.3g} GB state vectors per step vs 126 MB L2)"
+              if W.n_state(p) * 24 > 126e6 else "small problem: L2-resident, not flushed (latency-bound context case)")
+    else:
         l2 = "small problem: L2-resident, not flushed (latency-bound context case)"
     return {"workload": wl, "n": W.n_state(p), "k": p["k"], "n_steps": p["n_steps"], "directions": W.n_dirs(p),
             "parallelism": f"zslab{n}" if n > 1 else "single-gpu", "l2": l2}
@@ -183,6 +213,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         comm = KrComm(rank, world, local, torch_broadcast_id)
     p = W.CONFIGS[args.config]()
+    if p.get("eps", 0.0) > 0.0:  # adaptive: time every Lanczos step kernel (the roofline covers the whole run)
+        os.environ.setdefault("KR_MAX_EV", str(p["k"]))
     stream = torch.cuda.current_stream(dev)
     kw = dict(device=local, stream=stream.cuda_stream, comm=comm, part="zslab" if world > 1 else None)
     from paper_1804_01583_b200 import krylov_workspace_bytes
@@ -290,8 +322,14 @@ def main():
                             "algorithmic_bytes": "12 nnz + 8 (n+1) (A once) + 16 N per direction",
                             "peak_source": peak_src}
         line.pop("fused_step")
-    if not args.no_cpu_baseline and world == 1 and p["op"] == "stencil" and args.config == "C5":
-        line["cpu_baseline"] = cpu_baseline(p)
+    if p.get("eps", 0.0) > 0.0:
+        line["adaptive"] = {"k_accepted": stats[0]["k_eff"], "lemma1_bound": stats[0]["lemma1"],
+                            "large_route_ms": timing["large_ms"], "checkpoints": timing["large_evals"],
+                            "lanczos_ms": timing["iter_ms"] - timing["large_ms"],
+                            "note": "step kernel mean over every Lanczos step of the run (CUDA events)"}
+    if not args.no_cpu_baseline and world == 1 and p["op"] == "stencil" and (args.config == "C5" or
+                                                                              p.get("eps", 0.0) > 0.0):
+        line["cpu_baseline"] = cpu_baseline(p, k_full=stats[0]["k_eff"])
     print(json.dumps(line), flush=True)
     if world > 1:
         comm.close()

@@ -674,7 +674,11 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         h->d_sense = reinterpret_cast<int32_t*>(dalloc(h, (size_t)h->n_out * 4));
         h->d_thr = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * 8));
         h->timing = true;
-        h->ev.resize((size_t)2 * std::min(k, 256));
+        {
+            int cap = 256;  // step-kernel event pairs (the timing mean covers the first `cap` steps)
+            if (const char* e = getenv("KR_MAX_EV")) cap = std::max(1, atoi(e));
+            h->ev.resize((size_t)2 * std::min(k, cap));
+        }
         for (auto& e : h->ev) KR_CUDA(cudaEventCreate(&e));
         KR_CUDA(cudaEventCreate(&h->ev_it0));
         KR_CUDA(cudaEventCreate(&h->ev_it1));
@@ -835,12 +839,20 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             if (h->large_route) keff0 = h->steps_run0;  // Lanczos steps enqueued for direction 0
             const int nev = (int)(h->ev.size() / 2);
             const int nrec = std::min(std::min(h->k, nev), std::max(1, keff0));  // pairs recorded this run
+            FILE* trace = nullptr;
+            if (const char* tp = getenv("KR_STEP_TRACE")) trace = fopen(tp, "w");  // diagnostics: per-step ms
             for (int i = 0; i < nrec; ++i) {
                 float t = 0.f;
                 KR_CUDA(cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]));
                 tot += t;
                 cnt++;
+                if (trace) {
+                    float g = 0.f;
+                    if (i + 1 < nrec) KR_CUDA(cudaEventElapsedTime(&g, h->ev[2 * i], h->ev[2 * i + 2]));
+                    fprintf(trace, "%d %.6f %.6f\n", i + 1, t, g);
+                }
             }
+            if (trace) fclose(trace);
             h->last_step_ms_mean = cnt ? tot / cnt : 0.0;
             h->last_step_launches = (h->large_route ? (int64_t)keff0 : cnt) *
                                     (h->path == PATH_FUSED_LANCZOS ? (int64_t)h->slabs.size() : 1);

@@ -15,8 +15,10 @@
 //     first squarings stay banded: the fp64 GEMM below skips the structural zeros tile by tile (exact —
 //     products of banded matrices are exactly zero outside the band) and only the last few squarings
 //     are dense kc x kc products;
-//   * the time march x_{j+1} = E x_j (N sequential matrix-vector products) runs in ONE cooperative
-//     kernel: warp per row, fixed-order warp reductions, a grid barrier per time step;
+//   * the time grid: for kc <= 3000 by doubling — x_{2^q + j} = E^{2^q} x_j, one GEMM of width 2^q per
+//     level with E^{2^q} from further squarings (log2 N dependent launches instead of N); for larger kc,
+//     where those squarings cost more than N passes over E, by the march x_{j+1} = E x_j in ONE
+//     cooperative kernel (warp per row, fixed-order warp reductions, a grid barrier per time step);
 //   * t = 0 is e_1 exactly.
 // The GEMM is plain fp64 (DFMA; B200 runs fp64 at the same rate on its CUDA cores as on the fp64 MMA
 // path, and this step is a few percent of the adaptive run).
@@ -39,41 +41,59 @@ constexpr int SP = GT + 4;  // smem row stride (doubles) of the k-major tiles
 
 int kpad(int kc) { return ((kc + GT - 1) / GT) * GT; }
 
-// C = scale * (A B) + diag * I (diagonal added for rows < kc only), all kp x kp row-major, with A of
-// bandwidth ba and B of bandwidth bb (>= kp - 1 means dense): tiles outside the band of C are written
-// as zeros, and the k-loop of each tile is clipped to the band.
-__global__ void __launch_bounds__(GTH) gemm_band_kernel(const double* __restrict__ A, const double* __restrict__ B,
-                                                        double* __restrict__ C, int kp, int kc, int ba, int bb,
-                                                        double scale, double diag) {
+// C = scale * (A B) + diag * I (diagonal added for i == j < kc), row-major with leading dimensions, M and K
+// multiples of GT, N arbitrary (columns >= N are neither read from B nor written to C). A has bandwidth ba
+// and B bandwidth bb (>= K - 1 means dense; banded only for square products): tiles outside the band of C
+// are written as zeros and the k-loop of each tile is clipped to the band (products of banded matrices
+// are exactly zero outside the band).
+struct GemmArgs {
+    const double* A;
+    const double* B;
+    double* C;
+    int M, N, K, lda, ldb, ldc;
+    int ba, bb, kc;
+    double scale, diag;
+};
+
+__global__ void __launch_bounds__(GTH) gemm_band_kernel(const GemmArgs g) {
     __shared__ double As[2][GK][SP];  // As[k][m] (k-major: conflict-free broadcast reads)
     __shared__ double Bs[2][GK][SP];  // Bs[k][n]
     const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const long long bc = (long long)ba + bb;
+    // band structure only where declared (a bandwidth >= K - 1 means dense, e.g. the tall trajectory block)
+    const bool bandA = g.ba < g.K - 1, bandB = g.bb < g.K - 1;
+    const long long bc = (long long)g.ba + g.bb;
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    const bool outside = ((long long)j0 - (i0 + GT - 1) > bc) || ((long long)i0 - (j0 + GT - 1) > bc);
+    const bool outside =
+        bandA && bandB && (((long long)j0 - (i0 + GT - 1) > bc) || ((long long)i0 - (j0 + GT - 1) > bc));
     if (!outside) {
-        long long lo = max((long long)i0 - ba, (long long)j0 - bb);
-        long long hi = min((long long)i0 + GT - 1 + ba, (long long)j0 + GT - 1 + bb) + 1;
-        lo = max(lo, 0LL);
-        hi = min(hi, (long long)kp);
+        long long lo = 0, hi = g.K;
+        if (bandA) {
+            lo = max(lo, (long long)i0 - g.ba);
+            hi = min(hi, (long long)i0 + GT + g.ba);
+        }
+        if (bandB) {
+            lo = max(lo, (long long)j0 - g.bb);
+            hi = min(hi, (long long)j0 + GT + g.bb);
+        }
         const int l0 = (int)(lo / GK) * GK;
         const int l1 = (int)((hi + GK - 1) / GK) * GK;
         const int nkt = (l1 - l0) / GK;
         // global -> register staging: A tile rows i0..i0+63, cols l..l+15 (4 per thread); B rows l..l+15,
         // cols j0..j0+63 (4 per thread)
-        const int ar = tid >> 4, ac = tid & 15;  // A: row ar + 16q, col ac
-        const int br = tid >> 6, bcn = tid & 63; // B: row br + 4q, col bcn
+        const int ar = tid >> 4, ac = tid & 15;   // A: row ar + 16q, col ac
+        const int br = tid >> 6, bcn = tid & 63;  // B: row br + 4q, col bcn
+        const bool bin = j0 + bcn < g.N;
         double ra[4], rb[4];
         auto gload = [&](int l) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) ra[q] = A[(size_t)(i0 + ar + 16 * q) * kp + l + ac];
+            for (int q = 0; q < 4; ++q) ra[q] = g.A[(size_t)(i0 + ar + 16 * q) * g.lda + l + ac];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) rb[q] = B[(size_t)(l + br + 4 * q) * kp + j0 + bcn];
+            for (int q = 0; q < 4; ++q) rb[q] = bin ? g.B[(size_t)(l + br + 4 * q) * g.ldb + j0 + bcn] : 0.0;
         };
         auto sstore = [&](int buf) {
 #pragma unroll
@@ -110,9 +130,10 @@ __global__ void __launch_bounds__(GTH) gemm_band_kernel(const double* __restrict
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
-            double v = scale * acc[a][b];
-            if (i == j && i < kc) v += diag;
-            C[(size_t)i * kp + j] = v;
+            if (j >= g.N) continue;
+            double v = g.scale * acc[a][b];
+            if (i == j && i < g.kc) v += g.diag;
+            g.C[(size_t)i * g.ldc + j] = v;
         }
 }
 
@@ -206,6 +227,27 @@ __global__ void large_project_kernel(const double* traj, int kp, int kc, const d
     if (threadIdx.x == 0) hlast[j] = x[kc - 1];
 }
 
+// Column layout (doubling route): x_j[l] = Xc[l * ldx + j]. One thread per time step j, fixed-order sums.
+__global__ void large_project_cols_kernel(const double* Xc, int ldx, int kc, const double* P, int kstride, int n_out,
+                                          const double* beta0, double* coeff, int ndl_stride, int dl, double* hlast,
+                                          int64_t n_steps) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j > n_steps) return;
+    const double b0 = *beta0;
+    for (int r = 0; r < n_out; ++r) {
+        const double* Pr = P + (int64_t)r * kstride;
+        double s = 0.0;
+        for (int l = 0; l < kc; ++l) s = fma(Pr[l], Xc[(int64_t)l * ldx + j], s);
+        coeff[(j * n_out + r) * ndl_stride + dl] = b0 * s;
+    }
+    hlast[j] = Xc[(int64_t)(kc - 1) * ldx + j];
+}
+
+__global__ void large_e1_col_kernel(double* Xc, int ldx, int kp) {
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < kp; l += gridDim.x * blockDim.x)
+        Xc[(int64_t)l * ldx] = l == 0 ? 1.0 : 0.0;  // x_0 = e^{H 0} e_1 = e_1 exactly
+}
+
 // Lemma 1 for the unit start vector: h_{kc+1,kc} e^{max(mu,0) T} int_0^T |h(t)| dt, trapezoid on
 // the t_j grid, fixed-order reduction. out[0] = bound; with fin != 0 also the direction's stats.
 __global__ void large_bound_kernel(const double* hlast, int64_t n_steps, double step, double mu, const LzScalars* sc,
@@ -235,14 +277,31 @@ __global__ void large_bound_kernel(const double* hlast, int64_t n_steps, double 
 
 }  // namespace
 
+static int pow2_at_least(int64_t n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
 void kr_large_alloc(kr_handle* h) {
     if (h->d_big) return;
     const int kp = kpad(h->k);
     const size_t mat = (size_t)kp * kp;
     KR_CUDA(cudaMalloc(&h->d_big, 3 * mat * sizeof(double)));
     h->extra_allocs.push_back(h->d_big);
-    KR_CUDA(cudaMalloc(&h->d_traj, (size_t)(h->n_steps + 1) * kp * sizeof(double)));
+    // row layout [(N+1)][kp] for the march, column layout [kp][pow2 >= N+1] for the doubling route
+    const size_t tr = std::max((size_t)(h->n_steps + 1) * kp, (size_t)kp * pow2_at_least(h->n_steps + 1));
+    KR_CUDA(cudaMalloc(&h->d_traj, tr * sizeof(double)));
     h->extra_allocs.push_back(h->d_traj);
+}
+
+static void gemm(kr_handle* h, const double* A, const double* B, double* C, int M, int N, int K, int lda, int ldb,
+                 int ldc, int ba, int bb, int kc, double scale, double diag) {
+    GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, ba, bb, kc, scale, diag};
+    const dim3 grid((unsigned)((N + GT - 1) / GT), (unsigned)(M / GT));
+    gemm_band_kernel<<<grid, GTH, 0, h->stream>>>(g);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
 }
 
 // Evaluate the large-k route for local direction dl at dimension kc (the leading kc x kc block of the
@@ -284,27 +343,51 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
         h->launches++;
     }
     // Horner: Y = I + X Y / q, q = 17..1  ->  Y = T_18(X); bandwidth of Y grows by one per product
-    const dim3 grid(kp / GT, kp / GT);
     int bwY = 1;
     double* Y = Y0;
     double* Z = Y1;
     for (int q = 17; q >= 1; --q) {
-        gemm_band_kernel<<<grid, GTH, 0, st>>>(X, Y, Z, kp, kc, 1, std::min(bwY, bmax), 1.0 / q, 1.0);
-        KR_CUDA(cudaGetLastError());
-        h->launches++;
+        gemm(h, X, Y, Z, kp, kp, kp, kp, kp, kp, 1, std::min(bwY, bmax), kc, 1.0 / q, 1.0);
         bwY = std::min(bwY + 1, bmax);
         std::swap(Y, Z);
     }
     // squaring: E = Y^(2^s)
     for (int r = 0; r < s; ++r) {
-        gemm_band_kernel<<<grid, GTH, 0, st>>>(Y, Y, Z, kp, kc, bwY, bwY, 1.0, 0.0);
-        KR_CUDA(cudaGetLastError());
-        h->launches++;
+        gemm(h, Y, Y, Z, kp, kp, kp, kp, kp, kp, bwY, bwY, kc, 1.0, 0.0);
         bwY = std::min(2 * bwY, bmax);
         std::swap(Y, Z);
     }
-    // time march (cooperative: every CTA co-resident for the per-step grid barrier)
-    {
+    const int ndl = (int)h->my_dirs.size();
+    const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
+    double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
+    const int64_t np1 = h->n_steps + 1;
+    int kdouble = 3000;  // doubling (GEMM-batched) time march up to this kc, the sequential march above
+    if (const char* e = getenv("KR_KDOUBLE")) kdouble = atoi(e);
+    if (kc <= kdouble) {
+        // Doubling: with the columns x_0 .. x_{2^q - 1} known, x_{2^q + j} = E^{2^q} x_j — one GEMM of width
+        // 2^q per level, E^{2^q} by further squaring (the "squaring" of P:508-510 applied to the time grid):
+        // log2(N) sequential launches instead of N dependent matrix-vector products.
+        const int ldx = pow2_at_least(np1);
+        double* Xc = h->d_traj;
+        large_e1_col_kernel<<<(kp + 255) / 256, 256, 0, st>>>(Xc, ldx, kp);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        for (int64_t w0 = 1; w0 < np1; w0 <<= 1) {
+            const int w = (int)std::min<int64_t>(w0, np1 - w0);
+            gemm(h, Y, Xc, Xc + w0, kp, w, kp, kp, ldx, ldx, bwY, kp - 1, -1, 1.0, 0.0);
+            if (2 * w0 < np1) {  // next power E^{2^{q+1}}
+                gemm(h, Y, Y, Z, kp, kp, kp, kp, kp, kp, bwY, bwY, kc, 1.0, 0.0);
+                bwY = std::min(2 * bwY, bmax);
+                std::swap(Y, Z);
+            }
+        }
+        large_project_cols_kernel<<<(unsigned)((np1 + 127) / 128), 128, 0, st>>>(
+            Xc, ldx, kc, h->d_P + (size_t)dl * h->n_out * h->k, h->k, h->n_out, h->d_beta0 + dl, h->d_coeff_loc,
+            ndl_stride, dl, hl, h->n_steps);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+    } else {
+        // time march (cooperative: every CTA co-resident for the per-step grid barrier)
         int dev = 0, sms = 148, per_sm = 0;
         KR_CUDA(cudaGetDevice(&dev));
         KR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -319,15 +402,12 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
         void* args[] = {(void*)&Ec, (void*)&kpa, (void*)&kca, (void*)&bw, (void*)&tr, (void*)&ns};
         KR_CUDA(cudaLaunchCooperativeKernel((const void*)large_chain_kernel, dim3(nb), dim3(256), args, 0, st));
         h->launches++;
+        large_project_kernel<<<(unsigned)(h->n_steps + 1), 256, 0, st>>>(
+            h->d_traj, kp, kc, h->d_P + (size_t)dl * h->n_out * h->k, h->k, h->n_out, h->d_beta0 + dl, h->d_coeff_loc,
+            ndl_stride, dl, hl, h->n_steps);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
     }
-    const int ndl = (int)h->my_dirs.size();
-    const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
-    double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
-    large_project_kernel<<<(unsigned)(h->n_steps + 1), 256, 0, st>>>(
-        h->d_traj, kp, kc, h->d_P + (size_t)dl * h->n_out * h->k, h->k, h->n_out, h->d_beta0 + dl, h->d_coeff_loc,
-        ndl_stride, dl, hl, h->n_steps);
-    KR_CUDA(cudaGetLastError());
-    h->launches++;
     large_bound_kernel<<<1, 256, 0, st>>>(hl, h->n_steps, h->step, h->mu, sc, kc, zero_bound ? 1 : 0, h->d_scratch + 1,
                                           fin ? 1 : 0, h->d_beta0 + dl, h->d_lemma + dl, h->d_hnext + dl,
                                           h->d_keff + dl);

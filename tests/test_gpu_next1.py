@@ -145,3 +145,25 @@ def test_adaptive_kmax_not_met_returns_kmax():
     r = oracle.lanczos(p, oracle.directions(p)[0], 40)
     X = oracle.eig_e1_times(r["alpha"], r["beta"], p["step"], p["n_steps"])
     assert_coeff(coeff, (r["beta0"] * (X @ r["P"].T))[:, :, None], "kmax")
+
+
+@pytest.mark.parametrize("k", [65, 154])
+def test_large_route_doubling_equals_march(k, monkeypatch):
+    """The two time-grid strategies of the large-k route — doubling (x_{2^q+j} = E^{2^q} x_j by GEMM) and
+    the sequential march (x_{j+1} = E x_j) — agree, including where e^{H delta} is still banded
+    (paper heat m = 30: ||H delta|| ~ 2.3, two squarings) and the trajectory block is wider than k."""
+    p = W.heat_paper(30, eps=0.0, k_max=k)
+    p["eps"] = 0.0
+    out = {}
+    for kd in ("0", "100000"):
+        monkeypatch.setenv("KR_KDOUBLE", kd)
+        out[kd] = gpu(p)
+    c0, s0 = out["0"][0], out["0"][1][0]
+    c1, s1 = out["100000"][0], out["100000"][1][0]
+    assert_coeff(c1, c0, f"doubling vs march k={k}")
+    assert abs(s1["lemma1"] - s0["lemma1"]) <= 1e-10 * s0["lemma1"]
+    r = oracle.lanczos(p, oracle.directions(p)[0], k)
+    X = oracle.eig_e1_times(r["alpha"], r["beta"], p["step"], p["n_steps"])
+    b_or = r["beta0"] * oracle.lemma1_bound(r["beta"][k - 1], X, p["step"], 0.0)
+    assert abs(s1["lemma1"] - b_or) <= 1e-8 * b_or
+    assert_coeff(c1, (r["beta0"] * (X @ r["P"].T))[:, :, None], f"oracle k={k}")
