@@ -359,6 +359,59 @@ def krylov_project(p, method=None):
             "times": np.arange(N + 1) * p["step"]}
 
 
+def transpose_problem(p):
+    """The transpose-dynamics problem of §4.1: C e^{At} E = (E^T e^{A^T t} C^T)^T, so the basis
+    matrix can be computed from o simulations of x' = A^T x started at the output rows C_r^T, each then
+    projected with E^T (the "(or the transpose of the initial space matrix E^T)" of Alg. 4).
+    With an affine term the lifted matrix A' = [[A, b], [0, 0]] is transposed explicitly:
+    A'^T = [[A^T, 0], [b^T, 0]]; the output rows have 0 in the lifted coordinate and the projection rows
+    are the forward directions (generators and v_f = [c; 1]). The stencil operator is symmetric."""
+    fwd = directions(p)
+    n_lift = len(fwd[0])
+    q = dict(p)
+    if p["op"] == "csr":
+        n = p["n"]
+        rp, ci, va = p["row_ptr"], p["col_idx"], p["val"]
+        b = p.get("b")
+        ent = []  # (row, col, value) of A'^T, in the order met while scanning A' row by row
+        for r in range(n):
+            for e in range(int(rp[r]), int(rp[r + 1])):
+                ent.append((int(ci[e]), r, float(va[e])))
+            if b is not None and b[r] != 0.0:
+                ent.append((n, r, float(b[r])))
+        ent.sort(key=lambda t: (t[0], t[1]))
+        row_ptr = np.zeros(n_lift + 1, dtype=np.int64)
+        for (r, c, v) in ent:
+            row_ptr[r + 1] += 1
+        row_ptr = np.cumsum(row_ptr)
+        q.update(n=n_lift, row_ptr=row_ptr, col_idx=np.array([c for (_, c, _) in ent], dtype=np.int32),
+                 val=np.array([v for (_, _, v) in ent]), b=None)
+    # simulation directions: the output rows (as explicit vectors, 0 in the lifted coordinate)
+    nb = n_lift - 1 if (p["op"] == "csr" and p.get("b") is not None) else n_lift
+    gens = []
+    for o in p["outs"]:
+        v = _dense(o, p, nb)
+        nz = np.nonzero(v)[0]
+        gens.append({"kind": "sparse", "idx": nz.astype(np.int64), "val": v[nz]})
+    outs = []
+    for v in fwd:
+        nz = np.nonzero(v)[0]
+        outs.append({"kind": "sparse", "idx": nz.astype(np.int64), "val": v[nz]})
+    q.update(gens=gens, outs=outs, center=None, z_lo=np.zeros(len(gens)), z_hi=np.zeros(len(gens)),
+             thresholds=[], name=p.get("name", "") + "_T")
+    return q
+
+
+def krylov_project_transpose(p, method=None):
+    """Basis-matrix sequence by the transpose dynamics: one Krylov simulation per output row,
+    projected with E^T, transposed back: coeff[j][r][d] ~= C_r e^{A t_j} v_d. Same return layout as
+    krylov_project; per_dir / lemma1 are per simulation (output row)."""
+    q = transpose_problem(p)
+    res = krylov_project(q, method=method or ("arnoldi" if q["op"] == "csr" else p["method"]))
+    res["coeff"] = np.ascontiguousarray(np.transpose(res["coeff"], (0, 2, 1)))
+    return res
+
+
 def z_bounds(p):
     """Box bounds per direction; the fixed-term direction has z_f = 1."""
     lo = list(np.asarray(p["z_lo"], dtype=np.float64))

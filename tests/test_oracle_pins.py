@@ -503,3 +503,79 @@ def test_adaptive_k_reproduces_paper_m100():
     assert r["k_eff"] == 544
     assert abs(r["bound"] - 5.8e-7) <= 0.02 * 5.8e-7
     assert r["checks"][-2][0] == 494 and r["checks"][-2][1] > 1e-6
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-2: transpose dynamics, min(i, o) simulations (§4.1)
+# ---------------------------------------------------------------------------------------------
+def test_transpose_oscillator_paper_example():
+    """one simulation of A^T from the output direction, projected with E^T, gives the basis
+    row (0.707, 3.54) at 3pi/4; same verdict (unsafe at step 3) and witness y0 = 4 sqrt2 - 5."""
+    g = json.load(open(os.path.join(GOLD, "oscillator.json")))
+    p = W.oscillator()
+    res = oracle.krylov_project_transpose(p)
+    assert len(res["per_dir"]) == 1  # o = 1 simulation instead of i + 1 = 2
+    row = res["coeff"][3, 0, :]
+    assert np.allclose(row, g["basis_row_3pi4"]["value"], atol=g["basis_row_3pi4"]["printed_digits_tol"])
+    cb = oracle.check_box(p, res["coeff"])
+    assert cb["found"] and cb["step"] == g["first_unsafe_step"]["value"]
+    assert abs(cb["z"][0] - (4 * math.sqrt(2) - 5)) <= 1e-12
+
+
+def test_transpose_problem_matrix_is_lifted_transpose():
+    """The explicit A'^T equals the transpose of the augmented matrix [[A, b], [0, 0]], built
+    independently with numpy."""
+    rp, ci, va, dense = W.random_csr(30, 4, seed=3)
+    b = np.random.default_rng(4).uniform(-1, 1, 30)
+    p = {"op": "csr", "n": 30, "row_ptr": rp, "col_idx": ci, "val": va, "b": b, "gens": [W.sparse([0], [1.0])],
+         "z_lo": [0.0], "z_hi": [1.0], "center": None, "outs": [W.allv()], "step": 0.1, "n_steps": 3, "k": 4,
+         "method": "arnoldi"}
+    q = oracle.transpose_problem(p)
+    Aq = sp.csr_matrix((q["val"], q["col_idx"], q["row_ptr"]), shape=(31, 31)).toarray()
+    Ap = np.zeros((31, 31))
+    Ap[:30, :30] = dense
+    Ap[:30, 30] = b
+    assert np.array_equal(Aq, Ap.T)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_transpose_equals_dense_expm_when_exact(seed):
+    """Random affine CSR system (n = 24, lifted to 25), 5 generators + center, 3 output rows, k = 25 >= the
+    Krylov dimension: forward (6 simulations) and transpose (3 simulations) both equal C' e^{A' t} E (scipy)."""
+    n = 24
+    rp, ci, va, dense = W.random_csr(n, 4, seed=seed, scale=0.5)
+    rng = np.random.default_rng(seed + 10)
+    b = rng.uniform(-1, 1, n)
+    p = {"name": "rnd", "op": "csr", "n": n, "row_ptr": rp, "col_idx": ci, "val": va, "b": b,
+         "gens": [W.sparse([i], [1.0]) for i in range(5)], "z_lo": -np.ones(5), "z_hi": np.ones(5),
+         "center": W.sparse([7, 9], [0.5, -1.0]),
+         "outs": [W.sparse(list(range(n)), list(rng.standard_normal(n))) for _ in range(3)],
+         "step": 0.05, "n_steps": 40, "k": n + 1, "method": "arnoldi", "thresholds": []}
+    fw = oracle.krylov_project(p)["coeff"]
+    tr = oracle.krylov_project_transpose(p)["coeff"]
+    Ap = np.zeros((n + 1, n + 1))
+    Ap[:n, :n] = dense
+    Ap[:n, n] = b
+    C = np.zeros((3, n + 1))
+    for r, o in enumerate(p["outs"]):
+        C[r, o["idx"]] = o["val"]
+    E = np.array(oracle.directions(p)).T
+    scale = np.abs(fw).max()
+    for j in range(0, 41, 5):
+        ref = C @ sla.expm(Ap * (j * 0.05)) @ E
+        assert np.max(np.abs(fw[j] - ref)) <= 1e-11 * scale
+        assert np.max(np.abs(tr[j] - ref)) <= 1e-11 * scale
+
+
+def test_transpose_config1_equals_dense_expm():
+    """C1: o = 1 simulation of the (symmetric) stencil from the center cell, projected on the 8 unit
+    generators, equals O e^{At} E (scipy) — one simulation instead of eight."""
+    p = W.config1()
+    res = oracle.krylov_project_transpose(p)
+    assert len(res["per_dir"]) == 1
+    A = kron_laplacian(5, 5, 5, 0.01).toarray()
+    O = np.array([W.dense_vec(o, p) for o in p["outs"]])
+    E = np.array([W.dense_vec(g, p) for g in p["gens"]]).T
+    scale = np.abs(res["coeff"]).max()
+    for j in range(0, p["n_steps"] + 1, 9):
+        assert np.max(np.abs(res["coeff"][j] - O @ sla.expm(A * (j * p["step"])) @ E)) <= 1e-12 * scale
