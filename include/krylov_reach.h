@@ -56,6 +56,13 @@ typedef enum { KR_VEC_SPARSE = 0, KR_VEC_BOX = 1, KR_VEC_ALL = 2 } kr_vec_kind;
  *  KR_BC_ROBIN:     insulated plus exchange with a zero ambient: the face cell's diagonal also gets -gamma
  *                   (gamma in units of A, e.g. 0.01 * 0.5 / h for the paper's x = 1 face).             */
 typedef enum { KR_BC_DIRICHLET = 0, KR_BC_INSULATED = 1, KR_BC_ROBIN = 2 } kr_bc;
+/* Which simulations compute the basis matrix C e^{A t} E (§4.1):
+ *  KR_SIM_FORWARD:   one Krylov simulation of x' = A x per direction (generator columns of E + v_f);
+ *  KR_SIM_TRANSPOSE: one simulation of x' = A'^T x per output row C_r^T, projected with E^T and
+ *                    transposed back ("(E^T e^{A^T t} C^T)^T") — o simulations instead of i;
+ *                    with an affine term the lifted A' = [[A, b], [0, 0]] is transposed explicitly;
+ *  KR_SIM_AUTO:      the smaller of the two counts, min(i, o).                           */
+typedef enum { KR_SIM_FORWARD = 0, KR_SIM_TRANSPOSE = 1, KR_SIM_AUTO = 2 } kr_sim_dir;
 #define KR_K_MAX_FIXED_PADE 64   /* fixed k up to this uses per-step Pade-13 exponentials            */
 #define KR_K_MAX 16384           /* Lanczos (stencil) Krylov dimension cap; Arnoldi stays <= 64     */
 
@@ -116,6 +123,9 @@ typedef struct {
        the BASELINE configs) and the Robin exchange coefficients (used where bc = KR_BC_ROBIN, >= 0).   */
     int32_t bc[6];
     double gamma[6];
+    /* Simulation direction (kr_sim_dir; 0 = forward). TRANSPOSE needs n_dir <= 64 (the directions become
+       the projection rows) and is not combined with eps > 0.                                          */
+    int32_t sim_dir;
     /* Partitioning. */
     int32_t part;               /* kr_partition. ZSLAB: STENCIL7 + LANCZOS only; DIRS: any             */
     int32_t virtual_slabs;      /* ZSLAB without a comm: emulate P = virtual_slabs slabs in this process
@@ -132,7 +142,8 @@ typedef struct {
 
 typedef struct kr_handle kr_handle;
 
-/* Per-direction diagnostics (Lemma 1). */
+/* Per-simulation diagnostics (Lemma 1): one per direction (forward) or per output row
+ * (transpose mode); krylov_sim_info gives the count. */
 typedef struct {
     int32_t k_eff;              /* Krylov dimension actually used                                       */
     double beta0;               /* ||v_d||                                                              */
@@ -162,8 +173,8 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out);
 /* Run the hot path: start vectors, k Krylov steps per direction (fused stencil Lanczos in one HBM pass
  * per step, or batched SpMM + Gram-Schmidt Arnoldi), batched k x k Pade exponentials for every t_j
  * (Eq. 2) and the projection through P = C V_k (Alg. 4).
- * coeff: HOST [(n_steps+1)][n_out][n_dir] basis-matrix entries c[j][r][d] ~= C_r e^{A t_j} v_d.
- * stats: HOST [n_dir] or NULL. Either output may be NULL to leave the results on the device only
+ * coeff: HOST [(n_steps+1)][n_out][n_dir] basis-matrix entries c[j][r][d] ~= C_r e^{A t_j} v_d (same
+ * layout in transpose mode). stats: HOST [n_sim] (krylov_sim_info) or NULL. Either output may be NULL to leave the results on the device only
  * (then krylov_check_box still works). Synchronises the stream before returning. */
 kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats);
 
@@ -179,6 +190,11 @@ kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr
 void krylov_reach_destroy(kr_handle* h);
 
 const char* krylov_last_error(void);
+
+/* Simulation layout of h: *transposed = 1 in transpose mode (KR_SIM_TRANSPOSE, or AUTO with n_out < n_dir),
+ * *n_sim = number of Krylov simulations (= length of the stats array of krylov_project): n_dir forward,
+ * n_out transposed. Either pointer may be NULL. */
+kr_status krylov_sim_info(const kr_handle* h, int32_t* transposed, int32_t* n_sim);
 
 /* Number of this library's kernel launches issued so far on h (graph nodes counted per replay). */
 int64_t krylov_launch_count(const kr_handle* h);

@@ -222,6 +222,12 @@ def expm_e1_times(H, step, n_steps):
     return X
 
 
+def _exp_or_inf(x):
+    """e^x, +inf past the fp64 range: Lemma 1's e^{max(mu,0) T} factor for lifted affine systems, whose
+    Gershgorin mu is large (DESIGN R16: the bound is then astronomically loose, diagnostic only)."""
+    return math.exp(x) if x < 709.0 else math.inf
+
+
 def checkpoints(k_max):
     """Alg. 2/4 error-check points: k = 4, then k <- ceil(1.1 k) evaluated in
     fp64 (the paper's k = 63, 544, 5932 lie on this sequence, not on the exact-rational one)."""
@@ -252,7 +258,8 @@ def lemma1_bound(h_next, X, step, mu=0.0):
     int_0^T |e_k^T e^{H t} e_1| dt, trapezoid on the t_j grid (reading: DESIGN R16)."""
     h = np.abs(X[:, -1])
     T = (X.shape[0] - 1) * step
-    return h_next * math.exp(max(mu, 0.0) * T) * float(np.sum(0.5 * step * (h[1:] + h[:-1])))
+    base = h_next * float(np.sum(0.5 * step * (h[1:] + h[:-1])))
+    return 0.0 if base == 0.0 else base * _exp_or_inf(max(mu, 0.0) * T)
 
 
 def lanczos_adaptive(p, v, eps, k_max):
@@ -353,7 +360,8 @@ def krylov_project(p, method=None):
         # Lemma 1: ||v|| h_{k+1,k} e^{max(mu,0) T} int_0^T |e_k^T e^{Ht} e_1| dt, trapezoid
         h = np.abs(X[:, -1])
         integral = float(np.sum(0.5 * p["step"] * (h[1:] + h[:-1]))) if N > 0 else 0.0
-        lemma[d] = r["beta0"] * r["h_next"] * math.exp(max(mu, 0.0) * T) * integral
+        base = r["beta0"] * r["h_next"] * integral
+        lemma[d] = 0.0 if base == 0.0 else base * _exp_or_inf(max(mu, 0.0) * T)
         per_dir.append(r)
     return {"coeff": coeff, "per_dir": per_dir, "lemma1": lemma, "mu": mu,
             "times": np.arange(N + 1) * p["step"]}

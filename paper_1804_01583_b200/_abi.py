@@ -19,6 +19,7 @@ KR_GE, KR_LE, KR_EQ, KR_NONE = 0, 1, 2, 3
 KR_VEC_SPARSE, KR_VEC_BOX, KR_VEC_ALL = 0, 1, 2
 KR_BC_DIRICHLET, KR_BC_INSULATED, KR_BC_ROBIN = 0, 1, 2
 KR_K_MAX_FIXED_PADE, KR_K_MAX = 64, 16384
+KR_SIM_FORWARD, KR_SIM_TRANSPOSE, KR_SIM_AUTO = 0, 1, 2
 
 
 class kr_vec(C.Structure):
@@ -36,7 +37,7 @@ class kr_problem(C.Structure):
         ("n_out", C.c_int32), ("out", C.POINTER(kr_vec)),
         ("step", C.c_double), ("n_steps", C.c_int64),
         ("k", C.c_int32), ("method", C.c_int32), ("eps", C.c_double),
-        ("bc", C.c_int32 * 6), ("gamma", C.c_double * 6),
+        ("bc", C.c_int32 * 6), ("gamma", C.c_double * 6), ("sim_dir", C.c_int32),
         ("part", C.c_int32), ("virtual_slabs", C.c_int32), ("comm", C.c_void_p), ("device", C.c_int32),
         ("stream", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
     ]
@@ -59,7 +60,7 @@ EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "k
            "krylov_reach_destroy", "krylov_last_error", "krylov_launch_count", "krylov_last_timing",
            "krylov_comm_unique_id", "krylov_comm_create", "krylov_comm_destroy", "krylov_zslab_range",
            "krylov_krylov_data", "krylov_transfer_bytes", "krylov_zslab_halo_plan", "krylov_tridiag",
-           "krylov_adaptive_checks", "krylov_last_timing_large"]
+           "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info"]
 
 _lib = None
 
@@ -90,6 +91,7 @@ def lib():
     L.krylov_comm_destroy.argtypes = [vp]
     L.krylov_comm_destroy.restype = None
     L.krylov_krylov_data.argtypes = [vp, C.c_int32, vp, vp]
+    L.krylov_sim_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.krylov_last_timing_large.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     L.krylov_tridiag.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.POINTER(C.c_int32)]
     L.krylov_adaptive_checks.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.POINTER(C.c_int32)]

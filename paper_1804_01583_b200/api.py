@@ -11,6 +11,7 @@ from . import _abi as A
 _METHOD = {"auto": A.KR_AUTO, "arnoldi": A.KR_ARNOLDI, "lanczos": A.KR_LANCZOS}
 _PART = {None: A.KR_PART_NONE, "none": A.KR_PART_NONE, "zslab": A.KR_PART_ZSLAB, "dirs": A.KR_PART_DIRS}
 _KIND = {"sparse": A.KR_VEC_SPARSE, "box": A.KR_VEC_BOX, "all": A.KR_VEC_ALL}
+_SIM = {None: A.KR_SIM_FORWARD, "forward": A.KR_SIM_FORWARD, "transpose": A.KR_SIM_TRANSPOSE, "auto": A.KR_SIM_AUTO}
 
 
 def _p(a):
@@ -21,7 +22,7 @@ class _Marshal:
     """Builds a kr_problem and keeps every numpy buffer alive while the C call borrows it."""
 
     def __init__(self, prob, device=0, stream=None, workspace=None, workspace_bytes=0, comm=None, part=None,
-                 virtual_slabs=0, method=None):
+                 virtual_slabs=0, method=None, sim=None):
         self.keep = []
         p = A.kr_problem()
         if prob["op"] == "stencil":
@@ -60,6 +61,7 @@ class _Marshal:
         p.step, p.n_steps = float(prob["step"]), int(prob["n_steps"])
         p.k = int(prob["k"])
         p.eps = float(prob.get("eps", 0.0) or 0.0)
+        p.sim_dir = _SIM[sim or prob.get("sim")]
         p.method = _METHOD[method or prob.get("method", "auto")]
         p.part = _PART[part]
         p.virtual_slabs = int(virtual_slabs)
@@ -107,22 +109,25 @@ class KrylovReach:
     check_box() the per-step safety check."""
 
     def __init__(self, prob, device=0, stream=None, workspace=None, workspace_bytes=0, comm=None, part=None,
-                 virtual_slabs=0, method=None):
+                 virtual_slabs=0, method=None, sim=None):
         self.prob = prob
-        m = _Marshal(prob, device, stream, workspace, workspace_bytes, comm, part, virtual_slabs, method)
+        m = _Marshal(prob, device, stream, workspace, workspace_bytes, comm, part, virtual_slabs, method, sim)
         h = C.c_void_p()
         A.check(A.lib().krylov_reach_create(C.byref(m.p), C.byref(h)))
         self.h = h
         self.n_out = len(prob["outs"])
         self.n_dir = n_dirs(prob)
         self.n_steps = int(prob["n_steps"])
+        tr, ns = C.c_int32(), C.c_int32()
+        A.check(A.lib().krylov_sim_info(h, C.byref(tr), C.byref(ns)))
+        self.transposed, self.n_sim = bool(tr.value), int(ns.value)
 
     def project(self, want=True):
         if not want:
             A.check(A.lib().krylov_project(self.h, None, None))
             return None, None
         coeff = np.empty((self.n_steps + 1, self.n_out, self.n_dir))
-        st = (A.kr_dir_stats * self.n_dir)()
+        st = (A.kr_dir_stats * self.n_sim)()
         A.check(A.lib().krylov_project(self.h, _p(coeff), st))
         stats = [{"k_eff": s.k_eff, "beta0": s.beta0, "h_next": s.h_next, "lemma1": s.lemma1_bound} for s in st]
         return coeff, stats

@@ -232,6 +232,7 @@ void validate(const kr_problem* p) {
         if (p->k < 1 || p->k > kmax)
             KR_THROW(KR_EINVAL, "k must be 1.." + std::to_string(kmax) + (stencil_lz ? "" : " (Arnoldi / CSR)"));
         if (!(p->eps >= 0.0) || !finite(p->eps)) KR_THROW(KR_EINVAL, "eps must be >= 0");
+        if (p->sim_dir < KR_SIM_FORWARD || p->sim_dir > KR_SIM_AUTO) KR_THROW(KR_EINVAL, "bad sim_dir");
         if (p->eps > 0.0 && !stencil_lz) KR_THROW(KR_EINVAL, "adaptive k (eps > 0) needs the stencil Lanczos path");
         for (int f = 0; f < 6; ++f) {
             if (p->bc[f] < KR_BC_DIRICHLET || p->bc[f] > KR_BC_ROBIN) KR_THROW(KR_EINVAL, "bad boundary condition");
@@ -327,6 +328,128 @@ kr_status guarded(F&& f) {
     }
 }
 
+int n_dirs_of(const kr_problem* p) { return p->n_gen + ((p->center || p->b) ? 1 : 0); }
+
+bool transposed_mode(const kr_problem* p) {
+    if (p->sim_dir == KR_SIM_TRANSPOSE) return true;
+    if (p->sim_dir == KR_SIM_AUTO) return p->n_out < n_dirs_of(p);
+    return false;
+}
+
+// Host storage of the transposed problem (borrowed by create, like the caller's arrays).
+struct TransposeStore {
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> val;
+    std::vector<kr_vec> gens, outs;
+    std::vector<int64_t> fidx;
+    std::vector<double> fval, zlo, zhi;
+};
+
+// The transpose-dynamics problem of §4.1: simulate x' = A'^T x from each output row C_r^T
+// and project with E^T. A'^T of the lifted CSR is built explicitly: A'^T = [[A^T, 0], [b^T, 0]]
+// (counting sort by column, rows of A' scanned in order, so each row of A'^T has ascending columns).
+// The stencil operator is symmetric (also with insulated / Robin faces) and is kept as is.
+void build_transposed(const kr_problem* p, TransposeStore& T, kr_problem& q) {
+    q = *p;
+    const int nd = n_dirs_of(p);
+    if (nd > KR_MAX_OUT) KR_THROW(KR_EINVAL, "transpose mode: at most 64 directions (they become projection rows)");
+    if (p->eps > 0.0) KR_THROW(KR_EINVAL, "transpose mode is not combined with adaptive k (eps > 0)");
+    const bool csr = p->op == KR_OP_CSR;
+    const int64_t n = n_state(p);
+    const bool lifted = csr && p->b;
+    if (csr) {
+        const int64_t N = n + (lifted ? 1 : 0);
+        T.rp.assign((size_t)N + 1, 0);
+        for (int64_t e = 0; e < p->nnz; ++e) T.rp[(size_t)p->col_idx[e] + 1]++;
+        if (lifted)
+            for (int64_t r = 0; r < n; ++r)
+                if (p->b[r] != 0.0) T.rp[(size_t)n + 1]++;
+        for (int64_t r = 0; r < N; ++r) T.rp[(size_t)r + 1] += T.rp[(size_t)r];
+        T.ci.resize((size_t)T.rp[(size_t)N]);
+        T.val.resize((size_t)T.rp[(size_t)N]);
+        std::vector<int64_t> next(T.rp.begin(), T.rp.end() - 1);
+        for (int64_t r = 0; r < n; ++r) {
+            for (int64_t e = p->row_ptr[r]; e < p->row_ptr[r + 1]; ++e) {
+                const int64_t pos = next[(size_t)p->col_idx[e]]++;
+                T.ci[(size_t)pos] = (int32_t)r;
+                T.val[(size_t)pos] = p->val[e];
+            }
+            if (lifted && p->b[r] != 0.0) {  // A'[r][n] = b_r  ->  A'^T[n][r] = b_r
+                const int64_t pos = next[(size_t)n]++;
+                T.ci[(size_t)pos] = (int32_t)r;
+                T.val[(size_t)pos] = p->b[r];
+            }
+        }
+        q.n = N;
+        q.nnz = T.rp[(size_t)N];
+        q.row_ptr = T.rp.data();
+        q.col_idx = T.ci.data();
+        q.val = T.val.data();
+        q.b = nullptr;
+    }
+    auto unlifted = [&](kr_vec v) {  // an ALL vector of the unlifted space stays off the lifted coordinate
+        if (lifted && v.kind == KR_VEC_ALL) {
+            v.kind = KR_VEC_BOX;
+            v.lo[0] = 0;
+            v.hi[0] = n;
+        }
+        return v;
+    };
+    for (int r = 0; r < p->n_out; ++r) T.gens.push_back(unlifted(p->out[r]));
+    T.zlo.assign(p->n_out, 0.0);
+    T.zhi.assign(p->n_out, 0.0);
+    for (int d = 0; d < p->n_gen; ++d) T.outs.push_back(unlifted(p->gen[d]));
+    if (nd > p->n_gen) {  // v_f = [c; 1] (lifted) or c
+        if (!lifted) {
+            T.outs.push_back(*p->center);
+        } else {
+            if (p->center) {
+                const kr_vec& c = *p->center;
+                if (c.kind == KR_VEC_SPARSE) {
+                    for (int64_t e = 0; e < c.nnz; ++e) {
+                        T.fidx.push_back(c.idx[e]);
+                        T.fval.push_back(c.val[e]);
+                    }
+                } else {
+                    const int64_t lo = c.kind == KR_VEC_ALL ? 0 : c.lo[0], hi = c.kind == KR_VEC_ALL ? n : c.hi[0];
+                    for (int64_t i = lo; i < hi; ++i) {
+                        T.fidx.push_back(i);
+                        T.fval.push_back(c.value);
+                    }
+                }
+            }
+            T.fidx.push_back(n);
+            T.fval.push_back(1.0);
+            kr_vec f{};
+            f.kind = KR_VEC_SPARSE;
+            f.nnz = (int64_t)T.fidx.size();
+            f.idx = T.fidx.data();
+            f.val = T.fval.data();
+            T.outs.push_back(f);
+        }
+    }
+    q.n_gen = p->n_out;
+    q.gen = T.gens.data();
+    q.z_lo = T.zlo.data();
+    q.z_hi = T.zhi.data();
+    q.center = nullptr;
+    q.n_out = nd;
+    q.out = T.outs.data();
+    q.sim_dir = KR_SIM_FORWARD;
+}
+
+// final layout c[j][r][d] = simulation layout s[j][d][r]
+__global__ void transpose_coeff_kernel(const double* sim, double* cf, int64_t np1, int cf_nout, int cf_ndir) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= np1 * cf_nout * cf_ndir) return;
+    const int d = (int)(e % cf_ndir);
+    const int64_t jr = e / cf_ndir;
+    const int r = (int)(jr % cf_nout);
+    const int64_t j = jr / cf_nout;
+    cf[e] = sim[(j * cf_ndir + d) * cf_nout + r];
+}
+
 void free_handle(kr_handle* h) {
     if (!h) return;
     if (h->graph_ready) cudaGraphExecDestroy(h->gexec);
@@ -390,7 +513,15 @@ kr_status krylov_workspace_bytes(const kr_problem* p, size_t* bytes) {
         validate(p);
         if (!bytes) KR_THROW(KR_EINVAL, "NULL bytes");
         const int rank = p->comm ? p->comm->rank : 0, world = p->comm ? p->comm->world : 1;
-        *bytes = plan(p, rank, world).state_bytes;
+        if (transposed_mode(p)) {
+            TransposeStore T;
+            kr_problem q;
+            build_transposed(p, T, q);
+            validate(&q);
+            *bytes = plan(&q, rank, world).state_bytes;
+        } else {
+            *bytes = plan(p, rank, world).state_bytes;
+        }
     });
 }
 
@@ -408,7 +539,51 @@ kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int
 
 void krylov_comm_destroy(kr_comm* c) { kr_comm_destroy_impl(c); }
 
+static kr_status create_impl(const kr_problem* p, kr_handle** out);
+
 kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
+    if (!p || !transposed_mode(p)) return create_impl(p, out);
+    TransposeStore T;
+    kr_problem q;
+    kr_status st = guarded([&] {
+        validate(p);
+        build_transposed(p, T, q);
+    });
+    if (st != KR_OK) return st;
+    st = create_impl(&q, out);
+    if (st != KR_OK) return st;
+    kr_handle* h = *out;
+    st = guarded([&] {  // final layout: the caller's outputs and directions
+        h->transposed = true;
+        h->cf_nout = p->n_out;
+        h->cf_ndir = n_dirs_of(p);
+        h->zlo.clear();
+        h->zhi.clear();
+        for (int d = 0; d < p->n_gen; ++d) {
+            h->zlo.push_back(p->z_lo[d]);
+            h->zhi.push_back(p->z_hi[d]);
+        }
+        if (h->cf_ndir > p->n_gen) {
+            h->zlo.push_back(1.0);
+            h->zhi.push_back(1.0);
+        }
+        h->d_zlo = upload(h, h->zlo.data(), h->zlo.size());
+        h->d_zhi = upload(h, h->zhi.data(), h->zhi.size());
+        const int64_t np1 = h->n_steps + 1;
+        h->d_cf = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->cf_nout * h->cf_ndir * 8));
+        h->d_box = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->cf_nout * (8 + 8 + 4) + 16));
+        h->d_cex = dalloc(h, 64 + (size_t)h->cf_ndir * 8);
+        h->d_sense = reinterpret_cast<int32_t*>(dalloc(h, (size_t)h->cf_nout * 4));
+        h->d_thr = reinterpret_cast<double*>(dalloc(h, (size_t)h->cf_nout * 8));
+    });
+    if (st != KR_OK) {
+        free_handle(h);
+        *out = nullptr;
+    }
+    return st;
+}
+
+static kr_status create_impl(const kr_problem* p, kr_handle** out) {
     kr_handle* h = nullptr;
     kr_status st = guarded([&] {
         if (!out) KR_THROW(KR_EINVAL, "NULL out");
@@ -519,6 +694,9 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         KR_CUDA(cudaMemsetAsync(h->d_hnext, 0, (size_t)ndl * 8, h->stream));
         KR_CUDA(cudaMemsetAsync(h->d_status, 0, (size_t)ndl * 4 + 64, h->stream));
         h->d_coeff = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * h->n_dir * 8));
+        h->d_cf = h->d_coeff;
+        h->cf_nout = h->n_out;
+        h->cf_ndir = h->n_dir;
         if (p->part == KR_PART_DIRS && h->world > 1) {
             const int ndl_max = (h->n_dir + h->world - 1) / h->world;
             h->d_coeff_loc = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * ndl_max * 8 * h->world));
@@ -719,6 +897,13 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                 kr_nccl_allgather(h->comm, h->d_gather + (size_t)h->rank * ndl_max * 4, h->d_gather,
                                   (size_t)ndl_max * 4, h->stream);
             }
+            if (h->transposed) {
+                const int64_t tot = np1 * h->cf_nout * h->cf_ndir;
+                transpose_coeff_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(h->d_coeff, h->d_cf, np1,
+                                                                                            h->cf_nout, h->cf_ndir);
+                KR_CUDA(cudaGetLastError());
+                h->launches++;
+            }
         };
         auto enqueue = [&](bool ev) {
             KR_CUDA(kr_event_record(h->ev_it0, h->stream));
@@ -858,8 +1043,8 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                                     (h->path == PATH_FUSED_LANCZOS ? (int64_t)h->slabs.size() : 1);
         }
         if (coeff) {
-            KR_CUDA(cudaMemcpy(coeff, h->d_coeff, (size_t)np1 * h->n_out * h->n_dir * 8, cudaMemcpyDeviceToHost));
-            h->d2h_bytes += (int64_t)np1 * h->n_out * h->n_dir * 8;
+            KR_CUDA(cudaMemcpy(coeff, h->d_cf, (size_t)np1 * h->cf_nout * h->cf_ndir * 8, cudaMemcpyDeviceToHost));
+            h->d2h_bytes += (int64_t)np1 * h->cf_nout * h->cf_ndir * 8;
         }
         if (stats) h->d2h_bytes += (int64_t)ndl * 28;
         if (stats) {
@@ -899,20 +1084,20 @@ kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr
     return guarded([&] {
         if (!h || !sense || !thr || !cex) KR_THROW(KR_EINVAL, "NULL argument");
         if (!h->projected) KR_THROW(KR_ESTATE, "krylov_check_box before krylov_project");
-        for (int r = 0; r < h->n_out; ++r) {
+        for (int r = 0; r < h->cf_nout; ++r) {
             if (sense[r] < 0 || sense[r] > KR_NONE) KR_THROW(KR_EINVAL, "bad sense");
             if (sense[r] != KR_NONE && !std::isfinite(thr[r])) KR_THROW(KR_ENONFINITE, "non-finite threshold");
         }
         KR_CUDA(cudaSetDevice(h->device));
         const int64_t np1 = h->n_steps + 1;
-        const int64_t total = np1 * h->n_out;
+        const int64_t total = np1 * h->cf_nout;
         int32_t* ds = h->d_sense;
         double* dt = h->d_thr;
-        KR_CUDA(cudaMemcpyAsync(ds, sense, (size_t)h->n_out * 4, cudaMemcpyHostToDevice, h->stream));
-        KR_CUDA(cudaMemcpyAsync(dt, thr, (size_t)h->n_out * 8, cudaMemcpyHostToDevice, h->stream));
-        h->h2d_bytes += (int64_t)h->n_out * 12;
+        KR_CUDA(cudaMemcpyAsync(ds, sense, (size_t)h->cf_nout * 4, cudaMemcpyHostToDevice, h->stream));
+        KR_CUDA(cudaMemcpyAsync(dt, thr, (size_t)h->cf_nout * 8, cudaMemcpyHostToDevice, h->stream));
+        h->h2d_bytes += (int64_t)h->cf_nout * 12;
         kr_box_enqueue(h, ds, dt);
-        h->d2h_bytes += (lo ? total * 8 : 0) + (hi ? total * 8 : 0) + 32 + (int64_t)h->n_dir * 8;
+        h->d2h_bytes += (lo ? total * 8 : 0) + (hi ? total * 8 : 0) + 32 + (int64_t)h->cf_ndir * 8;
         if (lo) KR_CUDA(cudaMemcpyAsync(lo, h->d_box, total * 8, cudaMemcpyDeviceToHost, h->stream));
         if (hi) KR_CUDA(cudaMemcpyAsync(hi, h->d_box + total, total * 8, cudaMemcpyDeviceToHost, h->stream));
         struct {
@@ -923,8 +1108,8 @@ kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr
         } dc;
         static_assert(sizeof(dc) <= 64, "cex");
         KR_CUDA(cudaMemcpyAsync(&dc, h->d_cex, sizeof(dc), cudaMemcpyDeviceToHost, h->stream));
-        std::vector<double> zw(h->n_dir);
-        KR_CUDA(cudaMemcpyAsync(zw.data(), reinterpret_cast<char*>(h->d_cex) + 64, (size_t)h->n_dir * 8,
+        std::vector<double> zw(h->cf_ndir);
+        KR_CUDA(cudaMemcpyAsync(zw.data(), reinterpret_cast<char*>(h->d_cex) + 64, (size_t)h->cf_ndir * 8,
                                 cudaMemcpyDeviceToHost, h->stream));
         KR_CUDA(cudaStreamSynchronize(h->stream));
         cex->found = dc.found;
@@ -933,7 +1118,7 @@ kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr
         cex->y = dc.y;
         cex->time = dc.found ? (double)dc.step * h->step : 0.0;
         if (z_witness)
-            for (int d = 0; d < h->n_dir; ++d) z_witness[d] = zw[d];
+            for (int d = 0; d < h->cf_ndir; ++d) z_witness[d] = zw[d];
     });
 }
 
@@ -1016,6 +1201,13 @@ kr_status krylov_last_timing_large(const kr_handle* h, double* expm_ms, int32_t*
     if (!h) return KR_EINVAL;
     if (expm_ms) *expm_ms = h->large_ms;
     if (n_evals) *n_evals = h->large_evals;
+    return KR_OK;
+}
+
+kr_status krylov_sim_info(const kr_handle* h, int32_t* transposed, int32_t* n_sim) {
+    if (!h) return KR_EINVAL;
+    if (transposed) *transposed = h->transposed ? 1 : 0;
+    if (n_sim) *n_sim = h->n_dir;
     return KR_OK;
 }
 

@@ -93,17 +93,17 @@ size_t kr_box_cex_bytes() { return sizeof(DevCex); }
 
 void kr_box_enqueue(kr_handle* h, const int32_t* d_sense, const double* d_thr) {
     const int64_t np1 = h->n_steps + 1;
-    const int64_t total = np1 * h->n_out;
+    const int64_t total = np1 * h->cf_nout;
     double* lo = h->d_box;
     double* hi = h->d_box + total;
     int32_t* viol = reinterpret_cast<int32_t*>(h->d_box + 2 * total);
     box_bounds_kernel<<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(
-        h->d_coeff, np1, h->n_out, h->n_dir, h->d_zlo, h->d_zhi, d_sense, d_thr, lo, hi, viol);
+        h->d_cf, np1, h->cf_nout, h->cf_ndir, h->d_zlo, h->d_zhi, d_sense, d_thr, lo, hi, viol);
     KR_CUDA(cudaGetLastError());
     h->launches++;
     DevCex* cex = reinterpret_cast<DevCex*>(h->d_cex);
     double* zw = reinterpret_cast<double*>(reinterpret_cast<char*>(h->d_cex) + 64);
-    first_violation_kernel<<<1, 256, 0, h->stream>>>(h->d_coeff, lo, hi, viol, total, h->n_out, h->n_dir, h->d_zlo,
+    first_violation_kernel<<<1, 256, 0, h->stream>>>(h->d_cf, lo, hi, viol, total, h->cf_nout, h->cf_ndir, h->d_zlo,
                                                      h->d_zhi, d_sense, d_thr, cex, zw);
     KR_CUDA(cudaGetLastError());
     h->launches++;

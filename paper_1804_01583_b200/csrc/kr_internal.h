@@ -112,7 +112,11 @@ struct kr_handle {
     int64_t n;  // unlifted state count
     int64_t N;  // operator dimension (n or n+1)
     bool lifted;
-    int32_t n_gen, n_dir, n_out, k;
+    int32_t n_gen, n_dir, n_out, k;  // simulation view: n_dir simulations, n_out projection rows each
+    // final basis-matrix layout [(N+1)][cf_nout][cf_ndir] (= n_out / n_dir, swapped in transpose mode)
+    bool transposed = false;
+    int32_t cf_nout = 0, cf_ndir = 0;
+    double* d_cf = nullptr;  // final coefficients (= d_coeff unless transposed)
     int64_t n_steps;
     double step;
     double mu;  // Gershgorin upper bound of lambda_max(sym A)

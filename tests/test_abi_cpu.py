@@ -130,3 +130,15 @@ def test_product_fails_loudly_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(_abi, "_lib", None)
     with pytest.raises(ImportError):
         _abi.lib()
+
+
+def test_transpose_mode_host_side():
+    """NEXT-2: the transposed problem's workspace is sized for o simulations of the lifted A'^T."""
+    from paper_1804_01583_b200 import KrylovError, krylov_workspace_bytes
+    q = W.config2()
+    assert krylov_workspace_bytes(q, sim="transpose") == 3 * 42 * 20001 * 8 + 512
+    assert krylov_workspace_bytes(q, sim="auto") == 3 * 42 * 20001 * 8 + 512
+    p = W.heat_paper(20)
+    with pytest.raises(KrylovError) as e:
+        krylov_workspace_bytes(p, sim="transpose")  # not combined with adaptive k
+    assert "KR_EINVAL" in str(e.value)

@@ -1,0 +1,78 @@
+"""GPU parity for SURVEY §8(f) NEXT-2: the basis matrix by transpose dynamics (§4.1) — o
+Krylov simulations of x' = A'^T x from the output rows, projected with E^T — against the oracle's
+transpose mode (tolerance tests/parity.py), verdicts identical, and against the forward mode where both
+are exact."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import assert_coeff, bounds_close
+
+pytestmark = pytest.mark.gpu
+
+
+def run(p, **kw):
+    from paper_1804_01583_b200 import KrylovReach
+    with KrylovReach(p, **kw) as h:
+        coeff, stats = h.project()
+        cb = h.check_box()
+        info = (h.transposed, h.n_sim, h.launch_count())
+    assert info[2] > 0
+    return coeff, stats, cb, info
+
+
+def test_transpose_oscillator_paper_example():
+    p = W.oscillator()
+    coeff, stats, cb, (tr, ns, _) = run(p, sim="transpose")
+    assert tr and ns == 1  # o = 1 simulation
+    res = oracle.krylov_project_transpose(p)
+    assert_coeff(coeff, res["coeff"], "oscillator^T")
+    assert np.allclose(coeff[3, 0], [0.707, 3.54], atol=5e-3)
+    assert cb["found"] and cb["step"] == 3 and abs(cb["z"][0] - (4 * math.sqrt(2) - 5)) <= 1e-12
+
+
+def test_transpose_config1_one_simulation():
+    """C1: 1 simulation from the center cell instead of 8; equal to the forward result (both exact)."""
+    p = W.config1()
+    coeff, stats, cb, (tr, ns, _) = run(p, sim="transpose")
+    assert tr and ns == 1
+    assert_coeff(coeff, oracle.krylov_project_transpose(p)["coeff"], "C1^T")
+    assert_coeff(coeff, oracle.krylov_project(p)["coeff"], "C1^T vs forward")
+    assert not cb["found"]
+    _, _, cb2, _ = run(dict(p, thresholds=[(0, W.GE, 0.02)]), sim="transpose")
+    assert cb2["found"] and cb2["step"] == 74
+
+
+def test_transpose_config2_full_size():
+    """BASELINE configs[1] at full size: 3 simulations of the lifted A'^T (n' = 20001) instead of 21,
+    against the oracle's transpose mode on every step; AUTO picks the transpose (o = 3 < i = 21)."""
+    p = W.config2()
+    coeff, stats, cb, (tr, ns, _) = run(p, sim="auto")
+    assert tr and ns == 3
+    res = oracle.krylov_project_transpose(p)
+    assert_coeff(coeff, res["coeff"], "C2^T")
+    for s, r in zip(stats, res["per_dir"]):
+        assert s["k_eff"] == r["k_eff"]
+    ocb = oracle.check_box(p, res["coeff"], [])
+    zlo, zhi = oracle.z_bounds(p)
+    ok, worst = bounds_close(cb["hi"], ocb["hi"], res["coeff"], zlo, zhi)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("vs", [0, 2])
+def test_transpose_stencil_lanczos(vs):
+    """Fused stencil Lanczos in transpose mode: simulations start at the 4 output rows (center, total heat,
+    two cells), projected on the corner-block generator; 1 and 2 virtual z-slabs."""
+    p = W.heat(30, 4, 30, n_steps=150, my=21, mz=13)
+    coeff, stats, cb, (tr, ns, _) = run(p, sim="transpose", virtual_slabs=vs)
+    assert tr and ns == 4
+    assert_coeff(coeff, oracle.krylov_project_transpose(p)["coeff"], f"heat^T vs={vs}")
+
+
+def test_auto_keeps_forward_when_fewer_directions():
+    p = W.heat(20, 3, 20, n_steps=40)
+    _, stats, _, (tr, ns, _) = run(p, sim="auto")
+    assert not tr and ns == 1
