@@ -430,6 +430,41 @@ def z_bounds(p):
     return np.array(lo), np.array(hi)
 
 
+def check_lp(p, coeff, init_A=None, init_b=None, unsafe_A=None, unsafe_b=None):
+    """The per-step LP of §2.1 in the initial / output spaces (Fig. 2(c); §3,
+    P:467-496) for a general polytope: at step j the constraints are
+        z_lo <= z <= z_hi,   I_z z <= iota            (initial set, "I_x x0 <= iota_x" on z)
+        U_y (B_j z + c_f,j) <= upsilon                 (unsafe set, "U_x x <= upsilon_x" on y = C x)
+    with B_j the generator columns of the basis matrix and c_f,j the fixed-term column (z_f = 1,
+    P:1221-1225). The system is unsafe at the first j where the LP is feasible; the witness is
+    the solver's assignment. Solver: scipy linprog / HiGHS (a library routine), zero objective.
+    Returns dict(feasible [(N+1)] bool, found, step, z, y)."""
+    from scipy.optimize import linprog
+    ng = len(p["gens"])
+    has_fixed = coeff.shape[2] > ng
+    zlo = np.asarray(p["z_lo"], dtype=np.float64)[:ng]
+    zhi = np.asarray(p["z_hi"], dtype=np.float64)[:ng]
+    IA = np.zeros((0, ng)) if init_A is None else np.asarray(init_A, dtype=np.float64).reshape(-1, ng)
+    Ib = np.zeros(0) if init_b is None else np.asarray(init_b, dtype=np.float64).reshape(-1)
+    o = coeff.shape[1]
+    UA = np.zeros((0, o)) if unsafe_A is None else np.asarray(unsafe_A, dtype=np.float64).reshape(-1, o)
+    Ub = np.zeros(0) if unsafe_b is None else np.asarray(unsafe_b, dtype=np.float64).reshape(-1)
+    Np1 = coeff.shape[0]
+    feas = np.zeros(Np1, dtype=bool)
+    res = {"feasible": feas, "found": False, "step": -1, "z": None, "y": None}
+    for j in range(Np1):
+        B = coeff[j, :, :ng]
+        cf = coeff[j, :, ng] if has_fixed else np.zeros(o)
+        A_ub = np.vstack([IA, UA @ B])
+        b_ub = np.concatenate([Ib, Ub - UA @ cf])
+        r = linprog(np.zeros(ng), A_ub=A_ub if A_ub.size else None, b_ub=b_ub if A_ub.size else None,
+                    bounds=list(zip(zlo, zhi)), method="highs")
+        feas[j] = r.status == 0
+        if feas[j] and not res["found"]:
+            res.update(found=True, step=j, z=np.array(r.x), y=B @ np.array(r.x) + cf)
+    return res
+
+
 def check_box(p, coeff, thresholds=None):
     """Per-step interval bounds of each output over the box initial set, the exact LP optimum for a
     box (Fig. 2(c)), the first violating step and a witness.

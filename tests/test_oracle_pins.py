@@ -579,3 +579,71 @@ def test_transpose_config1_equals_dense_expm():
     scale = np.abs(res["coeff"]).max()
     for j in range(0, p["n_steps"] + 1, 9):
         assert np.max(np.abs(res["coeff"][j] - O @ sla.expm(A * (j * p["step"])) @ E)) <= 1e-12 * scale
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-3: general per-step LP (polytope initial set in z, polytope unsafe set in y)
+# ---------------------------------------------------------------------------------------------
+def brute_force_feasible(A, b, lo, hi, tol=1e-9):
+    """Nonempty {z : A z <= b, lo <= z <= hi} by vertex enumeration (the box makes it bounded, so it is
+    nonempty iff it has a vertex: i tight constraints with a nonsingular system)."""
+    import itertools
+    i = len(lo)
+    G = np.vstack([A, np.eye(i), -np.eye(i)])
+    h = np.concatenate([b, hi, -lo])
+    for rows in itertools.combinations(range(len(h)), i):
+        M = G[list(rows)]
+        if abs(np.linalg.det(M)) < 1e-12:
+            continue
+        z = np.linalg.solve(M, h[list(rows)])
+        if np.all(G @ z <= h + tol * (1 + np.abs(h))):
+            return True, z
+    return False, None
+
+
+def test_lp_box_halfspace_equals_interval_check():
+    """A box initial set with one output half-space: the LP verdict per step equals the closed-form
+    interval check (the LP optimum of Fig. 2(c) for a box is sum max(c lo, c hi)) — C1, theta = 0.02."""
+    p = W.config1()
+    coeff = oracle.krylov_project(p)["coeff"]
+    lp = oracle.check_lp(p, coeff, unsafe_A=[[-1.0]], unsafe_b=[-0.02])  # y >= 0.02  <=>  -y <= -0.02
+    cb = oracle.check_box(p, coeff, [(0, W.GE, 0.02)])
+    hi = cb["hi"][:, 0]
+    margin = np.abs(hi - 0.02) > 1e-9
+    assert np.array_equal(lp["feasible"][margin], (hi >= 0.02)[margin])
+    assert lp["found"] and lp["step"] == cb["step"] == 74
+
+
+def test_lp_oscillator_paper_constraints():
+    """Fig. 2(c): z_y in [0, 1], fixed term, unsafe x = 4 as x <= 4 and -x <= -4: infeasible at
+    steps 0-2, feasible at 3pi/4 with the witness output x = 4."""
+    p = W.oscillator()
+    coeff = oracle.krylov_project(p)["coeff"]
+    lp = oracle.check_lp(p, coeff, unsafe_A=[[1.0], [-1.0]], unsafe_b=[4.0, -4.0])
+    assert list(lp["feasible"][:4]) == [False, False, False, True]
+    assert lp["step"] == 3 and abs(lp["y"][0] - 4.0) < 1e-7
+    assert abs(lp["z"][0] - (4 * math.sqrt(2) - 5)) < 1e-7  # the only feasible z_y (P:415-416)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_lp_matches_vertex_enumeration(seed):
+    """Random 3-generator problems with a polytope initial set (2 extra rows) and a 2-row unsafe polytope
+    in a 2-output space: per-step feasibility equals brute-force vertex enumeration (tiny instances)."""
+    rng = np.random.default_rng(100 + seed)
+    ng, o, N = 3, 2, 30
+    coeff = rng.standard_normal((N + 1, o, ng + 1))
+    p = {"gens": [W.sparse([d], [1.0]) for d in range(ng)], "z_lo": -np.ones(ng), "z_hi": np.ones(ng)}
+    IA = rng.standard_normal((2, ng))
+    Ib = np.abs(rng.standard_normal(2)) * 0.5
+    UA = rng.standard_normal((2, o))
+    Ub = rng.standard_normal(2)
+    lp = oracle.check_lp(p, coeff, IA, Ib, UA, Ub)
+    for j in range(N + 1):
+        B, cf = coeff[j, :, :ng], coeff[j, :, ng]
+        ok, _ = brute_force_feasible(np.vstack([IA, UA @ B]), np.concatenate([Ib, Ub - UA @ cf]), -np.ones(ng),
+                                     np.ones(ng))
+        assert ok == lp["feasible"][j], j
+    if lp["found"]:
+        z, j = lp["z"], lp["step"]
+        B, cf = coeff[j, :, :ng], coeff[j, :, ng]
+        assert np.all(IA @ z <= Ib + 1e-7) and np.all(UA @ (B @ z + cf) <= Ub + 1e-7)
