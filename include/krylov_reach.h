@@ -191,6 +191,26 @@ void krylov_reach_destroy(kr_handle* h);
 
 const char* krylov_last_error(void);
 
+/* The general per-step LP (NEXT-3; §2.1 P:145-152 in the initial / output spaces of §3; the LP
+ * of Fig. 2(c), for polytopes): at every step j, is there z with
+ *     z_lo <= z <= z_hi,   init_A z <= init_b,   unsafe_A (B_j z + c_f,j) <= unsafe_b ?
+ * B_j = c[j][.][0..n_gen) (generator columns), c_f,j = c[j][.][n_gen] (fixed direction, z_f = 1) or 0.
+ * init_A: HOST [m_init][n_gen] row-major (on the generator coordinates only), init_b [m_init];
+ * unsafe_A: HOST [m_unsafe][n_out], unsafe_b [m_unsafe] (an equality is two rows). All N+1 LPs are solved
+ * independently on the device (dense Phase-I simplex, Bland's rule, feasibility tolerance 1e-9 after row
+ * normalisation). feasible: HOST [(n_steps+1)] or NULL: 1 feasible, 0 infeasible, -1 iteration cap.
+ * cex: first feasible step (found, step, time; row = -1, y = first output at the witness). z_witness
+ * [n_dir] (fixed coordinate 1) and y_witness [n_out] receive the solver's assignment, or may be NULL.
+ * Requires krylov_project. KR_EINVAL if m_init + m_unsafe + n_gen exceeds the one-CTA tableau (~100).  */
+kr_status krylov_check_lp(kr_handle* h, int32_t m_init, const double* init_A, const double* init_b, int32_t m_unsafe,
+                          const double* unsafe_A, const double* unsafe_b, int32_t* feasible, kr_cex* cex,
+                          double* z_witness, double* y_witness);
+
+/* The outputs at one initial-space point: y[r] = sum_d c[step][r][d] z[d] (the basis matrix of P:481
+ * applied to z; z HOST [n_dir] including z_f = 1 for the fixed direction, y HOST [n_out]). Used to check a
+ * counter-example against an independent higher-accuracy re-simulation. */
+kr_status krylov_eval_outputs(kr_handle* h, int64_t step, const double* z, double* y);
+
 /* Simulation layout of h: *transposed = 1 in transpose mode (KR_SIM_TRANSPOSE, or AUTO with n_out < n_dir),
  * *n_sim = number of Krylov simulations (= length of the stats array of krylov_project): n_dir forward,
  * n_out transposed. Either pointer may be NULL. */

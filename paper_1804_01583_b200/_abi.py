@@ -60,7 +60,8 @@ EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "k
            "krylov_reach_destroy", "krylov_last_error", "krylov_launch_count", "krylov_last_timing",
            "krylov_comm_unique_id", "krylov_comm_create", "krylov_comm_destroy", "krylov_zslab_range",
            "krylov_krylov_data", "krylov_transfer_bytes", "krylov_zslab_halo_plan", "krylov_tridiag",
-           "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info"]
+           "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info", "krylov_check_lp",
+           "krylov_eval_outputs"]
 
 _lib = None
 
@@ -91,6 +92,8 @@ def lib():
     L.krylov_comm_destroy.argtypes = [vp]
     L.krylov_comm_destroy.restype = None
     L.krylov_krylov_data.argtypes = [vp, C.c_int32, vp, vp]
+    L.krylov_check_lp.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, vp, vp, vp, C.POINTER(kr_cex), vp, vp]
+    L.krylov_eval_outputs.argtypes = [vp, C.c_int64, vp, vp]
     L.krylov_sim_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.krylov_last_timing_large.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     L.krylov_tridiag.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.POINTER(C.c_int32)]

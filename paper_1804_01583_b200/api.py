@@ -150,6 +150,31 @@ class KrylovReach:
         return {"lo": lo, "hi": hi, "found": bool(cex.found), "step": int(cex.step), "time": cex.time,
                 "row": int(cex.row), "y": cex.y, "z": z if cex.found else None}
 
+    def check_lp(self, init_A=None, init_b=None, unsafe_A=None, unsafe_b=None, want_feasible=True):
+        """Per-step LP feasibility for a polytope initial set (rows on the generator coordinates) and a
+        polytope unsafe set in output space (krylov_check_lp)."""
+        ng = len(self.prob["gens"])
+        IA = np.ascontiguousarray(np.zeros((0, ng)) if init_A is None else init_A, dtype=np.float64).reshape(-1, ng)
+        Ib = np.ascontiguousarray(np.zeros(0) if init_b is None else init_b, dtype=np.float64).reshape(-1)
+        UA = np.ascontiguousarray(np.zeros((0, self.n_out)) if unsafe_A is None else unsafe_A,
+                                  dtype=np.float64).reshape(-1, self.n_out)
+        Ub = np.ascontiguousarray(np.zeros(0) if unsafe_b is None else unsafe_b, dtype=np.float64).reshape(-1)
+        feas = np.zeros(self.n_steps + 1, dtype=np.int32) if want_feasible else None
+        cex = A.kr_cex()
+        z = np.zeros(self.n_dir)
+        y = np.zeros(self.n_out)
+        A.check(A.lib().krylov_check_lp(self.h, IA.shape[0], _p(IA), _p(Ib), UA.shape[0], _p(UA), _p(Ub), _p(feas),
+                                        C.byref(cex), _p(z), _p(y)))
+        return {"feasible": feas, "found": bool(cex.found), "step": int(cex.step), "time": cex.time,
+                "z": z if cex.found else None, "y": y if cex.found else None}
+
+    def eval_outputs(self, step, z):
+        """y = c[step] z on the device (krylov_eval_outputs); z has n_dir entries (fixed direction: 1)."""
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        y = np.zeros(self.n_out)
+        A.check(A.lib().krylov_eval_outputs(self.h, int(step), _p(z), _p(y)))
+        return y
+
     def krylov_data(self, d=0):
         """(H [(k+1) x k], P [n_out x k]) of direction d (Hessenberg / tridiagonal and P = C V)."""
         k = int(self.prob["k"])
@@ -208,6 +233,24 @@ class KrylovReach:
 
     def __exit__(self, *a):
         self.close()
+
+
+def validate_counterexample(prob, step, z, y, k=None, **kw):
+    """Counter-example check by an independent, higher-accuracy re-simulation: the
+    problem is simulated again with a larger Krylov dimension (2k, capped at the path's maximum; for the
+    stencil Lanczos path an adaptive run to eps = 1e-12 when k is not given), the outputs at the witness
+    z are evaluated on the device, and the relative error against the LP's / box check's outputs y is
+    returned as (rel_err, y_resim)."""
+    q = dict(prob)
+    lanczos_stencil = prob["op"] == "stencil" and prob.get("method", "lanczos") != "arnoldi"
+    cap = A.KR_K_MAX if lanczos_stencil else A.KR_K_MAX_FIXED_PADE
+    q["k"] = int(k) if k else min(2 * int(prob["k"]), cap)
+    with KrylovReach(q, **kw) as h:
+        h.project(want=False)
+        yr = h.eval_outputs(step, z)
+    y = np.atleast_1d(np.asarray(y, dtype=np.float64))
+    rel = float(np.max(np.abs(yr[:y.size] - y)) / max(np.max(np.abs(yr[:y.size])), 1e-300))
+    return rel, yr
 
 
 # ABI-named functional wrappers

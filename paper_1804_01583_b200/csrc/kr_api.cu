@@ -557,6 +557,7 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
         h->transposed = true;
         h->cf_nout = p->n_out;
         h->cf_ndir = n_dirs_of(p);
+        h->n_gen_cf = p->n_gen;
         h->zlo.clear();
         h->zhi.clear();
         for (int d = 0; d < p->n_gen; ++d) {
@@ -697,6 +698,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         h->d_cf = h->d_coeff;
         h->cf_nout = h->n_out;
         h->cf_ndir = h->n_dir;
+        h->n_gen_cf = h->n_gen;
         if (p->part == KR_PART_DIRS && h->world > 1) {
             const int ndl_max = (h->n_dir + h->world - 1) / h->world;
             h->d_coeff_loc = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * ndl_max * 8 * h->world));
@@ -1202,6 +1204,52 @@ kr_status krylov_last_timing_large(const kr_handle* h, double* expm_ms, int32_t*
     if (expm_ms) *expm_ms = h->large_ms;
     if (n_evals) *n_evals = h->large_evals;
     return KR_OK;
+}
+
+kr_status krylov_check_lp(kr_handle* h, int32_t m_init, const double* init_A, const double* init_b, int32_t m_unsafe,
+                          const double* unsafe_A, const double* unsafe_b, int32_t* feasible, kr_cex* cex,
+                          double* z_witness, double* y_witness) {
+    return guarded([&] {
+        if (!h || !cex || m_init < 0 || m_unsafe < 0) KR_THROW(KR_EINVAL, "bad arguments");
+        if (!h->projected) KR_THROW(KR_ESTATE, "krylov_check_lp before krylov_project");
+        const int ng = h->n_gen_cf, o = h->cf_nout;
+        if ((m_init > 0 && (!init_A || !init_b)) || (m_unsafe > 0 && (!unsafe_A || !unsafe_b)))
+            KR_THROW(KR_EINVAL, "NULL constraint block");
+        for (int64_t e = 0; e < (int64_t)m_init * ng; ++e)
+            if (!std::isfinite(init_A[e])) KR_THROW(KR_ENONFINITE, "init_A");
+        for (int r = 0; r < m_init; ++r)
+            if (!std::isfinite(init_b[r])) KR_THROW(KR_ENONFINITE, "init_b");
+        for (int64_t e = 0; e < (int64_t)m_unsafe * o; ++e)
+            if (!std::isfinite(unsafe_A[e])) KR_THROW(KR_ENONFINITE, "unsafe_A");
+        for (int r = 0; r < m_unsafe; ++r)
+            if (!std::isfinite(unsafe_b[r])) KR_THROW(KR_ENONFINITE, "unsafe_b");
+        KR_CUDA(cudaSetDevice(h->device));
+        std::vector<double> out((size_t)2 + h->cf_ndir + o);
+        kr_lp_run(h, m_init, init_A, init_b, m_unsafe, unsafe_A, unsafe_b, feasible, out.data());
+        cex->found = out[0] != 0.0;
+        cex->step = (int64_t)out[1];
+        cex->time = cex->found ? (double)cex->step * h->step : 0.0;
+        cex->row = -1;
+        cex->y = cex->found ? out[(size_t)2 + h->cf_ndir] : 0.0;
+        if (cex->found) {
+            if (z_witness)
+                for (int d = 0; d < h->cf_ndir; ++d) z_witness[d] = out[(size_t)2 + d];
+            if (y_witness)
+                for (int q = 0; q < o; ++q) y_witness[q] = out[(size_t)2 + h->cf_ndir + q];
+        }
+    });
+}
+
+kr_status krylov_eval_outputs(kr_handle* h, int64_t step, const double* z, double* y) {
+    return guarded([&] {
+        if (!h || !z || !y) KR_THROW(KR_EINVAL, "NULL argument");
+        if (!h->projected) KR_THROW(KR_ESTATE, "krylov_eval_outputs before krylov_project");
+        if (step < 0 || step > h->n_steps) KR_THROW(KR_EDIM, "step out of range");
+        for (int d = 0; d < h->cf_ndir; ++d)
+            if (!std::isfinite(z[d])) KR_THROW(KR_ENONFINITE, "z");
+        KR_CUDA(cudaSetDevice(h->device));
+        kr_eval_outputs(h, step, z, y);
+    });
 }
 
 kr_status krylov_sim_info(const kr_handle* h, int32_t* transposed, int32_t* n_sim) {

@@ -108,3 +108,34 @@ void kr_box_enqueue(kr_handle* h, const int32_t* d_sense, const double* d_thr) {
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }
+
+namespace {
+// y_r = sum_d c[step][r][d] z_d (the basis matrix applied to one initial-space point)
+__global__ void eval_outputs_kernel(const double* cf, int64_t step, int o, int nd, const double* z, double* y) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= o) return;
+    const double* c = cf + (step * o + r) * (int64_t)nd;
+    double s = 0.0;
+    for (int d = 0; d < nd; ++d) s = fma(c[d], z[d], s);
+    y[r] = s;
+}
+}  // namespace
+
+void kr_eval_outputs(kr_handle* h, int64_t step, const double* z_h, double* y_h) {
+    double* dz = nullptr;
+    KR_CUDA(cudaMalloc(&dz, ((size_t)h->cf_ndir + h->cf_nout) * sizeof(double)));
+    double* dy = dz + h->cf_ndir;
+    cudaError_t e = cudaMemcpyAsync(dz, z_h, (size_t)h->cf_ndir * 8, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) {
+        eval_outputs_kernel<<<(h->cf_nout + 127) / 128, 128, 0, h->stream>>>(h->d_cf, step, h->cf_nout, h->cf_ndir, dz, dy);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(y_h, dy, (size_t)h->cf_nout * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(dz);
+    if (e != cudaSuccess) KR_THROW(KR_ECUDA, std::string("kr_eval_outputs: ") + cudaGetErrorString(e));
+    h->launches++;
+    h->h2d_bytes += (int64_t)h->cf_ndir * 8;
+    h->d2h_bytes += (int64_t)h->cf_nout * 8;
+}
+

@@ -96,7 +96,12 @@ struct SlabInfo {  // device-visible copy for the local-reduce sparse gather
 enum { PATH_FUSED_LANCZOS = 0, PATH_GENERIC = 1 };
 
 struct kr_comm {
-    void* nccl;  // ncclComm_t
+    void* nccl;  void kr_eval_outputs(kr_handle* h, int64_t step, const double* z_h, double* y_h);
+// per-step LP (kr_lp.cu)
+void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int m_uns, const double* UA,
+               const double* Ub, int32_t* feas_h, double* out_h);
+
+// ncclComm_t
     int32_t rank, world, device;
 };
 
@@ -115,6 +120,7 @@ struct kr_handle {
     int32_t n_gen, n_dir, n_out, k;  // simulation view: n_dir simulations, n_out projection rows each
     // final basis-matrix layout [(N+1)][cf_nout][cf_ndir] (= n_out / n_dir, swapped in transpose mode)
     bool transposed = false;
+    int32_t n_gen_cf = 0;    // generator directions of the final layout (the fixed direction, if any, is last)
     int32_t cf_nout = 0, cf_ndir = 0;
     double* d_cf = nullptr;  // final coefficients (= d_coeff unless transposed)
     int64_t n_steps;
@@ -241,6 +247,11 @@ void kr_lz_enqueue_init(kr_handle* h, int dl);
 void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events);
 // box
 void kr_box_enqueue(kr_handle* h, const int32_t* d_sense, const double* d_thr);
+
+void kr_eval_outputs(kr_handle* h, int64_t step, const double* z_h, double* y_h);
+// per-step LP (kr_lp.cu)
+void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int m_uns, const double* UA,
+               const double* Ub, int32_t* feas_h, double* out_h);
 
 // nccl
 void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s);
