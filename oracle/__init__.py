@@ -93,7 +93,11 @@ class Operator:
         self.p = p
         self.keep = []
         if p["op"] == "stencil":
-            self.s = _Op(0, p["mx"], p["my"], p["mz"], p["alpha"], 0, None, None, None, None,
+            b = None if p.get("b") is None else np.ascontiguousarray(_dense(p["b"], p, p["mx"] * p["my"] * p["mz"])
+                                                                     if isinstance(p["b"], dict) else p["b"],
+                                                                     dtype=np.float64)
+            self.keep.append(b)
+            self.s = _Op(0, p["mx"], p["my"], p["mz"], p["alpha"], 0, None, None, None, _ptr(b),
                          (C.c_int32 * 6)(*p.get("bc", [0] * 6)), (C.c_double * 6)(*p.get("gamma", [0.0] * 6)))
         else:
             rp = np.ascontiguousarray(p["row_ptr"], dtype=np.int64)
@@ -150,7 +154,7 @@ def directions(p):
     v_f = [c; 1] (lifted) or v_f = c (no affine term) — superposition."""
     op = Operator(p)
     n = op.dim
-    nb = n - 1 if (p["op"] == "csr" and p.get("b") is not None) else n
+    nb = n - 1 if p.get("b") is not None else n
     dirs = []
     for g in p["gens"]:
         v = np.zeros(n)
@@ -316,6 +320,9 @@ def gershgorin_mu(p):
         nb = [min(2, p[a] - 1) for a in ("mx", "my", "mz")]
         # the most interior cell maximises diag + sum |offdiag| (all off-diagonals are positive)
         best = p["alpha"] * sum((nb[a] - 2) * ih[a] for a in range(3))
+        if p.get("b") is not None:  # lifted: row r gains |b_r|/2, the lifted row sum_r |b_r|/2
+            bd = np.abs(_dense(p["b"], p, p["mx"] * p["my"] * p["mz"]) if isinstance(p["b"], dict) else p["b"])
+            best = max(best + 0.5 * float(bd.max()), 0.5 * float(bd.sum()))
         return best
     n = p["n"]
     rp, ci, va = p["row_ptr"], p["col_idx"], p["val"]

@@ -57,7 +57,7 @@ typedef struct {
     const int64_t* row_ptr;
     const int32_t* col_idx;
     const double* val;
-    const double* b; /* NULL = no affine term */
+    const double* b; /* NULL = no affine term; CSR or stencil: lifted x' = [[A, b], [0, 0]] x */
     /* stencil boundary per face (x-, x+, y-, y+, z-, z+): 0 Dirichlet (zero ghost, BASELINE configs),
        1 insulated (the missing neighbour is dropped), 2 insulated + exchange: diagonal -= gamma[f]
        (units of A). The paper's heat benchmark (SURVEY A1/A2 reconstruction): all faces
@@ -67,7 +67,7 @@ typedef struct {
 } oracle_op;
 
 int64_t oracle_op_dim(const oracle_op* A) {
-    if (A->op == 0) return A->mx * A->my * A->mz;
+    if (A->op == 0) return A->mx * A->my * A->mz + (A->b ? 1 : 0);
     return A->n + (A->b ? 1 : 0);
 }
 
@@ -140,11 +140,17 @@ void oracle_csr_apply(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
 void oracle_op_apply(const oracle_op* A, const double* x, double* y) {
     int dirichlet = 1;
     for (int f = 0; f < 6; ++f) dirichlet &= A->bc[f] == 0;
-    if (A->op == 0 && dirichlet)
-        oracle_stencil_apply(A->mx, A->my, A->mz, A->alpha, x, y);
-    else if (A->op == 0)
-        oracle_stencil_apply_bc(A->mx, A->my, A->mz, A->alpha, A->bc, A->gamma, x, y);
-    else
+    if (A->op == 0) {
+        if (dirichlet)
+            oracle_stencil_apply(A->mx, A->my, A->mz, A->alpha, x, y);
+        else
+            oracle_stencil_apply_bc(A->mx, A->my, A->mz, A->alpha, A->bc, A->gamma, x, y);
+        if (A->b) { /* lifted affine term: y += b x_n, y_n = 0 */
+            const int64_t n = A->mx * A->my * A->mz;
+            for (int64_t c = 0; c < n; ++c) y[c] += A->b[c] * x[n];
+            y[n] = 0.0;
+        }
+    } else
         oracle_csr_apply(A->n, A->row_ptr, A->col_idx, A->val, A->b, x, y);
 }
 

@@ -647,3 +647,51 @@ def test_lp_matches_vertex_enumeration(seed):
         z, j = lp["z"], lp["step"]
         B, cf = coeff[j, :, :ng], coeff[j, :, ng]
         assert np.all(IA @ z <= Ib + 1e-7) and np.all(UA @ (B @ z + cf) <= Ub + 1e-7)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-4: nonsymmetric heat with a permanent heater (P:1133-1147): lifted stencil, Arnoldi
+# ---------------------------------------------------------------------------------------------
+def heater_augmented(m):
+    """[[A, b], [0, 0]] built independently: the paper heat matrix (Kronecker sum + face terms) and the
+    heater column b = 0.01 (m+1) on the z = 0 cells with x_i <= 0.4, y_j <= 0.2 (DESIGN R19)."""
+    A = paper_matrix(m).toarray()
+    n = m ** 3
+    b = np.zeros(n)
+    nx, ny = int(np.floor(0.4 * (m + 1) + 1e-9)), int(np.floor(0.2 * (m + 1) + 1e-9))
+    for y in range(ny):
+        for x in range(nx):
+            b[x + m * y] = 0.01 * (m + 1)
+    M = np.zeros((n + 1, n + 1))
+    M[:n, :n] = A
+    M[:n, n] = b
+    return M
+
+
+def test_heater_lifted_operator():
+    p = W.heat_heater(6)
+    op = oracle.Operator(p)
+    M = heater_augmented(6)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        x = rng.standard_normal(op.dim)
+        assert np.allclose(op.apply(x), M @ x, rtol=1e-13, atol=1e-12)
+
+
+def test_heater_equals_dense_expm():
+    """m = 4 (n' = 65), k = 65 >= the Krylov dimension: Arnoldi from e_{n'} equals C e^{A' t} e_{n'} (scipy)
+    at every step up to T = 500; the lifted coordinate stays 1."""
+    p = W.heat_heater(4, k=65)
+    res = oracle.krylov_project(p)
+    M = heater_augmented(4)
+    C = np.array([W.dense_vec(o, p) for o in p["outs"]])
+    e = np.zeros(65)
+    e[64] = 1.0
+    E1 = sla.expm(M * p["step"])
+    x = e.copy()
+    scale = np.abs(res["coeff"]).max()
+    for j in range(p["n_steps"] + 1):
+        if j % 50 == 0:
+            assert np.max(np.abs(res["coeff"][j, :, 0] - C @ x[:64])) <= 1e-10 * scale, j
+            assert abs(x[64] - 1.0) < 1e-12
+        x = E1 @ x

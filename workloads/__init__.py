@@ -227,8 +227,34 @@ def heat_paper(m, eps=1e-6, k_max=8000, n_steps=1000, step=0.02):
     }
 
 
+def heat_heater(m, k=64, n_steps=1000, step=0.5):
+    """The paper's nonsymmetric 3D heat variant: the heat model of
+    heat_paper (insulated faces, Robin 0.5 at x = 1, 'alpha = 0.01' as A = 0.01 L) with the initially heated
+    region replaced by a permanent heater on the bottom face z = 0 over x in [0, 0.4], y in [0, 0.2]
+    (P:1136-1138); T = 500, delta = 0.5. Reading (DESIGN R19): the heater is a unit heat flux
+    through the z = 0 face into the first cell layer, i.e. the affine term b = 0.01 * 1/h on those cells
+    (the same scaling as the Robin term 0.01 * 0.5/h); the initial temperature is 0, so the only Krylov
+    simulation is the lifted fixed direction e_{n+1} and the reachable output is one trajectory
+    (the paper plots "the temperature reachable at the center"). Lifting makes the system
+    nonsymmetric: Arnoldi."""
+    h = 1.0 / (m + 1)
+    n_x = int(math.floor(0.4 * (m + 1) + 1e-9))
+    n_y = int(math.floor(0.2 * (m + 1) + 1e-9))
+    c = center_index(m)
+    return {
+        "name": f"heat_heater{m}", "op": "stencil", "mx": m, "my": m, "mz": m, "alpha": 0.01,
+        "bc": [BC_NEUMANN, BC_ROBIN, BC_NEUMANN, BC_NEUMANN, BC_NEUMANN, BC_NEUMANN],
+        "gamma": [0.0, 0.01 * 0.5 / h, 0.0, 0.0, 0.0, 0.0],
+        "b": box((0, 0, 0), (n_x, n_y, 1), 0.01 / h),
+        "gens": [], "z_lo": np.zeros(0), "z_hi": np.zeros(0), "center": None,
+        "outs": [point(c, c, c), allv(1.0)],
+        "step": float(step), "n_steps": int(n_steps), "k": int(k), "method": "arnoldi", "thresholds": [],
+    }
+
+
 CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5,
-           "P100": lambda: heat_paper(100), "P1000": lambda: heat_paper(1000)}
+           "P100": lambda: heat_paper(100), "P1000": lambda: heat_paper(1000),
+           "H10": lambda: heat_heater(10), "H100": lambda: heat_heater(100, k=400)}
 
 
 def n_state(p):
