@@ -64,7 +64,8 @@ typedef enum { KR_BC_DIRICHLET = 0, KR_BC_INSULATED = 1, KR_BC_ROBIN = 2 } kr_bc
  *  KR_SIM_AUTO:      the smaller of the two counts, min(i, o).                           */
 typedef enum { KR_SIM_FORWARD = 0, KR_SIM_TRANSPOSE = 1, KR_SIM_AUTO = 2 } kr_sim_dir;
 #define KR_K_MAX_FIXED_PADE 64   /* fixed k up to this uses per-step Pade-13 exponentials            */
-#define KR_K_MAX 16384           /* Lanczos (stencil) Krylov dimension cap; Arnoldi stays <= 64     */
+#define KR_K_MAX 16384           /* Lanczos (stencil) Krylov dimension cap                          */
+#define KR_K_MAX_ARNOLDI 2048    /* stored-basis (Arnoldi) Krylov dimension cap                     */
 
 /* An n-vector given compactly: a generator column of E, the center c, or an output row of C
  * (P:447). Linear index of stencil cell (x,y,z) is x + mx*(y + my*z) (x fastest).
@@ -94,6 +95,9 @@ typedef struct {
     const double* val;
     const double* b;            /* CSR only: affine term (length n) or NULL. Lifted into A' = [[A,b],[0,0]]
                                    with the extra coordinate fixed at 1. Must be NULL for STENCIL7. */
+    const kr_vec* b_vec;        /* STENCIL7 only: the affine term as a compact vector (e.g. the permanent heater
+                                   patch of P:1136-1138), lifted the same way (the system becomes nonsymmetric:
+                                   Arnoldi); NULL = none. Must be NULL for CSR.                            */
     /* Initial set. */
     int32_t n_gen;              /* generator directions g_d, d < n_gen                                  */
     const kr_vec* gen;
@@ -108,9 +112,9 @@ typedef struct {
     double step;
     int64_t n_steps;
     /* Krylov iteration. */
-    int32_t k;                  /* Krylov dimension (max; k_eff < k on breakdown). Arnoldi and
-                                   CSR: 1..64. Stencil Lanczos: 1..KR_K_MAX (k > 64 or eps > 0 use the
-                                   large-k exponential route, see krylov_project)                         */
+    int32_t k;                  /* Krylov dimension (max; k_eff < k on breakdown). Stored-basis
+                                   paths (Arnoldi, CSR): 1..KR_K_MAX_ARNOLDI. Stencil Lanczos: 1..KR_K_MAX.
+                                   k > 64 or eps > 0 use the large-k exponential route (krylov_project)   */
     int32_t method;             /* kr_method. AUTO: Lanczos for STENCIL7 or exactly symmetric CSR (b=NULL) */
     /* Adaptive Krylov dimension, Alg. 2/4: eps > 0 runs the stencil Lanczos with
        error control — the Lemma 1 bound (unit start vector, tau = T, trapezoid on the t_j grid)

@@ -18,7 +18,7 @@ KR_PART_NONE, KR_PART_ZSLAB, KR_PART_DIRS = 0, 1, 2
 KR_GE, KR_LE, KR_EQ, KR_NONE = 0, 1, 2, 3
 KR_VEC_SPARSE, KR_VEC_BOX, KR_VEC_ALL = 0, 1, 2
 KR_BC_DIRICHLET, KR_BC_INSULATED, KR_BC_ROBIN = 0, 1, 2
-KR_K_MAX_FIXED_PADE, KR_K_MAX = 64, 16384
+KR_K_MAX_FIXED_PADE, KR_K_MAX, KR_K_MAX_ARNOLDI = 64, 16384, 2048
 KR_SIM_FORWARD, KR_SIM_TRANSPOSE, KR_SIM_AUTO = 0, 1, 2
 
 
@@ -31,7 +31,7 @@ class kr_problem(C.Structure):
     _fields_ = [
         ("op", C.c_int32), ("mx", C.c_int64), ("my", C.c_int64), ("mz", C.c_int64), ("alpha", C.c_double),
         ("n", C.c_int64), ("nnz", C.c_int64), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
-        ("val", C.c_void_p), ("b", C.c_void_p),
+        ("val", C.c_void_p), ("b", C.c_void_p), ("b_vec", C.c_void_p),
         ("n_gen", C.c_int32), ("gen", C.POINTER(kr_vec)), ("z_lo", C.c_void_p), ("z_hi", C.c_void_p),
         ("center", C.POINTER(kr_vec)),
         ("n_out", C.c_int32), ("out", C.POINTER(kr_vec)),

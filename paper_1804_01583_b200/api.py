@@ -33,6 +33,12 @@ class _Marshal:
             gm = prob.get("gamma") or [0.0] * 6
             p.bc = (C.c_int32 * 6)(*[int(b) for b in bc])
             p.gamma = (C.c_double * 6)(*[float(g) for g in gm])
+            if prob.get("b") is not None:  # compact affine term of the stencil (lifted)
+                bv = prob["b"] if isinstance(prob["b"], dict) else {"kind": "sparse", "idx": np.nonzero(prob["b"])[0],
+                                                                    "val": np.asarray(prob["b"])[np.nonzero(prob["b"])[0]]}
+                kb = self._vec(bv)
+                self.keep.append(kb)
+                p.b_vec = C.addressof(kb)
         else:
             p.op = A.KR_OP_CSR
             rp = self._arr(prob["row_ptr"], np.int64)
@@ -242,8 +248,9 @@ def validate_counterexample(prob, step, z, y, k=None, **kw):
     z are evaluated on the device, and the relative error against the LP's / box check's outputs y is
     returned as (rel_err, y_resim)."""
     q = dict(prob)
-    lanczos_stencil = prob["op"] == "stencil" and prob.get("method", "lanczos") != "arnoldi"
-    cap = A.KR_K_MAX if lanczos_stencil else A.KR_K_MAX_FIXED_PADE
+    lanczos_stencil = (prob["op"] == "stencil" and prob.get("method", "lanczos") != "arnoldi"
+                       and prob.get("b") is None)
+    cap = A.KR_K_MAX if lanczos_stencil else A.KR_K_MAX_ARNOLDI
     q["k"] = int(k) if k else min(2 * int(prob["k"]), cap)
     with KrylovReach(q, **kw) as h:
         h.project(want=False)

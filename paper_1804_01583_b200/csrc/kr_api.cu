@@ -32,6 +32,9 @@ namespace {
 
 bool finite(double v) { return std::isfinite(v); }
 
+// an affine term lifts the system: CSR b (dense) or the stencil's compact b_vec
+bool has_affine(const kr_problem* p) { return p->b != nullptr || (p->op == KR_OP_STENCIL7 && p->b_vec != nullptr); }
+
 int64_t n_state(const kr_problem* p) { return p->op == KR_OP_STENCIL7 ? p->mx * p->my * p->mz : p->n; }
 
 void validate_vec(const kr_problem* p, const kr_vec& v, const char* what) {
@@ -91,7 +94,27 @@ double gershgorin_mu(const kr_problem* p) {
             const double ih = (double)(m[a] + 1) * (double)(m[a] + 1);
             s += (double)(std::min<int64_t>(2, m[a] - 1) - 2) * ih;
         }
-        return p->alpha * s;
+        double mu = p->alpha * s;
+        if (p->b_vec) {  // lifted: row r gains |b_r|/2, the lifted row sum_r |b_r|/2
+            const kr_vec& v = *p->b_vec;
+            double bmax = 0.0, bsum = 0.0;
+            if (v.kind == KR_VEC_SPARSE) {
+                std::map<int64_t, double> acc;
+                for (int64_t e = 0; e < v.nnz; ++e) acc[v.idx[e]] += v.val[e];
+                for (auto& kv : acc) {
+                    bmax = std::max(bmax, std::fabs(kv.second));
+                    bsum += std::fabs(kv.second);
+                }
+            } else {
+                int64_t cnt = p->mx * p->my * p->mz;
+                if (v.kind == KR_VEC_BOX)
+                    cnt = (v.hi[0] - v.lo[0]) * (v.hi[1] - v.lo[1]) * (v.hi[2] - v.lo[2]);
+                bmax = cnt > 0 ? std::fabs(v.value) : 0.0;
+                bsum = std::fabs(v.value) * (double)cnt;
+            }
+            mu = std::max(mu + 0.5 * bmax, 0.5 * bsum);
+        }
+        return mu;
     }
     const int64_t n = p->n, N = n + (p->b ? 1 : 0);
     std::vector<double> diag(N, 0.0), rad(N, 0.0);
@@ -188,7 +211,7 @@ struct Sizes {
 
 int resolve_method(const kr_problem* p) {
     if (p->method == KR_ARNOLDI || p->method == KR_LANCZOS) return p->method;
-    if (p->op == KR_OP_STENCIL7) return KR_LANCZOS;
+    if (p->op == KR_OP_STENCIL7) return p->b_vec ? KR_ARNOLDI : KR_LANCZOS;
     if (!p->b && csr_exactly_symmetric(p)) return KR_LANCZOS;
     return KR_ARNOLDI;
 }
@@ -207,7 +230,8 @@ void validate(const kr_problem* p) {
         if (p->mx < 1 || p->my < 1 || p->mz < 1) KR_THROW(KR_EDIM, "stencil grid must be >= 1 per axis");
         if (p->mx > (1 << 30) || p->my > (1 << 30) || p->mz > (1 << 30)) KR_THROW(KR_EDIM, "grid too large");
         if (!finite(p->alpha)) KR_THROW(KR_ENONFINITE, "alpha");
-        if (p->b) KR_THROW(KR_EINVAL, "affine term b is supported for CSR only (lift explicitly)");
+        if (p->b) KR_THROW(KR_EINVAL, "stencil affine term: pass it as b_vec (compact), not b");
+        if (p->b_vec) validate_vec(p, *p->b_vec, "b_vec");
     } else {
         if (p->n < 1 || !p->row_ptr || (p->nnz > 0 && (!p->col_idx || !p->val))) KR_THROW(KR_EINVAL, "bad CSR");
         if (p->row_ptr[0] != 0 || p->row_ptr[p->n] != p->nnz) KR_THROW(KR_EDIM, "row_ptr inconsistent with nnz");
@@ -217,6 +241,7 @@ void validate(const kr_problem* p) {
             if (p->col_idx[e] < 0 || p->col_idx[e] >= p->n) KR_THROW(KR_EDIM, "col_idx out of range");
             if (!finite(p->val[e])) KR_THROW(KR_ENONFINITE, "non-finite matrix value");
         }
+        if (p->b_vec) KR_THROW(KR_EINVAL, "b_vec is for the stencil operator; CSR takes a dense b");
         if (p->b)
             for (int64_t r = 0; r < p->n; ++r)
                 if (!finite(p->b[r])) KR_THROW(KR_ENONFINITE, "non-finite b");
@@ -227,8 +252,8 @@ void validate(const kr_problem* p) {
     if (p->n_steps < 0) KR_THROW(KR_EINVAL, "n_steps must be >= 0");
     if (p->method < 0 || p->method > 2) KR_THROW(KR_EINVAL, "bad method");
     {
-        const bool stencil_lz = p->op == KR_OP_STENCIL7 && p->method != KR_ARNOLDI;
-        const int kmax = stencil_lz ? KR_K_MAX : KR_K_MAX_FIXED_PADE;
+        const bool stencil_lz = p->op == KR_OP_STENCIL7 && p->method != KR_ARNOLDI && !p->b_vec;
+        const int kmax = stencil_lz ? KR_K_MAX : KR_K_MAX_ARNOLDI;
         if (p->k < 1 || p->k > kmax)
             KR_THROW(KR_EINVAL, "k must be 1.." + std::to_string(kmax) + (stencil_lz ? "" : " (Arnoldi / CSR)"));
         if (!(p->eps >= 0.0) || !finite(p->eps)) KR_THROW(KR_EINVAL, "eps must be >= 0");
@@ -250,9 +275,9 @@ void validate(const kr_problem* p) {
         if (vec_is_zero(p, p->gen[d])) KR_THROW(KR_EZERO, "generator " + std::to_string(d) + " is zero");
     }
     if (p->center) validate_vec(p, *p->center, "center");
-    if (p->center && !p->b && vec_is_zero(p, *p->center)) KR_THROW(KR_EZERO, "center is zero (pass NULL)");
+    if (p->center && !has_affine(p) && vec_is_zero(p, *p->center)) KR_THROW(KR_EZERO, "center is zero (pass NULL)");
     for (int r = 0; r < p->n_out; ++r) validate_vec(p, p->out[r], "output row");
-    const int n_dir = p->n_gen + ((p->center || p->b) ? 1 : 0);
+    const int n_dir = p->n_gen + ((p->center || has_affine(p)) ? 1 : 0);
     if (n_dir < 1) KR_THROW(KR_EINVAL, "no directions");
 }
 
@@ -260,11 +285,11 @@ Sizes plan(const kr_problem* p, int rank, int world) {
     Sizes s{};
     s.method = resolve_method(p);
     if (s.method == KR_LANCZOS) {
-        if (p->b) KR_THROW(KR_ENOTSYM, "lifted affine system is not symmetric; use Arnoldi");
+        if (has_affine(p)) KR_THROW(KR_ENOTSYM, "lifted affine system is not symmetric; use Arnoldi");
         if (p->op == KR_OP_CSR && !csr_exactly_symmetric(p)) KR_THROW(KR_ENOTSYM, "CSR matrix is not symmetric");
     }
-    s.N = p->op == KR_OP_STENCIL7 ? p->mx * p->my * p->mz : p->n + (p->b ? 1 : 0);
-    const int n_dir = p->n_gen + ((p->center || p->b) ? 1 : 0);
+    s.N = (p->op == KR_OP_STENCIL7 ? p->mx * p->my * p->mz : p->n) + (has_affine(p) ? 1 : 0);
+    const int n_dir = p->n_gen + ((p->center || has_affine(p)) ? 1 : 0);
     s.ndl = local_dirs(p, n_dir, rank, world);
     s.path = (p->op == KR_OP_STENCIL7 && s.method == KR_LANCZOS) ? PATH_FUSED_LANCZOS : PATH_GENERIC;
     if (s.path == PATH_GENERIC && (p->part == KR_PART_ZSLAB || p->virtual_slabs > 1))
@@ -287,7 +312,8 @@ Sizes plan(const kr_problem* p, int rank, int world) {
         }
         s.state_bytes = b + (size_t)3 * 256 * (size_t)nsl;  // + 256-byte alignment of each carved buffer
     } else {
-        if (s.N > 27648) KR_THROW(KR_EDIM, "the stored-basis (Arnoldi) path supports operator dimension <= 27648");
+        if (s.N > KR_ORTHO_ONE_CTA_MAX && s.method == KR_LANCZOS)
+            KR_THROW(KR_EINVAL, "stored-basis Lanczos needs operator dimension <= 27648 (use the stencil path or Arnoldi)");
         s.state_bytes = (size_t)s.ndl * (size_t)(p->k + 2) * (size_t)s.N * sizeof(double) + 2 * 256;
     }
     return s;
@@ -328,7 +354,7 @@ kr_status guarded(F&& f) {
     }
 }
 
-int n_dirs_of(const kr_problem* p) { return p->n_gen + ((p->center || p->b) ? 1 : 0); }
+int n_dirs_of(const kr_problem* p) { return p->n_gen + ((p->center || has_affine(p)) ? 1 : 0); }
 
 bool transposed_mode(const kr_problem* p) {
     if (p->sim_dir == KR_SIM_TRANSPOSE) return true;
@@ -354,6 +380,7 @@ void build_transposed(const kr_problem* p, TransposeStore& T, kr_problem& q) {
     q = *p;
     const int nd = n_dirs_of(p);
     if (nd > KR_MAX_OUT) KR_THROW(KR_EINVAL, "transpose mode: at most 64 directions (they become projection rows)");
+    if (p->op == KR_OP_STENCIL7 && p->b_vec) KR_THROW(KR_EINVAL, "transpose mode: lifted stencil not supported");
     if (p->eps > 0.0) KR_THROW(KR_EINVAL, "transpose mode is not combined with adaptive k (eps > 0)");
     const bool csr = p->op == KR_OP_CSR;
     const int64_t n = n_state(p);
@@ -620,9 +647,9 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         }
         h->n = n_state(p);
         h->N = sz.N;
-        h->lifted = p->b != nullptr;
+        h->lifted = has_affine(p);
         h->n_gen = p->n_gen;
-        h->n_dir = p->n_gen + ((p->center || p->b) ? 1 : 0);
+        h->n_dir = p->n_gen + ((p->center || has_affine(p)) ? 1 : 0);
         h->n_out = p->n_out;
         h->k = p->k;
         h->n_steps = p->n_steps;
@@ -655,7 +682,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 z.value = 0.0;
                 h->dirs_h.push_back(z);
             }
-            h->dir_lift1.push_back(p->b ? 1 : 0);
+            h->dir_lift1.push_back(has_affine(p) ? 1 : 0);
             h->zlo.push_back(1.0);
             h->zhi.push_back(1.0);
         }
@@ -676,10 +703,10 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         }
         const int k = h->k;
         const int64_t np1 = h->n_steps + 1;
-        h->large_route = h->path == PATH_FUSED_LANCZOS && (h->eps > 0.0 || k > KR_K_MAX_FIXED_PADE);
+        h->large_route = (h->path == PATH_FUSED_LANCZOS && h->eps > 0.0) || k > KR_K_MAX_FIXED_PADE;
         h->checks.assign(ndl, {});
         h->d_scratch = reinterpret_cast<double*>(dalloc(h, 64));
-        if (!h->large_route) {
+        if (!h->large_route || h->path == PATH_GENERIC) {  // dense H: per-step Pade, or Arnoldi's Hessenberg
             h->d_H = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * (k + 1) * k * 8));
             KR_CUDA(cudaMemsetAsync(h->d_H, 0, (size_t)ndl * (k + 1) * k * 8, h->stream));
         }
@@ -845,6 +872,13 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             for (int r = 0; r < h->n_out; ++r)
                 kr_fill_dense(h->stream, h->d_O + (int64_t)r * h->N, h->N, h->n, h->mx, h->my,
                               h->op == KR_OP_STENCIL7, h->outs_h[r], 0, 1.0, 0, &dummy);
+            if (p->op == KR_OP_STENCIL7 && p->b_vec) {  // dense affine term for the lifted stencil apply
+                h->d_bl = reinterpret_cast<double*>(dalloc(h, (size_t)h->n * 8));
+                const DVec bv = make_dvec(h, *p->b_vec);
+                kr_fill_dense(h->stream, h->d_bl, h->n, h->n, h->mx, h->my, true, bv, 0, 1.0, 0, &dummy);
+            }
+            h->use_cgs = h->N > KR_ORTHO_ONE_CTA_MAX || (getenv("KR_FORCE_CGS") && h->method == KR_ARNOLDI);
+            if (h->use_cgs) h->d_cgs = reinterpret_cast<double*>(dalloc(h, kr_cgs_scratch_doubles(h, ndl) * 8));
             KR_CUDA(cudaStreamSynchronize(h->stream));
             // bytes per batched operator launch: A once + X and Y per direction (context only)
             h->step_bytes = (h->op == KR_OP_CSR ? (double)p->nnz * 12.0 + (double)(p->n + 1) * 8.0 : 0.0) +
@@ -930,6 +964,19 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             h->large_ms = 0.0;
             h->large_evals = 0;
             KR_CUDA(cudaEventRecord(h->ev_it0, h->stream));
+            if (h->path == PATH_GENERIC) {  // stored-basis Arnoldi with k > 64: all steps, then the exponentials
+                kr_ge_enqueue_direction_set(h);
+                KR_CUDA(cudaEventRecord(h->ev_it1, h->stream));
+                std::vector<int32_t> ke(ndl), stv(ndl);
+                KR_CUDA(cudaMemcpyAsync(ke.data(), h->d_keff, ndl * 4, cudaMemcpyDeviceToHost, h->stream));
+                KR_CUDA(cudaMemcpyAsync(stv.data(), h->d_status, ndl * 4, cudaMemcpyDeviceToHost, h->stream));
+                KR_CUDA(cudaStreamSynchronize(h->stream));
+                h->steps_run0 = ndl > 0 ? ke[0] : 0;
+                for (int dl = 0; dl < ndl; ++dl)
+                    if (!stv[dl]) kr_large_eval(h, dl, std::max(1, (int)ke[dl]), true, false);
+                post();
+                return;
+            }
             for (int dl = 0; dl < ndl; ++dl) {
                 h->checks[dl].clear();
                 kr_lz_enqueue_init(h, dl);

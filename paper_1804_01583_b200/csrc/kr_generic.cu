@@ -130,7 +130,8 @@ struct FaceCor {  // per-face diagonal correction of face cells relative to Diri
 
 __global__ void stencil_apply_kernel(int64_t mx, int64_t my, int64_t mz, double cx, double cy, double cz,
                                      const double* __restrict__ X, int64_t xstride, double* __restrict__ Y,
-                                     int64_t ystride, const int32_t* __restrict__ done, FaceCor fc) {
+                                     int64_t ystride, const int32_t* __restrict__ done, FaceCor fc,
+                                     const double* __restrict__ bl) {
     const int d = blockIdx.y;
     if (done[d]) return;
     const double* u = X + (int64_t)d * xstride;
@@ -146,8 +147,11 @@ __global__ void stencil_apply_kernel(int64_t mx, int64_t my, int64_t mz, double 
         const double dg = diag - (x == 0 ? fc.e[0] : 0.0) - (x == mx - 1 ? fc.e[1] : 0.0) -
                           (yy == 0 ? fc.e[2] : 0.0) - (yy == my - 1 ? fc.e[3] : 0.0) -
                           (z == 0 ? fc.e[4] : 0.0) - (z == mz - 1 ? fc.e[5] : 0.0);
-        y[c] = cx * sx + cy * sy + cz * sz - dg * u[c];
+        double v = cx * sx + cy * sy + cz * sz - dg * u[c];
+        if (bl) v = fma(bl[c], u[n], v);  // lifted affine term: y = A u + b u_n
+        y[c] = v;
     }
+    if (bl && blockIdx.x == 0 && threadIdx.x == 0) y[n] = 0.0;  // the lifted row of A' is zero
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -306,6 +310,10 @@ __global__ void __launch_bounds__(OT) ortho_kernel(OrthoArgs a) {
 }
 
 static void launch_ortho(kr_handle* h, int j, int ndl) {
+    if (h->use_cgs) {  // N > KR_ORTHO_ONE_CTA_MAX: stream the basis with the whole GPU (CGS2, kr_arnoldi.cu)
+        kr_cgs_step(h, j, ndl, h->d_cgs);
+        return;
+    }
     OrthoArgs a;
     a.V = h->d_V;
     a.W = h->d_W;
@@ -395,7 +403,7 @@ void kr_ge_enqueue_direction_set(kr_handle* h) {
                                                                   vstride, h->d_W, N, ndl, h->d_done);
         else
             stencil_apply_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->mx, h->my, h->mz, h->cx, h->cy, h->cz, X,
-                                                                       vstride, h->d_W, N, h->d_done, fc);
+                                                                       vstride, h->d_W, N, h->d_done, fc, h->d_bl);
         KR_CUDA(cudaGetLastError());
         h->launches++;
         if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1) + 1], h->stream));

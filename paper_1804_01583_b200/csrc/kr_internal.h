@@ -14,6 +14,7 @@
 #define KR_KMAX KR_K_MAX   // max Krylov dimension (stencil Lanczos; Arnoldi <= KR_K_MAX_FIXED_PADE)
 #define KR_MAX_BOX 8       // box-kind output rows handled inside the fused stencil kernel
 #define KR_MAX_OUT 64      // output rows
+#define KR_ORTHO_ONE_CTA_MAX 27648  // stored-basis N up to which one CTA per direction runs MGS on chip
 
 // ------------------------------------------------------------------------------------------------
 // error plumbing
@@ -198,6 +199,9 @@ struct kr_handle {
     std::vector<std::vector<std::pair<int32_t, double>>> checks;  // per local direction: (k, bound)
 
     // generic path
+    double* d_bl = nullptr;   // stencil affine term b (dense, length n) when lifted, else NULL
+    double* d_cgs = nullptr;  // CGS2 scratch (N > KR_ORTHO_ONE_CTA_MAX)
+    bool use_cgs = false;     // stored-basis orthogonalisation by the multi-CTA CGS2 path
     double* d_V;  // [ndl][k+1][N]
     double* d_W;  // [ndl][N]
 
@@ -234,6 +238,8 @@ size_t kr_lz_step_smem(int TX, int TY);
 
 // generic
 void kr_ge_enqueue_direction_set(kr_handle* h);
+size_t kr_cgs_scratch_doubles(const kr_handle* h, int ndl);
+void kr_cgs_step(kr_handle* h, int j, int ndl, double* scratch);
 
 // expm + projection + lemma
 void kr_expm_enqueue(kr_handle* h);

@@ -174,6 +174,34 @@ __global__ void large_build_kernel(const LzScalars* sc, int kc, int kp, double f
     }
 }
 
+// Dense (Arnoldi, upper Hessenberg) H: ||H delta||_1 over the leading kc x kc block (row stride ks).
+__global__ void large_norm_dense_kernel(const double* H, int ks, int kc, double delta, double* out) {
+    __shared__ double red[256];
+    double m = 0.0;
+    for (int c = threadIdx.x; c < kc; c += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < kc; ++r) s += fabs(H[(int64_t)r * ks + c]);
+        m = fmax(m, s);
+    }
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + st]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = red[0] * delta;
+}
+
+__global__ void large_build_dense_kernel(const double* H, int ks, int kc, int kp, double f, double* X, double* Y) {
+    const int64_t n = (int64_t)kp * kp;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / kp), j = (int)(e - (int64_t)i * kp);
+        const double x = (i < kc && j < kc) ? H[(int64_t)i * ks + j] * f : 0.0;
+        X[e] = x;
+        Y[e] = x * (1.0 / 18.0) + ((i == j && i < kc) ? 1.0 : 0.0);
+    }
+}
+
 // x_0 = e_1; x_{j+1} = E x_j (E banded with bandwidth bw), one warp per row, grid barrier per step.
 __global__ void __launch_bounds__(256) large_chain_kernel(const double* __restrict__ E, int kp, int kc, int bw,
                                                           double* traj, int64_t n_steps) {
@@ -250,7 +278,7 @@ __global__ void large_e1_col_kernel(double* Xc, int ldx, int kp) {
 
 // Lemma 1 for the unit start vector: h_{kc+1,kc} e^{max(mu,0) T} int_0^T |h(t)| dt, trapezoid on
 // the t_j grid, fixed-order reduction. out[0] = bound; with fin != 0 also the direction's stats.
-__global__ void large_bound_kernel(const double* hlast, int64_t n_steps, double step, double mu, const LzScalars* sc,
+__global__ void large_bound_kernel(const double* hlast, int64_t n_steps, double step, double mu, const double* hn_src,
                                    int kc, int zero_bound, double* out, int fin, const double* beta0, double* lemma,
                                    double* hnext, int32_t* keff) {
     __shared__ double red[256];
@@ -263,9 +291,10 @@ __global__ void large_bound_kernel(const double* hlast, int64_t n_steps, double 
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const double hn = zero_bound ? 0.0 : sc->beta[kc];
+        const double hn = zero_bound ? 0.0 : *hn_src;
         const double T = (double)n_steps * step;
-        const double b = zero_bound ? 0.0 : hn * exp(fmax(mu, 0.0) * T) * red[0];
+        const double base = hn * red[0];  // e^{max(mu,0) T} may overflow to inf (lifted systems, DESIGN R16)
+        const double b = (zero_bound || base == 0.0) ? 0.0 : base * exp(fmax(mu, 0.0) * T);
         out[0] = b;
         if (fin) {
             *lemma = *beta0 * b;
@@ -321,10 +350,18 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     double* X = h->d_big;
     double* Y0 = X + mat;
     double* Y1 = Y0 + mat;
-    LzScalars* sc = h->d_sc + dl;
+    const bool tri = h->path == PATH_FUSED_LANCZOS;  // Lanczos tridiagonal arrays, else dense Hessenberg H
+    LzScalars* sc = tri ? h->d_sc + dl : nullptr;
+    const double* Hd = tri ? nullptr : h->d_H + (size_t)dl * (h->k + 1) * h->k;
+    // h_{kc+1,kc} (1-based): beta[kc] of the Lanczos arrays, or H[kc][kc-1] of the Hessenberg
+    const double* hn_src = tri ? h->d_lzarr + (size_t)dl * 3 * (h->k + 2) + (h->k + 2) + kc
+                               : Hd + (size_t)kc * h->k + (kc - 1);
     cudaStream_t st = h->stream;
     // scaling: ||H delta||_1 -> s with ||H delta||_1 / 2^s <= 1
-    large_norm_kernel<<<1, 256, 0, st>>>(sc, kc, h->step, h->d_scratch);
+    if (tri)
+        large_norm_kernel<<<1, 256, 0, st>>>(sc, kc, h->step, h->d_scratch);
+    else
+        large_norm_dense_kernel<<<1, 256, 0, st>>>(Hd, h->k, kc, h->step, h->d_scratch);
     KR_CUDA(cudaGetLastError());
     h->launches++;
     double nrm = 0.0;
@@ -338,16 +375,21 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     {
         const int64_t n = (int64_t)mat;
         const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-        large_build_kernel<<<blocks, 256, 0, st>>>(sc, kc, kp, f, X, Y0);
+        if (tri)
+            large_build_kernel<<<blocks, 256, 0, st>>>(sc, kc, kp, f, X, Y0);
+        else
+            large_build_dense_kernel<<<blocks, 256, 0, st>>>(Hd, h->k, kc, kp, f, X, Y0);
         KR_CUDA(cudaGetLastError());
         h->launches++;
     }
     // Horner: Y = I + X Y / q, q = 17..1  ->  Y = T_18(X); bandwidth of Y grows by one per product
-    int bwY = 1;
+    // (tridiagonal X); a Hessenberg X is treated as dense
+    const int bwX = tri ? 1 : bmax;
+    int bwY = tri ? 1 : bmax;
     double* Y = Y0;
     double* Z = Y1;
     for (int q = 17; q >= 1; --q) {
-        gemm(h, X, Y, Z, kp, kp, kp, kp, kp, kp, 1, std::min(bwY, bmax), kc, 1.0 / q, 1.0);
+        gemm(h, X, Y, Z, kp, kp, kp, kp, kp, kp, bwX, std::min(bwY, bmax), kc, 1.0 / q, 1.0);
         bwY = std::min(bwY + 1, bmax);
         std::swap(Y, Z);
     }
@@ -408,7 +450,7 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
         KR_CUDA(cudaGetLastError());
         h->launches++;
     }
-    large_bound_kernel<<<1, 256, 0, st>>>(hl, h->n_steps, h->step, h->mu, sc, kc, zero_bound ? 1 : 0, h->d_scratch + 1,
+    large_bound_kernel<<<1, 256, 0, st>>>(hl, h->n_steps, h->step, h->mu, hn_src, kc, zero_bound ? 1 : 0, h->d_scratch + 1,
                                           fin ? 1 : 0, h->d_beta0 + dl, h->d_lemma + dl, h->d_hnext + dl,
                                           h->d_keff + dl);
     KR_CUDA(cudaGetLastError());

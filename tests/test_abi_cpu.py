@@ -75,7 +75,7 @@ def test_workspace_bytes_host_only():
 @pytest.mark.parametrize("mutate,code", [
     (lambda p: p.update(k=0), "KR_EINVAL"),
     (lambda p: p.update(k=16385), "KR_EINVAL"),
-    (lambda p: p.update(k=65, method="arnoldi"), "KR_EINVAL"),
+    (lambda p: p.update(k=2049, method="arnoldi"), "KR_EINVAL"),
     (lambda p: p.update(eps=-1e-6), "KR_EINVAL"),
     (lambda p: p.update(eps=1e-6, method="arnoldi"), "KR_EINVAL"),
     (lambda p: p.update(bc=[3, 0, 0, 0, 0, 0]), "KR_EINVAL"),
@@ -142,3 +142,16 @@ def test_transpose_mode_host_side():
     with pytest.raises(KrylovError) as e:
         krylov_workspace_bytes(p, sim="transpose")  # not combined with adaptive k
     assert "KR_EINVAL" in str(e.value)
+
+
+def test_lifted_stencil_host_side():
+    """NEXT-4: the heater's compact affine term lifts the stencil (N = n + 1, one fixed direction, Arnoldi);
+    beyond one CTA the stored basis is orthogonalised by the CGS2 path (no dimension cap)."""
+    from paper_1804_01583_b200 import KrylovError, krylov_workspace_bytes
+    p = W.heat_heater(10)
+    assert krylov_workspace_bytes(p) == 1 * (64 + 2) * 1001 * 8 + 512
+    q = W.heat_heater(100, k=400)
+    assert krylov_workspace_bytes(q) == 1 * 402 * 1000001 * 8 + 512
+    with pytest.raises(KrylovError) as e:
+        krylov_workspace_bytes(q, method="lanczos")
+    assert "KR_ENOTSYM" in str(e.value)
