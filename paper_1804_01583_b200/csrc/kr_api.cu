@@ -863,6 +863,11 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 h->d_ci = upload(h, p->col_idx, (size_t)p->nnz);
                 h->d_val = upload(h, p->val, (size_t)p->nnz);
                 h->d_b = p->b ? upload(h, p->b, (size_t)p->n) : nullptr;
+                std::vector<int64_t> lr;
+                for (int64_t r = 0; r < p->n; ++r)
+                    if (p->row_ptr[r + 1] - p->row_ptr[r] > KR_LONG_ROW) lr.push_back(r);
+                h->n_long = (int64_t)lr.size();
+                if (h->n_long) h->d_long = upload(h, lr.data(), lr.size());
             }
             kr_ge_prepare();
             h->d_V = reinterpret_cast<double*>(carve(h, (size_t)ndl * (k + 1) * h->N * 8));

@@ -117,10 +117,35 @@ __global__ void spmm_csr_kernel(const int64_t* __restrict__ rp, const int32_t* _
         double s = 0.0;
         if (r < n) {
             const int64_t e1 = rp[r + 1];
+            if (e1 - rp[r] > KR_LONG_ROW) continue;  // long rows (e.g. the b^T row of a transposed lift): CTA each
             for (int64_t e = rp[r]; e < e1; ++e) s = fma(val[e], __ldg(&x[ci[e]]), s);
             if (b) s = fma(b[r], x[n], s);
         }
         y[r] = s;
+    }
+}
+
+// rows with more than KR_LONG_ROW entries: one CTA per (long row, direction), fixed-order block reduction
+__global__ void spmm_long_rows_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                      const double* __restrict__ val, const double* __restrict__ b, int64_t n,
+                                      const int64_t* __restrict__ rows, const double* __restrict__ X, int64_t xstride,
+                                      double* __restrict__ Y, int64_t ystride, const int32_t* __restrict__ done) {
+    const int d = blockIdx.y;
+    if (done[d]) return;
+    const int64_t r = rows[blockIdx.x];
+    const double* x = X + (int64_t)d * xstride;
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t e = rp[r] + threadIdx.x; e < rp[r + 1]; e += blockDim.x) s = fma(val[e], __ldg(&x[ci[e]]), s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        if (b) t = fma(b[r], x[n], t);
+        Y[(int64_t)d * ystride + r] = t;
     }
 }
 
@@ -399,8 +424,16 @@ void kr_ge_enqueue_direction_set(kr_handle* h) {
         const bool evj = h->timing && (size_t)(2 * j) <= h->ev.size();
         if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1)], h->stream));
         if (h->op == KR_OP_CSR)
+        {
             spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X,
                                                                   vstride, h->d_W, N, ndl, h->d_done);
+            if (h->n_long) {
+                KR_CUDA(cudaGetLastError());
+                h->launches++;
+                spmm_long_rows_kernel<<<dim3((unsigned)h->n_long, ndl), 256, 0, h->stream>>>(
+                    h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, h->d_long, X, vstride, h->d_W, N, h->d_done);
+            }
+        }
         else
             stencil_apply_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->mx, h->my, h->mz, h->cx, h->cy, h->cz, X,
                                                                        vstride, h->d_W, N, h->d_done, fc, h->d_bl);

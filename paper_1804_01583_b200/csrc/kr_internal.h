@@ -15,6 +15,7 @@
 #define KR_MAX_BOX 8       // box-kind output rows handled inside the fused stencil kernel
 #define KR_MAX_OUT 64      // output rows
 #define KR_ORTHO_ONE_CTA_MAX 27648  // stored-basis N up to which one CTA per direction runs MGS on chip
+#define KR_LONG_ROW 256             // CSR rows longer than this get a CTA of their own in the SpMM
 
 // ------------------------------------------------------------------------------------------------
 // error plumbing
@@ -194,12 +195,15 @@ struct kr_handle {
     // large-k route scratch (allocated at the first project that needs it, for kcap = k)
     double* d_big;         // 6 x kcap^2 doubles: X, X^2, X^3, X^4, Y, Y'
     double* d_traj;        // [(n_steps+1)][kcap] x_j = e^{H t_j} e_1
+    int large_cap = 0;     // padded dimension the large-route scratch is sized for
     double* d_lbound;      // [ndl] unit-vector Lemma 1 bound of the accepted k
     double* d_scratch;     // small device scratch (norms, bound)
     std::vector<std::vector<std::pair<int32_t, double>>> checks;  // per local direction: (k, bound)
 
     // generic path
     double* d_bl = nullptr;   // stencil affine term b (dense, length n) when lifted, else NULL
+    int64_t* d_long = nullptr;  // CSR rows with > KR_LONG_ROW entries
+    int64_t n_long = 0;
     double* d_cgs = nullptr;  // CGS2 scratch (N > KR_ORTHO_ONE_CTA_MAX)
     bool use_cgs = false;     // stored-basis orthogonalisation by the multi-CTA CGS2 path
     double* d_V;  // [ndl][k+1][N]
@@ -247,7 +251,7 @@ void kr_expm_enqueue(kr_handle* h);
 // kc, the coefficients c[j][.][d] of direction dl and the unit-vector Lemma 1 bound (returned; 0 with
 // zero_bound, an exact breakdown); fin also writes the direction's stats. Synchronises the stream.
 double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound);
-void kr_large_alloc(kr_handle* h);
+void kr_large_alloc(kr_handle* h, int kc);
 // fused Lanczos building blocks for the adaptive (host-driven) loop
 void kr_lz_enqueue_init(kr_handle* h, int dl);
 void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events);

@@ -312,9 +312,20 @@ static int pow2_at_least(int64_t n) {
     return p;
 }
 
-void kr_large_alloc(kr_handle* h) {
-    if (h->d_big) return;
-    const int kp = kpad(h->k);
+// Scratch for dimension kc, grown on demand (x1.5, capped at k): adaptive runs stop far below k_max.
+void kr_large_alloc(kr_handle* h, int kc) {
+    if (h->d_big && kc <= h->large_cap) return;
+    int cap = std::max(kc, std::min(h->k, std::max(64, h->large_cap + h->large_cap / 2)));
+    if (cap < kc) cap = kc;
+    const int kp = kpad(cap);
+    for (double* q : {h->d_big, h->d_traj}) {
+        if (!q) continue;
+        KR_CUDA(cudaStreamSynchronize(h->stream));
+        cudaFree(q);
+        h->extra_allocs.erase(std::remove(h->extra_allocs.begin(), h->extra_allocs.end(), (void*)q),
+                              h->extra_allocs.end());
+    }
+    h->d_big = h->d_traj = nullptr;
     const size_t mat = (size_t)kp * kp;
     KR_CUDA(cudaMalloc(&h->d_big, 3 * mat * sizeof(double)));
     h->extra_allocs.push_back(h->d_big);
@@ -322,6 +333,7 @@ void kr_large_alloc(kr_handle* h) {
     const size_t tr = std::max((size_t)(h->n_steps + 1) * kp, (size_t)kp * pow2_at_least(h->n_steps + 1));
     KR_CUDA(cudaMalloc(&h->d_traj, tr * sizeof(double)));
     h->extra_allocs.push_back(h->d_traj);
+    h->large_cap = kp;
 }
 
 static void gemm(kr_handle* h, const double* A, const double* B, double* C, int M, int N, int K, int lda, int ldb,
@@ -339,7 +351,7 @@ static void gemm(kr_handle* h, const double* A, const double* B, double* C, int 
 // coefficients of direction dl are always written (the last evaluation is the accepted one).
 // zero_bound: exact breakdown at kc (the approximation is exact): bound 0.
 double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
-    kr_large_alloc(h);
+    kr_large_alloc(h, kc);
     if (!h->ev_lg0) {
         KR_CUDA(cudaEventCreate(&h->ev_lg0));
         KR_CUDA(cudaEventCreate(&h->ev_lg1));

@@ -254,7 +254,8 @@ def heat_heater(m, k=64, n_steps=1000, step=0.5):
 
 CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5,
            "P100": lambda: heat_paper(100), "P1000": lambda: heat_paper(1000),
-           "H10": lambda: heat_heater(10), "H100": lambda: heat_heater(100, k=400)}
+           "H10": lambda: heat_heater(10), "H100": lambda: heat_heater(100, k=800),
+           "C2T": lambda: dict(config2(), sim="transpose")}
 
 
 def n_state(p):
