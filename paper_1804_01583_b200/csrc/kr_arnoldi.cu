@@ -7,7 +7,7 @@
 // GPU, and MGS's j dependent dot/axpy pairs per step become j grid-wide round trips. Here the projection
 // is classical Gram-Schmidt applied twice (CGS2: h = V^T w, w -= V h, repeated once), so each half-step is
 // ONE streaming pass over the j basis vectors:
-//   * dots:   part[b][l] = sum_{i in chunk b} V[l][i] w[i]   (grid = row chunks x blocks of 8 vectors)
+//   * dots:   part[b][l] = sum_{i in chunk b} V[l][i] w[i]   (grid = row chunks x blocks of 16 vectors)
 //   * reduce: h[l] = sum_b part[b][l] in chunk order; H[l][j] accumulates h1 + h2
 //   * update: w[i] -= sum_l V[l][i] h[l] (thread per row, coalesced over i), with sum w^2 partials on the
 //     second pass; then h_{j+1,j} = ||w||, the breakdown test, v_{j+1} = w / h_{j+1,j} and
@@ -23,7 +23,7 @@
 namespace {
 
 constexpr int CT = 256;
-constexpr int LB = 8;  // basis vectors per dots CTA
+constexpr int LB = 16;  // basis vectors per dots CTA
 
 struct CgsArgs {
     double* V;         // [ndl][k+1][N]
@@ -73,11 +73,23 @@ __global__ void __launch_bounds__(CT) cgs_dots_kernel(CgsArgs a) {
     double s[LB];
 #pragma unroll
     for (int q = 0; q < LB; ++q) s[q] = 0.0;
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += CT) {
-        const double wi = w[i];
+    const int nq = min(LB, a.j - l0);
+    if (nq == LB) {  // full block: all LB basis loads of a row issued together
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += CT) {
+            const double wi = w[i];
+            double v[LB];
 #pragma unroll
-        for (int q = 0; q < LB; ++q)
-            if (l0 + q < a.j) s[q] = fma(V[(int64_t)(l0 + q) * a.N + i], wi, s[q]);
+            for (int q = 0; q < LB; ++q) v[q] = __ldcs(&V[(int64_t)(l0 + q) * a.N + i]);
+#pragma unroll
+            for (int q = 0; q < LB; ++q) s[q] = fma(v[q], wi, s[q]);
+        }
+    } else {
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += CT) {
+            const double wi = w[i];
+#pragma unroll
+            for (int q = 0; q < LB; ++q)
+                if (q < nq) s[q] = fma(V[(int64_t)(l0 + q) * a.N + i], wi, s[q]);
+        }
     }
     double* out = a.part + ((int64_t)d * a.nchunk + b) * a.pstride;
 #pragma unroll
@@ -119,10 +131,31 @@ __global__ void __launch_bounds__(CT) cgs_update_kernel(CgsArgs a, int with_norm
         __syncthreads();
         for (int l = threadIdx.x; l < ln; l += CT) hs[l] = hv[lb + l];
         __syncthreads();
-        for (int64_t i = i0 + threadIdx.x; i < i1; i += CT) {
-            double acc = 0.0;
-            for (int l = 0; l < ln; ++l) acc = fma(V[(int64_t)(lb + l) * a.N + i], hs[l], acc);
-            w[i] -= acc;
+        // 4 rows per thread at a time, l unrolled: 16 independent basis loads in flight per thread
+        for (int64_t ib = i0 + threadIdx.x; ib < i1; ib += 4 * CT) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            const double* Vb = V + (int64_t)lb * a.N + ib;
+            int l = 0;
+            for (; l + 4 <= ln; l += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double hl = hs[l + u];
+                    const double* Vr = Vb + (int64_t)(l + u) * a.N;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (ib + q * CT < i1) acc[q] = fma(__ldcs(Vr + q * CT), hl, acc[q]);
+                }
+            }
+            for (; l < ln; ++l) {
+                const double hl = hs[l];
+                const double* Vr = Vb + (int64_t)l * a.N;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (ib + q * CT < i1) acc[q] = fma(Vr[q * CT], hl, acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (ib + q * CT < i1) w[ib + q * CT] -= acc[q];
         }
     }
     if (with_norm) {
