@@ -20,8 +20,7 @@
 //     where those squarings cost more than N passes over E, by the march x_{j+1} = E x_j in ONE
 //     cooperative kernel (warp per row, fixed-order warp reductions, a grid barrier per time step);
 //   * t = 0 is e_1 exactly.
-// The GEMM is plain fp64 (DFMA; B200 runs fp64 at the same rate on its CUDA cores as on the fp64 MMA
-// path, and this step is a few percent of the adaptive run).
+// The GEMM runs on the fp64 tensor cores (DMMA.8x8x4 through mma.sync: tcgen05 has no fp64 kind).
 #include <cooperative_groups.h>
 #include <math.h>
 
@@ -55,19 +54,32 @@ struct GemmArgs {
     double scale, diag;
 };
 
-__global__ void __launch_bounds__(GTH) gemm_band_kernel(const GemmArgs g) {
-    __shared__ double As[2][GK][SP];  // As[k][m] (k-major: conflict-free broadcast reads)
-    __shared__ double Bs[2][GK][SP];  // Bs[k][n]
+// fp64 tensor-core tile: DMMA.8x8x4 (mma.sync m8n8k4 f64) — 4 warps, each a 32x32 block of the 64x64 CTA tile
+// as 4x4 MMA tiles; operands staged k-major in shared memory (row stride 72 doubles: the 32 lanes of a
+// fragment load hit each bank pair exactly twice), double-buffered through registers.
+constexpr int DT = 128;
+constexpr int DSP = GT + 8;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(DT) gemm_band_kernel(const GemmArgs g) {
+    __shared__ double As[2][GK][DSP];  // As[k][m]
+    __shared__ double Bs[2][GK][DSP];  // Bs[k][n]
     const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
     // band structure only where declared (a bandwidth >= K - 1 means dense, e.g. the tall trajectory block)
     const bool bandA = g.ba < g.K - 1, bandB = g.bb < g.K - 1;
     const long long bc = (long long)g.ba + g.bb;
-    double acc[4][4];
+    double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     const bool outside =
         bandA && bandB && (((long long)j0 - (i0 + GT - 1) > bc) || ((long long)i0 - (j0 + GT - 1) > bc));
     if (!outside) {
@@ -83,24 +95,24 @@ __global__ void __launch_bounds__(GTH) gemm_band_kernel(const GemmArgs g) {
         const int l0 = (int)(lo / GK) * GK;
         const int l1 = (int)((hi + GK - 1) / GK) * GK;
         const int nkt = (l1 - l0) / GK;
-        // global -> register staging: A tile rows i0..i0+63, cols l..l+15 (4 per thread); B rows l..l+15,
-        // cols j0..j0+63 (4 per thread)
-        const int ar = tid >> 4, ac = tid & 15;   // A: row ar + 16q, col ac
-        const int br = tid >> 6, bcn = tid & 63;  // B: row br + 4q, col bcn
+        // global -> register staging (8 + 8 doubles per thread): A rows i0 + ar + 8q, col ac; B row br + 2q, col bcn
+        const int ar = tid >> 4, ac = tid & 15;
+        const int br = tid >> 6, bcn = tid & 63;
         const bool bin = j0 + bcn < g.N;
-        double ra[4], rb[4];
+        double ra[8], rb[8];
         auto gload = [&](int l) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) ra[q] = g.A[(size_t)(i0 + ar + 16 * q) * g.lda + l + ac];
+            for (int q = 0; q < 8; ++q) ra[q] = g.A[(size_t)(i0 + ar + 8 * q) * g.lda + l + ac];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) rb[q] = bin ? g.B[(size_t)(l + br + 4 * q) * g.ldb + j0 + bcn] : 0.0;
+            for (int q = 0; q < 8; ++q) rb[q] = bin ? g.B[(size_t)(l + br + 2 * q) * g.ldb + j0 + bcn] : 0.0;
         };
         auto sstore = [&](int buf) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) As[buf][ac][ar + 16 * q] = ra[q];
+            for (int q = 0; q < 8; ++q) As[buf][ac][ar + 8 * q] = ra[q];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) Bs[buf][br + 4 * q][bcn] = rb[q];
+            for (int q = 0; q < 8; ++q) Bs[buf][br + 2 * q][bcn] = rb[q];
         };
+        const int fk = lane & 3, fm = lane >> 2;  // fragment: k index and row / column index
         if (nkt > 0) {
             gload(l0);
             sstore(0);
@@ -109,32 +121,36 @@ __global__ void __launch_bounds__(GTH) gemm_band_kernel(const GemmArgs g) {
                 const int buf = t & 1;
                 if (t + 1 < nkt) gload(l0 + (t + 1) * GK);
 #pragma unroll
-                for (int kk = 0; kk < GK; ++kk) {
-                    double av[4], bv[4];
+                for (int k4 = 0; k4 < GK; k4 += 4) {
+                    double af[4], bf[4];
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) av[a] = As[buf][kk][ty + 16 * a];
+                    for (int a = 0; a < 4; ++a) af[a] = As[buf][k4 + fk][wm + 8 * a + fm];
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) bv[b] = Bs[buf][kk][tx + 16 * b];
+                    for (int b = 0; b < 4; ++b) bf[b] = Bs[buf][k4 + fk][wn + 8 * b + fm];
 #pragma unroll
                     for (int a = 0; a < 4; ++a)
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+                        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
                 }
                 if (t + 1 < nkt) sstore(buf ^ 1);
                 __syncthreads();
             }
         }
     }
+    // C fragment: row fm, columns 2 fk, 2 fk + 1 of each 8x8 tile
+    const int fk = lane & 3, fm = lane >> 2;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
-            if (j >= g.N) continue;
-            double v = g.scale * acc[a][b];
-            if (i == j && i < g.kc) v += g.diag;
-            g.C[(size_t)i * g.ldc + j] = v;
-        }
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = i0 + wm + 8 * a + fm, j = j0 + wn + 8 * b + 2 * fk + h;
+                if (j >= g.N) continue;
+                double v = g.scale * acc[a][b][h];
+                if (i == j && i < g.kc) v += g.diag;
+                g.C[(size_t)i * g.ldc + j] = v;
+            }
 }
 
 // ||H delta||_1 (max column sum of the symmetric tridiagonal; 1-based alpha[1..kc], beta[1..kc-1]).
@@ -340,7 +356,7 @@ static void gemm(kr_handle* h, const double* A, const double* B, double* C, int 
                  int ldc, int ba, int bb, int kc, double scale, double diag) {
     GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, ba, bb, kc, scale, diag};
     const dim3 grid((unsigned)((N + GT - 1) / GT), (unsigned)(M / GT));
-    gemm_band_kernel<<<grid, GTH, 0, h->stream>>>(g);
+    gemm_band_kernel<<<grid, DT, 0, h->stream>>>(g);
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }
