@@ -15,7 +15,7 @@
 //     first squarings stay banded: the fp64 GEMM below skips the structural zeros tile by tile (exact —
 //     products of banded matrices are exactly zero outside the band) and only the last few squarings
 //     are dense kc x kc products;
-//   * the time grid: for kc <= 3000 by doubling — x_{2^q + j} = E^{2^q} x_j, one GEMM of width 2^q per
+//   * the time grid: for kc <= 6000 by doubling — x_{2^q + j} = E^{2^q} x_j, one GEMM of width 2^q per
 //     level with E^{2^q} from further squarings (log2 N dependent launches instead of N); for larger kc,
 //     where those squarings cost more than N passes over E, by the march x_{j+1} = E x_j in ONE
 //     cooperative kernel (warp per row, fixed-order warp reductions, a grid barrier per time step);
@@ -431,7 +431,7 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
     double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
     const int64_t np1 = h->n_steps + 1;
-    int kdouble = 3000;  // doubling (GEMM-batched) time march up to this kc, the sequential march above
+    int kdouble = 6000;  // doubling (GEMM-batched) time march up to this kc, the sequential march above
     if (const char* e = getenv("KR_KDOUBLE")) kdouble = atoi(e);
     if (kc <= kdouble) {
         // Doubling: with the columns x_0 .. x_{2^q - 1} known, x_{2^q + j} = E^{2^q} x_j — one GEMM of width
