@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkrylov_reach.so")
+LIB_PATH = os.environ.get("KR_LIB_PATH") or os.path.join(HERE, "libkrylov_reach.so")  # override: A/B diagnostics
 
 KR_OK, KR_EINVAL, KR_EDIM, KR_ENOMEM, KR_ECUDA, KR_ENCCL, KR_ENOTSYM, KR_EZERO, KR_ENONFINITE, KR_ESTATE = range(10)
 STATUS_NAMES = ["KR_OK", "KR_EINVAL", "KR_EDIM", "KR_ENOMEM", "KR_ECUDA", "KR_ENCCL", "KR_ENOTSYM", "KR_EZERO",

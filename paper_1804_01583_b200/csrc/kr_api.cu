@@ -834,6 +834,17 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 KR_CUDA(cudaMemsetAsync(sl.counter, 0, (size_t)(1 + ngrp) * 4, h->stream));
                 h->slabs.push_back(sl);
             }
+            // virtual slabs: halos are written by the step kernel straight into the sibling slabs (the same
+            // code path as NVLink peer memory across processes); KR_HALO_COPY=1 keeps the copy transport
+            if (h->slabs.size() > 1 && !getenv("KR_HALO_COPY")) {
+                for (size_t si = 0; si < h->slabs.size(); ++si)
+                    for (int b = 0; b < 3; ++b) {
+                        h->slabs[si].peer_lo[b] = si > 0 ? h->slabs[si - 1].u[b] : nullptr;
+                        h->slabs[si].peer_hi[b] = si + 1 < h->slabs.size() ? h->slabs[si + 1].u[b] : nullptr;
+                    }
+                for (size_t si = 1; si < h->slabs.size(); ++si) h->slabs[si].peer_lo_nz = h->slabs[si - 1].nz;
+                h->halo_inkernel = true;
+            }
             kr_lz_encode_maps(h);
             kr_lz_prepare(h);
             const int R_total = (int)h->slabs.size() * h->world;

@@ -81,6 +81,9 @@ struct Slab {
     double* partials;    // [nblk][nqp]
     int32_t* counter;    // last-CTA arrival counter of the fused reduction
     int64_t nblk;        // persistent CTAs (= number of partial-sum slots)
+    double* peer_lo[3];  // the lower / upper neighbour's state buffers (peer memory or a sibling slab), or NULL
+    double* peer_hi[3];
+    int64_t peer_lo_nz;  // owned planes of the lower neighbour
     int32_t gx, gy;      // tiles per x / y
     int64_t nitems;      // work items = gx * gy * z-chunks
     dim3 grid;
@@ -191,6 +194,9 @@ struct kr_handle {
     double large_ms = 0.0;  // device time of the large-k route (exponentials + bounds) in the last project
     int32_t large_evals = 0;
     cudaEvent_t ev_lg0 = nullptr, ev_lg1 = nullptr;    // Lanczos steps run for local direction 0 by the last large-route project
+    bool halo_inkernel = false;  // halo planes written by the step kernel into the neighbours' buffers
+    bool p2p = false;            // ... across processes through CUDA IPC peer memory (NVLink)
+    void* p2p_base[2] = {nullptr, nullptr};  // opened IPC bases (lower, upper neighbour)
     bool large_route;      // exponentials through the large-k route (kr_large.cu) instead of per-step Pade
     // large-k route scratch (allocated at the first project that needs it, for kcap = k)
     double* d_big;         // 6 x kcap^2 doubles: X, X^2, X^3, X^4, Y, Y'

@@ -60,6 +60,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 
 struct StepArgs {
     double* out;  // buffer receiving u_{i+1} (buffer plane 0 = ghost below the slab)
+    // halo planes written straight into the neighbouring slabs' buffers (peer memory over NVLink, or the
+    // sibling slab of a virtual-slab run): my owned planes 0, 1 -> lower neighbour planes lo_nz+1, +2;
+    // my last owned plane -> upper neighbour plane 0. NULL = no such neighbour / message transport.
+    double* rlo;
+    double* rhi;
+    int64_t rlo_plane0;  // offset (doubles) of the lower neighbour's plane lo_nz + 1
+    int32_t rfence;      // 1: remote (other GPU) stores -> system-scope fence before the kernel ends
     int64_t pitch, plane;
     int32_t mx, my, mz, nz, zoff, zchunk;
     int32_t gx, gy, nitems;  // persistent work items: gx * gy tiles x ceil(nz / zchunk) chunks
@@ -122,7 +129,7 @@ constexpr size_t step_smem_bytes() {
 // BCM: 0 = Dirichlet everywhere (zero ghosts from the TMA fill); 1 = general faces, but this tile has no
 // x/y face cell (only the uniform per-plane z-face terms and the ring cells' own corrections apply);
 // 2 = general faces on a tile that touches an x or y face (per-cell terms).
-template <int TX, int TY, int S, bool INIT, bool FULL, int BCM>
+template <int TX, int TY, int S, bool INIT, bool FULL, int BCM, bool HALO>
 __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
                                          unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
                                          int zc0, int zc1, bool cta_box, double* acc) {
@@ -312,6 +319,18 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 }
                 if (wr && (FULL || ing[m])) optr[m * rowstep] = w0;
             }
+            // halo planes for the neighbours, stored where they will be read (uniform per plane, rare):
+            // owned planes 0, 1 -> the lower neighbour, the last owned plane -> the upper neighbour
+            const int qq = q - 1;
+            if (HALO && wr && ((a.rlo && qq < 2) || (a.rhi && qq == a.nz - 1))) {
+                const int64_t off = (optr - a.out) - (int64_t)(qq + 1) * a.plane;  // in-plane offset of slot 0
+#pragma unroll
+                for (int m = 0; m < G::TS; ++m) {
+                    if (!(FULL || ing[m])) continue;
+                    if (a.rlo && qq < 2) a.rlo[a.rlo_plane0 + (int64_t)qq * a.plane + off + m * rowstep] = wp[m];
+                    if (a.rhi && qq == a.nz - 1) a.rhi[off + m * rowstep] = wp[m];
+                }
+            }
             optr += a.plane;
         }
 #pragma unroll
@@ -332,7 +351,7 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
     acc[2] += acc_sum;
 }
 
-template <int TX, int TY, int S, bool INIT, bool BC>
+template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false>
 __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(const __grid_constant__ CUtensorMap tmC,
                                                          const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
     using G = Geo<TX, TY>;
@@ -371,11 +390,11 @@ __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(c
         constexpr int BCE = BC ? 2 : 0;
         if (x0 + TX < a.mx && y0 + TY < a.my) {
             if (BC && x0 > 0 && y0 > 0)  // no x/y face cell in the tile: only per-plane z-face terms
-                lz_march<TX, TY, S, INIT, true, 1>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+                lz_march<TX, TY, S, INIT, true, 1, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
             else
-                lz_march<TX, TY, S, INIT, true, BCE>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+                lz_march<TX, TY, S, INIT, true, BCE, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
         } else {
-            lz_march<TX, TY, S, INIT, false, BCE>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+            lz_march<TX, TY, S, INIT, false, BCE, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
         }
         __syncthreads();  // every issued plane was consumed: the barriers can be recycled for the next item
         if (tid == 0) {
@@ -385,6 +404,7 @@ __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(c
         }
     }
 
+    if (HALO && a.rfence) __threadfence_system();  // peer-memory halo stores visible before the collective that follows
     __syncthreads();  // stage buffers are free: reuse them as reduction scratch
     lz_epilogue(a, acc, reinterpret_cast<double*>(smem), a.plane);
 }
@@ -731,9 +751,9 @@ void kr_lz_encode_maps(kr_handle* h) {
         }
 }
 
-template <int TX, int TY, bool INIT, bool BC>
+template <int TX, int TY, bool INIT, bool BC, bool HALO = false>
 static void set_smem_attr() {
-    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, Stages<TX, TY>::S, INIT, BC>,
+    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, Stages<TX, TY>::S, INIT, BC, HALO>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
 }
@@ -744,6 +764,8 @@ static int occupancy_t() {
     set_smem_attr<TX, TY, true, false>();
     set_smem_attr<TX, TY, false, true>();
     set_smem_attr<TX, TY, true, true>();
+    set_smem_attr<TX, TY, false, false, true>();
+    set_smem_attr<TX, TY, false, true, true>();
     int nb = 0, nb2 = 0;
     KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, false>,
                                                           256, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
@@ -794,6 +816,15 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     a.step = step;
     a.has_prev = (!init && step > 1) ? 1 : 0;
     a.write_out = write ? 1 : 0;
+    a.rlo = a.rhi = nullptr;
+    a.rlo_plane0 = 0;
+    a.rfence = 0;
+    if (write && !init && h->halo_inkernel) {
+        a.rlo = sl.peer_lo[nxt];
+        a.rhi = sl.peer_hi[nxt];
+        a.rlo_plane0 = (sl.peer_lo_nz + 1) * (int64_t)h->pitch * h->my;
+        a.rfence = h->p2p ? 1 : 0;
+    }
     a.nqp = h->nqp;
     a.partials = sl.partials;
     a.nbox = (int)h->boxes.size();
@@ -838,14 +869,19 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
         const CUtensorMap& tc = sl.tmC[cur];
         const CUtensorMap& tp = sl.tmP[prev < 0 ? cur : prev];
         constexpr int S = Stages<TX, TY>::S;
+        const bool halo = a.rlo || a.rhi;  // this slab writes halo planes into a neighbour's buffer
         if (h->gen_bc) {
             if (init)
                 lz_step_kernel<TX, TY, S, true, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+            else if (halo)
+                lz_step_kernel<TX, TY, S, false, true, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
             else
                 lz_step_kernel<TX, TY, S, false, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
         } else {
             if (init)
                 lz_step_kernel<TX, TY, S, true, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+            else if (halo)
+                lz_step_kernel<TX, TY, S, false, false, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
             else
                 lz_step_kernel<TX, TY, S, false, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
         }
@@ -950,7 +986,7 @@ void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events) {
     for (auto& sl : h->slabs) step_launch(h, sl, dl, cur, prev, nxt, i, false, write);
     if (ev) KR_CUDA(kr_event_record(h->ev[2 * i - 1], h->stream));
     for (auto& sl : h->slabs) reduce_launch(h, sl, dl, nxt, i, false, write, write ? nxt : -1);
-    if (write) {
+    if (write && !h->halo_inkernel) {  // message transport: copies / NCCL send-recv after the step
         if (h->slabs.size() > 1) halo_exchange_virtual(h, nxt);
         if (h->world > 1) kr_nccl_halo(h->comm, h, nxt, h->stream);
     }
