@@ -271,6 +271,16 @@ def main():
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     h = KrylovReach(p, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw)
 
+    def attach(handle):
+        """z-slab ranks: halo planes stored by the step kernel into the neighbours' buffers over NVLink (CUDA IPC),
+        verified with a test pattern on every rank; otherwise (or with KR_P2P=0) the NCCL halo exchange."""
+        if world > 1 and kw.get("part") == "zslab" and os.environ.get("KR_P2P", "1") != "0":
+            from paper_1804_01583_b200 import torch_allgather_bytes
+            return handle.attach_peers(rank, world, torch_allgather_bytes, torch.distributed.barrier)
+        return False
+
+    p2p_on = attach(h)
+
     def one_step():
         h.project(want=False)
         return h.check_box(want_bounds=False)
@@ -329,6 +339,7 @@ def main():
             barrier()
             t0 = time.perf_counter()
             with KrylovReach(p, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw) as h2:
+                attach(h2)
                 c2, st2 = h2.project()
                 cb2 = h2.check_box()
                 tb = h2.transfer_bytes()
@@ -361,6 +372,8 @@ def main():
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "halo_transport": ("peer-memory stores from the step kernel (NVLink, CUDA IPC)" if p2p_on else
+                           ("NCCL send/recv" if world > 1 else "none (one rank)")),
         "iter_ms_mean": float(np.mean(iter_ms)),
         "verdict": {"found": cb["found"], "step": cb["step"]},
     }

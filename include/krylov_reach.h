@@ -260,6 +260,26 @@ kr_status krylov_comm_unique_id(void* id128);
 kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int32_t device, kr_comm** out);
 void krylov_comm_destroy(kr_comm* c);
 
+/* ---- peer-memory halo transport (NVLink P2P through CUDA IPC; one process per GPU) --------------
+ * With it the fused step kernel stores the halo planes of u_{i+1} straight into the neighbouring ranks'
+ * state buffers (the compute and the exchange in one kernel), instead of a halo message after each step;
+ * the per-step scalar all-gather, which follows every step anyway, orders those stores before any read.
+ * Protocol (every rank, in this order, before the first krylov_project; the caller provides the
+ * all-gather and the barrier, e.g. torch.distributed):
+ *   krylov_ipc_blob(h, blob)                     this rank's export, KR_IPC_BLOB_BYTES bytes (HOST)
+ *   all-gather the blobs in rank order          -> blobs [world][KR_IPC_BLOB_BYTES]
+ *   krylov_p2p_open(h, blobs, rank, world)       opens the neighbours' buffers, writes a test pattern
+ *   barrier
+ *   krylov_p2p_verify(h, &ok)                    checks the pattern the neighbours wrote into my halos
+ *   all-reduce ok (min) over ranks
+ *   krylov_p2p_enable(h, ok_all)                 1: switch to the peer-memory transport; 0: close, keep NCCL
+ * Stencil Lanczos path with one slab per rank only (KR_EINVAL otherwise). Collective.              */
+#define KR_IPC_BLOB_BYTES 512
+kr_status krylov_ipc_blob(kr_handle* h, void* blob);
+kr_status krylov_p2p_open(kr_handle* h, const void* blobs, int32_t rank, int32_t world);
+kr_status krylov_p2p_verify(kr_handle* h, int32_t* ok);
+kr_status krylov_p2p_enable(kr_handle* h, int32_t on);
+
 /* z-slab partition of the stencil grid (host logic, no GPU): rank r of world owns global planes
  * [z0, z1). Balanced: the first mz % world ranks own one extra plane. KR_EINVAL if a rank would own
  * fewer than 2 planes (the depth-2 halo comes from one neighbour). */

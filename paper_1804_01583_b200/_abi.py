@@ -20,6 +20,7 @@ KR_VEC_SPARSE, KR_VEC_BOX, KR_VEC_ALL = 0, 1, 2
 KR_BC_DIRICHLET, KR_BC_INSULATED, KR_BC_ROBIN = 0, 1, 2
 KR_K_MAX_FIXED_PADE, KR_K_MAX, KR_K_MAX_ARNOLDI = 64, 16384, 2048
 KR_SIM_FORWARD, KR_SIM_TRANSPOSE, KR_SIM_AUTO = 0, 1, 2
+KR_IPC_BLOB_BYTES = 512
 
 
 class kr_vec(C.Structure):
@@ -61,7 +62,7 @@ EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "k
            "krylov_comm_unique_id", "krylov_comm_create", "krylov_comm_destroy", "krylov_zslab_range",
            "krylov_krylov_data", "krylov_transfer_bytes", "krylov_zslab_halo_plan", "krylov_tridiag",
            "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info", "krylov_check_lp",
-           "krylov_eval_outputs"]
+           "krylov_eval_outputs", "krylov_ipc_blob", "krylov_p2p_open", "krylov_p2p_verify", "krylov_p2p_enable"]
 
 _lib = None
 
@@ -94,6 +95,10 @@ def lib():
     L.krylov_krylov_data.argtypes = [vp, C.c_int32, vp, vp]
     L.krylov_check_lp.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, vp, vp, vp, C.POINTER(kr_cex), vp, vp]
     L.krylov_eval_outputs.argtypes = [vp, C.c_int64, vp, vp]
+    L.krylov_ipc_blob.argtypes = [vp, vp]
+    L.krylov_p2p_open.argtypes = [vp, vp, C.c_int32, C.c_int32]
+    L.krylov_p2p_verify.argtypes = [vp, C.POINTER(C.c_int32)]
+    L.krylov_p2p_enable.argtypes = [vp, C.c_int32]
     L.krylov_sim_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.krylov_last_timing_large.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     L.krylov_tridiag.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.POINTER(C.c_int32)]

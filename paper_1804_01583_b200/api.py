@@ -181,6 +181,46 @@ class KrylovReach:
         A.check(A.lib().krylov_eval_outputs(self.h, int(step), _p(z), _p(y)))
         return y
 
+    def attach_peers(self, rank, world, allgather, barrier):
+        """Peer-memory halo transport (krylov_ipc_blob / p2p_open / p2p_verify / p2p_enable): the z-slab step
+        kernel then stores its halo planes straight into the neighbours' buffers over NVLink. allgather(bytes)
+        -> list of bytes in rank order and barrier() are collectives the caller provides (torch.distributed).
+        Every rank takes part even if its own part fails, and the transport is switched on only if every
+        rank verified the test pattern; otherwise the NCCL halo exchange stays. Returns True if enabled."""
+        ok = 0
+        blobs = None
+        self.p2p_error = None
+        try:
+            blob = (C.c_ubyte * A.KR_IPC_BLOB_BYTES)()
+            A.check(A.lib().krylov_ipc_blob(self.h, blob))
+            mine = bytes(blob)
+        except A.KrylovError as e:
+            self.p2p_error = repr(e)
+            mine = bytes(A.KR_IPC_BLOB_BYTES)
+        blobs = allgather(mine)
+        try:
+            allb = (C.c_ubyte * (A.KR_IPC_BLOB_BYTES * world)).from_buffer_copy(b"".join(blobs))
+            A.check(A.lib().krylov_p2p_open(self.h, allb, int(rank), int(world)))
+            opened = True
+        except A.KrylovError as e:
+            self.p2p_error = self.p2p_error or repr(e)
+            opened = False
+        barrier()
+        if opened:
+            v = C.c_int32()
+            try:
+                A.check(A.lib().krylov_p2p_verify(self.h, C.byref(v)))
+                ok = int(v.value)
+                if not ok:
+                    self.p2p_error = "test pattern mismatch"
+            except A.KrylovError as e:
+                self.p2p_error = self.p2p_error or repr(e)
+                ok = 0
+        oks = allgather(bytes([ok]))
+        on = all(len(o) == 1 and o[0] == 1 for o in oks)
+        A.check(A.lib().krylov_p2p_enable(self.h, 1 if on else 0))
+        return on
+
     def krylov_data(self, d=0):
         """(H [(k+1) x k], P [n_out x k]) of direction d (Hessenberg / tridiagonal and P = C V)."""
         k = int(self.prob["k"])
@@ -314,6 +354,14 @@ class KrComm:
         if self.ptr:
             A.lib().krylov_comm_destroy(self.ptr)
             self.ptr = None
+
+
+def torch_allgather_bytes(data):
+    """All-gather a bytes object over the default torch.distributed group (rank order)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, data)
+    return out
 
 
 def torch_broadcast_id(data):

@@ -479,6 +479,7 @@ __global__ void transpose_coeff_kernel(const double* sim, double* cf, int64_t np
 
 void free_handle(kr_handle* h) {
     if (!h) return;
+    kr_p2p_close(h);
     if (h->graph_ready) cudaGraphExecDestroy(h->gexec);
     for (auto e : h->ev) cudaEventDestroy(e);
     if (h->ev_it0) cudaEventDestroy(h->ev_it0);
@@ -1312,6 +1313,49 @@ kr_status krylov_eval_outputs(kr_handle* h, int64_t step, const double* z, doubl
             if (!std::isfinite(z[d])) KR_THROW(KR_ENONFINITE, "z");
         KR_CUDA(cudaSetDevice(h->device));
         kr_eval_outputs(h, step, z, y);
+    });
+}
+
+kr_status krylov_ipc_blob(kr_handle* h, void* blob) {
+    return guarded([&] {
+        if (!h || !blob) KR_THROW(KR_EINVAL, "NULL argument");
+        KR_CUDA(cudaSetDevice(h->device));
+        kr_p2p_blob(h, blob);
+    });
+}
+
+kr_status krylov_p2p_open(kr_handle* h, const void* blobs, int32_t rank, int32_t world) {
+    return guarded([&] {
+        if (!h || !blobs) KR_THROW(KR_EINVAL, "NULL argument");
+        KR_CUDA(cudaSetDevice(h->device));
+        kr_p2p_open(h, blobs, rank, world);
+    });
+}
+
+kr_status krylov_p2p_verify(kr_handle* h, int32_t* ok) {
+    return guarded([&] {
+        if (!h || !ok) KR_THROW(KR_EINVAL, "NULL argument");
+        KR_CUDA(cudaSetDevice(h->device));
+        kr_p2p_verify(h, ok);
+    });
+}
+
+kr_status krylov_p2p_enable(kr_handle* h, int32_t on) {
+    return guarded([&] {
+        if (!h) KR_THROW(KR_EINVAL, "NULL handle");
+        KR_CUDA(cudaSetDevice(h->device));
+        if (h->graph_ready) {  // kernel arguments change: recapture at the next project
+            KR_CUDA(cudaGraphExecDestroy(h->gexec));
+            h->graph_ready = false;
+        }
+        if (on) {
+            if (!h->p2p_base[0] && !h->p2p_base[1] && h->p2p_world > 1)
+                KR_THROW(KR_ESTATE, "krylov_p2p_enable before krylov_p2p_open");
+            h->p2p = h->halo_inkernel = h->p2p_world > 1;
+        } else {
+            kr_p2p_close(h);
+            h->p2p = h->halo_inkernel = false;
+        }
     });
 }
 

@@ -66,3 +66,157 @@ void kr_nccl_halo(kr_comm* c, kr_handle* h, int buf, cudaStream_t s) {
     }
     KR_NCCL(ncclGroupEnd());
 }
+
+// ------------------------------------------------------------------------------------------------
+// Peer-memory (NVLink P2P) halo transport across processes: the z-slab step kernel stores the halo planes
+// of u_{i+1} directly into the neighbouring ranks' state buffers (CUDA IPC), so the per-step halo
+// messages disappear; the per-step scalar all-gather that follows each step orders those stores before
+// any neighbour reads them (system-scope fence at the end of the step kernel).
+// ------------------------------------------------------------------------------------------------
+namespace {
+
+struct IpcBlob {
+    int32_t magic, rank;
+    int64_t nz, pitch, my;
+    int32_t device, pad;
+    cudaIpcMemHandle_t handle;  // of the allocation holding the three state buffers
+    int64_t off[3];             // byte offsets of u[0..2] from the allocation base
+};
+static_assert(sizeof(IpcBlob) <= KR_IPC_BLOB_BYTES, "blob size");
+constexpr int32_t kMagic = 0x4b525032;  // "KRP2"
+constexpr int kPat = 64;                // test-pattern doubles per halo plane
+
+__device__ __host__ inline double pattern(int src_rank, int plane_tag, int i) {
+    return 1000.0 * (src_rank + 1) + 10.0 * plane_tag + 1e-3 * i;
+}
+
+// writes the test pattern into the neighbours' halo planes of buffer 0 (tags: 1, 2 = lower neighbour's
+// upper halo planes; 0 = upper neighbour's lower halo plane)
+__global__ void p2p_write_kernel(double* lo, int64_t lo_off1, double* hi, int64_t plane, int rank) {
+    const int i = threadIdx.x;
+    if (i >= kPat) return;
+    if (lo) {
+        lo[lo_off1 + i] = pattern(rank, 1, i);
+        lo[lo_off1 + plane + i] = pattern(rank, 2, i);
+    }
+    if (hi) hi[i] = pattern(rank, 0, i);
+    __threadfence_system();
+}
+
+__global__ void p2p_check_kernel(double* own, int64_t nz, int64_t plane, int has_lo, int has_hi, int rank, int* ok) {
+    const int i = threadIdx.x;
+    if (i >= kPat) return;
+    bool good = true;
+    if (has_lo) {  // my plane 0 was written by rank - 1
+        good &= own[i] == pattern(rank - 1, 0, i);
+        own[i] = 0.0;
+    }
+    if (has_hi) {  // my planes nz+1, nz+2 were written by rank + 1
+        good &= own[(nz + 1) * plane + i] == pattern(rank + 1, 1, i);
+        good &= own[(nz + 2) * plane + i] == pattern(rank + 1, 2, i);
+        own[(nz + 1) * plane + i] = 0.0;
+        own[(nz + 2) * plane + i] = 0.0;
+    }
+    if (!good) atomicExch(ok, 0);
+}
+
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+AddrRangeFn get_addr_range() {
+    static AddrRangeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        KR_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) KR_THROW(KR_ECUDA, "cuMemGetAddressRange unavailable");
+        fn = reinterpret_cast<AddrRangeFn>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+void kr_p2p_blob(kr_handle* h, void* out) {
+    if (h->path != PATH_FUSED_LANCZOS || h->slabs.size() != 1)
+        KR_THROW(KR_EINVAL, "peer-memory halos need the stencil Lanczos path with one slab per rank");
+    const Slab& sl = h->slabs[0];
+    CUdeviceptr base = 0;
+    size_t sz = 0;
+    if (get_addr_range()(&base, &sz, reinterpret_cast<CUdeviceptr>(sl.u[0])) != CUDA_SUCCESS)
+        KR_THROW(KR_ECUDA, "cuMemGetAddressRange failed");
+    IpcBlob b{};
+    b.magic = kMagic;
+    b.rank = h->rank;
+    b.nz = sl.nz;
+    b.pitch = h->pitch;
+    b.my = h->my;
+    b.device = h->device;
+    KR_CUDA(cudaIpcGetMemHandle(&b.handle, reinterpret_cast<void*>(base)));
+    for (int k = 0; k < 3; ++k) b.off[k] = reinterpret_cast<char*>(sl.u[k]) - reinterpret_cast<char*>(base);
+    memset(out, 0, KR_IPC_BLOB_BYTES);
+    memcpy(out, &b, sizeof(b));
+}
+
+void kr_p2p_close(kr_handle* h) {
+    for (int s = 0; s < 2; ++s)
+        if (h->p2p_base[s]) {
+            cudaIpcCloseMemHandle(h->p2p_base[s]);
+            h->p2p_base[s] = nullptr;
+        }
+    if (!h->slabs.empty())
+        for (int k = 0; k < 3; ++k) h->slabs[0].peer_lo[k] = h->slabs[0].peer_hi[k] = nullptr;
+}
+
+void kr_p2p_open(kr_handle* h, const void* blobs, int32_t rank, int32_t world) {
+    if (h->path != PATH_FUSED_LANCZOS || h->slabs.size() != 1) KR_THROW(KR_EINVAL, "peer-memory halos: one slab per rank");
+    if (rank < 0 || rank >= world) KR_THROW(KR_EINVAL, "bad rank / world");
+    if (h->comm && (h->comm->rank != rank || h->comm->world != world)) KR_THROW(KR_EINVAL, "rank / world != comm");
+    kr_p2p_close(h);
+    const char* all = reinterpret_cast<const char*>(blobs);
+    auto blob = [&](int r) {
+        IpcBlob b;
+        memcpy(&b, all + (size_t)r * KR_IPC_BLOB_BYTES, sizeof(b));
+        if (b.magic != kMagic) KR_THROW(KR_EINVAL, "bad peer blob");
+        if (h->comm && b.rank != r) KR_THROW(KR_EINVAL, "peer blob of another rank");
+        if (b.pitch != h->pitch || b.my != h->my) KR_THROW(KR_EINVAL, "peer grid layout differs");
+        return b;
+    };
+    Slab& sl = h->slabs[0];
+    h->p2p_rank = rank;
+    h->p2p_world = world;
+    for (int s = 0; s < 2; ++s) {
+        const int peer = s == 0 ? rank - 1 : rank + 1;
+        if (peer < 0 || peer >= world) continue;
+        const IpcBlob b = blob(peer);
+        void* base = nullptr;
+        KR_CUDA(cudaIpcOpenMemHandle(&base, b.handle, cudaIpcMemLazyEnablePeerAccess));
+        h->p2p_base[s] = base;
+        for (int k = 0; k < 3; ++k) {
+            double* u = reinterpret_cast<double*>(reinterpret_cast<char*>(base) + b.off[k]);
+            (s == 0 ? sl.peer_lo : sl.peer_hi)[k] = u;
+        }
+        if (s == 0) sl.peer_lo_nz = b.nz;
+    }
+    const int64_t plane = h->pitch * h->my;
+    p2p_write_kernel<<<1, kPat, 0, h->stream>>>(sl.peer_lo[0], (sl.peer_lo_nz + 1) * plane, sl.peer_hi[0], plane, rank);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    KR_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+void kr_p2p_verify(kr_handle* h, int32_t* ok) {
+    if (h->slabs.size() != 1) KR_THROW(KR_EINVAL, "peer-memory halos: one slab per rank");
+    const Slab& sl = h->slabs[0];
+    const int64_t plane = h->pitch * h->my;
+    int* d_ok = reinterpret_cast<int*>(h->d_scratch + 4);  // d_scratch holds 8 doubles; 0-1 belong to the large route
+    const int one = 1;
+    KR_CUDA(cudaMemcpyAsync(d_ok, &one, 4, cudaMemcpyHostToDevice, h->stream));
+    p2p_check_kernel<<<1, kPat, 0, h->stream>>>(sl.u[0], sl.nz, plane, h->p2p_rank > 0,
+                                                h->p2p_rank + 1 < h->p2p_world, h->p2p_rank, d_ok);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    int got = 0;
+    KR_CUDA(cudaMemcpyAsync(&got, d_ok, 4, cudaMemcpyDeviceToHost, h->stream));
+    KR_CUDA(cudaStreamSynchronize(h->stream));
+    *ok = got;
+}

@@ -197,6 +197,7 @@ struct kr_handle {
     bool halo_inkernel = false;  // halo planes written by the step kernel into the neighbours' buffers
     bool p2p = false;            // ... across processes through CUDA IPC peer memory (NVLink)
     void* p2p_base[2] = {nullptr, nullptr};  // opened IPC bases (lower, upper neighbour)
+    int32_t p2p_rank = 0, p2p_world = 1;
     bool large_route;      // exponentials through the large-k route (kr_large.cu) instead of per-step Pade
     // large-k route scratch (allocated at the first project that needs it, for kcap = k)
     double* d_big;         // 6 x kcap^2 doubles: X, X^2, X^3, X^4, Y, Y'
@@ -272,3 +273,8 @@ void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int
 // nccl
 void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s);
 void kr_nccl_halo(kr_comm* c, kr_handle* h, int buf, cudaStream_t s);
+// peer-memory halo transport (kr_comm.cu)
+void kr_p2p_blob(kr_handle* h, void* out);
+void kr_p2p_open(kr_handle* h, const void* blobs, int32_t rank, int32_t world);
+void kr_p2p_verify(kr_handle* h, int32_t* ok);
+void kr_p2p_close(kr_handle* h);
