@@ -167,3 +167,22 @@ def test_large_route_doubling_equals_march(k, monkeypatch):
     b_or = r["beta0"] * oracle.lemma1_bound(r["beta"][k - 1], X, p["step"], 0.0)
     assert abs(s1["lemma1"] - b_or) <= 1e-8 * b_or
     assert_coeff(c1, (r["beta0"] * (X @ r["P"].T))[:, :, None], f"oracle k={k}")
+
+
+def test_large_fixed_k_on_virtual_slabs():
+    """k > 64 (large-k route) with the z-slab decomposition (3 slabs, in-kernel halo stores)."""
+    p = W.heat(20, 4, 90, n_steps=100, mz=17)
+    c1, s1, _, _ = gpu(p)
+    c3, s3, _, _ = gpu(p, virtual_slabs=3)
+    assert s1[0]["k_eff"] == s3[0]["k_eff"]
+    assert_coeff(c3, c1, "large k vs=3")
+
+
+def test_adaptive_zero_horizon():
+    """n_steps = 0 (T = 0): the Lemma-1 integral vanishes, the first checkpoint (k = 4) is accepted and the
+    only output is the t = 0 identity c = O v."""
+    p = W.heat_paper(15, k_max=100, n_steps=0)
+    ref = oracle.krylov_project_adaptive(p)
+    coeff, stats, _, checks = gpu(p)
+    assert stats[0]["k_eff"] == ref["per_dir"][0]["k_eff"] == 4 and checks == [(4, 0.0)]
+    assert_coeff(coeff, ref["coeff"], "adaptive T=0")

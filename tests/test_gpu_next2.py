@@ -76,3 +76,11 @@ def test_auto_keeps_forward_when_fewer_directions():
     p = W.heat(20, 3, 20, n_steps=40)
     _, stats, _, (tr, ns, _) = run(p, sim="auto")
     assert not tr and ns == 1
+
+
+def test_transpose_more_simulations_than_directions():
+    """Forced transpose with o = 4 > i = 1 (AUTO would stay forward): still the oracle's transpose result."""
+    p = W.heat(14, 3, 20, n_steps=40)
+    coeff, stats, cb, (tr, ns, _) = run(p, sim="transpose")
+    assert tr and ns == 4 and len(stats) == 4
+    assert_coeff(coeff, oracle.krylov_project_transpose(p)["coeff"], "heat^T o>i")

@@ -130,3 +130,22 @@ def test_counterexample_resimulation():
         assert np.allclose(y_dev, lp["y"], rtol=1e-12, atol=1e-14)
     rel, y_re = validate_counterexample(p, lp["step"], lp["z"], lp["y"], k=64, sim="forward")
     assert rel < 1e-9, rel
+
+
+def test_lp_degenerate_cases():
+    """No constraints at all (every step feasible: first unsafe step 0, witness in the box); an empty initial
+    polytope (z_0 <= -2 with z_0 in [0.9, 1.1]: never feasible); n_steps = 0."""
+    from paper_1804_01583_b200 import KrylovReach
+    p = W.heat(12, 2, 10, n_steps=20)
+    with KrylovReach(p) as h:
+        h.project()
+        lp = h.check_lp()
+        assert lp["found"] and lp["step"] == 0 and 0.9 <= lp["z"][0] <= 1.1
+        assert np.all(lp["feasible"] == 1)
+        lp = h.check_lp([[1.0]], [-2.0], None, None)
+        assert not lp["found"] and np.all(lp["feasible"] == 0)
+    q = W.heat(12, 2, 10, n_steps=0)
+    with KrylovReach(q) as h:
+        c, _ = h.project()
+        lp = h.check_lp(None, None, [[-1.0, 0, 0, 0]], [-1e9])  # center >= 1e9: infeasible
+        assert not lp["found"] and lp["feasible"].shape == (1,)
