@@ -9,6 +9,8 @@
 // and integrates it (trapezoid on the t_j grid).
 #include <math.h>
 
+#include <algorithm>
+
 #include "kr_internal.h"
 
 namespace {
@@ -62,6 +64,156 @@ struct ExpmArgs {
     double* hlast;       // [ndl][n_steps+1]
 };
 
+// e^{H t} of the leading n x n block of H (row stride k) by scaling and squaring with the degree-13 diagonal
+// Pade approximant (Higham 2005): six n x (n+1) buffers of shared memory in sm; returns the buffer holding the
+// result (row stride n + 1). All threads of the CTA must call it.
+__device__ double* pade13(const double* Hd, int k, int n, double t, double* sm, double* fac, int& piv_s, int& sq_s) {
+    const int ld = n + 1;
+    const int msz = n * ld;
+    double* B0 = sm;
+    double* B1 = B0 + msz;
+    double* B2 = B1 + msz;
+    double* B3 = B2 + msz;
+    double* B4 = B3 + msz;
+    double* B5 = B4 + msz;
+    for (int e = threadIdx.x; e < n * n; e += ET) {
+        const int r = e / n, c = e - r * n;
+        B0[r * ld + c] = Hd[r * k + c] * t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // 1-norm (max column sum) -> number of squarings
+        double cmax = 0.0;
+        for (int c = threadIdx.x; c < n; c += 32) {
+            double s = 0.0;
+            for (int r = 0; r < n; ++r) s += fabs(B0[r * ld + c]);
+            cmax = fmax(cmax, s);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cmax = fmax(cmax, __shfl_down_sync(0xffffffffu, cmax, o));
+        if (threadIdx.x == 0) {
+            const double theta13 = 5.371920351148152;
+            int s = 0;
+            if (cmax > theta13) s = (int)ceil(log2(cmax / theta13));
+            while (ldexp(cmax, -s) > theta13) ++s;
+            sq_s = s < 0 ? 0 : s;
+        }
+    }
+    __syncthreads();
+    const int s = sq_s;
+    if (s > 0)
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int r = e / n, c = e - r * n;
+            B0[r * ld + c] = ldexp(B0[r * ld + c], -s);
+        }
+    __syncthreads();
+    const double b0 = 64764752532480000.0, b1 = 32382376266240000.0, b2 = 7771770303897600.0,
+                 b3 = 1187353796428800.0, b4 = 129060195264000.0, b5 = 10559470521600.0, b6 = 670442572800.0,
+                 b7 = 33522128640.0, b8 = 1323241920.0, b9 = 40840800.0, b10 = 960960.0, b11 = 16380.0,
+                 b12 = 182.0, b13 = 1.0;
+    mm(B0, B0, B1, n, ld);  // A2
+    __syncthreads();
+    mm(B1, B1, B2, n, ld);  // A4
+    __syncthreads();
+    mm(B2, B1, B3, n, ld);  // A6
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += ET) {
+        const int o = (e / n) * ld + e % n;
+        B4[o] = b13 * B3[o] + b11 * B2[o] + b9 * B1[o];
+    }
+    __syncthreads();
+    mm(B3, B4, B5, n, ld);  // A6 (b13 A6 + b11 A4 + b9 A2)
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += ET) {
+        const int r = e / n, c = e - r * n, o = r * ld + c;
+        B5[o] = B5[o] + b7 * B3[o] + b5 * B2[o] + b3 * B1[o] + (r == c ? b1 : 0.0);
+    }
+    __syncthreads();
+    mm(B0, B5, B4, n, ld);  // U = A * (...)
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += ET) {
+        const int o = (e / n) * ld + e % n;
+        B5[o] = b12 * B3[o] + b10 * B2[o] + b8 * B1[o];
+    }
+    __syncthreads();
+    mm(B3, B5, B0, n, ld);  // A6 (b12 A6 + b10 A4 + b8 A2)  (A no longer needed)
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += ET) {
+        const int r = e / n, c = e - r * n, o = r * ld + c;
+        const double V = B0[o] + b6 * B3[o] + b4 * B2[o] + b2 * B1[o] + (r == c ? b0 : 0.0);
+        const double U = B4[o];
+        B1[o] = V + U;  // P
+        B2[o] = V - U;  // Q
+    }
+    __syncthreads();
+    // solve Q F = P: LU with partial pivoting (lowest index wins ties), F overwrites P
+    double* Q = B2;
+    double* F = B1;
+    for (int c = 0; c < n; ++c) {
+        if (threadIdx.x < 32) {
+            double best = -1.0;
+            int bi = c;
+            for (int i = c + threadIdx.x; i < n; i += 32) {
+                const double v = fabs(Q[i * ld + c]);
+                if (v > best) {
+                    best = v;
+                    bi = i;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_down_sync(0xffffffffu, best, o);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
+            }
+            if (threadIdx.x == 0) piv_s = bi;
+        }
+        __syncthreads();
+        const int p = piv_s;
+        if (p != c)
+            for (int col = threadIdx.x; col < n; col += ET) {
+                double t0 = Q[c * ld + col];
+                Q[c * ld + col] = Q[p * ld + col];
+                Q[p * ld + col] = t0;
+                t0 = F[c * ld + col];
+                F[c * ld + col] = F[p * ld + col];
+                F[p * ld + col] = t0;
+            }
+        __syncthreads();
+        for (int i = c + 1 + threadIdx.x; i < n; i += ET) fac[i] = Q[i * ld + c] / Q[c * ld + c];
+        __syncthreads();
+        const int rows = n - c - 1;
+        for (int e = threadIdx.x; e < rows * n; e += ET) {
+            const int i = c + 1 + e / n, col = e % n;
+            const double f = fac[i];
+            F[i * ld + col] -= f * F[c * ld + col];
+            if (col > c) Q[i * ld + col] -= f * Q[c * ld + col];
+        }
+        __syncthreads();
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        for (int col = threadIdx.x; col < n; col += ET) {
+            double t0 = F[i * ld + col];
+            for (int l = i + 1; l < n; ++l) t0 -= Q[i * ld + l] * F[l * ld + col];
+            F[i * ld + col] = t0 / Q[i * ld + i];
+        }
+        __syncthreads();
+    }
+    // square s times
+    double* X = F;
+    double* Y = B3;
+    for (int r = 0; r < s; ++r) {
+        mm(X, X, Y, n, ld);
+        __syncthreads();
+        double* t0 = X;
+        X = Y;
+        Y = t0;
+    }
+    return X;
+}
+
 __global__ void __launch_bounds__(ET) expm_project_kernel(ExpmArgs a) {
     const int64_t j = blockIdx.x;
     const int d = blockIdx.y;
@@ -77,153 +229,10 @@ __global__ void __launch_bounds__(ET) expm_project_kernel(ExpmArgs a) {
         return;
     }
     const int ld = n + 1;
-    const int msz = n * ld;
-    double* B0 = sm;
-    double* B1 = B0 + msz;
-    double* B2 = B1 + msz;
-    double* B3 = B2 + msz;
-    double* B4 = B3 + msz;
-    double* B5 = B4 + msz;
     if (j == 0) {
         for (int i = threadIdx.x; i < n; i += ET) xs[i] = i == 0 ? 1.0 : 0.0;  // e^{H 0} e_1 = e_1 exactly
     } else {
-        const double t = (double)j * a.step;
-        const double* Hd = a.H + (int64_t)d * (k + 1) * k;
-        for (int e = threadIdx.x; e < n * n; e += ET) {
-            const int r = e / n, c = e - r * n;
-            B0[r * ld + c] = Hd[r * k + c] * t;
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {  // 1-norm (max column sum) -> number of squarings
-            double cmax = 0.0;
-            for (int c = threadIdx.x; c < n; c += 32) {
-                double s = 0.0;
-                for (int r = 0; r < n; ++r) s += fabs(B0[r * ld + c]);
-                cmax = fmax(cmax, s);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) cmax = fmax(cmax, __shfl_down_sync(0xffffffffu, cmax, o));
-            if (threadIdx.x == 0) {
-                const double theta13 = 5.371920351148152;
-                int s = 0;
-                if (cmax > theta13) s = (int)ceil(log2(cmax / theta13));
-                while (ldexp(cmax, -s) > theta13) ++s;
-                sq_s = s < 0 ? 0 : s;
-            }
-        }
-        __syncthreads();
-        const int s = sq_s;
-        if (s > 0)
-            for (int e = threadIdx.x; e < n * n; e += ET) {
-                const int r = e / n, c = e - r * n;
-                B0[r * ld + c] = ldexp(B0[r * ld + c], -s);
-            }
-        __syncthreads();
-        const double b0 = 64764752532480000.0, b1 = 32382376266240000.0, b2 = 7771770303897600.0,
-                     b3 = 1187353796428800.0, b4 = 129060195264000.0, b5 = 10559470521600.0, b6 = 670442572800.0,
-                     b7 = 33522128640.0, b8 = 1323241920.0, b9 = 40840800.0, b10 = 960960.0, b11 = 16380.0,
-                     b12 = 182.0, b13 = 1.0;
-        mm(B0, B0, B1, n, ld);  // A2
-        __syncthreads();
-        mm(B1, B1, B2, n, ld);  // A4
-        __syncthreads();
-        mm(B2, B1, B3, n, ld);  // A6
-        __syncthreads();
-        for (int e = threadIdx.x; e < n * n; e += ET) {
-            const int o = (e / n) * ld + e % n;
-            B4[o] = b13 * B3[o] + b11 * B2[o] + b9 * B1[o];
-        }
-        __syncthreads();
-        mm(B3, B4, B5, n, ld);  // A6 (b13 A6 + b11 A4 + b9 A2)
-        __syncthreads();
-        for (int e = threadIdx.x; e < n * n; e += ET) {
-            const int r = e / n, c = e - r * n, o = r * ld + c;
-            B5[o] = B5[o] + b7 * B3[o] + b5 * B2[o] + b3 * B1[o] + (r == c ? b1 : 0.0);
-        }
-        __syncthreads();
-        mm(B0, B5, B4, n, ld);  // U = A * (...)
-        __syncthreads();
-        for (int e = threadIdx.x; e < n * n; e += ET) {
-            const int o = (e / n) * ld + e % n;
-            B5[o] = b12 * B3[o] + b10 * B2[o] + b8 * B1[o];
-        }
-        __syncthreads();
-        mm(B3, B5, B0, n, ld);  // A6 (b12 A6 + b10 A4 + b8 A2)  (A no longer needed)
-        __syncthreads();
-        for (int e = threadIdx.x; e < n * n; e += ET) {
-            const int r = e / n, c = e - r * n, o = r * ld + c;
-            const double V = B0[o] + b6 * B3[o] + b4 * B2[o] + b2 * B1[o] + (r == c ? b0 : 0.0);
-            const double U = B4[o];
-            B1[o] = V + U;  // P
-            B2[o] = V - U;  // Q
-        }
-        __syncthreads();
-        // solve Q F = P: LU with partial pivoting (lowest index wins ties), F overwrites P
-        double* Q = B2;
-        double* F = B1;
-        for (int c = 0; c < n; ++c) {
-            if (threadIdx.x < 32) {
-                double best = -1.0;
-                int bi = c;
-                for (int i = c + threadIdx.x; i < n; i += 32) {
-                    const double v = fabs(Q[i * ld + c]);
-                    if (v > best) {
-                        best = v;
-                        bi = i;
-                    }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double ob = __shfl_down_sync(0xffffffffu, best, o);
-                    const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-                    if (ob > best || (ob == best && oi < bi)) {
-                        best = ob;
-                        bi = oi;
-                    }
-                }
-                if (threadIdx.x == 0) piv_s = bi;
-            }
-            __syncthreads();
-            const int p = piv_s;
-            if (p != c)
-                for (int col = threadIdx.x; col < n; col += ET) {
-                    double t0 = Q[c * ld + col];
-                    Q[c * ld + col] = Q[p * ld + col];
-                    Q[p * ld + col] = t0;
-                    t0 = F[c * ld + col];
-                    F[c * ld + col] = F[p * ld + col];
-                    F[p * ld + col] = t0;
-                }
-            __syncthreads();
-            for (int i = c + 1 + threadIdx.x; i < n; i += ET) fac[i] = Q[i * ld + c] / Q[c * ld + c];
-            __syncthreads();
-            const int rows = n - c - 1;
-            for (int e = threadIdx.x; e < rows * n; e += ET) {
-                const int i = c + 1 + e / n, col = e % n;
-                const double f = fac[i];
-                F[i * ld + col] -= f * F[c * ld + col];
-                if (col > c) Q[i * ld + col] -= f * Q[c * ld + col];
-            }
-            __syncthreads();
-        }
-        for (int i = n - 1; i >= 0; --i) {
-            for (int col = threadIdx.x; col < n; col += ET) {
-                double t0 = F[i * ld + col];
-                for (int l = i + 1; l < n; ++l) t0 -= Q[i * ld + l] * F[l * ld + col];
-                F[i * ld + col] = t0 / Q[i * ld + i];
-            }
-            __syncthreads();
-        }
-        // square s times
-        double* X = F;
-        double* Y = B3;
-        for (int r = 0; r < s; ++r) {
-            mm(X, X, Y, n, ld);
-            __syncthreads();
-            double* t0 = X;
-            X = Y;
-            Y = t0;
-        }
+        const double* X = pade13(a.H + (int64_t)d * (k + 1) * k, k, n, (double)j * a.step, sm, fac, piv_s, sq_s);
         for (int i = threadIdx.x; i < n; i += ET) xs[i] = X[i * ld + 0];
     }
     __syncthreads();
@@ -235,6 +244,69 @@ __global__ void __launch_bounds__(ET) expm_project_kernel(ExpmArgs a) {
         a.coeff[(j * a.n_out + r) * a.ndl_stride + d] = bz * s;
     }
     if (threadIdx.x == 0) a.hlast[(int64_t)d * (a.n_steps + 1) + j] = xs[n - 1];
+}
+
+// The uniform time grid by doubling (one CTA per direction): E = e^{H delta} by the same Pade-13 scaling and
+// squaring, then x_0 = e_1 and x_{2^q + j} = E^{2^q} x_j for j < 2^q (one small matrix-matrix product per
+// level), E^{2^{q+1}} = (E^{2^q})^2 — log2(N) levels instead of N independent Pade-13 exponentials
+// (C2: 42021 of them). x_j kept column-wise in global memory X [n][ldx] (L2-resident); then the projection
+// c[j][r][d] = ||v_d|| (P x_j)_r and h(t_j) = x_j[n-1] for Lemma 1.
+__global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* xt, int ldx) {
+    const int d = blockIdx.x;
+    const int n = a.keff[d];
+    const int k = a.k;
+    const int64_t np1 = a.n_steps + 1;
+    extern __shared__ double sm[];
+    __shared__ double fac[64];
+    __shared__ int piv_s;
+    __shared__ int sq_s;
+    if (n <= 0) {
+        for (int64_t e = threadIdx.x; e < np1 * a.n_out; e += ET)
+            a.coeff[((e / a.n_out) * a.n_out + e % a.n_out) * a.ndl_stride + d] = 0.0;
+        return;
+    }
+    const int ld = n + 1;
+    double* X = xt + (int64_t)d * 64 * ldx;  // [n][ldx]
+    for (int l = threadIdx.x; l < n; l += ET) X[(int64_t)l * ldx] = l == 0 ? 1.0 : 0.0;  // x_0 = e_1 exactly
+    double* E = np1 > 1 ? pade13(a.H + (int64_t)d * (k + 1) * k, k, n, a.step, sm, fac, piv_s, sq_s) : sm;
+    // E lives in one of the six buffers; use two others (disjoint from it) for the powers
+    const int msz = n * ld;
+    const int ei = (int)((E - sm) / msz);
+    double* Pw = sm + (size_t)((ei + 1) % 6) * msz;
+    double* Tw = sm + (size_t)((ei + 2) % 6) * msz;
+    for (int e = threadIdx.x; e < n * n; e += ET) {
+        const int o = (e / n) * ld + e % n;
+        Pw[o] = E[o];
+    }
+    __syncthreads();
+    for (int64_t w0 = 1; w0 < np1; w0 <<= 1) {
+        const int64_t w = min(w0, np1 - w0);
+        for (int64_t e = threadIdx.x; e < (int64_t)n * w; e += ET) {
+            const int i = (int)(e / w);
+            const int64_t c = e - (int64_t)i * w;
+            double s = 0.0;
+            for (int l = 0; l < n; ++l) s = fma(Pw[i * ld + l], X[(int64_t)l * ldx + c], s);
+            X[(int64_t)i * ldx + w0 + c] = s;
+        }
+        __syncthreads();
+        if (2 * w0 < np1) {
+            mm(Pw, Pw, Tw, n, ld);
+            __syncthreads();
+            double* t0 = Pw;
+            Pw = Tw;
+            Tw = t0;
+        }
+    }
+    const double* Pd = a.P + (int64_t)d * a.n_out * k;
+    const double bz = a.beta0[d];
+    for (int64_t j = threadIdx.x; j < np1; j += ET) {
+        for (int r = 0; r < a.n_out; ++r) {
+            double s = 0.0;
+            for (int l = 0; l < n; ++l) s = fma(Pd[(int64_t)r * k + l], X[(int64_t)l * ldx + j], s);
+            a.coeff[(j * a.n_out + r) * a.ndl_stride + d] = bz * s;
+        }
+        a.hlast[(int64_t)d * np1 + j] = X[(int64_t)(n - 1) * ldx + j];
+    }
 }
 
 __global__ void lemma_kernel(const double* hlast, const double* beta0, const double* hnext, const int32_t* keff,
@@ -257,6 +329,15 @@ __global__ void lemma_kernel(const double* hlast, const double* beta0, const dou
 void kr_expm_prepare(kr_handle* h) {
     const size_t smem = (size_t)6 * h->k * (h->k + 1) * sizeof(double);
     KR_CUDA(cudaFuncSetAttribute(expm_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    KR_CUDA(cudaFuncSetAttribute(expm_doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    h->expm_doubling = getenv("KR_EXPM_PADE") == nullptr;  // KR_EXPM_PADE=1: one Pade-13 per (step, direction)
+    if (h->expm_doubling) {
+        int ldx = 1;
+        while (ldx < h->n_steps + 1) ldx <<= 1;
+        h->xt_ld = ldx;
+        KR_CUDA(cudaMalloc(&h->d_xt, (size_t)std::max<size_t>(1, h->my_dirs.size()) * 64 * ldx * sizeof(double)));
+        h->extra_allocs.push_back(h->d_xt);
+    }
 }
 
 void kr_expm_enqueue(kr_handle* h) {
@@ -276,7 +357,10 @@ void kr_expm_enqueue(kr_handle* h) {
     a.step = h->step;
     a.coeff = h->d_coeff_loc;
     a.hlast = h->d_hlast;
-    expm_project_kernel<<<dim3((unsigned)(h->n_steps + 1), ndl), ET, smem, h->stream>>>(a);
+    if (h->expm_doubling)
+        expm_doubling_kernel<<<ndl, ET, smem, h->stream>>>(a, h->d_xt, h->xt_ld);
+    else
+        expm_project_kernel<<<dim3((unsigned)(h->n_steps + 1), ndl), ET, smem, h->stream>>>(a);
     KR_CUDA(cudaGetLastError());
     h->launches++;
     lemma_kernel<<<(ndl + 63) / 64, 64, 0, h->stream>>>(h->d_hlast, h->d_beta0, h->d_hnext, h->d_keff, h->n_steps,

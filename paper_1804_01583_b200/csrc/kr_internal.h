@@ -198,6 +198,9 @@ struct kr_handle {
     bool p2p = false;            // ... across processes through CUDA IPC peer memory (NVLink)
     void* p2p_base[2] = {nullptr, nullptr};  // opened IPC bases (lower, upper neighbour)
     int32_t p2p_rank = 0, p2p_world = 1;
+    bool expm_doubling = false;  // small-k exponentials: doubling over the time grid (else Pade per step)
+    double* d_xt = nullptr;      // doubling trajectories [ndl][64][xt_ld]
+    int xt_ld = 0;
     bool large_route;      // exponentials through the large-k route (kr_large.cu) instead of per-step Pade
     // large-k route scratch (allocated at the first project that needs it, for kcap = k)
     double* d_big;         // 6 x kcap^2 doubles: X, X^2, X^3, X^4, Y, Y'

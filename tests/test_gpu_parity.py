@@ -230,3 +230,15 @@ def test_errors():
         h.check_box()
     assert "KR_ESTATE" in str(e.value)
     h.close()
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C3"])
+def test_expm_doubling_equals_per_step_pade(cfg, monkeypatch):
+    """The small-k exponentials by doubling over the time grid (default: E = e^{H delta} by Pade-13, then
+    x_{2^q+j} = E^{2^q} x_j) agree with one Pade-13 per (step, direction) (KR_EXPM_PADE=1) and the oracle."""
+    p = W.CONFIGS[cfg]()
+    a, _, _, _ = gpu_run(p)
+    monkeypatch.setenv("KR_EXPM_PADE", "1")
+    b, _, _, _ = gpu_run(p)
+    assert_coeff(a, b, f"{cfg} doubling vs per-step Pade")
+    assert_coeff(a, oracle.krylov_project(p)["coeff"], f"{cfg} doubling vs oracle")
