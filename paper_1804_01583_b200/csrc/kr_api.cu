@@ -894,7 +894,11 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 const DVec bv = make_dvec(h, *p->b_vec);
                 kr_fill_dense(h->stream, h->d_bl, h->n, h->n, h->mx, h->my, true, bv, 0, 1.0, 0, &dummy);
             }
-            h->use_cgs = h->N > KR_ORTHO_ONE_CTA_MAX || (getenv("KR_FORCE_CGS") && h->method == KR_ARNOLDI);
+            // CGS2 across the GPU beyond one CTA's reach, and already from 4096 states for Arnoldi, where one
+            // CTA per direction serialises j block-wide reductions per step (C2: 8.1 -> 6.1 ms); small systems
+            // (C1, the oscillator) keep the one-CTA MGS of Alg. 1. KR_FORCE_CGS=0/1 overrides.
+            h->use_cgs = h->N > KR_ORTHO_ONE_CTA_MAX || (h->method == KR_ARNOLDI && h->N >= 4096);
+            if (const char* e = getenv("KR_FORCE_CGS")) h->use_cgs = h->N > KR_ORTHO_ONE_CTA_MAX || (atoi(e) != 0 && h->method == KR_ARNOLDI);
             if (h->use_cgs) h->d_cgs = reinterpret_cast<double*>(dalloc(h, kr_cgs_scratch_doubles(h, ndl) * 8));
             KR_CUDA(cudaStreamSynchronize(h->stream));
             // bytes per batched operator launch: A once + X and Y per direction (context only)

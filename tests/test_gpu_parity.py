@@ -86,8 +86,11 @@ def test_config2_csr_affine_sampled_full_size():
         assert np.all(np.abs(got - ref) <= tol), (d, np.max(np.abs(got - ref) / tol))
 
 
-def test_config2_small_full_parity():
-    """Config-2 recipe at n=2000, 5 generators, 300 steps: every output, bound and verdict."""
+@pytest.mark.parametrize("cgs", ["0", "1"])
+def test_config2_small_full_parity(cgs, monkeypatch):
+    """Config-2 recipe at n=2000, 5 generators, 300 steps: every output, bound and verdict — with the one-CTA
+    MGS of Alg. 1 and with the multi-CTA CGS2 orthogonalisation."""
+    monkeypatch.setenv("KR_FORCE_CGS", cgs)
     p = W.config2(n=2000, n_gen=5, n_steps=300, k=30)
     res = oracle.krylov_project(p)
     th = float(np.median(res["coeff"][:, 0, :].sum(axis=1)))
