@@ -175,11 +175,15 @@ kr_status krylov_workspace_bytes(const kr_problem* p, size_t* bytes);
 kr_status krylov_reach_create(const kr_problem* p, kr_handle** out);
 
 /* Run the hot path: start vectors, k Krylov steps per direction (fused stencil Lanczos in one HBM pass
- * per step, or batched SpMM + Gram-Schmidt Arnoldi), batched k x k Pade exponentials for every t_j
- * (Eq. 2) and the projection through P = C V_k (Alg. 4).
+ * per step, or batched SpMM + Gram-Schmidt Arnoldi: one-CTA MGS below 4096 states, multi-CTA CGS2 above),
+ * the k x k exponentials x_j = e^{H t_j} e_1 for every t_j (Eq. 2; "squaring and scaling and Pade",
+ * e^{H delta} by Pade-13 scaling and squaring, then the uniform grid by doubling,
+ * x_{2^q+j} = e^{H 2^q delta} x_j; for k > 64 or eps > 0 the large-k route with fp64 tensor-core GEMMs and,
+ * with eps > 0, the Alg. 2/4 checkpoints) and the projection through P = C V_k (Alg. 4).
  * coeff: HOST [(n_steps+1)][n_out][n_dir] basis-matrix entries c[j][r][d] ~= C_r e^{A t_j} v_d (same
- * layout in transpose mode). stats: HOST [n_sim] (krylov_sim_info) or NULL. Either output may be NULL to leave the results on the device only
- * (then krylov_check_box still works). Synchronises the stream before returning. */
+ * layout in transpose mode). stats: HOST [n_sim] (krylov_sim_info) or NULL. Either output may be NULL to
+ * leave the results on the device only (then krylov_check_box still works). Synchronises the stream
+ * before returning. */
 kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats);
 
 /* Per-step safety check over the box initial set (the exact LP optimum of Fig. 2(c) for a box and one
