@@ -128,7 +128,8 @@ constexpr size_t step_smem_bytes() {
 
 // BCM: 0 = Dirichlet everywhere (zero ghosts from the TMA fill); 1 = general faces, but this tile has no
 // x/y face cell (only the uniform per-plane z-face terms and the ring cells' own corrections apply);
-// 2 = general faces on a tile that touches an x or y face (per-cell terms).
+// 2 = general faces on a tile that touches a y face (per-cell terms); 3 = general faces on a tile that
+// touches an x face only (per-thread x terms, no per-slot y terms).
 template <int TX, int TY, int S, bool INIT, bool FULL, int BCM, bool HALO>
 __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
                                          unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
@@ -181,12 +182,12 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         bm[m] = bb;
     }
     // ghost-edge coefficients of the low faces (Dirichlet: c_a): x == 0, y == 0 (only slot 0 can have y == 0)
-    constexpr bool BC = BCM > 0, BCXY = BCM == 2;
+    constexpr bool BC = BCM > 0, BCX = BCM == 2 || BCM == 3, BCY = BCM == 2;
     const double gex = gx == 0 ? (BC ? a.gq[0] : cx) : 0.0;
     const double gey0 = (y0 + ty == 0) ? (BC ? a.gq[2] : cy) : 0.0;
     // general boundaries: diagonal corrections of face cells and the high-face edge coefficients
-    const double ex = BCXY ? ((gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0)) : 0.0;
-    const double kx = (BCXY && gx == a.mx - 1) ? a.gq[1] : cx;
+    const double ex = BCX ? ((gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0)) : 0.0;
+    const double kx = (BCX && gx == a.mx - 1) ? a.gq[1] : cx;
     double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)(y0 + ty) * a.pitch + gx;
     const int64_t rowstep = (int64_t)RS * a.pitch;
 
@@ -255,7 +256,7 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 const double sy = Cq[o - G::CW] + Cq[o + G::CW];
                 const double sz = up[m] + un;
                 double dg = dgz;
-                if (BCXY) {
+                if (BCY) {
                     const int gy = y0 + ty + m * RS;
                     dg -= (gy == 0 ? a.ecor[2] : 0.0) + (gy == a.my - 1 ? a.ecor[3] : 0.0);
                 }
@@ -307,7 +308,7 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 const double dz = wc[m] - w0;
                 const double w2 = w0 * w0;
                 const double g = gex + gz + (m == 0 ? gey0 : 0.0);
-                const double ky = (BCXY && y0 + ty + m * RS == a.my - 1) ? a.gq[3] : cy;
+                const double ky = (BCY && y0 + ty + m * RS == a.my - 1) ? a.gq[3] : cy;
                 acc_d = fma(kx, dx * dx, fma(ky, dy * dy, fma(kz, dz * dz, fma(g, w2, acc_d))));
                 acc_ww += w2;
                 acc_sum += w0;
@@ -388,11 +389,16 @@ __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(c
                 cta_box = true;
         // interior tiles (the forward ring inside the grid) skip all x/y masking
         constexpr int BCE = BC ? 2 : 0;
+        const bool yin = y0 > 0 && y0 + TY < a.my - 1;  // no y face cell (y = 0 or my - 1) in the tile
         if (x0 + TX < a.mx && y0 + TY < a.my) {
             if (BC && x0 > 0 && y0 > 0)  // no x/y face cell in the tile: only per-plane z-face terms
                 lz_march<TX, TY, S, INIT, true, 1, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+            else if (BC && yin)  // x face only
+                lz_march<TX, TY, S, INIT, true, 3, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
             else
                 lz_march<TX, TY, S, INIT, true, BCE, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
+        } else if (BC && yin) {
+            lz_march<TX, TY, S, INIT, false, 3, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
         } else {
             lz_march<TX, TY, S, INIT, false, BCE, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
         }
