@@ -73,16 +73,57 @@ bool vec_is_zero(const kr_problem* p, const kr_vec& v) {
     return false;
 }
 
-bool csr_exactly_symmetric(const kr_problem* p) {
-    std::map<std::pair<int64_t, int64_t>, double> m;
-    for (int64_t r = 0; r < p->n; ++r)
-        for (int64_t e = p->row_ptr[r]; e < p->row_ptr[r + 1]; ++e) m[{r, p->col_idx[e]}] += p->val[e];
-    for (auto& kv : m) {
-        auto it = m.find({kv.first.second, kv.first.first});
-        const double o = it == m.end() ? 0.0 : it->second;
-        if (o != kv.second) return false;
+// CSR rows with ascending columns and duplicates summed (host, O(nnz log row length)), and its transpose
+// by a counting sort (rows of A^T then also have ascending columns).
+struct RowsCsr {
+    std::vector<int64_t> rp, ci;
+    std::vector<double> v;
+};
+
+RowsCsr merged_rows(const kr_problem* p) {
+    RowsCsr m;
+    m.rp.assign((size_t)p->n + 1, 0);
+    m.ci.reserve((size_t)p->nnz);
+    m.v.reserve((size_t)p->nnz);
+    std::vector<std::pair<int64_t, double>> row;
+    for (int64_t r = 0; r < p->n; ++r) {
+        row.clear();
+        for (int64_t e = p->row_ptr[r]; e < p->row_ptr[r + 1]; ++e) row.push_back({p->col_idx[e], p->val[e]});
+        std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (size_t i = 0; i < row.size();) {
+            size_t j = i;
+            double acc = 0.0;
+            while (j < row.size() && row[j].first == row[i].first) acc += row[j++].second;
+            m.ci.push_back(row[i].first);
+            m.v.push_back(acc);
+            i = j;
+        }
+        m.rp[(size_t)r + 1] = (int64_t)m.ci.size();
     }
-    return true;
+    return m;
+}
+
+RowsCsr transpose_rows(const RowsCsr& a, int64_t n) {
+    RowsCsr t;
+    t.rp.assign((size_t)n + 1, 0);
+    for (int64_t c : a.ci) t.rp[(size_t)c + 1]++;
+    for (int64_t r = 0; r < n; ++r) t.rp[(size_t)r + 1] += t.rp[(size_t)r];
+    t.ci.resize(a.ci.size());
+    t.v.resize(a.v.size());
+    std::vector<int64_t> next(t.rp.begin(), t.rp.end() - 1);
+    for (int64_t r = 0; r < n; ++r)
+        for (int64_t e = a.rp[(size_t)r]; e < a.rp[(size_t)r + 1]; ++e) {
+            const int64_t pos = next[(size_t)a.ci[(size_t)e]]++;
+            t.ci[(size_t)pos] = r;
+            t.v[(size_t)pos] = a.v[(size_t)e];
+        }
+    return t;
+}
+
+bool csr_exactly_symmetric(const kr_problem* p) {
+    const RowsCsr a = merged_rows(p);
+    const RowsCsr t = transpose_rows(a, p->n);
+    return a.rp == t.rp && a.ci == t.ci && a.v == t.v;
 }
 
 // Gershgorin upper bound of lambda_max((A+A^T)/2) (Lemma 1's nu(B) = -mu(A), B = -A).
@@ -117,31 +158,27 @@ double gershgorin_mu(const kr_problem* p) {
         return mu;
     }
     const int64_t n = p->n, N = n + (p->b ? 1 : 0);
+    const RowsCsr a = merged_rows(p);
+    const RowsCsr t = transpose_rows(a, n);
     std::vector<double> diag(N, 0.0), rad(N, 0.0);
-    std::vector<std::pair<std::pair<int64_t, int64_t>, double>> off;
-    off.reserve((size_t)p->nnz * 2 + (p->b ? 2 * n : 0));
-    for (int64_t r = 0; r < n; ++r) {
-        for (int64_t e = p->row_ptr[r]; e < p->row_ptr[r + 1]; ++e) {
-            const int64_t c = p->col_idx[e];
+    for (int64_t r = 0; r < n; ++r) {  // merge row r of A and of A^T: s_rc = (a_rc + a_cr) / 2
+        int64_t i = a.rp[(size_t)r], j = t.rp[(size_t)r];
+        const int64_t i1 = a.rp[(size_t)r + 1], j1 = t.rp[(size_t)r + 1];
+        while (i < i1 || j < j1) {
+            const int64_t ca = i < i1 ? a.ci[(size_t)i] : INT64_MAX, ct = j < j1 ? t.ci[(size_t)j] : INT64_MAX;
+            const int64_t c = std::min(ca, ct);
+            double sv = 0.0;
+            if (ca == c) sv += 0.5 * a.v[(size_t)i++];
+            if (ct == c) sv += 0.5 * t.v[(size_t)j++];
             if (c == r)
-                diag[r] += p->val[e];
-            else {
-                off.push_back({{r, c}, 0.5 * p->val[e]});
-                off.push_back({{c, r}, 0.5 * p->val[e]});
-            }
+                diag[(size_t)r] += sv;
+            else
+                rad[(size_t)r] += std::fabs(sv);
         }
-        if (p->b && p->b[r] != 0.0) {
-            off.push_back({{r, n}, 0.5 * p->b[r]});
-            off.push_back({{n, r}, 0.5 * p->b[r]});
+        if (p->b && p->b[r] != 0.0) {  // lifted column b and (zero) lifted row: s_{r,n} = s_{n,r} = b_r / 2
+            rad[(size_t)r] += std::fabs(0.5 * p->b[r]);
+            rad[(size_t)n] += std::fabs(0.5 * p->b[r]);
         }
-    }
-    std::sort(off.begin(), off.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    for (size_t i = 0; i < off.size();) {
-        size_t j = i;
-        double s = 0.0;
-        while (j < off.size() && off[j].first == off[i].first) s += off[j++].second;
-        rad[off[i].first.first] += std::fabs(s);
-        i = j;
     }
     double mu = -INFINITY;
     for (int64_t r = 0; r < N; ++r) mu = std::max(mu, diag[r] + rad[r]);

@@ -62,6 +62,11 @@ struct ExpmArgs {
     double step;
     double* coeff;       // [(n_steps+1)][n_out][ndl_stride]
     double* hlast;       // [ndl][n_steps+1]
+    // single-direction use by the large-k route's small checkpoints (expm_doubling_kernel only)
+    int dsel = -1;               // >= 0: one CTA, for this local direction
+    int nfix = 0;                // > 0: dimension (instead of keff)
+    const double* Hsrc = nullptr;  // non-NULL: H from here, row stride hstride
+    int hstride = 0;
 };
 
 // e^{H t} of the leading n x n block of H (row stride k) by scaling and squaring with the degree-13 diagonal
@@ -252,8 +257,8 @@ __global__ void __launch_bounds__(ET) expm_project_kernel(ExpmArgs a) {
 // (C2: 42021 of them). x_j kept column-wise in global memory X [n][ldx] (L2-resident); then the projection
 // c[j][r][d] = ||v_d|| (P x_j)_r and h(t_j) = x_j[n-1] for Lemma 1.
 __global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* xt, int ldx) {
-    const int d = blockIdx.x;
-    const int n = a.keff[d];
+    const int d = a.dsel >= 0 ? a.dsel : blockIdx.x;
+    const int n = a.nfix > 0 ? a.nfix : a.keff[d];
     const int k = a.k;
     const int64_t np1 = a.n_steps + 1;
     extern __shared__ double sm[];
@@ -266,9 +271,10 @@ __global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* x
         return;
     }
     const int ld = n + 1;
-    double* X = xt + (int64_t)d * 64 * ldx;  // [n][ldx]
+    double* X = xt + (a.dsel >= 0 ? 0 : (int64_t)d * 64 * ldx);  // [n][ldx]
     for (int l = threadIdx.x; l < n; l += ET) X[(int64_t)l * ldx] = l == 0 ? 1.0 : 0.0;  // x_0 = e_1 exactly
-    double* E = np1 > 1 ? pade13(a.H + (int64_t)d * (k + 1) * k, k, n, a.step, sm, fac, piv_s, sq_s) : sm;
+    const double* Hd = a.Hsrc ? a.Hsrc : a.H + (int64_t)d * (k + 1) * k;
+    double* E = np1 > 1 ? pade13(Hd, a.Hsrc ? a.hstride : k, n, a.step, sm, fac, piv_s, sq_s) : sm;
     // E lives in one of the six buffers; use two others (disjoint from it) for the powers
     const int msz = n * ld;
     const int ei = (int)((E - sm) / msz);
@@ -338,6 +344,38 @@ void kr_expm_prepare(kr_handle* h) {
         KR_CUDA(cudaMalloc(&h->d_xt, (size_t)std::max<size_t>(1, h->my_dirs.size()) * 64 * ldx * sizeof(double)));
         h->extra_allocs.push_back(h->d_xt);
     }
+}
+
+// One direction at dimension kc <= 64 through the doubling kernel (the large-k route's small checkpoints):
+// Hdense [kc][kc] on the device, trajectory scratch xt [64][ldx]; writes the coefficients of local
+// direction dl and hlast. One launch.
+void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, double* xt, int ldx) {
+    static bool attr = false;
+    const size_t smem = (size_t)6 * 64 * 65 * sizeof(double);
+    if (!attr) {
+        KR_CUDA(cudaFuncSetAttribute(expm_doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int ndl = (int)h->my_dirs.size();
+    ExpmArgs a;
+    a.H = nullptr;
+    a.P = h->d_P;
+    a.beta0 = h->d_beta0;
+    a.keff = h->d_keff;
+    a.k = h->k;
+    a.n_out = h->n_out;
+    a.ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
+    a.n_steps = h->n_steps;
+    a.step = h->step;
+    a.coeff = h->d_coeff_loc;
+    a.hlast = h->d_hlast;
+    a.dsel = dl;
+    a.nfix = kc;
+    a.Hsrc = Hdense;
+    a.hstride = kc;
+    expm_doubling_kernel<<<1, ET, (size_t)6 * kc * (kc + 1) * sizeof(double), h->stream>>>(a, xt, ldx);
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
 }
 
 void kr_expm_enqueue(kr_handle* h) {

@@ -190,6 +190,14 @@ __global__ void large_build_kernel(const LzScalars* sc, int kc, int kp, double f
     }
 }
 
+// the leading kc x kc tridiagonal as a dense matrix (row stride kc), for the one-CTA small-checkpoint path
+__global__ void tri_dense_kernel(const LzScalars* sc, int kc, double* H) {
+    for (int e = threadIdx.x; e < kc * kc; e += blockDim.x) {
+        const int i = e / kc, j = e - i * kc;
+        H[e] = i == j ? sc->alpha[i + 1] : (j == i + 1 ? sc->beta[i + 1] : (i == j + 1 ? sc->beta[j + 1] : 0.0));
+    }
+}
+
 // Dense (Arnoldi, upper Hessenberg) H: ||H delta||_1 over the leading kc x kc block (row stride ks).
 __global__ void large_norm_dense_kernel(const double* H, int ks, int kc, double delta, double* out) {
     __shared__ double red[256];
@@ -385,6 +393,18 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     const double* hn_src = tri ? h->d_lzarr + (size_t)dl * 3 * (h->k + 2) + (h->k + 2) + kc
                                : Hd + (size_t)kc * h->k + (kc - 1);
     cudaStream_t st = h->stream;
+    const int ndl = (int)h->my_dirs.size();
+    const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
+    double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
+    const int64_t np1 = h->n_steps + 1;
+    if (tri && kc <= 64 && !getenv("KR_LARGE_ONLY")) {
+        // small checkpoint: one CTA (Pade-13 scaling and squaring + doubling over the time grid, in shared
+        // memory) instead of the ~50 launches of the GEMM route
+        tri_dense_kernel<<<1, 256, 0, st>>>(sc, kc, h->d_big);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        kr_expm_small_eval(h, dl, kc, h->d_big, h->d_traj, pow2_at_least(np1));
+    } else {
     // scaling: ||H delta||_1 -> s with ||H delta||_1 / 2^s <= 1
     if (tri)
         large_norm_kernel<<<1, 256, 0, st>>>(sc, kc, h->step, h->d_scratch);
@@ -427,10 +447,6 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
         bwY = std::min(2 * bwY, bmax);
         std::swap(Y, Z);
     }
-    const int ndl = (int)h->my_dirs.size();
-    const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
-    double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
-    const int64_t np1 = h->n_steps + 1;
     int kdouble = 6000;  // doubling (GEMM-batched) time march up to this kc, the sequential march above
     if (const char* e = getenv("KR_KDOUBLE")) kdouble = atoi(e);
     if (kc <= kdouble) {
@@ -478,6 +494,7 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
         KR_CUDA(cudaGetLastError());
         h->launches++;
     }
+    }  // GEMM route
     large_bound_kernel<<<1, 256, 0, st>>>(hl, h->n_steps, h->step, h->mu, hn_src, kc, zero_bound ? 1 : 0, h->d_scratch + 1,
                                           fin ? 1 : 0, h->d_beta0 + dl, h->d_lemma + dl, h->d_hnext + dl,
                                           h->d_keff + dl);
