@@ -295,16 +295,48 @@ def lanczos_adaptive(p, v, eps, k_max):
     return r
 
 
+def arnoldi_adaptive(p, v, eps, k_max):
+    """Alg. 2: Arnoldi (Alg. 1, MGS) with the error checked at the checkpoints k = 4, ceil(1.1 k),
+    ... (fp64) by Lemma 1 for the unit start vector; x(t_j) = e^{H_k t_j} e_1 by the oracle's
+    per-step Pade. As in lanczos_adaptive, one Arnoldi run to k_max is cut at the accepted
+    checkpoint (its first k columns do not depend on later steps)."""
+    full = arnoldi(p, v, k_max)
+    mu = gershgorin_mu(p)
+    Hf = full["Hfull"]
+    checks = []
+    kk = full["k_eff"]
+    for k in checkpoints(kk):
+        if k == kk and kk < k_max:  # exact breakdown before k_max
+            break
+        X = expm_e1_times(Hf[:k, :k], p["step"], p["n_steps"])
+        b = lemma1_bound(Hf[k, k - 1], X, p["step"], mu)
+        checks.append((k, b))
+        if b < eps:
+            kk = k
+            break
+    else:
+        if kk == k_max and (not checks or checks[-1][1] >= eps):
+            raise RuntimeError("adaptive Krylov: k_max reached before the error target")
+    return {"H": Hf[:kk, :kk].copy(), "P": full["P"][:, :kk], "beta0": full["beta0"], "k_eff": kk,
+            "h_next": Hf[kk, kk - 1], "checks": checks,
+            "bound": checks[-1][1] if checks and checks[-1][0] == kk else 0.0}
+
+
 def krylov_project_adaptive(p):
-    """Basis-matrix sequence with adaptive k (p['eps'], p['k_max']) for the symmetric stencil path:
-    coeff[j][r][0] = ||v|| (P e^{H t_j} e_1)_r through the eigendecomposition route."""
+    """Basis-matrix sequence with adaptive k (p['eps'], p['k_max']): Lanczos (Alg. 4) through the
+    eigendecomposition route, or Arnoldi (Alg. 2, p['method'] == 'arnoldi') through per-step Pade:
+    coeff[j][r][d] = ||v_d|| (P_d e^{H_d t_j} e_1)_r."""
     dirs = directions(p)
     o, N = len(p["outs"]), p["n_steps"]
     coeff = np.zeros((N + 1, o, len(dirs)))
     per = []
     for d, v in enumerate(dirs):
-        r = lanczos_adaptive(p, v, p["eps"], p["k_max"])
-        X = eig_e1_times(r["alpha"], r["beta"], p["step"], N)
+        if p.get("method") == "arnoldi":
+            r = arnoldi_adaptive(p, v, p["eps"], p["k_max"])
+            X = expm_e1_times(r["H"], p["step"], N)
+        else:
+            r = lanczos_adaptive(p, v, p["eps"], p["k_max"])
+            X = eig_e1_times(r["alpha"], r["beta"], p["step"], N)
         coeff[:, :, d] = r["beta0"] * (X @ r["P"].T)
         r["X"] = X
         per.append(r)

@@ -295,7 +295,8 @@ void validate(const kr_problem* p) {
             KR_THROW(KR_EINVAL, "k must be 1.." + std::to_string(kmax) + (stencil_lz ? "" : " (Arnoldi / CSR)"));
         if (!(p->eps >= 0.0) || !finite(p->eps)) KR_THROW(KR_EINVAL, "eps must be >= 0");
         if (p->sim_dir < KR_SIM_FORWARD || p->sim_dir > KR_SIM_AUTO) KR_THROW(KR_EINVAL, "bad sim_dir");
-        if (p->eps > 0.0 && !stencil_lz) KR_THROW(KR_EINVAL, "adaptive k (eps > 0) needs the stencil Lanczos path");
+        if (p->eps > 0.0 && p->method == KR_LANCZOS && p->op != KR_OP_STENCIL7)
+            KR_THROW(KR_EINVAL, "adaptive k (eps > 0): stencil Lanczos (Alg. 4) or Arnoldi (Alg. 2)");
         for (int f = 0; f < 6; ++f) {
             if (p->bc[f] < KR_BC_DIRICHLET || p->bc[f] > KR_BC_ROBIN) KR_THROW(KR_EINVAL, "bad boundary condition");
             if (p->bc[f] != KR_BC_DIRICHLET && p->op != KR_OP_STENCIL7)
@@ -741,7 +742,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         }
         const int k = h->k;
         const int64_t np1 = h->n_steps + 1;
-        h->large_route = (h->path == PATH_FUSED_LANCZOS && h->eps > 0.0) || k > KR_K_MAX_FIXED_PADE;
+        h->large_route = h->eps > 0.0 || k > KR_K_MAX_FIXED_PADE;
         h->checks.assign(ndl, {});
         h->d_scratch = reinterpret_cast<double*>(dalloc(h, 64));
         if (!h->large_route || h->path == PATH_GENERIC) {  // dense H: per-step Pade, or Arnoldi's Hessenberg
@@ -1022,6 +1023,57 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             h->large_ms = 0.0;
             h->large_evals = 0;
             KR_CUDA(cudaEventRecord(h->ev_it0, h->stream));
+            if (h->path == PATH_GENERIC && h->eps > 0.0) {
+                // Alg. 2: all local directions step together (one SpMM per step); each direction is
+                // checked at the checkpoints 4, ceil(1.1 k), ... until its Lemma-1 bound is below eps, then
+                // stopped (its first kc basis vectors and H entries are final)
+                kr_ge_enqueue_init(h);
+                std::vector<int> acc(ndl, -1);
+                std::vector<int32_t> ke(ndl), dn(ndl), stv(ndl);
+                int j = 0, left = ndl;
+                auto readback = [&]() {
+                    KR_CUDA(cudaMemcpyAsync(ke.data(), h->d_keff, ndl * 4, cudaMemcpyDeviceToHost, h->stream));
+                    KR_CUDA(cudaMemcpyAsync(dn.data(), h->d_done, ndl * 4, cudaMemcpyDeviceToHost, h->stream));
+                    KR_CUDA(cudaMemcpyAsync(stv.data(), h->d_status, ndl * 4, cudaMemcpyDeviceToHost, h->stream));
+                    KR_CUDA(cudaStreamSynchronize(h->stream));
+                };
+                const int32_t one = 1;
+                for (int kc = 4; kc <= h->k && left > 0; kc = (int)std::ceil(1.1 * (double)kc)) {
+                    while (j < kc) kr_ge_enqueue_step(h, ++j);
+                    readback();
+                    for (int dl = 0; dl < ndl; ++dl) {
+                        if (acc[dl] >= 0 || stv[dl]) continue;
+                        if (dn[dl] && ke[dl] < h->k) {  // exact breakdown: accepted, bound 0
+                            kr_large_eval(h, dl, std::max(1, (int)ke[dl]), true, true);
+                            acc[dl] = ke[dl];
+                            --left;
+                            continue;
+                        }
+                        const double b = kr_large_eval(h, dl, kc, true, false);
+                        h->checks[dl].push_back({kc, b});
+                        if (b < h->eps) {
+                            acc[dl] = kc;
+                            --left;
+                            KR_CUDA(cudaMemcpyAsync(h->d_done + dl, &one, 4, cudaMemcpyHostToDevice, h->stream));
+                        }
+                    }
+                }
+                if (left > 0) {  // k_max reached for some directions
+                    while (j < h->k) kr_ge_enqueue_step(h, ++j);
+                    readback();
+                    for (int dl = 0; dl < ndl; ++dl) {
+                        if (acc[dl] >= 0 || stv[dl]) continue;
+                        const bool brk = dn[dl] && ke[dl] < h->k;
+                        const double b = kr_large_eval(h, dl, std::max(1, (int)ke[dl]), true, brk);
+                        if (!brk) h->checks[dl].push_back({ke[dl], b});
+                    }
+                }
+                h->steps_run0 = j;
+                KR_CUDA(cudaEventRecord(h->ev_it1, h->stream));
+                KR_CUDA(cudaStreamSynchronize(h->stream));
+                post();
+                return;
+            }
             if (h->path == PATH_GENERIC) {  // stored-basis Arnoldi with k > 64: all steps, then the exponentials
                 kr_ge_enqueue_direction_set(h);
                 KR_CUDA(cudaEventRecord(h->ev_it1, h->stream));

@@ -349,7 +349,7 @@ void kr_expm_prepare(kr_handle* h) {
 // One direction at dimension kc <= 64 through the doubling kernel (the large-k route's small checkpoints):
 // Hdense [kc][kc] on the device, trajectory scratch xt [64][ldx]; writes the coefficients of local
 // direction dl and hlast. One launch.
-void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, double* xt, int ldx) {
+void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, int hstride, double* xt, int ldx) {
     static bool attr = false;
     const size_t smem = (size_t)6 * 64 * 65 * sizeof(double);
     if (!attr) {
@@ -372,7 +372,7 @@ void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, doub
     a.dsel = dl;
     a.nfix = kc;
     a.Hsrc = Hdense;
-    a.hstride = kc;
+    a.hstride = hstride;
     expm_doubling_kernel<<<1, ET, (size_t)6 * kc * (kc + 1) * sizeof(double), h->stream>>>(a, xt, ldx);
     KR_CUDA(cudaGetLastError());
     h->launches++;

@@ -398,7 +398,8 @@ void kr_ge_prepare() {
     KR_CUDA(cudaFuncSetAttribute(ortho_kernel<27, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 27 * OT * 8));
 }
 
-void kr_ge_enqueue_direction_set(kr_handle* h) {
+// Start of the stored-basis runs of all local directions: reset, v_0 = the start vectors, normalise (j = 0).
+void kr_ge_enqueue_init(kr_handle* h) {
     const int ndl = (int)h->my_dirs.size();
     const int64_t N = h->N;
     const int k = h->k;
@@ -411,6 +412,14 @@ void kr_ge_enqueue_direction_set(kr_handle* h) {
                       h->dirs_h[d], h->dir_lift1[d], 1.0, 0, &h->launches);
     }
     launch_ortho(h, 0, ndl);
+}
+
+// Krylov step j (1-based) of every local direction: w = A v_{j-1} for all directions at once (one SpMM /
+// stencil launch), then the orthogonalisation producing v_j (stopped directions exit at once).
+void kr_ge_enqueue_step(kr_handle* h, int j) {
+    const int ndl = (int)h->my_dirs.size();
+    const int64_t N = h->N;
+    const int k = h->k;
     const int64_t vstride = (int64_t)(k + 1) * N;
     const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
     FaceCor fc{};
@@ -419,27 +428,29 @@ void kr_ge_enqueue_direction_set(kr_handle* h) {
         for (int f = 0; f < 6; ++f)
             fc.e[f] = (h->bc[f] != KR_BC_DIRICHLET ? c[f / 2] : 0.0) - (h->bc[f] == KR_BC_ROBIN ? h->gamma[f] : 0.0);
     }
-    for (int j = 1; j <= k; ++j) {
-        const double* X = h->d_V + (int64_t)(j - 1) * N;
-        const bool evj = h->timing && (size_t)(2 * j) <= h->ev.size();
-        if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1)], h->stream));
-        if (h->op == KR_OP_CSR)
-        {
-            spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X,
-                                                                  vstride, h->d_W, N, ndl, h->d_done);
-            if (h->n_long) {
-                KR_CUDA(cudaGetLastError());
-                h->launches++;
-                spmm_long_rows_kernel<<<dim3((unsigned)h->n_long, ndl), 256, 0, h->stream>>>(
-                    h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, h->d_long, X, vstride, h->d_W, N, h->d_done);
-            }
+    const double* X = h->d_V + (int64_t)(j - 1) * N;
+    const bool evj = h->timing && (size_t)(2 * j) <= h->ev.size();
+    if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1)], h->stream));
+    if (h->op == KR_OP_CSR) {
+        spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X, vstride,
+                                                              h->d_W, N, ndl, h->d_done);
+        if (h->n_long) {
+            KR_CUDA(cudaGetLastError());
+            h->launches++;
+            spmm_long_rows_kernel<<<dim3((unsigned)h->n_long, ndl), 256, 0, h->stream>>>(
+                h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, h->d_long, X, vstride, h->d_W, N, h->d_done);
         }
-        else
-            stencil_apply_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->mx, h->my, h->mz, h->cx, h->cy, h->cz, X,
-                                                                       vstride, h->d_W, N, h->d_done, fc, h->d_bl);
-        KR_CUDA(cudaGetLastError());
-        h->launches++;
-        if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1) + 1], h->stream));
-        launch_ortho(h, j, ndl);
+    } else {
+        stencil_apply_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->mx, h->my, h->mz, h->cx, h->cy, h->cz, X, vstride,
+                                                                   h->d_W, N, h->d_done, fc, h->d_bl);
     }
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1) + 1], h->stream));
+    launch_ortho(h, j, ndl);
+}
+
+void kr_ge_enqueue_direction_set(kr_handle* h) {
+    kr_ge_enqueue_init(h);
+    for (int j = 1; j <= h->k; ++j) kr_ge_enqueue_step(h, j);
 }

@@ -252,12 +252,14 @@ size_t kr_lz_step_smem(int TX, int TY);
 
 // generic
 void kr_ge_enqueue_direction_set(kr_handle* h);
+void kr_ge_enqueue_init(kr_handle* h);
+void kr_ge_enqueue_step(kr_handle* h, int j);
 size_t kr_cgs_scratch_doubles(const kr_handle* h, int ndl);
 void kr_cgs_step(kr_handle* h, int j, int ndl, double* scratch);
 
 // expm + projection + lemma
 void kr_expm_enqueue(kr_handle* h);
-void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, double* xt, int ldx);
+void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, int hstride, double* xt, int ldx);
 // large-k route (kr_large.cu): x_j = e^{H t_j} e_1 for the tridiagonal of local direction dl at dimension
 // kc, the coefficients c[j][.][d] of direction dl and the unit-vector Lemma 1 bound (returned; 0 with
 // zero_bound, an exact breakdown); fin also writes the direction's stats. Synchronises the stream.

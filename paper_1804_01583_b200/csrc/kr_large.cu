@@ -397,13 +397,17 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
     double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
     const int64_t np1 = h->n_steps + 1;
-    if (tri && kc <= 64 && !getenv("KR_LARGE_ONLY")) {
+    if (kc <= 64 && !getenv("KR_LARGE_ONLY")) {
         // small checkpoint: one CTA (Pade-13 scaling and squaring + doubling over the time grid, in shared
         // memory) instead of the ~50 launches of the GEMM route
-        tri_dense_kernel<<<1, 256, 0, st>>>(sc, kc, h->d_big);
-        KR_CUDA(cudaGetLastError());
-        h->launches++;
-        kr_expm_small_eval(h, dl, kc, h->d_big, h->d_traj, pow2_at_least(np1));
+        if (tri) {
+            tri_dense_kernel<<<1, 256, 0, st>>>(sc, kc, h->d_big);
+            KR_CUDA(cudaGetLastError());
+            h->launches++;
+            kr_expm_small_eval(h, dl, kc, h->d_big, kc, h->d_traj, pow2_at_least(np1));
+        } else {
+            kr_expm_small_eval(h, dl, kc, Hd, h->k, h->d_traj, pow2_at_least(np1));
+        }
     } else {
     // scaling: ||H delta||_1 -> s with ||H delta||_1 / 2^s <= 1
     if (tri)

@@ -186,3 +186,26 @@ def test_adaptive_zero_horizon():
     coeff, stats, _, checks = gpu(p)
     assert stats[0]["k_eff"] == ref["per_dir"][0]["k_eff"] == 4 and checks == [(4, 0.0)]
     assert_coeff(coeff, ref["coeff"], "adaptive T=0")
+
+
+@pytest.mark.parametrize("route", ["small", "gemm"])
+def test_adaptive_arnoldi_alg2(route, monkeypatch):
+    """Alg. 2 on a nonsymmetric sparse system with a negative-definite symmetric part (Lemma 1's
+    factor is 1): 3 directions stepped together, each accepted at its own checkpoint; same checkpoints,
+    bounds, k and coefficients as the oracle. route: the one-CTA Pade + doubling checkpoint kernel (k <= 64)
+    or the fp64 tensor-core GEMM route (KR_LARGE_ONLY=1) on the dense Hessenberg."""
+    if route == "gemm":
+        monkeypatch.setenv("KR_LARGE_ONLY", "1")
+    p = W.csr_stable_nonsym(n_steps=400, step=0.05, scale=5.0, shift=0.01)
+    ref = oracle.krylov_project_adaptive(p)
+    from paper_1804_01583_b200 import KrylovReach
+    with KrylovReach(p) as h:
+        coeff, stats = h.project()
+        checks = [h.adaptive_checks(d) for d in range(3)]
+    for d in range(3):
+        r = ref["per_dir"][d]
+        assert stats[d]["k_eff"] == r["k_eff"], (d, stats[d]["k_eff"], r["k_eff"])
+        assert [k for k, _ in checks[d]] == [k for k, _ in r["checks"]]
+        for (kg, bg), (ko, bo) in zip(checks[d], r["checks"]):
+            assert abs(bg - bo) <= 1e-8 * abs(bo), (d, kg, bg, bo)
+    assert_coeff(coeff, ref["coeff"], f"adaptive Arnoldi ({route})")

@@ -695,3 +695,26 @@ def test_heater_equals_dense_expm():
             assert np.max(np.abs(res["coeff"][j, :, 0] - C @ x[:64])) <= 1e-10 * scale, j
             assert abs(x[64] - 1.0) < 1e-12
         x = E1 @ x
+
+
+def test_adaptive_arnoldi_sound_against_dense_expm():
+    """Alg. 2 on a nonsymmetric system with mu < 0: the accepted approximation is within its Lemma-1 bound
+    (x ||v||, unit-vector bound) of the exact C e^{At} v (scipy dense expm, n = 400), at every 20th step;
+    the accepted k is the first checkpoint below eps."""
+    p = W.csr_stable_nonsym(n_steps=100, step=0.05, scale=5.0, shift=0.01)
+    assert oracle.gershgorin_mu(p) < 0
+    res = oracle.krylov_project_adaptive(p)
+    A = sp.csr_matrix((p["val"], p["col_idx"], p["row_ptr"]), shape=(400, 400)).toarray()
+    C = np.zeros((2, 400))
+    for r, o in enumerate(p["outs"]):
+        C[r, o["idx"]] = o["val"]
+    dirs = oracle.directions(p)
+    for d, r in enumerate(res["per_dir"]):
+        ks = [k for k, _ in r["checks"]]
+        assert ks == oracle.checkpoints(ks[-1])[:len(ks)] and r["checks"][-1][1] < p["eps"]
+        assert all(b >= p["eps"] for _, b in r["checks"][:-1])
+        for j in range(0, p["n_steps"] + 1, 20):
+            exact = C @ sla.expm(A * (j * p["step"])) @ dirs[d]
+            err = np.abs(res["coeff"][j, :, d] - exact)
+            # ||C (x - x_k)|| <= ||C|| ||x - x_k|| <= ||C||_2 ||v|| bound
+            assert np.max(err) <= np.linalg.norm(C, 2) * r["beta0"] * r["bound"] + 1e-12, (d, j)

@@ -252,6 +252,41 @@ def heat_heater(m, k=64, n_steps=1000, step=0.5):
     }
 
 
+def csr_stable_nonsym(n=400, nnz_per_row=6, seed=7, n_gen=3, eps=1e-6, k_max=200, n_steps=200, step=0.02,
+                      scale=1.0, shift=1.0):
+    """A nonsymmetric sparse system whose symmetric part is negative definite by Gershgorin (diagonal =
+    -(row + column off-diagonal mass)/2 - 1), so Lemma 1's e^{-min(nu, 0) tau} factor is 1 and the adaptive
+    Arnoldi of Alg. 2 can meet eps: random off-diagonals scale * U[-1,1], diagonal
+    -(row + column off-diagonal mass)/2 - shift, no affine term, unit generators in [-1, 1], two Gaussian
+    output rows."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        js = rng.choice(np.delete(np.arange(n), i), size=nnz_per_row, replace=False)
+        for j in js:
+            rows.append(i)
+            cols.append(int(j))
+            vals.append(float(scale * rng.uniform(-1.0, 1.0)))
+    rows, cols, vals = np.array(rows), np.array(cols), np.array(vals)
+    rmass = np.bincount(rows, weights=np.abs(vals), minlength=n)
+    cmass = np.bincount(cols, weights=np.abs(vals), minlength=n)
+    diag = -(rmass + cmass) / 2.0 - shift
+    rows = np.concatenate([rows, np.arange(n)])
+    cols = np.concatenate([cols, np.arange(n)])
+    vals = np.concatenate([vals, diag])
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(row_ptr, rows + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    outs = [sparse(np.arange(n), rng.standard_normal(n)) for _ in range(2)]
+    return {"name": f"csr_stable{n}", "op": "csr", "n": n, "row_ptr": row_ptr, "col_idx": cols.astype(np.int32),
+            "val": vals, "b": None, "gens": [sparse([d * 7], [1.0]) for d in range(n_gen)],
+            "z_lo": -np.ones(n_gen), "z_hi": np.ones(n_gen), "center": None, "outs": outs,
+            "step": float(step), "n_steps": int(n_steps), "k": int(k_max), "method": "arnoldi",
+            "eps": float(eps), "k_max": int(k_max), "thresholds": []}
+
+
 CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5,
            "P100": lambda: heat_paper(100), "P1000": lambda: heat_paper(1000),
            "H10": lambda: heat_heater(10), "H100": lambda: heat_heater(100, k=800),
