@@ -284,6 +284,18 @@ kr_status krylov_p2p_open(kr_handle* h, const void* blobs, int32_t rank, int32_t
 kr_status krylov_p2p_verify(kr_handle* h, int32_t* ok);
 kr_status krylov_p2p_enable(kr_handle* h, int32_t on);
 
+/* ---- host utilities (no GPU work) --------------------------------------------------------------- */
+/* log10 of the a priori Krylov error bound of Eq. 3 for ||v|| = 1: ||At||^k e^{||At||} / k!
+ * (the bound the paper shows to be unusable: 10^16182319 at ||At|| = 32771611, k = 10^6).
+ * norm_At > 0, k >= 1; returns NaN otherwise. */
+double krylov_a_priori_bound_log10(double norm_At, int32_t k);
+
+/* Memory of the Krylov iteration in bytes: method KR_ARNOLDI (or a plain Lanczos storing V), Eq. 4
+ * (P:604-607): k (n + k) doubles; KR_LANCZOS with projection (Alg. 4), Eq. 6:
+ * (3k + n min(i, o) + 3n) doubles. -1 on bad arguments. (The GPU path's own footprint is
+ * krylov_workspace_bytes.) */
+int64_t krylov_memory_bytes(int64_t n, int32_t k, int32_t i, int32_t o, int32_t method);
+
 /* z-slab partition of the stencil grid (host logic, no GPU): rank r of world owns global planes
  * [z0, z1). Balanced: the first mz % world ranks own one extra plane. KR_EINVAL if a rank would own
  * fewer than 2 planes (the depth-2 halo comes from one neighbour). */

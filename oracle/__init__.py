@@ -232,6 +232,21 @@ def _exp_or_inf(x):
     return math.exp(x) if x < 709.0 else math.inf
 
 
+def a_priori_bound_log10(norm_At, k):
+    """log10 of the a priori Krylov error bound of Eq. 3, ||v|| ||At||^k e^{||At||} / k! for
+    ||v|| = 1: k log10 x + x log10 e - log10 k! (lgamma)."""
+    x = float(norm_At)
+    return k * math.log10(x) + x * math.log10(math.e) - math.lgamma(k + 1) / math.log(10.0)
+
+
+def memory_bytes(n, k, i=1, o=1, method="arnoldi"):
+    """Memory of the Krylov iteration in bytes: Eq. 4 k (n + k) doubles for Arnoldi / plain
+    Lanczos; Eq. 6 (3k + n min(i, o) + 3n) doubles for Lanczos with projection (Alg. 4)."""
+    if method == "arnoldi":
+        return k * (n + k) * 8
+    return (3 * k + n * min(i, o) + 3 * n) * 8
+
+
 def checkpoints(k_max):
     """Alg. 2/4 error-check points: k = 4, then k <- ceil(1.1 k) evaluated in
     fp64 (the paper's k = 63, 544, 5932 lie on this sequence, not on the exact-rational one)."""

@@ -62,7 +62,8 @@ EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "k
            "krylov_comm_unique_id", "krylov_comm_create", "krylov_comm_destroy", "krylov_zslab_range",
            "krylov_krylov_data", "krylov_transfer_bytes", "krylov_zslab_halo_plan", "krylov_tridiag",
            "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info", "krylov_check_lp",
-           "krylov_eval_outputs", "krylov_ipc_blob", "krylov_p2p_open", "krylov_p2p_verify", "krylov_p2p_enable"]
+           "krylov_eval_outputs", "krylov_ipc_blob", "krylov_p2p_open", "krylov_p2p_verify", "krylov_p2p_enable",
+           "krylov_a_priori_bound_log10", "krylov_memory_bytes"]
 
 _lib = None
 
@@ -96,6 +97,10 @@ def lib():
     L.krylov_check_lp.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, vp, vp, vp, C.POINTER(kr_cex), vp, vp]
     L.krylov_eval_outputs.argtypes = [vp, C.c_int64, vp, vp]
     L.krylov_ipc_blob.argtypes = [vp, vp]
+    L.krylov_a_priori_bound_log10.argtypes = [C.c_double, C.c_int32]
+    L.krylov_a_priori_bound_log10.restype = C.c_double
+    L.krylov_memory_bytes.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32]
+    L.krylov_memory_bytes.restype = C.c_int64
     L.krylov_p2p_open.argtypes = [vp, vp, C.c_int32, C.c_int32]
     L.krylov_p2p_verify.argtypes = [vp, C.POINTER(C.c_int32)]
     L.krylov_p2p_enable.argtypes = [vp, C.c_int32]
@@ -108,7 +113,8 @@ def lib():
     L.krylov_transfer_bytes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.krylov_zslab_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     for name in EXPORTS:
-        if name not in ("krylov_reach_destroy", "krylov_last_error", "krylov_launch_count", "krylov_comm_destroy"):
+        if name not in ("krylov_reach_destroy", "krylov_last_error", "krylov_launch_count", "krylov_comm_destroy",
+                        "krylov_a_priori_bound_log10", "krylov_memory_bytes"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L

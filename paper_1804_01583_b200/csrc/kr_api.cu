@@ -1452,6 +1452,19 @@ kr_status krylov_p2p_enable(kr_handle* h, int32_t on) {
     });
 }
 
+double krylov_a_priori_bound_log10(double norm_At, int32_t k) {
+    if (!(norm_At > 0.0) || !std::isfinite(norm_At) || k < 1) return NAN;
+    // log10(x^k e^x / k!) = k log10 x + x / ln 10 - lgamma(k + 1) / ln 10
+    const double ln10 = std::log(10.0);
+    return (double)k * std::log10(norm_At) + norm_At / ln10 - std::lgamma((double)k + 1.0) / ln10;
+}
+
+int64_t krylov_memory_bytes(int64_t n, int32_t k, int32_t i, int32_t o, int32_t method) {
+    if (n < 1 || k < 1 || i < 1 || o < 1) return -1;
+    if (method == KR_LANCZOS) return (3 * (int64_t)k + n * (int64_t)std::min(i, o) + 3 * n) * 8;
+    return (int64_t)k * (n + (int64_t)k) * 8;
+}
+
 kr_status krylov_sim_info(const kr_handle* h, int32_t* transposed, int32_t* n_sim) {
     if (!h) return KR_EINVAL;
     if (transposed) *transposed = h->transposed ? 1 : 0;

@@ -168,3 +168,18 @@ def test_adaptive_validation():
     with pytest.raises(KrylovError) as e:
         krylov_workspace_bytes(r, method="lanczos")
     assert "KR_EINVAL" in str(e.value)
+
+
+def test_host_utilities_match_oracle():
+    """Eq. 3 a priori bound and Eq. 4 / Eq. 6 memory (host utilities of the ABI) against the oracle's
+    definitions and the paper's printed values (10^16182319; 46 TB)."""
+    import oracle
+    from paper_1804_01583_b200 import _abi as A
+    L = A.lib()
+    for x, k in [(32771611.0, 10 ** 6), (2.5, 10), (100.0, 40)]:
+        assert abs(L.krylov_a_priori_bound_log10(x, k) - oracle.a_priori_bound_log10(x, k)) <= 1e-9 * abs(
+            oracle.a_priori_bound_log10(x, k)) + 1e-9
+    assert round(L.krylov_a_priori_bound_log10(32771611.0, 10 ** 6)) == 16182319
+    assert L.krylov_memory_bytes(10 ** 9, 5932, 1, 1, A.KR_ARNOLDI) == oracle.memory_bytes(10 ** 9, 5932)
+    assert L.krylov_memory_bytes(10923, 63, 10, 2, A.KR_LANCZOS) == oracle.memory_bytes(10923, 63, 10, 2, "lanczos")
+    assert L.krylov_memory_bytes(0, 5, 1, 1, A.KR_ARNOLDI) == -1

@@ -718,3 +718,15 @@ def test_adaptive_arnoldi_sound_against_dense_expm():
             err = np.abs(res["coeff"][j, :, d] - exact)
             # ||C (x - x_k)|| <= ||C|| ||x - x_k|| <= ||C||_2 ||v|| bound
             assert np.max(err) <= np.linalg.norm(C, 2) * r["beta0"] * r["bound"] + 1e-12, (d, j)
+
+
+def test_a_priori_bound_and_memory_formulas():
+    """P:674-676: at ||At|| = 32771611 even k = 10^6 gives an a priori bound of 10^16182319 (the printed value;
+    SURVEY A.1: 16182318.694); storing V for k = 5932 at n = 10^9 needs 46 TB (Eq. 4); Alg. 4's
+    Eq. 6 memory for the same run is three vectors (24 GB)."""
+    v = oracle.a_priori_bound_log10(32771611, 10 ** 6)
+    assert abs(v - 16182318.694) < 1e-3 and round(v) == 16182319
+    m = oracle.memory_bytes(10 ** 9, 5932, method="arnoldi")
+    assert m == 5932 * (10 ** 9 + 5932) * 8 and round(m / 2 ** 40) == 43 and round(m / 1e12) == 47  # "46 TB"
+    assert 45.5e12 < m < 47.5e12
+    assert oracle.memory_bytes(10 ** 9, 5932, 1, 1, "lanczos") == (3 * 5932 + 4 * 10 ** 9) * 8
