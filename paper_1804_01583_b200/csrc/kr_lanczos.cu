@@ -103,11 +103,13 @@ struct StepArgs {
     DVec gen;                // init pass with an analytic generator (box / all): fill u_1 in the same pass
 };
 
+template <int NT>
 __device__ void lz_epilogue(const StepArgs& a, const double* acc, double* red, int64_t plane_elems);
 
+// tiles of >= 2048 cells run with 512 threads (one CTA per SM), smaller ones with 256 (two CTAs per SM)
 template <int TX, int TY>
 struct Geo {
-    static constexpr int NT = 256;
+    static constexpr int NT = (TX * TY >= 2048) ? 512 : 256;
     static constexpr int CW = TX + 4, CH = TY + 3;  // u_i box: x0-2 .. x0+TX+1, y0-1 .. y0+TY+1
     static constexpr int PW = TX + 2, PH = TY + 1;  // u_{i-1} box: x0 .. x0+TX+1, y0 .. y0+TY
     static constexpr int WW = TX + 1, WH = TY + 1;  // w plane on the tile + forward ring
@@ -118,7 +120,7 @@ struct Geo {
     static constexpr int NTC = TX * TY;  // tile cells: NTC / NT per thread, always active
     static constexpr int TS = NTC / NT;
     static constexpr int NR = TX + TY;   // forward ring: right column + top row (no corner), tid < NR
-    static_assert(NTC % NT == 0 && NR <= NT, "tile must map onto 256 threads");
+    static_assert(NTC % NT == 0 && NR <= NT, "tile must map onto the CTA's threads");
 };
 
 template <int TX, int TY, int S>
@@ -353,7 +355,7 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
 }
 
 template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false>
-__global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(const __grid_constant__ CUtensorMap tmC,
+__global__ void __launch_bounds__(Geo<TX, TY>::NT, (TX * TY >= 2048) ? 1 : ((TX * TY > 512) ? 2 : 3)) lz_step_kernel(const __grid_constant__ CUtensorMap tmC,
                                                          const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
     using G = Geo<TX, TY>;
     if (a.sc->done) return;  // breakdown happened earlier: uniform early exit
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(256, (TX * TY > 512) ? 2 : 3) lz_step_kernel(c
 
     if (HALO && a.rfence) __threadfence_system();  // peer-memory halo stores visible before the collective that follows
     __syncthreads();  // stage buffers are free: reuse them as reduction scratch
-    lz_epilogue(a, acc, reinterpret_cast<double*>(smem), a.plane);
+    lz_epilogue<G::NT>(a, acc, reinterpret_cast<double*>(smem), a.plane);
 }
 
 // Scalar update after the (global) reduction: fixed-order sum over the R rank/slab vectors, then
@@ -482,11 +484,12 @@ __global__ void lz_finalize(const double* rankvec, int R, int nq, int n_out, int
 // Per-CTA partial sums, quantity-major [nqp][nblk]: [0] sum w^2, [1] sum D, [2 + r] box row r (all-grid
 // rows take sum w). No fence or atomic: the CTA exits immediately; lz_reduce_kernel (next launch)
 // reduces them in a fixed order.
+template <int NT>
 __device__ void lz_epilogue(const StepArgs& a, const double* acc, double* red, int64_t plane_elems) {
     (void)red;
     (void)plane_elems;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    __shared__ double wred[8][3 + KR_MAX_BOX];
+    __shared__ double wred[NT / 32][3 + KR_MAX_BOX];
 #pragma unroll
     for (int r = 0; r < 3 + KR_MAX_BOX; ++r) {
         if (r < 3 + a.nbox) {
@@ -500,7 +503,7 @@ __device__ void lz_epilogue(const StepArgs& a, const double* acc, double* red, i
     if (tid < a.nqp) {
         const int src = tid < 2 ? tid : (((a.all_mask >> (tid - 2)) & 1u) ? 2 : tid + 1);
         double s = 0.0;
-        for (int w = 0; w < 8; ++w) s += wred[w][src];
+        for (int w = 0; w < NT / 32; ++w) s += wred[w][src];
         const int64_t nblk = (int64_t)gridDim.x * gridDim.y * gridDim.z;
         const int64_t blk = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
         a.partials[(int64_t)tid * nblk + blk] = s;
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(RT) lz_reduce_kernel(const StepArgs a, int64_t
 // v = value * [x in X][y in Y][z in Z] with X, Y, Z the box ranges clipped to the grid (ALL = whole grid),
 // so membership is precomputed per axis.
 template <int TX, int TY>
-__global__ void __launch_bounds__(256) lz_fillinit_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(Geo<TX, TY>::NT) lz_fillinit_kernel(const StepArgs a) {
     using G = Geo<TX, TY>;
     if (a.sc->done) return;
     double* red_s = nullptr;  // the epilogue needs no scratch
@@ -694,7 +697,7 @@ __global__ void __launch_bounds__(256) lz_fillinit_kernel(const StepArgs a) {
             }
         }
     }
-    lz_epilogue(a, acc, red_s, a.plane);
+    lz_epilogue<G::NT>(a, acc, red_s, a.plane);
 }
 
 __global__ void lz_reset(LzScalars* sc) {
@@ -743,6 +746,7 @@ struct Stages {
 }  // namespace
 
 size_t kr_lz_step_smem(int TX, int TY) {
+    if (TX == 64 && TY == 32) return step_smem_bytes<64, 32, Stages<64, 32>::S>();
     if (TX == 64 && TY == 16) return step_smem_bytes<64, 16, Stages<64, 16>::S>();
     if (TX == 64 && TY == 8) return step_smem_bytes<64, 8, Stages<64, 8>::S>();
     if (TX == 32 && TY == 8) return step_smem_bytes<32, 8, Stages<32, 8>::S>();
@@ -774,13 +778,14 @@ static int occupancy_t() {
     set_smem_attr<TX, TY, false, true, true>();
     int nb = 0, nb2 = 0;
     KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, false>,
-                                                          256, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
+                                                          Geo<TX, TY>::NT, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
     KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, true>,
-                                                          256, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
+                                                          Geo<TX, TY>::NT, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
     return nb < nb2 ? nb : nb2;
 }
 
 int kr_lz_occupancy(int TX, int TY) {
+    if (TX == 64 && TY == 32) return occupancy_t<64, 32>();
     if (TX == 64 && TY == 16) return occupancy_t<64, 16>();
     if (TX == 64 && TY == 8) return occupancy_t<64, 8>();
     if (TX == 32 && TY == 8) return occupancy_t<32, 8>();
@@ -869,7 +874,7 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
     if (fillinit) {
         StepArgs a = make_args(h, sl, dl, cur, 0, true, false, cur);
         a.gen = h->dirs_h[h->my_dirs[dl]];
-        lz_fillinit_kernel<TX, TY><<<sl.grid, 256, 0, h->stream>>>(a);
+        lz_fillinit_kernel<TX, TY><<<sl.grid, Geo<TX, TY>::NT, 0, h->stream>>>(a);
     } else {
         StepArgs a = make_args(h, sl, dl, nxt, step, init, write, init ? cur : (write ? nxt : -1));
         const CUtensorMap& tc = sl.tmC[cur];
@@ -878,18 +883,18 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
         const bool halo = a.rlo || a.rhi;  // this slab writes halo planes into a neighbour's buffer
         if (h->gen_bc) {
             if (init)
-                lz_step_kernel<TX, TY, S, true, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, true, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else if (halo)
-                lz_step_kernel<TX, TY, S, false, true, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, true, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else
-                lz_step_kernel<TX, TY, S, false, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
         } else {
             if (init)
-                lz_step_kernel<TX, TY, S, true, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, true, false><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else if (halo)
-                lz_step_kernel<TX, TY, S, false, false, true><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, false, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else
-                lz_step_kernel<TX, TY, S, false, false><<<sl.grid, 256, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, false><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
         }
     }
     KR_CUDA(cudaGetLastError());
@@ -908,6 +913,8 @@ static void step_launch(kr_handle* h, Slab& sl, int dl, int cur, int prev, int n
                         bool fillinit = false) {
     if (h->TX == 64 && h->TY == 16)
         step_launch_t<64, 16>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
+    else if (h->TX == 64 && h->TY == 32)
+        step_launch_t<64, 32>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
     else if (h->TX == 64 && h->TY == 8)
         step_launch_t<64, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
     else if (h->TX == 32 && h->TY == 8)
