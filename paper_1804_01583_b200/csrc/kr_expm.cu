@@ -333,7 +333,9 @@ __global__ void lemma_kernel(const double* hlast, const double* beta0, const dou
 }  // namespace
 
 void kr_expm_prepare(kr_handle* h) {
-    const size_t smem = (size_t)6 * h->k * (h->k + 1) * sizeof(double);
+    // the attribute is a per-kernel, process-wide maximum: always the largest (k = 64) size, so that handles of
+    // different k (and the large route's small checkpoints) never lower it under each other
+    const size_t smem = (size_t)6 * 64 * 65 * sizeof(double);
     KR_CUDA(cudaFuncSetAttribute(expm_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KR_CUDA(cudaFuncSetAttribute(expm_doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     h->expm_doubling = getenv("KR_EXPM_PADE") == nullptr;  // KR_EXPM_PADE=1: one Pade-13 per (step, direction)
@@ -350,12 +352,8 @@ void kr_expm_prepare(kr_handle* h) {
 // Hdense [kc][kc] on the device, trajectory scratch xt [64][ldx]; writes the coefficients of local
 // direction dl and hlast. One launch.
 void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, int hstride, double* xt, int ldx) {
-    static bool attr = false;
     const size_t smem = (size_t)6 * 64 * 65 * sizeof(double);
-    if (!attr) {
-        KR_CUDA(cudaFuncSetAttribute(expm_doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    KR_CUDA(cudaFuncSetAttribute(expm_doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int ndl = (int)h->my_dirs.size();
     ExpmArgs a;
     a.H = nullptr;

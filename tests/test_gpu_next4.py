@@ -60,3 +60,26 @@ def test_cgs2_forced_on_config1():
     finally:
         del os.environ["KR_FORCE_CGS"]
     assert_coeff(coeff, oracle.krylov_project(p)["coeff"], "C1 CGS2")
+
+
+def test_new_paths_bitwise_deterministic():
+    """Fixed-order reductions everywhere: repeated runs of the adaptive large-k route, the CGS2 Arnoldi, the
+    transpose mode and the batched LP are bitwise identical."""
+    from paper_1804_01583_b200 import KrylovReach
+
+    def run_all():
+        out = []
+        with KrylovReach(W.heat_paper(20, k_max=400)) as h:
+            out.append(h.project()[0])
+        with KrylovReach(W.heat_heater(32, k=48, n_steps=100, step=2.5)) as h:
+            out.append(h.project()[0])
+        with KrylovReach(W.config2(n=3000, n_gen=6, n_steps=200, k=30), sim="transpose") as h:
+            c, _ = h.project()
+            out.append(c)
+            lp = h.check_lp(np.ones((1, 6)), [0.5], [[1.0, 0, 0]], [float(np.median(c[:, 0, :].sum(axis=1)))])
+            out.append(lp["feasible"].astype(np.float64))
+        return out
+
+    a, b = run_all(), run_all()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
