@@ -300,11 +300,14 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
+        per_step = []
         for _ in range(args.steps):
             cb = one_step()
             t = h.last_timing()
             step_ms.append(t["step_ms_mean"])
             iter_ms.append(t["iter_ms"])
+            st_ms = h.step_times()
+            per_step.extend(st_ms[1:-1] if len(st_ms) > 2 else st_ms)  # steps 2..k-1
         ev1.record(stream)
         barrier()
     launches = h.launch_count() - l0
@@ -364,6 +367,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(p, world),
         "fused_step": {"gbs": achieved, "pct_of_peak": 100.0 * achieved / peak, "ms_mean": sk,
+                       "ms_median_steps_2_to_k-1": float(np.median(per_step)) if per_step else None,
+                       "runs": args.steps,
                        "bytes_per_launch": n_local_bytes, "launches_per_step": timing["step_launches"]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "lz_step_kernel (fused Lanczos step)",

@@ -236,6 +236,11 @@ kr_status krylov_transfer_bytes(const kr_handle* h, int64_t* h2d, int64_t* d2h);
 kr_status krylov_last_timing(const kr_handle* h, double* iter_ms, double* step_kernel_ms_mean,
                              int64_t* step_kernel_launches, double* step_kernel_bytes);
 
+/* Per-step device times (ms, CUDA events around each Krylov step's operator/step kernel of local direction 0)
+ * of the last krylov_project, for the first min(k, KR_MAX_EV env, default 256) steps: ms HOST [cap] or NULL,
+ * *n receives the number recorded. */
+kr_status krylov_step_times(const kr_handle* h, double* ms, int32_t cap, int32_t* n);
+
 /* Device time in ms spent by the last krylov_project in the large-k exponential route (all checkpoint
  * evaluations: e^{H delta} by scaling and squaring, the time march, projection and Lemma 1 bound;
  * CUDA events on the library stream) and the number of evaluations. 0 / 0 on the small-k route.    */

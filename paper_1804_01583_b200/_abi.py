@@ -63,7 +63,7 @@ EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "k
            "krylov_krylov_data", "krylov_transfer_bytes", "krylov_zslab_halo_plan", "krylov_tridiag",
            "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info", "krylov_check_lp",
            "krylov_eval_outputs", "krylov_ipc_blob", "krylov_p2p_open", "krylov_p2p_verify", "krylov_p2p_enable",
-           "krylov_a_priori_bound_log10", "krylov_memory_bytes"]
+           "krylov_a_priori_bound_log10", "krylov_memory_bytes", "krylov_step_times"]
 
 _lib = None
 
@@ -97,6 +97,7 @@ def lib():
     L.krylov_check_lp.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, vp, vp, vp, C.POINTER(kr_cex), vp, vp]
     L.krylov_eval_outputs.argtypes = [vp, C.c_int64, vp, vp]
     L.krylov_ipc_blob.argtypes = [vp, vp]
+    L.krylov_step_times.argtypes = [vp, vp, C.c_int32, C.POINTER(C.c_int32)]
     L.krylov_a_priori_bound_log10.argtypes = [C.c_double, C.c_int32]
     L.krylov_a_priori_bound_log10.restype = C.c_double
     L.krylov_memory_bytes.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32]

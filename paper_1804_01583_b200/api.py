@@ -251,6 +251,14 @@ class KrylovReach:
         A.check(A.lib().krylov_transfer_bytes(self.h, C.byref(h2d), C.byref(d2h)))
         return h2d.value, d2h.value
 
+    def step_times(self):
+        """Per-step device times (ms) of the last project (krylov_step_times)."""
+        n = C.c_int32()
+        A.check(A.lib().krylov_step_times(self.h, None, 0, C.byref(n)))
+        ms = np.zeros(max(n.value, 1))
+        A.check(A.lib().krylov_step_times(self.h, _p(ms), n.value, C.byref(n)))
+        return ms[:n.value]
+
     def launch_count(self):
         return int(A.lib().krylov_launch_count(self.h))
 

@@ -1185,11 +1185,13 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             const int nrec = std::min(std::min(h->k, nev), std::max(1, keff0));  // pairs recorded this run
             FILE* trace = nullptr;
             if (const char* tp = getenv("KR_STEP_TRACE")) trace = fopen(tp, "w");  // diagnostics: per-step ms
+            h->step_ms.clear();
             for (int i = 0; i < nrec; ++i) {
                 float t = 0.f;
                 KR_CUDA(cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]));
                 tot += t;
                 cnt++;
+                h->step_ms.push_back(t);
                 if (trace) {
                     float g = 0.f;
                     if (i + 1 < nrec) KR_CUDA(cudaEventElapsedTime(&g, h->ev[2 * i], h->ev[2 * i + 2]));
@@ -1463,6 +1465,14 @@ int64_t krylov_memory_bytes(int64_t n, int32_t k, int32_t i, int32_t o, int32_t 
     if (n < 1 || k < 1 || i < 1 || o < 1) return -1;
     if (method == KR_LANCZOS) return (3 * (int64_t)k + n * (int64_t)std::min(i, o) + 3 * n) * 8;
     return (int64_t)k * (n + (int64_t)k) * 8;
+}
+
+kr_status krylov_step_times(const kr_handle* h, double* ms, int32_t cap, int32_t* n) {
+    if (!h || !n || cap < 0) return KR_EINVAL;
+    *n = (int32_t)h->step_ms.size();
+    for (int i = 0; i < (int)h->step_ms.size() && i < cap; ++i)
+        if (ms) ms[i] = h->step_ms[(size_t)i];
+    return KR_OK;
 }
 
 kr_status krylov_sim_info(const kr_handle* h, int32_t* transposed, int32_t* n_sim) {

@@ -231,6 +231,7 @@ struct kr_handle {
     std::vector<cudaEvent_t> ev;  // pairs around each step kernel
     cudaEvent_t ev_it0, ev_it1;
     double last_iter_ms, last_step_ms_mean;
+    std::vector<double> step_ms;  // per-step device times of the last project (first KR_MAX_EV steps, direction 0)
     int64_t last_step_launches;
     double step_bytes;  // algorithmic bytes per fused step launch (24 n_local)
     int64_t h2d_bytes, d2h_bytes;  // host<->device bytes moved by the ABI calls (create/project/check_box)
