@@ -1158,6 +1158,7 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             enqueue(h->timing);
         }
         KR_CUDA(cudaStreamSynchronize(h->stream));
+        if (h->world > 1) kr_nccl_check(h->comm);
         // device-side status (zero direction / non-finite)
         int32_t worst = 0;
         if (h->path == PATH_FUSED_LANCZOS) {

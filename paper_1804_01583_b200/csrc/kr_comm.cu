@@ -41,6 +41,14 @@ void kr_comm_destroy_impl(kr_comm* c) {
     delete c;
 }
 
+// Asynchronous NCCL failures (a peer died, a link error) surface here instead of as a hang later.
+void kr_nccl_check(kr_comm* c) {
+    if (!c) return;
+    ncclResult_t async = ncclSuccess;
+    KR_NCCL(ncclCommGetAsyncError(reinterpret_cast<ncclComm_t>(c->nccl), &async));
+    if (async != ncclSuccess) KR_THROW(KR_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(async));
+}
+
 // In-place all-gather: send = recv + rank * count.
 void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s) {
     KR_NCCL(ncclAllGather(send, recv, count, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), s));

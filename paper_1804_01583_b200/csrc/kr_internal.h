@@ -279,6 +279,7 @@ void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int
 
 // nccl
 void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s);
+void kr_nccl_check(kr_comm* c);
 void kr_nccl_halo(kr_comm* c, kr_handle* h, int buf, cudaStream_t s);
 // peer-memory halo transport (kr_comm.cu)
 void kr_p2p_blob(kr_handle* h, void* out);
