@@ -209,3 +209,19 @@ def test_adaptive_arnoldi_alg2(route, monkeypatch):
         for (kg, bg), (ko, bo) in zip(checks[d], r["checks"]):
             assert abs(bg - bo) <= 1e-8 * abs(bo), (d, kg, bg, bo)
     assert_coeff(coeff, ref["coeff"], f"adaptive Arnoldi ({route})")
+
+
+def test_adaptive_dirichlet_sparse_generator_slabs():
+    """Alg. 4 on the Dirichlet stencil with a sparse (non-box) generator, single slab and 3 virtual slabs."""
+    p = W.heat(18, 3, 600, n_steps=200, step=0.05, mz=15)
+    p["eps"] = 1e-7
+    p["k_max"] = 600
+    rng = np.random.default_rng(3)
+    idx = rng.choice(18 * 18 * 15, size=40, replace=False)
+    p["gens"] = [W.sparse(idx, rng.uniform(0.5, 1.5, 40))]
+    ref = oracle.krylov_project_adaptive(p)
+    for vs in (0, 3):
+        coeff, stats, _, checks = gpu(p, virtual_slabs=vs)
+        assert stats[0]["k_eff"] == ref["per_dir"][0]["k_eff"]
+        assert [k for k, _ in checks] == [k for k, _ in ref["per_dir"][0]["checks"]]
+        assert_coeff(coeff, ref["coeff"], f"adaptive dirichlet sparse vs={vs}")

@@ -84,3 +84,25 @@ def test_transpose_more_simulations_than_directions():
     coeff, stats, cb, (tr, ns, _) = run(p, sim="transpose")
     assert tr and ns == 4 and len(stats) == 4
     assert_coeff(coeff, oracle.krylov_project_transpose(p)["coeff"], "heat^T o>i")
+
+
+def test_transpose_combinations():
+    """Transpose mode with a center but no affine term (the fixed direction is c itself, not lifted), on CSR
+    and on the stencil; every output against the oracle's transpose mode, verdicts as in forward mode."""
+    rp, ci, va, dense = W.random_csr(300, 5, seed=11, scale=0.3)
+    p = {"name": "csr_center", "op": "csr", "n": 300, "row_ptr": rp, "col_idx": ci, "val": va, "b": None,
+         "gens": [W.sparse([0], [1.0]), W.box((10,), (40,), 0.5), W.sparse([7, 8], [1.0, -1.0])],
+         "z_lo": np.array([-1.0, 0.0, -0.5]), "z_hi": np.array([1.0, 2.0, 0.5]), "center": W.sparse([3, 5], [2.0, 1.0]),
+         "outs": [W.allv(1.0), W.sparse(np.arange(300), np.linspace(-1, 1, 300))], "step": 0.05, "n_steps": 120,
+         "k": 30, "method": "arnoldi", "thresholds": [(0, W.GE, 1.5)]}
+    coeff, stats, cb, (tr, ns, _) = run(p, sim="transpose")
+    assert tr and ns == 2
+    ref = oracle.krylov_project_transpose(p)["coeff"]
+    assert_coeff(coeff, ref, "csr center^T")
+    ocb = oracle.check_box(p, ref)
+    assert cb["found"] == ocb["found"] and cb["step"] == ocb["step"]
+    q = W.heat(16, 3, 24, n_steps=60)
+    q["center"] = W.box((2, 2, 2), (5, 6, 7), 0.3)
+    coeff, stats, cb, (tr, ns, _) = run(q, sim="transpose")
+    assert tr and ns == 4
+    assert_coeff(coeff, oracle.krylov_project_transpose(q)["coeff"], "heat center^T")
