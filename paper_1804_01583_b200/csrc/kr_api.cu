@@ -837,9 +837,20 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                     KR_THROW(KR_EINVAL, "each slab needs >= 2 planes");
                 sl.nz = sl.z1 - sl.z0;
                 const size_t vb = (size_t)(sl.nz + 3) * h->my * h->pitch * sizeof(double);
+                // Only the ghost / halo planes need zeros up front (global Dirichlet ghosts; neighbour halos
+                // are rewritten every step before they are read, u_1 is written on all planes by the init
+                // pass, and every later vector on all owned planes before its first read): 3 planes per
+                // buffer instead of the whole 24 GB at C5 (create time 4 ms shorter).
+                const size_t pb = (size_t)h->my * h->pitch * sizeof(double);
                 for (int b = 0; b < 3; ++b) {
                     sl.u[b] = reinterpret_cast<double*>(carve(h, vb));
-                    KR_CUDA(cudaMemsetAsync(sl.u[b], 0, vb, h->stream));
+                    if (getenv("KR_ZERO_ALL")) {
+                        KR_CUDA(cudaMemsetAsync(sl.u[b], 0, vb, h->stream));
+                    } else {
+                        KR_CUDA(cudaMemsetAsync(sl.u[b], 0, pb, h->stream));
+                        KR_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(sl.u[b]) + (size_t)(sl.nz + 1) * pb, 0, 2 * pb,
+                                                h->stream));
+                    }
                 }
                 const int64_t gx = (h->mx + h->TX - 1) / h->TX, gy = (h->my + h->TY - 1) / h->TY;
                 const int64_t slots_total = (int64_t)dev_sms * occ;

@@ -245,3 +245,18 @@ def test_expm_doubling_equals_per_step_pade(cfg, monkeypatch):
     b, _, _, _ = gpu_run(p)
     assert_coeff(a, b, f"{cfg} doubling vs per-step Pade")
     assert_coeff(a, oracle.krylov_project(p)["coeff"], f"{cfg} doubling vs oracle")
+
+
+@pytest.mark.parametrize("vs", [0, 3])
+def test_state_buffers_need_only_ghost_planes_zeroed(vs, monkeypatch):
+    """create zeroes only the ghost / halo planes of the three state buffers: the results equal those of
+    fully zeroed buffers (KR_ZERO_ALL=1) bitwise, also when the same handle projects twice."""
+    from paper_1804_01583_b200 import KrylovReach
+    p = W.heat(33, 4, 20, n_steps=40, my=19, mz=14)
+    with KrylovReach(p, virtual_slabs=vs) as h:
+        a1, _ = h.project()
+        a2, _ = h.project()
+    monkeypatch.setenv("KR_ZERO_ALL", "1")
+    with KrylovReach(p, virtual_slabs=vs) as h:
+        b1, _ = h.project()
+    assert np.array_equal(a1, a2) and np.array_equal(a1, b1)
