@@ -275,26 +275,39 @@ __global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* x
     for (int l = threadIdx.x; l < n; l += ET) X[(int64_t)l * ldx] = l == 0 ? 1.0 : 0.0;  // x_0 = e_1 exactly
     const double* Hd = a.Hsrc ? a.Hsrc : a.H + (int64_t)d * (k + 1) * k;
     double* E = np1 > 1 ? pade13(Hd, a.Hsrc ? a.hstride : k, n, a.step, sm, fac, piv_s, sq_s) : sm;
-    // E lives in one of the six buffers; use two others (disjoint from it) for the powers
+    // powers in two buffers (Pw, Tw), the remaining four (contiguous, 4 n (n+1) doubles) stage column tiles of the
+    // trajectory, so every product below reads shared memory only (a dot over n global-memory loads per output
+    // was latency-bound: ~0.6 ms per C2 run)
     const int msz = n * ld;
     const int ei = (int)((E - sm) / msz);
-    double* Pw = sm + (size_t)((ei + 1) % 6) * msz;
-    double* Tw = sm + (size_t)((ei + 2) % 6) * msz;
-    for (int e = threadIdx.x; e < n * n; e += ET) {
-        const int o = (e / n) * ld + e % n;
-        Pw[o] = E[o];
+    double* Pw = sm + (size_t)(ei == 1 ? 1 : 0) * msz;
+    double* Tw = sm + (size_t)(ei == 1 ? 0 : 1) * msz;
+    double* XT = sm + (size_t)2 * msz;
+    const int TC = min(128, 4 * (n + 1));  // columns per tile: n x TC doubles fit the four buffers
+    if (ei > 1) {
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int o = (e / n) * ld + e % n;
+            Pw[o] = E[o];
+        }
     }
     __syncthreads();
     for (int64_t w0 = 1; w0 < np1; w0 <<= 1) {
         const int64_t w = min(w0, np1 - w0);
-        for (int64_t e = threadIdx.x; e < (int64_t)n * w; e += ET) {
-            const int i = (int)(e / w);
-            const int64_t c = e - (int64_t)i * w;
-            double s = 0.0;
-            for (int l = 0; l < n; ++l) s = fma(Pw[i * ld + l], X[(int64_t)l * ldx + c], s);
-            X[(int64_t)i * ldx + w0 + c] = s;
+        for (int64_t c0 = 0; c0 < w; c0 += TC) {  // X[:, w0 + c] = Pw X[:, c], c in [c0, c0 + tc)
+            const int tc = (int)min((int64_t)TC, w - c0);
+            for (int e = threadIdx.x; e < n * tc; e += ET) {
+                const int l = e / tc, cc = e - l * tc;
+                XT[l * TC + cc] = X[(int64_t)l * ldx + c0 + cc];
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < n * tc; e += ET) {
+                const int i = e / tc, cc = e - i * tc;
+                double s = 0.0;
+                for (int l = 0; l < n; ++l) s = fma(Pw[i * ld + l], XT[l * TC + cc], s);
+                X[(int64_t)i * ldx + w0 + c0 + cc] = s;
+            }
+            __syncthreads();
         }
-        __syncthreads();
         if (2 * w0 < np1) {
             mm(Pw, Pw, Tw, n, ld);
             __syncthreads();
@@ -305,29 +318,49 @@ __global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* x
     }
     const double* Pd = a.P + (int64_t)d * a.n_out * k;
     const double bz = a.beta0[d];
-    for (int64_t j = threadIdx.x; j < np1; j += ET) {
-        for (int r = 0; r < a.n_out; ++r) {
-            double s = 0.0;
-            for (int l = 0; l < n; ++l) s = fma(Pd[(int64_t)r * k + l], X[(int64_t)l * ldx + j], s);
-            a.coeff[(j * a.n_out + r) * a.ndl_stride + d] = bz * s;
+    for (int64_t c0 = 0; c0 < np1; c0 += TC) {
+        const int tc = (int)min((int64_t)TC, np1 - c0);
+        for (int e = threadIdx.x; e < n * tc; e += ET) {
+            const int l = e / tc, cc = e - l * tc;
+            XT[l * TC + cc] = X[(int64_t)l * ldx + c0 + cc];
         }
-        a.hlast[(int64_t)d * np1 + j] = X[(int64_t)(n - 1) * ldx + j];
+        __syncthreads();
+        for (int e = threadIdx.x; e < a.n_out * tc; e += ET) {
+            const int r = e / tc, cc = e - r * tc;
+            double s = 0.0;
+            for (int l = 0; l < n; ++l) s = fma(Pd[(int64_t)r * k + l], XT[l * TC + cc], s);
+            a.coeff[((c0 + cc) * a.n_out + r) * a.ndl_stride + d] = bz * s;
+        }
+        for (int cc = threadIdx.x; cc < tc; cc += ET) a.hlast[(int64_t)d * np1 + c0 + cc] = XT[(n - 1) * TC + cc];
+        __syncthreads();
     }
 }
 
-__global__ void lemma_kernel(const double* hlast, const double* beta0, const double* hnext, const int32_t* keff,
-                             int64_t n_steps, double step, double mu, int ndl, double* lemma) {
-    const int d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= ndl) return;
+// Lemma 1: beta0 h_{k+1,k} e^{max(mu,0) T} int_0^T |x_k(t)| dt, trapezoid on the t_j grid. One CTA per
+// direction: each thread sums a contiguous run of trapezoids, the runs are combined in thread order (fixed order,
+// bit-reproducible; a serial per-thread loop over 2000 dependent loads was ~0.25 ms).
+__global__ void __launch_bounds__(256) lemma_kernel(const double* hlast, const double* beta0, const double* hnext,
+                                                    const int32_t* keff, int64_t n_steps, double step, double mu,
+                                                    double* lemma) {
+    const int d = blockIdx.x;
+    __shared__ double red[256];
     if (keff[d] <= 0) {
-        lemma[d] = 0.0;
+        if (threadIdx.x == 0) lemma[d] = 0.0;
         return;
     }
     const double* h = hlast + (int64_t)d * (n_steps + 1);
-    double integral = 0.0;
-    for (int64_t j = 0; j < n_steps; ++j) integral += 0.5 * step * (fabs(h[j]) + fabs(h[j + 1]));
-    const double T = (double)n_steps * step;
-    lemma[d] = beta0[d] * hnext[d] * exp(fmax(mu, 0.0) * T) * integral;
+    const int64_t per = (n_steps + 255) / 256;
+    const int64_t j0 = threadIdx.x * per, j1 = min(j0 + per, n_steps);
+    double s = 0.0;
+    for (int64_t j = j0; j < j1; ++j) s += 0.5 * step * (fabs(h[j]) + fabs(h[j + 1]));
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double integral = 0.0;
+        for (int t = 0; t < 256; ++t) integral += red[t];
+        const double T = (double)n_steps * step;
+        lemma[d] = beta0[d] * hnext[d] * exp(fmax(mu, 0.0) * T) * integral;
+    }
 }
 
 }  // namespace
@@ -399,8 +432,8 @@ void kr_expm_enqueue(kr_handle* h) {
         expm_project_kernel<<<dim3((unsigned)(h->n_steps + 1), ndl), ET, smem, h->stream>>>(a);
     KR_CUDA(cudaGetLastError());
     h->launches++;
-    lemma_kernel<<<(ndl + 63) / 64, 64, 0, h->stream>>>(h->d_hlast, h->d_beta0, h->d_hnext, h->d_keff, h->n_steps,
-                                                        h->step, h->mu, ndl, h->d_lemma);
+    lemma_kernel<<<ndl, 256, 0, h->stream>>>(h->d_hlast, h->d_beta0, h->d_hnext, h->d_keff, h->n_steps, h->step,
+                                             h->mu, h->d_lemma);
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }

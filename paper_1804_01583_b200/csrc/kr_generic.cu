@@ -149,10 +149,6 @@ __global__ void spmm_long_rows_kernel(const int64_t* __restrict__ rp, const int3
     }
 }
 
-struct FaceCor {  // per-face diagonal correction of face cells relative to Dirichlet (x-, x+, y-, y+, z-, z+)
-    double e[6];
-};
-
 __global__ void stencil_apply_kernel(int64_t mx, int64_t my, int64_t mz, double cx, double cy, double cz,
                                      const double* __restrict__ X, int64_t xstride, double* __restrict__ Y,
                                      int64_t ystride, const int32_t* __restrict__ done, FaceCor fc,
@@ -422,15 +418,15 @@ void kr_ge_enqueue_step(kr_handle* h, int j) {
     const int k = h->k;
     const int64_t vstride = (int64_t)(k + 1) * N;
     const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
-    FaceCor fc{};
-    {
-        const double c[3] = {h->cx, h->cy, h->cz};
-        for (int f = 0; f < 6; ++f)
-            fc.e[f] = (h->bc[f] != KR_BC_DIRICHLET ? c[f / 2] : 0.0) - (h->bc[f] == KR_BC_ROBIN ? h->gamma[f] : 0.0);
-    }
+    const FaceCor fc = kr_face_cor(h);
     const double* X = h->d_V + (int64_t)(j - 1) * N;
     const bool evj = h->timing && (size_t)(2 * j) <= h->ev.size();
     if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1)], h->stream));
+    if (h->use_cgs) {  // operator fused into the first CGS2 pass (kr_arnoldi.cu): the events bracket the whole step
+        kr_cgs_step(h, j, ndl, h->d_cgs);
+        if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1) + 1], h->stream));
+        return;
+    }
     if (h->op == KR_OP_CSR) {
         spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X, vstride,
                                                               h->d_W, N, ndl, h->d_done);

@@ -110,6 +110,10 @@ void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int
     int32_t rank, world, device;
 };
 
+struct FaceCor {  // per-face diagonal correction of face cells relative to Dirichlet (x-, x+, y-, y+, z-, z+)
+    double e[6];
+};
+
 struct kr_handle {
     // problem (host copies of scalars)
     int32_t op, method, path, part;
@@ -252,10 +256,20 @@ void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events);
 size_t kr_lz_step_smem(int TX, int TY);
 
 // generic
+// the stencil operator's per-face diagonal correction (insulated / Robin faces, NEXT-1) relative to Dirichlet
+inline FaceCor kr_face_cor(const kr_handle* h) {
+    FaceCor fc{};
+    const double c[3] = {h->cx, h->cy, h->cz};
+    for (int f = 0; f < 6; ++f)
+        fc.e[f] = (h->bc[f] != KR_BC_DIRICHLET ? c[f / 2] : 0.0) - (h->bc[f] == KR_BC_ROBIN ? h->gamma[f] : 0.0);
+    return fc;
+}
 void kr_ge_enqueue_direction_set(kr_handle* h);
 void kr_ge_enqueue_init(kr_handle* h);
 void kr_ge_enqueue_step(kr_handle* h, int j);
 size_t kr_cgs_scratch_doubles(const kr_handle* h, int ndl);
+// One stored-basis Krylov step of the multi-CTA CGS2 path: j == 0 normalises the start vectors; j >= 1 applies
+// the operator to v_{j-1} (fused with the first projection pass) and orthogonalises (kr_arnoldi.cu).
 void kr_cgs_step(kr_handle* h, int j, int ndl, double* scratch);
 
 // expm + projection + lemma
