@@ -300,11 +300,33 @@ __global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* x
                 XT[l * TC + cc] = X[(int64_t)l * ldx + c0 + cc];
             }
             __syncthreads();
-            for (int e = threadIdx.x; e < n * tc; e += ET) {
-                const int i = e / tc, cc = e - i * tc;
-                double s = 0.0;
-                for (int l = 0; l < n; ++l) s = fma(Pw[i * ld + l], XT[l * TC + cc], s);
-                X[(int64_t)i * ldx + w0 + c0 + cc] = s;
+            // n x tc product, 4 x 8 register micro-tile per thread (16 x 16 threads cover 64 x 128); each output is
+            // still one fma chain over l in order
+            {
+                const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+                double acc[4][8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+                for (int l = 0; l < n; ++l) {
+                    double av[4], bv[8];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) av[u] = ty + 16 * u < n ? Pw[(ty + 16 * u) * ld + l] : 0.0;
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) bv[v] = tx + 16 * v < tc ? XT[l * TC + tx + 16 * v] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        const int i = ty + 16 * u, cc = tx + 16 * v;
+                        if (i < n && cc < tc) X[(int64_t)i * ldx + w0 + c0 + cc] = acc[u][v];
+                    }
             }
             __syncthreads();
         }
@@ -325,11 +347,18 @@ __global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* x
             XT[l * TC + cc] = X[(int64_t)l * ldx + c0 + cc];
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < a.n_out * tc; e += ET) {
-            const int r = e / tc, cc = e - r * tc;
-            double s = 0.0;
-            for (int l = 0; l < n; ++l) s = fma(Pd[(int64_t)r * k + l], XT[l * TC + cc], s);
-            a.coeff[((c0 + cc) * a.n_out + r) * a.ndl_stride + d] = bz * s;
+        for (int e = threadIdx.x; e < ((a.n_out + 3) / 4) * tc; e += ET) {  // 4 output rows per thread
+            const int r0 = 4 * (e / tc), cc = e % tc;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int l = 0; l < n; ++l) {
+                const double x = XT[l * TC + cc];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (r0 + q < a.n_out) acc[q] = fma(Pd[(int64_t)(r0 + q) * k + l], x, acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (r0 + q < a.n_out) a.coeff[((c0 + cc) * a.n_out + r0 + q) * a.ndl_stride + d] = bz * acc[q];
         }
         for (int cc = threadIdx.x; cc < tc; cc += ET) a.hlast[(int64_t)d * np1 + c0 + cc] = XT[(n - 1) * TC + cc];
         __syncthreads();
