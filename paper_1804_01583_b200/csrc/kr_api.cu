@@ -1,12 +1,28 @@
 // kr_api.cu — the C ABI of include/krylov_reach.h: validation, device memory, descriptor upload,
 // CUDA-graph capture of the hot path, results download. See the header for the contract.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <map>
 #include <utility>
 
 #include "kr_internal.h"
+
+namespace {
+// KR_TRACE=1: host wall-clock of the create phases on stderr (diagnostics only).
+struct PhaseTrace {
+    bool on = getenv("KR_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[kr trace] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+}  // namespace
 
 static thread_local std::string g_err;
 void kr_set_error(const std::string& m) { g_err = m; }
@@ -517,16 +533,20 @@ __global__ void transpose_coeff_kernel(const double* sim, double* cf, int64_t np
 
 void free_handle(kr_handle* h) {
     if (!h) return;
+    PhaseTrace tr;
     kr_p2p_close(h);
     if (h->graph_ready) cudaGraphExecDestroy(h->gexec);
+    tr.mark("destroy: p2p + graph");
     for (auto e : h->ev) cudaEventDestroy(e);
     if (h->ev_it0) cudaEventDestroy(h->ev_it0);
     if (h->ev_it1) cudaEventDestroy(h->ev_it1);
     if (h->ev_lg0) cudaEventDestroy(h->ev_lg0);
     if (h->ev_lg1) cudaEventDestroy(h->ev_lg1);
+    tr.mark("destroy: events");
     for (void* p : h->extra_allocs) cudaFree(p);
     if (h->own_ws && h->ws) cudaFree(h->ws);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    tr.mark("destroy: frees");
     delete h;
 }
 
@@ -612,8 +632,10 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
     TransposeStore T;
     kr_problem q;
     kr_status st = guarded([&] {
+        PhaseTrace tr;
         validate(p);
         build_transposed(p, T, q);
+        tr.mark("transpose lowering");
     });
     if (st != KR_OK) return st;
     st = create_impl(&q, out);
@@ -653,9 +675,11 @@ kr_status krylov_reach_create(const kr_problem* p, kr_handle** out) {
 static kr_status create_impl(const kr_problem* p, kr_handle** out) {
     kr_handle* h = nullptr;
     kr_status st = guarded([&] {
+        PhaseTrace tr;
         if (!out) KR_THROW(KR_EINVAL, "NULL out");
         *out = nullptr;
         validate(p);
+        tr.mark("validate");
         h = new kr_handle();
         h->comm = p->comm;
         h->rank = p->comm ? p->comm->rank : 0;
@@ -663,6 +687,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         if (p->comm && p->comm->device != p->device) KR_THROW(KR_EINVAL, "comm device != problem device");
         if (p->virtual_slabs > 1 && h->world > 1) KR_THROW(KR_EINVAL, "virtual slabs need world == 1");
         const Sizes sz = plan(p, h->rank, h->world);
+        tr.mark("plan");
         h->op = p->op;
         h->method = sz.method;
         h->path = sz.path;
@@ -694,6 +719,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         h->n_steps = p->n_steps;
         h->step = p->step;
         h->mu = gershgorin_mu(p);
+        tr.mark("gershgorin mu");
         h->device = p->device;
         KR_CUDA(cudaSetDevice(p->device));
         if (p->stream) {
@@ -729,6 +755,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         h->d_outs = upload(h, h->outs_h.data(), h->outs_h.size());
         h->d_zlo = upload(h, h->zlo.data(), h->zlo.size());
         h->d_zhi = upload(h, h->zhi.data(), h->zhi.size());
+        tr.mark("stream + dirs + outs");
         // workspace (state vectors)
         if (p->workspace) {
             if (p->workspace_bytes < sz.state_bytes) KR_THROW(KR_ENOMEM, "caller workspace too small");
@@ -775,6 +802,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         h->d_hlast = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * np1 * 8));
         h->d_box = reinterpret_cast<double*>(dalloc(h, (size_t)np1 * h->n_out * (8 + 8 + 4) + 16));
         h->d_cex = dalloc(h, 64 + (size_t)h->n_dir * 8);
+        tr.mark("result buffers");
         if (h->path == PATH_FUSED_LANCZOS) {
             // box-kind output rows are reduced inside the fused kernel, sparse rows gathered after it
             std::vector<int32_t> slots;
@@ -954,7 +982,9 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             h->step_bytes = (h->op == KR_OP_CSR ? (double)p->nnz * 12.0 + (double)(p->n + 1) * 8.0 : 0.0) +
                             16.0 * (double)h->N * ndl;
         }
+        tr.mark("path set-up");
         if (!h->large_route) kr_expm_prepare(h);
+        tr.mark("expm prepare");
         h->d_sense = reinterpret_cast<int32_t*>(dalloc(h, (size_t)h->n_out * 4));
         h->d_thr = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * 8));
         h->timing = true;
@@ -966,9 +996,11 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         for (auto& e : h->ev) KR_CUDA(cudaEventCreate(&e));
         KR_CUDA(cudaEventCreate(&h->ev_it0));
         KR_CUDA(cudaEventCreate(&h->ev_it1));
+        tr.mark("events");
         // all set-up work (zeroing of the state buffers, descriptors) ran on h->stream, which does not
         // synchronise with the legacy default stream: finish it before the handle is used
         KR_CUDA(cudaStreamSynchronize(h->stream));
+        tr.mark("final sync");
         *out = h;
     });
     if (st != KR_OK) free_handle(h);

@@ -510,21 +510,27 @@ __device__ void lz_epilogue(const StepArgs& a, const double* acc, double* red, i
     }
 }
 
-// One CTA: fixed-order reduction of a slab's partials (per-thread strided sums with nqp independent
-// loads in flight, warp trees, warps in order), sparse output rows gathered from the new vector, the
-// slab's vector [2 + n_out] written to rankvec, and — for a single slab on a single rank — the scalar
-// update. Same result for every run (no atomics).
+// Fixed-order reduction of a slab's partials over G CTAs: CTA g sums the contiguous block range
+// [g*seg, (g+1)*seg) (per-thread strided sums with nqp independent loads in flight, warp trees, warps in
+// order) and stores its nqp sums; the last CTA to arrive (arrival counter, reset by it for the next graph
+// replay) adds the G sums in CTA order, gathers the sparse output rows from the new vector, writes the
+// slab's vector [2 + n_out] to rankvec and — for a single slab on a single rank — does the scalar update.
+// Same result for every run (fixed segments and order; the counter only elects the CTA, no float atomics).
 constexpr int RT = 512;
 __global__ void __launch_bounds__(RT) lz_reduce_kernel(const StepArgs a, int64_t nblk) {
     if (a.sc->done) return;
     __shared__ double red[KR_MAX_BOX + 2][RT / 32];
     __shared__ double res[2 + KR_MAX_OUT];
+    __shared__ int last;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int nqp = a.nqp;
+    const int G = (int)gridDim.x;
+    const int64_t seg = (nblk + G - 1) / G;
+    const int64_t b0 = (int64_t)blockIdx.x * seg, b1 = b0 + seg < nblk ? b0 + seg : nblk;
     double v[2 + KR_MAX_BOX];
 #pragma unroll
     for (int q = 0; q < 2 + KR_MAX_BOX; ++q) v[q] = 0.0;
-    for (int64_t b = tid; b < nblk; b += RT) {
+    for (int64_t b = b0 + tid; b < b1; b += RT) {
 #pragma unroll
         for (int q = 0; q < 2 + KR_MAX_BOX; ++q)
             if (q < nqp) v[q] += a.partials[(int64_t)q * nblk + b];
@@ -537,6 +543,29 @@ __global__ void __launch_bounds__(RT) lz_reduce_kernel(const StepArgs a, int64_t
             for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
             if (lane == 0) red[q][wid] = t;
         }
+    }
+    __syncthreads();
+    if (G > 1) {
+        double* gsum = a.partials + (int64_t)nqp * nblk;  // [G][nqp] behind the per-CTA partials
+        if (tid < nqp) {
+            double s = 0.0;
+            for (int w = 0; w < RT / 32; ++w) s += red[tid][w];
+            gsum[(int64_t)blockIdx.x * nqp + tid] = s;
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) last = atomicAdd(a.counter, 1) == G - 1;
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        if (tid == 0) *a.counter = 0;
+        if (tid < nqp) {
+            double s = 0.0;
+            for (int g = 0; g < G; ++g) s += __ldcg(gsum + (int64_t)g * nqp + tid);
+            red[tid][0] = s;
+            for (int w = 1; w < RT / 32; ++w) red[tid][w] = 0.0;
+        }
+        __syncthreads();
     }
     for (int r = tid; r < 2 + a.n_out; r += RT) res[r] = 0.0;
     __syncthreads();
@@ -901,10 +930,20 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
     h->launches++;
 }
 
+// CTAs of the slab reduction: ~512 per-CTA partials each, at most one per 64 partials (the [G][nqp] sums
+// live in the ngrp * nqp doubles behind the partials) and at most 148; KR_RED_CTAS overrides (tuning).
+static int kr_reduce_ctas(int64_t nblk) {
+    const int64_t ngrp = (nblk + 63) / 64;
+    int64_t g = (nblk + 511) / 512;
+    if (const char* e = getenv("KR_RED_CTAS")) g = atoi(e);
+    g = std::min<int64_t>(std::min<int64_t>(g, 148), ngrp);
+    return (int)std::max<int64_t>(1, g);
+}
+
 // The slab reduction (+ scalar update when fin) after a step / init launch on slab sl.
 static void reduce_launch(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf) {
     StepArgs a = make_args(h, sl, dl, nxt, step, init, write, gather_buf);
-    lz_reduce_kernel<<<1, RT, 0, h->stream>>>(a, sl.nblk);
+    lz_reduce_kernel<<<kr_reduce_ctas(sl.nblk), RT, 0, h->stream>>>(a, sl.nblk);
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }
