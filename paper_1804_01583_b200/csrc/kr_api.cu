@@ -924,6 +924,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 h->halo_inkernel = true;
             }
             kr_lz_encode_maps(h);
+            kr_lz_setup_compact(h);
             kr_lz_prepare(h);
             const int R_total = (int)h->slabs.size() * h->world;
             h->d_rankvec = reinterpret_cast<double*>(dalloc(h, (size_t)R_total * h->nq * 8));

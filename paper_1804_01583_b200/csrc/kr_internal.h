@@ -88,6 +88,19 @@ struct Slab {
     int64_t nitems;      // work items = gx * gy * z-chunks
     dim3 grid;
     int zchunk;
+    // Compact start vector u_1 of an analytic (box / all-grid) generator, per local direction: only the
+    // generator box clipped to this slab's buffer planes is stored (cells x0 .. x0+w, y0 .. y0+h, buffer
+    // planes p0 .. p0+d); the step kernels read it through tensor maps over that small array with shifted
+    // coordinates, and TMA's out-of-bounds zero fill supplies every other cell (exact: u_1 is 0 there).
+    struct CompactU1 {
+        bool on = false;
+        int64_t x0 = 0, y0 = 0, p0 = 0, w = 1, h = 1, d = 1, pitch = 2;
+        CUtensorMap tmC, tmP;
+        int32_t ix0 = 0, iy0 = 0, iz0 = 0, gx = 0, gy = 0;  // init-pass work items: tiles around the box only
+        int64_t nitems = 0;
+    };
+    std::vector<CompactU1> cu1;  // [local direction]
+    double* g1 = nullptr;        // compact u_1 buffer (largest region over the directions)
 };
 
 struct SlabInfo {  // device-visible copy for the local-reduce sparse gather
@@ -252,6 +265,7 @@ void kr_fill_dense(cudaStream_t s, double* dst, int64_t N, int64_t n, int64_t mx
 
 // fused Lanczos
 void kr_lz_encode_maps(kr_handle* h);
+void kr_lz_setup_compact(kr_handle* h);
 void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events);
 size_t kr_lz_step_smem(int TX, int TY);
 

@@ -101,6 +101,15 @@ struct StepArgs {
     int32_t* keff_out;
     LzScalars* scw;          // writable scalars (same as sc)
     DVec gen;                // init pass with an analytic generator (box / all): fill u_1 in the same pass
+    // compact u_1 (Slab::CompactU1): TMA coordinates of the u_i ("C") / u_{i-1} ("P") maps are shifted by
+    // these buffer-coordinate origins (0 for the full state buffers); work items start at tile (ix0, iy0)
+    // and z-chunk iz0 (0 except for the init pass over the box region)
+    int32_t shC[3], shP[3];
+    int32_t ix0, iy0, iz0;
+    // sparse output rows gathered from the compact u_1 (init pass) instead of gather_u
+    const double* gc;
+    int32_t gcx0, gcy0, gcp0, gcw, gch, gcd;
+    int64_t gcpitch;
 };
 
 template <int NT>
@@ -145,8 +154,8 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         unsigned char* st = smem + s * G::STAGE;
         const bool lp = has_prev && p > pfirst && p < plast;  // u_{i-1} is needed on planes zc0..zc1 only
         mbar_expect_tx(&bar[s], G::CBYTES + (lp ? G::PBYTES : 0));
-        tma_load_3d(st, tmC, x0 - 2, y0 - 1, p + 1, &bar[s]);  // x start must be 16-byte aligned
-        if (lp) tma_load_3d(st + G::POFF, tmP, x0, y0, p + 1, &bar[s]);
+        tma_load_3d(st, tmC, x0 - 2 - a.shC[0], y0 - 1 - a.shC[1], p + 1 - a.shC[2], &bar[s]);  // x start 16-byte aligned
+        if (lp) tma_load_3d(st + G::POFF, tmP, x0 - a.shP[0], y0 - a.shP[1], p + 1 - a.shP[2], &bar[s]);
     };
     if (tid == 0) {
         const int np = min(plast - pfirst + 1, S);
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(Geo<TX, TY>::NT, (TX * TY >= 2048) ? 1 : ((TX 
     // Persistent CTAs: work items (x-tile, y-tile, z-chunk) are dealt round-robin (fixed assignment,
     // deterministic); consecutive items run concurrently, so neighbouring tiles share halo planes in L2.
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
-        const int xt = item % a.gx, yt = (item / a.gx) % a.gy, zt = item / (a.gx * a.gy);
+        const int xt = a.ix0 + item % a.gx, yt = a.iy0 + (item / a.gx) % a.gy, zt = a.iz0 + item / (a.gx * a.gy);
         const int x0 = xt * TX, y0 = yt * TY;
         const int zc0 = zt * a.zchunk;
         const int zc1 = min(zc0 + a.zchunk, a.nz);
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(RT) lz_reduce_kernel(const StepArgs a, int64_t
             res[2 + a.box_slot[tid - 2]] = s * a.box_val[tid - 2];
     }
     __syncthreads();
-    if (a.gather_u) {  // sparse output rows from the freshly written vector (owned planes)
+    if (a.gather_u || a.gc) {  // sparse output rows from the freshly written vector (owned planes)
         __shared__ double gred[RT / 32];
         const int64_t mxy = (int64_t)a.mx * a.my;
         for (int r = 0; r < a.n_out; ++r) {
@@ -590,7 +599,14 @@ __global__ void __launch_bounds__(RT) lz_reduce_kernel(const StepArgs a, int64_t
                 const int64_t z = idx / mxy, rem = idx - z * mxy;
                 const int64_t y = rem / a.mx, x = rem - y * a.mx;
                 const int64_t zl = z - a.zoff;
-                if (zl >= 0 && zl < a.nz) t += o.val[e] * a.gather_u[(zl + 1) * a.plane + y * a.pitch + x];
+                if (zl < 0 || zl >= a.nz) continue;
+                if (a.gc) {  // compact u_1: zero outside the stored region
+                    const int64_t cx_ = x - a.gcx0, cy_ = y - a.gcy0, cp_ = zl + 1 - a.gcp0;
+                    if (cx_ >= 0 && cx_ < a.gcw && cy_ >= 0 && cy_ < a.gch && cp_ >= 0 && cp_ < a.gcd)
+                        t += o.val[e] * a.gc[(cp_ * a.gch + cy_) * a.gcpitch + cx_];
+                } else {
+                    t += o.val[e] * a.gather_u[(zl + 1) * a.plane + y * a.pitch + x];
+                }
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
@@ -729,6 +745,22 @@ __global__ void __launch_bounds__(Geo<TX, TY>::NT) lz_fillinit_kernel(const Step
     lz_epilogue<G::NT>(a, acc, red_s, a.plane);
 }
 
+// Compact u_1 (Slab::CompactU1): the generator's value on the stored region (indicator of the box clipped
+// to the grid; cells beyond the grid or the row length are 0, like the Dirichlet ghosts of the full maps).
+__global__ void lz_fill_compact_kernel(double* g, int64_t x0, int64_t y0, int64_t p0, int64_t w, int64_t hh, int64_t d,
+                                       int64_t pitch, int64_t zoff, int64_t mx, int64_t my, int64_t mz, DVec gen) {
+    const int64_t tot = pitch * hh * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cx = e % pitch, cy = (e / pitch) % hh, cp = e / (pitch * hh);
+        const int64_t X = x0 + cx, Y = y0 + cy, Z = zoff + p0 + cp - 1;  // buffer plane p <-> z = zoff + p - 1
+        bool in = cx < w && X < mx && Y < my && Z >= 0 && Z < mz;
+        if (gen.kind == KR_VEC_BOX)
+            in = in && X >= gen.lo[0] && X < gen.hi[0] && Y >= gen.lo[1] && Y < gen.hi[1] && Z >= gen.lo[2] &&
+                 Z < gen.hi[2];
+        g[e] = in ? gen.value : 0.0;
+    }
+}
+
 __global__ void lz_reset(LzScalars* sc) {
     if (threadIdx.x == 0) {
         sc->done = 0;
@@ -790,6 +822,69 @@ void kr_lz_encode_maps(kr_handle* h) {
         }
 }
 
+// Compact u_1 for analytic generators (box / all-grid): the stored region is the generator box clipped
+// to the slab's buffer planes, x start even (16-byte aligned TMA starts), at least one TMA box in x and y.
+// Skipped (full fill + init pass instead) for sparse generators, for regions above max(1/8 of a state
+// buffer, 8 MB) and with KR_NO_COMPACT=1.
+void kr_lz_setup_compact(kr_handle* h) {
+    const bool off = getenv("KR_NO_COMPACT") != nullptr;
+    const int ndl = (int)h->my_dirs.size();
+    auto clip = [](int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); };
+    for (auto& sl : h->slabs) {
+        sl.cu1.assign(ndl, Slab::CompactU1{});
+        int64_t maxe = 0;
+        for (int dl = 0; dl < ndl; ++dl) {
+            Slab::CompactU1& c = sl.cu1[dl];
+            const DVec& g = h->dirs_h[h->my_dirs[dl]];
+            if (off || (g.kind != KR_VEC_BOX && g.kind != KR_VEC_ALL)) continue;
+            const bool all = g.kind == KR_VEC_ALL;
+            const int64_t lx = all ? 0 : clip(g.lo[0], 0, h->mx), hx = all ? h->mx : clip(g.hi[0], 0, h->mx);
+            const int64_t ly = all ? 0 : clip(g.lo[1], 0, h->my), hy = all ? h->my : clip(g.hi[1], 0, h->my);
+            const int64_t lz = all ? 0 : clip(g.lo[2], 0, h->mz), hz = all ? h->mz : clip(g.hi[2], 0, h->mz);
+            // buffer plane p holds z = z0 + p - 1, p = 0 .. nz + 2
+            const int64_t p_lo = std::max<int64_t>(lz, sl.z0 - 1) - sl.z0 + 1;
+            const int64_t p_hi = std::min<int64_t>(hz, sl.z0 + sl.nz + 2) - sl.z0 + 1;
+            const bool empty = hx <= lx || hy <= ly || p_hi <= p_lo;
+            c.x0 = empty ? 0 : (lx & ~int64_t(1));
+            c.y0 = empty ? 0 : ly;
+            c.p0 = empty ? 0 : p_lo;
+            c.w = std::max<int64_t>(empty ? 1 : hx - c.x0, h->TX + 4);
+            c.h = std::max<int64_t>(empty ? 1 : hy - c.y0, h->TY + 3);
+            c.d = empty ? 1 : p_hi - p_lo;
+            c.pitch = (c.w + 1) & ~int64_t(1);
+            const int64_t vol = c.pitch * c.h * c.d;
+            if (vol * 8 > std::max<int64_t>((sl.nz + 3) * h->my * h->pitch, (int64_t)8 << 20)) continue;  // 1/8 of a buffer or 8 MB
+            c.on = true;
+            maxe = std::max(maxe, vol);
+            // init-pass work items: tiles / z-chunks meeting the box dilated by one cell towards -x, -y, -z
+            // (those cells' forward edges reach into the box), owned planes only
+            const int64_t zq0 = std::max<int64_t>(0, lz - 1 - sl.z0), zq1 = std::min<int64_t>(sl.nz, hz - sl.z0);
+            if (hx <= lx || hy <= ly || zq1 <= zq0) {
+                c.nitems = 0;
+                c.gx = c.gy = 0;
+            } else {
+                c.ix0 = (int32_t)(std::max<int64_t>(0, lx - 1) / h->TX);
+                c.iy0 = (int32_t)(std::max<int64_t>(0, ly - 1) / h->TY);
+                c.iz0 = (int32_t)(zq0 / sl.zchunk);
+                c.gx = (int32_t)((hx - 1) / h->TX) - c.ix0 + 1;
+                c.gy = (int32_t)((hy - 1) / h->TY) - c.iy0 + 1;
+                const int64_t nch = (zq1 - 1) / sl.zchunk - c.iz0 + 1;
+                c.nitems = (int64_t)c.gx * c.gy * nch;
+            }
+        }
+        if (maxe == 0) continue;
+        void* gp = nullptr;
+        if (cudaMalloc(&gp, (size_t)maxe * 8) != cudaSuccess) KR_THROW(KR_ENOMEM, "compact u_1 buffer");
+        h->extra_allocs.push_back(gp);  // freed with the handle
+        sl.g1 = reinterpret_cast<double*>(gp);
+        for (auto& c : sl.cu1) {
+            if (!c.on) continue;
+            encode(&c.tmC, sl.g1, c.w, c.h, c.d, c.pitch, h->TX + 4, h->TY + 3);
+            encode(&c.tmP, sl.g1, c.w, c.h, c.d, c.pitch, h->TX + 2, h->TY + 1);
+        }
+    }
+}
+
 template <int TX, int TY, bool INIT, bool BC, bool HALO = false>
 static void set_smem_attr() {
     KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, Stages<TX, TY>::S, INIT, BC, HALO>,
@@ -823,7 +918,9 @@ int kr_lz_occupancy(int TX, int TY) {
 
 void kr_lz_prepare(kr_handle* h) { (void)kr_lz_occupancy(h->TX, h->TY); }
 
-static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf) {
+// cmode: 0 = full state buffers; 1 = u_i is the compact u_1 (init pass / step 1); 2 = u_{i-1} is (step 2)
+static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf,
+                          int cmode = 0) {
     StepArgs a{};
     LzScalars* sc = h->d_sc + dl;
     const int k = h->k;
@@ -893,37 +990,64 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     a.beta0_out = h->d_beta0 + dl;
     a.hnext_out = h->d_hnext + dl;
     a.keff_out = h->d_keff + dl;
+    if (cmode) {
+        const Slab::CompactU1& c = sl.cu1[dl];
+        int32_t* sh = cmode == 1 ? a.shC : a.shP;
+        sh[0] = (int32_t)c.x0;
+        sh[1] = (int32_t)c.y0;
+        sh[2] = (int32_t)c.p0;
+        if (cmode == 1 && init) {  // the init pass only visits the tiles around the box
+            a.ix0 = c.ix0;
+            a.iy0 = c.iy0;
+            a.iz0 = c.iz0;
+            a.gx = c.gx;
+            a.gy = c.gy;
+            a.nitems = (int)c.nitems;
+            if (a.gather_u) {
+                a.gather_u = nullptr;
+                a.gc = sl.g1;
+                a.gcx0 = (int32_t)c.x0;
+                a.gcy0 = (int32_t)c.y0;
+                a.gcp0 = (int32_t)c.p0;
+                a.gcw = (int32_t)c.w;
+                a.gch = (int32_t)c.h;
+                a.gcd = (int32_t)c.d;
+                a.gcpitch = c.pitch;
+            }
+        }
+    }
     return a;
 }
 
 template <int TX, int TY>
 static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int nxt, int step, bool init,
-                          bool write, bool fillinit) {
+                          bool write, bool fillinit, int cmode) {
     const size_t smem = step_smem_bytes<TX, TY, Stages<TX, TY>::S>();
     if (fillinit) {
         StepArgs a = make_args(h, sl, dl, cur, 0, true, false, cur);
         a.gen = h->dirs_h[h->my_dirs[dl]];
         lz_fillinit_kernel<TX, TY><<<sl.grid, Geo<TX, TY>::NT, 0, h->stream>>>(a);
     } else {
-        StepArgs a = make_args(h, sl, dl, nxt, step, init, write, init ? cur : (write ? nxt : -1));
-        const CUtensorMap& tc = sl.tmC[cur];
-        const CUtensorMap& tp = sl.tmP[prev < 0 ? cur : prev];
+        StepArgs a = make_args(h, sl, dl, nxt, step, init, write, init ? cur : (write ? nxt : -1), cmode);
+        const CUtensorMap& tc = cmode == 1 ? sl.cu1[dl].tmC : sl.tmC[cur];
+        const CUtensorMap& tp = cmode == 2 ? sl.cu1[dl].tmP : sl.tmP[prev < 0 ? cur : prev];
+        const dim3 grid = (cmode == 1 && init) ? dim3((unsigned)std::max<int64_t>(1, sl.cu1[dl].nitems), 1, 1) : sl.grid;
         constexpr int S = Stages<TX, TY>::S;
         const bool halo = a.rlo || a.rhi;  // this slab writes halo planes into a neighbour's buffer
         if (h->gen_bc) {
             if (init)
-                lz_step_kernel<TX, TY, S, true, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, true, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else if (halo)
-                lz_step_kernel<TX, TY, S, false, true, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, true, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else
-                lz_step_kernel<TX, TY, S, false, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
         } else {
             if (init)
-                lz_step_kernel<TX, TY, S, true, false><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, true, false><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else if (halo)
-                lz_step_kernel<TX, TY, S, false, false, true><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, false, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
             else
-                lz_step_kernel<TX, TY, S, false, false><<<sl.grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel<TX, TY, S, false, false><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
         }
     }
     KR_CUDA(cudaGetLastError());
@@ -941,23 +1065,26 @@ static int kr_reduce_ctas(int64_t nblk) {
 }
 
 // The slab reduction (+ scalar update when fin) after a step / init launch on slab sl.
-static void reduce_launch(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf) {
-    StepArgs a = make_args(h, sl, dl, nxt, step, init, write, gather_buf);
-    lz_reduce_kernel<<<kr_reduce_ctas(sl.nblk), RT, 0, h->stream>>>(a, sl.nblk);
+static void reduce_launch(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf,
+                          int cmode = 0) {
+    StepArgs a = make_args(h, sl, dl, nxt, step, init, write, gather_buf, cmode);
+    // partial-sum slots = CTAs of the step launch (the compact init pass runs on the box's tiles only)
+    const int64_t nblk = (cmode == 1 && init) ? std::max<int64_t>(1, sl.cu1[dl].nitems) : sl.nblk;
+    lz_reduce_kernel<<<kr_reduce_ctas(nblk), RT, 0, h->stream>>>(a, nblk);
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }
 
 static void step_launch(kr_handle* h, Slab& sl, int dl, int cur, int prev, int nxt, int step, bool init, bool write,
-                        bool fillinit = false) {
+                        bool fillinit = false, int cmode = 0) {
     if (h->TX == 64 && h->TY == 16)
-        step_launch_t<64, 16>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
+        step_launch_t<64, 16>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else if (h->TX == 64 && h->TY == 32)
-        step_launch_t<64, 32>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
+        step_launch_t<64, 32>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else if (h->TX == 64 && h->TY == 8)
-        step_launch_t<64, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
+        step_launch_t<64, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else if (h->TX == 32 && h->TY == 8)
-        step_launch_t<32, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit);
+        step_launch_t<32, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else
         KR_THROW(KR_EINVAL, "unsupported tile");
 }
@@ -1015,15 +1142,32 @@ void kr_lz_enqueue_init(kr_handle* h, int dl) {
     h->launches++;
     // u_1 = v_d on every slab including halo planes (analytic: no exchange needed); init pass: beta0,
     // alpha_1, P_{.,1}. Box/all generators: one fused fill+init pass; sparse: fill then the init pass.
+    // Compact u_1 (analytic generator, small box): store only the box region; the init pass visits only
+    // the tiles around it, and steps 1 and 2 read u_1 through the shifted compact tensor maps (TMA zero
+    // fill elsewhere) — no 8n-byte fill pass, no full read of u_1.
     const DVec& g = h->dirs_h[d];
-    if (g.kind == KR_VEC_BOX || g.kind == KR_VEC_ALL) {
-        for (auto& sl : h->slabs) step_launch(h, sl, dl, 0, -1, 0, 0, true, false, true);
-    } else {
-        for (auto& sl : h->slabs)
+    for (auto& sl : h->slabs) {
+        const bool cmp = !sl.cu1.empty() && sl.cu1[dl].on;
+        if (cmp) {
+            const Slab::CompactU1& c = sl.cu1[dl];
+            const int64_t tot = c.pitch * c.h * c.d;
+            const unsigned nb = (unsigned)std::min<int64_t>((tot + 255) / 256, 4096);
+            lz_fill_compact_kernel<<<nb, 256, 0, h->stream>>>(sl.g1, c.x0, c.y0, c.p0, c.w, c.h, c.d, c.pitch, sl.z0,
+                                                              h->mx, h->my, h->mz, g);
+            KR_CUDA(cudaGetLastError());
+            h->launches++;
+            step_launch(h, sl, dl, 0, -1, 0, 0, true, false, false, 1);
+        } else if (g.kind == KR_VEC_BOX || g.kind == KR_VEC_ALL) {
+            step_launch(h, sl, dl, 0, -1, 0, 0, true, false, true);
+        } else {
             kr_fill_grid(h->stream, sl.u[0], h->mx, h->my, h->pitch, sl.nz + 3, sl.z0 - 1, h->mz, g, &h->launches);
-        for (auto& sl : h->slabs) step_launch(h, sl, dl, 0, -1, 0, 0, true, false);
+            step_launch(h, sl, dl, 0, -1, 0, 0, true, false);
+        }
     }
-    for (auto& sl : h->slabs) reduce_launch(h, sl, dl, 0, 0, true, false, 0);
+    for (auto& sl : h->slabs) {
+        const bool cmp = !sl.cu1.empty() && sl.cu1[dl].on;
+        reduce_launch(h, sl, dl, 0, 0, true, false, 0, cmp ? 1 : 0);
+    }
     combine_and_finalize(h, dl, 0);
 }
 
@@ -1035,7 +1179,10 @@ void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events) {
     const bool write = i < k;
     const bool ev = capture_events && dl == 0 && (size_t)(2 * i) <= h->ev.size();
     if (ev) KR_CUDA(kr_event_record(h->ev[2 * i - 2], h->stream));
-    for (auto& sl : h->slabs) step_launch(h, sl, dl, cur, prev, nxt, i, false, write);
+    for (auto& sl : h->slabs) {
+        const bool cmp = !sl.cu1.empty() && sl.cu1[dl].on && i <= 2;  // u_1 compact: u_i at step 1, u_{i-1} at 2
+        step_launch(h, sl, dl, cur, prev, nxt, i, false, write, false, cmp ? i : 0);
+    }
     if (ev) KR_CUDA(kr_event_record(h->ev[2 * i - 1], h->stream));
     for (auto& sl : h->slabs) reduce_launch(h, sl, dl, nxt, i, false, write, write ? nxt : -1);
     if (write && !h->halo_inkernel) {  // message transport: copies / NCCL send-recv after the step

@@ -260,3 +260,29 @@ def test_state_buffers_need_only_ghost_planes_zeroed(vs, monkeypatch):
     with KrylovReach(p, virtual_slabs=vs) as h:
         b1, _ = h.project()
     assert np.array_equal(a1, a2) and np.array_equal(a1, b1)
+
+
+@pytest.mark.parametrize("vs", [0, 2, 3])
+@pytest.mark.parametrize("lo,hi", [((0, 0, 0), (6, 5, 4)), ((37, 11, 9), (52, 20, 30)), ((71, 30, 0), (80, 40, 3)),
+                                   ((13, 0, 14), (14, 1, 15))])
+def test_compact_start_vector(lo, hi, vs, monkeypatch):
+    """Box generators store only the box region of u_1 (compact tensor maps, TMA zero fill elsewhere;
+    the init pass visits the box's tiles only; steps 1-2 read u_1 through the shifted maps). Boxes at a
+    corner, in the interior with an odd x start, on the high x / y / low z faces and a single cell; one and
+    several slabs (boxes inside one slab or crossing slab boundaries; a box outside a slab's planes).
+    Equal to the full fill + init pass (KR_NO_COMPACT=1) and to the oracle, incl. sparse and box output
+    rows that meet the box (the init pass gathers P_{.,1} from the compact u_1)."""
+    p = W.heat(80, 4, 20, n_steps=40, step=0.02, my=40, mz=30)
+    p["gens"] = [W.box(lo, hi, 1.0)]
+    inside = (lo[0] + (hi[0] - lo[0]) // 2, lo[1] + (hi[1] - lo[1]) // 2, lo[2] + (hi[2] - lo[2]) // 2)
+    idx = lambda x, y, z: x + 80 * (y + 40 * z)  # noqa: E731
+    p["outs"] += [W.sparse([idx(*inside), idx(lo[0], lo[1], lo[2]), idx(max(lo[0] - 1, 0), lo[1], lo[2])],
+                           [1.0, -0.5, 2.0]),
+                  W.box(lo, (hi[0], hi[1], min(hi[2], lo[2] + 2)), 0.25)]
+    kw = dict(virtual_slabs=vs, part="zslab") if vs else {}
+    a, sa, _, _ = gpu_run(p, **kw)
+    monkeypatch.setenv("KR_NO_COMPACT", "1")
+    b, sb, _, _ = gpu_run(p, **kw)
+    assert [s["k_eff"] for s in sa] == [s["k_eff"] for s in sb]
+    assert_coeff(a, b, f"compact vs full u_1 {lo}-{hi} vs={vs}")
+    assert_coeff(a, oracle.krylov_project(p)["coeff"], f"compact u_1 {lo}-{hi} vs={vs} vs oracle")
