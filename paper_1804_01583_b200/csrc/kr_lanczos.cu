@@ -157,7 +157,9 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         tma_load_3d(st, tmC, x0 - 2 - a.shC[0], y0 - 1 - a.shC[1], p + 1 - a.shC[2], &bar[s]);  // x start 16-byte aligned
         if (lp) tma_load_3d(st + G::POFF, tmP, x0 - a.shP[0], y0 - a.shP[1], p + 1 - a.shP[2], &bar[s]);
     };
-    if (tid == 0) {
+    // TMA loads are issued by lane 0 of the last warp: warps 0-2 carry the forward-ring cells
+    constexpr int ISSUER = G::NT - 32;
+    if (tid == ISSUER) {
         const int np = min(plast - pfirst + 1, S);
         for (int p = pfirst; p < pfirst + np; ++p) issue(p);
     }
@@ -220,8 +222,10 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         }
     }
 
-    double up[G::TS], uc[G::TS], wp[G::TS];
-    double rup = 0.0, ruc = 0.0;
+    // u of three consecutive planes per tile slot (and ring cell) in three register sets that take turns as
+    // u_{q-1}, u_q, u_{q+1}: the plane loop is unrolled by three, so no register moves rotate them
+    double R0[G::TS], R1[G::TS], R2[G::TS];
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
     mbar_wait(&bar[0], 0);
     mbar_wait(&bar[1 % S], 0);
     {
@@ -229,20 +233,22 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         const double* C1 = reinterpret_cast<const double*>(smem + (1 % S) * G::STAGE);
 #pragma unroll
         for (int m = 0; m < G::TS; ++m) {
-            up[m] = C0[ci0 + m * RS * G::CW];
-            uc[m] = C1[ci0 + m * RS * G::CW];
-            wp[m] = 0.0;
+            R0[m] = C0[ci0 + m * RS * G::CW];
+            R1[m] = C1[ci0 + m * RS * G::CW];
         }
         if (has_ring) {
-            rup = C0[rci];
-            ruc = C1[rci];
+            r0 = C0[rci];
+            r1 = C1[rci];
         }
     }
     double acc_ww = 0.0, acc_d = 0.0, acc_sum = 0.0;
     // plane q lives in stage sq; plane q+1 in stage sn with mbarrier phase ph (incremental, no modulo)
     int sq = 1 % S, sn = 2 % S;
     uint32_t ph = (2 / S) & 1;
-    for (int q = zc0; q <= zc1; ++q) {
+    // one plane q: w on the tile + forward ring (into the W buffer of q's parity), then the products of plane
+    // q-1 (w of q-1 is re-read from its W buffer); up / uc hold u_{q-1} / u_q, un receives u_{q+1}
+    auto plane = [&](const double (&up)[G::TS], const double (&uc)[G::TS], double (&un)[G::TS], const double rup,
+                     const double ruc, double& run, const int q) {
         mbar_wait(&bar[sn], ph);
         const unsigned char* stq = smem + sq * G::STAGE;
         const double* Cq = reinterpret_cast<const double*>(stq) + ci0;
@@ -258,14 +264,14 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
 #pragma unroll
         for (int m = 0; m < G::TS; ++m) {
             const int o = m * RS * G::CW;
-            const double un = Cn[o];
+            un[m] = Cn[o];
             double w;
             if (INIT) {
                 w = uc[m];
             } else {
                 const double sx = Cq[o - 1] + Cq[o + 1];
                 const double sy = Cq[o - G::CW] + Cq[o + G::CW];
-                const double sz = up[m] + un;
+                const double sz = up[m] + un[m];
                 double dg = dgz;
                 if (BCY) {
                     const int gy = y0 + ty + m * RS;
@@ -276,29 +282,30 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 if (has_prev) w = fma(-sp, Pq[m * RS * G::PW], w);
             }
             if (!FULL && !ing[m]) w = 0.0;
-            if (!zin) w = 0.0;
             Wq[m * RS * G::WW] = w;
             wc[m] = w;
-            up[m] = uc[m];
-            uc[m] = un;
         }
         if (has_ring) {
             const double* Cqb = reinterpret_cast<const double*>(stq);
-            const double un = reinterpret_cast<const double*>(smem + sn * G::STAGE)[rci];
+            run = reinterpret_cast<const double*>(smem + sn * G::STAGE)[rci];
             double w = ruc;
             if (!INIT) {
                 const double sx = Cqb[rci - 1] + Cqb[rci + 1];
                 const double sy = Cqb[rci - G::CW] + Cqb[rci + G::CW];
-                const double sz = rup + un;
+                const double sz = rup + run;
                 const double rdg = BC ? dgz + ex - rexy : diag;  // dgz holds this thread's ex: swap in the ring's
                 const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -rdg * ruc)));
                 w = fma(sa, Au, -sb * ruc);
                 if (has_prev) w = fma(-sp, reinterpret_cast<const double*>(stq + G::POFF)[rpi], w);
             }
-            if ((!FULL && !ring_in) || !zin) w = 0.0;
+            if (!FULL && !ring_in) w = 0.0;
             ((q & 1) ? Wb1 : Wb0)[rwi] = w;
-            rup = ruc;
-            ruc = un;
+        }
+        // the plane above the global grid is a zero ghost: its w enters only as the z+1 neighbour of the last
+        // owned plane (its W plane and ring values are never read), so one uniform branch replaces a select per cell
+        if (!zin) {
+#pragma unroll
+            for (int m = 0; m < G::TS; ++m) wc[m] = 0.0;
         }
         if (q > zc0) {  // products for plane q-1 (its w neighbours at x+1, y+1 were written last iteration)
             const double* Wp = ((q & 1) ? Wb0 : Wb1) + wi0;
@@ -310,10 +317,12 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 for (int r = 0; r < a.nbox; ++r)
                     if (gzp >= a.box[r].lo[2] && gzp < a.box[r].hi[2]) zmask |= 1u << r;
             const bool wr = !INIT && a.write_out;
+            double wp[G::TS];
 #pragma unroll
             for (int m = 0; m < G::TS; ++m) {
                 const int o = m * RS * G::WW;
-                const double w0 = wp[m];
+                const double w0 = Wp[o];
+                wp[m] = w0;
                 const double dx = Wp[o + 1] - w0;
                 const double dy = Wp[o + G::WW] - w0;
                 const double dz = wc[m] - w0;
@@ -323,13 +332,18 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 acc_d = fma(kx, dx * dx, fma(ky, dy * dy, fma(kz, dz * dz, fma(g, w2, acc_d))));
                 acc_ww += w2;
                 acc_sum += w0;
-                const uint32_t mk = bm[m] & zmask;
-                if (mk) {
-#pragma unroll
-                    for (int r = 0; r < KR_MAX_BOX; ++r)
-                        if ((mk >> r) & 1u) acc[3 + r] += w0;
-                }
                 if (wr && (FULL || ing[m])) optr[m * rowstep] = w0;
+            }
+            if (zmask) {  // box output rows meeting this tile and plane (uniform, rare)
+#pragma unroll
+                for (int m = 0; m < G::TS; ++m) {
+                    const uint32_t mk = bm[m] & zmask;
+                    if (mk) {
+#pragma unroll
+                        for (int r = 0; r < KR_MAX_BOX; ++r)
+                            if ((mk >> r) & 1u) acc[3 + r] += wp[m];
+                    }
+                }
             }
             // halo planes for the neighbours, stored where they will be read (uniform per plane, rare):
             // owned planes 0, 1 -> the lower neighbour, the last owned plane -> the upper neighbour
@@ -345,10 +359,8 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
             }
             optr += a.plane;
         }
-#pragma unroll
-        for (int m = 0; m < G::TS; ++m) wp[m] = wc[m];
         __syncthreads();
-        if (tid == 0) {
+        if (tid == ISSUER) {
             if (q == zc0 && pfirst + S <= plast) issue(pfirst + S);
             if (q + S <= plast) issue(q + S);
         }
@@ -357,6 +369,14 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
             sn = 0;
             ph ^= 1u;
         }
+    };
+    for (int q = zc0;;) {
+        plane(R0, R1, R2, r0, r1, r2, q);
+        if (++q > zc1) break;
+        plane(R1, R2, R0, r1, r2, r0, q);
+        if (++q > zc1) break;
+        plane(R2, R0, R1, r2, r0, r1, q);
+        if (++q > zc1) break;
     }
     acc[0] += acc_ww;
     acc[1] += acc_d;
