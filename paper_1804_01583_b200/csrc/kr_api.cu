@@ -105,7 +105,16 @@ RowsCsr merged_rows(const kr_problem* p) {
     for (int64_t r = 0; r < p->n; ++r) {
         row.clear();
         for (int64_t e = p->row_ptr[r]; e < p->row_ptr[r + 1]; ++e) row.push_back({p->col_idx[e], p->val[e]});
-        std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        if (row.size() > 32) {
+            std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        } else {  // stable insertion sort: no temporary buffer for the typical short row
+            for (size_t i = 1; i < row.size(); ++i) {
+                const auto x = row[i];
+                size_t j = i;
+                for (; j > 0 && row[j - 1].first > x.first; --j) row[j] = row[j - 1];
+                row[j] = x;
+            }
+        }
         for (size_t i = 0; i < row.size();) {
             size_t j = i;
             double acc = 0.0;
@@ -173,23 +182,42 @@ double gershgorin_mu(const kr_problem* p) {
         }
         return mu;
     }
+    // s_rc = (a_rc + a_cr) / 2 over the merged rows (ascending columns, duplicates summed): each stored entry
+    // (r, c) finds its mirror a_cr by binary search in row c; an entry without a stored mirror also carries
+    // the radius term of row c (whose row has no (c, r) entry to visit). O(nnz log row length), no transpose.
     const int64_t n = p->n, N = n + (p->b ? 1 : 0);
-    const RowsCsr a = merged_rows(p);
-    const RowsCsr t = transpose_rows(a, n);
+    // rows already strictly ascending (no duplicates) are used in place; otherwise merged copies
+    bool sorted = true;
+    for (int64_t r = 0; r < n && sorted; ++r)
+        for (int64_t e = p->row_ptr[r] + 1; e < p->row_ptr[r + 1]; ++e)
+            if (p->col_idx[e] <= p->col_idx[e - 1]) {
+                sorted = false;
+                break;
+            }
+    RowsCsr m;
+    if (!sorted) m = merged_rows(p);
+    auto rp = [&](int64_t r) { return sorted ? p->row_ptr[r] : m.rp[(size_t)r]; };
+    auto col = [&](int64_t e) { return sorted ? (int64_t)p->col_idx[e] : m.ci[(size_t)e]; };
+    auto val = [&](int64_t e) { return sorted ? p->val[e] : m.v[(size_t)e]; };
     std::vector<double> diag(N, 0.0), rad(N, 0.0);
-    for (int64_t r = 0; r < n; ++r) {  // merge row r of A and of A^T: s_rc = (a_rc + a_cr) / 2
-        int64_t i = a.rp[(size_t)r], j = t.rp[(size_t)r];
-        const int64_t i1 = a.rp[(size_t)r + 1], j1 = t.rp[(size_t)r + 1];
-        while (i < i1 || j < j1) {
-            const int64_t ca = i < i1 ? a.ci[(size_t)i] : INT64_MAX, ct = j < j1 ? t.ci[(size_t)j] : INT64_MAX;
-            const int64_t c = std::min(ca, ct);
-            double sv = 0.0;
-            if (ca == c) sv += 0.5 * a.v[(size_t)i++];
-            if (ct == c) sv += 0.5 * t.v[(size_t)j++];
-            if (c == r)
-                diag[(size_t)r] += sv;
-            else
-                rad[(size_t)r] += std::fabs(sv);
+    for (int64_t r = 0; r < n; ++r) {
+        for (int64_t e = rp(r); e < rp(r + 1); ++e) {
+            const int64_t c = col(e);
+            if (c == r) {
+                diag[(size_t)r] += val(e);  // 0.5 a_rr + 0.5 a_rr
+                continue;
+            }
+            int64_t lo = rp(c), hi = rp(c + 1);  // binary search of column r in row c
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (col(mid) < r) lo = mid + 1; else hi = mid;
+            }
+            if (lo < rp(c + 1) && col(lo) == r) {
+                rad[(size_t)r] += std::fabs(0.5 * val(e) + 0.5 * val(lo));
+            } else {
+                rad[(size_t)r] += std::fabs(0.5 * val(e));
+                rad[(size_t)c] += std::fabs(0.5 * val(e));
+            }
         }
         if (p->b && p->b[r] != 0.0) {  // lifted column b and (zero) lifted row: s_{r,n} = s_{n,r} = b_r / 2
             rad[(size_t)r] += std::fabs(0.5 * p->b[r]);
@@ -201,12 +229,27 @@ double gershgorin_mu(const kr_problem* p) {
     return mu;
 }
 
+// Device allocations owned by the handle: requests up to 1 MB are carved (256-byte aligned) from 4 MB
+// chunks, larger ones get their own cudaMalloc — a handle makes a few dozen small allocations, and each
+// cudaMalloc / cudaFree pair costs tens of microseconds to milliseconds of create / destroy time.
 void* dalloc(kr_handle* h, size_t bytes) {
-    if (bytes == 0) bytes = 8;
-    void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) KR_THROW(KR_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
-    h->extra_allocs.push_back(p);
+    constexpr size_t kChunk = size_t(4) << 20;
+    bytes = (std::max<size_t>(bytes, 8) + 255) & ~size_t(255);
+    auto device_alloc = [&](size_t b) {
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) KR_THROW(KR_ENOMEM, "cudaMalloc(" + std::to_string(b) + "): " + cudaGetErrorString(e));
+        h->extra_allocs.push_back(p);
+        return p;
+    };
+    if (bytes > kChunk / 4) return device_alloc(bytes);
+    if (h->arena_used + bytes > h->arena_cap) {
+        h->arena = reinterpret_cast<char*>(device_alloc(kChunk));
+        h->arena_used = 0;
+        h->arena_cap = kChunk;
+    }
+    void* p = h->arena + h->arena_used;
+    h->arena_used += bytes;
     return p;
 }
 
@@ -235,6 +278,14 @@ DVec make_dvec(kr_handle* h, const kr_vec& v) {
         d.hi[a] = v.hi[a];
     }
     if (v.kind == KR_VEC_SPARSE) {
+        bool sorted = true;  // strictly ascending indices (no duplicates): upload as is
+        for (int64_t i = 1; i < v.nnz && sorted; ++i) sorted = v.idx[i] > v.idx[i - 1];
+        if (sorted) {
+            d.nnz = v.nnz;
+            d.idx = upload(h, v.idx, (size_t)v.nnz);
+            d.val = upload(h, v.val, (size_t)v.nnz);
+            return d;
+        }
         std::vector<std::pair<int64_t, double>> e((size_t)v.nnz);
         for (int64_t i = 0; i < v.nnz; ++i) e[i] = {v.idx[i], v.val[i]};
         std::stable_sort(e.begin(), e.end(), [](const auto& a, const auto& b) { return a.first < b.first; });

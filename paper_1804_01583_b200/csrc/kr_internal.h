@@ -161,6 +161,8 @@ struct kr_handle {
     size_t ws_bytes, ws_used;
     bool own_ws;
     std::vector<void*> extra_allocs;
+    char* arena = nullptr;  // small device allocations are carved from 4 MB chunks (dalloc)
+    size_t arena_used = 0, arena_cap = 0;
 
     // descriptors
     std::vector<DVec> dirs_h;          // per global direction: up to 2 pieces (gen/center + lifted one)
