@@ -300,7 +300,7 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
-        per_step = []
+        per_step, per_step2 = [], []
         for _ in range(args.steps):
             cb = one_step()
             t = h.last_timing()
@@ -310,6 +310,7 @@ def main():
             # steps 3..k-1: the launches that move exactly 24 n_local bytes (steps 1-2 read the compact u_1 of
             # the box generator, the last step writes nothing)
             per_step.extend(st_ms[2:-1] if len(st_ms) > 3 else st_ms)
+            per_step2.extend(st_ms[1:-1] if len(st_ms) > 2 else st_ms)  # steps 2..k-1
         ev1.record(stream)
         barrier()
     launches = h.launch_count() - l0
@@ -338,27 +339,37 @@ def main():
     # project (D2H of all coefficients) -> check_box (D2H of bounds + counter-example) -> destroy.
     e2e = None
     if not args.no_e2e:
-        e_ms = []
+        e_ms, parts = [], []
         h2d = d2h = 0
-        for it in range(2):
+        for it in range(4):  # one warm-up call, then the median of three
             barrier()
             t0 = time.perf_counter()
             with KrylovReach(p, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw) as h2:
                 attach(h2)
+                t1 = time.perf_counter()
                 c2, st2 = h2.project()
+                t2 = time.perf_counter()
                 cb2 = h2.check_box()
+                t3 = time.perf_counter()
                 tb = h2.transfer_bytes()
+            t4 = time.perf_counter()
             barrier()
-            e_ms.append((time.perf_counter() - t0) * 1e3)
+            t5 = time.perf_counter()
+            e_ms.append((t5 - t0) * 1e3)
+            parts.append({"create_ms": (t1 - t0) * 1e3, "project_ms": (t2 - t1) * 1e3,
+                          "check_box_ms": (t3 - t2) * 1e3, "destroy_ms": (t4 - t3) * 1e3,
+                          "barrier_ms": (t5 - t4) * 1e3})
             h2d, d2h = tb
-        e_sec = max(e_ms[1:]) / 1e3 if len(e_ms) > 1 else e_ms[0] / 1e3
+        e_sec = float(np.median(e_ms[1:])) / 1e3
         if world > 1:
             tt = torch.tensor([e_sec], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             e_sec = float(tt.item())
         e2e = {"value": k_eff / e_sec, "unit": "Krylov steps/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_sec * 1e3,
-               "note": "wall clock of create+project+check_box+destroy on caller workspace; includes CUDA-graph capture"}
+               "phases_ms": parts[1:],
+               "note": "wall clock of create+project+check_box+destroy on caller workspace, median of 3 calls after one "
+                       "warm-up; includes CUDA-graph capture"}
     h.close()
     if rank != 0:
         if world > 1:
@@ -370,6 +381,7 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(p, world),
         "fused_step": {"gbs": achieved, "pct_of_peak": 100.0 * achieved / peak, "ms_mean": sk,
                        "ms_median_steps_3_to_k-1": float(np.median(per_step)) if per_step else None,
+                       "ms_median_steps_2_to_k-1": float(np.median(per_step2)) if per_step2 else None,
                        "ms_mean_all_steps": float(np.mean(step_ms)),
                        "runs": args.steps,
                        "bytes_per_launch": n_local_bytes, "launches_per_step": timing["step_launches"]},

@@ -13,7 +13,11 @@ from paper_1804_01583_b200 import KrylovReach, krylov_workspace_bytes  # noqa: E
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C5"
 runs = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-p = W.CONFIGS[name]()
+if name.startswith("PAPER:"):  # PAPER:m:k -> the paper's heat model at fixed k (no adaptive checkpoints)
+    _, m, k = name.split(":")
+    p = W.heat_paper(int(m), eps=0.0, k_max=int(k))
+else:
+    p = W.CONFIGS[name]()
 st = torch.cuda.current_stream().cuda_stream
 wsb = krylov_workspace_bytes(p, device=0, stream=st)
 ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
