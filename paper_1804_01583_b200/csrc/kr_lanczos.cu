@@ -370,13 +370,32 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
             ph ^= 1u;
         }
     };
-    for (int q = zc0;;) {
-        plane(R0, R1, R2, r0, r1, r2, q);
-        if (++q > zc1) break;
-        plane(R1, R2, R0, r1, r2, r0, q);
-        if (++q > zc1) break;
-        plane(R2, R0, R1, r2, r0, r1, q);
-        if (++q > zc1) break;
+    // The general-boundary kernel holds five tile variants; unrolling them all overflows the instruction cache
+    // (ncu: 30% of its stall samples "no instructions", a launch 36% slower than the Dirichlet kernel's), so
+    // there only the full interior tiles (almost all tiles) are unrolled and the face tiles rotate their
+    // registers by moves. The Dirichlet kernel (two variants) unrolls both.
+    constexpr bool UNROLL = BCM == 0 || (FULL && BCM == 1);
+    if (UNROLL) {
+        for (int q = zc0;;) {
+            plane(R0, R1, R2, r0, r1, r2, q);
+            if (++q > zc1) break;
+            plane(R1, R2, R0, r1, r2, r0, q);
+            if (++q > zc1) break;
+            plane(R2, R0, R1, r2, r0, r1, q);
+            if (++q > zc1) break;
+        }
+    } else {
+#pragma unroll 1
+        for (int q = zc0; q <= zc1; ++q) {
+            plane(R0, R1, R2, r0, r1, r2, q);
+#pragma unroll
+            for (int m = 0; m < G::TS; ++m) {
+                R0[m] = R1[m];
+                R1[m] = R2[m];
+            }
+            r0 = r1;
+            r1 = r2;
+        }
     }
     acc[0] += acc_ww;
     acc[1] += acc_d;
