@@ -365,6 +365,106 @@ __global__ void __launch_bounds__(ET) expm_doubling_kernel(ExpmArgs a, double* x
     }
 }
 
+// The time grid over many CTAs (default): expm_powers_kernel (one CTA per direction) forms E = e^{H delta}
+// by the Pade-13 scaling and squaring above and its powers E^{2^q}, q < Q (2^{Q-1} <= n_steps < 2^Q), into
+// pw [ndl][Q][64][65]; expm_march_kernel (CTA s of direction d owns the columns [s B, s B + B)) starts from
+// x_{sB} = prod_{bits q of sB} E^{2^q} e_1 (e_1 exactly for s = 0) and marches x_{j+1} = E x_j, with the
+// projection c[j][., d] = ||v_d|| P x_j in the same matrix-vector product ([E; P] x_j, one pass). The one-CTA
+// doubling above serialised ~0.3 ms per direction on one SM (C3); here it is the Pade-13 of one CTA plus a
+// few microseconds.
+constexpr int PW_LD = 65;
+constexpr size_t PW_MAT = (size_t)64 * PW_LD;
+
+__global__ void __launch_bounds__(ET) expm_powers_kernel(ExpmArgs a, double* pw, int Q) {
+    const int d = blockIdx.x;
+    const int n = a.keff[d];
+    if (n <= 0 || a.n_steps < 1) return;
+    const int k = a.k;
+    extern __shared__ double sm[];
+    __shared__ double fac[64];
+    __shared__ int piv_s;
+    __shared__ int sq_s;
+    const int ld = n + 1;
+    const int msz = n * ld;
+    double* E = pade13(a.H + (int64_t)d * (k + 1) * k, k, n, a.step, sm, fac, piv_s, sq_s);
+    const int ei = (int)((E - sm) / msz);
+    double* X = E;
+    double* Y = sm + (size_t)(ei == 0 ? 1 : 0) * msz;
+    double* out = pw + (size_t)d * Q * PW_MAT;
+    for (int q = 0; q < Q; ++q) {
+        for (int e = threadIdx.x; e < n * n; e += ET) {
+            const int r = e / n, c = e - r * n;
+            out[(size_t)q * PW_MAT + r * PW_LD + c] = X[r * ld + c];
+        }
+        if (q + 1 < Q) {
+            mm(X, X, Y, n, ld);
+            __syncthreads();
+            double* t0 = X;
+            X = Y;
+            Y = t0;
+        }
+    }
+}
+
+// y = M x for the rows [0, R) of M (row stride PW_LD, n columns); two threads per row split the columns, added
+// in a fixed order. x, part in shared memory; all threads call it.
+__device__ __forceinline__ void mv_rows(const double* M, int R, int n, const double* x, double* part, double* y) {
+    const int i = threadIdx.x & 127, h = threadIdx.x >> 7;
+    const int half = (n + 1) >> 1;
+    const int l0 = h ? half : 0, l1 = h ? n : half;
+    if (i < R) {
+        double s = 0.0;
+        for (int l = l0; l < l1; ++l) s = fma(M[i * PW_LD + l], x[l], s);
+        part[h * 128 + i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < R) y[threadIdx.x] = part[threadIdx.x] + part[128 + threadIdx.x];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(ET) expm_march_kernel(ExpmArgs a, const double* pw, int Q, int B) {
+    const int d = blockIdx.y;
+    const int n = a.keff[d];
+    const int k = a.k;
+    const int64_t np1 = a.n_steps + 1;
+    const int64_t c0 = (int64_t)blockIdx.x * B, c1 = min(c0 + B, np1);
+    if (c0 >= np1) return;
+    if (n <= 0) {
+        for (int64_t e = threadIdx.x; e < (c1 - c0) * a.n_out; e += ET)
+            a.coeff[((c0 + e / a.n_out) * a.n_out + e % a.n_out) * a.ndl_stride + d] = 0.0;
+        return;
+    }
+    extern __shared__ double sm[];
+    double* M = sm;                                   // [n + n_out][PW_LD]: E, then the rows of P
+    double* xv = M + (size_t)(64 + KR_MAX_OUT) * PW_LD;  // x_j
+    double* yv = xv + 128;                            // [E; P] x_j
+    double* part = yv + 128;                          // [2][128]
+    const double* pwd = pw + (size_t)d * Q * PW_MAT;
+    const double* Pd = a.P + (int64_t)d * a.n_out * k;
+    const int R = n + a.n_out;
+    for (int e = threadIdx.x; e < R * n; e += ET) {
+        const int r = e / n, c = e - r * n;
+        M[r * PW_LD + c] = r < n ? pwd[r * PW_LD + c] : Pd[(int64_t)(r - n) * k + c];
+    }
+    if (threadIdx.x < n) xv[threadIdx.x] = threadIdx.x == 0 ? 1.0 : 0.0;  // x_0 = e_1 exactly
+    __syncthreads();
+    for (int q = 0; q < Q; ++q)  // x_{c0} = prod over the set bits of c0 of E^{2^q}, applied to e_1
+        if ((c0 >> q) & 1) {
+            mv_rows(pwd + (size_t)q * PW_MAT, n, n, xv, part, yv);
+            if (threadIdx.x < n) xv[threadIdx.x] = yv[threadIdx.x];
+            __syncthreads();
+        }
+    const double bz = a.beta0[d];
+    for (int64_t j = c0; j < c1; ++j) {
+        mv_rows(M, R, n, xv, part, yv);  // yv[0..n) = E x_j = x_{j+1}, yv[n + r] = (P x_j)_r
+        if (threadIdx.x < a.n_out) a.coeff[(j * a.n_out + threadIdx.x) * a.ndl_stride + d] = bz * yv[n + threadIdx.x];
+        if (threadIdx.x == 0) a.hlast[(int64_t)d * np1 + j] = xv[n - 1];
+        __syncthreads();
+        if (threadIdx.x < n) xv[threadIdx.x] = yv[threadIdx.x];
+        __syncthreads();
+    }
+}
+
 // Lemma 1: beta0 h_{k+1,k} e^{max(mu,0) T} int_0^T |x_k(t)| dt, trapezoid on the t_j grid. One CTA per
 // direction: each thread sums a contiguous run of trapezoids, the runs are combined in thread order (fixed order,
 // bit-reproducible; a serial per-thread loop over 2000 dependent loads was ~0.25 ms).
@@ -401,7 +501,18 @@ void kr_expm_prepare(kr_handle* h) {
     KR_CUDA(cudaFuncSetAttribute(expm_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KR_CUDA(cudaFuncSetAttribute(expm_doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     h->expm_doubling = getenv("KR_EXPM_PADE") == nullptr;  // KR_EXPM_PADE=1: one Pade-13 per (step, direction)
-    if (h->expm_doubling) {
+    h->expm_onecta = getenv("KR_EXPM_ONECTA") != nullptr;  // KR_EXPM_ONECTA=1: the one-CTA doubling kernel
+    if (h->expm_doubling && !h->expm_onecta) {
+        int Q = 1;
+        while (((int64_t)1 << Q) <= h->n_steps) ++Q;
+        h->pw_q = Q;
+        const size_t ndl = std::max<size_t>(1, h->my_dirs.size());
+        KR_CUDA(cudaMalloc(&h->d_pw, ndl * Q * PW_MAT * sizeof(double)));
+        h->extra_allocs.push_back(h->d_pw);
+        KR_CUDA(cudaFuncSetAttribute(expm_powers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const size_t msm = ((size_t)(64 + KR_MAX_OUT) * PW_LD + 512) * sizeof(double);
+        KR_CUDA(cudaFuncSetAttribute(expm_march_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+    } else if (h->expm_doubling) {
         int ldx = 1;
         while (ldx < h->n_steps + 1) ldx <<= 1;
         h->xt_ld = ldx;
@@ -455,7 +566,18 @@ void kr_expm_enqueue(kr_handle* h) {
     a.step = h->step;
     a.coeff = h->d_coeff_loc;
     a.hlast = h->d_hlast;
-    if (h->expm_doubling)
+    if (h->expm_doubling && !h->expm_onecta) {
+        expm_powers_kernel<<<ndl, ET, smem, h->stream>>>(a, h->d_pw, h->pw_q);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        // columns per CTA: about three CTAs per SM over all directions, at least 8 columns each
+        const int64_t np1 = h->n_steps + 1;
+        int64_t B = std::max<int64_t>(8, (np1 * ndl + 443) / 444);
+        if (const char* e = getenv("KR_EXPM_B")) B = std::max(1, atoi(e));
+        const unsigned nseg = (unsigned)((np1 + B - 1) / B);
+        const size_t msm = ((size_t)(64 + KR_MAX_OUT) * PW_LD + 512) * sizeof(double);
+        expm_march_kernel<<<dim3(nseg, ndl), ET, msm, h->stream>>>(a, h->d_pw, h->pw_q, (int)B);
+    } else if (h->expm_doubling)
         expm_doubling_kernel<<<ndl, ET, smem, h->stream>>>(a, h->d_xt, h->xt_ld);
     else
         expm_project_kernel<<<dim3((unsigned)(h->n_steps + 1), ndl), ET, smem, h->stream>>>(a);

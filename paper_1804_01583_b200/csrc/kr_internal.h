@@ -218,7 +218,10 @@ struct kr_handle {
     void* p2p_base[2] = {nullptr, nullptr};  // opened IPC bases (lower, upper neighbour)
     int32_t p2p_rank = 0, p2p_world = 1;
     bool expm_doubling = false;  // small-k exponentials: doubling over the time grid (else Pade per step)
-    double* d_xt = nullptr;      // doubling trajectories [ndl][64][xt_ld]
+    double* d_xt = nullptr;      // doubling trajectories [ndl][64][xt_ld] (one-CTA doubling, KR_EXPM_ONECTA=1)
+    bool expm_onecta = false;
+    double* d_pw = nullptr;      // powers E^{2^q} of e^{H delta}, [ndl][pw_q][64][65] (multi-CTA march)
+    int pw_q = 0;
     int xt_ld = 0;
     bool large_route;      // exponentials through the large-k route (kr_large.cu) instead of per-step Pade
     // large-k route scratch (allocated at the first project that needs it, for kcap = k)

@@ -304,3 +304,25 @@ def test_compact_start_vector_several_directions(vs):
     res = oracle.krylov_project(p)
     assert [s["k_eff"] for s in stats] == [r["k_eff"] for r in res["per_dir"]]
     assert_coeff(coeff, res["coeff"], f"several directions vs={vs}")
+
+
+@pytest.mark.parametrize("n_steps,B", [(0, None), (1, None), (63, None), (64, None), (1000, None), (1000, "1"),
+                                       (1000, "7"), (1000, "1001")])
+def test_expm_march_equals_one_cta_doubling(n_steps, B, monkeypatch):
+    """The time grid over many CTAs (powers E^{2^q}, each CTA starting from x_{sB} = prod E^{2^q} e_1 and
+    marching x_{j+1} = E x_j with the projection in the same product) agrees with the one-CTA doubling
+    (KR_EXPM_ONECTA=1) and the oracle: grids of 1, 2, 64, 65 and 1001 points, segments of 1, 7, 8+ and all
+    columns; two directions."""
+    p = W.heat(16, 3, 30, n_steps=n_steps, step=0.05, my=12, mz=10)
+    p["gens"].append(W.sparse([W.center_index(16) + 16 * (5 + 12 * 4)], [1.0]))
+    p["z_lo"] = np.array([0.9, -1.0])
+    p["z_hi"] = np.array([1.1, 1.0])
+    if B:
+        monkeypatch.setenv("KR_EXPM_B", B)
+    a, sa, _, _ = gpu_run(p)
+    monkeypatch.setenv("KR_EXPM_ONECTA", "1")
+    b, sb, _, _ = gpu_run(p)
+    assert [s["k_eff"] for s in sa] == [s["k_eff"] for s in sb]
+    assert [s["lemma1"] for s in sa] == pytest.approx([s["lemma1"] for s in sb], rel=1e-9, abs=1e-300)
+    assert_coeff(a, b, f"march vs one-CTA doubling N={n_steps} B={B}")
+    assert_coeff(a, oracle.krylov_project(p)["coeff"], f"march vs oracle N={n_steps} B={B}")
