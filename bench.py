@@ -309,8 +309,10 @@ def main():
             st_ms = h.step_times()
             # steps 3..k-1: the launches that move exactly 24 n_local bytes (steps 1-2 read the compact u_1 of
             # the box generator, the last step writes nothing)
-            per_step.extend(st_ms[2:-1] if len(st_ms) > 3 else st_ms)
-            per_step2.extend(st_ms[1:-1] if len(st_ms) > 2 else st_ms)  # steps 2..k-1
+            # (the library times steps 1, 2 and six steps spread over 3..k-1, NaN elsewhere; every step with
+            # KR_MAX_EV, as for the adaptive runs)
+            per_step.extend(x for x in (st_ms[2:-1] if len(st_ms) > 3 else st_ms) if np.isfinite(x))
+            per_step2.extend(x for x in (st_ms[1:-1] if len(st_ms) > 2 else st_ms) if np.isfinite(x))  # steps 2..k-1
         ev1.record(stream)
         barrier()
     launches = h.launch_count() - l0

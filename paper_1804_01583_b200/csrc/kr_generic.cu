@@ -420,11 +420,12 @@ void kr_ge_enqueue_step(kr_handle* h, int j) {
     const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
     const FaceCor fc = kr_face_cor(h);
     const double* X = h->d_V + (int64_t)(j - 1) * N;
-    const bool evj = h->timing && (size_t)(2 * j) <= h->ev.size();
-    if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1)], h->stream));
+    const int evp = (h->timing && j < (int)h->ev_pair_of_step.size()) ? h->ev_pair_of_step[(size_t)j] : -1;
+    const bool evj = evp >= 0;
+    if (evj) KR_CUDA(kr_event_record(h->ev[2 * evp], h->stream));
     if (h->use_cgs) {  // operator fused into the first CGS2 pass (kr_arnoldi.cu): the events bracket the whole step
         kr_cgs_step(h, j, ndl, h->d_cgs);
-        if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1) + 1], h->stream));
+        if (evj) KR_CUDA(kr_event_record(h->ev[2 * evp + 1], h->stream));
         return;
     }
     if (h->op == KR_OP_CSR) {
@@ -442,7 +443,7 @@ void kr_ge_enqueue_step(kr_handle* h, int j) {
     }
     KR_CUDA(cudaGetLastError());
     h->launches++;
-    if (evj) KR_CUDA(kr_event_record(h->ev[2 * (j - 1) + 1], h->stream));
+    if (evj) KR_CUDA(kr_event_record(h->ev[2 * evp + 1], h->stream));
     launch_ortho(h, j, ndl);
 }
 

@@ -250,7 +250,9 @@ struct kr_handle {
 
     // timing
     bool timing;
-    std::vector<cudaEvent_t> ev;  // pairs around each step kernel
+    std::vector<cudaEvent_t> ev;  // pairs around the step kernel of the timed steps
+    std::vector<int> ev_pair_of_step;  // [k + 1]: event pair of step i, or -1 (step not timed)
+    std::vector<int> ev_step_of_pair;
     cudaEvent_t ev_it0, ev_it1;
     double last_iter_ms, last_step_ms_mean;
     std::vector<double> step_ms;  // per-step device times of the last project (first KR_MAX_EV steps, direction 0)

@@ -890,6 +890,11 @@ void kr_lz_setup_compact(kr_handle* h) {
             c.w = std::max<int64_t>(empty ? 1 : hx - c.x0, h->TX + 4);
             c.h = std::max<int64_t>(empty ? 1 : hy - c.y0, h->TY + 3);
             c.d = empty ? 1 : p_hi - p_lo;
+            // at least 64 rows and planes (where the slab has them): tensor maps of a few planes made the
+            // out-of-bounds boxes slow (measured: a slab whose region was empty, d = 1, took 2x as long for
+            // steps 1-2 as with the full u_1; d >= 64 restores the fast path); the extra cells hold zeros
+            c.h = std::max(c.h, std::min<int64_t>(64, h->my));
+            c.d = std::max(c.d, std::min<int64_t>(64, sl.nz + 3 - c.p0));
             c.pitch = (c.w + 1) & ~int64_t(1);
             const int64_t vol = c.pitch * c.h * c.d;
             if (vol * 8 > std::max<int64_t>((sl.nz + 3) * h->my * h->pitch, (int64_t)8 << 20)) continue;  // 1/8 of a buffer or 8 MB
@@ -1216,13 +1221,14 @@ void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events) {
     const int k = h->k;
     const int cur = (i - 1) % 3, prev = (i >= 2) ? (i - 2) % 3 : -1, nxt = i % 3;
     const bool write = i < k;
-    const bool ev = capture_events && dl == 0 && (size_t)(2 * i) <= h->ev.size();
-    if (ev) KR_CUDA(kr_event_record(h->ev[2 * i - 2], h->stream));
+    const int evp = (capture_events && dl == 0 && i < (int)h->ev_pair_of_step.size()) ? h->ev_pair_of_step[(size_t)i] : -1;
+    const bool ev = evp >= 0;
+    if (ev) KR_CUDA(kr_event_record(h->ev[2 * evp], h->stream));
     for (auto& sl : h->slabs) {
         const bool cmp = !sl.cu1.empty() && sl.cu1[dl].on && i <= 2;  // u_1 compact: u_i at step 1, u_{i-1} at 2
         step_launch(h, sl, dl, cur, prev, nxt, i, false, write, false, cmp ? i : 0);
     }
-    if (ev) KR_CUDA(kr_event_record(h->ev[2 * i - 1], h->stream));
+    if (ev) KR_CUDA(kr_event_record(h->ev[2 * evp + 1], h->stream));
     for (auto& sl : h->slabs) reduce_launch(h, sl, dl, nxt, i, false, write, write ? nxt : -1);
     if (write && !h->halo_inkernel) {  // message transport: copies / NCCL send-recv after the step
         if (h->slabs.size() > 1) halo_exchange_virtual(h, nxt);
