@@ -239,7 +239,8 @@ kr_status krylov_last_timing(const kr_handle* h, double* iter_ms, double* step_k
 /* Per-step device times (ms, CUDA events around the Krylov step's operator/step kernel of local direction 0)
  * of the last krylov_project: ms HOST [cap] or NULL, ms[i] for step i + 1 of the *n steps run. Timed steps:
  * the first min(k, KR_MAX_EV) if that environment variable is set, else steps 1, 2 and six steps spread over
- * 3..k-1 (event nodes around every step cost ~8 us per step in the CUDA graph); other entries are NaN. */
+ * 3..k-1 (k <= 64) or every 16th step from 3 on (k > 64, adaptive runs); event nodes around every step cost
+ * ~8 us per step in the CUDA graph. Other entries are NaN. */
 kr_status krylov_step_times(const kr_handle* h, double* ms, int32_t cap, int32_t* n);
 
 /* Device time in ms spent by the last krylov_project in the large-k exponential route (all checkpoint

@@ -1041,12 +1041,14 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         h->d_thr = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * 8));
         h->timing = true;
         {
-            // timed steps: with KR_MAX_EV = c the first min(k, c) steps (every step of an adaptive trace);
-            // otherwise steps 1, 2 and six steps spread over 3..k-1 — event nodes around every step cost
-            // ~8 us per step inside the CUDA graph (C3: 1.03 -> 0.70 ms per 40-step run without them)
+            // timed steps: with KR_MAX_EV = c the first min(k, c) steps; for k <= 64 steps 1, 2 and six steps
+            // spread over 3..k-1, above (adaptive / large k) steps 1, 2 and every 16th step — event nodes around
+            // every step cost ~8 us per step inside the CUDA graph (C3: 1.03 -> 0.70 ms per 40-step run)
             std::vector<int> steps;
             if (const char* e = getenv("KR_MAX_EV")) {
                 for (int i = 1; i <= std::min(k, std::max(1, atoi(e))); ++i) steps.push_back(i);
+            } else if (k > 64) {  // adaptive / large k: steps 1, 2 and every 16th step from 3 on (clock drifts)
+                for (int i = 1; i <= k; i = i < 3 ? i + 1 : i + 16) steps.push_back(i);
             } else {
                 for (int i = 1; i <= std::min(k, 2); ++i) steps.push_back(i);
                 const int lo = 3, hi = k - 1, ns = 6;
