@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <unordered_map>
 #include <utility>
 
 #include "kr_internal.h"
@@ -229,6 +231,25 @@ double gershgorin_mu(const kr_problem* p) {
     return mu;
 }
 
+// Process-wide cache of device blocks released by destroyed handles, keyed by (device, size class): size
+// classes are 256-byte multiples up to 1 MiB and 1 MiB multiples above; at most 1 GiB stays cached (larger
+// releases go back to the driver). The cache object is never destroyed (no teardown ordering at exit).
+struct DevCache {
+    std::mutex mu;
+    std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;
+    std::unordered_map<void*, std::pair<int, size_t>> live;
+    size_t cached = 0;
+};
+DevCache& dev_cache() {
+    static DevCache* c = new DevCache();
+    return *c;
+}
+size_t size_class(size_t b) {
+    b = std::max<size_t>(b, 256);
+    return b <= (size_t(1) << 20) ? (b + 255) & ~size_t(255) : (b + (size_t(1) << 20) - 1) & ~((size_t(1) << 20) - 1);
+}
+constexpr size_t kCacheCap = size_t(1) << 30;
+
 // Device allocations owned by the handle: requests up to 1 MB are carved (256-byte aligned) from 4 MB
 // chunks, larger ones get their own cudaMalloc — a handle makes a few dozen small allocations, and each
 // cudaMalloc / cudaFree pair costs tens of microseconds to milliseconds of create / destroy time.
@@ -237,7 +258,7 @@ void* dalloc(kr_handle* h, size_t bytes) {
     bytes = (std::max<size_t>(bytes, 8) + 255) & ~size_t(255);
     auto device_alloc = [&](size_t b) {
         void* p = nullptr;
-        cudaError_t e = cudaMalloc(&p, b);
+        cudaError_t e = kr_dev_malloc(&p, b);
         if (e != cudaSuccess) KR_THROW(KR_ENOMEM, "cudaMalloc(" + std::to_string(b) + "): " + cudaGetErrorString(e));
         h->extra_allocs.push_back(p);
         return p;
@@ -584,6 +605,7 @@ __global__ void transpose_coeff_kernel(const double* sim, double* cf, int64_t np
 
 void free_handle(kr_handle* h) {
     if (!h) return;
+    if (h->stream) cudaStreamSynchronize(h->stream);  // the blocks go back to the cache: no work may still use them
     PhaseTrace tr;
     kr_p2p_close(h);
     if (h->graph_ready) cudaGraphExecDestroy(h->gexec);
@@ -594,14 +616,57 @@ void free_handle(kr_handle* h) {
     if (h->ev_lg0) cudaEventDestroy(h->ev_lg0);
     if (h->ev_lg1) cudaEventDestroy(h->ev_lg1);
     tr.mark("destroy: events");
-    for (void* p : h->extra_allocs) cudaFree(p);
-    if (h->own_ws && h->ws) cudaFree(h->ws);
+    for (void* p : h->extra_allocs) kr_dev_free(p);
+    if (h->own_ws && h->ws) kr_dev_free(h->ws);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     tr.mark("destroy: frees");
     delete h;
 }
 
 }  // namespace
+
+cudaError_t kr_dev_malloc(void** p, size_t bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const std::pair<int, size_t> key{dev, size_class(bytes)};
+    DevCache& c = dev_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.free_blocks.find(key);
+        if (it != c.free_blocks.end() && !it->second.empty()) {
+            *p = it->second.back();
+            it->second.pop_back();
+            c.cached -= key.second;
+            c.live[*p] = key;
+            return cudaSuccess;
+        }
+    }
+    e = cudaMalloc(p, key.second);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.live[*p] = key;
+    return cudaSuccess;
+}
+
+void kr_dev_free(void* p) {
+    if (!p) return;
+    DevCache& c = dev_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.live.find(p);
+        if (it != c.live.end()) {
+            const auto key = it->second;
+            c.live.erase(it);
+            if (c.cached + key.second <= kCacheCap) {
+                c.free_blocks[key].push_back(p);
+                c.cached += key.second;
+                return;
+            }
+        }
+    }
+    cudaFree(p);
+}
 
 extern "C" {
 
@@ -814,7 +879,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             h->ws_bytes = p->workspace_bytes;
         } else {
             h->ws_bytes = sz.state_bytes + 256 * 8;
-            cudaError_t e = cudaMalloc(&h->ws, h->ws_bytes);
+            cudaError_t e = kr_dev_malloc(reinterpret_cast<void**>(&h->ws), h->ws_bytes);
             if (e != cudaSuccess) KR_THROW(KR_ENOMEM, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
             h->own_ws = true;
         }

@@ -123,7 +123,7 @@ __global__ void eval_outputs_kernel(const double* cf, int64_t step, int o, int n
 
 void kr_eval_outputs(kr_handle* h, int64_t step, const double* z_h, double* y_h) {
     double* dz = nullptr;
-    KR_CUDA(cudaMalloc(&dz, ((size_t)h->cf_ndir + h->cf_nout) * sizeof(double)));
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&dz), ((size_t)h->cf_ndir + h->cf_nout) * sizeof(double)));
     double* dy = dz + h->cf_ndir;
     cudaError_t e = cudaMemcpyAsync(dz, z_h, (size_t)h->cf_ndir * 8, cudaMemcpyHostToDevice, h->stream);
     if (e == cudaSuccess) {
@@ -132,7 +132,7 @@ void kr_eval_outputs(kr_handle* h, int64_t step, const double* z_h, double* y_h)
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(y_h, dy, (size_t)h->cf_nout * 8, cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    cudaFree(dz);
+    kr_dev_free(dz);
     if (e != cudaSuccess) KR_THROW(KR_ECUDA, std::string("kr_eval_outputs: ") + cudaGetErrorString(e));
     h->launches++;
     h->h2d_bytes += (int64_t)h->cf_ndir * 8;

@@ -507,7 +507,7 @@ void kr_expm_prepare(kr_handle* h) {
         while (((int64_t)1 << Q) <= h->n_steps) ++Q;
         h->pw_q = Q;
         const size_t ndl = std::max<size_t>(1, h->my_dirs.size());
-        KR_CUDA(cudaMalloc(&h->d_pw, ndl * Q * PW_MAT * sizeof(double)));
+        KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&h->d_pw), ndl * Q * PW_MAT * sizeof(double)));
         h->extra_allocs.push_back(h->d_pw);
         KR_CUDA(cudaFuncSetAttribute(expm_powers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const size_t msm = ((size_t)(64 + KR_MAX_OUT) * PW_LD + 512) * sizeof(double);
@@ -516,7 +516,8 @@ void kr_expm_prepare(kr_handle* h) {
         int ldx = 1;
         while (ldx < h->n_steps + 1) ldx <<= 1;
         h->xt_ld = ldx;
-        KR_CUDA(cudaMalloc(&h->d_xt, (size_t)std::max<size_t>(1, h->my_dirs.size()) * 64 * ldx * sizeof(double)));
+        KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&h->d_xt),
+                              (size_t)std::max<size_t>(1, h->my_dirs.size()) * 64 * ldx * sizeof(double)));
         h->extra_allocs.push_back(h->d_xt);
     }
 }

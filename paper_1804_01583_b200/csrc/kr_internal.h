@@ -271,6 +271,11 @@ void kr_fill_dense(cudaStream_t s, double* dst, int64_t N, int64_t n, int64_t mx
                    const DVec& v, int lift1, double scale, int accumulate, int64_t* launches);
 
 // fused Lanczos
+// Device memory owned by handles (kr_api.cu): a process-wide cache of freed blocks by (device, size class),
+// so destroy / create do not pay cudaFree / cudaMalloc (blocks above the 1 GiB cache cap are freed).
+cudaError_t kr_dev_malloc(void** p, size_t bytes);
+void kr_dev_free(void* p);
+
 void kr_lz_encode_maps(kr_handle* h);
 void kr_lz_setup_compact(kr_handle* h);
 void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events);

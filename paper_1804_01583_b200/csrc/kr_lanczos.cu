@@ -918,7 +918,7 @@ void kr_lz_setup_compact(kr_handle* h) {
         }
         if (maxe == 0) continue;
         void* gp = nullptr;
-        if (cudaMalloc(&gp, (size_t)maxe * 8) != cudaSuccess) KR_THROW(KR_ENOMEM, "compact u_1 buffer");
+        if (kr_dev_malloc(&gp, (size_t)maxe * 8) != cudaSuccess) KR_THROW(KR_ENOMEM, "compact u_1 buffer");
         h->extra_allocs.push_back(gp);  // freed with the handle
         sl.g1 = reinterpret_cast<double*>(gp);
         for (auto& c : sl.cu1) {

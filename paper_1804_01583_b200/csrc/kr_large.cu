@@ -345,17 +345,17 @@ void kr_large_alloc(kr_handle* h, int kc) {
     for (double* q : {h->d_big, h->d_traj}) {
         if (!q) continue;
         KR_CUDA(cudaStreamSynchronize(h->stream));
-        cudaFree(q);
+        kr_dev_free(q);
         h->extra_allocs.erase(std::remove(h->extra_allocs.begin(), h->extra_allocs.end(), (void*)q),
                               h->extra_allocs.end());
     }
     h->d_big = h->d_traj = nullptr;
     const size_t mat = (size_t)kp * kp;
-    KR_CUDA(cudaMalloc(&h->d_big, 3 * mat * sizeof(double)));
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&h->d_big), 3 * mat * sizeof(double)));
     h->extra_allocs.push_back(h->d_big);
     // row layout [(N+1)][kp] for the march, column layout [kp][pow2 >= N+1] for the doubling route
     const size_t tr = std::max((size_t)(h->n_steps + 1) * kp, (size_t)kp * pow2_at_least(h->n_steps + 1));
-    KR_CUDA(cudaMalloc(&h->d_traj, tr * sizeof(double)));
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&h->d_traj), tr * sizeof(double)));
     h->extra_allocs.push_back(h->d_traj);
     h->large_cap = kp;
 }

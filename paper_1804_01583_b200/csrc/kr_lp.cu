@@ -244,17 +244,19 @@ void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int
     int32_t* dfeas = nullptr;
     double* dzw = nullptr;
     double* dout = nullptr;
-    KR_CUDA(cudaMalloc(&dbuf, nbytes + 64));
-    KR_CUDA(cudaMalloc(&dfeas, np1 * sizeof(int32_t)));
-    KR_CUDA(cudaMalloc(&dzw, (size_t)np1 * (ng > 0 ? ng : 1) * sizeof(double)));
-    KR_CUDA(cudaMalloc(&dout, (size_t)(2 + nd + o) * sizeof(double)));
-    struct Free {
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&dbuf), nbytes + 64));
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&dfeas), np1 * sizeof(int32_t)));
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&dzw), (size_t)np1 * (ng > 0 ? ng : 1) * sizeof(double)));
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&dout), (size_t)(2 + nd + o) * sizeof(double)));
+    struct Free {  // back to the block cache once the stream no longer uses them
         void* p[4];
+        cudaStream_t s;
         ~Free() {
+            cudaStreamSynchronize(s);
             for (void* q : p)
-                if (q) cudaFree(q);
+                if (q) kr_dev_free(q);
         }
-    } fr{{dbuf, dfeas, dzw, dout}};
+    } fr{{dbuf, dfeas, dzw, dout}, h->stream};
     double* dIA = dbuf;
     double* dIb = dIA + (size_t)m_init * ng;
     double* dUA = dIb + m_init;

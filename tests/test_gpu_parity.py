@@ -326,3 +326,20 @@ def test_expm_march_equals_one_cta_doubling(n_steps, B, monkeypatch):
     assert [s["lemma1"] for s in sa] == pytest.approx([s["lemma1"] for s in sb], rel=1e-9, abs=1e-300)
     assert_coeff(a, b, f"march vs one-CTA doubling N={n_steps} B={B}")
     assert_coeff(a, oracle.krylov_project(p)["coeff"], f"march vs oracle N={n_steps} B={B}")
+
+
+@pytest.mark.parametrize("k,expect", [(30, [1, 2, 3, 8, 13, 19, 24, 29]), (5, [1, 2, 3, 4]), (2, [1, 2])])
+def test_step_times_sampled(k, expect):
+    """krylov_step_times: one entry per step run; CUDA events around steps 1, 2 and six steps spread over
+    3..k-1 (finite, positive), NaN elsewhere."""
+    from paper_1804_01583_b200 import KrylovReach
+    p = W.heat(20, 3, k, n_steps=10)
+    with KrylovReach(p) as h:
+        h.project(want=False)
+        st = h.step_times()
+        t = h.last_timing()
+    assert len(st) == k
+    timed = [i + 1 for i, x in enumerate(st) if np.isfinite(x)]
+    assert timed == expect
+    assert all(st[i - 1] > 0 for i in timed)
+    assert t["step_ms_mean"] == pytest.approx(float(np.mean([st[i - 1] for i in timed])), rel=1e-12)
