@@ -343,3 +343,14 @@ def test_step_times_sampled(k, expect):
     assert timed == expect
     assert all(st[i - 1] > 0 for i in timed)
     assert t["step_ms_mean"] == pytest.approx(float(np.mean([st[i - 1] for i in timed])), rel=1e-12)
+
+
+def test_virtual_slabs_two_planes_each():
+    """halo correctness at the minimum slab thickness — m = 16 on 8 slabs (2 planes each, so every
+    owned plane is a halo plane of a neighbour): equal to one slab and to the oracle."""
+    p = W.heat(16, 3, 20, n_steps=60, step=0.05)
+    res = oracle.krylov_project(p)
+    c1, _, _, _ = gpu_run(p)
+    c8, _, _, _ = gpu_run(p, virtual_slabs=8, part="zslab")
+    assert_coeff(c8, res["coeff"], "m=16 P=8 vs oracle")
+    assert_coeff(c8, c1, "m=16 P=8 vs P=1")
