@@ -195,7 +195,14 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats);
 kr_status krylov_check_box(kr_handle* h, const int32_t* sense, const double* thr, double* lo, double* hi,
                            kr_cex* cex, double* z_witness);
 
+/* Destroys the handle after its stream has finished. Its device blocks (everything but a caller workspace)
+ * go to a process-wide cache, keyed by device and size class and capped at 1 GiB, from which the next
+ * handles allocate: create / destroy then pay no cudaMalloc / cudaFree. */
 void krylov_reach_destroy(kr_handle* h);
+
+/* Returns every cached device block (see krylov_reach_destroy) to the driver, e.g. before cudaDeviceReset
+ * or when the memory is needed elsewhere. Live handles are unaffected. Returns the bytes released.        */
+size_t krylov_release_cached_memory(void);
 
 const char* krylov_last_error(void);
 

@@ -63,7 +63,8 @@ EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "k
            "krylov_krylov_data", "krylov_transfer_bytes", "krylov_zslab_halo_plan", "krylov_tridiag",
            "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info", "krylov_check_lp",
            "krylov_eval_outputs", "krylov_ipc_blob", "krylov_p2p_open", "krylov_p2p_verify", "krylov_p2p_enable",
-           "krylov_a_priori_bound_log10", "krylov_memory_bytes", "krylov_step_times"]
+           "krylov_a_priori_bound_log10", "krylov_memory_bytes", "krylov_step_times",
+           "krylov_release_cached_memory"]
 
 _lib = None
 
@@ -84,6 +85,8 @@ def lib():
     L.krylov_check_box.argtypes = [vp, vp, vp, vp, vp, C.POINTER(kr_cex), vp]
     L.krylov_reach_destroy.argtypes = [vp]
     L.krylov_reach_destroy.restype = None
+    L.krylov_release_cached_memory.argtypes = []
+    L.krylov_release_cached_memory.restype = C.c_size_t
     L.krylov_last_error.restype = C.c_char_p
     L.krylov_launch_count.argtypes = [vp]
     L.krylov_launch_count.restype = C.c_int64

@@ -325,6 +325,11 @@ def krylov_reach_destroy(handle):
     handle.close()
 
 
+def krylov_release_cached_memory():
+    """Return the device blocks cached from destroyed handles to the driver; bytes released."""
+    return int(A.lib().krylov_release_cached_memory())
+
+
 def krylov_zslab_range(mz, world, rank):
     z0, z1 = C.c_int64(), C.c_int64()
     A.check(A.lib().krylov_zslab_range(int(mz), int(world), int(rank), C.byref(z0), C.byref(z1)))

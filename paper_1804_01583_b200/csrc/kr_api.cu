@@ -670,6 +670,25 @@ void kr_dev_free(void* p) {
 
 extern "C" {
 
+size_t krylov_release_cached_memory(void) {
+    DevCache& c = dev_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    size_t released = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : c.free_blocks) {
+        cudaSetDevice(kv.first.first);
+        for (void* p : kv.second) {
+            cudaFree(p);
+            released += kv.first.second;
+        }
+    }
+    cudaSetDevice(cur);
+    c.free_blocks.clear();
+    c.cached = 0;
+    return released;
+}
+
 const char* krylov_last_error(void) { return g_err.c_str(); }
 
 kr_status krylov_zslab_range(int64_t mz, int32_t world, int32_t rank, int64_t* z0, int64_t* z1) {

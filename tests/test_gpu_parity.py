@@ -354,3 +354,17 @@ def test_virtual_slabs_two_planes_each():
     c8, _, _, _ = gpu_run(p, virtual_slabs=8, part="zslab")
     assert_coeff(c8, res["coeff"], "m=16 P=8 vs oracle")
     assert_coeff(c8, c1, "m=16 P=8 vs P=1")
+
+
+def test_device_block_cache_reuse_and_release():
+    """Handles take their device blocks from the process-wide cache filled by destroyed handles (same results,
+    bitwise); krylov_release_cached_memory returns them to the driver, and new handles still work."""
+    from paper_1804_01583_b200 import krylov_release_cached_memory
+    p = W.heat(30, 4, 20, n_steps=40)
+    a, _, _, _ = gpu_run(p)
+    b, _, _, _ = gpu_run(p)  # blocks from the cache
+    assert np.array_equal(a, b)
+    assert krylov_release_cached_memory() > 0
+    assert krylov_release_cached_memory() == 0
+    c, _, _, _ = gpu_run(p)
+    assert np.array_equal(a, c)
