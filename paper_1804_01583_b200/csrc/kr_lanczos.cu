@@ -302,11 +302,8 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
             ((q & 1) ? Wb1 : Wb0)[rwi] = w;
         }
         // the plane above the global grid is a zero ghost: its w enters only as the z+1 neighbour of the last
-        // owned plane (its W plane and ring values are never read), so one uniform branch replaces a select per cell
-        if (!zin) {
-#pragma unroll
-            for (int m = 0; m < G::TS; ++m) wc[m] = 0.0;
-        }
+        // owned plane (its W plane and ring values are never read), through dz = zf * w_{q} - w_{q-1} below
+        const double zf = zin ? 1.0 : 0.0;
         if (q > zc0) {  // products for plane q-1 (its w neighbours at x+1, y+1 were written last iteration)
             const double* Wp = ((q & 1) ? Wb0 : Wb1) + wi0;
             const int gzp = a.zoff + q - 1;
@@ -325,7 +322,7 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 wp[m] = w0;
                 const double dx = Wp[o + 1] - w0;
                 const double dy = Wp[o + G::WW] - w0;
-                const double dz = wc[m] - w0;
+                const double dz = fma(wc[m], zf, -w0);  // exactly wc - w0, or -w0 above the grid
                 const double w2 = w0 * w0;
                 const double g = gex + gz + (m == 0 ? gey0 : 0.0);
                 const double ky = (BCY && y0 + ty + m * RS == a.my - 1) ? a.gq[3] : cy;
