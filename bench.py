@@ -90,7 +90,7 @@ class ClockSampler:
 def cpu_baseline_other(p_full, budget="bench"):
     """Oracle baselines for the non-headline workloads (bounded samples, stated in `sample`)."""
     import oracle
-    if p_full["op"] == "csr":  # C2 / C2T: literal MGS Arnoldi + per-step Pade of the oracle
+    if p_full["op"] == "csr" or p_full.get("b") is None:  # C1 / C2 / C2T: literal MGS Arnoldi + per-step Pade
         transpose = p_full.get("sim") == "transpose"
         q = oracle.transpose_problem(p_full) if transpose else p_full
         dirs = oracle.directions(q)
@@ -127,7 +127,7 @@ def cpu_baseline(p_full, budget="bench", k_full=None):
     the workload: the same recipe on a smaller grid (Lanczos cost is linear in n) plus the full
     1001-step k x k exponential sweep; scaled to Krylov steps/s at the full n."""
     import oracle
-    if p_full["op"] == "csr" or p_full.get("b") is not None:
+    if p_full["op"] == "csr" or p_full.get("b") is not None or p_full.get("method") == "arnoldi":
         return cpu_baseline_other(p_full, budget)
     m_full = p_full["mx"]
     if p_full.get("eps", 0.0) > 0.0:  # the paper's heat model (adaptive): literal Alg. 3 steps + one eig checkpoint
@@ -152,7 +152,7 @@ def cpu_baseline(p_full, budget="bench", k_full=None):
                           f"the Lemma 1 checkpoints (numpy eigh route; one at k={kc} took {t2 - t1:.2f} s) "
                           f"are not included",
                 "sample_seconds": t2 - t0}
-    m_s = 160 if budget == "reference" else 250
+    m_s = min(m_full, 160 if budget == "reference" else 250)  # C3 (m = 100) runs in full
     b_s = max(2, round(p_full["gens"][0]["hi"][0] * m_s / m_full))
     ps = W.heat(m_s, b_s, p_full["k"], n_steps=p_full["n_steps"], step=p_full["step"])
     v = oracle.directions(ps)[0]
@@ -423,8 +423,7 @@ def main():
                             "large_route_ms": timing["large_ms"], "checkpoints": timing["large_evals"],
                             "lanczos_ms": timing["iter_ms"] - timing["large_ms"],
                             "note": "step kernel mean over steps 1, 2 and every 16th step of the run (CUDA events)"}
-    if not args.no_cpu_baseline and world == 1 and (args.config == "C5" or p.get("eps", 0.0) > 0.0 or
-                                                      p["op"] == "csr" or p.get("b") is not None):
+    if not args.no_cpu_baseline and world == 1:  # every config (oracle steps/s beside the GPU's)
         line["cpu_baseline"] = cpu_baseline(p, k_full=stats[0]["k_eff"])
     print(json.dumps(line), flush=True)
     if world > 1:

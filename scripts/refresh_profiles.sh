@@ -3,7 +3,7 @@
 # full ncu capture of the step kernel on C4. Usage (under gpurun): bash scripts/refresh_profiles.sh <tag>
 tag=${1:-x}
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_c5_$tag.log 2>&1; echo c5=$?
-for c in C3 C4; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c,,}_$tag.log 2>&1; echo $c=$?; done
+for c in C3 C4; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_${c,,}_$tag.log 2>&1; echo $c=$?; done
 for c in P100 C2 C2T; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_${c,,}_$tag.log 2>&1; echo $c=$?; done
 timeout 900 python bench.py --config H100 --steps 3 --warmup 3 > gpurun_out/bench_h100_$tag.log 2>&1; echo h100=$?
 timeout 1200 python bench.py --config P1000 --steps 1 --warmup 3 --no-e2e > gpurun_out/bench_p1000_$tag.log 2>&1; echo p1000=$?
