@@ -184,11 +184,11 @@ double gershgorin_mu(const kr_problem* p) {
         }
         return mu;
     }
-    // s_rc = (a_rc + a_cr) / 2 over the merged rows (ascending columns, duplicates summed): each stored entry
-    // (r, c) finds its mirror a_cr by binary search in row c; an entry without a stored mirror also carries
-    // the radius term of row c (whose row has no (c, r) entry to visit). O(nnz log row length), no transpose.
+    // s_rc = (a_rc + a_cr) / 2 over rows with ascending columns and no duplicates (the caller's rows when they
+    // already are, else merged copies). Each pair {r, c} is visited once, from its entry with c > r: the mirror
+    // a_cr is found by binary search in row c and marked, |s_rc| goes to both radii; entries with c < r whose
+    // mirror was not marked (a_cr absent) add |a_rc| / 2 to both. O(nnz log row length), no transpose.
     const int64_t n = p->n, N = n + (p->b ? 1 : 0);
-    // rows already strictly ascending (no duplicates) are used in place; otherwise merged copies
     bool sorted = true;
     for (int64_t r = 0; r < n && sorted; ++r)
         for (int64_t e = p->row_ptr[r] + 1; e < p->row_ptr[r + 1]; ++e)
@@ -196,35 +196,47 @@ double gershgorin_mu(const kr_problem* p) {
                 sorted = false;
                 break;
             }
-    RowsCsr m;
-    if (!sorted) m = merged_rows(p);
-    auto rp = [&](int64_t r) { return sorted ? p->row_ptr[r] : m.rp[(size_t)r]; };
-    auto col = [&](int64_t e) { return sorted ? (int64_t)p->col_idx[e] : m.ci[(size_t)e]; };
-    auto val = [&](int64_t e) { return sorted ? p->val[e] : m.v[(size_t)e]; };
     std::vector<double> diag(N, 0.0), rad(N, 0.0);
-    for (int64_t r = 0; r < n; ++r) {
-        for (int64_t e = rp(r); e < rp(r + 1); ++e) {
-            const int64_t c = col(e);
-            if (c == r) {
-                diag[(size_t)r] += val(e);  // 0.5 a_rr + 0.5 a_rr
-                continue;
+    auto pass = [&](const int64_t* rp, const auto* ci, const double* v) {
+        std::vector<uint8_t> paired((size_t)rp[n], 0);
+        for (int64_t r = 0; r < n; ++r) {
+            for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+                const int64_t c = ci[e];
+                if (c == r) {
+                    diag[(size_t)r] += v[e];  // 0.5 a_rr + 0.5 a_rr
+                    continue;
+                }
+                double s;
+                if (c > r) {
+                    int64_t lo = rp[c], hi = rp[c + 1];  // binary search of column r in row c
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        if (ci[mid] < r) lo = mid + 1; else hi = mid;
+                    }
+                    if (lo < rp[c + 1] && ci[lo] == r) {
+                        s = std::fabs(0.5 * v[e] + 0.5 * v[lo]);
+                        paired[(size_t)lo] = 1;
+                    } else {
+                        s = std::fabs(0.5 * v[e]);
+                    }
+                } else {
+                    if (paired[(size_t)e]) continue;  // counted from row c
+                    s = std::fabs(0.5 * v[e]);
+                }
+                rad[(size_t)r] += s;
+                rad[(size_t)c] += s;
             }
-            int64_t lo = rp(c), hi = rp(c + 1);  // binary search of column r in row c
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (col(mid) < r) lo = mid + 1; else hi = mid;
-            }
-            if (lo < rp(c + 1) && col(lo) == r) {
-                rad[(size_t)r] += std::fabs(0.5 * val(e) + 0.5 * val(lo));
-            } else {
-                rad[(size_t)r] += std::fabs(0.5 * val(e));
-                rad[(size_t)c] += std::fabs(0.5 * val(e));
+            if (p->b && p->b[r] != 0.0) {  // lifted column b and (zero) lifted row: s_{r,n} = s_{n,r} = b_r / 2
+                rad[(size_t)r] += std::fabs(0.5 * p->b[r]);
+                rad[(size_t)n] += std::fabs(0.5 * p->b[r]);
             }
         }
-        if (p->b && p->b[r] != 0.0) {  // lifted column b and (zero) lifted row: s_{r,n} = s_{n,r} = b_r / 2
-            rad[(size_t)r] += std::fabs(0.5 * p->b[r]);
-            rad[(size_t)n] += std::fabs(0.5 * p->b[r]);
-        }
+    };
+    if (sorted) {
+        pass(p->row_ptr, p->col_idx, p->val);
+    } else {
+        const RowsCsr m = merged_rows(p);
+        pass(m.rp.data(), m.ci.data(), m.v.data());
     }
     double mu = -INFINITY;
     for (int64_t r = 0; r < N; ++r) mu = std::max(mu, diag[r] + rad[r]);
