@@ -261,6 +261,7 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
         const double dgz = BC ? diag - ex - ((a.zoff + q == 0) ? a.ecor[4] : 0.0) -
                                     ((a.zoff + q == a.mz - 1) ? a.ecor[5] : 0.0)
                               : diag;
+        const double cfz = fma(sa, dgz, sb);  // coefficient of u_i in w for this plane's cells
 #pragma unroll
         for (int m = 0; m < G::TS; ++m) {
             const int o = m * RS * G::CW;
@@ -272,13 +273,14 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 const double sx = Cq[o - 1] + Cq[o + 1];
                 const double sy = Cq[o - G::CW] + Cq[o + G::CW];
                 const double sz = up[m] + un[m];
-                double dg = dgz;
+                // w = s_i (A u_i) - alpha_i s_i u_i - ... = s_i (off-diagonal part) - (s_i diag + alpha_i s_i) u_i
+                double cf = cfz;
                 if (BCY) {
                     const int gy = y0 + ty + m * RS;
-                    dg -= (gy == 0 ? a.ecor[2] : 0.0) + (gy == a.my - 1 ? a.ecor[3] : 0.0);
+                    cf = fma(sa, dgz - ((gy == 0 ? a.ecor[2] : 0.0) + (gy == a.my - 1 ? a.ecor[3] : 0.0)), sb);
                 }
-                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -dg * uc[m])));
-                w = fma(sa, Au, -sb * uc[m]);
+                const double Ao = fma(cx, sx, fma(cy, sy, cz * sz));
+                w = fma(sa, Ao, -cf * uc[m]);
                 if (has_prev) w = fma(-sp, Pq[m * RS * G::PW], w);
             }
             if (!FULL && !ing[m]) w = 0.0;
@@ -294,8 +296,8 @@ __device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorM
                 const double sy = Cqb[rci - G::CW] + Cqb[rci + G::CW];
                 const double sz = rup + run;
                 const double rdg = BC ? dgz + ex - rexy : diag;  // dgz holds this thread's ex: swap in the ring's
-                const double Au = fma(cx, sx, fma(cy, sy, fma(cz, sz, -rdg * ruc)));
-                w = fma(sa, Au, -sb * ruc);
+                const double Ao = fma(cx, sx, fma(cy, sy, cz * sz));
+                w = fma(sa, Ao, -fma(sa, rdg, sb) * ruc);
                 if (has_prev) w = fma(-sp, reinterpret_cast<const double*>(stq + G::POFF)[rpi], w);
             }
             if (!FULL && !ring_in) w = 0.0;
