@@ -627,6 +627,11 @@ void free_handle(kr_handle* h) {
     if (h->ev_it1) cudaEventDestroy(h->ev_it1);
     if (h->ev_lg0) cudaEventDestroy(h->ev_lg0);
     if (h->ev_lg1) cudaEventDestroy(h->ev_lg1);
+    if (h->ev_spec) cudaEventDestroy(h->ev_spec);
+    if (h->stream2) {
+        cudaStreamSynchronize(h->stream2);
+        cudaStreamDestroy(h->stream2);
+    }
     tr.mark("destroy: events");
     for (void* p : h->extra_allocs) kr_dev_free(p);
     if (h->own_ws && h->ws) kr_dev_free(h->ws);
@@ -1301,8 +1306,18 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                 int i = 0, accepted = -1;
                 bool failed = false;
                 if (h->eps > 0.0) {
-                    // checkpoints k = 4, ceil(1.1 k), ... in fp64 (Alg. 2 lines 11-16)
-                    for (int kc = 4; kc <= h->k; kc = (int)std::ceil(1.1 * (double)kc)) {
+                    // checkpoints k = 4, ceil(1.1 k), ... in fp64 (Alg. 2 lines 11-16).
+                    // Pipelined: while checkpoint kc is evaluated on a second stream (it reads only alpha_1..kc,
+                    // beta_1..kc, which later steps do not touch), the steps up to the next checkpoint already run
+                    // on the main stream; if kc is accepted they are discarded (k_eff, h_next reset to kc below).
+                    if (!h->stream2) {
+                        KR_CUDA(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+                        KR_CUDA(cudaEventCreateWithFlags(&h->ev_spec, cudaEventDisableTiming));
+                    }
+                    const bool pipe = getenv("KR_NO_SPECULATE") == nullptr;
+                    bool by_bound = false;
+                    int kc = 4;
+                    while (kc <= h->k) {
                         while (i < kc) kr_lz_enqueue_step(h, dl, ++i, h->timing);
                         const LzScalars sc = read_sc(dl);
                         if (sc.status) {
@@ -1315,12 +1330,39 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                             accepted = sc.k_eff;
                             break;
                         }
-                        const double b = kr_large_eval(h, dl, kc, true, false);
+                        const int kn = (int)std::ceil(1.1 * (double)kc);
+                        double b;
+                        if (pipe && kn <= h->k) {
+                            KR_CUDA(cudaEventRecord(h->ev_spec, h->stream));
+                            while (i < kn) kr_lz_enqueue_step(h, dl, ++i, h->timing);  // speculative
+                            std::swap(h->stream, h->stream2);
+                            try {
+                                KR_CUDA(cudaStreamWaitEvent(h->stream, h->ev_spec, 0));
+                                b = kr_large_eval(h, dl, kc, true, false);
+                            } catch (...) {
+                                std::swap(h->stream, h->stream2);
+                                throw;
+                            }
+                            std::swap(h->stream, h->stream2);
+                        } else {
+                            b = kr_large_eval(h, dl, kc, true, false);
+                        }
                         h->checks[dl].push_back({kc, b});
                         if (b < h->eps) {
                             accepted = kc;
+                            by_bound = true;
                             break;
                         }
+                        kc = kn;
+                    }
+                    if (by_bound && i > accepted) {  // speculative steps past the accepted checkpoint
+                        KR_CUDA(cudaStreamSynchronize(h->stream));
+                        const int32_t ka = accepted;
+                        KR_CUDA(cudaMemcpyAsync(h->d_keff + dl, &ka, 4, cudaMemcpyHostToDevice, h->stream));
+                        KR_CUDA(cudaMemcpyAsync(h->d_hnext + dl, h->d_lzarr + (size_t)dl * 3 * (h->k + 2) + (h->k + 2) + ka,
+                                                8, cudaMemcpyDeviceToDevice, h->stream));
+                        KR_CUDA(cudaStreamSynchronize(h->stream));
+                        if (dl == 0) h->steps_run0 = i;
                     }
                 }
                 if (accepted < 0 && !failed) {  // fixed k, or k_max reached without meeting eps

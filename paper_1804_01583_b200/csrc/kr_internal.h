@@ -212,7 +212,9 @@ struct kr_handle {
     int steps_run0 = 0;
     double large_ms = 0.0;  // device time of the large-k route (exponentials + bounds) in the last project
     int32_t large_evals = 0;
-    cudaEvent_t ev_lg0 = nullptr, ev_lg1 = nullptr;    // Lanczos steps run for local direction 0 by the last large-route project
+    cudaEvent_t ev_lg0 = nullptr, ev_lg1 = nullptr;
+    cudaStream_t stream2 = nullptr;  // adaptive runs: checkpoint evaluations beside the next checkpoint's steps
+    cudaEvent_t ev_spec = nullptr;    // Lanczos steps run for local direction 0 by the last large-route project
     bool halo_inkernel = false;  // halo planes written by the step kernel into the neighbours' buffers
     bool p2p = false;            // ... across processes through CUDA IPC peer memory (NVLink)
     void* p2p_base[2] = {nullptr, nullptr};  // opened IPC bases (lower, upper neighbour)

@@ -225,3 +225,19 @@ def test_adaptive_dirichlet_sparse_generator_slabs():
         assert stats[0]["k_eff"] == ref["per_dir"][0]["k_eff"]
         assert [k for k, _ in checks] == [k for k, _ in ref["per_dir"][0]["checks"]]
         assert_coeff(coeff, ref["coeff"], f"adaptive dirichlet sparse vs={vs}")
+
+
+@pytest.mark.parametrize("vs", [0, 2])
+def test_adaptive_speculative_steps_match_sequential(vs, monkeypatch):
+    """Checkpoint k_c is evaluated on a second stream while the steps up to the next checkpoint already run;
+    accepting k_c discards them. Same checkpoints, bounds, accepted k, h_next, tridiagonal and coefficients,
+    bitwise, as the sequential schedule (KR_NO_SPECULATE=1), on one and two slabs."""
+    p = W.heat_paper(20, k_max=2000)
+    kw = dict(virtual_slabs=vs) if vs else {}
+    a = gpu(p, **kw)
+    monkeypatch.setenv("KR_NO_SPECULATE", "1")
+    b = gpu(p, **kw)
+    assert np.array_equal(a[0], b[0])
+    assert [(s["k_eff"], s["h_next"], s["lemma1"]) for s in a[1]] == [(s["k_eff"], s["h_next"], s["lemma1"]) for s in b[1]]
+    assert np.array_equal(a[2][0], b[2][0]) and np.array_equal(a[2][1], b[2][1])
+    assert a[3] == b[3]
