@@ -1314,7 +1314,13 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                         KR_CUDA(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
                         KR_CUDA(cudaEventCreateWithFlags(&h->ev_spec, cudaEventDisableTiming));
                     }
-                    const bool pipe = getenv("KR_NO_SPECULATE") == nullptr;
+                    // only where the steps are latency-bound (slabs up to 2^24 cells): on large grids the step
+                    // kernels fill the GPU and concurrent checkpoint GEMMs slow both (paper heat 10^9: 28.9 -> 31.6 s)
+                    int64_t ncell = 0;
+                    for (const auto& sl : h->slabs) ncell = std::max<int64_t>(ncell, sl.nz * h->mx * h->my);
+                    bool pipe = ncell <= (int64_t(1) << 24);
+                    if (getenv("KR_NO_SPECULATE")) pipe = false;
+                    if (getenv("KR_SPECULATE")) pipe = true;
                     bool by_bound = false;
                     int kc = 4;
                     while (kc <= h->k) {
