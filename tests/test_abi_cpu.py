@@ -183,3 +183,9 @@ def test_host_utilities_match_oracle():
     assert L.krylov_memory_bytes(10 ** 9, 5932, 1, 1, A.KR_ARNOLDI) == oracle.memory_bytes(10 ** 9, 5932)
     assert L.krylov_memory_bytes(10923, 63, 10, 2, A.KR_LANCZOS) == oracle.memory_bytes(10923, 63, 10, 2, "lanczos")
     assert L.krylov_memory_bytes(0, 5, 1, 1, A.KR_ARNOLDI) == -1
+
+
+def test_release_cached_memory_without_gpu(lib):
+    """The block cache is empty without a GPU: releasing it is a no-op returning 0 bytes."""
+    from paper_1804_01583_b200 import krylov_release_cached_memory
+    assert krylov_release_cached_memory() == 0
