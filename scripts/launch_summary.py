@@ -8,10 +8,11 @@ rows = list(csv.reader(open(sys.argv[1])))
 i = [k for k, r in enumerate(rows) if r and r[0] == 'ID'][0]
 hdr = rows[i]
 ki, vi, ui = hdr.index('Kernel Name'), hdr.index('Metric Value'), hdr.index('Metric Unit')
+mi = hdr.index('Metric Name')
 scale = {'ns': 1e-3, 'nsecond': 1e-3, 'us': 1.0, 'usecond': 1.0, 'ms': 1e3, 'msecond': 1e3}
 tot, cnt = collections.Counter(), collections.Counter()
 for r in rows[i + 1:]:
-    if len(r) <= vi:
+    if len(r) <= vi or r[mi] != 'gpu__time_duration.sum':  # other metrics of the same capture are ignored
         continue
     name = re.sub(r'^void\s+', '', r[ki])
     name = re.sub(r'\(.*$', '', name).replace('<unnamed>::', '').replace('(anonymous namespace)::', '')
