@@ -1112,6 +1112,18 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 if (h->n_long) h->d_long = upload(h, lr.data(), lr.size());
             }
             kr_ge_prepare();
+            {  // the local start vectors for the one-launch fill of kr_ge_enqueue_init
+                std::vector<DVec> gd;
+                std::vector<int32_t> gl;
+                for (int dl = 0; dl < ndl; ++dl) {
+                    gd.push_back(h->dirs_h[h->my_dirs[dl]]);
+                    gl.push_back(h->dir_lift1[h->my_dirs[dl]]);
+                }
+                if (ndl > 0) {
+                    h->d_gdirs = upload(h, gd.data(), gd.size());
+                    h->d_glift = upload(h, gl.data(), gl.size());
+                }
+            }
             h->d_V = reinterpret_cast<double*>(carve(h, (size_t)ndl * (k + 1) * h->N * 8));
             h->d_W = reinterpret_cast<double*>(carve(h, (size_t)ndl * h->N * 8));
             h->d_O = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * h->N * 8));

@@ -83,6 +83,37 @@ __global__ void fill_dense_kernel(double* dst, int64_t N, int64_t n, int64_t mx,
     }
 }
 
+// All local start vectors at once (one launch instead of a fill + scatter per direction): V[dl][0][c] =
+// v_dl[c] (box / all-grid by membership, sparse by binary search in the sorted, merged index list), the lifted
+// coordinate lift1[dl].
+__global__ void fill_dirs_kernel(double* V, int64_t vstride, int64_t N, int64_t n, int64_t mx, int64_t my, int stencil,
+                                 const DVec* dirs, const int32_t* lift1) {
+    const int dl = blockIdx.y;
+    const DVec v = dirs[dl];
+    double* dst = V + (int64_t)dl * vstride;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N; c += (int64_t)gridDim.x * blockDim.x) {
+        double val = 0.0;
+        if (c >= n) {
+            val = lift1[dl] ? 1.0 : 0.0;
+        } else if (v.kind == KR_VEC_SPARSE) {
+            int64_t lo = 0, hi = v.nnz;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (v.idx[mid] < c) lo = mid + 1; else hi = mid;
+            }
+            if (lo < v.nnz && v.idx[lo] == c) val = v.val[lo];
+        } else if (stencil) {
+            const int64_t z = c / (mx * my), rem = c - z * mx * my;
+            const int64_t y = rem / mx, x = rem - y * mx;
+            val = box_value(v, x, y, z);
+        } else {
+            if (v.kind == KR_VEC_ALL) val = v.value;
+            if (v.kind == KR_VEC_BOX) val = (c >= v.lo[0] && c < v.hi[0]) ? v.value : 0.0;
+        }
+        dst[c] = val;
+    }
+}
+
 __global__ void scatter_dense_kernel(double* dst, DVec v) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < v.nnz; e += (int64_t)gridDim.x * blockDim.x)
         dst[v.idx[e]] = v.val[e];
@@ -402,10 +433,19 @@ void kr_ge_enqueue_init(kr_handle* h) {
     ge_reset<<<1, 256, 0, h->stream>>>(h->d_done, h->d_status, ndl);
     KR_CUDA(cudaGetLastError());
     h->launches++;
-    for (int dl = 0; dl < ndl; ++dl) {
-        const int d = h->my_dirs[dl];
-        kr_fill_dense(h->stream, h->d_V + (int64_t)dl * (k + 1) * N, N, h->n, h->mx, h->my, h->op == KR_OP_STENCIL7,
-                      h->dirs_h[d], h->dir_lift1[d], 1.0, 0, &h->launches);
+    if (h->d_gdirs && ndl > 0) {
+        const int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 4);
+        fill_dirs_kernel<<<dim3(blocks, ndl), 256, 0, h->stream>>>(h->d_V, (int64_t)(k + 1) * N, N, h->n, h->mx, h->my,
+                                                                     h->op == KR_OP_STENCIL7 ? 1 : 0, h->d_gdirs,
+                                                                     h->d_glift);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+    } else {
+        for (int dl = 0; dl < ndl; ++dl) {
+            const int d = h->my_dirs[dl];
+            kr_fill_dense(h->stream, h->d_V + (int64_t)dl * (k + 1) * N, N, h->n, h->mx, h->my,
+                          h->op == KR_OP_STENCIL7, h->dirs_h[d], h->dir_lift1[d], 1.0, 0, &h->launches);
+        }
     }
     launch_ortho(h, 0, ndl);
 }

@@ -168,6 +168,8 @@ struct kr_handle {
     std::vector<DVec> dirs_h;          // per global direction: up to 2 pieces (gen/center + lifted one)
     std::vector<int32_t> dir_lift1;    // per global direction: 1 if the lifted coordinate is 1
     DVec* d_outs;                      // [n_out]
+    DVec* d_gdirs = nullptr;           // stored-basis paths: the local directions' start vectors [ndl]
+    int32_t* d_glift = nullptr;        // ... and their lifted coordinate (1 for v_f = [c; 1]) [ndl]
     std::vector<DVec> outs_h;
     double* d_O;                       // generic path: dense [n_out][N]
     // CSR
