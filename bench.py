@@ -152,23 +152,33 @@ def cpu_baseline(p_full, budget="bench", k_full=None):
                           f"the Lemma 1 checkpoints (numpy eigh route; one at k={kc} took {t2 - t1:.2f} s) "
                           f"are not included",
                 "sample_seconds": t2 - t0}
-    m_s = min(m_full, 160 if budget == "reference" else 250)  # C3 (m = 100) runs in full
-    b_s = max(2, round(p_full["gens"][0]["hi"][0] * m_s / m_full))
-    ps = W.heat(m_s, b_s, p_full["k"], n_steps=p_full["n_steps"], step=p_full["step"])
-    v = oracle.directions(ps)[0]
+    # fixed-k stencil Lanczos (C3-C5): the oracle at the FULL size (same grid, same start vector), bounded by the
+    # number of Lanczos steps: oracle.lanczos with k = 1 and k = 2 (each = start-vector pass + k literal Alg. 3
+    # steps), so t(step) = t2 - t1 and t(start) = t1 - t(step); plus the full (N+1)-step k x k Pade sweep (MvL
+    # q = 8) on a k x k Lanczos tridiagonal of the same recipe on a small grid. A whole oracle pass is then
+    # t(start) + k t(step) + t(sweep).
+    v = oracle.directions(p_full)[0]
     t0 = time.perf_counter()
-    r = oracle.lanczos(ps, v, ps["k"])
+    oracle.lanczos(p_full, v, 1)
     t1 = time.perf_counter()
-    oracle.expm_e1_times(r["H"], ps["step"], ps["n_steps"])
+    oracle.lanczos(p_full, v, 2)
     t2 = time.perf_counter()
-    n_s, n_f = m_s ** 3, W.n_state(p_full)
-    t_full = (t1 - t0) * (n_f / n_s) + (t2 - t1)
-    k = r["k_eff"]
-    return {"value": k / t_full, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle",
-            "sample": f"oracle (1 thread, C -O2) Lanczos k={k} on the C5 recipe at m={m_s} "
-                      f"({n_s:.3g} states, block {b_s}^3) = {t1 - t0:.2f} s scaled x{n_f / n_s:.1f} to n={n_f:.3g}, "
-                      f"plus the full {ps['n_steps'] + 1}-step {k}x{k} Pade sweep {t2 - t1:.2f} s",
-            "sample_seconds": t2 - t0}
+    del v
+    small = W.heat(24, 3, p_full["k"], n_steps=p_full["n_steps"], step=p_full["step"])
+    r = oracle.lanczos(small, oracle.directions(small)[0], p_full["k"])
+    t3 = time.perf_counter()
+    oracle.expm_e1_times(r["H"], p_full["step"], p_full["n_steps"])
+    t4 = time.perf_counter()
+    k = int(k_full or p_full["k"])
+    t_step = (t2 - t1) - (t1 - t0)
+    t_start = (t1 - t0) - t_step
+    t_pass = t_start + k * t_step + (t4 - t3)
+    return {"value": k / t_pass, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle (1 thread, C -O2) at the full size n={W.n_state(p_full):.3g}: literal Alg. 3 with k=1 "
+                      f"({t1 - t0:.2f} s) and k=2 ({t2 - t1:.2f} s) -> {t_step:.2f} s per Lanczos step, {t_start:.2f} s "
+                      f"start-vector pass; plus the full {p_full['n_steps'] + 1}-step {k}x{k} Pade sweep "
+                      f"({t4 - t3:.2f} s); whole pass = start + {k} steps + sweep = {t_pass:.1f} s",
+            "sample_seconds": (t2 - t0) + (t4 - t3), "pass_seconds": t_pass}
 
 
 def dist_env():
@@ -179,20 +189,40 @@ def dist_env():
 
 
 def run_reference(args):
+    """The base contract's reference arm for this tier: the oracle as it stands (1 thread) on the host cores, on
+    the same config / metric / unit. Fixed-k stencil configs (C3-C5): every step is one oracle call at the FULL
+    size with k = 1 (start-vector pass + one literal Alg. 3 step), counted as one Krylov step, so value is the
+    oracle's measured Krylov steps/s at full size (slightly under its pure per-step rate) and ms_per_step the
+    wall time of that call. Other configs: the bounded samples of cpu_baseline()."""
     world, rank, local = dist_env()
     if rank != 0:
         return 0
+    import oracle
     p = W.CONFIGS[args.config]()
+    fixed_stencil = p["op"] == "stencil" and p.get("b") is None and p.get("eps", 0.0) == 0.0 and p["method"] == "lanczos"
+    if fixed_stencil:
+        v = oracle.directions(p)[0]
+
+        def sample():
+            t0 = time.perf_counter()
+            oracle.lanczos(p, v, 1)
+            t = time.perf_counter() - t0
+            return {"value": 1.0 / t, "sample_seconds": t,
+                    "sample": f"one oracle call (1 thread, C -O2) at the full size n={W.n_state(p):.3g} with k=1: the "
+                              f"start-vector pass (beta0, P_1) + one literal Alg. 3 step, counted as one Krylov step"}
+    else:
+        def sample():
+            return cpu_baseline(p, "reference")
     for _ in range(args.warmup):
-        cpu_baseline(p, "reference")
+        sample()
     vals, secs = [], []
     for _ in range(args.steps):
-        cb = cpu_baseline(p, "reference")
+        cb = sample()
         vals.append(cb["value"])
         secs.append(cb["sample_seconds"])
     v = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Krylov steps/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * p["k"] / v,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean(secs)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_dict(p, args.gpus),
             "cpu_baseline": {"value": v, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle",
@@ -215,8 +245,11 @@ def config_dict(p, n):
               f"Arnoldi k={p['k']} (CGS2 above 27648 states), {p['n_steps']} steps of {p['step']}, "
               f"{len(p['outs'])} output rows")
     elif p["op"] == "stencil":
+        g = p["gens"][0]
+        start = (f"seeded dense start field (rand seed {g['seed']}) in [0.9,1.1]" if g["kind"] == "rand"
+                 else f"corner block {g['hi'][0]}^3 in [0.9,1.1]")
         wl = (f"{p['name']}: 3D heat {p['mx']}^3 (n={W.n_state(p):.3g}) Dirichlet 7-point stencil, "
-              f"corner block {p['gens'][0]['hi'][0]}^3 in [0.9,1.1], {p['method'].capitalize()} k={p['k']}, "
+              f"{start}, {p['method'].capitalize()} k={p['k']}, "
               f"{p['n_steps']} steps of {p['step']}, {len(p['outs'])} output rows")
     else:
         sims = (f"{len(p['outs'])} transpose-dynamics simulations (P:544-568)" if p.get("sim") == "transpose"
@@ -235,6 +268,71 @@ def config_dict(p, n):
             "parallelism": f"zslab{n}" if n > 1 else "single-gpu", "l2": l2}
 
 
+def timed_runs(h, args, stream, barrier, local):
+    """W untimed passes, then K timed passes (barrier + synchronize on both sides, CUDA events on the library's
+    stream); the library's per-step event pairs give the step-kernel durations. Returns the raw timings."""
+    def one_step():
+        h.project(want=False)
+        return h.check_box(want_bounds=False)
+
+    import torch
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    barrier()
+    l0 = h.launch_count()
+    step_ms, iter_ms, per_step, per_step2 = [], [], [], []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            cb = one_step()
+            t = h.last_timing()
+            step_ms.append(t["step_ms_mean"])
+            iter_ms.append(t["iter_ms"])
+            st_ms = h.step_times()
+            # steps 3..k-1: the launches that move exactly 24 n_local bytes (steps 1-2 read the compact u_1 of
+            # the box generator, the last step writes nothing); the library times steps 1, 2 and six steps spread
+            # over 3..k-1 (every 16th step for k > 64) and returns NaN for the others
+            per_step.extend(x for x in (st_ms[2:-1] if len(st_ms) > 3 else st_ms) if np.isfinite(x))
+            per_step2.extend(x for x in (st_ms[1:-1] if len(st_ms) > 2 else st_ms) if np.isfinite(x))  # steps 2..k-1
+        ev1.record(stream)
+        barrier()
+    return {"elapsed": ev0.elapsed_time(ev1), "launches": h.launch_count() - l0, "step_ms": step_ms,
+            "iter_ms": iter_ms, "per_step": per_step, "per_step2": per_step2, "clocks": clk.summary(), "cb": cb}
+
+
+def fused_roofline(tm, timing, peak, peak_src, traffic, kernel_note=None):
+    """roofline object of the fused Lanczos step kernel: 24 n_local bytes per launch / mean launch duration."""
+    per_step = tm["per_step"]
+    sk = float(np.mean(per_step)) if per_step else float(np.mean(tm["step_ms"]))
+    achieved = timing["step_bytes"] / (sk * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "lz_step_kernel (fused Lanczos step)",
+            "algorithmic_bytes": "24 n_local per launch (read u_i, read u_{i-1}, write u_{i+1}); mean duration over "
+                                 "the launches of steps 3..k-1 of every timed run (steps 1-2 read the compact u_1 of a "
+                                 "box generator, the last writes nothing)",
+            "peak_source": peak_src}
+    if kernel_note:
+        roof["note"] = kernel_note
+    fused = {"gbs": achieved, "pct_of_peak": 100.0 * achieved / peak,
+             "pct_of_nominal_8tbs": 100.0 * achieved / 8000.0,  # BASELINE's ~8 TB/s datasheet figure
+             "ms_mean": sk,
+             "ms_median_steps_3_to_k-1": float(np.median(per_step)) if per_step else None,
+             "ms_median_steps_2_to_k-1": float(np.median(tm["per_step2"])) if tm["per_step2"] else None,
+             "ms_mean_all_steps": float(np.mean(tm["step_ms"])),
+             "bytes_per_launch": timing["step_bytes"], "launches_per_step": timing["step_launches"]}
+    return roof, fused
+
+
+def load_traffic(cfg):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(cfg)
+    except Exception:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -244,6 +342,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="C5: skip the dense-data companion measurement (C5D)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -267,7 +366,6 @@ def main():
     from paper_1804_01583_b200 import krylov_workspace_bytes
     wsb = krylov_workspace_bytes(p, **kw)
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
-    h = KrylovReach(p, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw)
 
     def attach(handle):
         """z-slab ranks: halo planes stored by the step kernel into the neighbours' buffers over NVLink (CUDA IPC),
@@ -277,63 +375,30 @@ def main():
             return handle.attach_peers(rank, world, torch_allgather_bytes, torch.distributed.barrier)
         return False
 
-    p2p_on = attach(h)
-
-    def one_step():
-        h.project(want=False)
-        return h.check_box(want_bounds=False)
-
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(max(3, args.warmup)):
-        one_step()
-    barrier()
-    l0 = h.launch_count()
-    step_ms, iter_ms = [], []
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        ev0.record(stream)
-        per_step, per_step2 = [], []
-        for _ in range(args.steps):
-            cb = one_step()
-            t = h.last_timing()
-            step_ms.append(t["step_ms_mean"])
-            iter_ms.append(t["iter_ms"])
-            st_ms = h.step_times()
-            # steps 3..k-1: the launches that move exactly 24 n_local bytes (steps 1-2 read the compact u_1 of
-            # the box generator, the last step writes nothing)
-            # (the library times steps 1, 2 and six steps spread over 3..k-1 — every 16th step for k > 64 —
-            # and returns NaN for the others)
-            per_step.extend(x for x in (st_ms[2:-1] if len(st_ms) > 3 else st_ms) if np.isfinite(x))
-            per_step2.extend(x for x in (st_ms[1:-1] if len(st_ms) > 2 else st_ms) if np.isfinite(x))  # steps 2..k-1
-        ev1.record(stream)
-        barrier()
-    launches = h.launch_count() - l0
-    elapsed = ev0.elapsed_time(ev1)
-    if world > 1:
-        tt = torch.tensor([elapsed], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        elapsed = float(tt.item())
+    def max_over_ranks(x):
+        if world > 1:
+            tt = torch.tensor([x], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            return float(tt.item())
+        return x
+
+    h = KrylovReach(p, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw)
+    p2p_on = attach(h)
+    tm = timed_runs(h, args, stream, barrier, local)
+    elapsed = max_over_ranks(tm["elapsed"])
     coeff, stats = h.project()
     k_eff = sum(s["k_eff"] for s in stats)  # Krylov steps of all directions in one pass
     ms_per_step = elapsed / args.steps
     value = k_eff / (ms_per_step / 1000.0)
     timing = h.last_timing()
-    n_local_bytes = timing["step_bytes"]
-    sk = float(np.mean(per_step)) if per_step else float(np.mean(step_ms))
-    achieved = n_local_bytes / (sk * 1e-3) / 1e9
     peak, peak_src = peaks()
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tr.get(args.config)
-    except Exception:
-        pass
+    roof, fused = fused_roofline(tm, timing, peak, peak_src, load_traffic(args.config))
+    fused["runs"] = args.steps
 
     # e2e: the same metric through the public API with host buffers: create (H2D of the problem) ->
     # project (D2H of all coefficients) -> check_box (D2H of bounds + counter-example) -> destroy.
@@ -360,47 +425,52 @@ def main():
                           "check_box_ms": (t3 - t2) * 1e3, "destroy_ms": (t4 - t3) * 1e3,
                           "barrier_ms": (t5 - t4) * 1e3})
             h2d, d2h = tb
-        e_sec = float(np.median(e_ms[1:])) / 1e3
-        if world > 1:
-            tt = torch.tensor([e_sec], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            e_sec = float(tt.item())
+        e_sec = max_over_ranks(float(np.median(e_ms[1:])) / 1e3)
         e2e = {"value": k_eff / e_sec, "unit": "Krylov steps/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_sec * 1e3,
                "phases_ms": parts[1:],
                "note": "wall clock of create+project+check_box+destroy on caller workspace, median of 3 calls after one "
                        "warm-up; includes CUDA-graph capture"}
     h.close()
+
+    # C5: the same recipe with a dense start vector (C5D: every Krylov vector dense from step 1, as in the paper's
+    # own 10^9 run) — the step kernel's roofline on realistic data, same handle layout and launch configuration
+    dense = None
+    if args.config == "C5" and not args.no_dense:
+        pd = W.CONFIGS["C5D"]()
+        hd = KrylovReach(pd, workspace=ws.data_ptr(), workspace_bytes=wsb, **kw)
+        attach(hd)
+        tmd = timed_runs(hd, args, stream, barrier, local)
+        el_d = max_over_ranks(tmd["elapsed"])
+        _, std = hd.project()
+        td = hd.last_timing()
+        roof_d, fused_d = fused_roofline(tmd, td, peak, peak_src, load_traffic("C5D"))
+        kd = sum(s["k_eff"] for s in std)
+        dense = {"config": config_dict(pd, world)["workload"], "value": kd / (el_d / args.steps / 1000.0),
+                 "unit": "Krylov steps/s", "ms_per_step": el_d / args.steps, "roofline": roof_d, "fused_step": fused_d,
+                 "clocks": tmd["clocks"], "gpu_launches": tmd["launches"]}
+        hd.close()
     if rank != 0:
         if world > 1:
+            comm.close()
             torch.distributed.destroy_process_group()
         return 0
     line = {
         "metric": METRIC, "value": value, "unit": "Krylov steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(p, world),
-        "fused_step": {"gbs": achieved, "pct_of_peak": 100.0 * achieved / peak,
-                       "pct_of_nominal_8tbs": 100.0 * achieved / 8000.0,  # BASELINE's ~8 TB/s datasheet figure
-                       "ms_mean": sk,
-                       "ms_median_steps_3_to_k-1": float(np.median(per_step)) if per_step else None,
-                       "ms_median_steps_2_to_k-1": float(np.median(per_step2)) if per_step2 else None,
-                       "ms_mean_all_steps": float(np.mean(step_ms)),
-                       "runs": args.steps,
-                       "bytes_per_launch": n_local_bytes, "launches_per_step": timing["step_launches"]},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "lz_step_kernel (fused Lanczos step)",
-                     "algorithmic_bytes": "24 n_local per launch (read u_i, read u_{i-1}, write u_{i+1}); mean "
-                                          "duration over the launches of steps 3..k-1 of every timed run (steps 1-2 "
-                                          "read the compact u_1 of the box generator, the last writes nothing)",
-                     "peak_source": peak_src},
+        "fused_step": fused, "roofline": roof,
         "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "gpu_launches": tm["launches"],
+        "clocks": tm["clocks"],
         "halo_transport": ("peer-memory stores from the step kernel (NVLink, CUDA IPC)" if p2p_on else
                            ("NCCL send/recv" if world > 1 else "none (one rank)")),
-        "iter_ms_mean": float(np.mean(iter_ms)),
-        "verdict": {"found": cb["found"], "step": cb["step"]},
+        "iter_ms_mean": float(np.mean(tm["iter_ms"])),
+        "verdict": {"found": tm["cb"]["found"], "step": tm["cb"]["step"]},
     }
+    if dense is not None:
+        line["roofline_dense"] = dense["roofline"]
+        line["dense"] = dense
     if p["op"] == "csr" or p.get("b") is not None:  # stored-basis Arnoldi (C2, C2T, heater): CGS2 passes
         N = (p["n"] if p["op"] == "csr" else W.n_state(p)) + (1 if p.get("b") is not None else 0)
         # per step j of each direction: 4 passes over v_0..v_{j-1} (two CGS2 projections: dots + update each)
@@ -426,6 +496,8 @@ def main():
                             "lanczos_ms": timing["iter_ms"] - timing["large_ms"],
                             "note": "step kernel mean over steps 1, 2 and every 16th step of the run (CUDA events)"}
     if not args.no_cpu_baseline and world == 1:  # every config (oracle steps/s beside the GPU's)
+        del ws
+        torch.cuda.empty_cache()
         line["cpu_baseline"] = cpu_baseline(p, k_full=stats[0]["k_eff"])
     print(json.dumps(line), flush=True)
     if world > 1:

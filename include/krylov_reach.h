@@ -48,7 +48,7 @@ typedef enum { KR_OP_STENCIL7 = 0, KR_OP_CSR = 1 } kr_op;
 typedef enum { KR_AUTO = 0, KR_ARNOLDI = 1, KR_LANCZOS = 2 } kr_method;
 typedef enum { KR_PART_NONE = 0, KR_PART_ZSLAB = 1, KR_PART_DIRS = 2 } kr_partition;
 typedef enum { KR_GE = 0, KR_LE = 1, KR_EQ = 2, KR_NONE = 3 } kr_sense;
-typedef enum { KR_VEC_SPARSE = 0, KR_VEC_BOX = 1, KR_VEC_ALL = 2 } kr_vec_kind;
+typedef enum { KR_VEC_SPARSE = 0, KR_VEC_BOX = 1, KR_VEC_ALL = 2, KR_VEC_RAND = 3 } kr_vec_kind;
 /* Stencil boundary condition of one grid face (the paper's heat model, §5.3: all faces insulated
  * except x = 1, which exchanges heat with constant 0.5; SURVEY A1/A2 reconstruction, DESIGN R18):
  *  KR_BC_DIRICHLET: zero ghost value beyond the face (BASELINE configs; A = alpha L_h).
@@ -71,7 +71,12 @@ typedef enum { KR_SIM_FORWARD = 0, KR_SIM_TRANSPOSE = 1, KR_SIM_AUTO = 2 } kr_si
  * (P:447). Linear index of stencil cell (x,y,z) is x + mx*(y + my*z) (x fastest).
  *  KR_VEC_SPARSE: entries val[e] at idx[e] (e < nnz; duplicates add).
  *  KR_VEC_BOX:    value on the index box [lo, hi) (stencil: 3D; CSR: axis 0 only, lo[1..2]/hi[1..2] ignored).
- *  KR_VEC_ALL:    value everywhere (e.g. total heat). Never includes the lifted coordinate. */
+ *  KR_VEC_ALL:    value everywhere (e.g. total heat). Never includes the lifted coordinate.
+ *  KR_VEC_RAND:   a seeded dense field value * u_c over all n states, u_c = (mix(seed + (c+1) G) >> 11) 2^-53 in
+ *                 [0, 1) with c the linear index, G = 0x9E3779B97F4A7C15 and mix the splitmix64 finaliser
+ *                 (z ^= z >> 30; z *= 0xBF58476D1CE4E5B9; z ^= z >> 27; z *= 0x94D049BB133111EB; z ^= z >> 31),
+ *                 all mod 2^64. A synthetic dense start vector (the dense-data bench workload); only
+ *                 for generators and the center, forward simulations, no affine term (else KR_EINVAL). */
 typedef struct {
     int32_t kind;
     int64_t nnz;
@@ -79,6 +84,7 @@ typedef struct {
     const double* val;
     int64_t lo[3], hi[3];
     double value;
+    uint64_t seed;              /* KR_VEC_RAND only */
 } kr_vec;
 
 /* Opaque multi-GPU communicator (one process per GPU; NCCL over NVLink/NVSwitch). */

@@ -132,8 +132,27 @@ def _rows(p):
     return rows, keep
 
 
+def _rand_field(seed, n, value, chunk=1 << 24):
+    """The seeded dense field of include/krylov_reach.h KR_VEC_RAND, written out with numpy uint64 arithmetic
+    (mod 2^64): u_c = (splitmix64 finaliser of seed + (c+1) G) >> 11, times 2^-53, times value."""
+    out = np.empty(n)
+    G = np.uint64(0x9E3779B97F4A7C15)
+    M1, M2 = np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB)
+    s30, s27, s31, s11 = np.uint64(30), np.uint64(27), np.uint64(31), np.uint64(11)
+    for c0 in range(0, n, chunk):
+        c = np.arange(c0 + 1, min(n, c0 + chunk) + 1, dtype=np.uint64)
+        z = np.uint64(seed) + c * G
+        z = (z ^ (z >> s30)) * M1
+        z = (z ^ (z >> s27)) * M2
+        z = z ^ (z >> s31)
+        out[c0:c0 + len(c)] = (z >> s11).astype(np.float64) * (2.0 ** -53) * value
+    return out
+
+
 def _dense(v, p, n):
-    """Dense materialisation of a compact vector (box / all / sparse entries) of length n."""
+    """Dense materialisation of a compact vector (box / all / sparse entries / seeded field) of length n."""
+    if v["kind"] == "rand":
+        return _rand_field(int(v["seed"]), n, float(v["value"]))
     out = np.zeros(n)
     if v["kind"] == "all":
         out[:] = v["value"]
@@ -403,7 +422,6 @@ def krylov_project(p, method=None):
     nd = len(dirs)
     coeff = np.zeros((N + 1, o, nd))
     per_dir = []
-    T = N * p["step"]
     mu = gershgorin_mu(p)
     lemma = np.zeros(nd)
     for d, v in enumerate(dirs):
@@ -411,11 +429,9 @@ def krylov_project(p, method=None):
         X = expm_e1_times(r["H"], p["step"], N)  # (N+1) x k_eff
         coeff[:, :, d] = r["beta0"] * (X @ r["P"].T)  # c[j][r] = ||v|| (P x_j)_r
         r["X"] = X
-        # Lemma 1: ||v|| h_{k+1,k} e^{max(mu,0) T} int_0^T |e_k^T e^{Ht} e_1| dt, trapezoid
-        h = np.abs(X[:, -1])
-        integral = float(np.sum(0.5 * p["step"] * (h[1:] + h[:-1]))) if N > 0 else 0.0
-        base = r["beta0"] * r["h_next"] * integral
-        lemma[d] = 0.0 if base == 0.0 else base * _exp_or_inf(max(mu, 0.0) * T)
+        # Lemma 1 for the start vector v: ||v|| times the unit-vector bound
+        # h_{k+1,k} e^{max(mu,0) T} int_0^T |e_k^T e^{Ht} e_1| dt (trapezoid) of lemma1_bound
+        lemma[d] = r["beta0"] * lemma1_bound(r["h_next"], X, p["step"], mu) if N > 0 else 0.0
         per_dir.append(r)
     return {"coeff": coeff, "per_dir": per_dir, "lemma1": lemma, "mu": mu,
             "times": np.arange(N + 1) * p["step"]}

@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("KR_LIB_PATH") or os.path.join(HERE, "libkrylov_reach.so")  # override: A/B diagnostics
+LIB_PATH = os.path.join(HERE, "libkrylov_reach.so")  # the in-tree build, nothing else
 
 KR_OK, KR_EINVAL, KR_EDIM, KR_ENOMEM, KR_ECUDA, KR_ENCCL, KR_ENOTSYM, KR_EZERO, KR_ENONFINITE, KR_ESTATE = range(10)
 STATUS_NAMES = ["KR_OK", "KR_EINVAL", "KR_EDIM", "KR_ENOMEM", "KR_ECUDA", "KR_ENCCL", "KR_ENOTSYM", "KR_EZERO",
@@ -16,7 +16,7 @@ KR_OP_STENCIL7, KR_OP_CSR = 0, 1
 KR_AUTO, KR_ARNOLDI, KR_LANCZOS = 0, 1, 2
 KR_PART_NONE, KR_PART_ZSLAB, KR_PART_DIRS = 0, 1, 2
 KR_GE, KR_LE, KR_EQ, KR_NONE = 0, 1, 2, 3
-KR_VEC_SPARSE, KR_VEC_BOX, KR_VEC_ALL = 0, 1, 2
+KR_VEC_SPARSE, KR_VEC_BOX, KR_VEC_ALL, KR_VEC_RAND = 0, 1, 2, 3
 KR_BC_DIRICHLET, KR_BC_INSULATED, KR_BC_ROBIN = 0, 1, 2
 KR_K_MAX_FIXED_PADE, KR_K_MAX, KR_K_MAX_ARNOLDI = 64, 16384, 2048
 KR_SIM_FORWARD, KR_SIM_TRANSPOSE, KR_SIM_AUTO = 0, 1, 2
@@ -25,7 +25,7 @@ KR_IPC_BLOB_BYTES = 512
 
 class kr_vec(C.Structure):
     _fields_ = [("kind", C.c_int32), ("nnz", C.c_int64), ("idx", C.c_void_p), ("val", C.c_void_p),
-                ("lo", C.c_int64 * 3), ("hi", C.c_int64 * 3), ("value", C.c_double)]
+                ("lo", C.c_int64 * 3), ("hi", C.c_int64 * 3), ("value", C.c_double), ("seed", C.c_uint64)]
 
 
 class kr_problem(C.Structure):

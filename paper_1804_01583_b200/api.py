@@ -10,7 +10,7 @@ from . import _abi as A
 
 _METHOD = {"auto": A.KR_AUTO, "arnoldi": A.KR_ARNOLDI, "lanczos": A.KR_LANCZOS}
 _PART = {None: A.KR_PART_NONE, "none": A.KR_PART_NONE, "zslab": A.KR_PART_ZSLAB, "dirs": A.KR_PART_DIRS}
-_KIND = {"sparse": A.KR_VEC_SPARSE, "box": A.KR_VEC_BOX, "all": A.KR_VEC_ALL}
+_KIND = {"sparse": A.KR_VEC_SPARSE, "box": A.KR_VEC_BOX, "all": A.KR_VEC_ALL, "rand": A.KR_VEC_RAND}
 _SIM = {None: A.KR_SIM_FORWARD, "forward": A.KR_SIM_FORWARD, "transpose": A.KR_SIM_TRANSPOSE, "auto": A.KR_SIM_AUTO}
 
 
@@ -92,6 +92,8 @@ class _Marshal:
             kv.nnz, kv.idx, kv.val = idx.size, _p(idx), _p(val)
         else:
             kv.value = float(v["value"])
+            if v["kind"] == "rand":
+                kv.seed = int(v["seed"])
             if v["kind"] == "box":
                 lo, hi = list(v["lo"]) + [0] * (3 - len(v["lo"])), list(v["hi"]) + [0] * (3 - len(v["hi"]))
                 kv.lo = (C.c_int64 * 3)(*lo)

@@ -44,21 +44,40 @@ def needs_build():
     return any(os.path.getmtime(s) > t for s in SRCS + HDRS)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, out=None):
+    """Compile each translation unit in parallel (nvcc -c), then link the shared library. out: another
+    output path (A/B builds of kernel variants under scratch_libs/); the product loads only LIB."""
+    out = out or LIB
+    if out == LIB and not force and not needs_build():
         return LIB
     inc, lib = nccl_dirs()
-    cmd = [nvcc(), "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-           "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           "-o", LIB] + SRCS + ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
+    flags = [nvcc(), "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+             "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+             "-I", os.path.join(ROOT, "include"), "-I", inc] + os.environ.get("KR_NVCC_FLAGS", "").split()
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.basename(s) + ".o") for s in SRCS]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(so):
+        src, obj = so
+        return subprocess.run(flags + ["-c", "-o", obj, src], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(SRCS), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(one, zip(SRCS, objs)))
+    for r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libkrylov_reach.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out] + objs + \
+          ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libkrylov_reach.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
-    return LIB
+        raise RuntimeError("nvcc failed linking libkrylov_reach.so")
+    return out
 
 
 if __name__ == "__main__":

@@ -8,6 +8,7 @@
 #include <map>
 #include <mutex>
 #include <unordered_map>
+#include <unordered_set>
 #include <utility>
 
 #include "kr_internal.h"
@@ -63,7 +64,7 @@ void validate_vec(const kr_problem* p, const kr_vec& v, const char* what) {
             if (v.idx[e] < 0 || v.idx[e] >= n) KR_THROW(KR_EDIM, std::string(what) + ": index out of range");
             if (!finite(v.val[e])) KR_THROW(KR_ENONFINITE, std::string(what) + ": non-finite value");
         }
-    } else if (v.kind == KR_VEC_BOX || v.kind == KR_VEC_ALL) {
+    } else if (v.kind == KR_VEC_BOX || v.kind == KR_VEC_ALL || v.kind == KR_VEC_RAND) {
         if (!finite(v.value)) KR_THROW(KR_ENONFINITE, std::string(what) + ": non-finite value");
         if (v.kind == KR_VEC_BOX) {
             const int axes = p->op == KR_OP_STENCIL7 ? 3 : 1;
@@ -84,7 +85,7 @@ bool vec_is_zero(const kr_problem* p, const kr_vec& v) {
         return true;
     }
     if (v.value == 0.0) return true;
-    if (v.kind == KR_VEC_ALL) return n_state(p) == 0;
+    if (v.kind == KR_VEC_ALL || v.kind == KR_VEC_RAND) return n_state(p) == 0;
     const int axes = p->op == KR_OP_STENCIL7 ? 3 : 1;
     for (int a = 0; a < axes; ++a)
         if (v.hi[a] <= v.lo[a]) return true;
@@ -250,6 +251,7 @@ struct DevCache {
     std::mutex mu;
     std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;
     std::unordered_map<void*, std::pair<int, size_t>> live;
+    std::unordered_set<void*> exported;  // blocks exported over CUDA IPC: never recycled (peers may map them)
     size_t cached = 0;
 };
 DevCache& dev_cache() {
@@ -296,7 +298,14 @@ void* carve(kr_handle* h, size_t bytes) {
 template <class T>
 T* upload(kr_handle* h, const T* src, size_t count) {
     T* d = reinterpret_cast<T*>(dalloc(h, count * sizeof(T)));
-    if (count) KR_CUDA(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    // on the handle's (non-blocking) stream: a pageable source is staged before the call returns, and every
+    // consumer enqueued later on h->stream is ordered after the copy (a legacy-stream cudaMemcpy is not)
+    if (count) {
+        if (h->stream)
+            KR_CUDA(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+        else
+            KR_CUDA(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    }
     h->h2d_bytes += (int64_t)(count * sizeof(T));
     return d;
 }
@@ -306,6 +315,7 @@ DVec make_dvec(kr_handle* h, const kr_vec& v) {
     DVec d{};
     d.kind = v.kind;
     d.value = v.value;
+    d.seed = v.seed;
     for (int a = 0; a < 3; ++a) {
         d.lo[a] = v.lo[a];
         d.hi[a] = v.hi[a];
@@ -415,6 +425,15 @@ void validate(const kr_problem* p) {
     if (p->center) validate_vec(p, *p->center, "center");
     if (p->center && !has_affine(p) && vec_is_zero(p, *p->center)) KR_THROW(KR_EZERO, "center is zero (pass NULL)");
     for (int r = 0; r < p->n_out; ++r) validate_vec(p, p->out[r], "output row");
+    {  // the seeded dense field: a start vector of forward simulations only (no lifting, no transpose, no rows)
+        bool rnd = p->center && p->center->kind == KR_VEC_RAND;
+        for (int d = 0; d < p->n_gen; ++d) rnd |= p->gen[d].kind == KR_VEC_RAND;
+        for (int r = 0; r < p->n_out; ++r)
+            if (p->out[r].kind == KR_VEC_RAND) KR_THROW(KR_EINVAL, "KR_VEC_RAND is not allowed for output rows");
+        if (p->b_vec && p->b_vec->kind == KR_VEC_RAND) KR_THROW(KR_EINVAL, "KR_VEC_RAND is not allowed for b_vec");
+        if (rnd && (has_affine(p) || p->sim_dir == KR_SIM_TRANSPOSE))
+            KR_THROW(KR_EINVAL, "KR_VEC_RAND start vectors need forward simulations without an affine term");
+    }
     const int n_dir = p->n_gen + ((p->center || has_affine(p)) ? 1 : 0);
     if (n_dir < 1) KR_THROW(KR_EINVAL, "no directions");
 }
@@ -496,6 +515,9 @@ int n_dirs_of(const kr_problem* p) { return p->n_gen + ((p->center || has_affine
 
 bool transposed_mode(const kr_problem* p) {
     if (p->sim_dir == KR_SIM_TRANSPOSE) return true;
+    if (p->center && p->center->kind == KR_VEC_RAND) return false;  // dense seeded start: forward only
+    for (int d = 0; d < p->n_gen; ++d)
+        if (p->gen[d].kind == KR_VEC_RAND) return false;
     if (p->sim_dir == KR_SIM_AUTO) return p->n_out < n_dirs_of(p);
     return false;
 }
@@ -675,7 +697,7 @@ void kr_dev_free(void* p) {
         if (it != c.live.end()) {
             const auto key = it->second;
             c.live.erase(it);
-            if (c.cached + key.second <= kCacheCap) {
+            if (c.exported.erase(p) == 0 && c.cached + key.second <= kCacheCap) {
                 c.free_blocks[key].push_back(p);
                 c.cached += key.second;
                 return;
@@ -683,6 +705,14 @@ void kr_dev_free(void* p) {
         }
     }
     cudaFree(p);
+}
+
+// A block whose IPC handle was given to peer processes goes straight back to the driver at its free (no reuse
+// by a new handle while a peer may still store halo planes into it). No-op for memory the library does not own.
+void kr_dev_mark_exported(void* base) {
+    DevCache& c = dev_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (c.live.count(base)) c.exported.insert(base);
 }
 
 extern "C" {
@@ -1374,11 +1404,21 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                         kc = kn;
                     }
                     if (by_bound && i > accepted) {  // speculative steps past the accepted checkpoint
-                        KR_CUDA(cudaStreamSynchronize(h->stream));
+                        // the direction's state becomes that of the sequential schedule stopped at kc: k_eff = kc,
+                        // h_next = beta_kc, done; a status (non-finite) set by a discarded step is dropped with it
+                        // (a status of the steps up to kc was caught by read_sc before the evaluation)
+                        LzScalars sc = read_sc(dl);
                         const int32_t ka = accepted;
+                        double hn = 0.0;
+                        KR_CUDA(cudaMemcpy(&hn, h->d_lzarr + (size_t)dl * 3 * (h->k + 2) + (h->k + 2) + ka, 8,
+                                           cudaMemcpyDeviceToHost));
+                        sc.status = 0;
+                        sc.done = 1;
+                        sc.k_eff = ka;
+                        sc.h_next = hn;
+                        KR_CUDA(cudaMemcpyAsync(h->d_sc + dl, &sc, sizeof(LzScalars), cudaMemcpyHostToDevice, h->stream));
                         KR_CUDA(cudaMemcpyAsync(h->d_keff + dl, &ka, 4, cudaMemcpyHostToDevice, h->stream));
-                        KR_CUDA(cudaMemcpyAsync(h->d_hnext + dl, h->d_lzarr + (size_t)dl * 3 * (h->k + 2) + (h->k + 2) + ka,
-                                                8, cudaMemcpyDeviceToDevice, h->stream));
+                        KR_CUDA(cudaMemcpyAsync(h->d_hnext + dl, &hn, 8, cudaMemcpyHostToDevice, h->stream));
                         KR_CUDA(cudaStreamSynchronize(h->stream));
                         if (dl == 0) h->steps_run0 = i;
                     }

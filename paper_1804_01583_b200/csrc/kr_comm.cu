@@ -160,6 +160,7 @@ void kr_p2p_blob(kr_handle* h, void* out) {
     b.my = h->my;
     b.device = h->device;
     KR_CUDA(cudaIpcGetMemHandle(&b.handle, reinterpret_cast<void*>(base)));
+    kr_dev_mark_exported(reinterpret_cast<void*>(base));
     for (int k = 0; k < 3; ++k) b.off[k] = reinterpret_cast<char*>(sl.u[k]) - reinterpret_cast<char*>(base);
     memset(out, 0, KR_IPC_BLOB_BYTES);
     memcpy(out, &b, sizeof(b));

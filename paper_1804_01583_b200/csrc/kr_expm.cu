@@ -488,7 +488,9 @@ __global__ void __launch_bounds__(256) lemma_kernel(const double* hlast, const d
         double integral = 0.0;
         for (int t = 0; t < 256; ++t) integral += red[t];
         const double T = (double)n_steps * step;
-        lemma[d] = beta0[d] * hnext[d] * exp(fmax(mu, 0.0) * T) * integral;
+        // an exact breakdown (h_{k+1,k} = 0) gives 0 even when e^{mu T} overflows (no 0 * inf = NaN)
+        const double base = beta0[d] * hnext[d] * integral;
+        lemma[d] = base == 0.0 ? 0.0 : base * exp(fmax(mu, 0.0) * T);
     }
 }
 

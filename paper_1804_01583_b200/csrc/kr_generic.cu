@@ -32,7 +32,8 @@ __global__ void fill_grid_kernel(double* dst, int64_t mx, int64_t my, int64_t pi
         const int64_t y = rem / pitch, x = rem - y * pitch;
         const int64_t gz = zbase + b;
         double val = 0.0;
-        if (x < mx && gz >= 0 && gz < mz) val = box_value(v, x, y, gz);
+        if (x < mx && gz >= 0 && gz < mz)
+            val = v.kind == KR_VEC_RAND ? kr_rand_entry(v.seed, x + mx * (y + my * gz), v.value) : box_value(v, x, y, gz);
         dst[e] = val;
     }
 }
@@ -68,7 +69,9 @@ __global__ void fill_dense_kernel(double* dst, int64_t N, int64_t n, int64_t mx,
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N; c += (int64_t)gridDim.x * blockDim.x) {
         double val = 0.0;
         if (c < n) {
-            if (stencil) {
+            if (v.kind == KR_VEC_RAND) {
+                val = kr_rand_entry(v.seed, c, v.value);
+            } else if (stencil) {
                 const int64_t z = c / (mx * my), rem = c - z * mx * my;
                 const int64_t y = rem / mx, x = rem - y * mx;
                 val = box_value(v, x, y, z);
@@ -102,6 +105,8 @@ __global__ void fill_dirs_kernel(double* V, int64_t vstride, int64_t N, int64_t 
                 if (v.idx[mid] < c) lo = mid + 1; else hi = mid;
             }
             if (lo < v.nnz && v.idx[lo] == c) val = v.val[lo];
+        } else if (v.kind == KR_VEC_RAND) {
+            val = kr_rand_entry(v.seed, c, v.value);
         } else if (stencil) {
             const int64_t z = c / (mx * my), rem = c - z * mx * my;
             const int64_t y = rem / mx, x = rem - y * mx;

@@ -47,7 +47,17 @@ struct DVec {
     const double* val;
     int64_t lo[3], hi[3];
     double value;
+    uint64_t seed;  // KR_VEC_RAND
 };
+
+// KR_VEC_RAND entry c (include/krylov_reach.h): value * (splitmix64(seed + (c + 1) G) >> 11) * 2^-53
+__host__ __device__ __forceinline__ double kr_rand_entry(uint64_t seed, int64_t c, double value) {
+    uint64_t z = seed + (uint64_t)(c + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return value * ((double)(z >> 11) * 0x1.0p-53);
+}
 
 struct BoxRow {  // a KR_VEC_BOX / KR_VEC_ALL output row as seen by the fused kernel (global coords)
     int32_t lo[3], hi[3];
@@ -279,6 +289,7 @@ void kr_fill_dense(cudaStream_t s, double* dst, int64_t N, int64_t n, int64_t mx
 // so destroy / create do not pay cudaFree / cudaMalloc (blocks above the 1 GiB cache cap are freed).
 cudaError_t kr_dev_malloc(void** p, size_t bytes);
 void kr_dev_free(void* p);
+void kr_dev_mark_exported(void* base);  // an IPC-exported block: cudaFree at its free, never cached
 
 void kr_lz_encode_maps(kr_handle* h);
 void kr_lz_setup_compact(kr_handle* h);

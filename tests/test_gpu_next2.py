@@ -58,8 +58,12 @@ def test_transpose_config2_full_size():
         assert s["k_eff"] == r["k_eff"]
     ocb = oracle.check_box(p, res["coeff"], [])
     zlo, zhi = oracle.z_bounds(p)
-    ok, worst = bounds_close(cb["hi"], ocb["hi"], res["coeff"], zlo, zhi)
-    assert ok, worst
+    for side in ("lo", "hi"):
+        ok, worst = bounds_close(cb[side], ocb[side], res["coeff"], zlo, zhi)
+        assert ok, (side, worst)
+    # the Lemma-1 diagnostic of each transposed simulation (+inf on both sides: mu > 0 for the lifted A'^T)
+    from tests.test_gpu_parity import assert_lemma1
+    assert_lemma1(stats, res["lemma1"], "C2^T")
 
 
 @pytest.mark.parametrize("vs", [0, 2])

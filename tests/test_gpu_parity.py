@@ -22,8 +22,8 @@ def gpu_run(prob, thresholds=None, **kw):
     return coeff, stats, cb, launches
 
 
-def compare_full(prob, thresholds=None, method=None, **kw):
-    res = oracle.krylov_project(prob, method=method)
+def compare_full(prob, thresholds=None, method=None, res=None, **kw):
+    res = res if res is not None else oracle.krylov_project(prob, method=method)
     coeff, stats, cb, launches = gpu_run(prob, thresholds, method=method, **kw)
     assert launches > 0
     worst = assert_coeff(coeff, res["coeff"], prob["name"])
@@ -43,7 +43,20 @@ def compare_full(prob, thresholds=None, method=None, **kw):
     for d, (s, r) in enumerate(zip(stats, res["per_dir"])):
         assert s["k_eff"] == r["k_eff"], (d, s["k_eff"], r["k_eff"])
         assert abs(s["beta0"] - r["beta0"]) <= 1e-12 * r["beta0"]
+    assert_lemma1(stats, res["lemma1"], prob["name"])
     return coeff, res, cb, ocb, stats, worst
+
+
+def assert_lemma1(stats, orc, what=""):
+    """Lemma 1 diagnostic (P:709-720) per direction: the same value (1e-9 relative; both +inf where e^{mu T}
+    overflows for a lifted system, both exactly 0 on an exact breakdown)."""
+    for d, (s, o) in enumerate(zip(stats, orc)):
+        g = s["lemma1"]
+        assert not math.isnan(g), (what, d)
+        if math.isinf(o) or o == 0.0:
+            assert g == o, (what, d, g, o)
+        else:
+            assert abs(g - o) <= 1e-9 * abs(o), (what, d, g, o)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -66,24 +79,31 @@ def test_oscillator_paper_example():
     assert stats[0]["k_eff"] == 2 and stats[0]["h_next"] == 0.0  # exact breakdown
 
 
-def test_config2_csr_affine_sampled_full_size():
-    """BASELINE configs[1] at full size (n=20000 lifted to 20001, 21 directions, k=40, 2001 steps):
-    the oracle runs the full Arnoldi per direction and evaluates e^{H t_j} e_1 on sampled steps."""
+def test_config2_full_size_parity():
+    """BASELINE configs[1] at full size (n = 20000 lifted to 20001, 21 directions, k = 40, 2001 steps): every
+    coefficient, both bounds, the Lemma-1 diagnostic and the verdict of an oracle-chosen threshold (SURVEY A11 iv:
+    first violation mid-trajectory, >= 1e-6 relative margin from every step's bound) against the full oracle run."""
     p = W.config2()
-    from paper_1804_01583_b200 import KrylovReach
-    with KrylovReach(p) as h:
-        coeff, stats = h.project()
-    dirs = oracle.directions(p)
-    samples = [0, 1, 2, 7, 100, 999, 1500, 2000]
-    zlo, zhi = oracle.z_bounds(p)
-    for d in range(len(dirs)):
-        r = oracle.arnoldi(p, dirs[d], p["k"])
-        assert stats[d]["k_eff"] == r["k_eff"]
-        ref = np.array([r["beta0"] * r["P"] @ oracle.expm(r["H"] * (j * p["step"]))[:, 0] for j in samples])
-        S = np.max(np.abs(ref), axis=0)
-        got = coeff[samples, :, d]
-        tol = 1e-9 * np.maximum(np.abs(ref), 1e-3 * S[None, :])
-        assert np.all(np.abs(got - ref) <= tol), (d, np.max(np.abs(got - ref) / tol))
+    res = oracle.krylov_project(p)
+    ob = oracle.check_box(p, res["coeff"], [])
+    th = choose_threshold(ob["hi"][:, 0], W.GE)
+    coeff, res2, cb, ocb, stats, _ = compare_full(p, [(0, W.GE, th)], res=res)
+    assert cb["found"] and 0 < cb["step"] < p["n_steps"]
+
+
+def choose_threshold(series, sense, margin=1e-6):
+    """A threshold whose first violation falls mid-trajectory, at least margin (relative to the series scale)
+    away from the bound of every step (no ties within the parity tolerance, SURVEY §8(c) C-parity)."""
+    s = np.asarray(series, dtype=np.float64)
+    scale = float(np.max(np.abs(s)))
+    lo, hi = float(s.min()), float(s.max())
+    for f in np.linspace(0.5, 0.95, 46):
+        th = lo + f * (hi - lo) if sense == W.GE else hi - f * (hi - lo)
+        if np.min(np.abs(s - th)) >= margin * scale:
+            bad = s >= th if sense == W.GE else s <= th
+            if bad.any() and 0 < int(np.argmax(bad)) < len(s) - 1:
+                return float(th)
+    raise AssertionError("no threshold with margin")
 
 
 @pytest.mark.parametrize("cgs", ["0", "1"])
@@ -134,6 +154,46 @@ def test_config5_full_size_properties():
     assert abs(coeff[0, 1, 0] - b ** 3) <= 1e-12 * b ** 3  # total heat at t=0
     assert coeff[0, 2, 0] == 0.0 and abs(coeff[0, 3, 0] - 1.0) <= 1e-14
     assert np.all(np.diff(coeff[:, 1, 0]) <= 1e-9 * b ** 3)  # total heat non-increasing (up to tolerance)
+
+
+def test_config5_full_size_oracle_golden():
+    """BASELINE configs[4] (north_star's target) element by element at full size: 10^9 states, k = 30, 1001 steps,
+    four output rows, against tests/golden/C5_heat1000_oracle.json — the oracle's own full run (written by
+    scripts/gen_golden.py, which calls only oracle/). Every coefficient (1e-9 floored relative), both bounds,
+    beta0, k_eff, the tridiagonal H, the Lemma-1 diagnostic, and the verdict / step / row / witness of the BASELINE
+    threshold (center y >= 0.012: never) plus the oracle-chosen LE threshold on total heat (SURVEY A11 iv)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "C5_heat1000_oracle.json")
+    g = json.load(open(path))
+    p = W.config5()
+    assert (g["m"], g["k"], g["n_steps"], g["step"]) == (1000, p["k"], p["n_steps"], p["step"])
+    thresholds = [(int(r), int(s), float(t)) for (r, s, t) in g["thresholds"]]
+    orc = np.array(g["coeff"])[:, :, None]
+    from paper_1804_01583_b200 import KrylovReach
+    with KrylovReach(p) as h:
+        coeff, stats = h.project()
+        cb = h.check_box(thresholds)
+        H, P = h.krylov_data(0)
+    assert_coeff(coeff, orc, "C5 full size vs oracle golden")
+    assert stats[0]["k_eff"] == g["k_eff"] == 30
+    assert abs(stats[0]["beta0"] - g["beta0"]) <= 1e-12 * g["beta0"]
+    k = g["k_eff"]
+    assert np.allclose(np.diag(H[:k, :k]), g["alpha"], rtol=1e-9, atol=0)
+    assert np.allclose(np.diag(H[1:k + 1, :k]), g["beta"], rtol=1e-9, atol=0)
+    assert_lemma1(stats, [g["lemma1"]], "C5")
+    ocb = oracle.check_box(p, orc, thresholds)
+    zlo, zhi = oracle.z_bounds(p)
+    for side in ("lo", "hi"):
+        ok, worst = bounds_close(cb[side], ocb[side], orc, zlo, zhi)
+        assert ok, (side, worst)
+    v = g["verdict"]
+    assert cb["found"] == v["found"] == ocb["found"] and v["found"]
+    assert cb["step"] == v["step"] == ocb["step"] and cb["row"] == v["row"] == 1
+    assert 0 < v["step"] < p["n_steps"]
+    assert abs(cb["y"] - v["y"]) <= 1e-9 * abs(v["y"])
+    assert np.allclose(cb["z"], v["z"], rtol=1e-12, atol=0)
+    assert np.all(coeff[:, 0, 0] == 0.0)  # the BASELINE center row: exactly 0 at k = 30 (SURVEY A11)
 
 
 def test_config5_first_step_closed_form():
@@ -354,6 +414,35 @@ def test_virtual_slabs_two_planes_each():
     c8, _, _, _ = gpu_run(p, virtual_slabs=8, part="zslab")
     assert_coeff(c8, res["coeff"], "m=16 P=8 vs oracle")
     assert_coeff(c8, c1, "m=16 P=8 vs P=1")
+
+
+@pytest.mark.parametrize("vs", [0, 3])
+def test_dense_rand_start_vector(vs):
+    """A seeded dense start vector (KR_VEC_RAND, the C5D recipe at small size): the field is generated on the
+    device by the library's own counter-based generator and by the oracle's numpy one; every output (the center
+    row is non-vacuous here), bound, Lemma 1 and the verdict of an oracle-chosen threshold match; 1 and 3 slabs;
+    plus the stored-basis Arnoldi path on the same field."""
+    p = W.heat(45, 4, 25, n_steps=200, step=0.02, my=30, mz=20)
+    p["gens"] = [W.rand(5)]
+    res = oracle.krylov_project(p)
+    ob = oracle.check_box(p, res["coeff"], [])
+    th = choose_threshold(ob["hi"][:, 0], W.GE)
+    kw = dict(virtual_slabs=vs, part="zslab") if vs else {}
+    coeff, _, cb, _, stats, _ = compare_full(p, [(0, W.GE, th)], res=res, **kw)
+    assert np.all(coeff[:, 0, 0] != 0.0) and cb["found"]
+    if not vs:
+        compare_full(dict(p, k=15), method="arnoldi")
+
+
+def test_rand_vector_rejected_where_not_defined():
+    from paper_1804_01583_b200 import KrylovError, KrylovReach
+    p = W.heat(8, 2, 5)
+    for q in (dict(p, outs=[W.rand(1)]), dict(p, gens=[W.rand(1)], b=W.box((0, 0, 0), (1, 1, 1), 1.0))):
+        with pytest.raises(KrylovError) as e:
+            KrylovReach(q)
+        assert "KR_EINVAL" in str(e.value)
+    with pytest.raises(KrylovError):
+        KrylovReach(dict(p, gens=[W.rand(1)]), sim="transpose")
 
 
 def test_device_block_cache_reuse_and_release():

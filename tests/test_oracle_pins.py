@@ -404,6 +404,91 @@ def test_lemma1_sound_on_heat():
         assert err <= res["lemma1"][0] + 1e-13 * np.linalg.norm(v)
 
 
+def test_rand_field_splitmix64_reference_values():
+    """The seeded dense field (include/krylov_reach.h KR_VEC_RAND): u_c is the (c+1)-th output of SplitMix64
+    started at state `seed`, top 53 bits. Pinned to the generator's published first outputs for state 0
+    (0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F, 0xF88BB8A8724C81EC), the stream property
+    (seed + G shifts the stream by one), and uniformity on [0, 1)."""
+    ref = [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F, 0xF88BB8A8724C81EC]
+    u = oracle._rand_field(0, 4, 1.0)
+    assert [float(r >> 11) * 2.0 ** -53 for r in ref] == list(u)
+    G = 0x9E3779B97F4A7C15
+    a = oracle._rand_field(0, 1001, 2.5)
+    b = oracle._rand_field(G, 1000, 2.5)
+    assert np.array_equal(a[1:], b)
+    big = oracle._rand_field(12345, 1 << 20, 1.0)
+    assert big.min() >= 0.0 and big.max() < 1.0 and abs(big.mean() - 0.5) < 2e-3
+    p = W.heat(6, 2, 3)
+    assert np.array_equal(oracle.directions(dict(p, gens=[W.rand(7, 0.5)]))[0], oracle._rand_field(7, 216, 0.5))
+
+
+def _diag_csr(lams):
+    n = len(lams)
+    return {"op": "csr", "n": n, "row_ptr": np.arange(n + 1, dtype=np.int64), "col_idx": np.arange(n, dtype=np.int32),
+            "val": np.asarray(lams, dtype=np.float64), "b": None}
+
+
+@pytest.mark.parametrize("lams,v,k", [((-1.0, -2.0), (3.0, 4.0), 1), ((-1.0, -2.5, 0.3), (1.0, -2.0, 0.5), 2),
+                                      ((-0.5, -3.0, -1.2), (2.0, 1.0, -1.0), 2)])
+def test_lemma1_closed_form_value(lams, v, k):
+    """Lemma 1 as krylov_project reports it, against its value in closed form: A = diag(lams)
+    (so mu = max lams exactly), start v with ||v|| != 1. Lanczos is written out here from its definition
+    (alpha_1 = q1'Aq1, beta_1 = ||Aq1 - alpha_1 q1||, ...); for k = 1, x(t) = e^{alpha_1 t}; for k = 2 the
+    2 x 2 symmetric H has x_2(t) = beta_1 (e^{th1 t} - e^{th2 t}) / (th1 - th2) >= 0, integrated exactly.
+    bound = ||v|| h_{k+1,k} e^{max(mu,0) T} int_0^T |x_k| dt; the trapezoid rule is within ~d^2 |H|^2 / 12."""
+    A = np.diag(lams)
+    v = np.asarray(v, dtype=np.float64)
+    q1 = v / np.linalg.norm(v)
+    a1 = q1 @ A @ q1
+    r1 = A @ q1 - a1 * q1
+    b1 = np.linalg.norm(r1)
+    T, N = 2.0, 4000
+    if k == 1:
+        h_next = b1
+        integral = (math.exp(a1 * T) - 1.0) / a1
+    else:
+        q2 = r1 / b1
+        a2 = q2 @ A @ q2
+        h_next = np.linalg.norm(A @ q2 - a2 * q2 - b1 * q1)
+        tr, det = a1 + a2, a1 * a2 - b1 * b1
+        th1 = 0.5 * (tr + math.sqrt(tr * tr - 4 * det))
+        th2 = 0.5 * (tr - math.sqrt(tr * tr - 4 * det))
+        integral = b1 / (th1 - th2) * ((math.exp(th1 * T) - 1) / th1 - (math.exp(th2 * T) - 1) / th2)
+    exact = np.linalg.norm(v) * h_next * math.exp(max(max(lams), 0.0) * T) * integral
+    p = dict(_diag_csr(lams), name="diag", gens=[W.sparse(np.arange(len(v)), v)], z_lo=[1.0], z_hi=[1.0], center=None,
+             outs=[W.sparse([0], [1.0])], step=T / N, n_steps=N, k=k, method="lanczos", thresholds=[])
+    res = oracle.krylov_project(p)
+    assert res["per_dir"][0]["k_eff"] == k
+    assert abs(res["lemma1"][0] - exact) <= 2e-7 * exact, (res["lemma1"][0], exact)
+
+
+def test_output_rows_csr_box_all_sparse():
+    """P_{r,i} = C_r V_{*,i} (Alg. 4) with compact rows on a CSR operator, lifted and not: a box row
+    [lo, hi) (clipped to the unlifted length n: the lifted coordinate never belongs to an output row), an
+    all-ones row and a sparse row, against the dense row vector dotted with v by numpy."""
+    import ctypes as C
+    n = 50
+    rp, ci, va, _ = W.random_csr(n, 4, seed=5)
+    v = np.random.default_rng(9).standard_normal(n + 1)
+    rows = [W.box((3,), (17,), 0.5), W.box((-4,), (9,), 2.0), W.box((40,), (n + 7,), -1.5), W.box((20,), (20,), 1.0),
+            W.allv(0.25), W.sparse([0, 7, n - 1], [1.0, -2.0, 3.0])]
+    for b in (None, np.linspace(-0.1, 0.1, n)):
+        p = {"op": "csr", "n": n, "row_ptr": rp, "col_idx": ci, "val": va, "b": b, "outs": rows}
+        op = oracle.Operator(p)
+        N = n + (b is not None)
+        crow, keep = oracle._rows(p)
+        for r, row in enumerate(rows):
+            dense = np.zeros(N)
+            if row["kind"] == "box":
+                dense[max(row["lo"][0], 0):min(row["hi"][0], n)] = row["value"]
+            elif row["kind"] == "all":
+                dense[:n] = row["value"]
+            else:
+                dense[np.asarray(row["idx"])] = row["val"]
+            got = oracle.lib().oracle_row_dot(C.byref(op.s), C.byref(crow[r]), v[:N].ctypes.data)
+            assert abs(got - dense @ v[:N]) <= 1e-14 * (1 + np.abs(dense) @ np.abs(v[:N])), (r, b is None)
+
+
 def test_gershgorin_mu_upper_bounds_symmetric_part():
     rp, ci, va, dense = W.random_csr(30, 5, seed=21)
     b = np.random.default_rng(3).uniform(-0.1, 0.1, 30)
