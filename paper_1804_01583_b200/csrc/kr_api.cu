@@ -42,7 +42,7 @@ kr_status kr_comm_unique_id_impl(void* id128);
 kr_comm* kr_comm_create_impl(const void* id128, int32_t rank, int32_t world, int32_t device);
 void kr_comm_destroy_impl(kr_comm* c);
 size_t kr_box_cex_bytes();
-int kr_lz_occupancy(int TX, int TY);
+int kr_lz_occupancy(int TX, int TY, int kv);
 void kr_lz_prepare(kr_handle* h);
 void kr_expm_prepare(kr_handle* h);
 void kr_ge_prepare();
@@ -1028,6 +1028,9 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                     h->TY = ty;
                 }
             }
+            // step kernel: v2 (2 x 2 cells per thread) for 64-wide tiles; KR_STEP_V=1 keeps v1 (A/B)
+            h->step_kv = 1;
+            if (const char* e = getenv("KR_STEP_V")) h->step_kv = (atoi(e) == 1 || h->TX != 64) ? 1 : 2;
             int nsl = 1, W = h->world, R = h->rank;
             if (p->virtual_slabs > 1) {
                 nsl = p->virtual_slabs;
@@ -1037,7 +1040,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 W = 1;
                 R = 0;
             }
-            const int occ = std::max(1, kr_lz_occupancy(h->TX, h->TY));
+            const int occ = std::max(1, kr_lz_occupancy(h->TX, h->TY, h->step_kv));
             int dev_sms = 148;
             KR_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
             const char* env_zc = getenv("KR_ZCHUNK");

@@ -464,6 +464,431 @@ __global__ void __launch_bounds__(Geo<TX, TY>::NT, (TX * TY >= 2048) ? 1 : ((TX 
     lz_epilogue<G::NT>(a, acc, reinterpret_cast<double*>(smem), a.plane);
 }
 
+// ================================================================================================
+// Step kernel v2: 2 x 2 cells per thread.
+// Lane l owns the x-pair (x0 + 2l, x0 + 2l + 1), warp w the row pair (y0 + 2w, y0 + 2w + 1). The centre values
+// of a plane arrive as two 16-byte shared-memory loads; the in-pair x neighbours and the in-pair y neighbours are
+// registers; only the outer x neighbours (x - 1, x + 2), the outer rows and u_{i-1} are loaded: 15 shared-memory
+// instructions per 4 cells (v1, 4 cells strided in y per thread, every neighbour from shared memory: 36). The
+// products -w^T A w are kept per axis (sums of squared forward differences) and combined with the edge
+// coefficients once at the end of the kernel; the few face cells (ghost edges of low faces, the edges of high
+// faces) go to one face accumulator with their own coefficients (Dirichlet: c_a; insulated: 0; Robin: gamma).
+// The forward ring (top row: warp 0, one x-pair per lane; right column: warp 1, one cell per lane) is computed
+// beside the tile, as in v1.
+// ================================================================================================
+template <int TX, int TY>
+struct Geo2 {
+    static_assert(TX == 64, "v2 maps one x-pair per lane: TX = 64");
+    static constexpr int NT = 16 * TY;  // one warp per row pair
+    static constexpr int CW = TX + 4, CH = TY + 3;  // u_i box: x0-2 .. x0+TX+1, y0-1 .. y0+TY+1 (as v1)
+    static constexpr int PW = TX + 2, PH = TY + 1;  // u_{i-1} box: x0 .. x0+TX+1, y0 .. y0+TY (as v1)
+    static constexpr int WW = TX + 2, WH = TY + 1;  // w plane on the tile + forward ring, rows of 16-byte multiples
+    static constexpr int CBYTES = CW * CH * 8, PBYTES = PW * PH * 8;
+    static constexpr int POFF = ((CBYTES + 127) / 128) * 128;
+    static constexpr int STAGE = ((POFF + PBYTES + 127) / 128) * 128;
+    static constexpr int WBYTES = ((2 * WW * WH * 8 + 127) / 128) * 128;
+};
+
+template <int TX, int TY, int S>
+constexpr size_t step2_smem_bytes() {
+    return (size_t)S * Geo2<TX, TY>::STAGE + Geo2<TX, TY>::WBYTES + 8 * S + 16;
+}
+
+struct Acc2 {
+    double ww, sum;      // sum w^2, sum w
+    double dx, dy, dz;   // sums of squared forward differences per axis (coefficient c_a)
+    double face;         // face edge terms with their coefficients: gq[f] w^2
+};
+
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
+
+// BCM: 0 = Dirichlet everywhere; 1 = general faces, tile without x/y face cells (full, x0 > 0, y0 > 0): only the
+// per-plane z-face terms; 2 = general faces, per-cell diagonal corrections.
+template <int TX, int TY, int S, bool INIT, bool FULL, int BCM, bool HALO>
+__device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
+                                          unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
+                                          int zc0, int zc1, bool cta_box, Acc2& A, double* accb) {
+    using G = Geo2<TX, TY>;
+    constexpr int CW = G::CW, PW = G::PW, WW = G::WW;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int pfirst = zc0 - 1, plast = zc1 + 1;
+    const bool has_prev = a.has_prev != 0;
+    auto issue = [&](int p) {
+        const int s = (p - pfirst) % S;
+        unsigned char* st = smem + s * G::STAGE;
+        const bool lp = has_prev && p > pfirst && p < plast;  // u_{i-1} is needed on planes zc0..zc1 only
+        mbar_expect_tx(&bar[s], G::CBYTES + (lp ? G::PBYTES : 0));
+        tma_load_3d(st, tmC, x0 - 2 - a.shC[0], y0 - 1 - a.shC[1], p + 1 - a.shC[2], &bar[s]);
+        if (lp) tma_load_3d(st + G::POFF, tmP, x0 - a.shP[0], y0 - a.shP[1], p + 1 - a.shP[2], &bar[s]);
+    };
+    constexpr int ISSUER = G::NT - 32;  // lane 0 of the last warp (warps 0-1 carry the ring)
+    if (tid == ISSUER) {
+        const int np = min(plast - pfirst + 1, S);
+        for (int p = pfirst; p < pfirst + np; ++p) issue(p);
+    }
+    double sa = 1.0, sb = 0.0, sp = 0.0;
+    if (!INIT) {
+        const LzScalars* sc = a.sc;
+        const int i = a.step;
+        sa = sc->s[i];
+        sb = sc->alpha[i] * sc->s[i];
+        sp = (i > 1) ? sc->beta[i - 1] * sc->s[i - 1] : 0.0;
+    }
+    const double diag = 2.0 * (a.cx + a.cy + a.cz);
+    const double scx = sa * a.cx, scy = sa * a.cy, scz = sa * a.cz;
+
+    const int rx = 2 * lane, ry = 2 * wid;  // tile coordinates of the thread's first cell
+    const int gx = x0 + rx, gy = y0 + ry;
+    const int cb = (ry + 1) * CW + rx + 2, pb = ry * PW + rx, wb = ry * WW + rx;
+    // cells c = 2 * row + column: (gx, gy), (gx + 1, gy), (gx, gy + 1), (gx + 1, gy + 1)
+    bool in[4];
+    in[0] = FULL || (gx < a.mx && gy < a.my);
+    in[1] = FULL || (gx + 1 < a.mx && gy < a.my);
+    in[2] = FULL || (gx < a.mx && gy + 1 < a.my);
+    in[3] = FULL || (gx + 1 < a.mx && gy + 1 < a.my);
+    // face cells: low faces in any tile at x0 = 0 / y0 = 0; high faces only in ragged (not FULL) tiles
+    const bool xlo = x0 == 0 && lane == 0;  // cells 0, 2
+    const bool ylo = y0 == 0 && wid == 0;   // cells 0, 1
+    const bool xhi0 = !FULL && gx == a.mx - 1, xhi1 = !FULL && gx + 1 == a.mx - 1;
+    const bool yhi0 = !FULL && gy == a.my - 1, yhi1 = !FULL && gy + 1 == a.my - 1;
+    double exy[4] = {0.0, 0.0, 0.0, 0.0};  // per-cell x/y diagonal corrections (BCM 2)
+    if (BCM == 2) {
+        const double ex0 = (gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0);
+        const double ex1 = (gx + 1 == a.mx - 1 ? a.ecor[1] : 0.0);
+        const double ey0 = (gy == 0 ? a.ecor[2] : 0.0) + (gy == a.my - 1 ? a.ecor[3] : 0.0);
+        const double ey1 = (gy + 1 == a.my - 1 ? a.ecor[3] : 0.0);
+        exy[0] = ex0 + ey0;
+        exy[1] = ex1 + ey0;
+        exy[2] = ex0 + ey1;
+        exy[3] = ex1 + ey1;
+    }
+    uint32_t bm[4] = {0u, 0u, 0u, 0u};
+    if (cta_box)
+        for (int c = 0; c < 4; ++c) {
+            const int cx_ = gx + (c & 1), cy_ = gy + (c >> 1);
+            for (int r = 0; r < a.nbox; ++r)
+                if (!((a.all_mask >> r) & 1u) && cx_ >= a.box[r].lo[0] && cx_ < a.box[r].hi[0] && cy_ >= a.box[r].lo[1] &&
+                    cy_ < a.box[r].hi[1])
+                    bm[c] |= 1u << r;
+        }
+    // forward ring: warp 0 = top row (x-pair per lane at tile row TY), warp 1 lanes < TY = right column (x = TX)
+    const bool rtop = wid == 0, rright = wid == 1 && lane < TY;
+    int rcb = 0, rpb = 0, rwb = 0;
+    bool rin0 = false, rin1 = false;
+    double rex0 = 0.0, rex1 = 0.0;
+    if (rtop) {
+        rcb = (TY + 1) * CW + rx + 2;
+        rpb = TY * PW + rx;
+        rwb = TY * WW + rx;
+        rin0 = FULL || (gx < a.mx && y0 + TY < a.my);
+        rin1 = FULL || (gx + 1 < a.mx && y0 + TY < a.my);
+        if (BCM) {
+            const double ey = (y0 + TY == 0 ? a.ecor[2] : 0.0) + (y0 + TY == a.my - 1 ? a.ecor[3] : 0.0);
+            rex0 = ey + (gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0);
+            rex1 = ey + (gx + 1 == a.mx - 1 ? a.ecor[1] : 0.0);
+        }
+    } else if (rright) {
+        rcb = (lane + 1) * CW + TX + 2;
+        rpb = lane * PW + TX;
+        rwb = lane * WW + TX;
+        rin0 = FULL || (x0 + TX < a.mx && y0 + lane < a.my);
+        if (BCM)
+            rex0 = (x0 + TX == a.mx - 1 ? a.ecor[1] : 0.0) + (y0 + lane == 0 ? a.ecor[2] : 0.0) +
+                   (y0 + lane == a.my - 1 ? a.ecor[3] : 0.0);
+    }
+    double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)gy * a.pitch + gx;
+    const bool st0 = FULL || (gx < a.mx && gy < a.my), st1 = FULL || (gx < a.mx && gy + 1 < a.my);
+
+    // u of three consecutive planes (4 cells + ring) in three register sets that take turns as u_{q-1}, u_q,
+    // u_{q+1}; w of two consecutive planes in two sets (w_{q-1}, w_q): the interior loop is unrolled by six
+    double U0[4], U1[4], U2[4], WA[4] = {0.0, 0.0, 0.0, 0.0}, WB[4] = {0.0, 0.0, 0.0, 0.0};
+    double2 R0 = make_double2(0.0, 0.0), R1 = R0, R2 = R0;
+    mbar_wait(&bar[0], 0);
+    mbar_wait(&bar[1 % S], 0);
+    {
+        const double* C0 = reinterpret_cast<const double*>(smem);
+        const double* C1 = reinterpret_cast<const double*>(smem + (1 % S) * G::STAGE);
+        double2 t = ld2(C0 + cb);
+        U0[0] = t.x; U0[1] = t.y;
+        t = ld2(C0 + cb + CW);
+        U0[2] = t.x; U0[3] = t.y;
+        t = ld2(C1 + cb);
+        U1[0] = t.x; U1[1] = t.y;
+        t = ld2(C1 + cb + CW);
+        U1[2] = t.x; U1[3] = t.y;
+        if (rtop) {
+            R0 = ld2(C0 + rcb);
+            R1 = ld2(C1 + rcb);
+        } else if (rright) {
+            R0.x = C0[rcb];
+            R1.x = C1[rcb];
+        }
+    }
+    int sq = 1 % S, sn = 2 % S;
+    uint32_t ph = (2 / S) & 1;
+    // one plane q: w_q on the tile (wc) and the ring (into the W buffer of q's parity), then the products of plane
+    // q - 1 (wp = w_{q-1}; its x+2 / row+2 neighbours from the W buffer written last iteration, its z+1 neighbour wc)
+    auto plane = [&](const double (&up)[4], const double (&uc)[4], double (&un)[4], const double2 rp, const double2 rc,
+                     double2& rn, const double (&wp)[4], double (&wc)[4], const int q) {
+        mbar_wait(&bar[sn], ph);
+        const unsigned char* stq = smem + sq * G::STAGE;
+        const double* Cq = reinterpret_cast<const double*>(stq);
+        const double* Pq = reinterpret_cast<const double*>(stq + G::POFF);
+        const double* Cn = reinterpret_cast<const double*>(smem + sn * G::STAGE);
+        {
+            const double2 t0 = ld2(Cn + cb), t1 = ld2(Cn + cb + CW);
+            un[0] = t0.x; un[1] = t0.y; un[2] = t1.x; un[3] = t1.y;
+        }
+        const int gzq = a.zoff + q;
+        double* Wq = (q & 1) ? Wb1 : Wb0;
+        const double dgz = BCM ? diag - (gzq == 0 ? a.ecor[4] : 0.0) - (gzq == a.mz - 1 ? a.ecor[5] : 0.0) : diag;
+        const double cf = fma(sa, dgz, sb);  // coefficient of u_i in w (this plane, no x/y face)
+        if (INIT) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) wc[c] = uc[c];
+        } else {
+            const double xm0 = Cq[cb - 1], xp0 = Cq[cb + 2], xm1 = Cq[cb + CW - 1], xp1 = Cq[cb + CW + 2];
+            const double2 ym = ld2(Cq + cb - CW), yp = ld2(Cq + cb + 2 * CW);
+            double cfc[4] = {cf, cf, cf, cf};
+            if (BCM == 2) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) cfc[c] = fma(sa, dgz - exy[c], sb);
+            }
+            // w = s_i (off-diagonal part of A u_i) - (s_i diag + alpha_i s_i) u_i - beta_{i-1} s_{i-1} u_{i-1}
+            wc[0] = fma(scx, xm0 + uc[1], fma(scy, ym.x + uc[2], fma(scz, up[0] + un[0], -cfc[0] * uc[0])));
+            wc[1] = fma(scx, uc[0] + xp0, fma(scy, ym.y + uc[3], fma(scz, up[1] + un[1], -cfc[1] * uc[1])));
+            wc[2] = fma(scx, xm1 + uc[3], fma(scy, uc[0] + yp.x, fma(scz, up[2] + un[2], -cfc[2] * uc[2])));
+            wc[3] = fma(scx, uc[2] + xp1, fma(scy, uc[1] + yp.y, fma(scz, up[3] + un[3], -cfc[3] * uc[3])));
+            if (has_prev) {
+                const double2 p0 = ld2(Pq + pb), p1 = ld2(Pq + pb + PW);
+                wc[0] = fma(-sp, p0.x, wc[0]);
+                wc[1] = fma(-sp, p0.y, wc[1]);
+                wc[2] = fma(-sp, p1.x, wc[2]);
+                wc[3] = fma(-sp, p1.y, wc[3]);
+            }
+        }
+        if (!FULL) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (!in[c]) wc[c] = 0.0;
+        }
+        st2(Wq + wb, wc[0], wc[1]);
+        st2(Wq + wb + WW, wc[2], wc[3]);
+        if (rtop) {
+            rn = ld2(Cn + rcb);
+            double r0 = rc.x, r1 = rc.y;
+            if (!INIT) {
+                const double xm = Cq[rcb - 1], xp = Cq[rcb + 2];
+                const double2 ym = ld2(Cq + rcb - CW), yp = ld2(Cq + rcb + CW);
+                const double c0 = BCM ? fma(sa, dgz - rex0, sb) : cf, c1 = BCM ? fma(sa, dgz - rex1, sb) : cf;
+                r0 = fma(scx, xm + rc.y, fma(scy, ym.x + yp.x, fma(scz, rp.x + rn.x, -c0 * rc.x)));
+                r1 = fma(scx, rc.x + xp, fma(scy, ym.y + yp.y, fma(scz, rp.y + rn.y, -c1 * rc.y)));
+                if (has_prev) {
+                    const double2 pv = ld2(Pq + rpb);
+                    r0 = fma(-sp, pv.x, r0);
+                    r1 = fma(-sp, pv.y, r1);
+                }
+            }
+            if (!FULL) {
+                if (!rin0) r0 = 0.0;
+                if (!rin1) r1 = 0.0;
+            }
+            st2(Wq + rwb, r0, r1);
+        } else if (rright) {
+            rn.x = Cn[rcb];
+            double r0 = rc.x;
+            if (!INIT) {
+                const double c0 = BCM ? fma(sa, dgz - rex0, sb) : cf;
+                r0 = fma(scx, Cq[rcb - 1] + Cq[rcb + 1],
+                         fma(scy, Cq[rcb - CW] + Cq[rcb + CW], fma(scz, rp.x + rn.x, -c0 * rc.x)));
+                if (has_prev) r0 = fma(-sp, Pq[rpb], r0);
+            }
+            if (!FULL && !rin0) r0 = 0.0;
+            Wq[rwb] = r0;
+        }
+        if (q > zc0) {  // products of plane q - 1 (its ring / x+2 / row+2 neighbours were written last iteration)
+            const double* Wp = ((q & 1) ? Wb0 : Wb1) + wb;
+            const int gzp = gzq - 1;
+            const double xr0 = Wp[2], xr1 = Wp[WW + 2];
+            const double2 yu = ld2(Wp + 2 * WW);
+            double dx[4] = {wp[1] - wp[0], xr0 - wp[1], wp[3] - wp[2], xr1 - wp[3]};
+            const double dy[4] = {wp[2] - wp[0], wp[3] - wp[1], yu.x - wp[2], yu.y - wp[3]};
+            if (!FULL) {  // high x / y faces: the edge to the (zero) ghost takes the face coefficient
+                if (xhi0) { dx[0] = 0.0; dx[2] = 0.0; A.face = fma(a.gq[1], fma(wp[0], wp[0], wp[2] * wp[2]), A.face); }
+                if (xhi1) { dx[1] = 0.0; dx[3] = 0.0; A.face = fma(a.gq[1], fma(wp[1], wp[1], wp[3] * wp[3]), A.face); }
+            }
+            double ddy[4] = {dy[0], dy[1], dy[2], dy[3]};
+            if (!FULL) {
+                if (yhi0) { ddy[0] = 0.0; ddy[1] = 0.0; A.face = fma(a.gq[3], fma(wp[0], wp[0], wp[1] * wp[1]), A.face); }
+                if (yhi1) { ddy[2] = 0.0; ddy[3] = 0.0; A.face = fma(a.gq[3], fma(wp[2], wp[2], wp[3] * wp[3]), A.face); }
+            }
+            if (xlo) A.face = fma(a.gq[0], fma(wp[0], wp[0], wp[2] * wp[2]), A.face);  // ghost edges of the low faces
+            if (ylo) A.face = fma(a.gq[2], fma(wp[0], wp[0], wp[1] * wp[1]), A.face);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                A.ww = fma(wp[c], wp[c], A.ww);
+                A.sum += wp[c];
+                A.dx = fma(dx[c], dx[c], A.dx);
+                A.dy = fma(ddy[c], ddy[c], A.dy);
+            }
+            if (gzp == a.mz - 1) {  // the z+1 neighbour is the zero ghost above the grid: face coefficient gq[5]
+                A.face = fma(a.gq[5], fma(wp[0], wp[0], fma(wp[1], wp[1], fma(wp[2], wp[2], wp[3] * wp[3]))), A.face);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double dz = wc[c] - wp[c];
+                    A.dz = fma(dz, dz, A.dz);
+                }
+            }
+            if (gzp == 0)
+                A.face = fma(a.gq[4], fma(wp[0], wp[0], fma(wp[1], wp[1], fma(wp[2], wp[2], wp[3] * wp[3]))), A.face);
+            const bool wr = !INIT && a.write_out;
+            if (wr) {
+                if (st0) st2(optr, wp[0], wp[1]);
+                if (st1) st2(optr + a.pitch, wp[2], wp[3]);
+            }
+            if (cta_box) {  // box output rows meeting this tile and plane (uniform, rare)
+                uint32_t zmask = 0;
+                for (int r = 0; r < a.nbox; ++r)
+                    if (gzp >= a.box[r].lo[2] && gzp < a.box[r].hi[2]) zmask |= 1u << r;
+                if (zmask) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const uint32_t mk = bm[c] & zmask;
+                        if (mk) {
+#pragma unroll
+                            for (int r = 0; r < KR_MAX_BOX; ++r)
+                                if ((mk >> r) & 1u) accb[r] += wp[c];
+                        }
+                    }
+                }
+            }
+            // halo planes for the neighbours, stored where they will be read (uniform per plane, rare): owned
+            // planes 0, 1 -> the lower neighbour, the last owned plane -> the upper neighbour
+            const int qq = q - 1;
+            if (HALO && wr && ((a.rlo && qq < 2) || (a.rhi && qq == a.nz - 1))) {
+                const int64_t off = (optr - a.out) - (int64_t)(qq + 1) * a.plane;  // in-plane offset of cell 0
+                if (a.rlo && qq < 2) {
+                    double* d = a.rlo + a.rlo_plane0 + (int64_t)qq * a.plane + off;
+                    if (st0) st2(d, wp[0], wp[1]);
+                    if (st1) st2(d + a.pitch, wp[2], wp[3]);
+                }
+                if (a.rhi && qq == a.nz - 1) {
+                    double* d = a.rhi + off;
+                    if (st0) st2(d, wp[0], wp[1]);
+                    if (st1) st2(d + a.pitch, wp[2], wp[3]);
+                }
+            }
+            optr += a.plane;
+        }
+        __syncthreads();
+        if (tid == ISSUER) {
+            if (q == zc0 && pfirst + S <= plast) issue(pfirst + S);
+            if (q + S <= plast) issue(q + S);
+        }
+        sq = sn;
+        if (++sn == S) {
+            sn = 0;
+            ph ^= 1u;
+        }
+    };
+    constexpr bool UNROLL = FULL && BCM < 2;
+    if (UNROLL) {
+        for (int q = zc0;;) {
+            plane(U0, U1, U2, R0, R1, R2, WA, WB, q);
+            if (++q > zc1) break;
+            plane(U1, U2, U0, R1, R2, R0, WB, WA, q);
+            if (++q > zc1) break;
+            plane(U2, U0, U1, R2, R0, R1, WA, WB, q);
+            if (++q > zc1) break;
+            plane(U0, U1, U2, R0, R1, R2, WB, WA, q);
+            if (++q > zc1) break;
+            plane(U1, U2, U0, R1, R2, R0, WA, WB, q);
+            if (++q > zc1) break;
+            plane(U2, U0, U1, R2, R0, R1, WB, WA, q);
+            if (++q > zc1) break;
+        }
+    } else {
+#pragma unroll 1
+        for (int q = zc0; q <= zc1; ++q) {
+            plane(U0, U1, U2, R0, R1, R2, WA, WB, q);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                U0[c] = U1[c];
+                U1[c] = U2[c];
+                WA[c] = WB[c];
+            }
+            R0 = R1;
+            R1 = R2;
+        }
+    }
+}
+
+template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false>
+__global__ void __launch_bounds__(Geo2<TX, TY>::NT, (TY >= 32) ? 1 : 2)
+    lz_step_kernel2(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
+    using G = Geo2<TX, TY>;
+    if (a.sc->done) return;  // breakdown happened earlier: uniform early exit
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* Wb0 = reinterpret_cast<double*>(smem + S * G::STAGE);
+    double* Wb1 = Wb0 + G::WW * G::WH;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * G::STAGE + G::WBYTES);
+
+    const int tid = threadIdx.x;
+    Acc2 A{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    double accb[KR_MAX_BOX];
+#pragma unroll
+    for (int r = 0; r < KR_MAX_BOX; ++r) accb[r] = 0.0;
+    // Persistent CTAs: work items (x-tile, y-tile, z-chunk) dealt round-robin (fixed assignment, deterministic)
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+        const int xt = a.ix0 + item % a.gx, yt = a.iy0 + (item / a.gx) % a.gy, zt = a.iz0 + item / (a.gx * a.gy);
+        const int x0 = xt * TX, y0 = yt * TY;
+        const int zc0 = zt * a.zchunk;
+        const int zc1 = min(zc0 + a.zchunk, a.nz);
+        if (tid == 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        bool cta_box = false;
+        for (int r = 0; r < a.nbox; ++r)
+            if (!((a.all_mask >> r) & 1u) && a.box[r].lo[0] < x0 + TX && a.box[r].hi[0] > x0 &&
+                a.box[r].lo[1] < y0 + TY && a.box[r].hi[1] > y0 && a.box[r].lo[2] < a.zoff + zc1 &&
+                a.box[r].hi[2] > a.zoff + zc0)
+                cta_box = true;
+        if (x0 + TX < a.mx && y0 + TY < a.my) {
+            if (!BC)
+                lz_march2<TX, TY, S, INIT, true, 0, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, accb);
+            else if (x0 > 0 && y0 > 0)
+                lz_march2<TX, TY, S, INIT, true, 1, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, accb);
+            else
+                lz_march2<TX, TY, S, INIT, true, 2, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, accb);
+        } else {
+            lz_march2<TX, TY, S, INIT, false, BC ? 2 : 0, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1,
+                                                             cta_box, A, accb);
+        }
+        __syncthreads();  // every issued plane was consumed: the barriers can be recycled for the next item
+        if (tid == 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar[s])) : "memory");
+        }
+    }
+
+    if (HALO && a.rfence) __threadfence_system();  // peer-memory halo stores visible before the collective that follows
+    __syncthreads();
+    double acc[3 + KR_MAX_BOX];
+    acc[0] = A.ww;
+    acc[1] = fma(a.cx, A.dx, fma(a.cy, A.dy, fma(a.cz, A.dz, A.face)));  // -w^T A w
+    acc[2] = A.sum;
+#pragma unroll
+    for (int r = 0; r < KR_MAX_BOX; ++r) acc[3 + r] = accb[r];
+    lz_epilogue<G::NT>(a, acc, reinterpret_cast<double*>(smem), a.plane);
+}
+
 // Scalar update after the (global) reduction: fixed-order sum over the R rank/slab vectors, then
 // beta_i, alpha_{i+1}, s_{i+1}, H and P entries, breakdown test.
 __device__ void lz_finalize_dev(const double* rankvec, int R, int nq, int n_out, int step, int k, LzScalars* sc,
@@ -935,14 +1360,40 @@ static void set_smem_attr() {
                                  (int)step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
 }
 
+template <int TX, int TY, bool INIT, bool BC, bool HALO = false>
+static void set_smem_attr2() {
+    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel2<TX, TY, Stages<TX, TY>::S, INIT, BC, HALO>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)step2_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
+}
+
 template <int TX, int TY>
-static int occupancy_t() {
+static int occupancy_t(int kv) {
+    if constexpr (TX == 64) {
+        set_smem_attr2<TX, TY, false, false>();
+        set_smem_attr2<TX, TY, true, false>();
+        set_smem_attr2<TX, TY, false, true>();
+        set_smem_attr2<TX, TY, true, true>();
+        set_smem_attr2<TX, TY, false, false, true>();
+        set_smem_attr2<TX, TY, false, true, true>();
+    }
     set_smem_attr<TX, TY, false, false>();
     set_smem_attr<TX, TY, true, false>();
     set_smem_attr<TX, TY, false, true>();
     set_smem_attr<TX, TY, true, true>();
     set_smem_attr<TX, TY, false, false, true>();
     set_smem_attr<TX, TY, false, true, true>();
+    if constexpr (TX == 64) {
+        if (kv == 2) {
+            int n1 = 0, n2 = 0;
+            const size_t sm2 = step2_smem_bytes<TX, TY, Stages<TX, TY>::S>();
+            KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, false>,
+                                                                  Geo2<TX, TY>::NT, sm2));
+            KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, true>,
+                                                                  Geo2<TX, TY>::NT, sm2));
+            return n1 < n2 ? n1 : n2;
+        }
+    }
     int nb = 0, nb2 = 0;
     KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, false>,
                                                           Geo<TX, TY>::NT, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
@@ -951,15 +1402,15 @@ static int occupancy_t() {
     return nb < nb2 ? nb : nb2;
 }
 
-int kr_lz_occupancy(int TX, int TY) {
-    if (TX == 64 && TY == 32) return occupancy_t<64, 32>();
-    if (TX == 64 && TY == 16) return occupancy_t<64, 16>();
-    if (TX == 64 && TY == 8) return occupancy_t<64, 8>();
-    if (TX == 32 && TY == 8) return occupancy_t<32, 8>();
+int kr_lz_occupancy(int TX, int TY, int kv) {
+    if (TX == 64 && TY == 32) return occupancy_t<64, 32>(kv);
+    if (TX == 64 && TY == 16) return occupancy_t<64, 16>(kv);
+    if (TX == 64 && TY == 8) return occupancy_t<64, 8>(kv);
+    if (TX == 32 && TY == 8) return occupancy_t<32, 8>(1);
     return 1;
 }
 
-void kr_lz_prepare(kr_handle* h) { (void)kr_lz_occupancy(h->TX, h->TY); }
+void kr_lz_prepare(kr_handle* h) { (void)kr_lz_occupancy(h->TX, h->TY, h->step_kv); }
 
 // cmode: 0 = full state buffers; 1 = u_i is the compact u_1 (init pass / step 1); 2 = u_{i-1} is (step 2)
 static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf,
@@ -1077,6 +1528,30 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
         const dim3 grid = (cmode == 1 && init) ? dim3((unsigned)std::max<int64_t>(1, sl.cu1[dl].nitems), 1, 1) : sl.grid;
         constexpr int S = Stages<TX, TY>::S;
         const bool halo = a.rlo || a.rhi;  // this slab writes halo planes into a neighbour's buffer
+        if constexpr (TX == 64) {
+            if (h->step_kv == 2) {
+                const size_t smem2 = step2_smem_bytes<TX, TY, S>();
+                constexpr int NT2 = Geo2<TX, TY>::NT;
+                if (h->gen_bc) {
+                    if (init)
+                        lz_step_kernel2<TX, TY, S, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+                    else if (halo)
+                        lz_step_kernel2<TX, TY, S, false, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+                    else
+                        lz_step_kernel2<TX, TY, S, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+                } else {
+                    if (init)
+                        lz_step_kernel2<TX, TY, S, true, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+                    else if (halo)
+                        lz_step_kernel2<TX, TY, S, false, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+                    else
+                        lz_step_kernel2<TX, TY, S, false, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+                }
+                KR_CUDA(cudaGetLastError());
+                h->launches++;
+                return;
+            }
+        }
         if (h->gen_bc) {
             if (init)
                 lz_step_kernel<TX, TY, S, true, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);

@@ -62,8 +62,8 @@ def test_transpose_config2_full_size():
         ok, worst = bounds_close(cb[side], ocb[side], res["coeff"], zlo, zhi)
         assert ok, (side, worst)
     # the Lemma-1 diagnostic of each transposed simulation (+inf on both sides: mu > 0 for the lifted A'^T)
-    from tests.test_gpu_parity import assert_lemma1
-    assert_lemma1(stats, res["lemma1"], "C2^T")
+    from tests.test_gpu_parity import assert_lemma1, hmax_of
+    assert_lemma1(stats, res["lemma1"], "C2^T", T=p["n_steps"] * p["step"], mu=res["mu"], hmax=hmax_of(res["per_dir"]))
 
 
 @pytest.mark.parametrize("vs", [0, 2])
