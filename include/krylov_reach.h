@@ -284,6 +284,27 @@ kr_status krylov_comm_unique_id(void* id128);
 kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int32_t device, kr_comm** out);
 void krylov_comm_destroy(kr_comm* c);
 
+/* Direction sharding (KR_PART_DIRS): the global directions (generator columns of E, then the
+ * fixed direction v_f) that rank `rank` of `world` simulates — round robin, d = rank, rank + world,
+ * ... — written to HOST dirs[cap], count in *n. Its local direction dl is global direction rank + dl * world;
+ * the final gather places local block dl of rank w at global direction w + dl * world. Host only. KR_EINVAL on
+ * bad arguments (cap too small included). */
+kr_status krylov_dirs_of_rank(int32_t n_dir, int32_t world, int32_t rank, int32_t* dirs, int32_t cap, int32_t* n);
+
+/* Host transport: a communicator whose collectives are all-gathers of HOST buffers performed by the caller's
+ * function — fn(ctx, send, recv, bytes) must gather `bytes` bytes from every rank into recv in rank order
+ * (recv holds world * bytes; e.g. torch.distributed.all_gather_into_tensor over gloo) and return 0 (non-zero:
+ * the library call fails with KR_ENCCL). For several ranks sharing one GPU (NCCL needs one GPU per rank)
+ * and for testing the multi-rank path: the per-step scalar all-gather, the halo exchange (an all-gather of
+ * each rank's three boundary planes) and the direction-sharding gather are staged through pinned host memory
+ * with a stream synchronisation around each; no kernel ever waits on another process; the fixed-k run is
+ * not captured into a CUDA graph. The peer-memory halo transport (krylov_ipc_blob ...) works on top of it:
+ * the host all-gather that follows every step orders the halo stores. fn is called from the thread that
+ * calls krylov_project / krylov_check_box. Collective (every rank, same world).                         */
+typedef int32_t (*kr_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
+kr_status krylov_comm_create_host(int32_t rank, int32_t world, int32_t device, kr_allgather_fn fn, void* ctx,
+                                  kr_comm** out);
+
 /* ---- peer-memory halo transport (NVLink P2P through CUDA IPC; one process per GPU) --------------
  * With it the fused step kernel stores the halo planes of u_{i+1} straight into the neighbouring ranks'
  * state buffers (the compute and the exchange in one kernel), instead of a halo message after each step;

@@ -338,6 +338,15 @@ def krylov_zslab_range(mz, world, rank):
     return z0.value, z1.value
 
 
+def krylov_dirs_of_rank(n_dir, world, rank):
+    """Global directions simulated by `rank` under direction sharding (round robin; host only)."""
+    n = C.c_int32()
+    A.check(A.lib().krylov_dirs_of_rank(int(n_dir), int(world), int(rank), None, 0, C.byref(n)))
+    out = (C.c_int32 * max(1, n.value))()
+    A.check(A.lib().krylov_dirs_of_rank(int(n_dir), int(world), int(rank), out, n.value, C.byref(n)))
+    return [int(x) for x in out[:n.value]]
+
+
 def krylov_zslab_halo_plan(mz, world, rank):
     """Halo schedule of a z-slab rank: list of (is_send, peer, first_buffer_plane, nplanes)."""
     ops = (A.kr_halo_op * 4)()
@@ -365,10 +374,47 @@ class KrComm:
         self.ptr = ptr
         self.rank, self.world = rank, world
 
+    @classmethod
+    def host(cls, rank, world, device, allgather=None):
+        """Host-transport communicator (krylov_comm_create_host): the library's collectives become all-gathers
+        of host buffers done by `allgather(bytes) -> list of bytes` (default: torch.distributed over the
+        default group, e.g. gloo) — several ranks may share one GPU. Marshalling only: the callback moves
+        bytes, the library stages them."""
+        self = cls.__new__(cls)
+        gather = allgather or torch_allgather_raw
+
+        def fn(ctx, send, recv, nbytes):
+            try:
+                parts = gather(C.string_at(send, nbytes))
+                blob = b"".join(parts)
+                if len(blob) != nbytes * world:
+                    return 1
+                C.memmove(recv, blob, len(blob))
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+                return 1
+
+        self._fn = A.ALLGATHER_FN(fn)  # kept alive with the communicator
+        ptr = C.c_void_p()
+        A.check(A.lib().krylov_comm_create_host(int(rank), int(world), int(device), self._fn, None, C.byref(ptr)))
+        self.ptr = ptr
+        self.rank, self.world = rank, world
+        return self
+
     def close(self):
         if self.ptr:
             A.lib().krylov_comm_destroy(self.ptr)
             self.ptr = None
+
+
+def torch_allgather_raw(data):
+    """All-gather equal-length bytes over the default torch.distributed group (CPU tensors: gloo), rank order."""
+    import torch
+    import torch.distributed as dist
+    t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.numpy().tobytes() for o in out]
 
 
 def torch_allgather_bytes(data):

@@ -41,6 +41,7 @@ cudaError_t kr_event_record(cudaEvent_t e, cudaStream_t s) {
 kr_status kr_comm_unique_id_impl(void* id128);
 kr_comm* kr_comm_create_impl(const void* id128, int32_t rank, int32_t world, int32_t device);
 void kr_comm_destroy_impl(kr_comm* c);
+kr_comm* kr_comm_create_host_impl(int32_t rank, int32_t world, int32_t device, kr_allgather_fn fn, void* ctx);
 size_t kr_box_cex_bytes();
 int kr_lz_occupancy(int TX, int TY, int kv);
 void kr_lz_prepare(kr_handle* h);
@@ -365,8 +366,8 @@ int resolve_method(const kr_problem* p) {
 
 int local_dirs(const kr_problem* p, int n_dir, int rank, int world) {
     if (p->part != KR_PART_DIRS || world <= 1) return n_dir;
-    int c = 0;
-    for (int d = rank; d < n_dir; d += world) ++c;
+    int32_t c = 0;
+    if (krylov_dirs_of_rank(n_dir, world, rank, nullptr, 0, &c) != KR_OK) KR_THROW(KR_EINVAL, "direction partition");
     return c;
 }
 
@@ -738,6 +739,26 @@ size_t krylov_release_cached_memory(void) {
 
 const char* krylov_last_error(void) { return g_err.c_str(); }
 
+kr_status krylov_dirs_of_rank(int32_t n_dir, int32_t world, int32_t rank, int32_t* dirs, int32_t cap, int32_t* n) {
+    if (world < 1 || rank < 0 || rank >= world || n_dir < 0 || !n) {
+        kr_set_error("krylov_dirs_of_rank: bad arguments");
+        return KR_EINVAL;
+    }
+    int32_t c = 0;
+    for (int32_t d = rank; d < n_dir; d += world) {
+        if (dirs) {
+            if (c >= cap) {
+                kr_set_error("krylov_dirs_of_rank: cap too small");
+                return KR_EINVAL;
+            }
+            dirs[c] = d;
+        }
+        ++c;
+    }
+    *n = c;
+    return KR_OK;
+}
+
 kr_status krylov_zslab_range(int64_t mz, int32_t world, int32_t rank, int64_t* z0, int64_t* z1) {
     if (world < 1 || rank < 0 || rank >= world || mz < 1 || !z0 || !z1) {
         kr_set_error("krylov_zslab_range: bad arguments");
@@ -806,6 +827,14 @@ kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int
 }
 
 void krylov_comm_destroy(kr_comm* c) { kr_comm_destroy_impl(c); }
+
+kr_status krylov_comm_create_host(int32_t rank, int32_t world, int32_t device, kr_allgather_fn fn, void* ctx,
+                                  kr_comm** out) {
+    return guarded([&] {
+        if (!fn || !out || world < 1 || rank < 0 || rank >= world) KR_THROW(KR_EINVAL, "bad comm arguments");
+        *out = kr_comm_create_host_impl(rank, world, device, fn, ctx);
+    });
+}
 
 static kr_status create_impl(const kr_problem* p, kr_handle** out);
 
@@ -910,8 +939,15 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             KR_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
             h->own_stream = true;
         }
-        for (int d = 0; d < h->n_dir; ++d)
-            if (p->part != KR_PART_DIRS || h->world <= 1 || d % h->world == h->rank) h->my_dirs.push_back(d);
+        if (p->part == KR_PART_DIRS && h->world > 1) {  // round robin (krylov_dirs_of_rank)
+            int32_t cnt = 0;
+            krylov_dirs_of_rank(h->n_dir, h->world, h->rank, nullptr, 0, &cnt);
+            h->my_dirs.resize((size_t)cnt);
+            if (krylov_dirs_of_rank(h->n_dir, h->world, h->rank, h->my_dirs.data(), cnt, &cnt) != KR_OK)
+                KR_THROW(KR_EINVAL, "direction partition");
+        } else {
+            for (int d = 0; d < h->n_dir; ++d) h->my_dirs.push_back(d);
+        }
         const int ndl = (int)h->my_dirs.size();
         // directions and box bounds
         for (int d = 0; d < p->n_gen; ++d) {
@@ -1029,7 +1065,8 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 }
             }
             // step kernel: v2 (2 x 2 cells per thread) for 64-wide tiles; KR_STEP_V=1 keeps v1 (A/B)
-            h->step_kv = 1;
+            // step kernel: v2 (2 x 2 cells per thread) for 64-wide tiles; KR_STEP_V=1 keeps v1 (A/B)
+            h->step_kv = h->TX == 64 ? 2 : 1;
             if (const char* e = getenv("KR_STEP_V")) h->step_kv = (atoi(e) == 1 || h->TX != 64) ? 1 : 2;
             int nsl = 1, W = h->world, R = h->rank;
             if (p->virtual_slabs > 1) {
@@ -1067,11 +1104,15 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 }
                 const int64_t gx = (h->mx + h->TX - 1) / h->TX, gy = (h->my + h->TY - 1) / h->TY;
                 const int64_t slots_total = (int64_t)dev_sms * occ;
-                // z-chunking: enough CTAs for ~full waves; each chunk re-reads 3 halo planes
+                // z-chunking: enough CTAs for ~full waves; each chunk re-reads 3 halo planes. Chunks of at most
+                // 80 planes: many short CTAs keep neighbouring tiles co-resident, so their halo rows are L2 hits
+                // (C5, v2 kernel: 143-plane chunks 3.89 ms per step, 72-plane 3.70 ms; profiles/r02_zchunk.txt)
                 int best_zc = (int)sl.nz;
                 double best_cost = 1e300;
+                const int64_t zc_max = h->step_kv == 2 ? 80 : (int64_t)sl.nz;
                 for (int nzc = 1; nzc <= 256 && nzc <= sl.nz; ++nzc) {
                     const int64_t zc = (sl.nz + nzc - 1) / nzc;
+                    if (zc > zc_max && nzc < 256 && nzc < sl.nz) continue;
                     const int64_t nch = (sl.nz + zc - 1) / zc;
                     const int64_t nb = gx * gy * nch;
                     const double waves = (double)nb / (double)slots_total;
@@ -1111,7 +1152,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             kr_lz_encode_maps(h);
             kr_lz_setup_compact(h);
             kr_lz_prepare(h);
-            const int R_total = (int)h->slabs.size() * h->world;
+            const int R_total = (int)h->slabs.size() * kr_zworld(h);
             h->d_rankvec = reinterpret_cast<double*>(dalloc(h, (size_t)R_total * h->nq * 8));
             h->d_sc = reinterpret_cast<LzScalars*>(dalloc(h, (size_t)ndl * sizeof(LzScalars)));
             h->d_lzarr = reinterpret_cast<double*>(dalloc(h, (size_t)ndl * 3 * (k + 2) * 8));
@@ -1441,7 +1482,8 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             KR_CUDA(cudaEventRecord(h->ev_it1, h->stream));
             post();
         };
-        const bool use_graph = getenv("KR_NO_GRAPH") == nullptr && !h->large_route;
+        // host transport: its collectives synchronise the stream on the host (no stream capture)
+        const bool use_graph = getenv("KR_NO_GRAPH") == nullptr && !h->large_route && !kr_comm_is_host(h->comm);
         if (h->large_route) {
             run_large();
         } else if (use_graph && !h->graph_ready) {

@@ -63,6 +63,7 @@ struct CgsArgs {
     int64_t n;
     const int64_t* longr;
     int n_long;
+    int prew;  // CSR: w = A v_{j-1} already in W (the block SpMM, kr_csr_spmm), all rows including long ones
     // ... or the 7-point stencil with per-face corrections and the lifted affine column bl
     int64_t mx, my, mz;
     double cx, cy, cz;
@@ -264,7 +265,9 @@ __global__ void __launch_bounds__(CT) cgs_apply_dots_kernel(CgsArgs a) {
     double* w = a.W + (int64_t)d * N;
     for (int64_t i = i0 + threadIdx.x; i < i1; i += CT) {
         double y = 0.0;
-        if (i < a.n) {  // the lifted row n of A' is zero
+        if (!STENCIL && a.prew) {
+            y = w[i];
+        } else if (i < a.n) {  // the lifted row n of A' is zero
             if (STENCIL) {
                 y = stencil_row(a, x, i);
             } else {
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(CT) cgs_apply_dots_kernel(CgsArgs a) {
         w[i] = y;
         S.ws[i - i0] = y;
     }
-    if (!STENCIL)
+    if (!STENCIL && !a.prew)
         for (int q = 0; q < a.n_long; ++q) {  // long rows (e.g. the b^T row of a transposed lift)
             const int64_t r = a.longr[q];
             if (r < i0 || r >= i1) continue;
@@ -521,10 +524,14 @@ void kr_cgs_step(kr_handle* h, int j, int ndl, double* scratch) {
         cgs_norm_kernel<<<grid, CT, 0, st>>>(a);
         chk();
     } else {
-        if (h->op == KR_OP_CSR)
+        if (h->op == KR_OP_CSR) {
+            // A streamed once for all directions (block SpMM into W), then the first projection pass
+            a.prew = getenv("KR_SPMM_PER_DIR") ? 0 : 1;
+            if (a.prew) kr_csr_spmm(h, h->d_V + (int64_t)(j - 1) * h->N, (int64_t)(h->k + 1) * h->N, h->d_W, h->N, ndl);
             cgs_apply_dots_kernel<0><<<grid, CT, sm, st>>>(a);
-        else
+        } else {
             cgs_apply_dots_kernel<1><<<grid, CT, sm, st>>>(a);
+        }
         chk();
         const dim3 rg((j + 127) / 128, ndl);
         if (a.red_sep) {

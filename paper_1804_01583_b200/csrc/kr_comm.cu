@@ -4,6 +4,8 @@
 // 128-byte ncclUniqueId that the caller broadcasts (torch.distributed) — no private torch API.
 #include <nccl.h>
 
+#include <algorithm>
+
 #include "kr_internal.h"
 
 #define KR_NCCL(call)                                                                                      \
@@ -35,15 +37,51 @@ kr_comm* kr_comm_create_impl(const void* id128, int32_t rank, int32_t world, int
     return k;
 }
 
+kr_comm* kr_comm_create_host_impl(int32_t rank, int32_t world, int32_t device, kr_allgather_fn fn, void* ctx) {
+    KR_CUDA(cudaSetDevice(device));
+    kr_comm* k = new kr_comm;
+    k->nccl = nullptr;
+    k->rank = rank;
+    k->world = world;
+    k->device = device;
+    k->host_fn = fn;
+    k->host_ctx = ctx;
+    return k;
+}
+
 void kr_comm_destroy_impl(kr_comm* c) {
     if (!c) return;
-    ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->nccl));
+    if (c->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->nccl));
+    if (c->pinned) cudaFreeHost(c->pinned);
     delete c;
 }
 
+namespace {
+// host transport: pinned staging buffer of at least n doubles (grown by doubling)
+double* host_stage(kr_comm* c, size_t n) {
+    if (c->pinned_doubles < n) {
+        if (c->pinned) KR_CUDA(cudaFreeHost(c->pinned));
+        c->pinned = nullptr;
+        const size_t cap = std::max<size_t>(n, 2 * c->pinned_doubles);
+        KR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->pinned), cap * sizeof(double)));
+        c->pinned_doubles = cap;
+    }
+    return c->pinned;
+}
+
+// all-gather of `count` doubles per rank through the caller's host function: send (count) -> pinned,
+// fn gathers world * count into pinned + count, which the caller of this helper reads
+double* host_allgather(kr_comm* c, size_t count) {
+    double* st = c->pinned;
+    if (c->host_fn(c->host_ctx, st, st + count, count * sizeof(double)) != 0)
+        KR_THROW(KR_ENCCL, "host all-gather callback failed");
+    return st + count;
+}
+}  // namespace
+
 // Asynchronous NCCL failures (a peer died, a link error) surface here instead of as a hang later.
 void kr_nccl_check(kr_comm* c) {
-    if (!c) return;
+    if (!c || !c->nccl) return;
     ncclResult_t async = ncclSuccess;
     KR_NCCL(ncclCommGetAsyncError(reinterpret_cast<ncclComm_t>(c->nccl), &async));
     if (async != ncclSuccess) KR_THROW(KR_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(async));
@@ -51,6 +89,15 @@ void kr_nccl_check(kr_comm* c) {
 
 // In-place all-gather: send = recv + rank * count.
 void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s) {
+    if (kr_comm_is_host(c)) {
+        double* st = host_stage(c, count * (size_t)(c->world + 1));
+        KR_CUDA(cudaMemcpyAsync(st, send, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+        KR_CUDA(cudaStreamSynchronize(s));
+        const double* g = host_allgather(c, count);
+        KR_CUDA(cudaMemcpyAsync(recv, g, count * c->world * sizeof(double), cudaMemcpyHostToDevice, s));
+        KR_CUDA(cudaStreamSynchronize(s));  // the staging buffer is reused by the next collective
+        return;
+    }
     KR_NCCL(ncclAllGather(send, recv, count, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), s));
 }
 
@@ -61,6 +108,26 @@ void kr_nccl_halo(kr_comm* c, kr_handle* h, int buf, cudaStream_t s) {
     ncclComm_t comm = reinterpret_cast<ncclComm_t>(c->nccl);
     Slab& sl = h->slabs[0];
     const size_t plane = (size_t)h->pitch * h->my;
+    if (kr_comm_is_host(c)) {
+        // every rank contributes its first two and its last owned planes (buffer planes 1, 2, nz); the lower
+        // neighbour's last plane becomes my plane 0, the upper neighbour's first two my planes nz+1, nz+2
+        // (the same exchange as krylov_zslab_halo_plan, as one all-gather)
+        const size_t cnt = 3 * plane;
+        double* st = host_stage(c, cnt * (size_t)(c->world + 1));
+        double* u = sl.u[buf];
+        KR_CUDA(cudaMemcpyAsync(st, u + plane, 2 * plane * sizeof(double), cudaMemcpyDeviceToHost, s));
+        KR_CUDA(cudaMemcpyAsync(st + 2 * plane, u + sl.nz * plane, plane * sizeof(double), cudaMemcpyDeviceToHost, s));
+        KR_CUDA(cudaStreamSynchronize(s));
+        const double* g = host_allgather(c, cnt);
+        if (c->rank > 0)
+            KR_CUDA(cudaMemcpyAsync(u, g + (size_t)(c->rank - 1) * cnt + 2 * plane, plane * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+        if (c->rank < c->world - 1)
+            KR_CUDA(cudaMemcpyAsync(u + (sl.nz + 1) * plane, g + (size_t)(c->rank + 1) * cnt, 2 * plane * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+        KR_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
     kr_halo_op ops[4];
     int32_t n = 0;
     if (krylov_zslab_halo_plan(h->mz, c->world, c->rank, ops, &n) != KR_OK) KR_THROW(KR_EINVAL, "halo plan");

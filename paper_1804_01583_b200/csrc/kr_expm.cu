@@ -62,7 +62,7 @@ struct ExpmArgs {
     double step;
     double* coeff;       // [(n_steps+1)][n_out][ndl_stride]
     double* hlast;       // [ndl][n_steps+1]
-    // single-direction use by the large-k route's small checkpoints (expm_doubling_kernel only)
+    // single-direction use by the large-k route's small checkpoints (doubling, powers and march kernels)
     int dsel = -1;               // >= 0: one CTA, for this local direction
     int nfix = 0;                // > 0: dimension (instead of keff)
     const double* Hsrc = nullptr;  // non-NULL: H from here, row stride hstride
@@ -376,8 +376,8 @@ constexpr int PW_LD = 65;
 constexpr size_t PW_MAT = (size_t)64 * PW_LD;
 
 __global__ void __launch_bounds__(ET) expm_powers_kernel(ExpmArgs a, double* pw, int Q) {
-    const int d = blockIdx.x;
-    const int n = a.keff[d];
+    const int d = a.dsel >= 0 ? a.dsel : blockIdx.x;
+    const int n = a.nfix > 0 ? a.nfix : a.keff[d];
     if (n <= 0 || a.n_steps < 1) return;
     const int k = a.k;
     extern __shared__ double sm[];
@@ -386,7 +386,8 @@ __global__ void __launch_bounds__(ET) expm_powers_kernel(ExpmArgs a, double* pw,
     __shared__ int sq_s;
     const int ld = n + 1;
     const int msz = n * ld;
-    double* E = pade13(a.H + (int64_t)d * (k + 1) * k, k, n, a.step, sm, fac, piv_s, sq_s);
+    const double* Hd = a.Hsrc ? a.Hsrc : a.H + (int64_t)d * (k + 1) * k;
+    double* E = pade13(Hd, a.Hsrc ? a.hstride : k, n, a.step, sm, fac, piv_s, sq_s);
     const int ei = (int)((E - sm) / msz);
     double* X = E;
     double* Y = sm + (size_t)(ei == 0 ? 1 : 0) * msz;
@@ -423,8 +424,8 @@ __device__ __forceinline__ void mv_rows(const double* M, int R, int n, const dou
 }
 
 __global__ void __launch_bounds__(ET) expm_march_kernel(ExpmArgs a, const double* pw, int Q, int B) {
-    const int d = blockIdx.y;
-    const int n = a.keff[d];
+    const int d = a.dsel >= 0 ? a.dsel : blockIdx.y;
+    const int n = a.nfix > 0 ? a.nfix : a.keff[d];
     const int k = a.k;
     const int64_t np1 = a.n_steps + 1;
     const int64_t c0 = (int64_t)blockIdx.x * B, c1 = min(c0 + B, np1);
@@ -547,7 +548,20 @@ void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, int 
     a.nfix = kc;
     a.Hsrc = Hdense;
     a.hstride = hstride;
-    expm_doubling_kernel<<<1, ET, (size_t)6 * kc * (kc + 1) * sizeof(double), h->stream>>>(a, xt, ldx);
+    if (h->d_pw && !h->expm_onecta) {
+        // E = e^{H delta} and its powers in one CTA, then the time grid over many CTAs (as kr_expm_enqueue): the
+        // one-CTA doubling took ~0.3 ms per checkpoint on one SM (81% of the paper-heat m = 100 adaptive run)
+        expm_powers_kernel<<<1, ET, (size_t)6 * kc * (kc + 1) * sizeof(double), h->stream>>>(a, h->d_pw, h->pw_q);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        const int64_t np1 = h->n_steps + 1;
+        const int64_t B = std::max<int64_t>(8, (np1 + 443) / 444);
+        const unsigned nseg = (unsigned)((np1 + B - 1) / B);
+        const size_t msm = ((size_t)(64 + KR_MAX_OUT) * PW_LD + 512) * sizeof(double);
+        expm_march_kernel<<<dim3(nseg, 1), ET, msm, h->stream>>>(a, h->d_pw, h->pw_q, (int)B);
+    } else {
+        expm_doubling_kernel<<<1, ET, (size_t)6 * kc * (kc + 1) * sizeof(double), h->stream>>>(a, xt, ldx);
+    }
     KR_CUDA(cudaGetLastError());
     h->launches++;
 }

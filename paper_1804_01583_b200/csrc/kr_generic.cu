@@ -161,6 +161,49 @@ __global__ void spmm_csr_kernel(const int64_t* __restrict__ rp, const int32_t* _
     }
 }
 
+// Block SpMM (Alg. 1 line 3, for every direction at once): Y[d] = A' X[d] with each CSR
+// row streamed ONCE per Krylov step for all local directions. A warp per row, lane = direction (a further pass per
+// 32 directions): the lanes load the row's entries 32 at a time (one coalesced request for val and for ci) and
+// broadcast them by shuffles; each lane gathers x_d[col] from its own direction's vector. Entries are summed in
+// row order as in spmm_csr_kernel, so the results are those of one thread per (row, direction), bit for bit.
+// The lifted row n of A' is zero; rows longer than KR_LONG_ROW are left to spmm_long_rows_kernel.
+__global__ void __launch_bounds__(256) spmm_block_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                         const double* __restrict__ val, const double* __restrict__ b,
+                                                         int64_t n, int64_t N, const double* __restrict__ X,
+                                                         int64_t xstride, double* __restrict__ Y, int64_t ystride,
+                                                         int ndl, const int32_t* __restrict__ done) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < N; r += nwarps) {
+        const int64_t e0 = r < n ? rp[r] : 0, e1 = r < n ? rp[r + 1] : 0;
+        if (e1 - e0 > KR_LONG_ROW) continue;
+        for (int d0 = 0; d0 < ndl; d0 += 32) {
+            const int d = d0 + lane;
+            const bool act = d < ndl && !done[d];
+            const double* x = X + (int64_t)(act ? d : 0) * xstride;
+            double s = 0.0;
+            for (int64_t eb = e0; eb < e1; eb += 32) {
+                const int cnt = (int)min((int64_t)32, e1 - eb);
+                double v = 0.0;
+                int c = 0;
+                if (lane < cnt) {
+                    v = val[eb + lane];
+                    c = ci[eb + lane];
+                }
+                for (int t = 0; t < cnt; ++t) {
+                    const double vt = __shfl_sync(0xffffffffu, v, t);
+                    const int ct = __shfl_sync(0xffffffffu, c, t);
+                    if (act) s = fma(vt, __ldg(&x[ct]), s);
+                }
+            }
+            if (act) {
+                if (r < n && b) s = fma(b[r], x[n], s);
+                Y[(int64_t)d * ystride + r] = s;
+            }
+        }
+    }
+}
+
 // rows with more than KR_LONG_ROW entries: one CTA per (long row, direction), fixed-order block reduction
 __global__ void spmm_long_rows_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                       const double* __restrict__ val, const double* __restrict__ b, int64_t n,
@@ -184,6 +227,30 @@ __global__ void spmm_long_rows_kernel(const int64_t* __restrict__ rp, const int3
         Y[(int64_t)d * ystride + r] = t;
     }
 }
+
+// Y[d] = A' X[d] for every local direction, one launch (+ the long rows): the block SpMM above; KR_SPMM_PER_DIR=1
+// keeps one thread per (row, direction) (A re-read per direction, from L2)
+void kr_csr_spmm(kr_handle* h, const double* X, int64_t xstride, double* Y, int64_t ystride, int ndl) {
+    const int64_t N = h->N;
+    if (getenv("KR_SPMM_PER_DIR")) {
+        const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
+        spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X, xstride, Y,
+                                                              ystride, ndl, h->d_done);
+    } else {
+        const int blocks = (int)std::min<int64_t>((N + 7) / 8, 148 * 16);
+        spmm_block_kernel<<<blocks, 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X, xstride, Y,
+                                                         ystride, ndl, h->d_done);
+    }
+    KR_CUDA(cudaGetLastError());
+    h->launches++;
+    if (h->n_long) {
+        spmm_long_rows_kernel<<<dim3((unsigned)h->n_long, ndl), 256, 0, h->stream>>>(
+            h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, h->d_long, X, xstride, Y, ystride, h->d_done);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+    }
+}
+
 
 __global__ void stencil_apply_kernel(int64_t mx, int64_t my, int64_t mz, double cx, double cy, double cz,
                                      const double* __restrict__ X, int64_t xstride, double* __restrict__ Y,
@@ -474,20 +541,13 @@ void kr_ge_enqueue_step(kr_handle* h, int j) {
         return;
     }
     if (h->op == KR_OP_CSR) {
-        spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X, vstride,
-                                                              h->d_W, N, ndl, h->d_done);
-        if (h->n_long) {
-            KR_CUDA(cudaGetLastError());
-            h->launches++;
-            spmm_long_rows_kernel<<<dim3((unsigned)h->n_long, ndl), 256, 0, h->stream>>>(
-                h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, h->d_long, X, vstride, h->d_W, N, h->d_done);
-        }
+        kr_csr_spmm(h, X, vstride, h->d_W, N, ndl);
     } else {
         stencil_apply_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->mx, h->my, h->mz, h->cx, h->cy, h->cz, X, vstride,
                                                                    h->d_W, N, h->d_done, fc, h->d_bl);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
     }
-    KR_CUDA(cudaGetLastError());
-    h->launches++;
     if (evj) KR_CUDA(kr_event_record(h->ev[2 * evp + 1], h->stream));
     launch_ortho(h, j, ndl);
 }

@@ -124,13 +124,14 @@ struct SlabInfo {  // device-visible copy for the local-reduce sparse gather
 enum { PATH_FUSED_LANCZOS = 0, PATH_GENERIC = 1 };
 
 struct kr_comm {
-    void* nccl;  void kr_eval_outputs(kr_handle* h, int64_t step, const double* z_h, double* y_h);
-// per-step LP (kr_lp.cu)
-void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int m_uns, const double* UA,
-               const double* Ub, int32_t* feas_h, double* out_h);
-
-// ncclComm_t
+    void* nccl;  // ncclComm_t (NCCL transport), or NULL (host transport)
     int32_t rank, world, device;
+    // host transport (krylov_comm_create_host): every collective is an all-gather of host buffers done by the
+    // caller's function; the library stages through a pinned buffer and synchronises its stream around it
+    kr_allgather_fn host_fn = nullptr;
+    void* host_ctx = nullptr;
+    double* pinned = nullptr;
+    size_t pinned_doubles = 0;
 };
 
 struct FaceCor {  // per-face diagonal correction of face cells relative to Dirichlet (x-, x+, y-, y+, z-, z+)
@@ -313,6 +314,8 @@ size_t kr_cgs_scratch_doubles(const kr_handle* h, int ndl);
 // One stored-basis Krylov step of the multi-CTA CGS2 path: j == 0 normalises the start vectors; j >= 1 applies
 // the operator to v_{j-1} (fused with the first projection pass) and orthogonalises (kr_arnoldi.cu).
 void kr_cgs_step(kr_handle* h, int j, int ndl, double* scratch);
+// Y[d] = A' X[d] for the ndl local directions (CSR, lifted when b is set): block SpMM, each row read once (kr_generic.cu)
+void kr_csr_spmm(kr_handle* h, const double* X, int64_t xstride, double* Y, int64_t ystride, int ndl);
 
 // expm + projection + lemma
 void kr_expm_enqueue(kr_handle* h);
@@ -333,12 +336,20 @@ void kr_eval_outputs(kr_handle* h, int64_t step, const double* z_h, double* y_h)
 void kr_lp_run(kr_handle* h, int m_init, const double* IA, const double* Ib, int m_uns, const double* UA,
                const double* Ub, int32_t* feas_h, double* out_h);
 
-// nccl
+// collectives (kr_comm.cu): NCCL, or the caller's host all-gather (host transport)
 void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s);
 void kr_nccl_check(kr_comm* c);
 void kr_nccl_halo(kr_comm* c, kr_handle* h, int buf, cudaStream_t s);
+inline bool kr_comm_is_host(const kr_comm* c) { return c && c->host_fn; }
+// ranks that share one state vector: the z-slab partition's world (direction sharding keeps each direction on one
+// rank, so its Lanczos scalars are reduced locally)
+inline int kr_zworld(const kr_handle* h);
+inline int kr_zrank(const kr_handle* h);
 // peer-memory halo transport (kr_comm.cu)
 void kr_p2p_blob(kr_handle* h, void* out);
 void kr_p2p_open(kr_handle* h, const void* blobs, int32_t rank, int32_t world);
 void kr_p2p_verify(kr_handle* h, int32_t* ok);
 void kr_p2p_close(kr_handle* h);
+
+inline int kr_zworld(const kr_handle* h) { return h->part == KR_PART_ZSLAB ? h->world : 1; }
+inline int kr_zrank(const kr_handle* h) { return h->part == KR_PART_ZSLAB ? h->rank : 0; }

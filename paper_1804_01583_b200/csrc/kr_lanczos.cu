@@ -25,6 +25,8 @@
 #include <cuda.h>
 #include <float.h>
 
+#include <type_traits>
+
 #include "kr_internal.h"
 
 namespace {
@@ -505,10 +507,15 @@ __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpre
 
 // BCM: 0 = Dirichlet everywhere; 1 = general faces, tile without x/y face cells (full, x0 > 0, y0 > 0): only the
 // per-plane z-face terms; 2 = general faces, per-cell diagonal corrections.
-template <int TX, int TY, int S, bool INIT, bool FULL, int BCM, bool HALO>
+// FACE: the tile touches an x / y face of the grid (x0 = 0, y0 = 0, or a ragged tile): the ghost-edge / face terms
+// are checked per plane and cell. Tiles without (most of the grid) take the z faces without per-plane branches: the
+// bottom ghost edge of global plane 0 in the peeled first plane, the top one through the z difference of the last
+// plane, dz = zf w_q - zg w_{q-1} (zf = 0 on the ghost above the grid, zg^2 cz = gq[5]: Dirichlet 1, insulated 0).
+// Box output rows are summed per warp (shuffle tree, fixed order) into wbox.
+template <int TX, int TY, int S, bool INIT, bool FULL, int BCM, bool HALO, bool FACE>
 __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
                                           unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
-                                          int zc0, int zc1, bool cta_box, Acc2& A, double* accb) {
+                                          int zc0, int zc1, bool cta_box, Acc2& A, double (*wbox)[KR_MAX_BOX]) {
     using G = Geo2<TX, TY>;
     constexpr int CW = G::CW, PW = G::PW, WW = G::WW;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -522,7 +529,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
         tma_load_3d(st, tmC, x0 - 2 - a.shC[0], y0 - 1 - a.shC[1], p + 1 - a.shC[2], &bar[s]);
         if (lp) tma_load_3d(st + G::POFF, tmP, x0 - a.shP[0], y0 - a.shP[1], p + 1 - a.shP[2], &bar[s]);
     };
-    constexpr int ISSUER = G::NT - 32;  // lane 0 of the last warp (warps 0-1 carry the ring)
+    constexpr int ISSUER = G::NT - 32;  // lane 0 of the last warp (warps 0-2 carry the ring)
     if (tid == ISSUER) {
         const int np = min(plast - pfirst + 1, S);
         for (int p = pfirst; p < pfirst + np; ++p) issue(p);
@@ -572,30 +579,23 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                     cy_ < a.box[r].hi[1])
                     bm[c] |= 1u << r;
         }
-    // forward ring: warp 0 = top row (x-pair per lane at tile row TY), warp 1 lanes < TY = right column (x = TX)
-    const bool rtop = wid == 0, rright = wid == 1 && lane < TY;
+    // forward ring, one cell per lane on three warps (the barrier after each plane waits for the slowest warp,
+    // so no warp takes more than one extra cell): the top row y0 + TY on warps 0 (x0 .. x0+31) and 1 (x0+32 ..
+    // x0+63), the right column x0 + TX on warp 2 (lanes < TY)
+    const bool ring = wid < 2 || (wid == 2 && lane < TY);
     int rcb = 0, rpb = 0, rwb = 0;
-    bool rin0 = false, rin1 = false;
-    double rex0 = 0.0, rex1 = 0.0;
-    if (rtop) {
-        rcb = (TY + 1) * CW + rx + 2;
-        rpb = TY * PW + rx;
-        rwb = TY * WW + rx;
-        rin0 = FULL || (gx < a.mx && y0 + TY < a.my);
-        rin1 = FULL || (gx + 1 < a.mx && y0 + TY < a.my);
-        if (BCM) {
-            const double ey = (y0 + TY == 0 ? a.ecor[2] : 0.0) + (y0 + TY == a.my - 1 ? a.ecor[3] : 0.0);
-            rex0 = ey + (gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0);
-            rex1 = ey + (gx + 1 == a.mx - 1 ? a.ecor[1] : 0.0);
-        }
-    } else if (rright) {
-        rcb = (lane + 1) * CW + TX + 2;
-        rpb = lane * PW + TX;
-        rwb = lane * WW + TX;
-        rin0 = FULL || (x0 + TX < a.mx && y0 + lane < a.my);
+    bool rin = false;
+    double rex = 0.0;
+    if (ring) {
+        const int rxx = wid < 2 ? 32 * wid + lane : TX, ryy = wid < 2 ? TY : lane;
+        rcb = (ryy + 1) * CW + rxx + 2;
+        rpb = ryy * PW + rxx;
+        rwb = ryy * WW + rxx;
+        const int grx = x0 + rxx, gry = y0 + ryy;
+        rin = FULL || (grx < a.mx && gry < a.my);
         if (BCM)
-            rex0 = (x0 + TX == a.mx - 1 ? a.ecor[1] : 0.0) + (y0 + lane == 0 ? a.ecor[2] : 0.0) +
-                   (y0 + lane == a.my - 1 ? a.ecor[3] : 0.0);
+            rex = (grx == 0 ? a.ecor[0] : 0.0) + (grx == a.mx - 1 ? a.ecor[1] : 0.0) + (gry == 0 ? a.ecor[2] : 0.0) +
+                  (gry == a.my - 1 ? a.ecor[3] : 0.0);
     }
     double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)gy * a.pitch + gx;
     const bool st0 = FULL || (gx < a.mx && gy < a.my), st1 = FULL || (gx < a.mx && gy + 1 < a.my);
@@ -603,7 +603,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     // u of three consecutive planes (4 cells + ring) in three register sets that take turns as u_{q-1}, u_q,
     // u_{q+1}; w of two consecutive planes in two sets (w_{q-1}, w_q): the interior loop is unrolled by six
     double U0[4], U1[4], U2[4], WA[4] = {0.0, 0.0, 0.0, 0.0}, WB[4] = {0.0, 0.0, 0.0, 0.0};
-    double2 R0 = make_double2(0.0, 0.0), R1 = R0, R2 = R0;
+    double R0 = 0.0, R1 = 0.0, R2 = 0.0;
     mbar_wait(&bar[0], 0);
     mbar_wait(&bar[1 % S], 0);
     {
@@ -617,20 +617,19 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
         U1[0] = t.x; U1[1] = t.y;
         t = ld2(C1 + cb + CW);
         U1[2] = t.x; U1[3] = t.y;
-        if (rtop) {
-            R0 = ld2(C0 + rcb);
-            R1 = ld2(C1 + rcb);
-        } else if (rright) {
-            R0.x = C0[rcb];
-            R1.x = C1[rcb];
+        if (ring) {
+            R0 = C0[rcb];
+            R1 = C1[rcb];
         }
     }
     int sq = 1 % S, sn = 2 % S;
     uint32_t ph = (2 / S) & 1;
     // one plane q: w_q on the tile (wc) and the ring (into the W buffer of q's parity), then the products of plane
     // q - 1 (wp = w_{q-1}; its x+2 / row+2 neighbours from the W buffer written last iteration, its z+1 neighbour wc)
-    auto plane = [&](const double (&up)[4], const double (&uc)[4], double (&un)[4], const double2 rp, const double2 rc,
-                     double2& rn, const double (&wp)[4], double (&wc)[4], const int q) {
+    const double zgtop = BCM ? sqrt(a.gq[5] / a.cz) : 1.0;  // the top face's edge coefficient gq[5] = zg^2 cz
+    auto plane = [&](const double (&up)[4], const double (&uc)[4], double (&un)[4], const double rp, const double rc,
+                     double& rn, const double (&wp)[4], double (&wc)[4], const int q, auto first) {
+        constexpr bool FIRST = decltype(first)::value;  // q == zc0: w only, no products
         mbar_wait(&bar[sn], ph);
         const unsigned char* stq = smem + sq * G::STAGE;
         const double* Cq = reinterpret_cast<const double*>(stq);
@@ -675,39 +674,21 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
         }
         st2(Wq + wb, wc[0], wc[1]);
         st2(Wq + wb + WW, wc[2], wc[3]);
-        if (rtop) {
-            rn = ld2(Cn + rcb);
-            double r0 = rc.x, r1 = rc.y;
+        if (ring) {
+            rn = Cn[rcb];
+            double r0 = rc;
             if (!INIT) {
-                const double xm = Cq[rcb - 1], xp = Cq[rcb + 2];
-                const double2 ym = ld2(Cq + rcb - CW), yp = ld2(Cq + rcb + CW);
-                const double c0 = BCM ? fma(sa, dgz - rex0, sb) : cf, c1 = BCM ? fma(sa, dgz - rex1, sb) : cf;
-                r0 = fma(scx, xm + rc.y, fma(scy, ym.x + yp.x, fma(scz, rp.x + rn.x, -c0 * rc.x)));
-                r1 = fma(scx, rc.x + xp, fma(scy, ym.y + yp.y, fma(scz, rp.y + rn.y, -c1 * rc.y)));
-                if (has_prev) {
-                    const double2 pv = ld2(Pq + rpb);
-                    r0 = fma(-sp, pv.x, r0);
-                    r1 = fma(-sp, pv.y, r1);
-                }
-            }
-            if (!FULL) {
-                if (!rin0) r0 = 0.0;
-                if (!rin1) r1 = 0.0;
-            }
-            st2(Wq + rwb, r0, r1);
-        } else if (rright) {
-            rn.x = Cn[rcb];
-            double r0 = rc.x;
-            if (!INIT) {
-                const double c0 = BCM ? fma(sa, dgz - rex0, sb) : cf;
+                const double c0 = BCM ? fma(sa, dgz - rex, sb) : cf;
                 r0 = fma(scx, Cq[rcb - 1] + Cq[rcb + 1],
-                         fma(scy, Cq[rcb - CW] + Cq[rcb + CW], fma(scz, rp.x + rn.x, -c0 * rc.x)));
+                         fma(scy, Cq[rcb - CW] + Cq[rcb + CW], fma(scz, rp + rn, -c0 * rc)));
                 if (has_prev) r0 = fma(-sp, Pq[rpb], r0);
             }
-            if (!FULL && !rin0) r0 = 0.0;
+            if (!FULL && !rin) r0 = 0.0;
             Wq[rwb] = r0;
         }
-        if (q > zc0) {  // products of plane q - 1 (its ring / x+2 / row+2 neighbours were written last iteration)
+        if (!FACE && FIRST && a.zoff + zc0 == 0)  // ghost edge below global plane 0, coefficient gq[4]
+            A.face = fma(a.gq[4], fma(wc[0], wc[0], fma(wc[1], wc[1], fma(wc[2], wc[2], wc[3] * wc[3]))), A.face);
+        if (!FIRST && (!FACE || q > zc0)) {  // products of plane q - 1 (its x+2 / row+2 neighbours: last iteration)
             const double* Wp = ((q & 1) ? Wb0 : Wb1) + wb;
             const int gzp = gzq - 1;
             const double xr0 = Wp[2], xr1 = Wp[WW + 2];
@@ -723,8 +704,10 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                 if (yhi0) { ddy[0] = 0.0; ddy[1] = 0.0; A.face = fma(a.gq[3], fma(wp[0], wp[0], wp[1] * wp[1]), A.face); }
                 if (yhi1) { ddy[2] = 0.0; ddy[3] = 0.0; A.face = fma(a.gq[3], fma(wp[2], wp[2], wp[3] * wp[3]), A.face); }
             }
-            if (xlo) A.face = fma(a.gq[0], fma(wp[0], wp[0], wp[2] * wp[2]), A.face);  // ghost edges of the low faces
-            if (ylo) A.face = fma(a.gq[2], fma(wp[0], wp[0], wp[1] * wp[1]), A.face);
+            if (FACE) {  // ghost edges of the low x / y faces
+                if (xlo) A.face = fma(a.gq[0], fma(wp[0], wp[0], wp[2] * wp[2]), A.face);
+                if (ylo) A.face = fma(a.gq[2], fma(wp[0], wp[0], wp[1] * wp[1]), A.face);
+            }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 A.ww = fma(wp[c], wp[c], A.ww);
@@ -732,8 +715,25 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                 A.dx = fma(dx[c], dx[c], A.dx);
                 A.dy = fma(ddy[c], ddy[c], A.dy);
             }
-            if (gzp == a.mz - 1) {  // the z+1 neighbour is the zero ghost above the grid: face coefficient gq[5]
+            if (FACE && gzp == a.mz - 1) {  // the z+1 neighbour is the zero ghost above the grid: coefficient gq[5]
                 A.face = fma(a.gq[5], fma(wp[0], wp[0], fma(wp[1], wp[1], fma(wp[2], wp[2], wp[3] * wp[3]))), A.face);
+            } else if (!FACE) {
+                const bool top = gzp == a.mz - 1;  // uniform: the ghost above the grid (w there is not a state value)
+                const double zf = top ? 0.0 : 1.0;
+                if (BCM) {
+                    const double zg = top ? zgtop : 1.0;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const double dz = fma(wc[c], zf, -zg * wp[c]);
+                        A.dz = fma(dz, dz, A.dz);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const double dz = fma(wc[c], zf, -wp[c]);  // exactly wc - wp, or -wp above the grid
+                        A.dz = fma(dz, dz, A.dz);
+                    }
+                }
             } else {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -741,7 +741,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                     A.dz = fma(dz, dz, A.dz);
                 }
             }
-            if (gzp == 0)
+            if (FACE && gzp == 0)
                 A.face = fma(a.gq[4], fma(wp[0], wp[0], fma(wp[1], wp[1], fma(wp[2], wp[2], wp[3] * wp[3]))), A.face);
             const bool wr = !INIT && a.write_out;
             if (wr) {
@@ -752,16 +752,15 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                 uint32_t zmask = 0;
                 for (int r = 0; r < a.nbox; ++r)
                     if (gzp >= a.box[r].lo[2] && gzp < a.box[r].hi[2]) zmask |= 1u << r;
-                if (zmask) {
+                for (int r = 0; r < a.nbox; ++r) {  // uniform loop: a warp tree per box row meeting this plane
+                    if (!((zmask >> r) & 1u)) continue;
+                    double v = 0.0;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const uint32_t mk = bm[c] & zmask;
-                        if (mk) {
+                    for (int c = 0; c < 4; ++c)
+                        if ((bm[c] >> r) & 1u) v += wp[c];
 #pragma unroll
-                            for (int r = 0; r < KR_MAX_BOX; ++r)
-                                if ((mk >> r) & 1u) accb[r] += wp[c];
-                        }
-                    }
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                    if (lane == 0) wbox[wid][r] += v;
                 }
             }
             // halo planes for the neighbours, stored where they will be read (uniform per plane, rare): owned
@@ -793,26 +792,29 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
             ph ^= 1u;
         }
     };
-    constexpr bool UNROLL = FULL && BCM < 2;
-    if (UNROLL) {
-        for (int q = zc0;;) {
-            plane(U0, U1, U2, R0, R1, R2, WA, WB, q);
+    using F1 = std::integral_constant<bool, true>;
+    using F0 = std::integral_constant<bool, false>;
+    constexpr bool UNROLL = FULL && !FACE && BCM < 2;
+    if (UNROLL) {  // the first plane peeled (no products), then six planes per turn of the register rotation
+        plane(U0, U1, U2, R0, R1, R2, WA, WB, zc0, F1{});
+        for (int q = zc0 + 1; q <= zc1;) {
+            plane(U1, U2, U0, R1, R2, R0, WB, WA, q, F0{});
             if (++q > zc1) break;
-            plane(U1, U2, U0, R1, R2, R0, WB, WA, q);
+            plane(U2, U0, U1, R2, R0, R1, WA, WB, q, F0{});
             if (++q > zc1) break;
-            plane(U2, U0, U1, R2, R0, R1, WA, WB, q);
+            plane(U0, U1, U2, R0, R1, R2, WB, WA, q, F0{});
             if (++q > zc1) break;
-            plane(U0, U1, U2, R0, R1, R2, WB, WA, q);
+            plane(U1, U2, U0, R1, R2, R0, WA, WB, q, F0{});
             if (++q > zc1) break;
-            plane(U1, U2, U0, R1, R2, R0, WA, WB, q);
+            plane(U2, U0, U1, R2, R0, R1, WB, WA, q, F0{});
             if (++q > zc1) break;
-            plane(U2, U0, U1, R2, R0, R1, WB, WA, q);
+            plane(U0, U1, U2, R0, R1, R2, WA, WB, q, F0{});
             if (++q > zc1) break;
         }
     } else {
 #pragma unroll 1
         for (int q = zc0; q <= zc1; ++q) {
-            plane(U0, U1, U2, R0, R1, R2, WA, WB, q);
+            plane(U0, U1, U2, R0, R1, R2, WA, WB, q, F0{});
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 U0[c] = U1[c];
@@ -838,9 +840,9 @@ __global__ void __launch_bounds__(Geo2<TX, TY>::NT, (TY >= 32) ? 1 : 2)
 
     const int tid = threadIdx.x;
     Acc2 A{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    double accb[KR_MAX_BOX];
-#pragma unroll
-    for (int r = 0; r < KR_MAX_BOX; ++r) accb[r] = 0.0;
+    __shared__ double wbox[G::NT / 32][KR_MAX_BOX];  // per-warp box-row sums (lane 0 of each warp)
+    if ((tid & 31) == 0)
+        for (int r = 0; r < KR_MAX_BOX; ++r) wbox[tid >> 5][r] = 0.0;
     // Persistent CTAs: work items (x-tile, y-tile, z-chunk) dealt round-robin (fixed assignment, deterministic)
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
         const int xt = a.ix0 + item % a.gx, yt = a.iy0 + (item / a.gx) % a.gy, zt = a.iz0 + item / (a.gx * a.gy);
@@ -859,17 +861,17 @@ __global__ void __launch_bounds__(Geo2<TX, TY>::NT, (TY >= 32) ? 1 : 2)
                 a.box[r].lo[1] < y0 + TY && a.box[r].hi[1] > y0 && a.box[r].lo[2] < a.zoff + zc1 &&
                 a.box[r].hi[2] > a.zoff + zc0)
                 cta_box = true;
+#define KR_M2(FULL_, BCM_, FACE_) \
+    lz_march2<TX, TY, S, INIT, FULL_, BCM_, HALO, FACE_>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, wbox)
         if (x0 + TX < a.mx && y0 + TY < a.my) {
-            if (!BC)
-                lz_march2<TX, TY, S, INIT, true, 0, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, accb);
-            else if (x0 > 0 && y0 > 0)
-                lz_march2<TX, TY, S, INIT, true, 1, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, accb);
+            if (x0 > 0 && y0 > 0)
+                KR_M2(true, BC ? 1 : 0, false);
             else
-                lz_march2<TX, TY, S, INIT, true, 2, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, accb);
+                KR_M2(true, BC ? 2 : 0, true);
         } else {
-            lz_march2<TX, TY, S, INIT, false, BC ? 2 : 0, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1,
-                                                             cta_box, A, accb);
+            KR_M2(false, BC ? 2 : 0, true);
         }
+#undef KR_M2
         __syncthreads();  // every issued plane was consumed: the barriers can be recycled for the next item
         if (tid == 0) {
 #pragma unroll
@@ -885,7 +887,7 @@ __global__ void __launch_bounds__(Geo2<TX, TY>::NT, (TY >= 32) ? 1 : 2)
     acc[1] = fma(a.cx, A.dx, fma(a.cy, A.dy, fma(a.cz, A.dz, A.face)));  // -w^T A w
     acc[2] = A.sum;
 #pragma unroll
-    for (int r = 0; r < KR_MAX_BOX; ++r) acc[3 + r] = accb[r];
+    for (int r = 0; r < KR_MAX_BOX; ++r) acc[3 + r] = (tid & 31) == 0 ? wbox[tid >> 5][r] : 0.0;
     lz_epilogue<G::NT>(a, acc, reinterpret_cast<double*>(smem), a.plane);
 }
 
@@ -1469,7 +1471,7 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     a.counter = sl.counter;
     const int S = (int)h->slabs.size();
     const int sidx = (int)(&sl - &h->slabs[0]);
-    a.rankvec = h->d_rankvec + ((size_t)h->rank * S + sidx) * h->nq;
+    a.rankvec = h->d_rankvec + ((size_t)kr_zrank(h) * S + sidx) * h->nq;
     a.box_slot = h->d_box_slot;
     a.box_val = h->d_box_val;
     a.outs = h->d_outs;
@@ -1477,7 +1479,7 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     for (const DVec& o : h->outs_h) has_sparse |= o.kind == KR_VEC_SPARSE;
     a.gather_u = (gather_buf >= 0 && has_sparse) ? sl.u[gather_buf] : nullptr;
     a.n_out = h->n_out;
-    a.fin = (S == 1 && h->world == 1) ? 1 : 0;
+    a.fin = (S == 1 && kr_zworld(h) == 1) ? 1 : 0;
     a.k = k;
     a.H = h->d_H ? h->d_H + (size_t)dl * (k + 1) * k : nullptr;
     a.P = h->d_P + (size_t)dl * h->n_out * k;
@@ -1637,11 +1639,12 @@ static void halo_exchange_virtual(kr_handle* h, int buf) {
 // ranks and update the scalars — unless a single slab on a single rank already did it in-kernel.
 static void combine_and_finalize(kr_handle* h, int dl, int step) {
     const int S = (int)h->slabs.size();
-    if (S == 1 && h->world == 1) return;
+    const int zw = kr_zworld(h);
+    if (S == 1 && zw == 1) return;
     LzScalars* sc = h->d_sc + dl;
-    const int R = S * h->world;
-    double* rv_local = h->d_rankvec + (size_t)h->rank * S * h->nq;
-    if (h->world > 1) kr_nccl_allgather(h->comm, rv_local, h->d_rankvec, (size_t)S * h->nq, h->stream);
+    const int R = S * zw;
+    double* rv_local = h->d_rankvec + (size_t)kr_zrank(h) * S * h->nq;
+    if (zw > 1) kr_nccl_allgather(h->comm, rv_local, h->d_rankvec, (size_t)S * h->nq, h->stream);
     const int k = h->k;
     lz_finalize<<<1, 32, 0, h->stream>>>(h->d_rankvec, R, h->nq, h->n_out, step, k, sc,
                                          h->d_H ? h->d_H + (size_t)dl * (k + 1) * k : nullptr,
@@ -1706,7 +1709,7 @@ void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events) {
     for (auto& sl : h->slabs) reduce_launch(h, sl, dl, nxt, i, false, write, write ? nxt : -1);
     if (write && !h->halo_inkernel) {  // message transport: copies / NCCL send-recv after the step
         if (h->slabs.size() > 1) halo_exchange_virtual(h, nxt);
-        if (h->world > 1) kr_nccl_halo(h->comm, h, nxt, h->stream);
+        if (kr_zworld(h) > 1) kr_nccl_halo(h->comm, h, nxt, h->stream);
     }
     combine_and_finalize(h, dl, i);
 }

@@ -1,13 +1,15 @@
 #!/bin/bash
-# A/B/n of library builds in scratch_libs/ (LIBS="a b c" -> scratch_libs/libkr_<x>.so): per-step device times.
+# A/B of library builds (scratch_libs/libkr_<name>.so copied over the in-tree library in the box's copy of the
+# repo): per-step times of C5 and C4 (scripts/step_profile.py) and the dense C5D bench line, alternating twice.
+# Usage (under gpurun): bash scripts/ab_libs.sh name1 name2 ...
+export KR_STEP_V=${KR_STEP_V:-2}
 for rep in 1 2; do
-for lib in ${LIBS:-old}; do
-  export KR_LIB_PATH=scratch_libs/libkr_$lib.so
-  for c in ${CONFIGS:-C5 C4}; do
-    python scripts/step_times.py $c 3 2>&1 | python -c "
-import sys
-L=sys.stdin.read().splitlines(); it=L[0].split()[-1]; v=[float(x) for x in L[1].split(':')[1].split()]
-mid=v[2:-1]; print('$lib $c iter', it, 'step1 %.3f step2 %.3f mean3..k-1 %.4f' % (v[0], v[1], sum(mid)/len(mid)))"
+  for lib in "$@"; do
+    cp scratch_libs/libkr_$lib.so paper_1804_01583_b200/libkrylov_reach.so
+    for cfg in C5 C4; do echo "$lib $cfg: $(python scripts/step_profile.py $cfg | cut -d: -f2)"; done
+    timeout 300 python bench.py --config C5D --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/abl_$lib.log 2>&1
+    python -c "
+import json; d=json.loads([l for l in open('gpurun_out/abl_$lib.log') if l.startswith('{')][-1])
+print('$lib C5D:', round(d['value'],1), 'steps/s step', round(d['fused_step']['ms_mean'],4), 'frac', round(d['roofline']['frac'],4), d['clocks'])"
   done
-done
 done

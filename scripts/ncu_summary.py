@@ -15,6 +15,7 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
+raw_hdr, raw_row = rows[0], rows[2]
 for r in rows[2:]:
     print(r[hdr.index('Kernel Name')][:80])
     for w in WANT:
@@ -51,3 +52,16 @@ for r in data:
 for op, c in byop.most_common(16):
     print(f"  {op:22s} instr {100 * c / ti:5.1f}%  stall-samples {100 * bys[op] / ts:5.1f}%")
 stall_cols = [h for h in hdr if h.startswith('stall_') or 'Stall Reasons' in h]
+
+# stall reasons (pc sampling), largest first
+vals = []
+for i, n in enumerate(raw_hdr):
+    if 'pcsamp_warps_issue_stalled' in n and not n.endswith('not_issued'):
+        try:
+            vals.append((float(raw_row[i].replace(',', '')), n))
+        except (ValueError, IndexError):
+            pass
+tot = sum(v for v, _ in vals) or 1.0
+print("stall reasons (pc samples):")
+for v, n in sorted(vals, reverse=True)[:12]:
+    print(f"  {n.replace('smsp__pcsamp_warps_issue_stalled_', ''):32s} {100 * v / tot:5.1f}%")

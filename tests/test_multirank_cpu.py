@@ -177,3 +177,50 @@ def test_halo_plan_pairs_up():
                 recv_first_global = z0 - 1 + plane
                 assert send_first_global == recv_first_global
                 assert pz0 <= send_first_global and send_first_global + n <= pz1  # peer's owned planes
+
+
+def _par2_worker(rank, world, port, n_dir, out_dir):
+    """Direction sharding (PAR2) host logic on gloo: each rank takes its directions from the library's
+    partitioner (krylov_dirs_of_rank), fills its local coefficient block [(N+1)][o][ndl_max] with values that
+    encode (step, row, global direction), and all-gathers the blocks in rank order — the exchange the library
+    does with one collective after the Krylov loop; the gathered blocks are then reordered as the header states
+    (local block dl of rank w is global direction w + dl * world)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1804_01583_b200 import krylov_dirs_of_rank
+        mine = krylov_dirs_of_rank(n_dir, world, rank)
+        ndl_max = -(-n_dir // world)
+        np1, o = 7, 3
+        loc = np.full((np1, o, ndl_max), np.nan)
+        for dl, d in enumerate(mine):
+            loc[:, :, dl] = 1000.0 * d + 10.0 * np.arange(o)[None, :] + 0.01 * np.arange(np1)[:, None]
+        t = torch.from_numpy(loc)
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        lists = [None] * world
+        dist.all_gather_object(lists, mine)
+        np.savez(os.path.join(out_dir, f"p{rank}.npz"), G=np.stack([q.numpy() for q in parts]),
+                 lists=np.array([len(x) for x in lists]), flat=np.concatenate([np.array(x, dtype=np.int64) for x in lists]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_dir", [(2, 21), (3, 8), (3, 2), (2, 1)])
+def test_direction_sharding_gloo(world, n_dir, tmp_path):
+    mp.spawn(_par2_worker, args=(world, free_port(), n_dir, str(tmp_path)), nprocs=world, join=True)
+    r0 = np.load(tmp_path / "p0.npz")
+    flat = r0["flat"]
+    assert sorted(flat.tolist()) == list(range(n_dir))  # a partition: every direction exactly once
+    assert r0["lists"].tolist() == [len(range(w, n_dir, world)) for w in range(world)]
+    G = r0["G"]  # [world][N+1][o][ndl_max]
+    np1, o = G.shape[1], G.shape[2]
+    coeff = np.empty((np1, o, n_dir))
+    for d in range(n_dir):
+        coeff[:, :, d] = G[d % world, :, :, d // world]
+    want = 1000.0 * np.arange(n_dir)[None, None, :] + 10.0 * np.arange(o)[None, :, None] + \
+        0.01 * np.arange(np1)[:, None, None]
+    assert np.array_equal(coeff, want)
+    for r in range(1, world):  # every rank gathered the same blocks
+        assert np.array_equal(np.load(tmp_path / f"p{r}.npz")["G"], G, equal_nan=True)
