@@ -1065,7 +1065,6 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 }
             }
             // step kernel: v2 (2 x 2 cells per thread) for 64-wide tiles; KR_STEP_V=1 keeps v1 (A/B)
-            // step kernel: v2 (2 x 2 cells per thread) for 64-wide tiles; KR_STEP_V=1 keeps v1 (A/B)
             h->step_kv = h->TX == 64 ? 2 : 1;
             if (const char* e = getenv("KR_STEP_V")) h->step_kv = (atoi(e) == 1 || h->TX != 64) ? 1 : 2;
             int nsl = 1, W = h->world, R = h->rank;
@@ -1222,7 +1221,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                             16.0 * (double)h->N * ndl;
         }
         tr.mark("path set-up");
-        if (!h->large_route) kr_expm_prepare(h);
+        kr_expm_prepare(h);  // also for the large-k route: its checkpoints with k <= 64 use the powers + march kernels
         tr.mark("expm prepare");
         h->d_sense = reinterpret_cast<int32_t*>(dalloc(h, (size_t)h->n_out * 4));
         h->d_thr = reinterpret_cast<double*>(dalloc(h, (size_t)h->n_out * 8));

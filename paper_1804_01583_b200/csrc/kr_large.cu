@@ -190,6 +190,45 @@ __global__ void large_build_kernel(const LzScalars* sc, int kc, int kp, double f
     }
 }
 
+// The Horner steps Y <- I + X Y / q, q = 17 .. 1, of T_18(X) for the TRIDIAGONAL X = H delta / 2^s, in one CTA:
+// (X Y)_{ij} = X_{i,i-1} Y_{i-1,j} + X_{ii} Y_{ij} + X_{i,i+1} Y_{i+1,j}, and after m products Y is banded with
+// half-bandwidth m + 1, so each step touches only kc (2m + 3) entries (the band GEMM route took 17 launches).
+// Y0 holds I + X / 18 (large_build_kernel, zero elsewhere); the steps alternate Y0 -> Y1 -> Y0 ... and the band of
+// the last one (in Y1) is copied back into Y0, whose entries outside the band are still 0. Only band entries are
+// read, so the previous contents of Y1 do not matter.
+__global__ void __launch_bounds__(1024) large_taylor_tri_kernel(const LzScalars* sc, int kc, int kp, double f,
+                                                                 double* Y0, double* Y1) {
+    const double* Ycur = Y0;
+    double* Ynew = Y1;
+    int bc = 1;  // half-bandwidth of Ycur
+    for (int q = 17; q >= 1; --q) {
+        const int bn = bc + 1;
+        const int64_t ne = (int64_t)kc * (2 * bn + 1);
+        const double inv = 1.0 / q;
+        for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) {
+            const int i = (int)(e / (2 * bn + 1)), j = i + (int)(e % (2 * bn + 1)) - bn;
+            if (j < 0 || j >= kc) continue;
+            double s = 0.0;
+            if (i >= 1 && abs(i - 1 - j) <= bc) s = fma(sc->beta[i] * f, Ycur[(size_t)(i - 1) * kp + j], s);
+            if (abs(i - j) <= bc) s = fma(sc->alpha[i + 1] * f, Ycur[(size_t)i * kp + j], s);
+            if (i + 1 < kc && abs(i + 1 - j) <= bc) s = fma(sc->beta[i + 1] * f, Ycur[(size_t)(i + 1) * kp + j], s);
+            Ynew[(size_t)i * kp + j] = s * inv + (i == j ? 1.0 : 0.0);
+        }
+        __syncthreads();
+        const double* t = Ycur;
+        Ycur = Ynew;
+        Ynew = const_cast<double*>(t);
+        bc = bn;
+    }
+    if (Ycur != Y0) {
+        const int64_t ne = (int64_t)kc * (2 * bc + 1);
+        for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) {
+            const int i = (int)(e / (2 * bc + 1)), j = i + (int)(e % (2 * bc + 1)) - bc;
+            if (j >= 0 && j < kc) Y0[(size_t)i * kp + j] = Ycur[(size_t)i * kp + j];
+        }
+    }
+}
+
 // the leading kc x kc tridiagonal as a dense matrix (row stride kc), for the one-CTA small-checkpoint path
 __global__ void tri_dense_kernel(const LzScalars* sc, int kc, double* H) {
     for (int e = threadIdx.x; e < kc * kc; e += blockDim.x) {
@@ -435,15 +474,22 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
         h->launches++;
     }
     // Horner: Y = I + X Y / q, q = 17..1  ->  Y = T_18(X); bandwidth of Y grows by one per product
-    // (tridiagonal X); a Hessenberg X is treated as dense
+    // (tridiagonal X: one CTA over the band, large_taylor_tri_kernel); a Hessenberg X is treated as dense
     const int bwX = tri ? 1 : bmax;
     int bwY = tri ? 1 : bmax;
     double* Y = Y0;
     double* Z = Y1;
-    for (int q = 17; q >= 1; --q) {
-        gemm(h, X, Y, Z, kp, kp, kp, kp, kp, kp, bwX, std::min(bwY, bmax), kc, 1.0 / q, 1.0);
-        bwY = std::min(bwY + 1, bmax);
-        std::swap(Y, Z);
+    if (tri) {
+        large_taylor_tri_kernel<<<1, 1024, 0, st>>>(sc, kc, kp, f, Y0, Y1);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+        bwY = std::min(18, bmax);
+    } else {
+        for (int q = 17; q >= 1; --q) {
+            gemm(h, X, Y, Z, kp, kp, kp, kp, kp, kp, bwX, std::min(bwY, bmax), kc, 1.0 / q, 1.0);
+            bwY = std::min(bwY + 1, bmax);
+            std::swap(Y, Z);
+        }
     }
     // squaring: E = Y^(2^s)
     for (int r = 0; r < s; ++r) {
