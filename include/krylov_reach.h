@@ -283,6 +283,10 @@ kr_status krylov_adaptive_checks(const kr_handle* h, int32_t dir, int32_t* ks, d
 kr_status krylov_comm_unique_id(void* id128);
 kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int32_t device, kr_comm** out);
 void krylov_comm_destroy(kr_comm* c);
+/* Health check of a communicator as the fixed-k run uses it: the per-step all-gather of rank vectors (z-slab
+ * partition) issued inside a CUDA graph capture on `stream` (a cudaStream_t; NULL = a library stream), replayed
+ * `reps` times; every rank's slot must arrive. *ok = 1 on success. Collective. KR_ENCCL / KR_ECUDA on failure. */
+kr_status krylov_comm_selftest(kr_comm* c, void* stream, int32_t reps, int32_t* ok);
 
 /* Direction sharding (KR_PART_DIRS): the global directions (generator columns of E, then the
  * fixed direction v_f) that rank `rank` of `world` simulates — round robin, d = rank, rank + world,

@@ -64,7 +64,8 @@ EXPORTS = ["krylov_workspace_bytes", "krylov_reach_create", "krylov_project", "k
            "krylov_adaptive_checks", "krylov_last_timing_large", "krylov_sim_info", "krylov_check_lp",
            "krylov_eval_outputs", "krylov_ipc_blob", "krylov_p2p_open", "krylov_p2p_verify", "krylov_p2p_enable",
            "krylov_a_priori_bound_log10", "krylov_memory_bytes", "krylov_step_times",
-           "krylov_release_cached_memory", "krylov_comm_create_host", "krylov_dirs_of_rank"]
+           "krylov_release_cached_memory", "krylov_comm_create_host", "krylov_dirs_of_rank",
+           "krylov_comm_selftest"]
 
 # int32_t fn(void* ctx, const void* send, void* recv, size_t bytes): the host transport's all-gather
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
@@ -99,6 +100,7 @@ def lib():
     L.krylov_comm_create.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
     L.krylov_comm_create_host.argtypes = [C.c_int32, C.c_int32, C.c_int32, ALLGATHER_FN, vp, C.POINTER(vp)]
     L.krylov_comm_destroy.argtypes = [vp]
+    L.krylov_comm_selftest.argtypes = [vp, vp, C.c_int32, C.POINTER(C.c_int32)]
     L.krylov_dirs_of_rank.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, C.c_int32, C.POINTER(C.c_int32)]
     L.krylov_comm_destroy.restype = None
     L.krylov_krylov_data.argtypes = [vp, C.c_int32, vp, vp]

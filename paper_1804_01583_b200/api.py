@@ -401,6 +401,13 @@ class KrComm:
         self.rank, self.world = rank, world
         return self
 
+    def selftest(self, stream=None, reps=3):
+        """krylov_comm_selftest: the per-step all-gather inside a captured CUDA graph, replayed; True if every slot
+        arrived (collective)."""
+        ok = C.c_int32()
+        A.check(A.lib().krylov_comm_selftest(self.ptr, stream, int(reps), C.byref(ok)))
+        return bool(ok.value)
+
     def close(self):
         if self.ptr:
             A.lib().krylov_comm_destroy(self.ptr)

@@ -41,9 +41,10 @@ cudaError_t kr_event_record(cudaEvent_t e, cudaStream_t s) {
 kr_status kr_comm_unique_id_impl(void* id128);
 kr_comm* kr_comm_create_impl(const void* id128, int32_t rank, int32_t world, int32_t device);
 void kr_comm_destroy_impl(kr_comm* c);
+void kr_comm_selftest_impl(kr_comm* c, cudaStream_t s, int reps, int32_t* ok);
 kr_comm* kr_comm_create_host_impl(int32_t rank, int32_t world, int32_t device, kr_allgather_fn fn, void* ctx);
 size_t kr_box_cex_bytes();
-int kr_lz_occupancy(int TX, int TY, int kv);
+int kr_lz_occupancy(int TX, int TY);
 void kr_lz_prepare(kr_handle* h);
 void kr_expm_prepare(kr_handle* h);
 void kr_ge_prepare();
@@ -828,6 +829,26 @@ kr_status krylov_comm_create(const void* id128, int32_t rank, int32_t world, int
 
 void krylov_comm_destroy(kr_comm* c) { kr_comm_destroy_impl(c); }
 
+kr_status krylov_comm_selftest(kr_comm* c, void* stream, int32_t reps, int32_t* ok) {
+    return guarded([&] {
+        if (!c || !ok || reps < 1) KR_THROW(KR_EINVAL, "krylov_comm_selftest: bad arguments");
+        KR_CUDA(cudaSetDevice(c->device));
+        cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+        bool own = false;
+        if (!s) {
+            KR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            own = true;
+        }
+        try {
+            kr_comm_selftest_impl(c, s, reps, ok);
+        } catch (...) {
+            if (own) cudaStreamDestroy(s);
+            throw;
+        }
+        if (own) cudaStreamDestroy(s);
+    });
+}
+
 kr_status krylov_comm_create_host(int32_t rank, int32_t world, int32_t device, kr_allgather_fn fn, void* ctx,
                                   kr_comm** out) {
     return guarded([&] {
@@ -1052,21 +1073,9 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             h->d_box_val = upload(h, bvals.data(), bvals.size());
             h->nq = 2 + h->n_out;
             h->nqp = 2 + (int)h->boxes.size();
-            // tile choice: TX in {64, 32} by ragged waste, TY = 8
-            auto waste = [&](int64_t t) { return (double)(((h->mx + t - 1) / t) * t - h->mx) / (double)h->mx; };
-            h->TX = (waste(64) <= waste(32) + 0.10) ? 64 : 32;
-            h->TY = 8;
-            if (h->TX == 64 && h->my >= 64) h->TY = 16;  // 4 cells per thread, less y-halo re-read
-            if (const char* t = getenv("KR_TILE")) {  // tuning override "TXxTY"
-                int tx = 0, ty = 0;
-                if (sscanf(t, "%dx%d", &tx, &ty) == 2 && kr_lz_step_smem(tx, ty) > 0) {
-                    h->TX = tx;
-                    h->TY = ty;
-                }
-            }
-            // step kernel: v2 (2 x 2 cells per thread) for 64-wide tiles; KR_STEP_V=1 keeps v1 (A/B)
-            h->step_kv = h->TX == 64 ? 2 : 1;
-            if (const char* e = getenv("KR_STEP_V")) h->step_kv = (atoi(e) == 1 || h->TX != 64) ? 1 : 2;
+            // tile: 64 x 16 cells (one x-pair per lane, a warp per row pair: 256 threads), 64 x 8 below 64 rows
+            h->TX = 64;
+            h->TY = h->my >= 64 ? 16 : 8;
             int nsl = 1, W = h->world, R = h->rank;
             if (p->virtual_slabs > 1) {
                 nsl = p->virtual_slabs;
@@ -1076,7 +1085,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 W = 1;
                 R = 0;
             }
-            const int occ = std::max(1, kr_lz_occupancy(h->TX, h->TY, h->step_kv));
+            const int occ = std::max(1, kr_lz_occupancy(h->TX, h->TY));
             int dev_sms = 148;
             KR_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
             const char* env_zc = getenv("KR_ZCHUNK");
@@ -1108,7 +1117,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 // (C5, v2 kernel: 143-plane chunks 3.89 ms per step, 72-plane 3.70 ms; profiles/r02_zchunk.txt)
                 int best_zc = (int)sl.nz;
                 double best_cost = 1e300;
-                const int64_t zc_max = h->step_kv == 2 ? 80 : (int64_t)sl.nz;
+                const int64_t zc_max = 80;
                 for (int nzc = 1; nzc <= 256 && nzc <= sl.nz; ++nzc) {
                     const int64_t zc = (sl.nz + nzc - 1) / nzc;
                     if (zc > zc_max && nzc < 256 && nzc < sl.nz) continue;
@@ -1129,7 +1138,6 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 sl.gy = (int32_t)gy;
                 sl.nitems = gx * gy * nch;
                 sl.nblk = sl.nitems;  // one work item per CTA: the block scheduler keeps neighbours co-resident
-                if (const char* e = getenv("KR_PERSIST")) sl.nblk = std::min<int64_t>(sl.nitems, std::max(1, atoi(e)));
                 sl.grid = dim3((unsigned)sl.nblk, 1, 1);
                 const int64_t ngrp = (sl.nblk + 63) / 64;
                 sl.partials = reinterpret_cast<double*>(dalloc(h, (size_t)(sl.nblk + ngrp) * h->nqp * 8));

@@ -87,6 +87,53 @@ void kr_nccl_check(kr_comm* c) {
     if (async != ncclSuccess) KR_THROW(KR_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(async));
 }
 
+// Graph-captured all-gather self test (krylov_comm_selftest): each rank writes rank-tagged values into its slot,
+// the all-gather runs inside a captured graph replayed `reps` times, every slot is checked on the host.
+__global__ void selftest_fill_kernel(double* v, int rank, int count, int rep) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) v[(size_t)rank * count + i] = 1000.0 * (rank + 1) + i + 0.5 * rep;
+}
+
+void kr_comm_selftest_impl(kr_comm* c, cudaStream_t s, int reps, int32_t* ok) {
+    const int count = 8;
+    double* d = nullptr;
+    KR_CUDA(cudaMalloc(&d, sizeof(double) * count * c->world));
+    std::vector<double> h((size_t)count * c->world);
+    bool good = true;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    try {
+        for (int rep = 0; rep < reps; ++rep) {
+            selftest_fill_kernel<<<1, 32, 0, s>>>(d, c->rank, count, rep);
+            KR_CUDA(cudaGetLastError());
+            if (!kr_comm_is_host(c)) {
+                if (!ge) {  // the all-gather alone, captured once and replayed (as inside the Krylov graph)
+                    KR_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                    kr_nccl_allgather(c, d + (size_t)c->rank * count, d, count, s);
+                    KR_CUDA(cudaStreamEndCapture(s, &g));
+                    KR_CUDA(cudaGraphInstantiate(&ge, g, 0));
+                }
+                KR_CUDA(cudaGraphLaunch(ge, s));
+            } else {
+                kr_nccl_allgather(c, d + (size_t)c->rank * count, d, count, s);
+            }
+            KR_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+            KR_CUDA(cudaStreamSynchronize(s));
+            kr_nccl_check(c);
+            for (int r = 0; r < c->world; ++r)
+                for (int i = 0; i < count; ++i) good &= h[(size_t)r * count + i] == 1000.0 * (r + 1) + i + 0.5 * rep;
+        }
+    } catch (...) {
+        if (ge) cudaGraphExecDestroy(ge);
+        if (g) cudaGraphDestroy(g);
+        cudaFree(d);
+        throw;
+    }
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    cudaFree(d);
+    *ok = good ? 1 : 0;
+}
+
 // In-place all-gather: send = recv + rank * count.
 void kr_nccl_allgather(kr_comm* c, const double* send, double* recv, size_t count, cudaStream_t s) {
     if (kr_comm_is_host(c)) {

@@ -220,7 +220,6 @@ struct kr_handle {
     int32_t nq, nqp;       // 2 + n_out ; 2 + n_box
     std::vector<BoxRow> boxes;
     int32_t TX, TY;
-    int32_t step_kv = 2;   // fused step kernel: 2 = 2 x 2 cells per thread (TX = 64), 1 = 4 y-strided cells per thread
 
     double* d_lzarr;       // [ndl][3][k+2] alpha / beta / s arrays of d_sc
     int steps_run0 = 0;

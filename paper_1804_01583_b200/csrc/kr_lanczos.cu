@@ -134,337 +134,6 @@ struct Geo {
     static_assert(NTC % NT == 0 && NR <= NT, "tile must map onto the CTA's threads");
 };
 
-template <int TX, int TY, int S>
-constexpr size_t step_smem_bytes() {
-    return (size_t)S * Geo<TX, TY>::STAGE + Geo<TX, TY>::WBYTES + 8 * S + 16;
-}
-
-// BCM: 0 = Dirichlet everywhere (zero ghosts from the TMA fill); 1 = general faces, but this tile has no
-// x/y face cell (only the uniform per-plane z-face terms and the ring cells' own corrections apply);
-// 2 = general faces on a tile that touches a y face (per-cell terms); 3 = general faces on a tile that
-// touches an x face only (per-thread x terms, no per-slot y terms).
-template <int TX, int TY, int S, bool INIT, bool FULL, int BCM, bool HALO>
-__device__ __forceinline__ void lz_march(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
-                                         unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
-                                         int zc0, int zc1, bool cta_box, double* acc) {
-    using G = Geo<TX, TY>;
-    const int tid = threadIdx.x;
-    const int pfirst = zc0 - 1, plast = zc1 + 1;
-    const bool has_prev = a.has_prev != 0;
-    auto issue = [&](int p) {
-        const int s = (p - pfirst) % S;
-        unsigned char* st = smem + s * G::STAGE;
-        const bool lp = has_prev && p > pfirst && p < plast;  // u_{i-1} is needed on planes zc0..zc1 only
-        mbar_expect_tx(&bar[s], G::CBYTES + (lp ? G::PBYTES : 0));
-        tma_load_3d(st, tmC, x0 - 2 - a.shC[0], y0 - 1 - a.shC[1], p + 1 - a.shC[2], &bar[s]);  // x start 16-byte aligned
-        if (lp) tma_load_3d(st + G::POFF, tmP, x0 - a.shP[0], y0 - a.shP[1], p + 1 - a.shP[2], &bar[s]);
-    };
-    // TMA loads are issued by lane 0 of the last warp: warps 0-2 carry the forward-ring cells
-    constexpr int ISSUER = G::NT - 32;
-    if (tid == ISSUER) {
-        const int np = min(plast - pfirst + 1, S);
-        for (int p = pfirst; p < pfirst + np; ++p) issue(p);
-    }
-    double sa = 1.0, sb = 0.0, sp = 0.0;
-    if (!INIT) {
-        const LzScalars* sc = a.sc;
-        const int i = a.step;
-        sa = sc->s[i];
-        sb = sc->alpha[i] * sc->s[i];
-        sp = (i > 1) ? sc->beta[i - 1] * sc->s[i - 1] : 0.0;
-    }
-    const double cx = a.cx, cy = a.cy, cz = a.cz;
-    const double diag = 2.0 * (cx + cy + cz);
-
-    // Thread -> cells: tile slot m is cell (x, y0 + ty + m * (NT/TX)) with x = tid % TX, ty = tid / TX,
-    // so all slots of a thread share x and the smem offsets differ by compile-time constants.
-    constexpr int RS = G::NT / TX;  // rows per slot step
-    const int x = tid % TX, ty = tid / TX;
-    const int gx = x0 + x;
-    const int ci0 = (ty + 1) * G::CW + x + 2, pi0 = ty * G::PW + x, wi0 = ty * G::WW + x;
-    bool ing[G::TS];
-    uint32_t bm[G::TS];
-#pragma unroll
-    for (int m = 0; m < G::TS; ++m) {
-        const int gy = y0 + ty + m * RS;
-        ing[m] = FULL || (gx < a.mx && gy < a.my);
-        uint32_t bb = 0;
-        if (cta_box)
-            for (int r = 0; r < a.nbox; ++r)
-                if (!((a.all_mask >> r) & 1u) && gx >= a.box[r].lo[0] && gx < a.box[r].hi[0] &&
-                    gy >= a.box[r].lo[1] && gy < a.box[r].hi[1])
-                    bb |= 1u << r;
-        bm[m] = bb;
-    }
-    // ghost-edge coefficients of the low faces (Dirichlet: c_a): x == 0, y == 0 (only slot 0 can have y == 0)
-    constexpr bool BC = BCM > 0, BCX = BCM == 2 || BCM == 3, BCY = BCM == 2;
-    const double gex = gx == 0 ? (BC ? a.gq[0] : cx) : 0.0;
-    const double gey0 = (y0 + ty == 0) ? (BC ? a.gq[2] : cy) : 0.0;
-    // general boundaries: diagonal corrections of face cells and the high-face edge coefficients
-    const double ex = BCX ? ((gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0)) : 0.0;
-    const double kx = (BCX && gx == a.mx - 1) ? a.gq[1] : cx;
-    double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)(y0 + ty) * a.pitch + gx;
-    const int64_t rowstep = (int64_t)RS * a.pitch;
-
-    const bool has_ring = tid < G::NR;
-    int rci, rpi, rwi;
-    bool ring_in;
-    double rexy = 0.0;  // ring cell's x/y diagonal correction (general boundaries)
-    {
-        const int rx = tid < TY ? TX : tid - TY;
-        const int ry = tid < TY ? tid : TY;
-        rci = (ry + 1) * G::CW + rx + 2;
-        rpi = ry * G::PW + rx;
-        rwi = ry * G::WW + rx;
-        ring_in = has_ring && (FULL || (x0 + rx < a.mx && y0 + ry < a.my));
-        if (BC) {
-            const int rgx = x0 + rx, rgy = y0 + ry;
-            rexy = (rgx == 0 ? a.ecor[0] : 0.0) + (rgx == a.mx - 1 ? a.ecor[1] : 0.0) +
-                   (rgy == 0 ? a.ecor[2] : 0.0) + (rgy == a.my - 1 ? a.ecor[3] : 0.0);
-        }
-    }
-
-    // u of three consecutive planes per tile slot (and ring cell) in three register sets that take turns as
-    // u_{q-1}, u_q, u_{q+1}: the plane loop is unrolled by three, so no register moves rotate them
-    double R0[G::TS], R1[G::TS], R2[G::TS];
-    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-    mbar_wait(&bar[0], 0);
-    mbar_wait(&bar[1 % S], 0);
-    {
-        const double* C0 = reinterpret_cast<const double*>(smem);
-        const double* C1 = reinterpret_cast<const double*>(smem + (1 % S) * G::STAGE);
-#pragma unroll
-        for (int m = 0; m < G::TS; ++m) {
-            R0[m] = C0[ci0 + m * RS * G::CW];
-            R1[m] = C1[ci0 + m * RS * G::CW];
-        }
-        if (has_ring) {
-            r0 = C0[rci];
-            r1 = C1[rci];
-        }
-    }
-    double acc_ww = 0.0, acc_d = 0.0, acc_sum = 0.0;
-    // plane q lives in stage sq; plane q+1 in stage sn with mbarrier phase ph (incremental, no modulo)
-    int sq = 1 % S, sn = 2 % S;
-    uint32_t ph = (2 / S) & 1;
-    // one plane q: w on the tile + forward ring (into the W buffer of q's parity), then the products of plane
-    // q-1 (w of q-1 is re-read from its W buffer); up / uc hold u_{q-1} / u_q, un receives u_{q+1}
-    auto plane = [&](const double (&up)[G::TS], const double (&uc)[G::TS], double (&un)[G::TS], const double rup,
-                     const double ruc, double& run, const int q) {
-        mbar_wait(&bar[sn], ph);
-        const unsigned char* stq = smem + sq * G::STAGE;
-        const double* Cq = reinterpret_cast<const double*>(stq) + ci0;
-        const double* Pq = reinterpret_cast<const double*>(stq + G::POFF) + pi0;
-        const double* Cn = reinterpret_cast<const double*>(smem + sn * G::STAGE) + ci0;
-        const bool zin = a.zoff + q < a.mz;  // uniform: the plane above the global grid is a zero ghost
-        double* Wq = ((q & 1) ? Wb1 : Wb0) + wi0;
-        double wc[G::TS];
-        // general boundaries: diagonal of this plane's cells relative to the Dirichlet stencil
-        const double dgz = BC ? diag - ex - ((a.zoff + q == 0) ? a.ecor[4] : 0.0) -
-                                    ((a.zoff + q == a.mz - 1) ? a.ecor[5] : 0.0)
-                              : diag;
-        const double cfz = fma(sa, dgz, sb);  // coefficient of u_i in w for this plane's cells
-#pragma unroll
-        for (int m = 0; m < G::TS; ++m) {
-            const int o = m * RS * G::CW;
-            un[m] = Cn[o];
-            double w;
-            if (INIT) {
-                w = uc[m];
-            } else {
-                const double sx = Cq[o - 1] + Cq[o + 1];
-                const double sy = Cq[o - G::CW] + Cq[o + G::CW];
-                const double sz = up[m] + un[m];
-                // w = s_i (A u_i) - alpha_i s_i u_i - ... = s_i (off-diagonal part) - (s_i diag + alpha_i s_i) u_i
-                double cf = cfz;
-                if (BCY) {
-                    const int gy = y0 + ty + m * RS;
-                    cf = fma(sa, dgz - ((gy == 0 ? a.ecor[2] : 0.0) + (gy == a.my - 1 ? a.ecor[3] : 0.0)), sb);
-                }
-                const double Ao = fma(cx, sx, fma(cy, sy, cz * sz));
-                w = fma(sa, Ao, -cf * uc[m]);
-                if (has_prev) w = fma(-sp, Pq[m * RS * G::PW], w);
-            }
-            if (!FULL && !ing[m]) w = 0.0;
-            Wq[m * RS * G::WW] = w;
-            wc[m] = w;
-        }
-        if (has_ring) {
-            const double* Cqb = reinterpret_cast<const double*>(stq);
-            run = reinterpret_cast<const double*>(smem + sn * G::STAGE)[rci];
-            double w = ruc;
-            if (!INIT) {
-                const double sx = Cqb[rci - 1] + Cqb[rci + 1];
-                const double sy = Cqb[rci - G::CW] + Cqb[rci + G::CW];
-                const double sz = rup + run;
-                const double rdg = BC ? dgz + ex - rexy : diag;  // dgz holds this thread's ex: swap in the ring's
-                const double Ao = fma(cx, sx, fma(cy, sy, cz * sz));
-                w = fma(sa, Ao, -fma(sa, rdg, sb) * ruc);
-                if (has_prev) w = fma(-sp, reinterpret_cast<const double*>(stq + G::POFF)[rpi], w);
-            }
-            if (!FULL && !ring_in) w = 0.0;
-            ((q & 1) ? Wb1 : Wb0)[rwi] = w;
-        }
-        // the plane above the global grid is a zero ghost: its w enters only as the z+1 neighbour of the last
-        // owned plane (its W plane and ring values are never read), through dz = zf * w_{q} - w_{q-1} below
-        const double zf = zin ? 1.0 : 0.0;
-        if (q > zc0) {  // products for plane q-1 (its w neighbours at x+1, y+1 were written last iteration)
-            const double* Wp = ((q & 1) ? Wb0 : Wb1) + wi0;
-            const int gzp = a.zoff + q - 1;
-            const double gz = (gzp == 0) ? (BC ? a.gq[4] : cz) : 0.0;
-            const double kz = (BC && gzp == a.mz - 1) ? a.gq[5] : cz;
-            uint32_t zmask = 0;
-            if (cta_box)
-                for (int r = 0; r < a.nbox; ++r)
-                    if (gzp >= a.box[r].lo[2] && gzp < a.box[r].hi[2]) zmask |= 1u << r;
-            const bool wr = !INIT && a.write_out;
-            double wp[G::TS];
-#pragma unroll
-            for (int m = 0; m < G::TS; ++m) {
-                const int o = m * RS * G::WW;
-                const double w0 = Wp[o];
-                wp[m] = w0;
-                const double dx = Wp[o + 1] - w0;
-                const double dy = Wp[o + G::WW] - w0;
-                const double dz = fma(wc[m], zf, -w0);  // exactly wc - w0, or -w0 above the grid
-                const double w2 = w0 * w0;
-                const double g = gex + gz + (m == 0 ? gey0 : 0.0);
-                const double ky = (BCY && y0 + ty + m * RS == a.my - 1) ? a.gq[3] : cy;
-                acc_d = fma(kx, dx * dx, fma(ky, dy * dy, fma(kz, dz * dz, fma(g, w2, acc_d))));
-                acc_ww += w2;
-                acc_sum += w0;
-                if (wr && (FULL || ing[m])) optr[m * rowstep] = w0;
-            }
-            if (zmask) {  // box output rows meeting this tile and plane (uniform, rare)
-#pragma unroll
-                for (int m = 0; m < G::TS; ++m) {
-                    const uint32_t mk = bm[m] & zmask;
-                    if (mk) {
-#pragma unroll
-                        for (int r = 0; r < KR_MAX_BOX; ++r)
-                            if ((mk >> r) & 1u) acc[3 + r] += wp[m];
-                    }
-                }
-            }
-            // halo planes for the neighbours, stored where they will be read (uniform per plane, rare):
-            // owned planes 0, 1 -> the lower neighbour, the last owned plane -> the upper neighbour
-            const int qq = q - 1;
-            if (HALO && wr && ((a.rlo && qq < 2) || (a.rhi && qq == a.nz - 1))) {
-                const int64_t off = (optr - a.out) - (int64_t)(qq + 1) * a.plane;  // in-plane offset of slot 0
-#pragma unroll
-                for (int m = 0; m < G::TS; ++m) {
-                    if (!(FULL || ing[m])) continue;
-                    if (a.rlo && qq < 2) a.rlo[a.rlo_plane0 + (int64_t)qq * a.plane + off + m * rowstep] = wp[m];
-                    if (a.rhi && qq == a.nz - 1) a.rhi[off + m * rowstep] = wp[m];
-                }
-            }
-            optr += a.plane;
-        }
-        __syncthreads();
-        if (tid == ISSUER) {
-            if (q == zc0 && pfirst + S <= plast) issue(pfirst + S);
-            if (q + S <= plast) issue(q + S);
-        }
-        sq = sn;
-        if (++sn == S) {
-            sn = 0;
-            ph ^= 1u;
-        }
-    };
-    // The general-boundary kernel holds five tile variants; unrolling them all overflows the instruction cache
-    // (ncu: 30% of its stall samples "no instructions", a launch 36% slower than the Dirichlet kernel's), so
-    // there only the full interior tiles (almost all tiles) are unrolled and the face tiles rotate their
-    // registers by moves. The Dirichlet kernel (two variants) unrolls both.
-    constexpr bool UNROLL = BCM == 0 || (FULL && BCM == 1);
-    if (UNROLL) {
-        for (int q = zc0;;) {
-            plane(R0, R1, R2, r0, r1, r2, q);
-            if (++q > zc1) break;
-            plane(R1, R2, R0, r1, r2, r0, q);
-            if (++q > zc1) break;
-            plane(R2, R0, R1, r2, r0, r1, q);
-            if (++q > zc1) break;
-        }
-    } else {
-#pragma unroll 1
-        for (int q = zc0; q <= zc1; ++q) {
-            plane(R0, R1, R2, r0, r1, r2, q);
-#pragma unroll
-            for (int m = 0; m < G::TS; ++m) {
-                R0[m] = R1[m];
-                R1[m] = R2[m];
-            }
-            r0 = r1;
-            r1 = r2;
-        }
-    }
-    acc[0] += acc_ww;
-    acc[1] += acc_d;
-    acc[2] += acc_sum;
-}
-
-template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false>
-__global__ void __launch_bounds__(Geo<TX, TY>::NT, (TX * TY >= 2048) ? 1 : ((TX * TY > 512) ? 2 : 3)) lz_step_kernel(const __grid_constant__ CUtensorMap tmC,
-                                                         const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
-    using G = Geo<TX, TY>;
-    if (a.sc->done) return;  // breakdown happened earlier: uniform early exit
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    double* Wb0 = reinterpret_cast<double*>(smem + S * G::STAGE);
-    double* Wb1 = Wb0 + G::WW * G::WH;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * G::STAGE + G::WBYTES);
-
-    const int tid = threadIdx.x;
-    double acc[3 + KR_MAX_BOX];
-#pragma unroll
-    for (int r = 0; r < 3 + KR_MAX_BOX; ++r) acc[r] = 0.0;
-    // Persistent CTAs: work items (x-tile, y-tile, z-chunk) are dealt round-robin (fixed assignment,
-    // deterministic); consecutive items run concurrently, so neighbouring tiles share halo planes in L2.
-    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
-        const int xt = a.ix0 + item % a.gx, yt = a.iy0 + (item / a.gx) % a.gy, zt = a.iz0 + item / (a.gx * a.gy);
-        const int x0 = xt * TX, y0 = yt * TY;
-        const int zc0 = zt * a.zchunk;
-        const int zc1 = min(zc0 + a.zchunk, a.nz);
-        if (tid == 0) {
-#pragma unroll
-            for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-        // does any (non all-grid) box output row intersect this tile and z-chunk? (usually not)
-        bool cta_box = false;
-        for (int r = 0; r < a.nbox; ++r)
-            if (!((a.all_mask >> r) & 1u) && a.box[r].lo[0] < x0 + TX && a.box[r].hi[0] > x0 &&
-                a.box[r].lo[1] < y0 + TY && a.box[r].hi[1] > y0 && a.box[r].lo[2] < a.zoff + zc1 &&
-                a.box[r].hi[2] > a.zoff + zc0)
-                cta_box = true;
-        // interior tiles (the forward ring inside the grid) skip all x/y masking
-        constexpr int BCE = BC ? 2 : 0;
-        const bool yin = y0 > 0 && y0 + TY < a.my - 1;  // no y face cell (y = 0 or my - 1) in the tile
-        if (x0 + TX < a.mx && y0 + TY < a.my) {
-            if (BC && x0 > 0 && y0 > 0)  // no x/y face cell in the tile: only per-plane z-face terms
-                lz_march<TX, TY, S, INIT, true, 1, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
-            else if (BC && yin)  // x face only
-                lz_march<TX, TY, S, INIT, true, 3, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
-            else
-                lz_march<TX, TY, S, INIT, true, BCE, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
-        } else if (BC && yin) {
-            lz_march<TX, TY, S, INIT, false, 3, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
-        } else {
-            lz_march<TX, TY, S, INIT, false, BCE, HALO>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, acc);
-        }
-        __syncthreads();  // every issued plane was consumed: the barriers can be recycled for the next item
-        if (tid == 0) {
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-                asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar[s])) : "memory");
-        }
-    }
-
-    if (HALO && a.rfence) __threadfence_system();  // peer-memory halo stores visible before the collective that follows
-    __syncthreads();  // stage buffers are free: reuse them as reduction scratch
-    lz_epilogue<G::NT>(a, acc, reinterpret_cast<double*>(smem), a.plane);
-}
 
 // ================================================================================================
 // Step kernel v2: 2 x 2 cells per thread.
@@ -1272,10 +941,9 @@ struct Stages {
 }  // namespace
 
 size_t kr_lz_step_smem(int TX, int TY) {
-    if (TX == 64 && TY == 32) return step_smem_bytes<64, 32, Stages<64, 32>::S>();
-    if (TX == 64 && TY == 16) return step_smem_bytes<64, 16, Stages<64, 16>::S>();
-    if (TX == 64 && TY == 8) return step_smem_bytes<64, 8, Stages<64, 8>::S>();
-    if (TX == 32 && TY == 8) return step_smem_bytes<32, 8, Stages<32, 8>::S>();
+    if (TX == 64 && TY == 32) return step2_smem_bytes<64, 32, Stages<64, 32>::S>();
+    if (TX == 64 && TY == 16) return step2_smem_bytes<64, 16, Stages<64, 16>::S>();
+    if (TX == 64 && TY == 8) return step2_smem_bytes<64, 8, Stages<64, 8>::S>();
     return 0;
 }
 
@@ -1356,13 +1024,6 @@ void kr_lz_setup_compact(kr_handle* h) {
 }
 
 template <int TX, int TY, bool INIT, bool BC, bool HALO = false>
-static void set_smem_attr() {
-    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel<TX, TY, Stages<TX, TY>::S, INIT, BC, HALO>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
-}
-
-template <int TX, int TY, bool INIT, bool BC, bool HALO = false>
 static void set_smem_attr2() {
     KR_CUDA(cudaFuncSetAttribute(lz_step_kernel2<TX, TY, Stages<TX, TY>::S, INIT, BC, HALO>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1370,49 +1031,30 @@ static void set_smem_attr2() {
 }
 
 template <int TX, int TY>
-static int occupancy_t(int kv) {
-    if constexpr (TX == 64) {
-        set_smem_attr2<TX, TY, false, false>();
-        set_smem_attr2<TX, TY, true, false>();
-        set_smem_attr2<TX, TY, false, true>();
-        set_smem_attr2<TX, TY, true, true>();
-        set_smem_attr2<TX, TY, false, false, true>();
-        set_smem_attr2<TX, TY, false, true, true>();
-    }
-    set_smem_attr<TX, TY, false, false>();
-    set_smem_attr<TX, TY, true, false>();
-    set_smem_attr<TX, TY, false, true>();
-    set_smem_attr<TX, TY, true, true>();
-    set_smem_attr<TX, TY, false, false, true>();
-    set_smem_attr<TX, TY, false, true, true>();
-    if constexpr (TX == 64) {
-        if (kv == 2) {
-            int n1 = 0, n2 = 0;
-            const size_t sm2 = step2_smem_bytes<TX, TY, Stages<TX, TY>::S>();
-            KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, false>,
-                                                                  Geo2<TX, TY>::NT, sm2));
-            KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, true>,
-                                                                  Geo2<TX, TY>::NT, sm2));
-            return n1 < n2 ? n1 : n2;
-        }
-    }
-    int nb = 0, nb2 = 0;
-    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, false>,
-                                                          Geo<TX, TY>::NT, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
-    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, lz_step_kernel<TX, TY, Stages<TX, TY>::S, false, true>,
-                                                          Geo<TX, TY>::NT, step_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
-    return nb < nb2 ? nb : nb2;
+static int occupancy_t() {
+    set_smem_attr2<TX, TY, false, false>();
+    set_smem_attr2<TX, TY, true, false>();
+    set_smem_attr2<TX, TY, false, true>();
+    set_smem_attr2<TX, TY, true, true>();
+    set_smem_attr2<TX, TY, false, false, true>();
+    set_smem_attr2<TX, TY, false, true, true>();
+    int n1 = 0, n2 = 0;
+    const size_t sm2 = step2_smem_bytes<TX, TY, Stages<TX, TY>::S>();
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, false>,
+                                                          Geo2<TX, TY>::NT, sm2));
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, true>,
+                                                          Geo2<TX, TY>::NT, sm2));
+    return n1 < n2 ? n1 : n2;
 }
 
-int kr_lz_occupancy(int TX, int TY, int kv) {
-    if (TX == 64 && TY == 32) return occupancy_t<64, 32>(kv);
-    if (TX == 64 && TY == 16) return occupancy_t<64, 16>(kv);
-    if (TX == 64 && TY == 8) return occupancy_t<64, 8>(kv);
-    if (TX == 32 && TY == 8) return occupancy_t<32, 8>(1);
+int kr_lz_occupancy(int TX, int TY) {
+    if (TX == 64 && TY == 32) return occupancy_t<64, 32>();
+    if (TX == 64 && TY == 16) return occupancy_t<64, 16>();
+    if (TX == 64 && TY == 8) return occupancy_t<64, 8>();
     return 1;
 }
 
-void kr_lz_prepare(kr_handle* h) { (void)kr_lz_occupancy(h->TX, h->TY, h->step_kv); }
+void kr_lz_prepare(kr_handle* h) { (void)kr_lz_occupancy(h->TX, h->TY); }
 
 // cmode: 0 = full state buffers; 1 = u_i is the compact u_1 (init pass / step 1); 2 = u_{i-1} is (step 2)
 static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, bool init, bool write, int gather_buf,
@@ -1518,7 +1160,6 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
 template <int TX, int TY>
 static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int nxt, int step, bool init,
                           bool write, bool fillinit, int cmode) {
-    const size_t smem = step_smem_bytes<TX, TY, Stages<TX, TY>::S>();
     if (fillinit) {
         StepArgs a = make_args(h, sl, dl, cur, 0, true, false, cur);
         a.gen = h->dirs_h[h->my_dirs[dl]];
@@ -1530,44 +1171,22 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
         const dim3 grid = (cmode == 1 && init) ? dim3((unsigned)std::max<int64_t>(1, sl.cu1[dl].nitems), 1, 1) : sl.grid;
         constexpr int S = Stages<TX, TY>::S;
         const bool halo = a.rlo || a.rhi;  // this slab writes halo planes into a neighbour's buffer
-        if constexpr (TX == 64) {
-            if (h->step_kv == 2) {
-                const size_t smem2 = step2_smem_bytes<TX, TY, S>();
-                constexpr int NT2 = Geo2<TX, TY>::NT;
-                if (h->gen_bc) {
-                    if (init)
-                        lz_step_kernel2<TX, TY, S, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-                    else if (halo)
-                        lz_step_kernel2<TX, TY, S, false, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-                    else
-                        lz_step_kernel2<TX, TY, S, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-                } else {
-                    if (init)
-                        lz_step_kernel2<TX, TY, S, true, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-                    else if (halo)
-                        lz_step_kernel2<TX, TY, S, false, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-                    else
-                        lz_step_kernel2<TX, TY, S, false, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-                }
-                KR_CUDA(cudaGetLastError());
-                h->launches++;
-                return;
-            }
-        }
+        const size_t smem2 = step2_smem_bytes<TX, TY, S>();
+        constexpr int NT2 = Geo2<TX, TY>::NT;
         if (h->gen_bc) {
             if (init)
-                lz_step_kernel<TX, TY, S, true, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel2<TX, TY, S, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
             else if (halo)
-                lz_step_kernel<TX, TY, S, false, true, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel2<TX, TY, S, false, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
             else
-                lz_step_kernel<TX, TY, S, false, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel2<TX, TY, S, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
         } else {
             if (init)
-                lz_step_kernel<TX, TY, S, true, false><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel2<TX, TY, S, true, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
             else if (halo)
-                lz_step_kernel<TX, TY, S, false, false, true><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel2<TX, TY, S, false, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
             else
-                lz_step_kernel<TX, TY, S, false, false><<<grid, Geo<TX, TY>::NT, smem, h->stream>>>(tc, tp, a);
+                lz_step_kernel2<TX, TY, S, false, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
         }
     }
     KR_CUDA(cudaGetLastError());
@@ -1575,11 +1194,10 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
 }
 
 // CTAs of the slab reduction: ~512 per-CTA partials each, at most one per 64 partials (the [G][nqp] sums
-// live in the ngrp * nqp doubles behind the partials) and at most 148; KR_RED_CTAS overrides (tuning).
+// live in the ngrp * nqp doubles behind the partials) and at most 148.
 static int kr_reduce_ctas(int64_t nblk) {
     const int64_t ngrp = (nblk + 63) / 64;
     int64_t g = (nblk + 511) / 512;
-    if (const char* e = getenv("KR_RED_CTAS")) g = atoi(e);
     g = std::min<int64_t>(std::min<int64_t>(g, 148), ngrp);
     return (int)std::max<int64_t>(1, g);
 }
@@ -1603,8 +1221,6 @@ static void step_launch(kr_handle* h, Slab& sl, int dl, int cur, int prev, int n
         step_launch_t<64, 32>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else if (h->TX == 64 && h->TY == 8)
         step_launch_t<64, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
-    else if (h->TX == 32 && h->TY == 8)
-        step_launch_t<32, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else
         KR_THROW(KR_EINVAL, "unsupported tile");
 }

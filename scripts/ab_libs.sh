@@ -2,7 +2,7 @@
 # A/B of library builds (scratch_libs/libkr_<name>.so copied over the in-tree library in the box's copy of the
 # repo): per-step times of C5 and C4 (scripts/step_profile.py) and the dense C5D bench line, alternating twice.
 # Usage (under gpurun): bash scripts/ab_libs.sh name1 name2 ...
-export KR_STEP_V=${KR_STEP_V:-2}
+
 for rep in 1 2; do
   for lib in "$@"; do
     cp scratch_libs/libkr_$lib.so paper_1804_01583_b200/libkrylov_reach.so

@@ -21,5 +21,5 @@ with KrylovReach(p) as h:
         h.project(want=False)
         runs.append(h.step_times())
 st = np.nanmean(np.array(runs), axis=0)
-print(f"{cfg} KR_STEP_V={os.environ.get('KR_STEP_V', 'default')}: step1 {st[0]:.4f} ms step2 {st[1]:.4f} "
+print(f"{cfg}: step1 {st[0]:.4f} ms step2 {st[1]:.4f} "
       f"steps3..k-1 {np.mean(st[2:-1]):.4f} last {st[-1]:.4f}")

@@ -58,6 +58,7 @@ def worker(rank, world, port, name, thresholds, q):
     try:
         torch.cuda.set_device(0)
         comm = KrComm.host(rank, world, 0)
+        assert comm.selftest(reps=2), "host-transport all-gather self test"
         p, kw = case(name)
         with KrylovReach(p, device=0, comm=comm, **kw) as h:
             on = h.attach_peers(rank, world, torch_allgather_bytes, dist.barrier) if name.endswith("ipc") else False
@@ -113,3 +114,19 @@ def test_multirank_processes_on_one_gpu(name, world):
             assert on, (name, rank, "peer-memory halo transport not enabled")
     if adaptive:
         assert [s["k_eff"] for s in res[0][2]] == [r["k_eff"] for r in ref["per_dir"]]
+
+
+def test_nccl_one_rank_graph_capture():
+    """NCCL itself on this one-GPU box: a 1-rank communicator from a broadcast unique id (the KrComm path of
+    bench.py), its all-gather captured in a CUDA graph and replayed (krylov_comm_selftest — the same call the
+    z-slab run makes every Krylov step), and a krylov_project on a handle that carries the communicator."""
+    from paper_1804_01583_b200 import KrComm, KrylovReach
+    comm = KrComm(0, 1, 0, lambda data: data)
+    try:
+        assert comm.selftest(reps=4)
+        p = W.heat(20, 3, 12, n_steps=40)
+        with KrylovReach(p, device=0, comm=comm, part="zslab") as h:
+            coeff, _ = h.project()
+        assert_coeff(coeff, oracle.krylov_project(p)["coeff"], "1-rank NCCL communicator")
+    finally:
+        comm.close()
