@@ -243,6 +243,8 @@ struct kr_handle {
     double* d_big;         // 6 x kcap^2 doubles: X, X^2, X^3, X^4, Y, Y'
     double* d_traj;        // [(n_steps+1)][kcap] x_j = e^{H t_j} e_1
     int large_cap = 0;     // padded dimension the large-route scratch is sized for
+    double* d_gpart = nullptr;      // split-K partial sums of the band GEMMs
+    size_t large_part_doubles = 0;
     double* d_lbound;      // [ndl] unit-vector Lemma 1 bound of the accepted k
     double* d_scratch;     // small device scratch (norms, bound)
     std::vector<std::vector<std::pair<int32_t, double>>> checks;  // per local direction: (k, bound)

@@ -52,6 +52,12 @@ struct GemmArgs {
     int M, N, K, lda, ldb, ldc;
     int ba, bb, kc;
     double scale, diag;
+    // split-K (small grids: the 64 x 64 tiles of a kc ~ 500 product fill 9-81 SMs): blockIdx.z takes a contiguous
+    // share of the tile's k-tiles and writes its raw sums to part[z][M][ldp]; gemm_reduce_kernel adds the shares in
+    // z order (fixed order: deterministic) and applies scale and diag
+    int nsplit;
+    double* part;
+    int ldp;
 };
 
 // fp64 tensor-core tile: DMMA.8x8x4 (mma.sync m8n8k4 f64) — 4 warps, each a 32x32 block of the 64x64 CTA tile
@@ -92,9 +98,15 @@ __global__ void __launch_bounds__(DT) gemm_band_kernel(const GemmArgs g) {
             lo = max(lo, (long long)j0 - g.bb);
             hi = min(hi, (long long)j0 + GT + g.bb);
         }
-        const int l0 = (int)(lo / GK) * GK;
+        int l0 = (int)(lo / GK) * GK;
         const int l1 = (int)((hi + GK - 1) / GK) * GK;
-        const int nkt = (l1 - l0) / GK;
+        int nkt = (l1 - l0) / GK;
+        if (g.nsplit > 1) {  // this split's contiguous share of the k-tiles
+            const int per = (nkt + g.nsplit - 1) / g.nsplit;
+            const int t0 = min(nkt, (int)blockIdx.z * per), t1 = min(nkt, t0 + per);
+            l0 += t0 * GK;
+            nkt = t1 - t0;
+        }
         // global -> register staging (8 + 8 doubles per thread): A rows i0 + ar + 8q, col ac; B row br + 2q, col bcn
         const int ar = tid >> 4, ac = tid & 15;
         const int br = tid >> 6, bcn = tid & 63;
@@ -147,10 +159,27 @@ __global__ void __launch_bounds__(DT) gemm_band_kernel(const GemmArgs g) {
             for (int h = 0; h < 2; ++h) {
                 const int i = i0 + wm + 8 * a + fm, j = j0 + wn + 8 * b + 2 * fk + h;
                 if (j >= g.N) continue;
+                if (g.nsplit > 1) {
+                    g.part[((size_t)blockIdx.z * g.M + i) * g.ldp + j] = acc[a][b][h];
+                    continue;
+                }
                 double v = g.scale * acc[a][b][h];
                 if (i == j && i < g.kc) v += g.diag;
                 g.C[(size_t)i * g.ldc + j] = v;
             }
+}
+
+// split-K epilogue: C = scale * sum_z part[z] + diag * I (z in order)
+__global__ void gemm_reduce_kernel(const GemmArgs g) {
+    const int64_t n = (int64_t)g.M * g.N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / g.N), j = (int)(e - (int64_t)i * g.N);
+        double s = 0.0;
+        for (int z = 0; z < g.nsplit; ++z) s += g.part[((size_t)z * g.M + i) * g.ldp + j];
+        double v = g.scale * s;
+        if (i == j && i < g.kc) v += g.diag;
+        g.C[(size_t)i * g.ldc + j] = v;
+    }
 }
 
 // ||H delta||_1 (max column sum of the symmetric tridiagonal; 1-based alpha[1..kc], beta[1..kc-1]).
@@ -392,6 +421,15 @@ void kr_large_alloc(kr_handle* h, int kc) {
     const size_t mat = (size_t)kp * kp;
     KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&h->d_big), 3 * mat * sizeof(double)));
     h->extra_allocs.push_back(h->d_big);
+    // split-K partial sums: four k x k products' worth, at most 8 Mi doubles (64 MB)
+    if (h->d_gpart) {
+        kr_dev_free(h->d_gpart);
+        h->extra_allocs.erase(std::remove(h->extra_allocs.begin(), h->extra_allocs.end(), (void*)h->d_gpart),
+                              h->extra_allocs.end());
+    }
+    h->large_part_doubles = std::min<size_t>(4 * mat, (size_t)8 << 20);
+    KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&h->d_gpart), h->large_part_doubles * sizeof(double)));
+    h->extra_allocs.push_back(h->d_gpart);
     // row layout [(N+1)][kp] for the march, column layout [kp][pow2 >= N+1] for the doubling route
     const size_t tr = std::max((size_t)(h->n_steps + 1) * kp, (size_t)kp * pow2_at_least(h->n_steps + 1));
     KR_CUDA(kr_dev_malloc(reinterpret_cast<void**>(&h->d_traj), tr * sizeof(double)));
@@ -401,11 +439,25 @@ void kr_large_alloc(kr_handle* h, int kc) {
 
 static void gemm(kr_handle* h, const double* A, const double* B, double* C, int M, int N, int K, int lda, int ldb,
                  int ldc, int ba, int bb, int kc, double scale, double diag) {
-    GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, ba, bb, kc, scale, diag};
+    GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, ba, bb, kc, scale, diag, 1, nullptr, 0};
     const dim3 grid((unsigned)((N + GT - 1) / GT), (unsigned)(M / GT));
-    gemm_band_kernel<<<grid, DT, 0, h->stream>>>(g);
+    // split K when the tiles cover fewer than two waves of SMs (kc ~ 500: 9-81 tiles), into shares of >= 4 k-tiles
+    const int tiles = (int)(grid.x * grid.y), nkt = K / GK;
+    int ns = std::min(std::min(32, std::max(1, 296 / tiles)), std::max(1, nkt / 4));
+    g.ldp = (int)grid.x * GT;
+    while (ns > 1 && (size_t)ns * M * g.ldp > h->large_part_doubles) --ns;
+    if (getenv("KR_GEMM_NOSPLIT")) ns = 1;
+    g.nsplit = ns;
+    g.part = h->d_gpart;
+    gemm_band_kernel<<<dim3(grid.x, grid.y, ns), DT, 0, h->stream>>>(g);
     KR_CUDA(cudaGetLastError());
     h->launches++;
+    if (ns > 1) {
+        const int64_t n = (int64_t)M * N;
+        gemm_reduce_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, h->stream>>>(g);
+        KR_CUDA(cudaGetLastError());
+        h->launches++;
+    }
 }
 
 // Evaluate the large-k route for local direction dl at dimension kc (the leading kc x kc block of the

@@ -488,3 +488,33 @@ def test_device_block_cache_reuse_and_release():
     assert krylov_release_cached_memory() == 0
     c, _, _, _ = gpu_run(p)
     assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("env", [{"KR_ZCHUNK": "1"}, {"KR_ZCHUNK": "3"}, {"KR_ZCHUNK": "500"}, {"KR_NO_GRAPH": "1"},
+                                 {"KR_HALO_COPY": "1"}])
+def test_stencil_switches_keep_parity(env, monkeypatch):
+    """The diagnostic switches of the fused stencil path (README) change scheduling only: z-chunks of 1, 3 and all
+    planes, no CUDA graph, the copy halo transport on 3 virtual slabs — equal to the oracle; the z-chunk choice only
+    reorders the per-CTA partial sums."""
+    p = W.heat(70, 5, 20, n_steps=80, step=0.02, my=40, mz=33)
+    p["gens"].append(W.rand(11, 0.3))
+    p["z_lo"] = np.array([0.9, 0.0])
+    p["z_hi"] = np.array([1.1, 1.0])
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    kw = dict(virtual_slabs=3, part="zslab") if "KR_HALO_COPY" in env else {}
+    coeff, _, _, _ = gpu_run(p, **kw)
+    assert_coeff(coeff, oracle.krylov_project(p)["coeff"], f"switches {env}")
+
+
+def test_spmm_per_direction_equals_block(monkeypatch):
+    """The block SpMM (each CSR row read once for all directions) sums every row in entry order, like one thread per
+    (row, direction): bitwise equal results (C2 recipe, 5 directions, both Arnoldi routes)."""
+    p = W.config2(n=3000, n_gen=5, n_steps=100, k=25)
+    for cgs in ("0", "1"):
+        monkeypatch.setenv("KR_FORCE_CGS", cgs)
+        monkeypatch.delenv("KR_SPMM_PER_DIR", raising=False)
+        a, _, _, _ = gpu_run(p)
+        monkeypatch.setenv("KR_SPMM_PER_DIR", "1")
+        b, _, _, _ = gpu_run(p)
+        assert np.array_equal(a, b), cgs
