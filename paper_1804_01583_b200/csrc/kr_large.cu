@@ -219,42 +219,57 @@ __global__ void large_build_kernel(const LzScalars* sc, int kc, int kp, double f
     }
 }
 
-// The Horner steps Y <- I + X Y / q, q = 17 .. 1, of T_18(X) for the TRIDIAGONAL X = H delta / 2^s, in one CTA:
-// (X Y)_{ij} = X_{i,i-1} Y_{i-1,j} + X_{ii} Y_{ij} + X_{i,i+1} Y_{i+1,j}, and after m products Y is banded with
-// half-bandwidth m + 1, so each step touches only kc (2m + 3) entries (the band GEMM route took 17 launches).
-// Y0 holds I + X / 18 (large_build_kernel, zero elsewhere); the steps alternate Y0 -> Y1 -> Y0 ... and the band of
-// the last one (in Y1) is copied back into Y0, whose entries outside the band are still 0. Only band entries are
-// read, so the previous contents of Y1 do not matter.
-__global__ void __launch_bounds__(1024) large_taylor_tri_kernel(const LzScalars* sc, int kc, int kp, double f,
-                                                                 double* Y0, double* Y1) {
-    const double* Ycur = Y0;
-    double* Ynew = Y1;
-    int bc = 1;  // half-bandwidth of Ycur
-    for (int q = 17; q >= 1; --q) {
-        const int bn = bc + 1;
-        const int64_t ne = (int64_t)kc * (2 * bn + 1);
-        const double inv = 1.0 / q;
-        for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) {
-            const int i = (int)(e / (2 * bn + 1)), j = i + (int)(e % (2 * bn + 1)) - bn;
-            if (j < 0 || j >= kc) continue;
-            double s = 0.0;
-            if (i >= 1 && abs(i - 1 - j) <= bc) s = fma(sc->beta[i] * f, Ycur[(size_t)(i - 1) * kp + j], s);
-            if (abs(i - j) <= bc) s = fma(sc->alpha[i + 1] * f, Ycur[(size_t)i * kp + j], s);
-            if (i + 1 < kc && abs(i + 1 - j) <= bc) s = fma(sc->beta[i + 1] * f, Ycur[(size_t)(i + 1) * kp + j], s);
-            Ynew[(size_t)i * kp + j] = s * inv + (i == j ? 1.0 : 0.0);
-        }
-        __syncthreads();
-        const double* t = Ycur;
-        Ycur = Ynew;
-        Ynew = const_cast<double*>(t);
-        bc = bn;
+// Y = T_18(X) = sum_{m=0}^{18} X^m / m! for the TRIDIAGONAL X = H delta / 2^s by the Horner steps
+// Y <- I + X Y / q (q = 17 .. 1, from Y = I + X / 18), one column per thread: column j of X Y only involves column j
+// of Y, (X Y)_{ij} = X_{i,i-1} Y_{i-1,j} + X_{ii} Y_{ij} + X_{i,i+1} Y_{i+1,j}, and after m products the column is
+// non-zero only on rows j - m - 1 .. j + m + 1, so the whole polynomial is 37 registers per thread updated in place
+// (no synchronisation; the band GEMM route took 17 launches). The band is written into Y, whose entries outside
+// it are still 0 from large_build_kernel.
+constexpr int TB = 18;  // half-bandwidth of T_18(X)
+__global__ void __launch_bounds__(128) large_taylor_col_kernel(const LzScalars* sc, int kc, int kp, double f, double* Y) {
+    __shared__ double sa[128 + 2 * TB + 2], sb[128 + 2 * TB + 2];  // alpha, beta of the rows this CTA's columns touch
+    const int c0 = blockIdx.x * 128;
+    for (int e = threadIdx.x; e < 128 + 2 * TB + 2; e += blockDim.x) {
+        const int i = c0 - TB - 1 + e;  // 0-based row
+        sa[e] = (i >= 0 && i < kc) ? sc->alpha[i + 1] * f : 0.0;                  // X_{ii}
+        sb[e] = (i >= 0 && i + 1 < kc) ? sc->beta[i + 1] * f : 0.0;               // X_{i,i+1} = X_{i+1,i}
     }
-    if (Ycur != Y0) {
-        const int64_t ne = (int64_t)kc * (2 * bc + 1);
-        for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) {
-            const int i = (int)(e / (2 * bc + 1)), j = i + (int)(e % (2 * bc + 1)) - bc;
-            if (j >= 0 && j < kc) Y0[(size_t)i * kp + j] = Ycur[(size_t)i * kp + j];
+    __syncthreads();
+    const int j = c0 + threadIdx.x;
+    if (j >= kc) return;
+    double y[2 * TB + 1];  // y[o] = Y_{j + o - TB, j}
+#pragma unroll
+    for (int o = 0; o < 2 * TB + 1; ++o) y[o] = 0.0;
+    const int base = j - c0 + 1;  // sa / sb index of row j - TB is base + (o = 0)
+    // Y = I + X / 18 (the innermost Horner factor)
+    y[TB] = 1.0 + sa[base + TB] / 18.0;
+    if (j >= 1) y[TB - 1] = sb[base + TB - 1] / 18.0;
+    if (j + 1 < kc) y[TB + 1] = sb[base + TB] / 18.0;
+#pragma unroll
+    for (int q = 17; q >= 1; --q) {
+        const double inv = 1.0 / q;
+        double prev = 0.0;  // the old value of row i - 1
+#pragma unroll
+        for (int o = 0; o < 2 * TB + 1; ++o) {
+            const int i = j + o - TB;
+            const double cur = y[o];
+            const double nxt = o < 2 * TB ? y[o + 1] : 0.0;
+            double v = 0.0;
+            if (i >= 0 && i < kc) {
+                const double lo = sb[base + o - 1], dg = sa[base + o], up = sb[base + o];  // X_{i,i-1}, X_{ii}, X_{i,i+1}
+                double s = fma(lo, prev, 0.0);
+                s = fma(dg, cur, s);
+                s = fma(up, nxt, s);
+                v = s * inv + (o == TB ? 1.0 : 0.0);
+            }
+            prev = cur;
+            y[o] = v;
         }
+    }
+#pragma unroll
+    for (int o = 0; o < 2 * TB + 1; ++o) {
+        const int i = j + o - TB;
+        if (i >= 0 && i < kc) Y[(size_t)i * kp + j] = y[o];
     }
 }
 
@@ -526,13 +541,13 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
         h->launches++;
     }
     // Horner: Y = I + X Y / q, q = 17..1  ->  Y = T_18(X); bandwidth of Y grows by one per product
-    // (tridiagonal X: one CTA over the band, large_taylor_tri_kernel); a Hessenberg X is treated as dense
+    // (tridiagonal X: one column per thread, large_taylor_col_kernel); a Hessenberg X is treated as dense
     const int bwX = tri ? 1 : bmax;
     int bwY = tri ? 1 : bmax;
     double* Y = Y0;
     double* Z = Y1;
     if (tri) {
-        large_taylor_tri_kernel<<<1, 1024, 0, st>>>(sc, kc, kp, f, Y0, Y1);
+        large_taylor_col_kernel<<<(kc + 127) / 128, 128, 0, st>>>(sc, kc, kp, f, Y0);
         KR_CUDA(cudaGetLastError());
         h->launches++;
         bwY = std::min(18, bmax);
