@@ -176,6 +176,18 @@ __device__ __forceinline__ double chunk_update(const double* __restrict__ V, int
     return s2;
 }
 
+// sum over the chunks of a per-chunk partial (stride doubles apart), by one warp: lane t sums chunks t, t + 32, ...
+// in order, a shuffle tree adds the lanes, lane 0's value is broadcast (the same association on every lane and in
+// every CTA that computes it: bit-identical). All 32 lanes must call it.
+__device__ __forceinline__ double chunk_sum_warp(const double* p, int nchunk, int64_t stride) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int c = lane; c < nchunk; c += 32) s += p[(int64_t)c * stride];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    return __shfl_sync(0xffffffffu, s, 0);
+}
+
 // hs[l] = h of pass `pass` for l < j: from the reduce kernel, or summed here over the chunks in order
 __device__ __forceinline__ void load_h(const CgsArgs& a, int d, int pass, double* hs) {
     const int j = a.j;
@@ -253,12 +265,10 @@ __global__ void __launch_bounds__(CT) cgs_apply_dots_kernel(CgsArgs a) {
     const Smem S = smem_layout(a);
     const int b = blockIdx.x, j = a.j;
     const int64_t N = a.N, i0 = (int64_t)b * a.chunk, i1 = min(i0 + a.chunk, N);
-    if (b == 0)
-        for (int r = threadIdx.x; r < a.n_out; r += CT) {
-            const double* p = a.part + poff(a, d, 0) + 2 * (a.k + 1) + 1 + r;
-            double s = 0.0;
-            for (int c = 0; c < a.nchunk; ++c) s += p[(int64_t)c * a.pstride];
-            a.P[((int64_t)d * a.n_out + r) * a.k + (j - 1)] = s;
+    if (b == 0)  // P[., j-1] = C v_{j-1}: a warp per output row over the chunk partials
+        for (int r = threadIdx.x >> 5; r < a.n_out; r += CT / 32) {
+            const double s = chunk_sum_warp(a.part + poff(a, d, 0) + 2 * (a.k + 1) + 1 + r, a.nchunk, a.pstride);
+            if ((threadIdx.x & 31) == 0) a.P[((int64_t)d * a.n_out + r) * a.k + (j - 1)] = s;
         }
     const double* Vd = a.V + (int64_t)d * (a.k + 1) * N;
     const double* x = Vd + (int64_t)(j - 1) * N;
@@ -369,11 +379,10 @@ __global__ void __launch_bounds__(CT) cgs_normalize_kernel(CgsArgs a) {
     __shared__ int s_go;
     const int b = blockIdx.x, j = a.j, k = a.k;
     const bool lead = b == 0;
+    double s2 = 0.0;
+    if (threadIdx.x < 32) s2 = chunk_sum_warp(a.part + poff(a, d, 0) + 2 * (k + 1), a.nchunk, a.pstride);
     if (threadIdx.x == 0) {
-        const double* p = a.part + poff(a, d, 0) + 2 * (k + 1);
-        double s = 0.0;
-        for (int c = 0; c < a.nchunk; ++c) s += p[(int64_t)c * a.pstride];
-        const double nb = sqrt(s);
+        const double nb = sqrt(s2);
         int go = 1;
         if (j == 0) {
             if (lead) {

@@ -363,19 +363,36 @@ __global__ void large_project_kernel(const double* traj, int kp, int kc, const d
 }
 
 // Column layout (doubling route): x_j[l] = Xc[l * ldx + j]. One thread per time step j, fixed-order sums.
-__global__ void large_project_cols_kernel(const double* Xc, int ldx, int kc, const double* P, int kstride, int n_out,
-                                          const double* beta0, double* coeff, int ndl_stride, int dl, double* hlast,
-                                          int64_t n_steps) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j > n_steps) return;
+// c[j][r][dl] = beta0 (P x_j)_r and h(t_j) = x_j[kc-1] from the column-layout trajectory: a CTA per 32 time points,
+// lane = time point (coalesced rows of Xc), the 8 warps split the kc rows into contiguous ranges whose partial
+// sums are added in warp order (fixed order). One thread per time point over all kc rows was latency-bound
+// (76 us per checkpoint at kc = 544).
+__global__ void __launch_bounds__(256) large_project_cols_kernel(const double* Xc, int ldx, int kc, const double* P,
+                                                                  int kstride, int n_out, const double* beta0,
+                                                                  double* coeff, int ndl_stride, int dl, double* hlast,
+                                                                  int64_t n_steps) {
+    __shared__ double part[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t j = blockIdx.x * 32LL + lane;
+    const bool act = j <= n_steps;
+    const int per = (kc + 7) / 8, l0 = w * per, l1 = min(kc, l0 + per);
     const double b0 = *beta0;
     for (int r = 0; r < n_out; ++r) {
         const double* Pr = P + (int64_t)r * kstride;
         double s = 0.0;
-        for (int l = 0; l < kc; ++l) s = fma(Pr[l], Xc[(int64_t)l * ldx + j], s);
-        coeff[(j * n_out + r) * ndl_stride + dl] = b0 * s;
+        if (act)
+            for (int l = l0; l < l1; ++l) s = fma(Pr[l], Xc[(int64_t)l * ldx + j], s);
+        part[w][lane] = s;
+        __syncthreads();
+        if (w == 0 && act) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t += part[q][lane];
+            coeff[(j * n_out + r) * ndl_stride + dl] = b0 * t;
+        }
+        __syncthreads();
     }
-    hlast[j] = Xc[(int64_t)(kc - 1) * ldx + j];
+    if (w == 0 && act) hlast[j] = Xc[(int64_t)(kc - 1) * ldx + j];
 }
 
 __global__ void large_e1_col_kernel(double* Xc, int ldx, int kp) {
@@ -584,7 +601,7 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
                 std::swap(Y, Z);
             }
         }
-        large_project_cols_kernel<<<(unsigned)((np1 + 127) / 128), 128, 0, st>>>(
+        large_project_cols_kernel<<<(unsigned)((np1 + 31) / 32), 256, 0, st>>>(
             Xc, ldx, kc, h->d_P + (size_t)dl * h->n_out * h->k, h->k, h->n_out, h->d_beta0 + dl, h->d_coeff_loc,
             ndl_stride, dl, hl, h->n_steps);
         KR_CUDA(cudaGetLastError());
