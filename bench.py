@@ -359,13 +359,22 @@ def main():
     from paper_1804_01583_b200 import KrComm, KrylovReach, torch_broadcast_id
 
     world, rank, local = dist_env()
+    # KR_BENCH_SHARED_GPU=1 (diagnostics of this script's multi-rank plumbing on a one-GPU box): every rank on GPU 0,
+    # gloo for torch.distributed and the library's host transport (NCCL needs one GPU per rank). Not a measurement.
+    shared = world > 1 and os.environ.get("KR_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        comm = KrComm(rank, world, local, torch_broadcast_id)
+        if shared:
+            dist.init_process_group("gloo")
+            comm = KrComm.host(rank, world, local)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            comm = KrComm(rank, world, local, torch_broadcast_id)
     p = W.CONFIGS[args.config]()
     stream = torch.cuda.current_stream(dev)
     kw = dict(device=local, stream=stream.cuda_stream, comm=comm, part="zslab" if world > 1 else None)
@@ -390,7 +399,7 @@ def main():
 
     def max_over_ranks(x):
         if world > 1:
-            tt = torch.tensor([x], device=dev)
+            tt = torch.tensor([x], device="cpu" if shared else dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             return float(tt.item())
         return x
@@ -471,11 +480,16 @@ def main():
         "e2e": e2e,
         "gpu_launches": tm["launches"],
         "clocks": tm["clocks"],
-        "halo_transport": ("peer-memory stores from the step kernel (NVLink, CUDA IPC)" if p2p_on else
-                           ("NCCL send/recv" if world > 1 else "none (one rank)")),
+        "halo_transport": ("none (one rank)" if world == 1 else
+                           "none (direction sharding: one gather at the end)" if kw.get("part") == "dirs" else
+                           "peer-memory stores from the step kernel (NVLink, CUDA IPC)" if p2p_on else
+                           "host all-gather of the boundary planes" if shared else "NCCL send/recv"),
         "iter_ms_mean": float(np.mean(tm["iter_ms"])),
         "verdict": {"found": tm["cb"]["found"], "step": tm["cb"]["step"]},
     }
+    if shared:
+        line["note"] = ("KR_BENCH_SHARED_GPU diagnostic run: the ranks share GPU 0 through the host transport (gloo); "
+                        "checks the multi-rank plumbing, not a scaling measurement")
     if dense is not None:
         line["roofline_dense"] = dense["roofline"]
         line["dense"] = dense

@@ -228,6 +228,26 @@ def test_config5_full_size_oracle_golden():
     assert np.all(coeff[:, 0, 0] == 0.0)  # the BASELINE center row: exactly 0 at k = 30
 
 
+@pytest.mark.parametrize("P", [8])
+def test_config5_zslabs_oracle_golden(P):
+    """north_star's target configuration: the 10^9-state system decomposed into the z-slabs of 8 GPUs (125 planes
+    each, halo planes stored by the step kernel into the neighbouring slab — the peer-memory code path), emulated on
+    this GPU (virtual_slabs: the slabs run one after the other): every coefficient against the oracle's full run
+    (tests/golden), verdict / step identical."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "C5_heat1000_oracle.json")))
+    p = W.config5()
+    thresholds = [(int(r), int(s), float(t)) for (r, s, t) in g["thresholds"]]
+    from paper_1804_01583_b200 import KrylovReach
+    with KrylovReach(p, virtual_slabs=P, part="zslab") as h:
+        coeff, stats = h.project()
+        cb = h.check_box(thresholds)
+    assert_coeff(coeff, np.array(g["coeff"])[:, :, None], f"C5 on {P} z-slabs vs oracle golden")
+    assert stats[0]["k_eff"] == g["k_eff"]
+    assert cb["found"] and cb["step"] == g["verdict"]["step"] and cb["row"] == g["verdict"]["row"]
+
+
 def test_config5_first_step_closed_form():
     """alpha_1 = -6c/b, beta_1 from cell counting at 10^9 with k=2."""
     p = W.config5(n_steps=1)
