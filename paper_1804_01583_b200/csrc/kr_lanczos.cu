@@ -147,12 +147,13 @@ struct Geo {
 // The forward ring (top row: warp 0, one x-pair per lane; right column: warp 1, one cell per lane) is computed
 // beside the tile, as in v1.
 // ================================================================================================
-template <int TX, int TY>
+template <int TX, int TY, int R = 2>
 struct Geo2 {
     static_assert(TX == 64, "v2 maps one x-pair per lane: TX = 64");
-    static constexpr int NT = 16 * TY;  // one warp per row pair
-    static constexpr int CW = TX + 4, CH = TY + 3;  // u_i box: x0-2 .. x0+TX+1, y0-1 .. y0+TY+1 (as v1)
-    static constexpr int PW = TX + 2, PH = TY + 1;  // u_{i-1} box: x0 .. x0+TX+1, y0 .. y0+TY (as v1)
+    static_assert(TY % R == 0 && TY / R >= 3, "the ring needs three warps");
+    static constexpr int NT = 32 * TY / R;  // one warp per R rows
+    static constexpr int CW = TX + 4, CH = TY + 3;  // u_i box: x0-2 .. x0+TX+1, y0-1 .. y0+TY+1
+    static constexpr int PW = TX + 2, PH = TY + 1;  // u_{i-1} box: x0 .. x0+TX+1, y0 .. y0+TY
     static constexpr int WW = TX + 2, WH = TY + 1;  // w plane on the tile + forward ring, rows of 16-byte multiples
     static constexpr int CBYTES = CW * CH * 8, PBYTES = PW * PH * 8;
     static constexpr int POFF = ((CBYTES + 127) / 128) * 128;
@@ -174,6 +175,8 @@ struct Acc2 {
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
 
+// R rows per thread: lane l owns the x-pair (x0 + 2l, +1) on the rows y0 + R w .. y0 + R w + R - 1 of warp w
+// (cells c = 2 r + column). The in-pair x neighbours and the y neighbours inside the thread's rows are registers.
 // BCM: 0 = Dirichlet everywhere; 1 = general faces, tile without x/y face cells (full, x0 > 0, y0 > 0): only the
 // per-plane z-face terms; 2 = general faces, per-cell diagonal corrections.
 // FACE: the tile touches an x / y face of the grid (x0 = 0, y0 = 0, or a ragged tile): the ghost-edge / face terms
@@ -181,12 +184,12 @@ __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpre
 // bottom ghost edge of global plane 0 in the peeled first plane, the top one through the z difference of the last
 // plane, dz = zf w_q - zg w_{q-1} (zf = 0 on the ghost above the grid, zg^2 cz = gq[5]: Dirichlet 1, insulated 0).
 // Box output rows are summed per warp (shuffle tree, fixed order) into wbox.
-template <int TX, int TY, int S, bool INIT, bool FULL, int BCM, bool HALO, bool FACE>
+template <int TX, int TY, int R, int S, bool INIT, bool FULL, int BCM, bool HALO, bool FACE>
 __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
                                           unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
                                           int zc0, int zc1, bool cta_box, Acc2& A, double (*wbox)[KR_MAX_BOX]) {
-    using G = Geo2<TX, TY>;
-    constexpr int CW = G::CW, PW = G::PW, WW = G::WW;
+    using G = Geo2<TX, TY, R>;
+    constexpr int CW = G::CW, PW = G::PW, WW = G::WW, NC = 2 * R;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int pfirst = zc0 - 1, plast = zc1 + 1;
     const bool has_prev = a.has_prev != 0;
@@ -214,34 +217,31 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     const double diag = 2.0 * (a.cx + a.cy + a.cz);
     const double scx = sa * a.cx, scy = sa * a.cy, scz = sa * a.cz;
 
-    const int rx = 2 * lane, ry = 2 * wid;  // tile coordinates of the thread's first cell
+    const int rx = 2 * lane, ry = R * wid;  // tile coordinates of the thread's first cell
     const int gx = x0 + rx, gy = y0 + ry;
     const int cb = (ry + 1) * CW + rx + 2, pb = ry * PW + rx, wb = ry * WW + rx;
-    // cells c = 2 * row + column: (gx, gy), (gx + 1, gy), (gx, gy + 1), (gx + 1, gy + 1)
-    bool in[4];
-    in[0] = FULL || (gx < a.mx && gy < a.my);
-    in[1] = FULL || (gx + 1 < a.mx && gy < a.my);
-    in[2] = FULL || (gx < a.mx && gy + 1 < a.my);
-    in[3] = FULL || (gx + 1 < a.mx && gy + 1 < a.my);
+    bool in[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) in[c] = FULL || (gx + (c & 1) < a.mx && gy + (c >> 1) < a.my);
     // face cells: low faces in any tile at x0 = 0 / y0 = 0; high faces only in ragged (not FULL) tiles
-    const bool xlo = x0 == 0 && lane == 0;  // cells 0, 2
+    const bool xlo = x0 == 0 && lane == 0;  // cells 2 r
     const bool ylo = y0 == 0 && wid == 0;   // cells 0, 1
     const bool xhi0 = !FULL && gx == a.mx - 1, xhi1 = !FULL && gx + 1 == a.mx - 1;
-    const bool yhi0 = !FULL && gy == a.my - 1, yhi1 = !FULL && gy + 1 == a.my - 1;
-    double exy[4] = {0.0, 0.0, 0.0, 0.0};  // per-cell x/y diagonal corrections (BCM 2)
-    if (BCM == 2) {
-        const double ex0 = (gx == 0 ? a.ecor[0] : 0.0) + (gx == a.mx - 1 ? a.ecor[1] : 0.0);
-        const double ex1 = (gx + 1 == a.mx - 1 ? a.ecor[1] : 0.0);
-        const double ey0 = (gy == 0 ? a.ecor[2] : 0.0) + (gy == a.my - 1 ? a.ecor[3] : 0.0);
-        const double ey1 = (gy + 1 == a.my - 1 ? a.ecor[3] : 0.0);
-        exy[0] = ex0 + ey0;
-        exy[1] = ex1 + ey0;
-        exy[2] = ex0 + ey1;
-        exy[3] = ex1 + ey1;
+    double exy[NC];  // per-cell x/y diagonal corrections (BCM 2)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        exy[c] = 0.0;
+        if (BCM == 2) {
+            const int cx_ = gx + (c & 1), cy_ = gy + (c >> 1);
+            exy[c] = (cx_ == 0 ? a.ecor[0] : 0.0) + (cx_ == a.mx - 1 ? a.ecor[1] : 0.0) + (cy_ == 0 ? a.ecor[2] : 0.0) +
+                     (cy_ == a.my - 1 ? a.ecor[3] : 0.0);
+        }
     }
-    uint32_t bm[4] = {0u, 0u, 0u, 0u};
+    uint32_t bm[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) bm[c] = 0u;
     if (cta_box)
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < NC; ++c) {
             const int cx_ = gx + (c & 1), cy_ = gy + (c >> 1);
             for (int r = 0; r < a.nbox; ++r)
                 if (!((a.all_mask >> r) & 1u) && cx_ >= a.box[r].lo[0] && cx_ < a.box[r].hi[0] && cy_ >= a.box[r].lo[1] &&
@@ -267,25 +267,27 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                   (gry == a.my - 1 ? a.ecor[3] : 0.0);
     }
     double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)gy * a.pitch + gx;
-    const bool st0 = FULL || (gx < a.mx && gy < a.my), st1 = FULL || (gx < a.mx && gy + 1 < a.my);
 
-    // u of three consecutive planes (4 cells + ring) in three register sets that take turns as u_{q-1}, u_q,
+    // u of three consecutive planes (the thread's cells) in three register sets that take turns as u_{q-1}, u_q,
     // u_{q+1}; w of two consecutive planes in two sets (w_{q-1}, w_q): the interior loop is unrolled by six
-    double U0[4], U1[4], U2[4], WA[4] = {0.0, 0.0, 0.0, 0.0}, WB[4] = {0.0, 0.0, 0.0, 0.0};
+    double U0[NC], U1[NC], U2[NC], WA[NC], WB[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) WA[c] = WB[c] = 0.0;
     double R0 = 0.0, R1 = 0.0, R2 = 0.0;
     mbar_wait(&bar[0], 0);
     mbar_wait(&bar[1 % S], 0);
     {
         const double* C0 = reinterpret_cast<const double*>(smem);
         const double* C1 = reinterpret_cast<const double*>(smem + (1 % S) * G::STAGE);
-        double2 t = ld2(C0 + cb);
-        U0[0] = t.x; U0[1] = t.y;
-        t = ld2(C0 + cb + CW);
-        U0[2] = t.x; U0[3] = t.y;
-        t = ld2(C1 + cb);
-        U1[0] = t.x; U1[1] = t.y;
-        t = ld2(C1 + cb + CW);
-        U1[2] = t.x; U1[3] = t.y;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double2 t = ld2(C0 + cb + r * CW);
+            U0[2 * r] = t.x;
+            U0[2 * r + 1] = t.y;
+            t = ld2(C1 + cb + r * CW);
+            U1[2 * r] = t.x;
+            U1[2 * r + 1] = t.y;
+        }
         if (ring) {
             R0 = C0[rcb];
             R1 = C1[rcb];
@@ -294,19 +296,22 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     int sq = 1 % S, sn = 2 % S;
     uint32_t ph = (2 / S) & 1;
     // one plane q: w_q on the tile (wc) and the ring (into the W buffer of q's parity), then the products of plane
-    // q - 1 (wp = w_{q-1}; its x+2 / row+2 neighbours from the W buffer written last iteration, its z+1 neighbour wc)
+    // q - 1 (wp = w_{q-1}; its x+2 / row+R neighbours from the W buffer written last iteration, its z+1 neighbour wc)
     const double zgtop = BCM ? sqrt(a.gq[5] / a.cz) : 1.0;  // the top face's edge coefficient gq[5] = zg^2 cz
-    auto plane = [&](const double (&up)[4], const double (&uc)[4], double (&un)[4], const double rp, const double rc,
-                     double& rn, const double (&wp)[4], double (&wc)[4], const int q, auto first) {
+    auto plane = [&](const double (&up)[2 * R], const double (&uc)[2 * R], double (&un)[2 * R], const double rp,
+                     const double rc, double& rn, const double (&wp)[2 * R], double (&wc)[2 * R], const int q,
+                     auto first) {
         constexpr bool FIRST = decltype(first)::value;  // q == zc0: w only, no products
         mbar_wait(&bar[sn], ph);
         const unsigned char* stq = smem + sq * G::STAGE;
         const double* Cq = reinterpret_cast<const double*>(stq);
         const double* Pq = reinterpret_cast<const double*>(stq + G::POFF);
         const double* Cn = reinterpret_cast<const double*>(smem + sn * G::STAGE);
-        {
-            const double2 t0 = ld2(Cn + cb), t1 = ld2(Cn + cb + CW);
-            un[0] = t0.x; un[1] = t0.y; un[2] = t1.x; un[3] = t1.y;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double2 t = ld2(Cn + cb + r * CW);
+            un[2 * r] = t.x;
+            un[2 * r + 1] = t.y;
         }
         const int gzq = a.zoff + q;
         double* Wq = (q & 1) ? Wb1 : Wb0;
@@ -314,35 +319,50 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
         const double cf = fma(sa, dgz, sb);  // coefficient of u_i in w (this plane, no x/y face)
         if (INIT) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) wc[c] = uc[c];
+            for (int c = 0; c < NC; ++c) wc[c] = uc[c];
         } else {
-            const double xm0 = Cq[cb - 1], xp0 = Cq[cb + 2], xm1 = Cq[cb + CW - 1], xp1 = Cq[cb + CW + 2];
-            const double2 ym = ld2(Cq + cb - CW), yp = ld2(Cq + cb + 2 * CW);
-            double cfc[4] = {cf, cf, cf, cf};
-            if (BCM == 2) {
+            const double2 ym = ld2(Cq + cb - CW), yp = ld2(Cq + cb + R * CW);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) cfc[c] = fma(sa, dgz - exy[c], sb);
+            for (int r = 0; r < R; ++r) {
+                const double xm = Cq[cb + r * CW - 1], xp = Cq[cb + r * CW + 2];
+                double ydn0, ydn1, yup0, yup1;
+                if (r == 0) {
+                    ydn0 = ym.x;
+                    ydn1 = ym.y;
+                } else {
+                    ydn0 = uc[2 * r - 2];
+                    ydn1 = uc[2 * r - 1];
+                }
+                if (r == R - 1) {
+                    yup0 = yp.x;
+                    yup1 = yp.y;
+                } else {
+                    yup0 = uc[2 * r + 2];
+                    yup1 = uc[2 * r + 3];
+                }
+                const int c0 = 2 * r, c1 = 2 * r + 1;
+                const double cf0 = BCM == 2 ? fma(sa, dgz - exy[c0], sb) : cf;
+                const double cf1 = BCM == 2 ? fma(sa, dgz - exy[c1], sb) : cf;
+                // w = s_i (off-diagonal part of A u_i) - (s_i diag + alpha_i s_i) u_i - beta_{i-1} s_{i-1} u_{i-1}
+                wc[c0] = fma(scx, xm + uc[c1], fma(scy, ydn0 + yup0, fma(scz, up[c0] + un[c0], -cf0 * uc[c0])));
+                wc[c1] = fma(scx, uc[c0] + xp, fma(scy, ydn1 + yup1, fma(scz, up[c1] + un[c1], -cf1 * uc[c1])));
             }
-            // w = s_i (off-diagonal part of A u_i) - (s_i diag + alpha_i s_i) u_i - beta_{i-1} s_{i-1} u_{i-1}
-            wc[0] = fma(scx, xm0 + uc[1], fma(scy, ym.x + uc[2], fma(scz, up[0] + un[0], -cfc[0] * uc[0])));
-            wc[1] = fma(scx, uc[0] + xp0, fma(scy, ym.y + uc[3], fma(scz, up[1] + un[1], -cfc[1] * uc[1])));
-            wc[2] = fma(scx, xm1 + uc[3], fma(scy, uc[0] + yp.x, fma(scz, up[2] + un[2], -cfc[2] * uc[2])));
-            wc[3] = fma(scx, uc[2] + xp1, fma(scy, uc[1] + yp.y, fma(scz, up[3] + un[3], -cfc[3] * uc[3])));
             if (has_prev) {
-                const double2 p0 = ld2(Pq + pb), p1 = ld2(Pq + pb + PW);
-                wc[0] = fma(-sp, p0.x, wc[0]);
-                wc[1] = fma(-sp, p0.y, wc[1]);
-                wc[2] = fma(-sp, p1.x, wc[2]);
-                wc[3] = fma(-sp, p1.y, wc[3]);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double2 pv = ld2(Pq + pb + r * PW);
+                    wc[2 * r] = fma(-sp, pv.x, wc[2 * r]);
+                    wc[2 * r + 1] = fma(-sp, pv.y, wc[2 * r + 1]);
+                }
             }
         }
         if (!FULL) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < NC; ++c)
                 if (!in[c]) wc[c] = 0.0;
         }
-        st2(Wq + wb, wc[0], wc[1]);
-        st2(Wq + wb + WW, wc[2], wc[3]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) st2(Wq + wb + r * WW, wc[2 * r], wc[2 * r + 1]);
         if (ring) {
             rn = Cn[rcb];
             double r0 = rc;
@@ -355,67 +375,102 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
             if (!FULL && !rin) r0 = 0.0;
             Wq[rwb] = r0;
         }
-        if (!FACE && FIRST && a.zoff + zc0 == 0)  // ghost edge below global plane 0, coefficient gq[4]
-            A.face = fma(a.gq[4], fma(wc[0], wc[0], fma(wc[1], wc[1], fma(wc[2], wc[2], wc[3] * wc[3]))), A.face);
-        if (!FIRST && (!FACE || q > zc0)) {  // products of plane q - 1 (its x+2 / row+2 neighbours: last iteration)
+        if (!FACE && FIRST && a.zoff + zc0 == 0) {  // ghost edge below global plane 0, coefficient gq[4]
+            double s2 = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) s2 = fma(wc[c], wc[c], s2);
+            A.face = fma(a.gq[4], s2, A.face);
+        }
+        if (!FIRST && (!FACE || q > zc0)) {  // products of plane q - 1 (its x+2 / row+R neighbours: last iteration)
             const double* Wp = ((q & 1) ? Wb0 : Wb1) + wb;
             const int gzp = gzq - 1;
-            const double xr0 = Wp[2], xr1 = Wp[WW + 2];
-            const double2 yu = ld2(Wp + 2 * WW);
-            double dx[4] = {wp[1] - wp[0], xr0 - wp[1], wp[3] - wp[2], xr1 - wp[3]};
-            const double dy[4] = {wp[2] - wp[0], wp[3] - wp[1], yu.x - wp[2], yu.y - wp[3]};
-            if (!FULL) {  // high x / y faces: the edge to the (zero) ghost takes the face coefficient
-                if (xhi0) { dx[0] = 0.0; dx[2] = 0.0; A.face = fma(a.gq[1], fma(wp[0], wp[0], wp[2] * wp[2]), A.face); }
-                if (xhi1) { dx[1] = 0.0; dx[3] = 0.0; A.face = fma(a.gq[1], fma(wp[1], wp[1], wp[3] * wp[3]), A.face); }
+            const double2 yu = ld2(Wp + R * WW);
+            double dx[NC], dy[NC];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double xr = Wp[r * WW + 2];
+                dx[2 * r] = wp[2 * r + 1] - wp[2 * r];
+                dx[2 * r + 1] = xr - wp[2 * r + 1];
+                if (r == R - 1) {
+                    dy[2 * r] = yu.x - wp[2 * r];
+                    dy[2 * r + 1] = yu.y - wp[2 * r + 1];
+                } else {
+                    dy[2 * r] = wp[2 * r + 2] - wp[2 * r];
+                    dy[2 * r + 1] = wp[2 * r + 3] - wp[2 * r + 1];
+                }
             }
-            double ddy[4] = {dy[0], dy[1], dy[2], dy[3]};
-            if (!FULL) {
-                if (yhi0) { ddy[0] = 0.0; ddy[1] = 0.0; A.face = fma(a.gq[3], fma(wp[0], wp[0], wp[1] * wp[1]), A.face); }
-                if (yhi1) { ddy[2] = 0.0; ddy[3] = 0.0; A.face = fma(a.gq[3], fma(wp[2], wp[2], wp[3] * wp[3]), A.face); }
+            if (!FULL) {  // high x / y faces: the edge to the (zero) ghost takes the face coefficient
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (xhi0) {
+                        dx[2 * r] = 0.0;
+                        A.face = fma(a.gq[1], wp[2 * r] * wp[2 * r], A.face);
+                    }
+                    if (xhi1) {
+                        dx[2 * r + 1] = 0.0;
+                        A.face = fma(a.gq[1], wp[2 * r + 1] * wp[2 * r + 1], A.face);
+                    }
+                    if (gy + r == a.my - 1) {
+                        dy[2 * r] = 0.0;
+                        dy[2 * r + 1] = 0.0;
+                        A.face = fma(a.gq[3], fma(wp[2 * r], wp[2 * r], wp[2 * r + 1] * wp[2 * r + 1]), A.face);
+                    }
+                }
             }
             if (FACE) {  // ghost edges of the low x / y faces
-                if (xlo) A.face = fma(a.gq[0], fma(wp[0], wp[0], wp[2] * wp[2]), A.face);
+                if (xlo) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) A.face = fma(a.gq[0], wp[2 * r] * wp[2 * r], A.face);
+                }
                 if (ylo) A.face = fma(a.gq[2], fma(wp[0], wp[0], wp[1] * wp[1]), A.face);
             }
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < NC; ++c) {
                 A.ww = fma(wp[c], wp[c], A.ww);
                 A.sum += wp[c];
                 A.dx = fma(dx[c], dx[c], A.dx);
-                A.dy = fma(ddy[c], ddy[c], A.dy);
+                A.dy = fma(dy[c], dy[c], A.dy);
             }
             if (FACE && gzp == a.mz - 1) {  // the z+1 neighbour is the zero ghost above the grid: coefficient gq[5]
-                A.face = fma(a.gq[5], fma(wp[0], wp[0], fma(wp[1], wp[1], fma(wp[2], wp[2], wp[3] * wp[3]))), A.face);
+                double s2 = 0.0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) s2 = fma(wp[c], wp[c], s2);
+                A.face = fma(a.gq[5], s2, A.face);
             } else if (!FACE) {
                 const bool top = gzp == a.mz - 1;  // uniform: the ghost above the grid (w there is not a state value)
                 const double zf = top ? 0.0 : 1.0;
                 if (BCM) {
                     const double zg = top ? zgtop : 1.0;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < NC; ++c) {
                         const double dz = fma(wc[c], zf, -zg * wp[c]);
                         A.dz = fma(dz, dz, A.dz);
                     }
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < NC; ++c) {
                         const double dz = fma(wc[c], zf, -wp[c]);  // exactly wc - wp, or -wp above the grid
                         A.dz = fma(dz, dz, A.dz);
                     }
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < NC; ++c) {
                     const double dz = wc[c] - wp[c];
                     A.dz = fma(dz, dz, A.dz);
                 }
             }
-            if (FACE && gzp == 0)
-                A.face = fma(a.gq[4], fma(wp[0], wp[0], fma(wp[1], wp[1], fma(wp[2], wp[2], wp[3] * wp[3]))), A.face);
+            if (FACE && gzp == 0) {
+                double s2 = 0.0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) s2 = fma(wp[c], wp[c], s2);
+                A.face = fma(a.gq[4], s2, A.face);
+            }
             const bool wr = !INIT && a.write_out;
             if (wr) {
-                if (st0) st2(optr, wp[0], wp[1]);
-                if (st1) st2(optr + a.pitch, wp[2], wp[3]);
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (FULL || (gx < a.mx && gy + r < a.my)) st2(optr + r * a.pitch, wp[2 * r], wp[2 * r + 1]);
             }
             if (cta_box) {  // box output rows meeting this tile and plane (uniform, rare)
                 uint32_t zmask = 0;
@@ -425,7 +480,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                     if (!((zmask >> r) & 1u)) continue;
                     double v = 0.0;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c < NC; ++c)
                         if ((bm[c] >> r) & 1u) v += wp[c];
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -437,15 +492,12 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
             const int qq = q - 1;
             if (HALO && wr && ((a.rlo && qq < 2) || (a.rhi && qq == a.nz - 1))) {
                 const int64_t off = (optr - a.out) - (int64_t)(qq + 1) * a.plane;  // in-plane offset of cell 0
-                if (a.rlo && qq < 2) {
-                    double* d = a.rlo + a.rlo_plane0 + (int64_t)qq * a.plane + off;
-                    if (st0) st2(d, wp[0], wp[1]);
-                    if (st1) st2(d + a.pitch, wp[2], wp[3]);
-                }
-                if (a.rhi && qq == a.nz - 1) {
-                    double* d = a.rhi + off;
-                    if (st0) st2(d, wp[0], wp[1]);
-                    if (st1) st2(d + a.pitch, wp[2], wp[3]);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (!(FULL || (gx < a.mx && gy + r < a.my))) continue;
+                    if (a.rlo && qq < 2)
+                        st2(a.rlo + a.rlo_plane0 + (int64_t)qq * a.plane + off + r * a.pitch, wp[2 * r], wp[2 * r + 1]);
+                    if (a.rhi && qq == a.nz - 1) st2(a.rhi + off + r * a.pitch, wp[2 * r], wp[2 * r + 1]);
                 }
             }
             optr += a.plane;
@@ -485,7 +537,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
         for (int q = zc0; q <= zc1; ++q) {
             plane(U0, U1, U2, R0, R1, R2, WA, WB, q, F0{});
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < NC; ++c) {
                 U0[c] = U1[c];
                 U1[c] = U2[c];
                 WA[c] = WB[c];
@@ -496,10 +548,10 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     }
 }
 
-template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false>
-__global__ void __launch_bounds__(Geo2<TX, TY>::NT, (TY >= 32) ? 1 : 2)
+template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false, int R = 2>
+__global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 : 2)
     lz_step_kernel2(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
-    using G = Geo2<TX, TY>;
+    using G = Geo2<TX, TY, R>;
     if (a.sc->done) return;  // breakdown happened earlier: uniform early exit
 
     extern __shared__ __align__(128) unsigned char smem[];
@@ -531,7 +583,8 @@ __global__ void __launch_bounds__(Geo2<TX, TY>::NT, (TY >= 32) ? 1 : 2)
                 a.box[r].hi[2] > a.zoff + zc0)
                 cta_box = true;
 #define KR_M2(FULL_, BCM_, FACE_) \
-    lz_march2<TX, TY, S, INIT, FULL_, BCM_, HALO, FACE_>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, wbox)
+    lz_march2<TX, TY, R, S, INIT, FULL_, BCM_, HALO, FACE_>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, \
+                                                            wbox)
         if (x0 + TX < a.mx && y0 + TY < a.my) {
             if (x0 > 0 && y0 > 0)
                 KR_M2(true, BC ? 1 : 0, false);
@@ -941,7 +994,6 @@ struct Stages {
 }  // namespace
 
 size_t kr_lz_step_smem(int TX, int TY) {
-    if (TX == 64 && TY == 32) return step2_smem_bytes<64, 32, Stages<64, 32>::S>();
     if (TX == 64 && TY == 16) return step2_smem_bytes<64, 16, Stages<64, 16>::S>();
     if (TX == 64 && TY == 8) return step2_smem_bytes<64, 8, Stages<64, 8>::S>();
     return 0;
@@ -1023,34 +1075,33 @@ void kr_lz_setup_compact(kr_handle* h) {
     }
 }
 
-template <int TX, int TY, bool INIT, bool BC, bool HALO = false>
+template <int TX, int TY, bool INIT, bool BC, bool HALO = false, int R = 2>
 static void set_smem_attr2() {
-    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel2<TX, TY, Stages<TX, TY>::S, INIT, BC, HALO>,
+    KR_CUDA(cudaFuncSetAttribute(lz_step_kernel2<TX, TY, Stages<TX, TY>::S, INIT, BC, HALO, R>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)step2_smem_bytes<TX, TY, Stages<TX, TY>::S>()));
 }
 
-template <int TX, int TY>
+template <int TX, int TY, int R>
 static int occupancy_t() {
-    set_smem_attr2<TX, TY, false, false>();
-    set_smem_attr2<TX, TY, true, false>();
-    set_smem_attr2<TX, TY, false, true>();
-    set_smem_attr2<TX, TY, true, true>();
-    set_smem_attr2<TX, TY, false, false, true>();
-    set_smem_attr2<TX, TY, false, true, true>();
+    set_smem_attr2<TX, TY, false, false, false, R>();
+    set_smem_attr2<TX, TY, true, false, false, R>();
+    set_smem_attr2<TX, TY, false, true, false, R>();
+    set_smem_attr2<TX, TY, true, true, false, R>();
+    set_smem_attr2<TX, TY, false, false, true, R>();
+    set_smem_attr2<TX, TY, false, true, true, R>();
     int n1 = 0, n2 = 0;
     const size_t sm2 = step2_smem_bytes<TX, TY, Stages<TX, TY>::S>();
-    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, false>,
-                                                          Geo2<TX, TY>::NT, sm2));
-    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n2, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, true>,
-                                                          Geo2<TX, TY>::NT, sm2));
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &n1, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, false, false, R>, Geo2<TX, TY, R>::NT, sm2));
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &n2, lz_step_kernel2<TX, TY, Stages<TX, TY>::S, false, true, false, R>, Geo2<TX, TY, R>::NT, sm2));
     return n1 < n2 ? n1 : n2;
 }
 
 int kr_lz_occupancy(int TX, int TY) {
-    if (TX == 64 && TY == 32) return occupancy_t<64, 32>();
-    if (TX == 64 && TY == 16) return occupancy_t<64, 16>();
-    if (TX == 64 && TY == 8) return occupancy_t<64, 8>();
+    if (TX == 64 && TY == 16) return occupancy_t<64, 16, 2>();
+    if (TX == 64 && TY == 8) return occupancy_t<64, 8, 2>();
     return 1;
 }
 
@@ -1157,6 +1208,27 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     return a;
 }
 
+template <int TX, int TY, int S, int R>
+static void launch_step2(kr_handle* h, dim3 grid, size_t smem2, const CUtensorMap& tc, const CUtensorMap& tp,
+                         const StepArgs& a, bool init, bool halo) {
+    constexpr int NT2 = Geo2<TX, TY, R>::NT;
+    if (h->gen_bc) {
+        if (init)
+            lz_step_kernel2<TX, TY, S, true, true, false, R><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+        else if (halo)
+            lz_step_kernel2<TX, TY, S, false, true, true, R><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+        else
+            lz_step_kernel2<TX, TY, S, false, true, false, R><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+    } else {
+        if (init)
+            lz_step_kernel2<TX, TY, S, true, false, false, R><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+        else if (halo)
+            lz_step_kernel2<TX, TY, S, false, false, true, R><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+        else
+            lz_step_kernel2<TX, TY, S, false, false, false, R><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
+    }
+}
+
 template <int TX, int TY>
 static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int nxt, int step, bool init,
                           bool write, bool fillinit, int cmode) {
@@ -1172,22 +1244,9 @@ static void step_launch_t(kr_handle* h, Slab& sl, int dl, int cur, int prev, int
         constexpr int S = Stages<TX, TY>::S;
         const bool halo = a.rlo || a.rhi;  // this slab writes halo planes into a neighbour's buffer
         const size_t smem2 = step2_smem_bytes<TX, TY, S>();
-        constexpr int NT2 = Geo2<TX, TY>::NT;
-        if (h->gen_bc) {
-            if (init)
-                lz_step_kernel2<TX, TY, S, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-            else if (halo)
-                lz_step_kernel2<TX, TY, S, false, true, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-            else
-                lz_step_kernel2<TX, TY, S, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-        } else {
-            if (init)
-                lz_step_kernel2<TX, TY, S, true, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-            else if (halo)
-                lz_step_kernel2<TX, TY, S, false, false, true><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-            else
-                lz_step_kernel2<TX, TY, S, false, false><<<grid, NT2, smem2, h->stream>>>(tc, tp, a);
-        }
+        // two rows per thread (2 x 2 cells); four rows (2 x 4 cells, 128 threads) measured slower: C5 3.79-3.84 vs
+        // 3.73 ms per step, C4 0.267 vs 0.251 ms (fewer warps to hide the shared-memory and TMA latencies)
+        launch_step2<TX, TY, S, 2>(h, grid, smem2, tc, tp, a, init, halo);
     }
     KR_CUDA(cudaGetLastError());
     h->launches++;
@@ -1217,8 +1276,6 @@ static void step_launch(kr_handle* h, Slab& sl, int dl, int cur, int prev, int n
                         bool fillinit = false, int cmode = 0) {
     if (h->TX == 64 && h->TY == 16)
         step_launch_t<64, 16>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
-    else if (h->TX == 64 && h->TY == 32)
-        step_launch_t<64, 32>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else if (h->TX == 64 && h->TY == 8)
         step_launch_t<64, 8>(h, sl, dl, cur, prev, nxt, step, init, write, fillinit, cmode);
     else
