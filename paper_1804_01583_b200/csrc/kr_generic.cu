@@ -162,38 +162,42 @@ __global__ void spmm_csr_kernel(const int64_t* __restrict__ rp, const int32_t* _
 }
 
 // Block SpMM (Alg. 1 line 3, for every direction at once): Y[d] = A' X[d] with each CSR
-// row streamed ONCE per Krylov step for all local directions. A warp per row, lane = direction (a further pass per
-// 32 directions): the lanes load the row's entries 32 at a time (one coalesced request for val and for ci) and
-// broadcast them by shuffles; each lane gathers x_d[col] from its own direction's vector. Entries are summed in
-// row order as in spmm_csr_kernel, so the results are those of one thread per (row, direction), bit for bit.
-// The lifted row n of A' is zero; rows longer than KR_LONG_ROW are left to spmm_long_rows_kernel.
+// row streamed ONCE per Krylov step for all local directions. A group of G lanes per row (G = the directions rounded
+// up to a power of two, at most 32: 32 rows per warp for one direction, one row per warp for 17-32), lane = direction
+// (a further pass per G directions): the group loads the row's entries G at a time (coalesced) and broadcasts them by
+// shuffles; each lane gathers x_d[col] from its own direction's vector. Entries are summed in row order as in
+// spmm_csr_kernel, so the results are those of one thread per (row, direction), bit for bit. The lifted row n of A'
+// is zero; rows longer than KR_LONG_ROW are left to spmm_long_rows_kernel.
 __global__ void __launch_bounds__(256) spmm_block_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                          const double* __restrict__ val, const double* __restrict__ b,
                                                          int64_t n, int64_t N, const double* __restrict__ X,
                                                          int64_t xstride, double* __restrict__ Y, int64_t ystride,
-                                                         int ndl, const int32_t* __restrict__ done) {
+                                                         int ndl, const int32_t* __restrict__ done, int G) {
     const int lane = threadIdx.x & 31;
+    const int rpw = 32 / G, g = lane % G, base = lane - g;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < N; r += nwarps) {
+    for (int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * rpw; r0 < N; r0 += nwarps * rpw) {
+        const int64_t r = r0 + lane / G;
         const int64_t e0 = r < n ? rp[r] : 0, e1 = r < n ? rp[r + 1] : 0;
-        if (e1 - e0 > KR_LONG_ROW) continue;
-        for (int d0 = 0; d0 < ndl; d0 += 32) {
-            const int d = d0 + lane;
-            const bool act = d < ndl && !done[d];
+        const bool shortrow = e1 - e0 <= KR_LONG_ROW;
+        const int len = (r < N && shortrow) ? (int)(e1 - e0) : 0;
+        const int maxlen = __reduce_max_sync(0xffffffffu, len);
+        for (int d0 = 0; d0 < ndl; d0 += G) {
+            const int d = d0 + g;
+            const bool act = r < N && shortrow && d < ndl && !done[d];
             const double* x = X + (int64_t)(act ? d : 0) * xstride;
             double s = 0.0;
-            for (int64_t eb = e0; eb < e1; eb += 32) {
-                const int cnt = (int)min((int64_t)32, e1 - eb);
+            for (int eb = 0; eb < maxlen; eb += G) {
                 double v = 0.0;
                 int c = 0;
-                if (lane < cnt) {
-                    v = val[eb + lane];
-                    c = ci[eb + lane];
+                if (eb + g < len) {
+                    v = val[e0 + eb + g];
+                    c = ci[e0 + eb + g];
                 }
-                for (int t = 0; t < cnt; ++t) {
-                    const double vt = __shfl_sync(0xffffffffu, v, t);
-                    const int ct = __shfl_sync(0xffffffffu, c, t);
-                    if (act) s = fma(vt, __ldg(&x[ct]), s);
+                for (int t = 0; t < G; ++t) {
+                    const double vt = __shfl_sync(0xffffffffu, v, base + t);
+                    const int ct = __shfl_sync(0xffffffffu, c, base + t);
+                    if (act && eb + t < len) s = fma(vt, __ldg(&x[ct]), s);
                 }
             }
             if (act) {
@@ -228,18 +232,23 @@ __global__ void spmm_long_rows_kernel(const int64_t* __restrict__ rp, const int3
     }
 }
 
-// Y[d] = A' X[d] for every local direction, one launch (+ the long rows): the block SpMM above; KR_SPMM_PER_DIR=1
-// keeps one thread per (row, direction) (A re-read per direction, from L2)
+// Y[d] = A' X[d] for every local direction, one launch (+ the long rows): the block SpMM above from 8 directions
+// (C2: 21); below, or with KR_SPMM_PER_DIR=1, one thread per (row, direction) — A re-read per direction from L2,
+// which for a few directions is cheaper than the shuffles (the transpose dynamics of C2, 3 simulations: 2.35 vs
+// 3.34 ms per bench step; C2 with 21 directions: 3.74-3.85 vs 3.86-3.95 ms)
 void kr_csr_spmm(kr_handle* h, const double* X, int64_t xstride, double* Y, int64_t ystride, int ndl) {
     const int64_t N = h->N;
-    if (getenv("KR_SPMM_PER_DIR")) {
+    if (ndl < 8 || getenv("KR_SPMM_PER_DIR")) {
         const int bx = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
         spmm_csr_kernel<<<dim3(bx, ndl), 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X, xstride, Y,
                                                               ystride, ndl, h->d_done);
     } else {
-        const int blocks = (int)std::min<int64_t>((N + 7) / 8, 148 * 16);
+        int G = 1;
+        while (G < ndl && G < 32) G <<= 1;  // lanes per row: the directions, up to a warp
+        const int64_t rows_per_block = 8 * (32 / G);
+        const int blocks = (int)std::min<int64_t>((N + rows_per_block - 1) / rows_per_block, 148 * 16);
         spmm_block_kernel<<<blocks, 256, 0, h->stream>>>(h->d_rp, h->d_ci, h->d_val, h->d_b, h->n, N, X, xstride, Y,
-                                                         ystride, ndl, h->d_done);
+                                                         ystride, ndl, h->d_done, G);
     }
     KR_CUDA(cudaGetLastError());
     h->launches++;
