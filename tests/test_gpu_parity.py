@@ -529,7 +529,7 @@ def test_stencil_switches_keep_parity(env, monkeypatch):
 
 def test_spmm_per_direction_equals_block(monkeypatch):
     """The block SpMM (each CSR row read once for all directions) sums every row in entry order, like one thread per
-    (row, direction): bitwise equal results (C2 recipe, 10 and 21 directions — the block form runs from 8 —, both
+    (row, direction): bitwise equal results (C2 recipe, 10 directions — the block form runs from 8 —, both
     Arnoldi routes)."""
     p = W.config2(n=3000, n_gen=9, n_steps=100, k=25)
     for cgs in ("0", "1"):
