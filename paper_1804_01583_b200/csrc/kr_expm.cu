@@ -150,65 +150,62 @@ __device__ double* pade13(const double* Hd, int k, int n, double t, double* sm, 
         B2[o] = V - U;  // Q
     }
     __syncthreads();
-    // solve Q F = P by Gauss-Jordan elimination with partial pivoting (rows permuted implicitly through perm[]; the
-    // lowest position wins ties): two barriers per column and no back substitution — the LU with row swaps and
-    // back substitution needed five per column, most of this CTA's time at n = 40
-    (void)fac;
-    (void)piv_s;
-    __shared__ int perm[64];
-    __shared__ double inv_s;
+    // solve Q F = P: LU with partial pivoting (lowest index wins ties), F overwrites P
     double* Q = B2;
     double* F = B1;
-    for (int i = threadIdx.x; i < n; i += ET) perm[i] = i;
-    __syncthreads();
     for (int c = 0; c < n; ++c) {
         if (threadIdx.x < 32) {
             double best = -1.0;
-            int bk = c;
-            for (int k = c + threadIdx.x; k < n; k += 32) {
-                const double v = fabs(Q[perm[k] * ld + c]);
+            int bi = c;
+            for (int i = c + threadIdx.x; i < n; i += 32) {
+                const double v = fabs(Q[i * ld + c]);
                 if (v > best) {
                     best = v;
-                    bk = k;
+                    bi = i;
                 }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double ob = __shfl_down_sync(0xffffffffu, best, o);
-                const int ok = __shfl_down_sync(0xffffffffu, bk, o);
-                if (ob > best || (ob == best && ok < bk)) {
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
                     best = ob;
-                    bk = ok;
+                    bi = oi;
                 }
             }
-            if (threadIdx.x == 0) {
-                const int t0 = perm[c];
-                perm[c] = perm[bk];
-                perm[bk] = t0;
-                inv_s = 1.0 / Q[perm[c] * ld + c];
+            if (threadIdx.x == 0) piv_s = bi;
+        }
+        __syncthreads();
+        const int p = piv_s;
+        if (p != c)
+            for (int col = threadIdx.x; col < n; col += ET) {
+                double t0 = Q[c * ld + col];
+                Q[c * ld + col] = Q[p * ld + col];
+                Q[p * ld + col] = t0;
+                t0 = F[c * ld + col];
+                F[c * ld + col] = F[p * ld + col];
+                F[p * ld + col] = t0;
             }
-        }
         __syncthreads();
-        const int pr = perm[c];
-        const double inv = inv_s;
-        const int wq = n - c - 1, per = wq + n;  // Q columns c+1 .. n-1, then all of F
-        for (int e = threadIdx.x; e < n * per; e += ET) {
-            const int r = e / per, col = e - r * per;
-            if (r == pr) continue;
-            const double f = Q[r * ld + c] * inv;
-            if (col < wq)
-                Q[r * ld + c + 1 + col] -= f * Q[pr * ld + c + 1 + col];
-            else
-                F[r * ld + col - wq] -= f * F[pr * ld + col - wq];
+        for (int i = c + 1 + threadIdx.x; i < n; i += ET) fac[i] = Q[i * ld + c] / Q[c * ld + c];
+        __syncthreads();
+        const int rows = n - c - 1;
+        for (int e = threadIdx.x; e < rows * n; e += ET) {
+            const int i = c + 1 + e / n, col = e % n;
+            const double f = fac[i];
+            F[i * ld + col] -= f * F[c * ld + col];
+            if (col > c) Q[i * ld + col] -= f * Q[c * ld + col];
         }
         __syncthreads();
     }
-    for (int e = threadIdx.x; e < n * n; e += ET) {  // X row c = F row perm[c] / its pivot
-        const int c = e / n, col = e - c * n;
-        B0[c * ld + col] = F[perm[c] * ld + col] / Q[perm[c] * ld + c];
+    for (int i = n - 1; i >= 0; --i) {
+        for (int col = threadIdx.x; col < n; col += ET) {
+            double t0 = F[i * ld + col];
+            for (int l = i + 1; l < n; ++l) t0 -= Q[i * ld + l] * F[l * ld + col];
+            F[i * ld + col] = t0 / Q[i * ld + i];
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    F = B0;
     // square s times
     double* X = F;
     double* Y = B3;
