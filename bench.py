@@ -173,7 +173,16 @@ def cpu_baseline(p_full, budget="bench", k_full=None):
     t_step = (t2 - t1) - (t1 - t0)
     t_start = (t1 - t0) - t_step
     t_pass = t_start + k * t_step + (t4 - t3)
-    return {"value": k / t_pass, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle",
+    full = None  # the oracle's complete run of this config, when its golden file exists (scripts/gen_golden.py)
+    try:
+        g = json.load(open(os.path.join(ROOT, "tests", "golden", f"{p_full['name']}_oracle.json")))
+        full = {"seconds": g["oracle_seconds"]["total"], "lanczos_seconds": g["oracle_seconds"]["lanczos"],
+                "host": g["host"]["cpu"], "threads": g["host"]["threads_used"],
+                "what": "the oracle's full run (k steps + the Pade sweep + box check) that wrote tests/golden, on the "
+                        "build container's host"}
+    except Exception:
+        pass
+    return {"value": k / t_pass, "unit": "Krylov steps/s", "cores": 1, "kind": "oracle", "full_run": full,
             "sample": f"oracle (1 thread, C -O2) at the full size n={W.n_state(p_full):.3g}: literal Alg. 3 with k=1 "
                       f"({t1 - t0:.2f} s) and k=2 ({t2 - t1:.2f} s) -> {t_step:.2f} s per Lanczos step, {t_start:.2f} s "
                       f"start-vector pass; plus the full {p_full['n_steps'] + 1}-step {k}x{k} Pade sweep "
