@@ -245,6 +245,8 @@ struct kr_handle {
     int large_cap = 0;     // padded dimension the large-route scratch is sized for
     double* d_gpart = nullptr;      // split-K partial sums of the band GEMMs
     size_t large_part_doubles = 0;
+    void* d_tdc = nullptr;  // divide-and-conquer eigen-solve workspace (kr_tridc.cu), for dimension tdc_cap
+    int tdc_cap = 0;
     double* d_lbound;      // [ndl] unit-vector Lemma 1 bound of the accepted k
     double* d_scratch;     // small device scratch (norms, bound)
     std::vector<std::vector<std::pair<int32_t, double>>> checks;  // per local direction: (k, bound)
@@ -326,6 +328,10 @@ void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, int 
 // zero_bound, an exact breakdown); fin also writes the direction's stats. Synchronises the stream.
 double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound);
 void kr_large_alloc(kr_handle* h, int kc);
+// kr_tridc.cu: the same for the symmetric Lanczos tridiagonal through a device divide-and-conquer eigen-solve
+// (coefficients of direction dl and e_kc^T x_j into hl); kc up to kr_tridc_max_k()
+void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride);
+int kr_tridc_max_k();
 // fused Lanczos building blocks for the adaptive (host-driven) loop
 void kr_lz_enqueue_init(kr_handle* h, int dl);
 void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events);

@@ -27,6 +27,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cstdio>
+
 #include "kr_internal.h"
 
 namespace cg = cooperative_groups;
@@ -498,7 +500,13 @@ static void gemm(kr_handle* h, const double* A, const double* B, double* C, int 
 // coefficients of direction dl are always written (the last evaluation is the accepted one).
 // zero_bound: exact breakdown at kc (the approximation is exact): bound 0.
 double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
-    kr_large_alloc(h, kc);
+    const bool tri = h->path == PATH_FUSED_LANCZOS;  // Lanczos tridiagonal arrays, else dense Hessenberg H
+    // symmetric tridiagonal: the device eigen-solve route (kr_tridc.cu, the oracle's eigendecomposition route) at
+    // every checkpoint up to kr_tridc_max_k(); KR_LARGE_TAYLOR=1 keeps the Taylor + squaring route (and the one-CTA
+    // Pade route up to 64), KR_SMALL_PADE=1 the one-CTA Pade route up to 64 only
+    const bool dc = tri && kc <= kr_tridc_max_k() && !getenv("KR_LARGE_TAYLOR") &&
+                    (kc > 64 || getenv("KR_SMALL_PADE") == nullptr);
+    if (!dc) kr_large_alloc(h, kc);
     if (!h->ev_lg0) {
         KR_CUDA(cudaEventCreate(&h->ev_lg0));
         KR_CUDA(cudaEventCreate(&h->ev_lg1));
@@ -509,7 +517,6 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     double* X = h->d_big;
     double* Y0 = X + mat;
     double* Y1 = Y0 + mat;
-    const bool tri = h->path == PATH_FUSED_LANCZOS;  // Lanczos tridiagonal arrays, else dense Hessenberg H
     LzScalars* sc = tri ? h->d_sc + dl : nullptr;
     const double* Hd = tri ? nullptr : h->d_H + (size_t)dl * (h->k + 1) * h->k;
     // h_{kc+1,kc} (1-based): beta[kc] of the Lanczos arrays, or H[kc][kc-1] of the Hessenberg
@@ -520,7 +527,9 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     const int ndl_stride = (h->part == KR_PART_DIRS && h->world > 1) ? (int)((h->n_dir + h->world - 1) / h->world) : ndl;
     double* hl = h->d_hlast + (size_t)dl * (h->n_steps + 1);
     const int64_t np1 = h->n_steps + 1;
-    if (kc <= 64 && !getenv("KR_LARGE_ONLY")) {
+    if (dc) {
+        kr_tridc_eval(h, dl, kc, hl, ndl_stride);
+    } else if (kc <= 64 && !getenv("KR_LARGE_ONLY")) {
         // small checkpoint: one CTA (Pade-13 scaling and squaring + doubling over the time grid, in shared
         // memory) instead of the ~50 launches of the GEMM route
         if (tri) {
@@ -640,6 +649,7 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     KR_CUDA(cudaStreamSynchronize(st));
     float ms = 0.f;
     KR_CUDA(cudaEventElapsedTime(&ms, h->ev_lg0, h->ev_lg1));
+    if (getenv("KR_LARGE_PROF")) fprintf(stderr, "large_eval kc=%d %s %.1f us\n", kc, dc ? "tridc" : "taylor/small", ms * 1e3);
     h->large_ms += ms;
     h->large_evals++;
     return b;

@@ -11,8 +11,21 @@ RTOL = 1e-9
 FLOOR = 1e-3
 
 
-def coeff_close(gpu, orc, rtol=RTOL, floor=FLOOR):
-    """gpu, orc: [(N+1)][o][d]. Returns (ok, worst_ratio, where)."""
+def projection_envelope(beta0, P, c=64.0):
+    """Rounding envelope of c = beta0 P x for ||x||_inf <= 1 (e^{Ht} e_1 of a dissipative H) in ANY evaluation
+    order: c u beta0 sum_l |P_rl| per output row (DESIGN R28). beta0: [d]; P: [d][o][k] (or [o][k] for d = 1).
+    Returns [1][o][d] for coeff_close's atol."""
+    P = np.asarray(P, dtype=float)
+    if P.ndim == 2:
+        P = P[None]
+    b = np.atleast_1d(np.asarray(beta0, dtype=float))
+    env = c * np.finfo(float).eps / 2 * b[:, None] * np.sum(np.abs(P), axis=2)  # [d][o]
+    return env.T[None]
+
+
+def coeff_close(gpu, orc, rtol=RTOL, floor=FLOOR, atol=None):
+    """gpu, orc: [(N+1)][o][d]. atol: an optional absolute floor broadcastable to [1][o][d] (a rounding
+    envelope, projection_envelope). Returns (ok, worst_ratio, where)."""
     gpu = np.asarray(gpu)
     orc = np.asarray(orc)
     assert gpu.shape == orc.shape, (gpu.shape, orc.shape)
@@ -23,6 +36,8 @@ def coeff_close(gpu, orc, rtol=RTOL, floor=FLOOR):
         if np.any(gpu[m] != 0.0):
             return False, np.inf, "vacuous series not exactly zero"
     tol = rtol * np.maximum(np.abs(orc), floor * S)
+    if atol is not None:
+        tol = np.maximum(tol, atol)
     err = np.abs(gpu - orc)
     with np.errstate(divide="ignore", invalid="ignore"):
         ratio = np.where(tol > 0, err / np.where(tol > 0, tol, 1.0), np.where(err > 0, np.inf, 0.0))
@@ -42,7 +57,7 @@ def bounds_close(gpu, orc, coeff_orc, zlo, zhi, rtol=RTOL, floor=FLOOR):
     return bool(ok), worst
 
 
-def assert_coeff(gpu, orc, what=""):
-    ok, worst, where = coeff_close(gpu, orc)
+def assert_coeff(gpu, orc, what="", atol=None):
+    ok, worst, where = coeff_close(gpu, orc, atol=atol)
     assert ok, f"{what}: parity fails, worst err/tol = {worst:.3g} at {where}"
     return worst
