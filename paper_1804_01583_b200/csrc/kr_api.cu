@@ -647,6 +647,7 @@ void free_handle(kr_handle* h) {
     if (h->graph_ready) cudaGraphExecDestroy(h->gexec);
     tr.mark("destroy: p2p + graph");
     for (auto e : h->ev) cudaEventDestroy(e);
+    for (auto e : h->ms_events) cudaEventDestroy(e);
     if (h->ev_it0) cudaEventDestroy(h->ev_it0);
     if (h->ev_it1) cudaEventDestroy(h->ev_it1);
     if (h->ev_lg0) cudaEventDestroy(h->ev_lg0);
@@ -1158,6 +1159,11 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             }
             kr_lz_encode_maps(h);
             kr_lz_setup_compact(h);
+            kr_lz_multistep_setup(h);
+            if (h->multistep) {  // the multi-step kernel's partials, double-buffered by step parity
+                Slab& s0 = h->slabs[0];
+                s0.mspart = reinterpret_cast<double*>(dalloc(h, (size_t)2 * h->nqp * h->ms_grid * 8));
+            }
             kr_lz_prepare(h);
             const int R_total = (int)h->slabs.size() * kr_zworld(h);
             h->d_rankvec = reinterpret_cast<double*>(dalloc(h, (size_t)R_total * h->nq * 8));
@@ -1308,6 +1314,8 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
         };
         auto enqueue = [&](bool ev) {
             KR_CUDA(kr_event_record(h->ev_it0, h->stream));
+            h->ms_ev.clear();  // timed multi-step launches of this enqueue (a captured graph replays them)
+            h->ev_rec.assign(h->ev.size() / 2, 0);
             if (h->path == PATH_FUSED_LANCZOS) {
                 for (int dl = 0; dl < ndl; ++dl) kr_lz_enqueue_direction(h, dl, ev);
             } else {
@@ -1329,6 +1337,8 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             h->large_ms = 0.0;
             h->large_evals = 0;
             KR_CUDA(cudaEventRecord(h->ev_it0, h->stream));
+            h->ms_ev.clear();
+            h->ev_rec.assign(h->ev.size() / 2, 0);
             if (h->path == PATH_GENERIC && h->eps > 0.0) {
                 // Alg. 2: all local directions step together (one SpMM per step); each direction is
                 // checked at the checkpoints 4, ceil(1.1 k), ... until its Lemma-1 bound is below eps, then
@@ -1412,12 +1422,15 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                     int64_t ncell = 0;
                     for (const auto& sl : h->slabs) ncell = std::max<int64_t>(ncell, sl.nz * h->mx * h->my);
                     bool pipe = ncell <= (int64_t(1) << 24);
+                    // two cooperative kernels (the multi-step steps and the eigen-solve) are never run side by side
+                    if (h->multistep) pipe = false;
                     if (getenv("KR_NO_SPECULATE")) pipe = false;
                     if (getenv("KR_SPECULATE")) pipe = true;
                     bool by_bound = false;
                     int kc = 4;
                     while (kc <= h->k) {
-                        while (i < kc) kr_lz_enqueue_step(h, dl, ++i, h->timing);
+                        if (i < kc) kr_lz_enqueue_steps(h, dl, i + 1, kc, h->timing);
+                        i = std::max(i, kc);
                         const LzScalars sc = read_sc(dl);
                         if (sc.status) {
                             failed = true;
@@ -1433,7 +1446,8 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                         double b;
                         if (pipe && kn <= h->k) {
                             KR_CUDA(cudaEventRecord(h->ev_spec, h->stream));
-                            while (i < kn) kr_lz_enqueue_step(h, dl, ++i, h->timing);  // speculative
+                            if (i < kn) kr_lz_enqueue_steps(h, dl, i + 1, kn, h->timing);  // speculative
+                            i = std::max(i, kn);
                             std::swap(h->stream, h->stream2);
                             try {
                                 KR_CUDA(cudaStreamWaitEvent(h->stream, h->ev_spec, 0));
@@ -1475,7 +1489,8 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                     }
                 }
                 if (accepted < 0 && !failed) {  // fixed k, or k_max reached without meeting eps
-                    while (i < h->k) kr_lz_enqueue_step(h, dl, ++i, h->timing);
+                    if (i < h->k) kr_lz_enqueue_steps(h, dl, i + 1, h->k, h->timing);
+                    i = std::max(i, h->k);
                     if (dl == 0) h->steps_run0 = i;
                     const LzScalars sc = read_sc(dl);
                     if (!sc.status) {
@@ -1549,6 +1564,7 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
             for (size_t p = 0; p < h->ev_step_of_pair.size(); ++p) {
                 const int s = h->ev_step_of_pair[p];
                 if (s > nrun) break;
+                if (p >= h->ev_rec.size() || !h->ev_rec[p]) continue;  // ran inside a multi-step launch
                 float t = 0.f;
                 KR_CUDA(cudaEventElapsedTime(&t, h->ev[2 * p], h->ev[2 * p + 1]));
                 tot += t;
@@ -1562,6 +1578,17 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                 }
             }
             if (trace) fclose(trace);
+            // multi-step launches: their time spread evenly over the steps they ran (steps past k_eff exit at once)
+            for (const auto& pe : h->ms_ev) {
+                float t = 0.f;
+                KR_CUDA(cudaEventElapsedTime(&t, h->ms_events[2 * pe.pair], h->ms_events[2 * pe.pair + 1]));
+                const int n = std::min(pe.n, nrun - pe.i0 + 1);
+                if (n <= 0) continue;
+                const double per = (double)t / pe.n;
+                for (int s = pe.i0; s < pe.i0 + n; ++s) h->step_ms[(size_t)s - 1] = per;
+                tot += per * n;
+                cnt += n;
+            }
             h->last_step_ms_mean = cnt ? tot / cnt : 0.0;
             h->last_step_launches = (int64_t)nrun * (h->path == PATH_FUSED_LANCZOS ? (int64_t)h->slabs.size() : 1);
         }

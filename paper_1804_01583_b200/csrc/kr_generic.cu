@@ -544,6 +544,7 @@ void kr_ge_enqueue_step(kr_handle* h, int j) {
     const int evp = (h->timing && j < (int)h->ev_pair_of_step.size()) ? h->ev_pair_of_step[(size_t)j] : -1;
     const bool evj = evp >= 0;
     if (evj) KR_CUDA(kr_event_record(h->ev[2 * evp], h->stream));
+    if (evj && (size_t)evp < h->ev_rec.size()) h->ev_rec[(size_t)evp] = 1;
     if (h->use_cgs) {  // operator fused into the first CGS2 pass (kr_arnoldi.cu): the events bracket the whole step
         kr_cgs_step(h, j, ndl, h->d_cgs);
         if (evj) KR_CUDA(kr_event_record(h->ev[2 * evp + 1], h->stream));

@@ -89,6 +89,7 @@ struct Slab {
     CUtensorMap tmC[3];  // "center" role box (TX+4, TY+3, 1)
     CUtensorMap tmP[3];  // "previous" role box (TX+2, TY+1, 1)
     double* partials;    // [nblk][nqp]
+    double* mspart = nullptr;  // multi-step kernel partials [2][nqp][ms grid]
     int32_t* counter;    // last-CTA arrival counter of the fused reduction
     int64_t nblk;        // persistent CTAs (= number of partial-sum slots)
     double* peer_lo[3];  // the lower / upper neighbour's state buffers (peer memory or a sibling slab), or NULL
@@ -245,6 +246,14 @@ struct kr_handle {
     int large_cap = 0;     // padded dimension the large-route scratch is sized for
     double* d_gpart = nullptr;      // split-K partial sums of the band GEMMs
     size_t large_part_doubles = 0;
+    bool multistep = false;  // Lanczos steps >= 3 by the persistent multi-step kernel (single L2-resident slab)
+    int ms_grid = 0;         // its cooperative grid
+    struct MsEv {
+        int pair, i0, n;  // event pair index into ms_events, first step, steps
+    };
+    std::vector<MsEv> ms_ev;
+    std::vector<char> ev_rec;  // per-step event pair recorded by the last enqueue (steps inside a multi-step launch are not)  // timed multi-step launches: (event pair index into ms_events, steps)
+    std::vector<cudaEvent_t> ms_events;
     void* d_tdc = nullptr;  // divide-and-conquer eigen-solve workspace (kr_tridc.cu), for dimension tdc_cap
     int tdc_cap = 0;
     double* d_lbound;      // [ndl] unit-vector Lemma 1 bound of the accepted k
@@ -334,6 +343,8 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride);
 int kr_tridc_max_k();
 // fused Lanczos building blocks for the adaptive (host-driven) loop
 void kr_lz_enqueue_init(kr_handle* h, int dl);
+void kr_lz_enqueue_steps(kr_handle* h, int dl, int i0, int i1, bool capture_events);
+void kr_lz_multistep_setup(kr_handle* h);
 void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events);
 // box
 void kr_box_enqueue(kr_handle* h, const int32_t* d_sense, const double* d_thr);

@@ -22,12 +22,16 @@
 //     neighbours live in registers; w planes go through a 2-plane shared buffer;
 //   * per-CTA partial sums (sum w^2, sum D, box-row projections C w) are reduced in a fixed order
 //     (no floating-point atomics) so results are bit-reproducible.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <float.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "kr_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -166,6 +170,14 @@ constexpr size_t step2_smem_bytes() {
     return (size_t)S * Geo2<TX, TY>::STAGE + Geo2<TX, TY>::WBYTES + 8 * S + 16;
 }
 
+// The per-step values of the march (the rest of StepArgs is the same for every step of a run): the output buffer,
+// the step's recurrence coefficients sa = s_i, sb = alpha_i s_i, sp = beta_{i-1} s_{i-1} (1, 0, 0 for the init pass)
+struct StepDyn {
+    double* out;
+    double sa, sb, sp;
+    int32_t has_prev, write_out;
+};
+
 struct Acc2 {
     double ww, sum;      // sum w^2, sum w
     double dx, dy, dz;   // sums of squared forward differences per axis (coefficient c_a)
@@ -186,13 +198,13 @@ __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpre
 // Box output rows are summed per warp (shuffle tree, fixed order) into wbox.
 template <int TX, int TY, int R, int S, bool INIT, bool FULL, int BCM, bool HALO, bool FACE>
 __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
-                                          unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
+                                          const StepDyn& dyn, unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
                                           int zc0, int zc1, bool cta_box, Acc2& A, double (*wbox)[KR_MAX_BOX]) {
     using G = Geo2<TX, TY, R>;
     constexpr int CW = G::CW, PW = G::PW, WW = G::WW, NC = 2 * R;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int pfirst = zc0 - 1, plast = zc1 + 1;
-    const bool has_prev = a.has_prev != 0;
+    const bool has_prev = dyn.has_prev != 0;
     auto issue = [&](int p) {
         const int s = (p - pfirst) % S;
         unsigned char* st = smem + s * G::STAGE;
@@ -206,14 +218,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
         const int np = min(plast - pfirst + 1, S);
         for (int p = pfirst; p < pfirst + np; ++p) issue(p);
     }
-    double sa = 1.0, sb = 0.0, sp = 0.0;
-    if (!INIT) {
-        const LzScalars* sc = a.sc;
-        const int i = a.step;
-        sa = sc->s[i];
-        sb = sc->alpha[i] * sc->s[i];
-        sp = (i > 1) ? sc->beta[i - 1] * sc->s[i - 1] : 0.0;
-    }
+    const double sa = INIT ? 1.0 : dyn.sa, sb = INIT ? 0.0 : dyn.sb, sp = INIT ? 0.0 : dyn.sp;
     const double diag = 2.0 * (a.cx + a.cy + a.cz);
     const double scx = sa * a.cx, scy = sa * a.cy, scz = sa * a.cz;
 
@@ -266,7 +271,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
             rex = (grx == 0 ? a.ecor[0] : 0.0) + (grx == a.mx - 1 ? a.ecor[1] : 0.0) + (gry == 0 ? a.ecor[2] : 0.0) +
                   (gry == a.my - 1 ? a.ecor[3] : 0.0);
     }
-    double* optr = a.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)gy * a.pitch + gx;
+    double* optr = dyn.out + (int64_t)(zc0 + 1) * a.plane + (int64_t)gy * a.pitch + gx;
 
     // u of three consecutive planes (the thread's cells) in three register sets that take turns as u_{q-1}, u_q,
     // u_{q+1}; w of two consecutive planes in two sets (w_{q-1}, w_q): the interior loop is unrolled by six
@@ -466,7 +471,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
                 for (int c = 0; c < NC; ++c) s2 = fma(wp[c], wp[c], s2);
                 A.face = fma(a.gq[4], s2, A.face);
             }
-            const bool wr = !INIT && a.write_out;
+            const bool wr = !INIT && dyn.write_out;
             if (wr) {
 #pragma unroll
                 for (int r = 0; r < R; ++r)
@@ -491,7 +496,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
             // planes 0, 1 -> the lower neighbour, the last owned plane -> the upper neighbour
             const int qq = q - 1;
             if (HALO && wr && ((a.rlo && qq < 2) || (a.rhi && qq == a.nz - 1))) {
-                const int64_t off = (optr - a.out) - (int64_t)(qq + 1) * a.plane;  // in-plane offset of cell 0
+                const int64_t off = (optr - dyn.out) - (int64_t)(qq + 1) * a.plane;  // in-plane offset of cell 0
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     if (!(FULL || (gx < a.mx && gy + r < a.my))) continue;
@@ -548,22 +553,13 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     }
 }
 
-template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false, int R = 2>
-__global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 : 2)
-    lz_step_kernel2(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
-    using G = Geo2<TX, TY, R>;
-    if (a.sc->done) return;  // breakdown happened earlier: uniform early exit
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    double* Wb0 = reinterpret_cast<double*>(smem + S * G::STAGE);
-    double* Wb1 = Wb0 + G::WW * G::WH;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * G::STAGE + G::WBYTES);
-
+// The work items (x-tile, y-tile, z-chunk) of one step, dealt round-robin over the CTAs (fixed assignment,
+// deterministic): the march of each item, accumulating the CTA's sums in A and wbox.
+template <int TX, int TY, int S, bool INIT, bool BC, bool HALO, int R>
+__device__ __forceinline__ void lz_items2(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
+                                          const StepDyn& dy, unsigned char* smem, double* Wb0, double* Wb1,
+                                          uint64_t* bar, Acc2& A, double (*wbox)[KR_MAX_BOX]) {
     const int tid = threadIdx.x;
-    Acc2 A{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    __shared__ double wbox[G::NT / 32][KR_MAX_BOX];  // per-warp box-row sums (lane 0 of each warp)
-    if ((tid & 31) == 0)
-        for (int r = 0; r < KR_MAX_BOX; ++r) wbox[tid >> 5][r] = 0.0;
     // Persistent CTAs: work items (x-tile, y-tile, z-chunk) dealt round-robin (fixed assignment, deterministic)
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
         const int xt = a.ix0 + item % a.gx, yt = a.iy0 + (item / a.gx) % a.gy, zt = a.iz0 + item / (a.gx * a.gy);
@@ -583,8 +579,8 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
                 a.box[r].hi[2] > a.zoff + zc0)
                 cta_box = true;
 #define KR_M2(FULL_, BCM_, FACE_) \
-    lz_march2<TX, TY, R, S, INIT, FULL_, BCM_, HALO, FACE_>(&tmC, &tmP, a, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, A, \
-                                                            wbox)
+    lz_march2<TX, TY, R, S, INIT, FULL_, BCM_, HALO, FACE_>(tmC, tmP, a, dy, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, \
+                                                            A, wbox)
         if (x0 + TX < a.mx && y0 + TY < a.my) {
             if (x0 > 0 && y0 > 0)
                 KR_M2(true, BC ? 1 : 0, false);
@@ -601,6 +597,34 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
                 asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar[s])) : "memory");
         }
     }
+
+}
+
+template <int TX, int TY, int S, bool INIT, bool BC, bool HALO = false, int R = 2>
+__global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 : 2)
+    lz_step_kernel2(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP, const StepArgs a) {
+    using G = Geo2<TX, TY, R>;
+    if (a.sc->done) return;  // breakdown happened earlier: uniform early exit
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* Wb0 = reinterpret_cast<double*>(smem + S * G::STAGE);
+    double* Wb1 = Wb0 + G::WW * G::WH;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * G::STAGE + G::WBYTES);
+
+    const int tid = threadIdx.x;
+    StepDyn dy{a.out, 1.0, 0.0, 0.0, a.has_prev, a.write_out};
+    if (!INIT) {
+        const LzScalars* sc = a.sc;
+        const int i = a.step;
+        dy.sa = sc->s[i];
+        dy.sb = sc->alpha[i] * sc->s[i];
+        dy.sp = (i > 1) ? sc->beta[i - 1] * sc->s[i - 1] : 0.0;
+    }
+    Acc2 A{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    __shared__ double wbox[G::NT / 32][KR_MAX_BOX];  // per-warp box-row sums (lane 0 of each warp)
+    if ((tid & 31) == 0)
+        for (int r = 0; r < KR_MAX_BOX; ++r) wbox[tid >> 5][r] = 0.0;
+    lz_items2<TX, TY, S, INIT, BC, HALO, R>(&tmC, &tmP, a, dy, smem, Wb0, Wb1, bar, A, wbox);
 
     if (HALO && a.rfence) __threadfence_system();  // peer-memory halo stores visible before the collective that follows
     __syncthreads();
@@ -812,6 +836,142 @@ __global__ void __launch_bounds__(RT) lz_reduce_kernel(const StepArgs a, int64_t
     if (tid == 0 && a.fin)
         lz_finalize_dev(res, 1, 2 + a.n_out, a.n_out, a.step, a.k, a.scw, a.H, a.P, a.beta0_out, a.hnext_out,
                         a.keff_out);
+}
+
+// ---- persistent multi-step Lanczos (small grids) --------------------------------------------------------------
+// Steps i0..i1 of Alg. 3 / 4 in ONE cooperative launch, for a single slab on a single rank whose three
+// state vectors stay in the 126 MB L2 (10^6 cells: 24 MB): per step the same march as lz_step_kernel2 over the
+// CTA's work items, its partial sums, one grid barrier, then EVERY CTA reduces all partials in the same fixed order
+// and updates the scalars itself (identical values everywhere, so the breakdown / k test exits all CTAs at the
+// same step and no second barrier is needed). Replaces a step launch + a reduce launch per step (~21 us at 10^6
+// cells, latency-bound) by ~one barrier. The scalars (alpha, beta, s, P, H, k_eff, h_next, done) are written to
+// global memory by every CTA with the same bits; hmax lives in shared memory (a CTA must not read another CTA's
+// newer global hmax, which could flip its breakdown test).
+struct MultiArgs {
+    double* u[3];   // the slab's state buffers
+    double* part;   // [2][nqp][gridDim.x] per-CTA partial sums, double-buffered by step parity
+    int32_t i0, i1; // steps
+};
+
+template <int TX, int TY, int S, bool BC, int R>
+__global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 : 2)
+    lz_multistep_kernel(const __grid_constant__ CUtensorMap tmC0, const __grid_constant__ CUtensorMap tmC1,
+                        const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ CUtensorMap tmP0,
+                        const __grid_constant__ CUtensorMap tmP1, const __grid_constant__ CUtensorMap tmP2,
+                        const StepArgs a, const MultiArgs m) {
+    using G = Geo2<TX, TY, R>;
+    constexpr int NWp = G::NT / 32;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* Wb0 = reinterpret_cast<double*>(smem + S * G::STAGE);
+    double* Wb1 = Wb0 + G::WW * G::WH;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * G::STAGE + G::WBYTES);
+    __shared__ double wbox[NWp][KR_MAX_BOX];
+    __shared__ double wred[NWp][3 + KR_MAX_BOX];
+    __shared__ double qsum[2 + KR_MAX_BOX];
+    __shared__ double coef[3];
+    __shared__ double hmax;
+    __shared__ int done;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nblk = (int)gridDim.x, nqp = a.nqp, k = a.k;
+    LzScalars* sc = a.scw;
+    if (tid == 0) {  // read before the first barrier: no CTA has written step i0's scalars yet
+        const int i = m.i0;
+        done = sc->done;
+        hmax = sc->hmax;
+        coef[0] = sc->s[i];
+        coef[1] = sc->alpha[i] * sc->s[i];
+        coef[2] = i > 1 ? sc->beta[i - 1] * sc->s[i - 1] : 0.0;
+    }
+    __syncthreads();
+    for (int i = m.i0; i <= m.i1; ++i) {
+        if (done) break;  // uniform over the grid
+        const int cur = (i - 1) % 3, nxt = i % 3, prev = i >= 2 ? (i - 2) % 3 : cur;
+        const CUtensorMap* tc = cur == 0 ? &tmC0 : (cur == 1 ? &tmC1 : &tmC2);
+        const CUtensorMap* tp = prev == 0 ? &tmP0 : (prev == 1 ? &tmP1 : &tmP2);
+        const StepDyn dy{m.u[nxt], coef[0], coef[1], coef[2], i > 1 ? 1 : 0, i < k ? 1 : 0};
+        Acc2 A{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (lane == 0)
+            for (int r = 0; r < KR_MAX_BOX; ++r) wbox[wid][r] = 0.0;
+        lz_items2<TX, TY, S, false, BC, false, R>(tc, tp, a, dy, smem, Wb0, Wb1, bar, A, wbox);
+        __syncthreads();
+        // the CTA's sums (as lz_epilogue), into the partials of this step's parity
+        {
+            double acc[3 + KR_MAX_BOX];
+            acc[0] = A.ww;
+            acc[1] = fma(a.cx, A.dx, fma(a.cy, A.dy, fma(a.cz, A.dz, A.face)));  // -w^T A w
+            acc[2] = A.sum;
+#pragma unroll
+            for (int r = 0; r < KR_MAX_BOX; ++r) acc[3 + r] = lane == 0 ? wbox[wid][r] : 0.0;
+#pragma unroll
+            for (int r = 0; r < 3 + KR_MAX_BOX; ++r) {
+                if (r < 3 + a.nbox) {
+                    double v = acc[r];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                    if (lane == 0) wred[wid][r] = v;
+                }
+            }
+        }
+        __syncthreads();
+        double* part = m.part + (size_t)(i & 1) * nqp * nblk;
+        if (tid < nqp) {
+            const int src = tid < 2 ? tid : (((a.all_mask >> (tid - 2)) & 1u) ? 2 : tid + 1);
+            double s = 0.0;
+            for (int w = 0; w < NWp; ++w) s += wred[w][src];
+            part[(size_t)tid * nblk + blockIdx.x] = s;
+        }
+        // u_{i+1} was written by generic stores; the next step reads it through TMA (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        grid.sync();
+        // all partials, fixed order (lane-strided sums, xor tree): the same bits in every CTA
+        for (int q = wid; q < nqp; q += NWp) {
+            double v = 0.0;
+            for (int b = lane; b < nblk; b += 32) v += __ldcg(part + (size_t)q * nblk + b);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) qsum[q] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            // the scalar update of lz_finalize_dev for step i >= 1 (beta_i, alpha_{i+1}, s_{i+1}, P column, breakdown)
+            const double Sww = qsum[0], SD = qsum[1];
+            const double b = sqrt(Sww);
+            if (!isfinite(b)) {
+                sc->status = KR_ENONFINITE;
+                sc->done = 1;
+                done = 1;
+            } else {
+                sc->beta[i] = b;
+                if (a.H) a.H[(int64_t)i * k + (i - 1)] = b;
+                if (b == 0.0 || b <= 16.0 * DBL_EPSILON * hmax || i == k) {
+                    sc->done = 1;
+                    sc->k_eff = i;
+                    sc->h_next = b;
+                    *a.keff_out = i;
+                    *a.hnext_out = b;
+                    done = 1;
+                } else {
+                    if (a.H) a.H[(int64_t)(i - 1) * k + i] = b;
+                    const double sn = 1.0 / b;
+                    sc->s[i + 1] = sn;
+                    const double an = -SD / Sww;
+                    sc->alpha[i + 1] = an;
+                    if (a.H) a.H[(int64_t)i * k + i] = an;
+                    for (int r = 0; r < a.n_out; ++r) a.P[(int64_t)r * k + i] = 0.0;
+                    for (int q = 2; q < nqp; ++q) a.P[(int64_t)a.box_slot[q - 2] * k + i] = sn * (qsum[q] * a.box_val[q - 2]);
+                    hmax = fmax(hmax, fmax(b, fabs(an)));
+                    sc->hmax = hmax;
+                    sc->k_eff = i + 1;
+                    *a.keff_out = i + 1;
+                    coef[2] = b * coef[0];  // beta_i s_i
+                    coef[0] = sn;
+                    coef[1] = an * sn;
+                }
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // Init pass for an analytic generator (KR_VEC_BOX / KR_VEC_ALL): writes u_1 = v over the slab buffer
@@ -1374,6 +1534,7 @@ void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events) {
     const int evp = (capture_events && dl == 0 && i < (int)h->ev_pair_of_step.size()) ? h->ev_pair_of_step[(size_t)i] : -1;
     const bool ev = evp >= 0;
     if (ev) KR_CUDA(kr_event_record(h->ev[2 * evp], h->stream));
+    if (ev && (size_t)evp < h->ev_rec.size()) h->ev_rec[(size_t)evp] = 1;
     for (auto& sl : h->slabs) {
         const bool cmp = !sl.cu1.empty() && sl.cu1[dl].on && i <= 2;  // u_1 compact: u_i at step 1, u_{i-1} at 2
         step_launch(h, sl, dl, cur, prev, nxt, i, false, write, false, cmp ? i : 0);
@@ -1387,8 +1548,94 @@ void kr_lz_enqueue_step(kr_handle* h, int dl, int i, bool capture_events) {
     combine_and_finalize(h, dl, i);
 }
 
+// ---- the multi-step route ---------------------------------------------------------------------------------------
+template <int TX, int TY, bool BC>
+static void* multistep_fn() {
+    return (void*)lz_multistep_kernel<TX, TY, Stages<TX, TY>::S, BC, 2>;
+}
+
+template <int TX, int TY>
+static void multistep_setup_t(kr_handle* h) {
+    constexpr int S = Stages<TX, TY>::S;
+    const size_t smem = step2_smem_bytes<TX, TY, S>();
+    void* fn = h->gen_bc ? multistep_fn<TX, TY, true>() : multistep_fn<TX, TY, false>();
+    KR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148, per_sm = 0;
+    KR_CUDA(cudaGetDevice(&dev));
+    KR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Geo2<TX, TY, 2>::NT, smem));
+    h->ms_grid = (int)std::min<int64_t>(h->slabs[0].nitems, (int64_t)sms * per_sm);
+    if (per_sm < 1 || h->ms_grid < 1) h->multistep = false;
+}
+
+// Decide the multi-step route (after the slabs exist): one slab on one rank, no sparse output rows (their
+// gather needs the whole new vector after the step), state vectors small enough to stay in L2 (3 x 8 n bytes
+// <= ~100 MB: n <= 2^22 cells). KR_MULTISTEP=0 / 1 forces it off / on (on: any single-slab grid).
+void kr_lz_multistep_setup(kr_handle* h) {
+    h->multistep = false;
+    if (h->path != PATH_FUSED_LANCZOS || h->slabs.size() != 1 || kr_zworld(h) != 1 || h->halo_inkernel) return;
+    for (const DVec& o : h->outs_h)
+        if (o.kind == KR_VEC_SPARSE) return;
+    const Slab& sl = h->slabs[0];
+    const int64_t n = sl.nz * h->mx * h->my;
+    bool on = n <= (int64_t(1) << 22);
+    if (const char* e = getenv("KR_MULTISTEP")) on = atoi(e) != 0;
+    if (!on) return;
+    h->multistep = true;
+    if (h->TX == 64 && h->TY == 16)
+        multistep_setup_t<64, 16>(h);
+    else if (h->TX == 64 && h->TY == 8)
+        multistep_setup_t<64, 8>(h);
+    else
+        h->multistep = false;
+}
+
+template <int TX, int TY>
+static void multistep_launch_t(kr_handle* h, Slab& sl, int dl, int i0, int i1) {
+    constexpr int S = Stages<TX, TY>::S;
+    StepArgs a = make_args(h, sl, dl, i0 % 3, i0, false, true, -1, 0);
+    MultiArgs m{{sl.u[0], sl.u[1], sl.u[2]}, sl.mspart, i0, i1};
+    void* fn = h->gen_bc ? multistep_fn<TX, TY, true>() : multistep_fn<TX, TY, false>();
+    void* args[] = {(void*)&sl.tmC[0], (void*)&sl.tmC[1], (void*)&sl.tmC[2], (void*)&sl.tmP[0],
+                    (void*)&sl.tmP[1], (void*)&sl.tmP[2], (void*)&a, (void*)&m};
+    KR_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)h->ms_grid), dim3(Geo2<TX, TY, 2>::NT), args,
+                                        step2_smem_bytes<TX, TY, S>(), h->stream));
+    h->launches++;
+}
+
+// Enqueue Lanczos steps i0..i1 of local direction dl: the persistent multi-step kernel where it applies (steps
+// past the compact-u_1 ones), else one step launch + one reduce launch per step.
+void kr_lz_enqueue_steps(kr_handle* h, int dl, int i0, int i1, bool capture_events) {
+    int i = i0;
+    if (h->multistep) {
+        Slab& sl = h->slabs[0];
+        const bool cmp = !sl.cu1.empty() && sl.cu1[dl].on;
+        while (i <= i1 && cmp && i <= 2) kr_lz_enqueue_step(h, dl, i++, capture_events);
+        if (i > i1) return;
+        const bool ev = capture_events && dl == 0;
+        size_t pe = 0;
+        if (ev) {
+            pe = h->ms_ev.size();
+            while (h->ms_events.size() < 2 * (pe + 1)) {
+                cudaEvent_t e;
+                KR_CUDA(cudaEventCreate(&e));
+                h->ms_events.push_back(e);
+            }
+            h->ms_ev.push_back({(int)pe, i, i1 - i + 1});
+            KR_CUDA(kr_event_record(h->ms_events[2 * pe], h->stream));
+        }
+        if (h->TX == 64 && h->TY == 16)
+            multistep_launch_t<64, 16>(h, sl, dl, i, i1);
+        else
+            multistep_launch_t<64, 8>(h, sl, dl, i, i1);
+        if (ev) KR_CUDA(kr_event_record(h->ms_events[2 * pe + 1], h->stream));
+        return;
+    }
+    for (; i <= i1; ++i) kr_lz_enqueue_step(h, dl, i, capture_events);
+}
+
 // Enqueue the complete fixed-k Lanczos run for local direction dl on h->stream (capturable).
 void kr_lz_enqueue_direction(kr_handle* h, int dl, bool capture_events) {
     kr_lz_enqueue_init(h, dl);
-    for (int i = 1; i <= h->k; ++i) kr_lz_enqueue_step(h, dl, i, capture_events);
+    kr_lz_enqueue_steps(h, dl, 1, h->k, capture_events);
 }

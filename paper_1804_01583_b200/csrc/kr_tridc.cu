@@ -77,6 +77,13 @@ __device__ __forceinline__ void wstamp(const DC& g, int& k, int gw) {  // warp 0
     }
     ++k;
 }
+__device__ __forceinline__ void wend(const DC& g, int k) {  // the latest CTA to finish the work before barrier k
+    if (g.prof && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(g.prof + 150 + k, t);
+    }
+}
 __device__ __forceinline__ void stamp(const DC& g, int& k) {
     if (g.prof && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
@@ -190,6 +197,20 @@ __device__ __forceinline__ double gsum(double x) {
         for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     }
     return x;
+}
+// N sums reduced together: the N shuffles of a level are independent and issue back to back
+template <int G, int N>
+__device__ __forceinline__ void gsumN(double (&v)[N]) {
+    if (G > 1) {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            double t[N];
+#pragma unroll
+            for (int q = 0; q < N; ++q) t[q] = __shfl_xor_sync(0xffffffffu, v[q], o);
+#pragma unroll
+            for (int q = 0; q < N; ++q) v[q] += t[q];
+        }
+    }
 }
 template <int G>
 __device__ __forceinline__ double gprod(double x) {
@@ -417,7 +438,10 @@ __device__ void secular_root(const double* d, const double* z, int K, double rho
     if (j < K - 1) {
         const double mid = 0.5 * (d[j + 1] - d[j]);
         double s = 0.0;
-        for (int i = lane; i < K; i += G) s += z[i] * z[i] * frcp((d[i] - d[j]) - mid);
+        for (int i0 = 0; i0 < K; i0 += G) {  // uniform trip count: the shuffles below see a converged warp
+            const int i = i0 + lane;
+            if (i < K) s += z[i] * z[i] * frcp((d[i] - d[j]) - mid);
+        }
         const double fm = 1.0 + rho * gsum<G>(s);
         if (fm > 0.0) {
             org = j;
@@ -443,41 +467,48 @@ __device__ void secular_root(const double* d, const double* z, int K, double rho
     for (; it < 200; ++it) {
         double s1 = 0.0, s2 = 0.0, q1 = 0.0, q2 = 0.0, ea = 0.0;
 #pragma unroll 4
-        for (int i = lane; i < K; i += G) {
-            const double r = frcp((d[i] - dorg) - tau);
-            const double t = rho * z[i] * z[i] * r;
-            const double tq = t * r;
-            const bool left = i <= p1;
-            ea += fabs(t);
-            s1 += left ? t : 0.0;
-            q1 += left ? tq : 0.0;
-            s2 += left ? 0.0 : t;
-            q2 += left ? 0.0 : tq;
+        for (int i0 = 0; i0 < K; i0 += G) {
+            const int i = i0 + lane;
+            if (i < K) {
+                const double r = frcp((d[i] - dorg) - tau);
+                const double t = rho * z[i] * z[i] * r;
+                const double tq = t * r;
+                const bool left = i <= p1;
+                ea += fabs(t);
+                s1 += left ? t : 0.0;
+                q1 += left ? tq : 0.0;
+                s2 += left ? 0.0 : t;
+                q2 += left ? 0.0 : tq;
+            }
         }
-        s1 = gsum<G>(s1);
-        s2 = gsum<G>(s2);
-        q1 = gsum<G>(q1);
-        q2 = gsum<G>(q2);
-        ea = gsum<G>(ea);
+        double v5[5] = {s1, s2, q1, q2, ea};
+        gsumN<G, 5>(v5);
+        s1 = v5[0];
+        s2 = v5[1];
+        q1 = v5[2];
+        q2 = v5[3];
+        ea = v5[4];
         const double f = 1.0 + s1 + s2;
-        if (fabs(f) <= 8.0 * EPSM * (1.0 + ea)) break;
+        // every lane holds the same sums: the exits below are warp-uniform (told to the compiler by the votes)
+        if (G > 1 ? __all_sync(0xffffffffu, fabs(f) <= 8.0 * EPSM * (1.0 + ea)) : fabs(f) <= 8.0 * EPSM * (1.0 + ea)) break;
         if (f > 0.0) hi = tau; else lo = tau;
+        // the matched pole terms b / (pole - tau) with b = q (pole - tau)^2: a = s - q (pole - tau), no division
         const double D1 = dl1 - tau, D2 = dl2 - tau;
+        const double a1 = s1 - q1 * D1, a2 = s2 - q2 * D2;
         const double b1 = q1 * D1 * D1, b2 = q2 * D2 * D2;
-        const double a1 = s1 - b1 / D1, a2 = s2 - b2 / D2;
         const double c = 1.0 + a1 + a2;
         const double B = c * (D1 + D2) + b1 + b2;
         const double C = D1 * D2 * f;
         double eta;
         if (c == 0.0) {
-            eta = C / B;
+            eta = C * frcp(B);
         } else {
             const double disc = fmax(B * B - 4.0 * c * C, 0.0);
-            eta = 2.0 * C / (B + copysign(sqrt(disc), B));
+            eta = 2.0 * C * frcp(B + copysign(sqrt(disc), B));
         }
         double tn = tau + eta;
         if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
-        if (tn == tau) break;
+        if (G > 1 ? __all_sync(0xffffffffu, tn == tau) : tn == tau) break;
         tau = tn;
     }
     *dorg_o = dorg;
@@ -502,9 +533,12 @@ __device__ __forceinline__ double gu_eisenstat_z(const double* d, const double* 
     const double dx = d[x];
     double p = 1.0;
 #pragma unroll 4
-    for (int j = lane; j < K; j += G) {
-        const double lj = (dorg[j] - dx) + tau[j];
-        p *= lj * frcp(j == x ? rho : d[j] - dx);
+    for (int j0 = 0; j0 < K; j0 += G) {
+        const int j = j0 + lane;
+        if (j < K) {
+            const double lj = (dorg[j] - dx) + tau[j];
+            p *= lj * frcp(j == x ? rho : d[j] - dx);
+        }
     }
     p = gprod<G>(p);
     return copysign(sqrt(fmax(p, 0.0)), zsign);
@@ -517,19 +551,16 @@ __device__ __forceinline__ void eigvec_rows(const DC& g, const double* d, const 
                                             const double* src, int sld, int K, double dorg, double tj, int dst,
                                             int lane) {
     double nrm = 0.0;
-#pragma unroll 4
-    for (int i = lane; i < K; i += G) {
-        const double u = zh[i] * frcp((d[i] - dorg) - tj);
-        nrm += u * u;
-    }
-    const double inv = 1.0 / sqrt(gsum<G>(nrm));
     for (int r0 = 0; r0 < g.R; r0 += RMAX) {
         double acc[RMAX];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r) acc[r] = 0.0;
 #pragma unroll 4
-        for (int i = lane; i < K; i += G) {
+        for (int i0 = 0; i0 < K; i0 += G) {
+            const int i = i0 + lane;
+            if (i >= K) continue;
             const double u = zh[i] * frcp((d[i] - dorg) - tj);
+            if (r0 == 0) nrm = fma(u, u, nrm);
             if (STAGED) {
 #pragma unroll
                 for (int r = 0; r < RMAX; ++r)
@@ -541,13 +572,16 @@ __device__ __forceinline__ void eigvec_rows(const DC& g, const double* d, const 
                     if (r0 + r < g.R) acc[r] = fma(__ldcg(&g.Wp[(size_t)(r0 + r) * g.ld + col]), u, acc[r]);
             }
         }
+        double v[RMAX + 1];
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-            if (r0 + r < g.R) {
-                const double a = gsum<G>(acc[r]);
-                if (lane == 0) g.W[(size_t)(r0 + r) * g.ld + dst] = a * inv;
-            }
-        }
+        for (int r = 0; r < RMAX; ++r) v[r] = acc[r];
+        v[RMAX] = nrm;
+        gsumN<G, RMAX + 1>(v);
+        if (r0 == 0) nrm = v[RMAX];
+        const double inv = 1.0 / sqrt(nrm);
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+            if (r0 + r < g.R && lane == 0) g.W[(size_t)(r0 + r) * g.ld + dst] = v[r] * inv;
     }
 }
 
@@ -574,6 +608,8 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
         g.W[ld + i] = 1.0;
         for (int r = 0; r < g.n_out; ++r) g.W[(size_t)(2 + r) * ld + i] = g.P[(size_t)r * g.kstride + i];
     }
+    __syncthreads();
+    wend(g, ps);
     grid.sync();
     stamp(g, ps);
 
@@ -678,6 +714,8 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             __syncwarp();
         }
     }
+    __syncthreads();
+    wend(g, ps);
     grid.sync();
     stamp(g, ps);
 
@@ -704,7 +742,9 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             __syncthreads();
             deflate<NT>(g, team, n, 2.0 * fabs(b), nd.lo, sA, sD, sZ, sI, sF, node_global(g, q, nd.lo));
         }
-        grid.sync();
+        __syncthreads();
+    wend(g, ps);
+    grid.sync();
     stamp(g, ps);
         const int nunits = (kc + NW - 1) / NW;
         // roots
@@ -733,7 +773,9 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             }
             __syncthreads();
         }
-        grid.sync();
+        __syncthreads();
+    wend(g, ps);
+    grid.sync();
     stamp(g, ps);
         // z (entries < K) and the deflated columns' places (K <= entry < K + deflated)
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -770,7 +812,9 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             }
             __syncthreads();
         }
-        grid.sync();
+        __syncthreads();
+    wend(g, ps);
+    grid.sync();
     stamp(g, ps);
         // eigenvectors: the carried rows
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -813,7 +857,9 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             }
             __syncthreads();
         }
-        grid.sync();
+        __syncthreads();
+    wend(g, ps);
+    grid.sync();
     stamp(g, ps);
     }
 
@@ -867,6 +913,8 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             }
         }
     }
+    __syncthreads();
+    wend(g, ps);
     grid.sync();
     stamp(g, ps);
 }
@@ -961,7 +1009,7 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
         unsigned long long* pi = prof + 200;
         KR_CUDA(cudaMemcpyToSymbol(g_prof_iters, &pi, sizeof(pi)));
     }
-    if (want_prof) KR_CUDA(cudaMemsetAsync(prof + 200, 0, 8 * 8, h->stream));
+    if (want_prof) KR_CUDA(cudaMemsetAsync(prof + 150, 0, 58 * 8, h->stream));
     g.prof = want_prof ? prof : nullptr;
     void* args[] = {(void*)&g};
     KR_CUDA(cudaLaunchCooperativeKernel((const void*)tridc_kernel, dim3(nb), dim3(NT), args, smem, h->stream));
@@ -974,6 +1022,8 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
         for (int s = 2 * LOCAL; s < 2 * kc; s <<= 1) n += 4;
         fprintf(stderr, "tridc kc=%d nb=%d smem=%zu:", kc, nb, smem);
         for (int i = 1; i <= n; ++i) fprintf(stderr, " %.1f", (t[i] - t[i - 1]) * 1e-3);
+        fprintf(stderr, " | work:");
+        for (int i = 1; i <= n; ++i) fprintf(stderr, " %.1f", ((long long)t[150 + i] - (long long)t[i - 1]) * 1e-3);
         fprintf(stderr, " | warp 0 local:");
         for (int i = 101; i < 126; ++i) fprintf(stderr, " %.1f", (t[i] - t[i - 1]) * 1e-3);
         fprintf(stderr, " | secular iterations %llu over %llu roots, max %llu; cycles/root %.0f; warp roots %llu: cycles %.0f, K %.0f\n", t[200], t[201], t[202], (double)t[203] / t[201], t[205], (double)t[204] / (t[205] ? t[205] : 1), (double)t[206] / (t[205] ? t[205] : 1));

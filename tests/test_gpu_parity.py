@@ -441,10 +441,11 @@ def test_expm_march_equals_one_cta_doubling(n_steps, B, monkeypatch):
 
 
 @pytest.mark.parametrize("k,expect", [(30, [1, 2, 3, 8, 13, 19, 24, 29]), (5, [1, 2, 3, 4]), (2, [1, 2])])
-def test_step_times_sampled(k, expect):
-    """krylov_step_times: one entry per step run; CUDA events around steps 1, 2 and six steps spread over
-    3..k-1 (finite, positive), NaN elsewhere."""
+def test_step_times_sampled(k, expect, monkeypatch):
+    """krylov_step_times with one launch per step (KR_MULTISTEP=0): one entry per step run; CUDA events around
+    steps 1, 2 and six steps spread over 3..k-1 (finite, positive), NaN elsewhere."""
     from paper_1804_01583_b200 import KrylovReach
+    monkeypatch.setenv("KR_MULTISTEP", "0")
     p = W.heat(20, 3, k, n_steps=10)
     with KrylovReach(p) as h:
         h.project(want=False)
@@ -455,6 +456,21 @@ def test_step_times_sampled(k, expect):
     assert timed == expect
     assert all(st[i - 1] > 0 for i in timed)
     assert t["step_ms_mean"] == pytest.approx(float(np.mean([st[i - 1] for i in timed])), rel=1e-12)
+
+
+@pytest.mark.parametrize("k", [30, 5, 2])
+def test_step_times_multistep(k):
+    """With the persistent multi-step kernel (the default on small grids) steps 1-2 of a compact start vector are
+    timed one by one and every later step gets its launch's mean; step_ms_mean is their mean."""
+    from paper_1804_01583_b200 import KrylovReach
+    p = W.heat(20, 3, k, n_steps=10)
+    with KrylovReach(p) as h:
+        h.project(want=False)
+        st = h.step_times()
+        t = h.last_timing()
+    assert len(st) == k
+    assert all(np.isfinite(x) and x > 0 for x in st)
+    assert t["step_ms_mean"] == pytest.approx(float(np.mean(st)), rel=1e-12)
 
 
 def test_virtual_slabs_two_planes_each():
