@@ -648,6 +648,7 @@ void free_handle(kr_handle* h) {
     tr.mark("destroy: p2p + graph");
     for (auto e : h->ev) cudaEventDestroy(e);
     for (auto e : h->ms_events) cudaEventDestroy(e);
+    if (h->h_pin) cudaFreeHost(h->h_pin);
     if (h->ev_it0) cudaEventDestroy(h->ev_it0);
     if (h->ev_it1) cudaEventDestroy(h->ev_it1);
     if (h->ev_lg0) cudaEventDestroy(h->ev_lg0);
@@ -1077,6 +1078,7 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
             // tile: 64 x 16 cells (one x-pair per lane, a warp per row pair: 256 threads), 64 x 8 below 64 rows
             h->TX = 64;
             h->TY = h->my >= 64 ? 16 : 8;
+            if (const char* e = getenv("KR_TY")) h->TY = atoi(e) == 8 ? 8 : 16;  // diagnostic: tile height
             int nsl = 1, W = h->world, R = h->rank;
             if (p->virtual_slabs > 1) {
                 nsl = p->virtual_slabs;
@@ -1422,16 +1424,26 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                     int64_t ncell = 0;
                     for (const auto& sl : h->slabs) ncell = std::max<int64_t>(ncell, sl.nz * h->mx * h->my);
                     bool pipe = ncell <= (int64_t(1) << 24);
-                    // two cooperative kernels (the multi-step steps and the eigen-solve) are never run side by side
-                    if (h->multistep) pipe = false;
                     if (getenv("KR_NO_SPECULATE")) pipe = false;
                     if (getenv("KR_SPECULATE")) pipe = true;
+                    // two cooperative kernels (the multi-step steps and the eigen-solve) run side by side only when
+                    // both grids fit the GPU together (the multi-step kernel at one CTA per SM, KR_MS_PIPE=1)
+                    if (h->multistep && !(h->ms_one_per_sm && getenv("KR_MS_PIPE"))) pipe = false;
                     bool by_bound = false;
                     int kc = 4;
                     while (kc <= h->k) {
                         if (i < kc) kr_lz_enqueue_steps(h, dl, i + 1, kc, h->timing);
                         i = std::max(i, kc);
-                        const LzScalars sc = read_sc(dl);
+                        // sequential schedule: the checkpoint's evaluation is enqueued right behind the steps and
+                        // its bound and the scalars come back in one round trip (a breakdown found there discards
+                        // the evaluation below); pipelined: the scalars first, the evaluation beside the next steps
+                        LzScalars sc;
+                        double b_seq = 0.0;
+                        if (!pipe || kc >= h->k)
+                            b_seq = kr_large_eval(h, dl, kc, true, false, &sc);
+                        else
+                            sc = read_sc(dl);
+                        const bool have_b = !pipe || kc >= h->k;
                         if (sc.status) {
                             failed = true;
                             break;
@@ -1458,7 +1470,7 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                             }
                             std::swap(h->stream, h->stream2);
                         } else {
-                            b = kr_large_eval(h, dl, kc, true, false);
+                            b = have_b ? b_seq : kr_large_eval(h, dl, kc, true, false);
                         }
                         h->checks[dl].push_back({kc, b});
                         if (b < h->eps) {

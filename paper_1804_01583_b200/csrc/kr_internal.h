@@ -246,8 +246,10 @@ struct kr_handle {
     int large_cap = 0;     // padded dimension the large-route scratch is sized for
     double* d_gpart = nullptr;      // split-K partial sums of the band GEMMs
     size_t large_part_doubles = 0;
+    void* h_pin = nullptr;   // pinned host scratch (checkpoint bound + scalars in one round trip)
     bool multistep = false;  // Lanczos steps >= 3 by the persistent multi-step kernel (single L2-resident slab)
     int ms_grid = 0;         // its cooperative grid
+    bool ms_one_per_sm = false;  // ... at most one CTA per SM (room for the eigen-solve's CTAs beside it)
     struct MsEv {
         int pair, i0, n;  // event pair index into ms_events, first step, steps
     };
@@ -335,7 +337,7 @@ void kr_expm_small_eval(kr_handle* h, int dl, int kc, const double* Hdense, int 
 // large-k route (kr_large.cu): x_j = e^{H t_j} e_1 for the tridiagonal of local direction dl at dimension
 // kc, the coefficients c[j][.][d] of direction dl and the unit-vector Lemma 1 bound (returned; 0 with
 // zero_bound, an exact breakdown); fin also writes the direction's stats. Synchronises the stream.
-double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound);
+double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound, LzScalars* sc_out = nullptr);
 void kr_large_alloc(kr_handle* h, int kc);
 // kr_tridc.cu: the same for the symmetric Lanczos tridiagonal through a device divide-and-conquer eigen-solve
 // (coefficients of direction dl and e_kc^T x_j into hl); kc up to kr_tridc_max_k()

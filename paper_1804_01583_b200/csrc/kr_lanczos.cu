@@ -1564,7 +1564,9 @@ static void multistep_setup_t(kr_handle* h) {
     KR_CUDA(cudaGetDevice(&dev));
     KR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Geo2<TX, TY, 2>::NT, smem));
+    if (const char* e = getenv("KR_MS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     h->ms_grid = (int)std::min<int64_t>(h->slabs[0].nitems, (int64_t)sms * per_sm);
+    h->ms_one_per_sm = h->ms_grid <= sms;
     if (per_sm < 1 || h->ms_grid < 1) h->multistep = false;
 }
 

@@ -499,7 +499,7 @@ static void gemm(kr_handle* h, const double* A, const double* B, double* C, int 
 // unit-vector Lemma 1 bound. fin: also write stats (k_eff = kc, h_next, beta0 * bound) — the
 // coefficients of direction dl are always written (the last evaluation is the accepted one).
 // zero_bound: exact breakdown at kc (the approximation is exact): bound 0.
-double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
+double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound, LzScalars* sc_out) {
     const bool tri = h->path == PATH_FUSED_LANCZOS;  // Lanczos tridiagonal arrays, else dense Hessenberg H
     // symmetric tridiagonal: the device eigen-solve route (kr_tridc.cu, the oracle's eigendecomposition route) at
     // every checkpoint up to kr_tridc_max_k(); KR_LARGE_TAYLOR=1 keeps the Taylor + squaring route (and the one-CTA
@@ -644,9 +644,14 @@ double kr_large_eval(kr_handle* h, int dl, int kc, bool fin, bool zero_bound) {
     KR_CUDA(cudaGetLastError());
     h->launches++;
     KR_CUDA(cudaEventRecord(h->ev_lg1, st));
-    double b = 0.0;
-    KR_CUDA(cudaMemcpyAsync(&b, h->d_scratch + 1, 8, cudaMemcpyDeviceToHost, st));
+    if (!h->h_pin) KR_CUDA(cudaMallocHost(&h->h_pin, 256));
+    double* bp = reinterpret_cast<double*>(h->h_pin);
+    KR_CUDA(cudaMemcpyAsync(bp, h->d_scratch + 1, 8, cudaMemcpyDeviceToHost, st));
+    if (sc_out && tri)  // the direction's scalars in the same round trip (pinned: no staging)
+        KR_CUDA(cudaMemcpyAsync(bp + 1, h->d_sc + dl, sizeof(LzScalars), cudaMemcpyDeviceToHost, st));
     KR_CUDA(cudaStreamSynchronize(st));
+    const double b = bp[0];
+    if (sc_out && tri) memcpy(sc_out, bp + 1, sizeof(LzScalars));
     float ms = 0.f;
     KR_CUDA(cudaEventElapsedTime(&ms, h->ev_lg0, h->ev_lg1));
     if (getenv("KR_LARGE_PROF")) fprintf(stderr, "large_eval kc=%d %s %.1f us\n", kc, dc ? "tridc" : "taylor/small", ms * 1e3);

@@ -26,7 +26,8 @@ namespace {
 
 constexpr int NT = 256;  // threads per CTA
 constexpr int NW = NT / 32;
-constexpr int LOCAL = 32;  // node sizes handled by a warp per 32-block
+constexpr int LOCAL = 32;  // node sizes handled by a CTA per 32-block
+constexpr int LG = NT / LOCAL;  // lanes per entry in the 32-block levels
 constexpr int RMAX = 8;    // carried rows accumulated per pass in the rows update
 constexpr double EPSM = 0x1.0p-53;  // unit roundoff (LAPACK dlamch('E'))
 constexpr uint8_t F_SMALL = 1, F_MARK = 2;
@@ -107,26 +108,14 @@ __device__ __forceinline__ NodeArrays node_global(const DC& g, int q, int lo) {
                       g.rotN + lo, g.ninfo + 3 * q, g.nrho + q};
 }
 
-// ---- teams: one thread (small nodes) or the CTA (large nodes) ------------------------------------------------
-template <int T>
-struct Team;
-template <>
-struct Team<1> {
-    __device__ int rank() const { return 0; }
-    __device__ void sync() const {}
-    __device__ double max(double x) const { return x; }
-    __device__ bool any(bool x) const { return x; }
-    // exclusive prefix of x in rank order, total in *tot
-    __device__ int scan(int x, int* tot) const {
-        *tot = x;
-        return 0;
-    }
-};
-template <>
-struct Team<NT> {
+// ---- teams that merge one node: the CTA (large nodes) or a segment of w lanes of warp 0 (the nodes of a 32-block:
+// every lane of the warp calls in, each segment for its own node) ---------------------------------------------
+struct CtaTeam {
     double* rd;  // NW doubles
     int* ri;     // NW + 1 ints
     __device__ int rank() const { return threadIdx.x; }
+    __device__ int size() const { return NT; }
+    __device__ int span(int n) const { return n; }  // trip bound of loops containing team scans
     __device__ void sync() const { __syncthreads(); }
     __device__ double max(double x) const {
 #pragma unroll
@@ -139,6 +128,7 @@ struct Team<NT> {
         return m;
     }
     __device__ bool any(bool x) const { return __syncthreads_or(x) != 0; }
+    // exclusive prefix of x in rank order, total in *tot
     __device__ int scan(int x, int* tot) const {
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         int v = x;
@@ -157,6 +147,27 @@ struct Team<NT> {
         }
         *tot = all;
         return base + v - x;
+    }
+};
+struct SegTeam {
+    int w;  // segment width: a power of two <= 32
+    __device__ int rank() const { return (threadIdx.x & 31) & (w - 1); }
+    __device__ int size() const { return w; }
+    __device__ int span(int) const { return w; }  // one chunk for every segment: the same shuffles in all of them
+    __device__ void sync() const { __syncwarp(); }
+    __device__ double max(double x) const {
+        for (int o = w / 2; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+        return x;
+    }
+    __device__ bool any(bool x) const { return __any_sync(0xffffffffu, x); }  // warp-wide: one path for all segments
+    __device__ int scan(int x, int* tot) const {
+        int v = x;
+        for (int o = 1; o < w; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, v, o, w);
+            if (rank() >= o) v += y;
+        }
+        *tot = __shfl_sync(0xffffffffu, v, w - 1, w);
+        return v - x;
     }
 };
 
@@ -273,18 +284,18 @@ __device__ __forceinline__ void merge_entry(const DC& g, const double* lamIn, in
 // survivors p < q with rotation (c, s) zeroing z_p, |(d_q - d_p) c s| <= tol deflates p with the rotated pole
 // (chains: q's pole and z change and q is tested against the next survivor). The survivors go to na.dK / zK /
 // colK, the deflated to na.dval / dcol in ascending order, the rotations (in order) are applied to Wp.
-template <int T>
-__device__ void deflate(const DC& g, const Team<T>& tm, int n, double rho, int colLo, double* sA, double* sD,
+template <class TM>
+__device__ void deflate(const DC& g, const TM& tm, int n, double rho, int colLo, double* sA, double* sD,
                         double* sZ, int* sI, uint8_t* sF, const NodeArrays& na) {
     const int ld = g.ld, R = g.R;
     double mx = 0.0;
-    for (int i = tm.rank(); i < n; i += T) mx = fmax(mx, fmax(fabs(sD[i]), fabs(sZ[i])));
+    for (int i = tm.rank(); i < n; i += tm.size()) mx = fmax(mx, fmax(fabs(sD[i]), fabs(sZ[i])));
     mx = tm.max(mx);
     const double tol = 8.0 * EPSM * mx;
     // flags: small z; MARK: the rotation test against the next survivor passes on the unmodified values (only
     // then, or after a modification, does the sequential scan do any arithmetic)
     bool mark_any = false;
-    for (int i = tm.rank(); i < n; i += T) {
+    for (int i = tm.rank(); i < n; i += tm.size()) {
         uint8_t f = rho * fabs(sZ[i]) <= tol ? F_SMALL : 0;
         if (!f) {
             int j = i + 1;
@@ -303,7 +314,7 @@ __device__ void deflate(const DC& g, const Team<T>& tm, int n, double rho, int c
     if (!any) {
         // no rotation anywhere: keep the survivors, deflate the small ones, both already in sorted order
         int kept = 0, defl = 0;
-        for (int c0 = 0; c0 < n; c0 += T) {
+        for (int c0 = 0; c0 < tm.span(n); c0 += tm.size()) {
             const int i = c0 + tm.rank();
             const bool keep = i < n && !(sF[i] & F_SMALL);
             const bool dfl = i < n && (sF[i] & F_SMALL);
@@ -398,12 +409,12 @@ __device__ void deflate(const DC& g, const Team<T>& tm, int n, double rho, int c
     }
     tm.sync();
     const int ndf = na.info[1], nr = na.info[2];
-    for (int i = tm.rank(); i < ndf; i += T) {
+    for (int i = tm.rank(); i < ndf; i += tm.size()) {
         na.dval[i] = sA[i];
         na.dcol[i] = sI[i];
     }
     // rotations, in order, on the carried rows (DROT: x' = c x + s y, y' = c y - s x)
-    for (int rr = tm.rank(); rr < R; rr += T) {
+    for (int rr = tm.rank(); rr < R; rr += tm.size()) {
         double* w = g.Wp + (size_t)rr * ld;
         for (int r = 0; r < nr; ++r) {
             const int a = na.rotP[r], bb = na.rotN[r];
@@ -425,61 +436,59 @@ __device__ unsigned long long* g_prof_iters;  // KR_TRIDC_PROF: secular iteratio
 // nearest poles, the quadratic's near root taken (Li's "middle way", as dlaed4), a bisection step whenever it
 // leaves the bracket; stop when |f| is below its rounding bound.
 template <int G>
-__device__ void secular_root(const double* d, const double* z, int K, double rho, int j, int lane, double* dorg_o,
-                             double* tau_o) {
+__device__ void secular_root(const double* d, const double* z, int K, double rho, int j, int lane, bool active,
+                             double* dorg_o, double* tau_o) {
+    // every group of the warp runs the same loop (warp-wide shuffles and exit vote): inactive groups and K = 1
+    // (root d_0 + rho z_0^2, exact) start frozen
     const long long c_start = clock64();
-    if (K == 1) {
-        *dorg_o = d[0];
-        *tau_o = rho * z[0] * z[0];
-        return;
-    }
-    int org, p1;
-    double lo, hi;
-    if (j < K - 1) {
-        const double mid = 0.5 * (d[j + 1] - d[j]);
-        double s = 0.0;
-        for (int i0 = 0; i0 < K; i0 += G) {  // uniform trip count: the shuffles below see a converged warp
+    const bool solve = active && K > 1;
+    const bool interior = solve && j < K - 1;
+    int org = 0, p1 = 0;
+    double lo = 0.0, hi = 0.0;
+    {
+        const double mid = interior ? 0.5 * (d[j + 1] - d[j]) : 0.0;
+        const int Ki = interior ? K : 0;
+        double sm = 0.0;
+        for (int i0 = 0; i0 < Ki; i0 += G) {
             const int i = i0 + lane;
-            if (i < K) s += z[i] * z[i] * frcp((d[i] - d[j]) - mid);
+            if (i < Ki) sm += z[i] * z[i] * frcp((d[i] - d[j]) - mid);
         }
-        const double fm = 1.0 + rho * gsum<G>(s);
-        if (fm > 0.0) {
-            org = j;
-            lo = 0.0;
-            hi = mid;
-        } else {
-            org = j + 1;
-            lo = -mid;
-            hi = 0.0;
+        const double fm = 1.0 + rho * gsum<G>(sm);
+        if (interior) {
+            if (fm > 0.0) {
+                org = j;
+                hi = mid;
+            } else {
+                org = j + 1;
+                lo = -mid;
+            }
+            p1 = j;
+        } else if (solve) {
+            org = K - 1;
+            hi = rho;
+            p1 = K - 2;
         }
-        p1 = j;
-    } else {
-        org = K - 1;
-        lo = 0.0;
-        hi = rho;
-        p1 = K - 2;
     }
     const int p2 = p1 + 1;
-    const double dorg = d[org];
-    const double dl1 = d[p1] - dorg, dl2 = d[p2] - dorg;
+    const double dorg = solve ? d[org] : 0.0;
+    const double dl1 = solve ? d[p1] - dorg : 0.0, dl2 = solve ? d[p2] - dorg : 0.0;
+    const int Ks = solve ? K : 0;
     double tau = 0.5 * (lo + hi);
     int it = 0;
+    bool fin = !solve;
     for (; it < 200; ++it) {
         double s1 = 0.0, s2 = 0.0, q1 = 0.0, q2 = 0.0, ea = 0.0;
 #pragma unroll 4
-        for (int i0 = 0; i0 < K; i0 += G) {
-            const int i = i0 + lane;
-            if (i < K) {
-                const double r = frcp((d[i] - dorg) - tau);
-                const double t = rho * z[i] * z[i] * r;
-                const double tq = t * r;
-                const bool left = i <= p1;
-                ea += fabs(t);
-                s1 += left ? t : 0.0;
-                q1 += left ? tq : 0.0;
-                s2 += left ? 0.0 : t;
-                q2 += left ? 0.0 : tq;
-            }
+        for (int i = lane; i < Ks; i += G) {
+            const double r = frcp((d[i] - dorg) - tau);
+            const double t = rho * z[i] * z[i] * r;
+            const double tq = t * r;
+            const bool left = i <= p1;
+            ea += fabs(t);
+            s1 += left ? t : 0.0;
+            q1 += left ? tq : 0.0;
+            s2 += left ? 0.0 : t;
+            q2 += left ? 0.0 : tq;
         }
         double v5[5] = {s1, s2, q1, q2, ea};
         gsumN<G, 5>(v5);
@@ -489,31 +498,40 @@ __device__ void secular_root(const double* d, const double* z, int K, double rho
         q2 = v5[3];
         ea = v5[4];
         const double f = 1.0 + s1 + s2;
-        // every lane holds the same sums: the exits below are warp-uniform (told to the compiler by the votes)
-        if (G > 1 ? __all_sync(0xffffffffu, fabs(f) <= 8.0 * EPSM * (1.0 + ea)) : fabs(f) <= 8.0 * EPSM * (1.0 + ea)) break;
-        if (f > 0.0) hi = tau; else lo = tau;
-        // the matched pole terms b / (pole - tau) with b = q (pole - tau)^2: a = s - q (pole - tau), no division
-        const double D1 = dl1 - tau, D2 = dl2 - tau;
-        const double a1 = s1 - q1 * D1, a2 = s2 - q2 * D2;
-        const double b1 = q1 * D1 * D1, b2 = q2 * D2 * D2;
-        const double c = 1.0 + a1 + a2;
-        const double B = c * (D1 + D2) + b1 + b2;
-        const double C = D1 * D2 * f;
-        double eta;
-        if (c == 0.0) {
-            eta = C * frcp(B);
-        } else {
-            const double disc = fmax(B * B - 4.0 * c * C, 0.0);
-            eta = 2.0 * C * frcp(B + copysign(sqrt(disc), B));
+        // converged groups freeze; the loop ends when every group of the warp has (one warp-uniform exit, so the
+        // shuffles always see the whole warp)
+        if (!fin && fabs(f) <= 8.0 * EPSM * (1.0 + ea)) fin = true;
+        if (!fin) {
+            if (f > 0.0) hi = tau; else lo = tau;
+            // the matched pole terms b / (pole - tau) with b = q (pole - tau)^2: a = s - q (pole - tau), no division
+            const double D1 = dl1 - tau, D2 = dl2 - tau;
+            const double a1 = s1 - q1 * D1, a2 = s2 - q2 * D2;
+            const double b1 = q1 * D1 * D1, b2 = q2 * D2 * D2;
+            const double c = 1.0 + a1 + a2;
+            const double B = c * (D1 + D2) + b1 + b2;
+            const double C = D1 * D2 * f;
+            double eta;
+            if (c == 0.0) {
+                eta = C * frcp(B);
+            } else {
+                const double disc = fmax(B * B - 4.0 * c * C, 0.0);
+                eta = 2.0 * C * frcp(B + copysign(sqrt(disc), B));
+            }
+            double tn = tau + eta;
+            if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
+            if (tn == tau) fin = true;
+            tau = tn;
         }
-        double tn = tau + eta;
-        if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
-        if (G > 1 ? __all_sync(0xffffffffu, tn == tau) : tn == tau) break;
-        tau = tn;
+        if (__all_sync(0xffffffffu, fin)) break;
     }
-    *dorg_o = dorg;
-    *tau_o = tau;
-    if (g_prof_iters && lane == 0) {
+    if (active && K == 1) {
+        *dorg_o = d[0];
+        *tau_o = rho * z[0] * z[0];
+    } else {
+        *dorg_o = dorg;
+        *tau_o = tau;
+    }
+    if (g_prof_iters && lane == 0 && solve) {
         atomicAdd(g_prof_iters, (unsigned long long)it);
         atomicAdd(g_prof_iters + 1, 1ull);
         atomicMax(g_prof_iters + 2, (unsigned long long)it);
@@ -529,16 +547,14 @@ __device__ void secular_root(const double* d, const double* z, int K, double rho
 // ---- Gu-Eisenstat z_x^2 = prod_j (lam_j - d_x) / (rho prod_{j != x} (d_j - d_x)), lam_j - d_x = (dorg_j - d_x) + tau_j
 template <int G>
 __device__ __forceinline__ double gu_eisenstat_z(const double* d, const double* dorg, const double* tau, int K,
-                                                 double rho, double zsign, int x, int lane) {
-    const double dx = d[x];
+                                                 double rho, double zsign, int x, int lane, bool active = true) {
+    const int Ke = active ? K : 0;
+    const double dx = active ? d[x] : 0.0;
     double p = 1.0;
 #pragma unroll 4
-    for (int j0 = 0; j0 < K; j0 += G) {
-        const int j = j0 + lane;
-        if (j < K) {
-            const double lj = (dorg[j] - dx) + tau[j];
-            p *= lj * frcp(j == x ? rho : d[j] - dx);
-        }
+    for (int j = lane; j < Ke; j += G) {
+        const double lj = (dorg[j] - dx) + tau[j];
+        p *= lj * frcp(j == x ? rho : d[j] - dx);
     }
     p = gprod<G>(p);
     return copysign(sqrt(fmax(p, 0.0)), zsign);
@@ -548,17 +564,16 @@ __device__ __forceinline__ double gu_eisenstat_z(const double* d, const double* 
 // STAGED: the K source columns are in shared memory as src[r * sld + i]; else read from Wp through colK.
 template <int G, bool STAGED>
 __device__ __forceinline__ void eigvec_rows(const DC& g, const double* d, const double* zh, const int* colK,
-                                            const double* src, int sld, int K, double dorg, double tj, int dst,
-                                            int lane) {
+                                            const double* src, int sld, int Kn, double dorg, double tj, int dst,
+                                            int lane, bool active = true) {
+    const int K = active ? Kn : 0;  // inactive groups run the same reductions and write nothing
     double nrm = 0.0;
     for (int r0 = 0; r0 < g.R; r0 += RMAX) {
         double acc[RMAX];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r) acc[r] = 0.0;
 #pragma unroll 4
-        for (int i0 = 0; i0 < K; i0 += G) {
-            const int i = i0 + lane;
-            if (i >= K) continue;
+        for (int i = lane; i < K; i += G) {
             const double u = zh[i] * frcp((d[i] - dorg) - tj);
             if (r0 == 0) nrm = fma(u, u, nrm);
             if (STAGED) {
@@ -581,7 +596,7 @@ __device__ __forceinline__ void eigvec_rows(const DC& g, const double* d, const 
         const double inv = 1.0 / sqrt(nrm);
 #pragma unroll
         for (int r = 0; r < RMAX; ++r)
-            if (r0 + r < g.R && lane == 0) g.W[(size_t)(r0 + r) * g.ld + dst] = v[r] * inv;
+            if (active && r0 + r < g.R && lane == 0) g.W[(size_t)(r0 + r) * g.ld + dst] = v[r] * inv;
     }
 }
 
@@ -613,105 +628,113 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
     grid.sync();
     stamp(g, ps);
 
-    // ---- levels s = 2 .. 32: a warp per 32-block, everything but the rows in the warp's shared memory: a lane
-    // per entry (merge, roots, z, rows), a lane per node (deflation)
+    // ---- levels s = 2 .. 32: a CTA per 32-block, everything but the rows in shared memory: merge a lane of warp 0
+    // per entry, deflation a segment of s lanes of warp 0 per node, roots / z / rows a group of LG lanes per entry
     {
         constexpr int L = LOCAL;
-        double* wsm = smem + (size_t)wib * LOC_D * L;
+        double* wsm = smem;
         double *sLam = wsm, *sA = wsm + L, *sD = wsm + 2 * L, *sZ = wsm + 3 * L;
         double *nK = wsm + 4 * L, *nZ = wsm + 5 * L, *nOrg = wsm + 6 * L, *nTau = wsm + 7 * L, *nLamR = wsm + 8 * L,
                *nZh = wsm + 9 * L, *nDv = wsm + 10 * L, *nRc = wsm + 11 * L, *nRs = wsm + 12 * L, *nRho = wsm + 13 * L,
                *sRows = wsm + 14 * L;  // [RMAX][L]
-        int* wis = reinterpret_cast<int*>(smem + (size_t)NW * LOC_D * L) + wib * LOC_I * L;
+        int* wis = reinterpret_cast<int*>(smem + (size_t)LOC_D * L);
         int *sI = wis, *nCol = wis + L, *nDc = wis + 2 * L, *nRp = wis + 3 * L, *nRn = wis + 4 * L,
             *nInfo = wis + 5 * L;  // 3 ints per node (<= 16 nodes)
-        uint8_t* sF = reinterpret_cast<uint8_t*>(reinterpret_cast<int*>(smem + (size_t)NW * LOC_D * L) + NW * LOC_I * L) +
-                      wib * L;
+        uint8_t* sF = reinterpret_cast<uint8_t*>(wis + LOC_I * L);
+        const int e = threadIdx.x / LG, gl = threadIdx.x % LG;  // entry of the group, lane in the group
         const int nblk = (kc + L - 1) / L;
-        for (int blk = gw; blk < nblk; blk += nwarps) {
+        for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
             const int b0 = blk * L;
-            const bool act = b0 + lane < kc;
-            if (act) sLam[lane] = g.lam[b0 + lane];
-            __syncwarp();
+            if (threadIdx.x < L && b0 + threadIdx.x < kc) sLam[threadIdx.x] = g.lam[b0 + threadIdx.x];
+            __syncthreads();
             int wps = 0;
-            wstamp(g, wps, gw);
+            if (gw == 0) wstamp(g, wps, 0);
             for (int s = 2; s <= L && s < 2 * kc; s <<= 1) {
-                const int loc = lane & ~(s - 1);  // the node's offset in the block
-                const int q = (b0 + loc) / s, nq = L / s;
-                const Node nd = node_of(q, s, kc);
-                const bool mg = act && nd.merges();
-                const int n = nd.hi - nd.lo, n1 = nd.m - nd.lo, i = lane - loc;
-                // per-node scalars at the node's offset; info and rho by the node's index in the block
-                const int nib = loc / s;
-                NodeArrays na{nK + loc,  nZ + loc,  nOrg + loc, nTau + loc, nLamR + loc, nZh + loc, nDv + loc,
-                              nRc + loc, nRs + loc, nCol + loc, nDc + loc,  nRp + loc,   nRn + loc,
-                              nInfo + 3 * nib, nRho + nib};
-                if (mg) {
-                    const double b = g.sc->beta[nd.m];
-                    merge_entry(g, sLam + loc, n, n1, b >= 0.0 ? 1.0 : -1.0, b0 + loc, i, sD + loc, sZ + loc);
-                }
-                __syncwarp();
-                wstamp(g, wps, gw);
-                if (lane < nq) {
-                    const int qq = b0 / s + lane;
-                    const Node nn = node_of(qq, s, kc);
-                    if (nn.lo < kc && nn.merges()) {
-                        const int off = lane * s;
-                        NodeArrays nb{nK + off,  nZ + off,  nOrg + off, nTau + off, nLamR + off, nZh + off, nDv + off,
-                                      nRc + off, nRs + off, nCol + off, nDc + off,  nRp + off,   nRn + off,
-                                      nInfo + 3 * lane, nRho + lane};
-                        deflate<1>(g, Team<1>{}, nn.hi - nn.lo, 2.0 * fabs(g.sc->beta[nn.m]), b0 + off, sA + off,
-                                   sD + off, sZ + off, sI + off, sF + off, nb);
-                    }
-                }
-                __syncwarp();
-                wstamp(g, wps, gw);
-                const int K = mg ? na.info[0] : 0, ndf = mg ? na.info[1] : 0;
-                if (mg && i < K) {
-                    double dorg, t;
-                    secular_root<1>(na.dK, na.zK, K, *na.rho, i, 0, &dorg, &t);
-                    na.dorg[i] = dorg;
-                    na.tau[i] = t;
-                    na.lamR[i] = dorg + t;
-                }
-                __syncwarp();
-                wstamp(g, wps, gw);
-                if (mg && i < K) {
-                    na.zh[i] = gu_eisenstat_z<1>(na.dK, na.dorg, na.tau, K, *na.rho, na.zK[i], i, 0);
-                } else if (mg && i < K + ndf) {
-                    const int dq = i - K;
-                    const double v = na.dval[dq];
-                    const int pos = dq + count_le(na.lamR, K, v);
-                    sLam[loc + pos] = v;
-                    const int col = na.dcol[dq];
-                    for (int rr = 0; rr < g.R; ++rr)
-                        g.W[(size_t)rr * ld + b0 + loc + pos] = g.Wp[(size_t)rr * ld + col];
-                }
-                __syncwarp();
-                wstamp(g, wps, gw);
-                if (g.R <= RMAX) {  // the node's source columns into the warp's shared memory, [r][loc + i]
-                    if (mg && i < K) {
-                        const int col = na.colK[i];
-                        for (int rr = 0; rr < g.R; ++rr) sRows[rr * L + loc + i] = g.Wp[(size_t)rr * ld + col];
+                // the node of entry p of the block: offset loc, index in the block nib
+                auto node_at = [&](int p, int& loc, Node& nd) {
+                    loc = p & ~(s - 1);
+                    nd = node_of((b0 + loc) / s, s, kc);
+                };
+                auto arrays = [&](int loc) {
+                    const int nib = loc / s;
+                    return NodeArrays{nK + loc,  nZ + loc,  nOrg + loc, nTau + loc, nLamR + loc, nZh + loc, nDv + loc,
+                                      nRc + loc, nRs + loc, nCol + loc, nDc + loc,  nRp + loc,   nRn + loc,
+                                      nInfo + 3 * nib, nRho + nib};
+                };
+                if (wib == 0) {
+                    int loc;
+                    Node nd;
+                    node_at(lane, loc, nd);
+                    const bool mg = b0 + lane < kc && nd.merges();
+                    if (mg) {
+                        const double b = g.sc->beta[nd.m];
+                        merge_entry(g, sLam + loc, nd.hi - nd.lo, nd.m - nd.lo, b >= 0.0 ? 1.0 : -1.0, b0 + loc,
+                                    lane - loc, sD + loc, sZ + loc);
                     }
                     __syncwarp();
+                    // every lane calls in (segment of its node; n = 0 where the node does not merge)
+                    const bool nm = b0 + loc < kc && nd.merges();
+                    deflate(g, SegTeam{s}, nm ? nd.hi - nd.lo : 0, nm ? 2.0 * fabs(g.sc->beta[nd.m]) : 0.0, b0 + loc,
+                            sA + loc, sD + loc, sZ + loc, sI + loc, sF + loc, arrays(loc));
                 }
-                if (mg && i < K) {
-                    const double lj = na.lamR[i];
-                    const int pos = i + count_lt(na.dval, ndf, lj);
-                    sLam[loc + pos] = lj;
+                __syncthreads();
+                if (gw == 0) wstamp(g, wps, 0);
+                int loc;
+                Node nd;
+                node_at(e, loc, nd);
+                const bool mg = b0 + e < kc && nd.merges();
+                const NodeArrays na = arrays(loc);
+                const int i = e - loc;
+                const int K = mg ? na.info[0] : 0, ndf = mg ? na.info[1] : 0;
+                {
+                    double dorg, t;
+                    secular_root<LG>(na.dK, na.zK, K, mg ? *na.rho : 1.0, i, gl, mg && i < K, &dorg, &t);
+                    if (mg && i < K && gl == 0) {
+                        na.dorg[i] = dorg;
+                        na.tau[i] = t;
+                        na.lamR[i] = dorg + t;
+                    }
+                }
+                __syncthreads();
+                if (gw == 0) wstamp(g, wps, 0);
+                {
+                    const double zx = gu_eisenstat_z<LG>(na.dK, na.dorg, na.tau, K, mg ? *na.rho : 1.0,
+                                                         mg && i < K ? na.zK[i] : 1.0, i, gl, mg && i < K);
+                    if (mg && i < K && gl == 0) na.zh[i] = zx;
+                    if (mg && i >= K && i < K + ndf) {  // deflated column: its place among the roots
+                        const int dq = i - K;
+                        const double v = na.dval[dq];
+                        const int pos = dq + count_le(na.lamR, K, v);
+                        if (gl == 0) sLam[loc + pos] = v;
+                        const int col = na.dcol[dq];
+                        for (int rr = gl; rr < g.R; rr += LG)
+                            g.W[(size_t)rr * ld + b0 + loc + pos] = g.Wp[(size_t)rr * ld + col];
+                    }
+                    if (g.R <= RMAX && mg && i < K)  // the node's source columns into shared memory, [r][loc + i]
+                        for (int rr = gl; rr < g.R; rr += LG) sRows[rr * L + loc + i] = g.Wp[(size_t)rr * ld + na.colK[i]];
+                }
+                __syncthreads();
+                if (gw == 0) wstamp(g, wps, 0);
+                {
+                    const bool act = mg && i < K;
+                    int pos = 0;
+                    if (act) {
+                        pos = i + count_lt(na.dval, ndf, na.lamR[i]);
+                        if (gl == 0) sLam[loc + pos] = na.lamR[i];
+                    }
+                    const double dorg = act ? na.dorg[i] : 0.0, tj = act ? na.tau[i] : 0.0;
                     if (g.R <= RMAX)
-                        eigvec_rows<1, true>(g, na.dK, na.zh, nullptr, sRows + loc, L, K, na.dorg[i], na.tau[i],
-                                             b0 + loc + pos, 0);
+                        eigvec_rows<LG, true>(g, na.dK, na.zh, nullptr, sRows + loc, L, K, dorg, tj, b0 + loc + pos, gl,
+                                              act);
                     else
-                        eigvec_rows<1, false>(g, na.dK, na.zh, na.colK, nullptr, 0, K, na.dorg[i], na.tau[i],
-                                              b0 + loc + pos, 0);
+                        eigvec_rows<LG, false>(g, na.dK, na.zh, na.colK, nullptr, 0, K, dorg, tj, b0 + loc + pos, gl,
+                                               act);
                 }
-                __syncwarp();
-                wstamp(g, wps, gw);
+                __syncthreads();
+                if (gw == 0) wstamp(g, wps, 0);
             }
-            if (act) g.lam[b0 + lane] = sLam[lane];
-            __syncwarp();
+            if (threadIdx.x < L && b0 + threadIdx.x < kc) g.lam[b0 + threadIdx.x] = sLam[threadIdx.x];
+            __syncthreads();
         }
     }
     __syncthreads();
@@ -722,7 +745,7 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
     // ---- levels s = 64 .. : merge + deflation a CTA per node (shared memory), then roots, z and rows by units of
     // NW entries of one node (a warp per entry) with the node's scalars staged in the CTA's shared memory;
     // a grid barrier between the four phases
-    Team<NT> team{red_d, red_i};
+    CtaTeam team{red_d, red_i};
     for (int s = 2 * LOCAL; s < 2 * kc; s <<= 1) {
         const int nq = (kc + s - 1) / s;
         const int sz = min(s, kc);  // the largest node of the level
@@ -740,7 +763,7 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             __syncthreads();
             for (int i = threadIdx.x; i < n; i += NT) merge_entry(g, sA, n, n1, b >= 0.0 ? 1.0 : -1.0, nd.lo, i, sD, sZ);
             __syncthreads();
-            deflate<NT>(g, team, n, 2.0 * fabs(b), nd.lo, sA, sD, sZ, sI, sF, node_global(g, q, nd.lo));
+            deflate(g, team, n, 2.0 * fabs(b), nd.lo, sA, sD, sZ, sI, sF, node_global(g, q, nd.lo));
         }
         __syncthreads();
     wend(g, ps);
@@ -764,7 +787,7 @@ __global__ void __launch_bounds__(NT) tridc_kernel(const DC g) {
             const int j = c0 + wib;
             if (j < K) {
                 double dorg, t;
-                secular_root<32>(sd, szz, K, g.nrho[q], j, lane, &dorg, &t);
+                secular_root<32>(sd, szz, K, g.nrho[q], j, lane, true, &dorg, &t);
                 if (lane == 0) {
                     g.dorg[nd.lo + j] = dorg;
                     g.tau[nd.lo + j] = t;
@@ -985,7 +1008,7 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
     // rows phases (4 doubles per entry), the warps' 32-blocks, the time-grid chunks
     g.lch = R > 16 ? 64 : 256;
     const size_t sm_top = kc > LOCAL ? (size_t)kc * 32 : 0;
-    const size_t sm_loc = (size_t)NW * LOCAL * (LOC_D * 8 + LOC_I * 4 + 1);
+    const size_t sm_loc = (size_t)LOCAL * (LOC_D * 8 + LOC_I * 4 + 1);
     const size_t sm_grid = (size_t)g.lch * R * 8;
     const size_t sm_rows = std::min<size_t>((size_t)kc * (8 * R + 28), 200 * 1024);  // staged rows of phase D
     const size_t smem = (std::max(std::max(std::max(sm_top, sm_loc), sm_grid), sm_rows) + 15) / 16 * 16;
