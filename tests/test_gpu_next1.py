@@ -301,3 +301,36 @@ def test_adaptive_paper_heat_m100_k544():
         assert abs(bg - bo) <= 1e-7 * abs(bo), (kg, bg, bo)
     assert 5.8e-7 <= checks[-1][1] < 6.0e-7  # the paper prints 5.8e-7
     assert_coeff(coeff, ref["coeff"], p["name"], atol=projection_envelope(r0["beta0"], r0["P"]))
+
+
+@pytest.mark.parametrize("env", [{"KR_MULTISTEP": "0"}, {"KR_MS_PER_SM": "1", "KR_MS_PIPE": "1"},
+                                 {"KR_MS_PER_SM": "1"}, {"KR_TY": "8"}])
+def test_adaptive_step_schedules(env, monkeypatch):
+    """The step-schedule switches of the Lanczos path — one launch per step (KR_MULTISTEP=0), the persistent
+    multi-step kernel at one CTA per SM with the checkpoint evaluations beside it (KR_MS_PER_SM=1 KR_MS_PIPE=1) or
+    in sequence (KR_MS_PER_SM=1), 64 x 8 tiles (KR_TY=8) — on Alg. 4 with the paper's heat model: the same
+    checkpoints, accepted k and bounds as the oracle, coefficients within parity."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    p = W.heat_paper(20, k_max=2000)
+    ref = oracle.krylov_project_adaptive(p)
+    r0 = ref["per_dir"][0]
+    coeff, stats, _, checks = gpu(p)
+    assert stats[0]["k_eff"] == r0["k_eff"]
+    assert [k for k, _ in checks] == [k for k, _ in r0["checks"]]
+    for (kg, bg), (ko, bo) in zip(checks, r0["checks"]):
+        assert abs(bg - bo) <= 1e-8 * abs(bo) + 1e-300, (kg, bg, bo)
+    assert_coeff(coeff, ref["coeff"], f"{p['name']} {env}")
+
+
+def test_multistep_equals_per_step_launches(monkeypatch):
+    """Fixed k = 30 on a 40^3 Dirichlet grid: the persistent multi-step kernel and one launch per step agree
+    within parity (their partial sums are reduced in different fixed orders) and with the oracle."""
+    p = W.heat(40, 4, 30, n_steps=200)
+    res = oracle.krylov_project(p)
+    a = gpu(p)
+    monkeypatch.setenv("KR_MULTISTEP", "0")
+    b = gpu(p)
+    assert_coeff(a[0], b[0], "multistep vs per-step")
+    assert_coeff(a[0], res["coeff"], "multistep vs oracle")
+    assert a[1][0]["k_eff"] == b[1][0]["k_eff"] == res["per_dir"][0]["k_eff"]
