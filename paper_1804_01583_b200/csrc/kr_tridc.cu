@@ -443,37 +443,27 @@ __device__ void secular_root(const double* d, const double* z, int K, double rho
     const long long c_start = clock64();
     const bool solve = active && K > 1;
     const bool interior = solve && j < K - 1;
+    // interior root: the first pass is at the midpoint of (d_j, d_{j+1}) with the origin at d_j; its sign picks
+    // the half and the origin (the nearer pole) and its sums feed the first rational step. Last root: origin
+    // d_{K-1}, bracket (0, rho].
     int org = 0, p1 = 0;
-    double lo = 0.0, hi = 0.0;
-    {
-        const double mid = interior ? 0.5 * (d[j + 1] - d[j]) : 0.0;
-        const int Ki = interior ? K : 0;
-        double sm = 0.0;
-        for (int i0 = 0; i0 < Ki; i0 += G) {
-            const int i = i0 + lane;
-            if (i < Ki) sm += z[i] * z[i] * frcp((d[i] - d[j]) - mid);
-        }
-        const double fm = 1.0 + rho * gsum<G>(sm);
-        if (interior) {
-            if (fm > 0.0) {
-                org = j;
-                hi = mid;
-            } else {
-                org = j + 1;
-                lo = -mid;
-            }
-            p1 = j;
-        } else if (solve) {
-            org = K - 1;
-            hi = rho;
-            p1 = K - 2;
-        }
+    double lo = 0.0, hi = 0.0, tau = 0.0, gap = 0.0;
+    if (interior) {
+        org = j;
+        p1 = j;
+        gap = d[j + 1] - d[j];
+        hi = gap;
+        tau = 0.5 * gap;
+    } else if (solve) {
+        org = K - 1;
+        p1 = K - 2;
+        hi = rho;
+        tau = 0.5 * rho;
     }
     const int p2 = p1 + 1;
-    const double dorg = solve ? d[org] : 0.0;
-    const double dl1 = solve ? d[p1] - dorg : 0.0, dl2 = solve ? d[p2] - dorg : 0.0;
+    double dorg = solve ? d[org] : 0.0;
+    double dl1 = solve ? d[p1] - dorg : 0.0, dl2 = solve ? d[p2] - dorg : 0.0;
     const int Ks = solve ? K : 0;
-    double tau = 0.5 * (lo + hi);
     int it = 0;
     bool fin = !solve;
     for (; it < 200; ++it) {
@@ -503,6 +493,14 @@ __device__ void secular_root(const double* d, const double* z, int K, double rho
         if (!fin && fabs(f) <= 8.0 * EPSM * (1.0 + ea)) fin = true;
         if (!fin) {
             if (f > 0.0) hi = tau; else lo = tau;
+            if (it == 0 && interior && f <= 0.0) {  // root in the upper half: origin d_{j+1} (shift by the gap)
+                tau -= gap;
+                lo -= gap;
+                hi = 0.0;
+                dl1 -= gap;
+                dl2 = 0.0;
+                dorg = d[j + 1];
+            }
             // the matched pole terms b / (pole - tau) with b = q (pole - tau)^2: a = s - q (pole - tau), no division
             const double D1 = dl1 - tau, D2 = dl2 - tau;
             const double a1 = s1 - q1 * D1, a2 = s2 - q2 * D2;
@@ -518,8 +516,10 @@ __device__ void secular_root(const double* d, const double* z, int K, double rho
                 eta = 2.0 * C * frcp(B + copysign(sqrt(disc), B));
             }
             double tn = tau + eta;
-            if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
-            if (tn == tau) fin = true;
+            const bool bis = !(tn > lo && tn < hi) || !isfinite(tn);
+            if (bis) tn = 0.5 * (lo + hi);
+            // a rational step below 1e-10 of the offset: the next one (quadratic convergence) is below rounding
+            if (tn == tau || (!bis && fabs(eta) <= 1e-10 * fabs(tn))) fin = true;
             tau = tn;
         }
         if (__all_sync(0xffffffffu, fin)) break;
