@@ -1428,7 +1428,10 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                     if (getenv("KR_SPECULATE")) pipe = true;
                     // two cooperative kernels (the multi-step steps and the eigen-solve) run side by side only when
                     // both grids fit the GPU together (the multi-step kernel at one CTA per SM, KR_MS_PIPE=1)
-                    if (h->multistep && !(h->ms_one_per_sm && getenv("KR_MS_PIPE"))) pipe = false;
+                    // (the multi-step grid at one CTA per SM with KR_MS_PIPE=1, or at two per SM when it leaves >= 8
+                    // half-SM slots free for the evaluation, which then runs on those slots only)
+                    const bool ms_pipe = h->ms_free_slots >= 8 && !getenv("KR_MS_SEQ");
+                    if (h->multistep && !(h->ms_one_per_sm && getenv("KR_MS_PIPE")) && !ms_pipe) pipe = false;
                     bool by_bound = false;
                     int kc = 4;
                     while (kc <= h->k) {
@@ -1461,13 +1464,16 @@ kr_status krylov_project(kr_handle* h, double* coeff, kr_dir_stats* stats) {
                             if (i < kn) kr_lz_enqueue_steps(h, dl, i + 1, kn, h->timing);  // speculative
                             i = std::max(i, kn);
                             std::swap(h->stream, h->stream2);
+                            h->tdc_grid_cap = (h->multistep && !h->ms_one_per_sm) ? h->ms_free_slots : 0;
                             try {
                                 KR_CUDA(cudaStreamWaitEvent(h->stream, h->ev_spec, 0));
                                 b = kr_large_eval(h, dl, kc, true, false);
                             } catch (...) {
+                                h->tdc_grid_cap = 0;
                                 std::swap(h->stream, h->stream2);
                                 throw;
                             }
+                            h->tdc_grid_cap = 0;
                             std::swap(h->stream, h->stream2);
                         } else {
                             b = have_b ? b_seq : kr_large_eval(h, dl, kc, true, false);

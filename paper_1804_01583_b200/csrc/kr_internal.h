@@ -250,6 +250,8 @@ struct kr_handle {
     bool multistep = false;  // Lanczos steps >= 3 by the persistent multi-step kernel (single L2-resident slab)
     int ms_grid = 0;         // its cooperative grid
     bool ms_one_per_sm = false;  // ... at most one CTA per SM (room for the eigen-solve's CTAs beside it)
+    int ms_free_slots = 0;       // SM slots (half an SM each) a multi-step launch at two CTAs per SM leaves free
+    int tdc_grid_cap = 0;        // > 0: the eigen-solve runs beside a multi-step launch on at most this many CTAs
     struct MsEv {
         int pair, i0, n;  // event pair index into ms_events, first step, steps
     };

@@ -1567,6 +1567,9 @@ static void multistep_setup_t(kr_handle* h) {
     if (const char* e = getenv("KR_MS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     h->ms_grid = (int)std::min<int64_t>(h->slabs[0].nitems, (int64_t)sms * per_sm);
     h->ms_one_per_sm = h->ms_grid <= sms;
+    // both the multi-step kernel and the eigen-solve are half-SM CTAs (<= 128 registers x 256 threads): with the
+    // multi-step grid at two per SM, the rest of the 2 x SMs slots can host the checkpoint evaluation beside it
+    h->ms_free_slots = per_sm == 2 ? 2 * sms - h->ms_grid : 0;
     if (per_sm < 1 || h->ms_grid < 1) h->multistep = false;
 }
 

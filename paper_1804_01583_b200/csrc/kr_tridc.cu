@@ -1024,7 +1024,15 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
     KR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tridc_kernel, NT, smem));
     if (per_sm < 1) KR_THROW(KR_ECUDA, "tridc_kernel does not fit on an SM");
     const int64_t want = std::max<int64_t>((kc + NW - 1) / NW, (h->n_steps + NW - 1) / NW);
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::min(per_sm, 2)));
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::min(per_sm, 2)));
+    // beside a running multi-step launch: only the SM slots it leaves free (both kernels take half an SM each;
+    // with more than 100 KB of shared memory two of these CTAs may not share an SM: wait for the steps instead)
+    if (h->tdc_grid_cap > 0 && smem > 100 * 1024) {
+        KR_CUDA(cudaStreamSynchronize(h->stream2));  // the main stream (swapped) holding the multi-step launch
+    } else if (h->tdc_grid_cap > 0) {
+        if (per_sm < 2) KR_THROW(KR_ECUDA, "eigen-solve beside the multi-step kernel needs two CTAs per SM");
+        nb = std::min(nb, h->tdc_grid_cap);
+    }
     static unsigned long long* prof = nullptr;
     const bool want_prof = getenv("KR_TRIDC_PROF") != nullptr;
     if (want_prof && !prof) {
