@@ -304,11 +304,12 @@ def test_adaptive_paper_heat_m100_k544():
 
 
 @pytest.mark.parametrize("env", [{"KR_MULTISTEP": "0"}, {"KR_MS_PER_SM": "1", "KR_MS_PIPE": "1"},
-                                 {"KR_MS_PER_SM": "1"}, {"KR_TY": "8"}])
+                                 {"KR_MS_PER_SM": "1"}, {"KR_MS_SEQ": "1"}, {"KR_TY": "8"}])
 def test_adaptive_step_schedules(env, monkeypatch):
     """The step-schedule switches of the Lanczos path — one launch per step (KR_MULTISTEP=0), the persistent
     multi-step kernel at one CTA per SM with the checkpoint evaluations beside it (KR_MS_PER_SM=1 KR_MS_PIPE=1) or
-    in sequence (KR_MS_PER_SM=1), 64 x 8 tiles (KR_TY=8) — on Alg. 4 with the paper's heat model: the same
+    in sequence (KR_MS_PER_SM=1), the default two-CTA-per-SM grid with sequential checkpoints (KR_MS_SEQ=1; by
+    default they run on the slots it leaves free), 64 x 8 tiles (KR_TY=8) — on Alg. 4 with the paper's heat model: the same
     checkpoints, accepted k and bounds as the oracle, coefficients within parity."""
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
