@@ -926,8 +926,15 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
         grid.sync();
         // all partials, fixed order (lane-strided sums, xor tree): the same bits in every CTA
         for (int q = wid; q < nqp; q += NWp) {
-            double v = 0.0;
-            for (int b = lane; b < nblk; b += 32) v += __ldcg(part + (size_t)q * nblk + b);
+            // four independent loads in flight per lane (L2 round trips, not adds, bound this), summed in a fixed order
+            double v4[4] = {0.0, 0.0, 0.0, 0.0};
+            const double* pq = part + (size_t)q * nblk;
+            for (int b = lane; b < nblk; b += 128) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (b + 32 * u < nblk) v4[u] += __ldcg(pq + b + 32 * u);
+            }
+            double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (lane == 0) qsum[q] = v;

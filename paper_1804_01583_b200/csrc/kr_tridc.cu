@@ -253,6 +253,8 @@ __device__ __forceinline__ Node node_of(int q, int s, int kc) {
     return n;
 }
 
+__device__ unsigned long long* g_prof_iters;  // KR_TRIDC_PROF: secular iterations (sum, roots, max), deflation scans
+
 // ---- merge step 1: the children's sorted lists merged, z, the rows permuted ---------------------------------
 // Children eigenvalues lamIn[0..n1), lamIn[n1..n) (each ascending) and rows in g.W at columns colLo + i. The
 // tearing at the split (first index m of the right child) subtracts |b| from both adjacent diagonal entries (done
@@ -406,6 +408,10 @@ __device__ void deflate(const DC& g, const TM& tm, int n, double rho, int colLo,
         na.info[1] = nd;
         na.info[2] = nr;
         *na.rho = rho;
+        if (g_prof_iters) {  // KR_TRIDC_PROF: nodes through the sequential scan, rotations
+            atomicAdd(g_prof_iters + 7, 1ull);
+            atomicAdd(g_prof_iters + 8, (unsigned long long)nr);
+        }
     }
     tm.sync();
     const int ndf = na.info[1], nr = na.info[2];
@@ -427,7 +433,6 @@ __device__ void deflate(const DC& g, const TM& tm, int n, double rho, int colLo,
     tm.sync();
 }
 
-__device__ unsigned long long* g_prof_iters;  // KR_TRIDC_PROF: secular iterations (sum, roots, max)
 
 // ---- secular root j of f(lam) = 1 + rho sum_i z_i^2 / (d_i - lam), d ascending, rho > 0 -------------------------
 // Root j < K-1 lies in (d_j, d_{j+1}), the last in (d_{K-1}, d_{K-1} + rho |z|^2]. It is represented as
@@ -1040,7 +1045,7 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
         unsigned long long* pi = prof + 200;
         KR_CUDA(cudaMemcpyToSymbol(g_prof_iters, &pi, sizeof(pi)));
     }
-    if (want_prof) KR_CUDA(cudaMemsetAsync(prof + 150, 0, 58 * 8, h->stream));
+    if (want_prof) KR_CUDA(cudaMemsetAsync(prof + 150, 0, 60 * 8, h->stream));
     g.prof = want_prof ? prof : nullptr;
     void* args[] = {(void*)&g};
     KR_CUDA(cudaLaunchCooperativeKernel((const void*)tridc_kernel, dim3(nb), dim3(NT), args, smem, h->stream));
@@ -1057,6 +1062,6 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
         for (int i = 1; i <= n; ++i) fprintf(stderr, " %.1f", ((long long)t[150 + i] - (long long)t[i - 1]) * 1e-3);
         fprintf(stderr, " | warp 0 local:");
         for (int i = 101; i < 126; ++i) fprintf(stderr, " %.1f", (t[i] - t[i - 1]) * 1e-3);
-        fprintf(stderr, " | secular iterations %llu over %llu roots, max %llu; cycles/root %.0f; warp roots %llu: cycles %.0f, K %.0f\n", t[200], t[201], t[202], (double)t[203] / t[201], t[205], (double)t[204] / (t[205] ? t[205] : 1), (double)t[206] / (t[205] ? t[205] : 1));
+        fprintf(stderr, " | secular iterations %llu over %llu roots, max %llu; cycles/root %.0f; warp roots %llu: cycles %.0f, K %.0f; sequential deflation scans %llu, rotations %llu\n", t[200], t[201], t[202], (double)t[203] / t[201], t[205], (double)t[204] / (t[205] ? t[205] : 1), (double)t[206] / (t[205] ? t[205] : 1), t[207], t[208]);
     }
 }
