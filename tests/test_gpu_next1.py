@@ -335,3 +335,22 @@ def test_multistep_equals_per_step_launches(monkeypatch):
     assert_coeff(a[0], b[0], "multistep vs per-step")
     assert_coeff(a[0], res["coeff"], "multistep vs oracle")
     assert a[1][0]["k_eff"] == b[1][0]["k_eff"] == res["per_dir"][0]["k_eff"]
+
+
+def test_adaptive_many_output_rows():
+    """Alg. 4 with 8 box output rows (the fused kernel's maximum; 10 carried rows in the eigen-solve: more than one
+    register pass of 8, and no staged rows in the 32-block levels) on the multi-step path: same checkpoints,
+    accepted k and bounds as the oracle, every row within parity."""
+    p = W.heat_paper(20, k_max=2000)
+    m = 20
+    p["outs"] = [W.box((0, 0, 0), (m, m, m)), W.box((0, 0, 0), (5, 5, 5)), W.box((10, 3, 2), (14, 9, 7), 0.5),
+                 W.point(19, 19, 19), W.point(0, 19, 10), W.box((2, 2, 2), (18, 18, 18), -1.0),
+                 W.point(7, 7, 7), W.box((0, 0, 19), (20, 20, 20))]
+    ref = oracle.krylov_project_adaptive(p)
+    r0 = ref["per_dir"][0]
+    coeff, stats, _, checks = gpu(p)
+    assert stats[0]["k_eff"] == r0["k_eff"]
+    assert [k for k, _ in checks] == [k for k, _ in r0["checks"]]
+    for (kg, bg), (ko, bo) in zip(checks, r0["checks"]):
+        assert abs(bg - bo) <= 1e-8 * abs(bo) + 1e-300, (kg, bg, bo)
+    assert_coeff(coeff, ref["coeff"], "adaptive 8 rows", atol=projection_envelope(r0["beta0"], r0["P"]))
