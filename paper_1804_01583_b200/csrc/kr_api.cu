@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <utility>
@@ -952,7 +953,19 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         h->k = p->k;
         h->n_steps = p->n_steps;
         h->step = p->step;
-        h->mu = gershgorin_mu(p);
+        // Gershgorin mu of a CSR matrix (O(nnz log), 2.6 ms at C2's 240k entries) on a host thread beside the rest
+        // of the set-up; joined before create returns (the guard joins on every exit path)
+        struct Joiner {
+            std::thread t;
+            ~Joiner() {
+                if (t.joinable()) t.join();
+            }
+        } mu_job;
+        double mu_val = 0.0;
+        if (p->op == KR_OP_CSR && p->nnz > 20000)
+            mu_job.t = std::thread([&mu_val, p] { mu_val = gershgorin_mu(p); });
+        else
+            h->mu = gershgorin_mu(p);
         tr.mark("gershgorin mu");
         h->device = p->device;
         KR_CUDA(cudaSetDevice(p->device));
@@ -1271,6 +1284,10 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
         // all set-up work (zeroing of the state buffers, descriptors) ran on h->stream, which does not
         // synchronise with the legacy default stream: finish it before the handle is used
         KR_CUDA(cudaStreamSynchronize(h->stream));
+        if (mu_job.t.joinable()) {
+            mu_job.t.join();
+            h->mu = mu_val;
+        }
         tr.mark("final sync");
         *out = h;
     });
