@@ -1018,11 +1018,9 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
     const size_t sm_rows = std::min<size_t>((size_t)kc * (8 * R + 28), 200 * 1024);  // staged rows of phase D
     const size_t smem = (std::max(std::max(std::max(sm_top, sm_loc), sm_grid), sm_rows) + 15) / 16 * 16;
     g.smem_bytes = smem;
-    static size_t smem_set = 0;
-    if (smem > 48 * 1024 && smem > smem_set) {
+    // the attribute belongs to the current device's context: set it on every call (handles on several GPUs)
+    if (smem > 48 * 1024)
         KR_CUDA(cudaFuncSetAttribute(tridc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
-    }
     int dev = 0, sms = 148, per_sm = 0;
     KR_CUDA(cudaGetDevice(&dev));
     KR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1038,7 +1036,7 @@ void kr_tridc_eval(kr_handle* h, int dl, int kc, double* hl, int ndl_stride) {
         if (per_sm < 2) KR_THROW(KR_ECUDA, "eigen-solve beside the multi-step kernel needs two CTAs per SM");
         nb = std::min(nb, h->tdc_grid_cap);
     }
-    static unsigned long long* prof = nullptr;
+    static unsigned long long* prof = nullptr;  // KR_TRIDC_PROF diagnostics only (first device used)
     const bool want_prof = getenv("KR_TRIDC_PROF") != nullptr;
     if (want_prof && !prof) {
         KR_CUDA(cudaMalloc(&prof, 256 * 8));

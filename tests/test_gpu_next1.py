@@ -245,13 +245,14 @@ def test_adaptive_speculative_steps_match_sequential(vs, monkeypatch):
     assert a[3] == b[3]
 
 
-@pytest.mark.parametrize("k,m", [(65, 24), (200, 12), (400, 12), (700, 16)])
+@pytest.mark.parametrize("k,m", [(65, 24), (200, 12), (400, 12), (700, 16), (4500, 20)])
 def test_tridc_route_on_own_tridiagonal(k, m):
     """kr_tridc.cu (device divide and conquer, carried rows e_1^T Q, e_k^T Q, P Q) against the oracle's eigh
     route on the same tridiagonal: fixed k on small Dirichlet grids, where k well past the point of lost
     orthogonality (k = 400, 700 on 1728 / 4096 states) fills the tridiagonal with ghost copies of converged
-    eigenvalues — the deflation (small z and close-pole rotations) paths. Coefficients within parity, Lemma 1
-    to 1e-8."""
+    eigenvalues — the deflation (small z and close-pole rotations) paths; k = 4500 (13 levels, the top merges with
+    the rows read from global memory, ~180 KB of shared memory per CTA). Coefficients within parity, Lemma 1 to
+    1e-8."""
     from paper_1804_01583_b200 import KrylovReach
     p = W.heat(m, 3, k, n_steps=300)
     with KrylovReach(p) as h:
