@@ -1155,7 +1155,11 @@ void encode(CUtensorMap* tm, double* base, int64_t mx, int64_t my, int64_t nplan
 
 template <int TX, int TY>
 struct Stages {
+#ifdef KR_STAGES
+    static constexpr int S = KR_STAGES;
+#else
     static constexpr int S = (TX * TY > 512) ? 4 : 5;
+#endif
 };
 
 }  // namespace
