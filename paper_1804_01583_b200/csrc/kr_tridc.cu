@@ -10,8 +10,10 @@
 // so a merge is O(n^2) and the whole solve O(k^2) instead of the O(k^3) squarings of the Taylor route. Then
 //   e_k^T x_j = sum_l (e_k^T Q)_l (e_1^T Q)_l e^{lambda_l t_j},  c_j = beta0 sum_l (P Q)_{:,l} (e_1^T Q)_l e^{lambda_l t_j}
 // for every time point (t_0: x_0 = e_1 exactly, as the oracle). One cooperative kernel per checkpoint: the levels
-// with nodes of up to 32 entries in a warp per 32-block (warp syncs only), the larger levels in four grid-synced
-// phases (merge + deflation a CTA per node; roots, z, rows a warp per entry), then the time grid a warp per t_j.
+// with nodes of up to 32 entries on a CTA per 32-block (merge a lane per entry, deflation by warp segments, roots /
+// z / rows 8 lanes per entry; CTA barriers only), the larger levels in four grid-synced phases (merge + deflation a
+// CTA per node; roots, z, rows a warp per entry with the node's scalars staged in shared memory), then the time
+// grid a warp per t_j.
 // Every sum has a fixed order (lane-strided partials, xor-butterfly), so runs are bitwise reproducible.
 #include <cooperative_groups.h>
 
@@ -70,7 +72,7 @@ struct DC {
     unsigned long long* prof;  // KR_TRIDC_PROF: %globaltimer at every grid barrier (CTA 0), else NULL
 };
 
-__device__ __forceinline__ void wstamp(const DC& g, int& k, int gw) {  // warp 0 of the grid, local levels
+__device__ __forceinline__ void wstamp(const DC& g, int& k, int gw) {  // CTA 0's phases of the 32-block levels
     if (g.prof && gw == 0 && (threadIdx.x & 31) == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -94,7 +96,7 @@ __device__ __forceinline__ void stamp(const DC& g, int& k) {
     ++k;
 }
 
-// One node's scalar arrays (pointers offset to the node): in global memory for the large nodes, in the warp's
+// One node's scalar arrays (pointers offset to the node): in global memory for the large nodes, in the CTA's
 // shared memory for the nodes of a 32-block.
 struct NodeArrays {
     double *dK, *zK, *dorg, *tau, *lamR, *zh, *dval, *rotC, *rotS;
