@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(256) spmm_block_kernel(const int64_t* __restri
                     v = val[e0 + eb + g];
                     c = ci[e0 + eb + g];
                 }
-                for (int t = 0; t < G; ++t) {
+                const int tn = min(G, maxlen - eb);  // warp-uniform: no broadcasts past the longest row's end
+                for (int t = 0; t < tn; ++t) {
                     const double vt = __shfl_sync(0xffffffffu, v, base + t);
                     const int ct = __shfl_sync(0xffffffffu, c, base + t);
                     if (act && eb + t < len) s = fma(vt, __ldg(&x[ct]), s);
