@@ -180,9 +180,14 @@ struct StepDyn {
 
 struct Acc2 {
     double ww, sum;      // sum w^2, sum w
-    double dx, dy, dz;   // sums of squared forward differences per axis (coefficient c_a)
-    double face;         // face edge terms with their coefficients: gq[f] w^2
+    double px, py, pz;   // sums of neighbour products w_c w_{c+e_a} over the interior edges per axis (coefficient c_a)
+    double face;         // face cells: (d_c - diag) w_c^2, d_c the cell's diagonal of -A (Dirichlet: 0)
 };
+
+// -w^T A w = sum_c d_c w_c^2 - 2 sum_{interior edges} c_a w_a w_b = diag sum w^2 - 2 (cx px + cy py + cz pz) + face
+__device__ __forceinline__ double acc2_wAw(const StepArgs& a, const Acc2& A) {
+    return fma(2.0 * (a.cx + a.cy + a.cz), A.ww, fma(-2.0 * a.cx, A.px, fma(-2.0 * a.cy, A.py, fma(-2.0 * a.cz, A.pz, A.face))));
+}
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
@@ -190,13 +195,13 @@ __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpre
 // R rows per thread: lane l owns the x-pair (x0 + 2l, +1) on the rows y0 + R w .. y0 + R w + R - 1 of warp w
 // (cells c = 2 r + column). The in-pair x neighbours and the y neighbours inside the thread's rows are registers.
 // BCM: 0 = Dirichlet everywhere; 1 = general faces, tile without x/y face cells (full, x0 > 0, y0 > 0): only the
-// per-plane z-face terms; 2 = general faces, per-cell diagonal corrections.
-// FACE: the tile touches an x / y face of the grid (x0 = 0, y0 = 0, or a ragged tile): the ghost-edge / face terms
-// are checked per plane and cell. Tiles without (most of the grid) take the z faces without per-plane branches: the
-// bottom ghost edge of global plane 0 in the peeled first plane, the top one through the z difference of the last
-// plane, dz = zf w_q - zg w_{q-1} (zf = 0 on the ghost above the grid, zg^2 cz = gq[5]: Dirichlet 1, insulated 0).
+// per-plane z-face terms; 2 = general faces, per-cell diagonal corrections (a tile at x0 = 0, y0 = 0 or ragged).
+// -w^T A w is accumulated in the product form sum_c d_c w_c^2 - 2 sum_edges c_a w_a w_b (acc2_wAw): per cell the
+// three forward-neighbour products (one FMA each, no differences), sum w^2, and for general faces the face cells'
+// diagonal corrections; with Dirichlet faces no face code at all (edges to the zero ghosts drop out), so every
+// full tile takes the unrolled march. The only per-plane branch is uniform: no z edge above the top plane.
 // Box output rows are summed per warp (shuffle tree, fixed order) into wbox.
-template <int TX, int TY, int R, int S, bool INIT, bool FULL, int BCM, bool HALO, bool FACE>
+template <int TX, int TY, int R, int S, bool INIT, bool FULL, int BCM, bool HALO>
 __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensorMap* tmP, const StepArgs& a,
                                           const StepDyn& dyn, unsigned char* smem, double* Wb0, double* Wb1, uint64_t* bar, int x0, int y0,
                                           int zc0, int zc1, bool cta_box, Acc2& A, double (*wbox)[KR_MAX_BOX]) {
@@ -229,9 +234,6 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
 #pragma unroll
     for (int c = 0; c < NC; ++c) in[c] = FULL || (gx + (c & 1) < a.mx && gy + (c >> 1) < a.my);
     // face cells: low faces in any tile at x0 = 0 / y0 = 0; high faces only in ragged (not FULL) tiles
-    const bool xlo = x0 == 0 && lane == 0;  // cells 2 r
-    const bool ylo = y0 == 0 && wid == 0;   // cells 0, 1
-    const bool xhi0 = !FULL && gx == a.mx - 1, xhi1 = !FULL && gx + 1 == a.mx - 1;
     double exy[NC];  // per-cell x/y diagonal corrections (BCM 2)
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -302,7 +304,7 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     uint32_t ph = (2 / S) & 1;
     // one plane q: w_q on the tile (wc) and the ring (into the W buffer of q's parity), then the products of plane
     // q - 1 (wp = w_{q-1}; its x+2 / row+R neighbours from the W buffer written last iteration, its z+1 neighbour wc)
-    const double zgtop = BCM ? sqrt(a.gq[5] / a.cz) : 1.0;  // the top face's edge coefficient gq[5] = zg^2 cz
+    constexpr bool UNROLL = FULL && BCM < 2;  // the first plane peeled, six planes per turn of the register rotation
     auto plane = [&](const double (&up)[2 * R], const double (&uc)[2 * R], double (&un)[2 * R], const double rp,
                      const double rc, double& rn, const double (&wp)[2 * R], double (&wc)[2 * R], const int q,
                      auto first) {
@@ -380,96 +382,43 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
             if (!FULL && !rin) r0 = 0.0;
             Wq[rwb] = r0;
         }
-        if (!FACE && FIRST && a.zoff + zc0 == 0) {  // ghost edge below global plane 0, coefficient gq[4]
-            double s2 = 0.0;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) s2 = fma(wc[c], wc[c], s2);
-            A.face = fma(a.gq[4], s2, A.face);
-        }
-        if (!FIRST && (!FACE || q > zc0)) {  // products of plane q - 1 (its x+2 / row+R neighbours: last iteration)
+        if (!FIRST && (UNROLL || q > zc0)) {  // products of plane q - 1 (its x+2 / row+R neighbours: last iteration)
             const double* Wp = ((q & 1) ? Wb0 : Wb1) + wb;
             const int gzp = gzq - 1;
             const double2 yu = ld2(Wp + R * WW);
-            double dx[NC], dy[NC];
+            // neighbour products over the forward edges: w beyond the grid (cells outside a ragged tile, ring
+            // cells outside the grid) is stored as 0, so edges to the x / y ghosts drop out without face code
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const double xr = Wp[r * WW + 2];
-                dx[2 * r] = wp[2 * r + 1] - wp[2 * r];
-                dx[2 * r + 1] = xr - wp[2 * r + 1];
-                if (r == R - 1) {
-                    dy[2 * r] = yu.x - wp[2 * r];
-                    dy[2 * r + 1] = yu.y - wp[2 * r + 1];
-                } else {
-                    dy[2 * r] = wp[2 * r + 2] - wp[2 * r];
-                    dy[2 * r + 1] = wp[2 * r + 3] - wp[2 * r + 1];
-                }
-            }
-            if (!FULL) {  // high x / y faces: the edge to the (zero) ghost takes the face coefficient
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if (xhi0) {
-                        dx[2 * r] = 0.0;
-                        A.face = fma(a.gq[1], wp[2 * r] * wp[2 * r], A.face);
-                    }
-                    if (xhi1) {
-                        dx[2 * r + 1] = 0.0;
-                        A.face = fma(a.gq[1], wp[2 * r + 1] * wp[2 * r + 1], A.face);
-                    }
-                    if (gy + r == a.my - 1) {
-                        dy[2 * r] = 0.0;
-                        dy[2 * r + 1] = 0.0;
-                        A.face = fma(a.gq[3], fma(wp[2 * r], wp[2 * r], wp[2 * r + 1] * wp[2 * r + 1]), A.face);
-                    }
-                }
-            }
-            if (FACE) {  // ghost edges of the low x / y faces
-                if (xlo) {
-#pragma unroll
-                    for (int r = 0; r < R; ++r) A.face = fma(a.gq[0], wp[2 * r] * wp[2 * r], A.face);
-                }
-                if (ylo) A.face = fma(a.gq[2], fma(wp[0], wp[0], wp[1] * wp[1]), A.face);
+                const double yn0 = r == R - 1 ? yu.x : wp[2 * r + 2], yn1 = r == R - 1 ? yu.y : wp[2 * r + 3];
+                A.px = fma(wp[2 * r], wp[2 * r + 1], A.px);
+                A.px = fma(wp[2 * r + 1], xr, A.px);
+                A.py = fma(wp[2 * r], yn0, A.py);
+                A.py = fma(wp[2 * r + 1], yn1, A.py);
             }
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 A.ww = fma(wp[c], wp[c], A.ww);
                 A.sum += wp[c];
-                A.dx = fma(dx[c], dx[c], A.dx);
-                A.dy = fma(dy[c], dy[c], A.dy);
             }
-            if (FACE && gzp == a.mz - 1) {  // the z+1 neighbour is the zero ghost above the grid: coefficient gq[5]
-                double s2 = 0.0;
+            const bool ztop = gzp == a.mz - 1;  // uniform: the z+1 neighbour is the ghost above the grid (its w is
+            if (!ztop) {                        // not a state value): no edge
 #pragma unroll
-                for (int c = 0; c < NC; ++c) s2 = fma(wp[c], wp[c], s2);
-                A.face = fma(a.gq[5], s2, A.face);
-            } else if (!FACE) {
-                const bool top = gzp == a.mz - 1;  // uniform: the ghost above the grid (w there is not a state value)
-                const double zf = top ? 0.0 : 1.0;
-                if (BCM) {
-                    const double zg = top ? zgtop : 1.0;
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) {
-                        const double dz = fma(wc[c], zf, -zg * wp[c]);
-                        A.dz = fma(dz, dz, A.dz);
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) {
-                        const double dz = fma(wc[c], zf, -wp[c]);  // exactly wc - wp, or -wp above the grid
-                        A.dz = fma(dz, dz, A.dz);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const double dz = wc[c] - wp[c];
-                    A.dz = fma(dz, dz, A.dz);
-                }
+                for (int c = 0; c < NC; ++c) A.pz = fma(wp[c], wc[c], A.pz);
             }
-            if (FACE && gzp == 0) {
-                double s2 = 0.0;
+            if (BCM) {  // face cells: (d_c - diag) w_c^2 = -(sum of the cell's face corrections ecor) w_c^2
+                if (gzp == 0 || ztop) {  // uniform, rare
+                    double s2 = 0.0;
 #pragma unroll
-                for (int c = 0; c < NC; ++c) s2 = fma(wp[c], wp[c], s2);
-                A.face = fma(a.gq[4], s2, A.face);
+                    for (int c = 0; c < NC; ++c) s2 = fma(wp[c], wp[c], s2);
+                    const double ez = (gzp == 0 ? a.ecor[4] : 0.0) + (ztop ? a.ecor[5] : 0.0);
+                    A.face = fma(-ez, s2, A.face);
+                }
+                if (BCM == 2) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) A.face = fma(-exy[c] * wp[c], wp[c], A.face);
+                }
             }
             const bool wr = !INIT && dyn.write_out;
             if (wr) {
@@ -520,7 +469,6 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     };
     using F1 = std::integral_constant<bool, true>;
     using F0 = std::integral_constant<bool, false>;
-    constexpr bool UNROLL = FULL && !FACE && BCM < 2;
     if (UNROLL) {  // the first plane peeled (no products), then six planes per turn of the register rotation
         plane(U0, U1, U2, R0, R1, R2, WA, WB, zc0, F1{});
         for (int q = zc0 + 1; q <= zc1;) {
@@ -578,16 +526,20 @@ __device__ __forceinline__ void lz_items2(const CUtensorMap* tmC, const CUtensor
                 a.box[r].lo[1] < y0 + TY && a.box[r].hi[1] > y0 && a.box[r].lo[2] < a.zoff + zc1 &&
                 a.box[r].hi[2] > a.zoff + zc0)
                 cta_box = true;
-#define KR_M2(FULL_, BCM_, FACE_) \
-    lz_march2<TX, TY, R, S, INIT, FULL_, BCM_, HALO, FACE_>(tmC, tmP, a, dy, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, \
+#define KR_M2(FULL_, BCM_) \
+    lz_march2<TX, TY, R, S, INIT, FULL_, BCM_, HALO>(tmC, tmP, a, dy, smem, Wb0, Wb1, bar, x0, y0, zc0, zc1, cta_box, \
                                                             A, wbox)
         if (x0 + TX < a.mx && y0 + TY < a.my) {
-            if (x0 > 0 && y0 > 0)
-                KR_M2(true, BC ? 1 : 0, false);
-            else
-                KR_M2(true, BC ? 2 : 0, true);
+            if constexpr (BC) {
+                if (x0 > 0 && y0 > 0)
+                    KR_M2(true, 1);
+                else
+                    KR_M2(true, 2);
+            } else {
+                KR_M2(true, 0);  // Dirichlet: no face terms, every full tile takes the unrolled march
+            }
         } else {
-            KR_M2(false, BC ? 2 : 0, true);
+            KR_M2(false, BC ? 2 : 0);
         }
 #undef KR_M2
         __syncthreads();  // every issued plane was consumed: the barriers can be recycled for the next item
@@ -630,7 +582,7 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
     __syncthreads();
     double acc[3 + KR_MAX_BOX];
     acc[0] = A.ww;
-    acc[1] = fma(a.cx, A.dx, fma(a.cy, A.dy, fma(a.cz, A.dz, A.face)));  // -w^T A w
+    acc[1] = acc2_wAw(a, A);  // -w^T A w
     acc[2] = A.sum;
 #pragma unroll
     for (int r = 0; r < KR_MAX_BOX; ++r) acc[3 + r] = (tid & 31) == 0 ? wbox[tid >> 5][r] : 0.0;
@@ -899,7 +851,7 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
         {
             double acc[3 + KR_MAX_BOX];
             acc[0] = A.ww;
-            acc[1] = fma(a.cx, A.dx, fma(a.cy, A.dy, fma(a.cz, A.dz, A.face)));  // -w^T A w
+            acc[1] = acc2_wAw(a, A);  // -w^T A w
             acc[2] = A.sum;
 #pragma unroll
             for (int r = 0; r < KR_MAX_BOX; ++r) acc[3 + r] = lane == 0 ? wbox[wid][r] : 0.0;
