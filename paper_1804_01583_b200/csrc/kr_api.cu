@@ -1149,6 +1149,9 @@ static kr_status create_impl(const kr_problem* p, kr_handle** out) {
                 }
                 if (env_zc) best_zc = std::max(1, atoi(env_zc));
                 sl.zchunk = best_zc;
+                // items in windows of the resident CTAs (KR_WIN=0: z-chunk-major order, KR_WIN=n: window n)
+                sl.win = (int32_t)slots_total;
+                if (const char* e = getenv("KR_WIN")) sl.win = std::max(0, atoi(e));
                 const int64_t nch = (sl.nz + sl.zchunk - 1) / sl.zchunk;
                 sl.gx = (int32_t)gx;
                 sl.gy = (int32_t)gy;

@@ -99,6 +99,7 @@ struct Slab {
     int64_t nitems;      // work items = gx * gy * z-chunks
     dim3 grid;
     int zchunk;
+    int32_t win = 0;     // item order window (resident CTAs of the step kernel; 0 = z-chunk-major order)
     // Compact start vector u_1 of an analytic (box / all-grid) generator, per local direction: only the
     // generator box clipped to this slab's buffer planes is stored (cells x0 .. x0+w, y0 .. y0+h, buffer
     // planes p0 .. p0+d); the step kernels read it through tensor maps over that small array with shifted

@@ -76,6 +76,7 @@ struct StepArgs {
     int64_t pitch, plane;
     int32_t mx, my, mz, nz, zoff, zchunk;
     int32_t gx, gy, nitems;  // persistent work items: gx * gy tiles x ceil(nz / zchunk) chunks
+    int32_t win;             // > 0: items ordered in windows of `win` tiles, z-chunk by z-chunk (lz_item_coords)
     double cx, cy, cz;  // alpha / h_a^2
     // per-face boundary terms (x-, x+, y-, y+, z-, z+; kr_bc): ecor = diagonal correction of face cells
     // relative to the Dirichlet stencil ((bc != DIRICHLET) c_a - (bc == ROBIN) gamma); gq = coefficient of
@@ -501,6 +502,29 @@ __device__ __forceinline__ void lz_march2(const CUtensorMap* tmC, const CUtensor
     }
 }
 
+// Work item -> (x-tile, y-tile, z-chunk). win = 0: z-chunk-major (all tiles of chunk 0, then chunk 1, ...).
+// win = W (the resident CTAs of the launch): the tiles in groups of W, and within a group the z-chunks one after
+// the other, so chunk z + 1 of a tile column is dispatched W items (one wave of resident CTAs) after chunk z: it
+// starts as chunk z ends, and the three u_i planes and one u_{i-1} plane the two chunks share are still in L2
+// (z-chunk-major order re-reads them from DRAM one pass over all tiles later: ~2 % of a step's bytes at C5).
+__device__ __forceinline__ void lz_item_coords(const StepArgs& a, int item, int& xt, int& yt, int& zt) {
+    const int T = a.gx * a.gy;
+    int tile;
+    if (a.win > 0 && a.win < T) {
+        const int Z = a.nitems / T;
+        const int g = item / (a.win * Z), rem = item - g * a.win * Z;
+        const int gw = min(a.win, T - g * a.win);  // tiles in this group (the last one may be smaller)
+        zt = rem / gw;
+        tile = g * a.win + (rem - zt * gw);
+    } else {
+        tile = item % T;
+        zt = item / T;
+    }
+    xt = a.ix0 + tile % a.gx;
+    yt = a.iy0 + tile / a.gx;
+    zt += a.iz0;
+}
+
 // The work items (x-tile, y-tile, z-chunk) of one step, dealt round-robin over the CTAs (fixed assignment,
 // deterministic): the march of each item, accumulating the CTA's sums in A and wbox.
 template <int TX, int TY, int S, bool INIT, bool BC, bool HALO, int R>
@@ -510,7 +534,8 @@ __device__ __forceinline__ void lz_items2(const CUtensorMap* tmC, const CUtensor
     const int tid = threadIdx.x;
     // Persistent CTAs: work items (x-tile, y-tile, z-chunk) dealt round-robin (fixed assignment, deterministic)
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
-        const int xt = a.ix0 + item % a.gx, yt = a.iy0 + (item / a.gx) % a.gy, zt = a.iz0 + item / (a.gx * a.gy);
+        int xt, yt, zt;
+        lz_item_coords(a, item, xt, yt, zt);
         const int x0 = xt * TX, y0 = yt * TY;
         const int zc0 = zt * a.zchunk;
         const int zc1 = min(zc0 + a.zchunk, a.nz);
@@ -1245,6 +1270,7 @@ static StepArgs make_args(kr_handle* h, Slab& sl, int dl, int nxt, int step, boo
     a.nz = (int)sl.nz;
     a.zoff = (int)sl.z0;
     a.zchunk = sl.zchunk;
+    a.win = sl.win;
     a.gx = sl.gx;
     a.gy = sl.gy;
     a.nitems = (int)sl.nitems;

@@ -527,11 +527,14 @@ def test_device_block_cache_reuse_and_release():
 
 
 @pytest.mark.parametrize("env", [{"KR_ZCHUNK": "1"}, {"KR_ZCHUNK": "3"}, {"KR_ZCHUNK": "500"}, {"KR_NO_GRAPH": "1"},
-                                 {"KR_HALO_COPY": "1"}])
+                                 {"KR_HALO_COPY": "1"}, {"KR_WIN": "4", "KR_ZCHUNK": "3"},
+                                 {"KR_WIN": "1", "KR_ZCHUNK": "5"}, {"KR_WIN": "5", "KR_ZCHUNK": "2"},
+                                 {"KR_WIN": "0", "KR_ZCHUNK": "3"}])
 def test_stencil_switches_keep_parity(env, monkeypatch):
     """The diagnostic switches of the fused stencil path (README) change scheduling only: z-chunks of 1, 3 and all
-    planes, no CUDA graph, the copy halo transport on 3 virtual slabs — equal to the oracle; the z-chunk choice only
-    reorders the per-CTA partial sums."""
+    planes, no CUDA graph, the copy halo transport on 3 virtual slabs, the work-item order (windows of 4, 1 and 5
+    tiles over the 6 tiles of the grid, the last group smaller; z-chunk-major) — equal to the oracle; the z-chunk
+    choice and the item order only reorder the per-CTA partial sums."""
     p = W.heat(70, 5, 20, n_steps=80, step=0.02, my=40, mz=33)
     p["gens"].append(W.rand(11, 0.3))
     p["z_lo"] = np.array([0.9, 0.0])
