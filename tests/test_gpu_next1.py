@@ -355,3 +355,24 @@ def test_adaptive_many_output_rows():
     for (kg, bg), (ko, bo) in zip(checks, r0["checks"]):
         assert abs(bg - bo) <= 1e-8 * abs(bo) + 1e-300, (kg, bg, bo)
     assert_coeff(coeff, ref["coeff"], "adaptive 8 rows", atol=projection_envelope(r0["beta0"], r0["P"]))
+
+
+@pytest.mark.parametrize("env", [{}, {"KR_NO_ZINT": "1"}, {"KR_MULTISTEP": "0", "KR_ZCHUNK": "5"},
+                                 {"KR_MULTISTEP": "0", "KR_ZCHUNK": "5", "KR_NO_ZINT": "1"},
+                                 {"KR_MULTISTEP": "0", "KR_ZCHUNK": "4", "vs": 3}])
+def test_general_faces_interior_tiles(env, monkeypatch):
+    """General faces (the paper's insulated faces + Robin at x = 1) on a 200 x 40 x 30 grid with a fixed k = 30:
+    full 64 x 16 tiles away from every x / y face exist (x0 = 64, 128; y0 = 16), and with z-chunks of 4-5 planes so
+    do chunks away from both z faces — those take the Dirichlet march (KR_NO_ZINT=1: the general-face march
+    everywhere), the face tiles / chunks the face corrections; per-step launches, the multi-step kernel and 3
+    virtual z-slabs: equal to the oracle."""
+    env = dict(env)
+    vs = env.pop("vs", None)
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    p = W.heat_paper(30, k_max=30)
+    p.update(mx=200, my=40, mz=30, eps=0.0, n_steps=200)
+    ref = oracle.krylov_project(p)
+    coeff, stats, _, _ = gpu(p, virtual_slabs=vs) if vs else gpu(p)
+    assert stats[0]["k_eff"] == ref["per_dir"][0]["k_eff"]
+    assert_coeff(coeff, ref["coeff"], f"general faces 200x40x30 {env} vs={vs}")

@@ -304,7 +304,18 @@ def csr_stable_nonsym(n=400, nnz_per_row=6, seed=7, n_gen=3, eps=1e-6, k_max=200
             "eps": float(eps), "k_max": int(k_max), "thresholds": []}
 
 
+def paper1000_dense(k=30):
+    """The paper's 10^9-state heat model (insulated faces, Robin at x = 1; heat_paper(1000)) with a fixed k and the
+    dense start rand(5): the general-boundary step kernel on dense data, as in steps 1000+ of the paper's own run
+    (timing workload for A/B runs, not a bench line)."""
+    p = heat_paper(1000, k_max=k)
+    p["eps"] = 0.0
+    p["gens"] = [rand(5)]
+    return dict(p, name="P1000D_heat_paper1000_dense")
+
+
 CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5, "C5D": config5_dense,
+           "P1000D": paper1000_dense,
            "P100": lambda: heat_paper(100), "P1000": lambda: heat_paper(1000),
            "H10": lambda: heat_heater(10), "H100": lambda: heat_heater(100, k=800),
            "C2T": lambda: dict(config2(), sim="transpose")}
