@@ -201,46 +201,80 @@ double gershgorin_mu(const kr_problem* p) {
                 break;
             }
     std::vector<double> diag(N, 0.0), rad(N, 0.0);
-    auto pass = [&](const int64_t* rp, const auto* ci, const double* v) {
-        std::vector<uint8_t> paired((size_t)rp[n], 0);
-        for (int64_t r = 0; r < n; ++r) {
-            for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
-                const int64_t c = ci[e];
-                if (c == r) {
-                    diag[(size_t)r] += v[e];  // 0.5 a_rr + 0.5 a_rr
-                    continue;
-                }
-                double s;
-                if (c > r) {
+    // Row blocks on T host threads (C2: 240k entries, ~2.7 ms on one thread), two phases: (1) the pairs {r, c} from
+    // their entry with c > r (mirror found, marked, |s_rc| to both radii), (2) after all marks, the unmarked entries
+    // with c < r. Each thread adds into its own radius array; the arrays are summed in thread order (deterministic).
+    auto run = [&](const int64_t* rp, const auto* ci, const double* v) {
+        const int64_t nnz = rp[n];
+        const int T = (int)std::max<int64_t>(1, std::min<int64_t>({8, (int64_t)std::thread::hardware_concurrency(),
+                                                                    nnz / 16384}));
+        std::vector<uint8_t> paired((size_t)nnz, 0);
+        std::vector<std::vector<double>> radt((size_t)T, std::vector<double>(N, 0.0));
+        auto rows = [&](int t) { return std::make_pair(n * t / T, n * (t + 1) / T); };
+        auto phase1 = [&](int t) {
+            std::vector<double>& rd = radt[(size_t)t];
+            const auto [r0, r1] = rows(t);
+            for (int64_t r = r0; r < r1; ++r) {
+                for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+                    const int64_t c = ci[e];
+                    if (c == r) {
+                        diag[(size_t)r] += v[e];  // 0.5 a_rr + 0.5 a_rr
+                        continue;
+                    }
+                    if (c < r) continue;  // phase 2
                     int64_t lo = rp[c], hi = rp[c + 1];  // binary search of column r in row c
                     while (lo < hi) {
                         const int64_t mid = (lo + hi) >> 1;
                         if (ci[mid] < r) lo = mid + 1; else hi = mid;
                     }
+                    double s;
                     if (lo < rp[c + 1] && ci[lo] == r) {
                         s = std::fabs(0.5 * v[e] + 0.5 * v[lo]);
-                        paired[(size_t)lo] = 1;
+                        paired[(size_t)lo] = 1;  // the only writer of this byte (pair {r, c} is visited from r)
                     } else {
                         s = std::fabs(0.5 * v[e]);
                     }
-                } else {
-                    if (paired[(size_t)e]) continue;  // counted from row c
-                    s = std::fabs(0.5 * v[e]);
+                    rd[(size_t)r] += s;
+                    rd[(size_t)c] += s;
                 }
-                rad[(size_t)r] += s;
-                rad[(size_t)c] += s;
+                if (p->b && p->b[r] != 0.0) {  // lifted column b and (zero) lifted row: s_{r,n} = s_{n,r} = b_r / 2
+                    rd[(size_t)r] += std::fabs(0.5 * p->b[r]);
+                    rd[(size_t)n] += std::fabs(0.5 * p->b[r]);
+                }
             }
-            if (p->b && p->b[r] != 0.0) {  // lifted column b and (zero) lifted row: s_{r,n} = s_{n,r} = b_r / 2
-                rad[(size_t)r] += std::fabs(0.5 * p->b[r]);
-                rad[(size_t)n] += std::fabs(0.5 * p->b[r]);
-            }
+        };
+        auto phase2 = [&](int t) {
+            std::vector<double>& rd = radt[(size_t)t];
+            const auto [r0, r1] = rows(t);
+            for (int64_t r = r0; r < r1; ++r)
+                for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+                    const int64_t c = ci[e];
+                    if (c >= r || paired[(size_t)e]) continue;  // counted from row c
+                    const double s = std::fabs(0.5 * v[e]);
+                    rd[(size_t)r] += s;
+                    rd[(size_t)c] += s;
+                }
+        };
+        for (int ph = 0; ph < 2; ++ph) {
+            auto f = [&](int t) {
+                if (ph == 0)
+                    phase1(t);
+                else
+                    phase2(t);
+            };
+            std::vector<std::thread> th;
+            for (int t = 1; t < T; ++t) th.emplace_back(f, t);
+            f(0);
+            for (auto& x : th) x.join();
         }
+        for (int t = 0; t < T; ++t)
+            for (int64_t r = 0; r < N; ++r) rad[(size_t)r] += radt[(size_t)t][(size_t)r];
     };
     if (sorted) {
-        pass(p->row_ptr, p->col_idx, p->val);
+        run(p->row_ptr, p->col_idx, p->val);
     } else {
         const RowsCsr m = merged_rows(p);
-        pass(m.rp.data(), m.ci.data(), m.v.data());
+        run(m.rp.data(), m.ci.data(), m.v.data());
     }
     double mu = -INFINITY;
     for (int64_t r = 0; r < N; ++r) mu = std::max(mu, diag[r] + rad[r]);
