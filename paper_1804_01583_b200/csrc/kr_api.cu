@@ -263,8 +263,14 @@ double gershgorin_mu(const kr_problem* p) {
                     phase2(t);
             };
             std::vector<std::thread> th;
-            for (int t = 1; t < T; ++t) th.emplace_back(f, t);
+            int t_next = 1;
+            try {  // this may itself run on a helper thread: no exception may escape (threads that fail to start
+                   // are run inline below)
+                for (; t_next < T; ++t_next) th.emplace_back(f, t_next);
+            } catch (...) {
+            }
             f(0);
+            for (int t = t_next; t < T; ++t) f(t);
             for (auto& x : th) x.join();
         }
         for (int t = 0; t < T; ++t)
