@@ -835,7 +835,16 @@ struct MultiArgs {
     double* u[3];   // the slab's state buffers
     double* part;   // [2][nqp][gridDim.x] per-CTA partial sums, double-buffered by step parity
     int32_t i0, i1; // steps
+    uint64_t* prof; // KR_MS_PROF=1: %globaltimer per CTA at step start / march end / after the grid barrier / step
+                    // end for the first KR_MS_PROF_STEPS steps of the launch, [step][CTA][4]; else NULL
 };
+
+__device__ __forceinline__ uint64_t kr_globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr int KR_MS_PROF_STEPS = 8;
 
 template <int TX, int TY, int S, bool BC, int R>
 __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 : 2)
@@ -870,6 +879,9 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
     __syncthreads();
     for (int i = m.i0; i <= m.i1; ++i) {
         if (done) break;  // uniform over the grid
+        uint64_t* pr = (m.prof && i - m.i0 < KR_MS_PROF_STEPS && tid == 0)
+                           ? m.prof + ((size_t)(i - m.i0) * nblk + blockIdx.x) * 4 : nullptr;
+        if (pr) pr[0] = kr_globaltimer();
         const int cur = (i - 1) % 3, nxt = i % 3, prev = i >= 2 ? (i - 2) % 3 : cur;
         const CUtensorMap* tc = cur == 0 ? &tmC0 : (cur == 1 ? &tmC1 : &tmC2);
         const CUtensorMap* tp = prev == 0 ? &tmP0 : (prev == 1 ? &tmP1 : &tmP2);
@@ -907,18 +919,24 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
         }
         // u_{i+1} was written by generic stores; the next step reads it through TMA (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (pr) pr[1] = kr_globaltimer();
         grid.sync();
+        if (pr) pr[2] = kr_globaltimer();
         // all partials, fixed order (lane-strided sums, xor tree): the same bits in every CTA
         for (int q = wid; q < nqp; q += NWp) {
-            // four independent loads in flight per lane (L2 round trips, not adds, bound this), summed in a fixed order
-            double v4[4] = {0.0, 0.0, 0.0, 0.0};
+            // every partial of the lane in flight at once (one L2 round trip for grids up to 32 x 12 CTAs; the
+            // round trips, not the adds, bound this), summed in a fixed order
+            constexpr int U = 12;
+            double vu[U];
             const double* pq = part + (size_t)q * nblk;
-            for (int b = lane; b < nblk; b += 128) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (b + 32 * u < nblk) v4[u] += __ldcg(pq + b + 32 * u);
-            }
-            double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
+            for (int u = 0; u < U; ++u) vu[u] = lane + 32 * u < nblk ? __ldcg(pq + lane + 32 * u) : 0.0;
+            for (int b = lane + 32 * U; b < nblk; b += 32) vu[U - 1] += __ldcg(pq + b);  // larger grids
+#pragma unroll
+            for (int w = 1; w < U; w *= 2)
+#pragma unroll
+                for (int u = 0; u + w < U; u += 2 * w) vu[u] += vu[u + w];
+            double v = vu[0];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (lane == 0) qsum[q] = v;
@@ -962,6 +980,7 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
             }
         }
         __syncthreads();
+        if (pr) pr[3] = kr_globaltimer();
     }
 }
 
@@ -1597,13 +1616,54 @@ template <int TX, int TY>
 static void multistep_launch_t(kr_handle* h, Slab& sl, int dl, int i0, int i1) {
     constexpr int S = Stages<TX, TY>::S;
     StepArgs a = make_args(h, sl, dl, i0 % 3, i0, false, true, -1, 0);
-    MultiArgs m{{sl.u[0], sl.u[1], sl.u[2]}, sl.mspart, i0, i1};
+    MultiArgs m{{sl.u[0], sl.u[1], sl.u[2]}, sl.mspart, i0, i1, nullptr};
+    // KR_MS_PROF=1 (diagnostics, not inside graph capture): per-CTA phase times of the launch's first steps on stderr
+    static const bool prof = getenv("KR_MS_PROF") != nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    KR_CUDA(cudaStreamIsCapturing(h->stream, &cs));
+    const size_t np = (size_t)KR_MS_PROF_STEPS * h->ms_grid * 4;
+    if (prof && cs == cudaStreamCaptureStatusNone) {
+        KR_CUDA(cudaMalloc(&m.prof, np * 8));
+        KR_CUDA(cudaMemsetAsync(m.prof, 0, np * 8, h->stream));
+    }
     void* fn = h->gen_bc ? multistep_fn<TX, TY, true>() : multistep_fn<TX, TY, false>();
     void* args[] = {(void*)&sl.tmC[0], (void*)&sl.tmC[1], (void*)&sl.tmC[2], (void*)&sl.tmP[0],
                     (void*)&sl.tmP[1], (void*)&sl.tmP[2], (void*)&a, (void*)&m};
     KR_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)h->ms_grid), dim3(Geo2<TX, TY, 2>::NT), args,
                                         step2_smem_bytes<TX, TY, S>(), h->stream));
     h->launches++;
+    if (m.prof) {
+        std::vector<uint64_t> t(np);
+        KR_CUDA(cudaMemcpyAsync(t.data(), m.prof, np * 8, cudaMemcpyDeviceToHost, h->stream));
+        KR_CUDA(cudaStreamSynchronize(h->stream));
+        KR_CUDA(cudaFree(m.prof));
+        const int G = h->ms_grid;
+        for (int s = 0; s < KR_MS_PROF_STEPS && s <= i1 - i0; ++s) {
+            const uint64_t* b = t.data() + (size_t)s * G * 4;
+            if (b[0] == 0) break;
+            uint64_t t0 = UINT64_MAX, t1max = 0, t2min = UINT64_MAX, t3max = 0;
+            std::vector<double> march(G), wait(G);
+            for (int c = 0; c < G; ++c) {
+                const uint64_t* q = b + (size_t)c * 4;
+                t0 = std::min(t0, q[0]);
+                t1max = std::max(t1max, q[1]);
+                t2min = std::min(t2min, q[2]);
+                t3max = std::max(t3max, q[3]);
+                march[c] = 1e-3 * (double)(q[1] - q[0]);
+                wait[c] = 1e-3 * (double)(q[2] - q[1]);
+            }
+            std::vector<double> ms = march;
+            std::sort(ms.begin(), ms.end());
+            int slow = 0;
+            for (int c = 1; c < G; ++c)
+                if (march[c] > march[slow]) slow = c;
+            fprintf(stderr,
+                    "[kr ms prof] step %d: march min %.2f med %.2f max %.2f us (slowest CTA %d); last arrival -> first "
+                    "release %.2f us; release -> step end %.2f us; step %.2f us\n",
+                    i0 + s, ms[0], ms[G / 2], ms[G - 1], slow, 1e-3 * (double)((int64_t)t2min - (int64_t)t1max),
+                    1e-3 * (double)(t3max - t2min), 1e-3 * (double)(t3max - t0));
+        }
+    }
 }
 
 // Enqueue Lanczos steps i0..i1 of local direction dl: the persistent multi-step kernel where it applies (steps
