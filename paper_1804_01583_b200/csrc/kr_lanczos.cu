@@ -11,8 +11,8 @@
 //   * lookahead: with alpha_i known, w = s_i A u_i - alpha_i s_i u_i - beta_{i-1} s_{i-1} u_{i-1}
 //     (Alg. 3 lines 3-9 in one expression), and in the same pass
 //       beta_i^2 = sum w^2 and  alpha_{i+1} = v_{i+1}^T A v_{i+1} = w^T A w / beta_i^2,
-//     where -w^T A w = sum_axes c_a sum_{edges} (w_b - w_a)^2 (+ c_a w^2 on ghost edges) is a sum of
-//     non-negative terms (summation by parts, Dirichlet ghosts = 0) — no cancellation;
+//     where -w^T A w = sum_c d_c w_c^2 - 2 sum_axes c_a sum_{interior edges} w_a w_b (d_c the cell's diagonal of -A;
+//     the product form, whose rounding is of the order of the oracle's own v^T (A v));
 //   * the (x+1), (y+1), (z+1) neighbours of w are recomputed on a one-cell forward ring, so u_i is
 //     read with a depth-2 halo in-plane (TMA box (TX+4) x (TY+3) from x0-2: TMA needs 16-byte aligned
 //     starts in x) and u_{i-1} with depth 1;
@@ -81,7 +81,8 @@ struct StepArgs {
     double cx, cy, cz;  // alpha / h_a^2
     // per-face boundary terms (x-, x+, y-, y+, z-, z+; kr_bc): ecor = diagonal correction of face cells
     // relative to the Dirichlet stencil ((bc != DIRICHLET) c_a - (bc == ROBIN) gamma); gq = coefficient of
-    // w_c^2 in -w^T A w for a face cell (DIRICHLET c_a, INSULATED 0, ROBIN gamma). Dirichlet: ecor = 0, gq = c.
+    // w_c^2 in the edge form of -w^T A w for a face cell (DIRICHLET c_a, INSULATED 0, ROBIN gamma; the fill + init
+    // kernel). Dirichlet: ecor = 0, gq = c. The step kernels' product form uses -ecor of face cells.
     double ecor[6], gq[6];
     const LzScalars* sc;
     int32_t step;       // i (1-based); 0 = init pass
@@ -147,11 +148,9 @@ struct Geo {
 // of a plane arrive as two 16-byte shared-memory loads; the in-pair x neighbours and the in-pair y neighbours are
 // registers; only the outer x neighbours (x - 1, x + 2), the outer rows and u_{i-1} are loaded: 15 shared-memory
 // instructions per 4 cells (v1, 4 cells strided in y per thread, every neighbour from shared memory: 36). The
-// products -w^T A w are kept per axis (sums of squared forward differences) and combined with the edge
-// coefficients once at the end of the kernel; the few face cells (ghost edges of low faces, the edges of high
-// faces) go to one face accumulator with their own coefficients (Dirichlet: c_a; insulated: 0; Robin: gamma).
-// The forward ring (top row: warp 0, one x-pair per lane; right column: warp 1, one cell per lane) is computed
-// beside the tile, as in v1.
+// neighbour products of -w^T A w are kept per axis and combined with the edge coefficients once at the end of the
+// kernel (acc2_wAw); with general faces the face cells' diagonal corrections go to one face accumulator.
+// The forward ring (top row: warps 0-1, one cell per lane; right column: warp 2) is computed beside the tile.
 // ================================================================================================
 template <int TX, int TY, int R = 2>
 struct Geo2 {
@@ -986,7 +985,7 @@ __global__ void __launch_bounds__(Geo2<TX, TY, R>::NT, (TY >= 32 && R == 2) ? 1 
 
 // Init pass for an analytic generator (KR_VEC_BOX / KR_VEC_ALL): writes u_1 = v over the slab buffer
 // (owned planes, plus the ghost/halo planes from the global description) and, in the same pass,
-// accumulates ||v||^2, -v^T A v (edge form) and the box-row projections C v (Alg. 4 lines 1-2,
+// accumulates ||v||^2, -v^T A v (summation-by-parts edge form) and the box-row projections C v (Alg. 4 lines 1-2,
 // P:782-783). One 8n-byte write instead of a fill (8n write) followed by a read pass (8n).
 // v = value * [x in X][y in Y][z in Z] with X, Y, Z the box ranges clipped to the grid (ALL = whole grid),
 // so membership is precomputed per axis.
