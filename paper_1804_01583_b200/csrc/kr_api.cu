@@ -206,8 +206,9 @@ double gershgorin_mu(const kr_problem* p) {
     // with c < r. Each thread adds into its own radius array; the arrays are summed in thread order (deterministic).
     auto run = [&](const int64_t* rp, const auto* ci, const double* v) {
         const int64_t nnz = rp[n];
+        // at most 8 threads, ~16k entries per thread, and T per-thread radius arrays within 256 MB of host memory
         const int T = (int)std::max<int64_t>(1, std::min<int64_t>({8, (int64_t)std::thread::hardware_concurrency(),
-                                                                    nnz / 16384}));
+                                                                    nnz / 16384, (int64_t(256) << 20) / (8 * N)}));
         std::vector<uint8_t> paired((size_t)nnz, 0);
         std::vector<std::vector<double>> radt((size_t)T, std::vector<double>(N, 0.0));
         auto rows = [&](int t) { return std::make_pair(n * t / T, n * (t + 1) / T); };
