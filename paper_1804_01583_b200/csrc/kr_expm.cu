@@ -17,39 +17,54 @@ namespace {
 
 constexpr int ET = 256;
 
-// C = A * B (n x n, leading dimension ld); caller synchronises before and after.
-__device__ __forceinline__ void mm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                                   int n, int ld) {
+// C = A * B (n x n, leading dimension ld); caller synchronises before and after. 16 x 16 threads with MT x MT
+// register micro-tiles (rows ty + 16 a, columns tx + 16 b) covering 16 MT >= n: the smallest tile that covers n, so
+// no thread multiplies padding (n = 40: 48 x 48 instead of 64 x 64, 44 % fewer FMAs). Every C entry is summed over l
+// in order whatever MT is (bitwise the same result).
+template <int MT>
+__device__ __forceinline__ void mm_t(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                                     int n, int ld) {
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4];
+    double acc[MT][MT];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < MT; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int b = 0; b < MT; ++b) acc[a][b] = 0.0;
     for (int l = 0; l < n; ++l) {
-        double av[4], bv[4];
+        double av[MT], bv[MT];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < MT; ++a) {
             const int i = ty + 16 * a;
             av[a] = i < n ? A[i * ld + l] : 0.0;
         }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < MT; ++b) {
             const int j = tx + 16 * b;
             bv[b] = j < n ? B[l * ld + j] : 0.0;
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < MT; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            for (int b = 0; b < MT; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < MT; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < MT; ++b) {
             const int i = ty + 16 * a, j = tx + 16 * b;
             if (i < n && j < n) C[i * ld + j] = acc[a][b];
         }
+}
+__device__ __forceinline__ void mm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                                   int n, int ld) {
+    if (n <= 16)
+        mm_t<1>(A, B, C, n, ld);
+    else if (n <= 32)
+        mm_t<2>(A, B, C, n, ld);
+    else if (n <= 48)
+        mm_t<3>(A, B, C, n, ld);
+    else
+        mm_t<4>(A, B, C, n, ld);
 }
 
 struct ExpmArgs {
